@@ -1,0 +1,374 @@
+#!/usr/bin/env python
+"""Benchmark: train images/sec of one layer-parallel training iteration
+(DecoupledTrainer::step, reference decoupled.cpp:172-194) on B200.
+
+Default (N=1): BASELINE.json configs[1] == SURVEY §8 C2: ODE-ResNet 3x32x32, batch 256,
+C=64, L=16, K=4 stages, augmented Lagrangian (kappa updates), fp32, full batch
+(N_train = B).  Inputs are synthetic and device-resident for `value`; `e2e` times the
+same step through the public C ABI with pinned host buffers (H2D of x and labels,
+D2H of the loss inside the timed region).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--config C2]
+
+`--impl reference` times the reference's own CPU trainer (oracle/_ref, compiled from
+the reference sources) on the same config's dense 1x1-conv analogue, a bounded sample
+of images per step.
+"""
+from __future__ import annotations
+
+import argparse
+import ctypes as C
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+CONFIGS = {
+    # id: (Cin, H, W, C, Ch, L, K, B, mode, math, classes)
+    "C1": dict(cin=1, h=28, w=28, c=16, ch=16, L=8, K=2, B=128, mode="penalty", math="fp32"),
+    "C2": dict(cin=3, h=32, w=32, c=64, ch=64, L=16, K=4, B=256, mode="alm", math="fp32"),
+    "C3": dict(cin=3, h=32, w=32, c=64, ch=64, L=64, K=8, B=256, mode="alm", math="fp32"),
+    "C4": dict(cin=3, h=32, w=32, c=64, ch=64, L=64, K=1, B=256, mode="serial", math="fp32"),
+    "C5": dict(cin=3, h=32, w=32, c=256, ch=256, L=64, K=8, B=1024, mode="alm", math="bf16"),
+}
+CLASSES = 10
+METRIC = "train images/sec at K=1/2/4/8 B200 stages; conv tensor-pipe % of peak"
+
+
+def flops_per_image(cfg):
+    """108 C^2 HW per block (6 conv-equivalents) + stem fprop/wgrad."""
+    hw = cfg["h"] * cfg["w"]
+    return cfg["L"] * 6 * 2 * 9 * cfg["c"] * cfg["ch"] * hw + 2 * 2 * 9 * cfg["cin"] * cfg["c"] * hw
+
+
+def step_params(cfg):
+    import paper_2009_01462_b200 as rp
+    # paper schedules at epoch 0 (config.cpp:102-111): ALM beta 0.1, penalty beta 1; lr 0.1;
+    # lambda_lr = lr * lambda_lr_scale (1.0); kappa_lr 1e-9
+    beta = 0.1 if cfg["mode"] == "alm" else 1.0
+    return rp.StepParams(beta=beta, tau=-1.0, lr=0.1, lambda_lr=0.1, kappa_lr=1e-9, max_corrections=1)
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index):
+        self.gpu = gpu_index
+        self.proc = None
+        self.lines = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits", "-lms", "100",
+                 "-i", str(self.gpu)], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except FileNotFoundError:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.25)
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 7:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx = float(parts[1])
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[3:7]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def measured_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.isfile(p):
+        with open(p) as f:
+            d = json.load(f)
+        return d, "measured"
+    return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0}, "fallback"
+
+
+def profile_classes():
+    from paper_2009_01462_b200._lib import lib
+    n = 9
+    launches = (C.c_int64 * n)()
+    ms = (C.c_double * n)()
+    fl = (C.c_double * n)()
+    by = (C.c_double * n)()
+    from paper_2009_01462_b200 import check
+    check(lib().rp_profile_collect(launches, ms, fl, by))
+    out = {}
+    for i in range(n):
+        if launches[i]:
+            out[lib().rp_profile_class_name(i).decode()] = dict(launches=launches[i], ms=ms[i], flops=fl[i],
+                                                              bytes=by[i])
+    return out
+
+
+def run_ours(args, cfg, rank, world):
+    import numpy as np
+    import torch
+
+    import paper_2009_01462_b200 as rp
+    from paper_2009_01462_b200._lib import lib
+
+    dev = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(dev)
+    g = rp.Geometry(cfg["cin"], cfg["h"], cfg["w"], cfg["c"], cfg["ch"], cfg["L"], CLASSES)
+    B, K = cfg["B"], cfg["K"]
+    mode = {"alm": rp.ALM, "penalty": rp.PENALTY, "serial": rp.SERIAL}[cfg["mode"]]
+    # train(): root = Rng(seed); net_rng = root.split() (decoupled.cpp:274-276), seed 1
+    from paper_2009_01462_b200.trainer import SerialTrainer
+    mix = lambda z: _splitmix(z)  # noqa: E731
+    net_state = mix(1)
+    if mode == rp.SERIAL:
+        tr = SerialTrainer(g, B, seed_state=net_state, math=args.math or cfg["math"])
+    else:
+        tr = rp.DecoupledTrainer(g, K, mode, rp.SQUARED_L2, B, seed_state=net_state, math=args.math or cfg["math"])
+    # synthetic data, device-resident: pixels U[-1,1) from the splitmix64 stream (seed 1 + rank),
+    # labels uniform over the classes
+    x = torch.empty(B * g.raw_size, dtype=torch.float32, device="cuda")
+    st = C.c_uint64(1000 + rank)
+    rp.check(lib().rp_op_fill_uniform(C.c_void_p(x.data_ptr()), x.numel(), C.byref(st), -1.0, 1.0, 1.0, None))
+    gen = torch.Generator(device="cuda")
+    gen.manual_seed(7 + rank)
+    y = torch.randint(0, CLASSES, (B,), dtype=torch.int32, device="cuda", generator=gen)
+    torch.cuda.synchronize()
+    x_host = x.cpu().numpy()
+    tr.reset_lambda_from_forward(x_host)
+    sp = step_params(cfg)
+
+    for _ in range(args.warmup):
+        tr.step_device(x.data_ptr(), y.data_ptr(), B, 0, sp, read_loss=False)
+    torch.cuda.synchronize()
+    if world > 1:
+        import torch.distributed as dist
+        dist.barrier()
+    torch.cuda.synchronize()
+
+    clocks = ClockSampler(dev)
+    clocks.start()
+    lib().rp_profile_enable(1)
+    profile_classes()  # clear
+    n0 = rp.launch_count()
+    h = tr._h
+    rp.check(lib().rp_trainer_region(h, 0, None))
+    for _ in range(args.steps):
+        tr.step_device(x.data_ptr(), y.data_ptr(), B, 0, sp, read_loss=False)
+    ms = C.c_float()
+    rp.check(lib().rp_trainer_region(h, 1, C.byref(ms)))
+    torch.cuda.synchronize()
+    launches = rp.launch_count() - n0
+    lib().rp_profile_enable(0)
+    prof = profile_classes()
+    clk = clocks.stop()
+    total_ms = ms.value
+    if world > 1:
+        import torch.distributed as dist
+        t = torch.tensor([total_ms], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        total_ms = float(t.item())
+    loss = tr.last_loss()
+
+    # e2e through the public API with pinned host buffers (H2D x, labels; D2H loss)
+    xp = torch.from_numpy(x_host).pin_memory()
+    yp = y.cpu().pin_memory()
+    xpn = xp.numpy()
+    ypn = yp.numpy()
+    e2e_steps = max(1, min(args.steps, 10))
+    tr.step(xpn.reshape(B, -1), ypn, 0, sp)  # warm the staging buffers
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    for _ in range(e2e_steps):
+        tr.step(xpn.reshape(B, -1), ypn, 0, sp)
+    e2e_s = (time.perf_counter() - t0) / e2e_steps
+    return dict(tr=tr, total_ms=total_ms, prof=prof, clocks=clk, launches=launches, loss=loss, e2e_s=e2e_s,
+                B=B, K=K, g=g)
+
+
+def _splitmix(seed):
+    """Rng(seed).split().state == Rng(seed).next_u64() (tensor.cpp:163-175)."""
+    M = (1 << 64) - 1
+    z = (seed + 0x9E3779B97F4A7C15) & M
+    z = ((z ^ (z >> 30)) * 0xBF58476D1CE4E5B9) & M
+    z = ((z ^ (z >> 27)) * 0x94D049BB133111EB) & M
+    return z ^ (z >> 31)
+
+
+def cpu_reference_sample(cfg, images, workers):
+    """The reference's own DecoupledTrainer::step (oracle/_ref) on the dense 1x1-conv
+    analogue of cfg (rows = images*H*W, d = C, h = Ch, same L, K, mode): seconds/step."""
+    from oracle import refbind as R
+    hw = cfg["h"] * cfg["w"]
+    rows = images * hw
+    dims = (cfg["cin"], cfg["c"], cfg["ch"], cfg["L"], CLASSES)
+    rng = R.RefRng(1)
+    params = R.make_net(rng, *dims)
+    x = rng.uniform(rows, cfg["cin"], -1.0, 1.0)
+    import numpy as np
+    y = np.array([rng.next_u64() % CLASSES for _ in range(rows)], np.int32)
+    mode = {"alm": 2, "penalty": 1, "serial": 1}[cfg["mode"]]
+    K = cfg["K"]
+    tr = R.RefTrainer(dims, 0, params, K, mode, 0, rows, workers=workers)
+    tr.reset_lambda_from_forward(x)
+    beta = 0.1 if cfg["mode"] == "alm" else 1.0
+    t0 = time.perf_counter()
+    tr.step(x, y, 0, beta=beta, tau=-1.0, lr=0.1, lambda_lr=0.1, kappa_lr=1e-9, max_corrections=1)
+    return time.perf_counter() - t0
+
+
+def run_reference(args, cfg, rank, world):
+    if rank != 0:
+        return
+    from oracle import refbind as R
+    if not R.available():
+        print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref/librespar_ref.so not built"}))
+        return
+    workers = min(cfg["K"], os.cpu_count() or 1)
+    images = max(1, args.ref_images)
+    times = []
+    for i in range(args.warmup + args.steps):
+        t = cpu_reference_sample(cfg, images, workers)
+        if i >= args.warmup:
+            times.append(t)
+    per_step = statistics.mean(times)
+    v = images / per_step
+    line = {
+        "metric": METRIC, "value": v, "unit": "images/s", "impl": "reference", "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": per_step * 1e3 * cfg["B"] / images,
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic",
+        "config": {"workload": f"{args.config}: reference DecoupledTrainer::step (fp64 CPU) on the dense 1x1-conv "
+                               f"analogue rows=images*H*W", **_cfg_json(cfg)},
+        "cpu_baseline": {"value": v, "unit": "images/s", "cores": workers, "kind": "reference",
+                         "sample": f"{images} image(s) x {cfg['h']}x{cfg['w']} rows per step, one "
+                                   f"DecoupledTrainer::step, StagePool with {workers} workers"},
+        "e2e": {"value": v, "unit": "images/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line))
+
+
+def _cfg_json(cfg):
+    return {"in": [cfg["cin"], cfg["h"], cfg["w"]], "global_batch": cfg["B"], "channels": cfg["c"],
+            "hidden": cfg["ch"], "blocks": cfg["L"], "stages": cfg["K"], "mode": cfg["mode"],
+            "math": cfg["math"], "classes": CLASSES}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="C2", choices=sorted(CONFIGS))
+    ap.add_argument("--math", default=None, choices=[None, "fp32", "tf32", "bf16", "simt"])
+    ap.add_argument("--ref-images", type=int, default=2)
+    ap.add_argument("--cpu-images", type=int, default=4)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    cfg = dict(CONFIGS[args.config])
+    if args.math:
+        cfg["math"] = args.math
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+
+    if args.impl == "reference":
+        run_reference(args, cfg, rank, world)
+        return
+
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+        torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", "0")))
+        dist.init_process_group("nccl")
+
+    r = run_ours(args, cfg, rank, world)
+    if rank != 0:
+        return
+    B, K = r["B"], r["K"]
+    total_s = r["total_ms"] / 1e3
+    value = world * B * args.steps / total_s   # replicas: every rank ran B images per step
+    peaks, peaks_kind = measured_peaks()
+    prof = r["prof"]
+    convs = {k: v for k, v in prof.items() if k.startswith("conv_")}
+    dom = max(convs, key=lambda k: convs[k]["ms"]) if convs else max(prof, key=lambda k: prof[k]["ms"])
+    d = prof[dom]
+    avg_ms = d["ms"] / d["launches"]
+    achieved_tf = d["flops"] / d["launches"] / (avg_ms / 1e3) / 1e12
+    step_prof_ms = sum(v["ms"] for v in prof.values()) / args.steps
+    roof = {"bound": "tensor", "kernel": dom, "achieved": achieved_tf,
+            "peak": peaks["bf16_tflops_sustained"], "unit": "TFLOP/s",
+            "frac": achieved_tf / peaks["bf16_tflops_sustained"], "traffic": None,
+            "peak_source": f"{peaks_kind} bf16 dense sustained (MEASURED_PEAKS.json)",
+            "avg_launch_ms": avg_ms, "launches": d["launches"],
+            "share_of_step": d["ms"] / args.steps / step_prof_ms if step_prof_ms else None,
+            "kernel_classes": {k: {"launches": v["launches"], "ms_per_step": v["ms"] / args.steps,
+                                   "tflops": (v["flops"] / (v["ms"] / 1e3) / 1e12) if v["ms"] and v["flops"] else None,
+                                   "gbs": (v["bytes"] / (v["ms"] / 1e3) / 1e9) if v["ms"] and v["bytes"] else None}
+                               for k, v in prof.items()}}
+    flops_iter = flops_per_image(cfg) * B
+    line = {
+        "metric": METRIC, "value": value, "unit": "images/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": r["total_ms"] / args.steps, "higher_is_better": True,
+        "scaling": "weak" if world > 1 else "strong", "vs_baseline": None,
+        "dtype": "bf16" if cfg["math"] == "bf16" else "f32", "data": "synthetic",
+        "config": {"workload": f"{args.config}: ODE-ResNet {cfg['cin']}x{cfg['h']}x{cfg['w']}, batch {B}, "
+                               f"C={cfg['c']}, L={cfg['L']}, K={K} stages, {cfg['mode']}, math {cfg['math']}",
+                   **_cfg_json(cfg), "parallelism": f"{K} stages on {world} GPU(s)"
+                   + (" (replicas per GPU)" if world > 1 else ""),
+                   "l2": "inputs larger than L2 (per-iteration working set > 2 GB)",
+                   "model_flops_per_iter": flops_iter,
+                   "model_tflops": flops_iter * args.steps / total_s / 1e12 / world},
+        "loss": r["loss"],
+        "clocks": r["clocks"],
+        "gpu_launches": r["launches"],
+        "roofline": roof,
+        "e2e": {"value": B / r["e2e_s"], "unit": "images/s",
+                "h2d_bytes_per_step": B * r["g"].raw_size * 4 + B * 4, "d2h_bytes_per_step": 8},
+    }
+    if not args.no_cpu_baseline:
+        try:
+            workers = min(K, os.cpu_count() or 1)
+            t = cpu_reference_sample(cfg, args.cpu_images, workers)
+            line["cpu_baseline"] = {"value": args.cpu_images / t, "unit": "images/s", "cores": workers,
+                                    "kind": "reference",
+                                    "sample": f"{args.cpu_images} images (rows = images*{cfg['h']}*{cfg['w']}) "
+                                              f"of the dense 1x1-conv analogue, one reference "
+                                              f"DecoupledTrainer::step (fp64), {workers} StagePool workers"}
+        except Exception as e:  # reported, never fatal
+            line["cpu_baseline"] = {"value": None, "unit": "images/s", "cores": 0, "kind": "reference",
+                                    "sample": f"failed: {e}"}
+    print(json.dumps(line))
+
+
+if __name__ == "__main__":
+    main()

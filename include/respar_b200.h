@@ -1,0 +1,240 @@
+/*
+ * respar_b200.h — C ABI of the B200-native layer-parallel ResNet training step.
+ *
+ * This is the drop-in boundary.  The reference (respar,
+ * /root/reference/proj) has no FFI of its own: its boundary is the C++ library API
+ * in include/respar/*.hpp, consumed by train(), the CLI and the pybind11 module.
+ * The B200 build keeps that C++ surface (paper_2009_01462_b200/csrc/host/respar_b200.hpp,
+ * namespace respar::b200) and puts this C ABI under it and beside it:
+ *
+ *   - rp_op_*      stream-ordered kernels on caller-owned device buffers
+ *                  (what the C++ host classes call);
+ *   - rp_trainer_* an opaque DecoupledTrainer handle, one entry point per reference
+ *                  method (what a ctypes / cffi / pybind front end binds).
+ *
+ * Conventions
+ *   - every function returns int status (RP_OK = 0); rp_last_error() returns the
+ *     thread-local message of the last failure.  No C++ exception crosses the ABI;
+ *     the C++ and Python wrappers rethrow the reference's exception types
+ *     (ShapeError / ConfigError / std::logic_error / std::invalid_argument /
+ *     StageError) from the status code.
+ *   - device pointers are plain pointers; `stream` is a cudaStream_t passed as void*.
+ *   - the caller owns every buffer it passes; a trainer handle owns only its own
+ *     device state (parameters, lambda/kappa/boundary storage, tapes, workspaces).
+ *   - tensors are NHWC fp32 (a reference Tensor(rows = N*H*W, cols = C) is the
+ *     same bytes); conv weights are HWIO [3][3][Cin][Cout] (the centre tap is the
+ *     reference's in x out matrix, x . W).
+ *   - flat parameter layout == the reference make_net draw order
+ *     (include/respar/network.hpp:43-45):
+ *       s.w [3,3,Cin,C] s.b [C] { w1 [3,3,C,Ch] b1 [Ch] w2 [3,3,Ch,C] b2 [C] } x L
+ *       t.w [C,classes] t.b [classes]
+ */
+#ifndef RESPAR_B200_H
+#define RESPAR_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* ---- status codes (map to the reference's exception types) ---------------- */
+enum {
+  RP_OK = 0,
+  RP_ERR_SHAPE = 1,    /* respar::ShapeError            (tensor.hpp:11-13)   */
+  RP_ERR_CONFIG = 2,   /* respar::ConfigError           (config.hpp:13-15)   */
+  RP_ERR_STATE = 3,    /* std::logic_error  (protocol)  (decoupled.cpp:89-92, 197-199, 160-163) */
+  RP_ERR_RANGE = 4,    /* std::invalid_argument         (decoupled.cpp:66-69, 100-104, 117-122) */
+  RP_ERR_STAGE = 5,    /* respar::StageError            (runtime.hpp:15-20)  */
+  RP_ERR_CUDA = 6,
+  RP_ERR_NCCL = 7,
+  RP_ERR_DIVERGED = 8, /* std::runtime_error non-finite (decoupled.cpp:249-264) */
+  RP_ERR_INTERNAL = 9
+};
+
+/* enums mirror penalty.hpp:15, config.hpp:17, network.hpp:12 */
+enum { RP_PSI_SQUARED_L2 = 0, RP_PSI_L1 = 1, RP_PSI_LINF = 2 };
+enum { RP_MODE_SERIAL = 0, RP_MODE_PENALTY = 1, RP_MODE_ALM = 2 };
+enum { RP_ACT_TANH = 0, RP_ACT_IDENTITY = 1 };
+/* conv arithmetic: fp32-accurate (3xTF32 tensor cores), plain TF32, bf16 tensor
+ * cores with fp32 accumulate, or the SIMT FFMA path kept as an on-device checker. */
+enum { RP_MATH_FP32 = 0, RP_MATH_TF32 = 1, RP_MATH_BF16 = 2, RP_MATH_SIMT = 3 };
+/* multiplier rule: the reference's (decoupled.cpp:157-170) or the textbook one
+ * kappa += beta (lambda - X) (north_star wording; opt-in only). */
+enum { RP_KAPPA_RULE_REFERENCE = 0, RP_KAPPA_RULE_TEXTBOOK = 1 };
+
+/* ResidualNet geometry (network.hpp:29-41 + conv geometry). */
+typedef struct rp_geometry {
+  int32_t in_channels; /* reference in_dim   */
+  int32_t height;
+  int32_t width;
+  int32_t channels;    /* reference d        */
+  int32_t hidden;      /* reference h        */
+  int32_t blocks;      /* reference L        */
+  int32_t classes;
+  int32_t activation;  /* RP_ACT_*           */
+  double step_h;       /* x + h f(x); 1 == reference */
+} rp_geometry;
+
+/* StepParams (decoupled.hpp:45-52). */
+typedef struct rp_step_params {
+  double beta;
+  double tau;           /* < 0: single correction pass */
+  double lr;
+  double lambda_lr;
+  double kappa_lr;
+  int32_t max_corrections;
+  double momentum;      /* 0 == the reference's plain gradient descent */
+} rp_step_params;
+
+const char* rp_last_error(void);
+int rp_version(void);
+/* Number of kernel launches this thread has issued through the library (for the
+ * bench's gpu_launches claim). */
+uint64_t rp_launch_count(void);
+int64_t rp_param_count(const rp_geometry* g);
+/* Offsets (in floats) of s.w, block l's w1, t.w in the flat layout. */
+int64_t rp_param_offset_block(const rp_geometry* g, int32_t block);
+int64_t rp_param_offset_head(const rp_geometry* g);
+
+/* ---- live kernel profiling (bench roofline) ------------------------------- */
+/* While enabled, every kernel class launched through the op layer is bracketed by
+ * CUDA events on its own stream, with its algorithmic FLOPs and HBM bytes. */
+enum { RP_PROF_CONV_FPROP = 0, RP_PROF_CONV_DGRAD = 1, RP_PROF_CONV_WGRAD = 2, RP_PROF_SYNTHETIC = 3,
+       RP_PROF_CORRECT = 4, RP_PROF_SGD = 5, RP_PROF_HEAD = 6, RP_PROF_STEM = 7, RP_PROF_OTHER = 8,
+       RP_PROF_NUM_CLASSES = 9 };
+int rp_profile_enable(int32_t on);
+/* Per class: launches, summed device ms, summed algorithmic FLOPs and bytes (arrays of
+ * RP_PROF_NUM_CLASSES); synchronises the recorded events and clears the records. */
+int rp_profile_collect(int64_t* launches, double* ms, double* flops, double* bytes);
+const char* rp_profile_class_name(int32_t cls);
+
+/* ---- stream-ordered ops on caller-owned device buffers --------------------- */
+/* Counter-based splitmix64 fill: value i = lo + (hi-lo) * ((mix(state + (i+1)*gamma) >> 11) * 2^-53),
+ * bit-identical to n calls of Rng::next_double (tensor.cpp:163-185), rounded to fp32.
+ * Returns the advanced state in *state. */
+int rp_op_fill_uniform(float* dst, int64_t n, uint64_t* state, double lo, double hi, double scale,
+                       void* stream);
+/* Box-Muller normal (tensor.cpp:187-197), 2 draws per value; dst += value when accumulate. */
+int rp_op_fill_normal(float* dst, int64_t n, uint64_t* state, double mean, double sigma,
+                      int32_t accumulate, void* stream);
+/* Glorot-uniform conv net init (network.cpp:49-68), draw order s, blocks (w1, w2), t. */
+int rp_op_init_params(const rp_geometry* g, float* params, uint64_t* state, void* stream);
+
+/* Small reductions (psi, the LInf argmax) use `ws` (>= rp_op_reduce_workspace_bytes()). */
+int64_t rp_op_reduce_workspace_bytes(void);
+/* psi (penalty.cpp:38-58) over n elements, deterministic, fp64 accumulation; *out is host
+ * (the call synchronises `stream`). */
+int rp_op_psi(int32_t kind, const float* lam, const float* x, int64_t n, double* out, void* ws,
+              void* stream);
+/* psi_grads (penalty.cpp:60-87): d_lambda * scale into out (device); d_x == -d_lambda. */
+int rp_op_psi_grad(int32_t kind, const float* lam, const float* x, int64_t n, double scale, float* out,
+                   void* ws, void* stream);
+/* Synthetic-loss upstream (decoupled.cpp:105-110): g = w d_x psi(lam_next, x_end) + kappa_next,
+ * w = beta/# (kappa_next may be NULL == zero). */
+int rp_op_synthetic_grad(int32_t kind, const float* lam_next, const float* x_end, const float* kappa_next,
+                         int64_t n, double w, float* g, void* ws, void* stream);
+/* One correct_aux pass and/or correct_multiplier (decoupled.cpp:135-170), fused:
+ *   if update_lambda: lam -= eta_l * (w d_lambda psi(lam, x_prev) + p - kappa)
+ *   if update_kappa:  kappa -= kappa_coef * (lam - x_prev)   (lam already updated)
+ * kappa may be NULL (== 0) when update_kappa == 0. */
+int rp_op_correct(int32_t kind, float* lam, const float* x_prev, const float* p, float* kappa, int64_t n,
+                  double w, double eta_l, int32_t update_lambda, double kappa_coef, int32_t update_kappa,
+                  void* ws, void* stream);
+/* W -= lr * g (apply_updates, network.cpp:174-191); with momentum: v = mu v + g; W -= lr v. */
+int rp_op_sgd(float* w, const float* g, float* v, int64_t n, double lr, double momentum, void* stream);
+
+/* Residual block on nrows samples (network.cpp:82-106), block params at `pb` in the
+ * flat layout (w1 b1 w2 b2).  Forward writes a (tape) and x_next.  Backward takes the
+ * cotangent at the block output in g_io and overwrites it with the cotangent at the
+ * block input; writes the block's gradients at `gb` (same layout as pb); dpre is
+ * caller scratch of the hidden activation size. */
+int rp_op_block_fwd(const rp_geometry* g, int32_t nrows, const float* x, const float* pb, float* a,
+                    float* x_next, int32_t math, void* ws, int64_t ws_bytes, void* stream);
+int rp_op_block_bwd(const rp_geometry* g, int32_t nrows, const float* x, const float* a, const float* pb,
+                    float* g_io, float* dpre, float* gb, int32_t math, void* ws, int64_t ws_bytes,
+                    void* stream);
+/* Device workspace the block/stem/head ops need for nrows samples (weight relayouts,
+ * deterministic split-K partials). */
+int64_t rp_op_workspace_bytes(const rp_geometry* g, int32_t nrows, int32_t math);
+/* Stem S (affine_forward, network.cpp:108-110 as a 3x3 conv Cin->C). */
+int rp_op_stem_fwd(const rp_geometry* g, int32_t nrows, const float* x_raw, const float* ps, float* x0,
+                   int32_t math, void* ws, int64_t ws_bytes, void* stream);
+int rp_op_stem_bwd(const rp_geometry* g, int32_t nrows, const float* x_raw, const float* g0, float* gs,
+                   void* ws, int64_t ws_bytes, void* stream);
+/* Head T forward (affine_forward, network.cpp:108-110, as GAP + affine): pooled [nrows, C]
+ * and logits [nrows, classes] (device, caller-owned). */
+int rp_op_head_fwd(const rp_geometry* g, int32_t nrows, const float* x_end, const float* pt, float* pooled,
+                   float* logits, void* stream);
+/* loss_phi (network.cpp:193-221) + T backward: mean softmax-CE into *loss_dev (device
+ * double), T grads at gt (t.w then t.b), cotangent at the trunk output into g_out (NHWC).
+ * Labels are device int32 (out-of-range labels give a NaN loss). */
+int rp_op_head_loss_bwd(const rp_geometry* g, int32_t nrows, const float* pooled, const float* logits,
+                        const float* pt, const int32_t* labels, double* loss_dev, float* gt, float* g_out,
+                        void* ws, int64_t ws_bytes, void* stream);
+/* Argmax hits (accuracy, network.cpp:223-234; ties -> lowest class); *hits host. */
+int rp_op_argmax_hits(const float* logits, const int32_t* labels, int32_t nrows, int32_t classes,
+                      int64_t* hits, void* ws, void* stream);
+
+/* ---- DecoupledTrainer handle (decoupled.hpp:56-120) ------------------------ */
+typedef struct rp_trainer rp_trainer;
+
+/* DecoupledTrainer(ResidualNet net, int stages, TrainMode, PenaltyKind, int num_samples)
+ * (decoupled.hpp:58-59).  params_host: flat fp32 parameters (NULL: Glorot init from
+ * *seed_state on device).  devices/ndev: stage k runs on devices[floor(k*ndev/K)]
+ * (NULL/0 == the current device). mode RP_MODE_SERIAL builds a K=1 serial trainer. */
+int rp_trainer_create(const rp_geometry* g, int32_t stages, int32_t mode, int32_t penalty,
+                      int32_t num_samples, const float* params_host, uint64_t* seed_state,
+                      int32_t math, const int32_t* devices, int32_t ndev, rp_trainer** out);
+int rp_trainer_destroy(rp_trainer* t);
+int rp_trainer_set_kappa_rule(rp_trainer* t, int32_t rule);
+int rp_trainer_get_params(rp_trainer* t, float* host);
+int rp_trainer_set_params(rp_trainer* t, const float* host);
+/* Gradients of the last stage_backward_update / step (flat layout, host). */
+int rp_trainer_get_grads(rp_trainer* t, float* host);
+/* reset_lambda_from_forward (decoupled.cpp:44-63); x is host NHWC [num_samples,H,W,Cin]. */
+int rp_trainer_reset_lambda_from_forward(rp_trainer* t, const float* x_host);
+/* step (decoupled.cpp:172-194).  Host buffers (H2D inside) ... */
+int rp_trainer_step(rp_trainer* t, const float* x_host, const int32_t* labels_host, int32_t nrows,
+                    int32_t row0, const rp_step_params* p, double* loss_out);
+/* ... or device buffers already resident (loss_out NULL: no host sync; the loss stays
+ * on device and rp_trainer_last_loss() reads it). */
+int rp_trainer_step_device(rp_trainer* t, const float* x_dev, const int32_t* labels_dev, int32_t nrows,
+                           int32_t row0, const rp_step_params* p, double* loss_out);
+int rp_trainer_last_loss(rp_trainer* t, double* loss_out);
+/* The pieces of step (decoupled.hpp:71-89).  Host buffers. */
+int rp_trainer_take_snapshot(rp_trainer* t, int32_t k, int32_t row0, int32_t nrows);
+int rp_trainer_stage_forward(rp_trainer* t, int32_t k, const float* x_host, int32_t nrows, int32_t row0);
+int rp_trainer_stage_backward_update(rp_trainer* t, int32_t k, const int32_t* labels_host, int32_t nrows,
+                                     double beta, double lr, int32_t row0);
+int rp_trainer_correct_aux(rp_trainer* t, int32_t k, const rp_step_params* p, int32_t row0, int32_t nrows);
+int rp_trainer_correct_multiplier(rp_trainer* t, int32_t k, double beta, double kappa_lr, int32_t row0,
+                                  int32_t nrows);
+int rp_trainer_correction_gradient(rp_trainer* t, int32_t k, double beta, int32_t row0, int32_t nrows,
+                                   float* out_host);
+/* violation_report (decoupled.cpp:196-205): per_stage[K] host. */
+int rp_trainer_violation_report(rp_trainer* t, double* per_stage, double* max_violation,
+                                int64_t* normalizer);
+/* Per-stage state (decoupled.hpp:29-32): which 0 lambda, 1 kappa, 2 boundary_out, 3 boundary_adjoint. */
+int rp_trainer_get_state(rp_trainer* t, int32_t k, int32_t which, float* host);
+int rp_trainer_set_state(rp_trainer* t, int32_t k, int32_t which, const float* host);
+/* Full serial forward (eval, decoupled.cpp:332-347): logits host [n, classes]. */
+int rp_trainer_forward(rp_trainer* t, const float* x_host, int32_t nrows, float* logits_host);
+int64_t rp_trainer_iteration(rp_trainer* t);
+int32_t rp_trainer_stages(rp_trainer* t);
+/* Device-side timing of the last step: max over stage streams (ms). */
+int rp_trainer_last_step_ms(rp_trainer* t, float* ms);
+/* Device-timed region on the trainer's control stream: which = 0 begins (records an
+ * event after all previously issued work), which = 1 ends and returns the elapsed ms. */
+int rp_trainer_region(rp_trainer* t, int32_t which, float* ms);
+
+/* serial_train_step (network.cpp:236-244) on a K=1 trainer made with RP_MODE_SERIAL. */
+int rp_serial_train_step(rp_trainer* t, const float* x_host, const int32_t* labels_host, int32_t nrows,
+                         double lr, double* loss_out);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* RESPAR_B200_H */

@@ -1,0 +1,349 @@
+// C ABI, op layer (include/respar_b200.h "rp_op_*"): stream-ordered kernels on
+// caller-owned device buffers.  The C++ host classes (host/trainer.cpp) reach the GPU
+// only through these entry points.
+#include <cstring>
+#include <string>
+
+#include "capi_guard.hpp"
+#include "common.cuh"
+#include "kernels/kernels.cuh"
+#include "profile.hpp"
+
+namespace rp {
+
+namespace {
+
+cudaStream_t S(void* s) { return static_cast<cudaStream_t>(s); }
+
+int64_t align256(int64_t v) { return (v + 255) / 256 * 256; }
+
+void need(const void* p, const char* what) {
+  if (!p) fail(RP_ERR_RANGE, std::string(what) + ": null pointer");
+}
+
+struct Carve {
+  char* base;
+  int64_t cap;
+  int64_t off = 0;
+  template <class T>
+  T* take(int64_t count) {
+    const int64_t bytes = align256(count * (int64_t)sizeof(T));
+    if (off + bytes > cap) fail(RP_ERR_RANGE, "workspace too small");
+    T* p = reinterpret_cast<T*>(base + off);
+    off += bytes;
+    return p;
+  }
+};
+
+k::ConvShape shape(const rp_geometry& g, int nrows, int ci, int co) { return {nrows, g.height, g.width, ci, co}; }
+
+double conv_flops(const k::ConvShape& s) { return 2.0 * 9.0 * s.ci * s.co * (double)s.pixels(); }
+// algorithmic HBM bytes of one conv launch: read the input, write the output, plus
+// the epilogue's aux tensor when it has one (weights are negligible)
+double conv_bytes(const k::ConvShape& s, bool aux) {
+  return 4.0 * (double)s.pixels() * (s.ci + s.co + (aux ? s.co : 0));
+}
+
+void check_math(int math) {
+  if (math < RP_MATH_FP32 || math > RP_MATH_SIMT) fail(RP_ERR_CONFIG, "unknown math mode");
+}
+
+}  // namespace
+
+int64_t op_workspace_bytes(const rp_geometry& g, int nrows) {
+  const int64_t C = g.channels, Ch = g.hidden;
+  const int64_t wd = align256(9 * C * Ch * 4) * 2;
+  int64_t wg = k::conv3x3_wgrad_ws_bytes(shape(g, nrows, (int)Ch, (int)C));
+  wg = std::max(wg, k::conv3x3_wgrad_ws_bytes(shape(g, nrows, (int)C, (int)Ch)));
+  wg = std::max(wg, k::conv3x3_wgrad_ws_bytes(shape(g, nrows, g.in_channels, (int)C)));
+  const int64_t head = k::head_ws_bytes(nrows, g.channels, g.classes);
+  return std::max(wd + align256(wg), head) + 256;
+}
+
+void block_fwd(const rp_geometry& g, int nrows, const float* x, const float* pb, float* a, float* x_next, int math,
+               void*, int64_t, cudaStream_t st) {
+  const ParamLayout L = ParamLayout::of(g);
+  const bool tanh_act = g.activation == RP_ACT_TANH;
+  (void)math;
+  const k::ConvShape s1 = shape(g, nrows, g.channels, g.hidden), s2 = shape(g, nrows, g.hidden, g.channels);
+  {  // conv1 + b1 + act  ->  a      (network.cpp:85-86)
+    prof::Scope ps(RP_PROF_CONV_FPROP, st, conv_flops(s1), conv_bytes(s1, false));
+    k::conv3x3_fwd_simt(s1, x, pb + L.w1, pb + L.b1, nullptr, 1.f, tanh_act ? k::EPI_BIAS_TANH : k::EPI_BIAS, a, st);
+  }
+  {  // conv2 + b2, *h, + x  ->  x'   (network.cpp:87)
+    prof::Scope ps(RP_PROF_CONV_FPROP, st, conv_flops(s2), conv_bytes(s2, true));
+    k::conv3x3_fwd_simt(s2, a, pb + L.w2, pb + L.b2, x, (float)g.step_h, k::EPI_RESID, x_next, st);
+  }
+}
+
+void block_bwd(const rp_geometry& g, int nrows, const float* x, const float* a, const float* pb, float* gio,
+               float* dpre, float* gb, int math, void* ws, int64_t ws_bytes, cudaStream_t st) {
+  const ParamLayout L = ParamLayout::of(g);
+  const int C = g.channels, Ch = g.hidden;
+  const bool tanh_act = g.activation == RP_ACT_TANH;
+  const float h = (float)g.step_h;
+  (void)math;
+  Carve cv{static_cast<char*>(ws), ws_bytes};
+  float* w2d = cv.take<float>(9LL * C * Ch);
+  float* w1d = cv.take<float>(9LL * C * Ch);
+  const int64_t wg_bytes = std::max(k::conv3x3_wgrad_ws_bytes(shape(g, nrows, Ch, C)),
+                                    k::conv3x3_wgrad_ws_bytes(shape(g, nrows, C, Ch)));
+  void* wgws = cv.take<char>(wg_bytes);
+  {
+    prof::Scope ps(RP_PROF_OTHER, st, 0.0, 0.0);
+    k::conv3x3_dgrad_weights(pb + L.w2, Ch, C, w2d, st);
+    k::conv3x3_dgrad_weights(pb + L.w1, C, Ch, w1d, st);
+  }
+  const k::ConvShape d2 = shape(g, nrows, C, Ch), d1 = shape(g, nrows, Ch, C);
+  {  // dpre = h (g * W2^T) (1 - a^2)                            (network.cpp:100-101)
+    prof::Scope ps(RP_PROF_CONV_DGRAD, st, conv_flops(d2), conv_bytes(d2, tanh_act));
+    k::conv3x3_fwd_simt(d2, gio, w2d, nullptr, a, h, tanh_act ? k::EPI_TANH_BWD : k::EPI_SCALE, dpre, st);
+  }
+  {  // gW2 = h a^T g, gb2 = h sum g                             (network.cpp:98-99)
+    const k::ConvShape w2 = shape(g, nrows, Ch, C);
+    prof::Scope ps(RP_PROF_CONV_WGRAD, st, conv_flops(w2), conv_bytes(w2, false));
+    k::conv3x3_wgrad_simt(w2, a, gio, h, gb + L.w2, gb + L.b2, wgws, st);
+  }
+  {  // gW1 = x^T dpre, gb1 = sum dpre                           (network.cpp:102-103)
+    const k::ConvShape w1 = shape(g, nrows, C, Ch);
+    prof::Scope ps(RP_PROF_CONV_WGRAD, st, conv_flops(w1), conv_bytes(w1, false));
+    k::conv3x3_wgrad_simt(w1, x, dpre, 1.f, gb + L.w1, gb + L.b1, wgws, st);
+  }
+  {  // g <- g + dpre * W1^T   (in place)                        (network.cpp:104)
+    prof::Scope ps(RP_PROF_CONV_DGRAD, st, conv_flops(d1), conv_bytes(d1, true));
+    k::conv3x3_fwd_simt(d1, dpre, w1d, nullptr, gio, 1.f, k::EPI_ADD, gio, st);
+  }
+}
+
+void stem_fwd(const rp_geometry& g, int nrows, const float* xr, const float* ps, float* x0, cudaStream_t st) {
+  const ParamLayout L = ParamLayout::of(g);
+  const k::ConvShape sh = shape(g, nrows, g.in_channels, g.channels);
+  prof::Scope scope(RP_PROF_STEM, st, conv_flops(sh), conv_bytes(sh, false));
+  k::conv3x3_fwd_simt(sh, xr, ps + L.s_w, ps + L.s_b, nullptr, 1.f, k::EPI_BIAS, x0, st);
+}
+
+void stem_bwd(const rp_geometry& g, int nrows, const float* xr, const float* g0, float* gs, void* ws,
+              int64_t ws_bytes, cudaStream_t st) {
+  const ParamLayout L = ParamLayout::of(g);
+  const k::ConvShape sh = shape(g, nrows, g.in_channels, g.channels);
+  if (k::conv3x3_wgrad_ws_bytes(sh) > ws_bytes) fail(RP_ERR_RANGE, "stem_bwd: workspace too small");
+  prof::Scope scope(RP_PROF_STEM, st, conv_flops(sh), conv_bytes(sh, false));
+  k::conv3x3_wgrad_simt(sh, xr, g0, 1.f, gs + L.s_w, gs + L.s_b, ws, st);
+}
+
+void head_fwd(const rp_geometry& g, int nrows, const float* x_end, const float* pt, float* pooled, float* logits,
+              cudaStream_t st) {
+  prof::Scope scope(RP_PROF_HEAD, st, 0.0, 4.0 * nrows * g.height * g.width * g.channels);
+  k::head_forward(nrows, g.height * g.width, g.channels, g.classes, x_end, pt, pt + (int64_t)g.channels * g.classes,
+                  pooled, logits, st);
+}
+
+void head_loss_bwd(const rp_geometry& g, int nrows, const float* pooled, const float* logits, const float* pt,
+                   const int32_t* labels, double* loss_dev, float* gt, float* g_out, void* ws, int64_t ws_bytes,
+                   cudaStream_t st) {
+  if (k::head_ws_bytes(nrows, g.channels, g.classes) > ws_bytes) fail(RP_ERR_RANGE, "head: workspace too small");
+  prof::Scope scope(RP_PROF_HEAD, st, 0.0, 4.0 * nrows * g.height * g.width * g.channels);
+  k::head_loss_backward(nrows, g.height * g.width, g.channels, g.classes, pooled, logits, pt, labels, loss_dev, gt,
+                        gt + (int64_t)g.channels * g.classes, g_out, ws, st);
+}
+
+void init_params(const rp_geometry& g, float* params, uint64_t* state, cudaStream_t st) {
+  // make_net (network.cpp:49-68): s, blocks (w1, w2), t; Glorot with conv fans; zero biases.
+  const ParamLayout L = ParamLayout::of(g);
+  RP_CUDA(cudaMemsetAsync(params, 0, L.total * sizeof(float), st));
+  auto glorot = [&](float* dst, int64_t fan_in, int64_t fan_out, int64_t n, double gain) {
+    const double a = std::sqrt(6.0 / (double)(fan_in + fan_out));
+    k::fill_uniform(dst, n, *state, -a, a, gain, st);
+    *state += (uint64_t)n * kGamma;
+  };
+  const int64_t Ci = g.in_channels, C = g.channels, Ch = g.hidden;
+  glorot(params + L.s_w, 9 * Ci, 9 * C, 9 * Ci * C, 2.0);
+  const double branch = 2.2 / std::sqrt((double)std::max(g.blocks, 1));
+  for (int l = 0; l < g.blocks; ++l) {
+    float* pb = params + L.block0 + (int64_t)l * L.block_stride;
+    glorot(pb + L.w1, 9 * C, 9 * Ch, 9 * C * Ch, 1.2);
+    glorot(pb + L.w2, 9 * Ch, 9 * C, 9 * Ch * C, branch);
+  }
+  glorot(params + L.t_w, C, g.classes, C * g.classes, 1.0);
+}
+
+}  // namespace rp
+
+using namespace rp;
+
+extern "C" {
+
+int64_t rp_op_workspace_bytes(const rp_geometry* g, int32_t nrows, int32_t math) {
+  int64_t out = -1;
+  guard([&] {
+    need(g, "geometry");
+    validate_geometry(*g);
+    check_math(math);
+    out = op_workspace_bytes(*g, nrows);
+  });
+  return out;
+}
+
+int64_t rp_op_reduce_workspace_bytes(void) { return k::reduce_workspace_bytes(); }
+
+int rp_op_fill_uniform(float* dst, int64_t n, uint64_t* state, double lo, double hi, double scale, void* stream) {
+  return guard([&] {
+    need(state, "state");
+    if (!(lo < hi)) fail(RP_ERR_RANGE, "rng_uniform: requires lo < hi");
+    if (n > 0) need(dst, "dst");
+    k::fill_uniform(dst, n, *state, lo, hi, scale, S(stream));
+    *state += (uint64_t)n * kGamma;
+  });
+}
+
+int rp_op_fill_normal(float* dst, int64_t n, uint64_t* state, double mean, double sigma, int32_t accumulate,
+                      void* stream) {
+  return guard([&] {
+    need(state, "state");
+    if (sigma < 0.0) fail(RP_ERR_RANGE, "rng_normal: sigma must be >= 0");
+    if (n > 0) need(dst, "dst");
+    k::fill_normal(dst, n, *state, mean, sigma, accumulate != 0, S(stream));
+    *state += (uint64_t)(2 * n) * kGamma;
+  });
+}
+
+int rp_op_init_params(const rp_geometry* g, float* params, uint64_t* state, void* stream) {
+  return guard([&] {
+    need(g, "geometry");
+    need(params, "params");
+    need(state, "state");
+    validate_geometry(*g);
+    init_params(*g, params, state, S(stream));
+  });
+}
+
+int rp_op_psi(int32_t kind, const float* lam, const float* x, int64_t n, double* out, void* ws, void* stream) {
+  return guard([&] {
+    need(out, "out");
+    if (kind < 0 || kind > 2) fail(RP_ERR_RANGE, "unknown penalty kind");
+    if (n == 0) {
+      *out = 0.0;
+      return;
+    }
+    need(ws, "ws");
+    double* dev = reinterpret_cast<double*>(static_cast<char*>(ws) + k::reduce_workspace_bytes() - 16);
+    k::psi_device(kind, lam, x, n, ws, dev, S(stream));
+    RP_CUDA(cudaMemcpyAsync(out, dev, sizeof(double), cudaMemcpyDeviceToHost, S(stream)));
+    RP_CUDA(cudaStreamSynchronize(S(stream)));
+  });
+}
+
+int rp_op_psi_grad(int32_t kind, const float* lam, const float* x, int64_t n, double scale, float* out, void* ws,
+                   void* stream) {
+  return guard([&] {
+    if (kind < 0 || kind > 2) fail(RP_ERR_RANGE, "unknown penalty kind");
+    k::psi_grad(kind, lam, x, n, scale, out, ws, S(stream));
+  });
+}
+
+int rp_op_synthetic_grad(int32_t kind, const float* lam_next, const float* x_end, const float* kappa_next, int64_t n,
+                         double w, float* g, void* ws, void* stream) {
+  return guard([&] {
+    if (kind < 0 || kind > 2) fail(RP_ERR_RANGE, "unknown penalty kind");
+    prof::Scope scope(RP_PROF_SYNTHETIC, S(stream), 0.0, (double)n * (kappa_next ? 16.0 : 12.0));
+    k::synthetic_grad(kind, lam_next, x_end, kappa_next, n, w, g, ws, S(stream));
+  });
+}
+
+int rp_op_correct(int32_t kind, float* lam, const float* x_prev, const float* p, float* kappa, int64_t n, double w,
+                  double eta_l, int32_t update_lambda, double kappa_coef, int32_t update_kappa, void* ws,
+                  void* stream) {
+  return guard([&] {
+    if (kind < 0 || kind > 2) fail(RP_ERR_RANGE, "unknown penalty kind");
+    const double per = (update_lambda ? 12.0 + (kappa ? 4.0 : 0.0) : 8.0) + (update_kappa ? 8.0 : 0.0);
+    prof::Scope scope(RP_PROF_CORRECT, S(stream), 0.0, (double)n * per);
+    k::correct(kind, lam, x_prev, p, kappa, n, w, eta_l, update_lambda != 0, kappa_coef, update_kappa != 0, ws,
+               S(stream));
+  });
+}
+
+int rp_op_sgd(float* w, const float* g, float* v, int64_t n, double lr, double momentum, void* stream) {
+  return guard([&] {
+    prof::Scope scope(RP_PROF_SGD, S(stream), 0.0, (double)n * (v ? 20.0 : 12.0));
+    k::sgd(w, g, v, n, lr, momentum, S(stream));
+  });
+}
+
+int rp_op_block_fwd(const rp_geometry* g, int32_t nrows, const float* x, const float* pb, float* a, float* x_next,
+                    int32_t math, void* ws, int64_t ws_bytes, void* stream) {
+  return guard([&] {
+    need(g, "geometry");
+    validate_geometry(*g);
+    check_math(math);
+    if (nrows <= 0) return;
+    block_fwd(*g, nrows, x, pb, a, x_next, math, ws, ws_bytes, S(stream));
+  });
+}
+
+int rp_op_block_bwd(const rp_geometry* g, int32_t nrows, const float* x, const float* a, const float* pb,
+                    float* g_io, float* dpre, float* gb, int32_t math, void* ws, int64_t ws_bytes, void* stream) {
+  return guard([&] {
+    need(g, "geometry");
+    validate_geometry(*g);
+    check_math(math);
+    if (nrows <= 0) return;
+    need(ws, "ws");
+    block_bwd(*g, nrows, x, a, pb, g_io, dpre, gb, math, ws, ws_bytes, S(stream));
+  });
+}
+
+int rp_op_stem_fwd(const rp_geometry* g, int32_t nrows, const float* x_raw, const float* ps, float* x0, int32_t math,
+                   void*, int64_t, void* stream) {
+  return guard([&] {
+    need(g, "geometry");
+    validate_geometry(*g);
+    check_math(math);
+    if (nrows <= 0) return;
+    stem_fwd(*g, nrows, x_raw, ps, x0, S(stream));
+  });
+}
+
+int rp_op_stem_bwd(const rp_geometry* g, int32_t nrows, const float* x_raw, const float* g0, float* gs, void* ws,
+                   int64_t ws_bytes, void* stream) {
+  return guard([&] {
+    need(g, "geometry");
+    validate_geometry(*g);
+    if (nrows <= 0) return;
+    stem_bwd(*g, nrows, x_raw, g0, gs, ws, ws_bytes, S(stream));
+  });
+}
+
+int rp_op_head_fwd(const rp_geometry* g, int32_t nrows, const float* x_end, const float* pt, float* pooled,
+                   float* logits, void* stream) {
+  return guard([&] {
+    need(g, "geometry");
+    validate_geometry(*g);
+    head_fwd(*g, nrows, x_end, pt, pooled, logits, S(stream));
+  });
+}
+
+int rp_op_head_loss_bwd(const rp_geometry* g, int32_t nrows, const float* pooled, const float* logits,
+                        const float* pt, const int32_t* labels, double* loss_dev, float* gt, float* g_out, void* ws,
+                        int64_t ws_bytes, void* stream) {
+  return guard([&] {
+    need(g, "geometry");
+    validate_geometry(*g);
+    head_loss_bwd(*g, nrows, pooled, logits, pt, labels, loss_dev, gt, g_out, ws, ws_bytes, S(stream));
+  });
+}
+
+int rp_op_argmax_hits(const float* logits, const int32_t* labels, int32_t nrows, int32_t classes, int64_t* hits,
+                      void* ws, void* stream) {
+  return guard([&] {
+    need(hits, "hits");
+    need(ws, "ws");
+    auto* dev = static_cast<unsigned long long*>(ws);
+    k::argmax_hits(logits, labels, nrows, classes, dev, S(stream));
+    unsigned long long h = 0;
+    RP_CUDA(cudaMemcpyAsync(&h, dev, sizeof(h), cudaMemcpyDeviceToHost, S(stream)));
+    RP_CUDA(cudaStreamSynchronize(S(stream)));
+    *hits = (int64_t)h;
+  });
+}
+
+}  // extern "C"

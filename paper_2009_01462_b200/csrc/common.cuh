@@ -1,0 +1,81 @@
+// Shared helpers for the sm_100a kernels and the C ABI.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <stdexcept>
+#include <string>
+
+#include "respar_b200.h"
+
+namespace rp {
+
+// Status-carrying exception used inside the library; converted to an int status at
+// the C ABI (capi.cpp) and back to the reference's exception types by the wrappers.
+struct Error : std::runtime_error {
+  int code;
+  Error(int c, const std::string& m) : std::runtime_error(m), code(c) {}
+};
+
+[[noreturn]] inline void fail(int code, const std::string& msg) { throw Error(code, msg); }
+
+inline void cuda_check(cudaError_t e, const char* what, const char* file, int line) {
+  if (e != cudaSuccess) {
+    fail(RP_ERR_CUDA, std::string(what) + ": " + cudaGetErrorString(e) + " at " + file + ":" +
+                          std::to_string(line));
+  }
+}
+
+#define RP_CUDA(x) ::rp::cuda_check((x), #x, __FILE__, __LINE__)
+#define RP_LAUNCHED() \
+  do {                \
+    ::rp::note_launch(); \
+    RP_CUDA(cudaGetLastError()); \
+  } while (0)
+
+void note_launch();
+
+inline int ceil_div(int64_t a, int64_t b) { return static_cast<int>((a + b - 1) / b); }
+
+constexpr int kNumSMs = 148;
+
+// splitmix64, tensor.cpp:163-169.  Draw i of a stream at state s = mix(s + (i+1)*gamma).
+__host__ __device__ inline uint64_t splitmix_mix(uint64_t z) {
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ULL;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBULL;
+  return z ^ (z >> 31);
+}
+constexpr uint64_t kGamma = 0x9E3779B97F4A7C15ULL;
+
+// Flat parameter layout (network.hpp:43-45 draw order).
+struct ParamLayout {
+  int64_t s_w, s_b, block0, block_stride, w1, b1, w2, b2, t_w, t_b, total;
+  static ParamLayout of(const rp_geometry& g) {
+    ParamLayout p{};
+    const int64_t Ci = g.in_channels, C = g.channels, Ch = g.hidden;
+    p.s_w = 0;
+    p.s_b = 9 * Ci * C;
+    p.block0 = p.s_b + C;
+    p.w1 = 0;
+    p.b1 = 9 * C * Ch;
+    p.w2 = p.b1 + Ch;
+    p.b2 = p.w2 + 9 * Ch * C;
+    p.block_stride = p.b2 + C;
+    p.t_w = p.block0 + p.block_stride * g.blocks;
+    p.t_b = p.t_w + C * g.classes;
+    p.total = p.t_b + g.classes;
+    return p;
+  }
+};
+
+inline void validate_geometry(const rp_geometry& g) {
+  if (g.in_channels < 1 || g.height < 1 || g.width < 1 || g.channels < 1 || g.hidden < 1 ||
+      g.blocks < 1 || g.classes < 2)
+    fail(RP_ERR_CONFIG, "geometry: all sizes must be >= 1 (classes >= 2)");
+  if (g.activation != RP_ACT_TANH && g.activation != RP_ACT_IDENTITY)
+    fail(RP_ERR_CONFIG, "geometry: unknown activation");
+  if (g.classes > 1024) fail(RP_ERR_CONFIG, "geometry: at most 1024 classes");
+}
+
+}  // namespace rp

@@ -1,0 +1,238 @@
+// C++ host mirror of the reference library's model/stage/trainer API for the
+// layer-parallel training step (reference include/respar/decoupled.hpp:17-137,
+// network.hpp:29-117, runtime.hpp:15-74), re-designed for B200: device-resident NHWC
+// state, one CUDA stream per stage, events instead of the StagePool barrier, and every
+// GPU operation issued through the C ABI in include/respar_b200.h.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <memory>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "respar_b200.h"
+
+namespace respar::b200 {
+
+// ---- the reference's exception types (tensor.hpp:11-13, config.hpp:13-15, runtime.hpp:15-20)
+struct ShapeError : std::invalid_argument {
+  using std::invalid_argument::invalid_argument;
+};
+struct ConfigError : std::invalid_argument {
+  using std::invalid_argument::invalid_argument;
+};
+struct StageError : std::runtime_error {
+  int stage;
+  StageError(int s, const std::string& what) : std::runtime_error("stage " + std::to_string(s) + ": " + what), stage(s) {}
+};
+// CUDA / NCCL / internal failures.
+struct DeviceError : std::runtime_error {
+  int code;
+  DeviceError(int c, const std::string& m) : std::runtime_error(m), code(c) {}
+};
+
+// Throws the exception type the reference would throw for an rp status code.
+[[noreturn]] void throw_status(int code, const std::string& msg);
+// Status code for an exception thrown by this library (inverse of throw_status).
+int status_of(const std::exception& e);
+inline void check(int rc) {
+  if (rc != RP_OK) throw_status(rc, rp_last_error());
+}
+
+enum class TrainMode { Serial = RP_MODE_SERIAL, Penalty = RP_MODE_PENALTY, Alm = RP_MODE_ALM };
+enum class PenaltyKind { SquaredL2 = RP_PSI_SQUARED_L2, L1 = RP_PSI_L1, LInf = RP_PSI_LINF };
+
+// Owning device allocation (RAII), pinned to one device.
+class DeviceArray {
+ public:
+  DeviceArray() = default;
+  ~DeviceArray();
+  DeviceArray(const DeviceArray&) = delete;
+  DeviceArray& operator=(const DeviceArray&) = delete;
+  DeviceArray(DeviceArray&& o) noexcept { swap(o); }
+  DeviceArray& operator=(DeviceArray&& o) noexcept {
+    swap(o);
+    return *this;
+  }
+  void allocate(int device, int64_t bytes);  // no-op when already at least that big
+  void zero(cudaStream_t s);
+  template <class T = float>
+  T* get() const {
+    return static_cast<T*>(ptr_);
+  }
+  int64_t bytes() const { return bytes_; }
+  int device() const { return device_; }
+
+ private:
+  void swap(DeviceArray& o) noexcept {
+    std::swap(ptr_, o.ptr_);
+    std::swap(bytes_, o.bytes_);
+    std::swap(device_, o.device_);
+  }
+  void* ptr_ = nullptr;
+  int64_t bytes_ = 0;
+  int device_ = 0;
+};
+
+// StepParams (decoupled.hpp:45-52) + momentum (0 == the reference's plain GD).
+struct StepParams {
+  double beta = 1.0;
+  double tau = -1.0;
+  double lr = 0.1;
+  double lambda_lr = 0.1;
+  double kappa_lr = 1e-9;
+  int max_corrections = 1;
+  double momentum = 0.0;
+};
+
+struct ViolationReport {
+  std::vector<double> per_stage;
+  double max_violation = 0.0;
+  long normalizer = 0;
+};
+
+// partition (decoupled.cpp:10-21): K equal ranges; ConfigError unless K divides L.
+std::vector<std::pair<int, int>> partition(int num_blocks, int stages);
+
+// StagePool replacement (runtime.hpp:33-67): stage k runs on devices[floor(k*G/K)],
+// on its own stream; the iteration barrier is a control stream waiting on every stage's
+// completion event, so nothing host-side blocks unless a result is read back.
+class StageScheduler {
+ public:
+  StageScheduler(int stages, std::vector<int> devices);
+  ~StageScheduler();
+  StageScheduler(const StageScheduler&) = delete;
+  StageScheduler& operator=(const StageScheduler&) = delete;
+
+  int stages() const { return static_cast<int>(streams_.size()); }
+  int device_of(int k) const { return devices_.at(k); }
+  cudaStream_t stream(int k) const { return streams_.at(k); }
+  cudaStream_t control() const { return ctl_; }
+  int control_device() const { return devices_.at(0); }
+  // iteration bracket: begin() fans out from the control stream, end() joins.
+  void begin();
+  void end();
+  // stream `k` waits for the last record of `what` on stream `j`
+  enum Mark { kBackwardDone = 0, kCorrectionDone = 1, kStageDone = 2, kNumMarks = 3 };
+  void record(int j, Mark what);
+  void wait(int k, int j, Mark what);
+  float last_ms() const;  // device time between begin() and end() (control stream)
+  // device-timed region over many iterations on the control stream
+  void region_begin();
+  float region_end();
+  void sync();
+
+ private:
+  std::vector<int> devices_;
+  std::vector<cudaStream_t> streams_;
+  std::vector<cudaEvent_t> marks_;  // [stage][Mark]
+  cudaStream_t ctl_ = nullptr;
+  cudaEvent_t ev_begin_ = nullptr, ev_end_ = nullptr, ev_rb_ = nullptr, ev_re_ = nullptr;
+  bool timed_ = false;
+};
+
+// DecoupledTrainer (decoupled.hpp:56-120) on device.  Parameters are fp32 in the flat
+// layout of include/respar_b200.h; lambda/kappa/boundary state is N_train x (H W C) fp32.
+class DecoupledTrainer {
+ public:
+  DecoupledTrainer(const rp_geometry& g, int stages, TrainMode mode, PenaltyKind kind, int num_samples,
+                   int math = RP_MATH_FP32, std::vector<int> devices = {});
+  ~DecoupledTrainer();
+
+  // ---- parameters (ResidualNet, network.hpp:29-41) ----
+  void init_params(uint64_t& rng_state);  // make_net draw order (network.cpp:49-68)
+  void set_params(const float* host);
+  void get_params(float* host) const;
+  void get_grads(float* host) const;
+  int64_t param_count() const { return param_total_; }
+
+  // ---- reference methods; x / labels are device pointers ----
+  void reset_lambda_from_forward(const float* full_x);
+  double step(const float* batch_x, const int32_t* labels, int nrows, int row0, const StepParams& p,
+              bool read_loss = true);
+  void take_snapshot(int k, int row0, int nrows);
+  void stage_forward(int k, const float* batch_x, int nrows, int row0);
+  void stage_backward_update(int k, const int32_t* labels, double beta, double lr, int row0, double momentum = 0.0);
+  void correct_aux(int k, const StepParams& p, int row0, int nrows);
+  void correct_multiplier(int k, double beta, double kappa_lr, int row0, int nrows);
+  void correction_gradient(int k, double beta, int row0, int nrows, float* out) const;
+  ViolationReport violation_report() const;
+  double last_loss() const;
+  // full serial forward of the current net (eval): logits [nrows, classes] device
+  void forward(const float* x, int nrows, float* logits);
+
+  static long normalizer(int nrows, int feature_size) { return static_cast<long>(nrows) * feature_size; }
+
+  // ---- state access (decoupled.hpp:29-32): 0 lambda, 1 kappa, 2 boundary_out, 3 boundary_adjoint
+  int64_t state_elems(int k, int which) const;
+  void get_state(int k, int which, float* host) const;
+  void set_state(int k, int which, const float* host);
+
+  int stages() const { return static_cast<int>(stages_.size()); }
+  int blocks_per_stage() const { return blocks_per_stage_; }
+  long iteration() const { return iteration_; }
+  long stage_version(int k) const { return stages_.at(k).version; }
+  int num_samples() const { return num_samples_; }
+  const rp_geometry& geometry() const { return geo_; }
+  TrainMode mode() const { return mode_; }
+  PenaltyKind penalty_kind() const { return kind_; }
+  void set_kappa_rule(int rule) { kappa_rule_ = rule; }
+  StageScheduler& scheduler() { return *sched_; }
+  float last_step_ms() const { return sched_->last_ms(); }
+  // device staging for host inputs (used by the C ABI host-buffer entry points)
+  float* input_staging(int nrows);
+  int32_t* label_staging(int nrows);
+
+ private:
+  struct Stage {
+    int index = 0, begin = 0, end = 0, device = 0;
+    DeviceArray lam, kappa, bout, badj;  // [num_samples][feat]
+    bool kappa_zero = true;
+    std::vector<DeviceArray> xs;  // tape inputs x_1..x_{n-1}
+    std::vector<DeviceArray> as;  // tape activations a_0..a_{n-1}
+    DeviceArray x0, dpre, ws, red_ws, pooled, logits, loss;
+    DeviceArray snap_lam, snap_kappa;
+    int snap_rows = -1;
+    bool snap_has_kappa = false;
+    int cap_rows = 0;
+    long version = -1;
+    int fwd_rows = 0, fwd_row0 = 0;
+    const float* input0 = nullptr;  // x_0 of the last forward
+    const float* raw = nullptr;     // raw input of the last forward (stage 0)
+  };
+
+  void ensure_capacity(int nrows);
+  const float* params_for(int k) const;
+  float* params_for(int k);
+  float* grads_for(int k);
+  void run_forward(Stage& st, const float* input, int nrows, float* out_features, cudaStream_t s);
+  void run_backward(Stage& st, const int32_t* labels, int nrows, int row0, double beta, double lr, double momentum,
+                    bool use_snapshot, cudaStream_t s);
+  void run_correction(int k, const StepParams& p, int row0, int nrows, bool fuse_kappa, cudaStream_t s);
+  void check_rows(int row0, int nrows, const char* where) const;
+  int64_t feat() const { return (int64_t)geo_.height * geo_.width * geo_.channels; }
+  int64_t hid() const { return (int64_t)geo_.height * geo_.width * geo_.hidden; }
+  int64_t raw_feat() const { return (int64_t)geo_.height * geo_.width * geo_.in_channels; }
+
+  rp_geometry geo_;
+  TrainMode mode_;
+  PenaltyKind kind_;
+  int num_samples_;
+  int math_;
+  int kappa_rule_ = RP_KAPPA_RULE_REFERENCE;
+  int blocks_per_stage_ = 0;
+  int64_t param_total_ = 0;
+  std::vector<int> devices_;               // per stage
+  std::vector<int> unique_devices_;
+  std::vector<DeviceArray> params_, grads_, mom_;  // per unique device
+  std::vector<Stage> stages_;
+  std::unique_ptr<StageScheduler> sched_;
+  DeviceArray in_stage_, lab_stage_, eval_a_, eval_b_;
+  long iteration_ = 0;
+  bool has_forward_ = false;
+};
+
+}  // namespace respar::b200

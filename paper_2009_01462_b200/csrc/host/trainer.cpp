@@ -1,0 +1,745 @@
+// DecoupledTrainer / StageScheduler on device (reference decoupled.cpp:10-205,
+// runtime.cpp:9-110).  Every GPU operation goes through the C ABI (rp_op_*).
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+
+#include "respar_b200.hpp"
+
+namespace respar::b200 {
+
+namespace {
+
+void cu(cudaError_t e, const char* what) {
+  if (e != cudaSuccess) throw DeviceError(RP_ERR_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+struct DeviceGuard {
+  int prev = 0;
+  explicit DeviceGuard(int d) {
+    cudaGetDevice(&prev);
+    if (d != prev) cu(cudaSetDevice(d), "cudaSetDevice");
+  }
+  ~DeviceGuard() { cudaSetDevice(prev); }
+};
+
+struct Layout {
+  int64_t s_w, s_b, block0, block_stride, t_w, t_b, total;
+  explicit Layout(const rp_geometry& g) {
+    s_w = 0;
+    block0 = rp_param_offset_block(&g, 0);
+    block_stride = g.blocks > 1 ? rp_param_offset_block(&g, 1) - block0 : rp_param_offset_head(&g) - block0;
+    s_b = block0 - g.channels;
+    t_w = rp_param_offset_head(&g);
+    t_b = t_w + (int64_t)g.channels * g.classes;
+    total = rp_param_count(&g);
+  }
+};
+
+}  // namespace
+
+[[noreturn]] void throw_status(int code, const std::string& msg) {
+  switch (code) {
+    case RP_ERR_SHAPE: throw ShapeError(msg);
+    case RP_ERR_CONFIG: throw ConfigError(msg);
+    case RP_ERR_STATE: throw std::logic_error(msg);
+    case RP_ERR_RANGE: throw std::invalid_argument(msg);
+    case RP_ERR_STAGE: throw StageError(-1, msg);
+    case RP_ERR_DIVERGED: throw std::runtime_error(msg);
+    default: throw DeviceError(code, msg);
+  }
+}
+
+int status_of(const std::exception& e) {
+  if (dynamic_cast<const ShapeError*>(&e)) return RP_ERR_SHAPE;
+  if (dynamic_cast<const ConfigError*>(&e)) return RP_ERR_CONFIG;
+  if (dynamic_cast<const StageError*>(&e)) return RP_ERR_STAGE;
+  if (auto* d = dynamic_cast<const DeviceError*>(&e)) return d->code;
+  if (dynamic_cast<const std::invalid_argument*>(&e)) return RP_ERR_RANGE;
+  if (dynamic_cast<const std::logic_error*>(&e)) return RP_ERR_STATE;
+  return RP_ERR_INTERNAL;
+}
+
+// ------------------------------------------------------------- DeviceArray
+DeviceArray::~DeviceArray() {
+  if (ptr_) {
+    int prev = 0;
+    cudaGetDevice(&prev);
+    cudaSetDevice(device_);
+    cudaFree(ptr_);
+    cudaSetDevice(prev);
+  }
+}
+
+void DeviceArray::allocate(int device, int64_t bytes) {
+  if (ptr_ && bytes <= bytes_ && device == device_) return;
+  if (ptr_) {
+    DeviceGuard g(device_);
+    cudaFree(ptr_);
+    ptr_ = nullptr;
+    bytes_ = 0;
+  }
+  if (bytes <= 0) return;
+  DeviceGuard g(device);
+  cu(cudaMalloc(&ptr_, static_cast<size_t>(bytes)), "cudaMalloc");
+  bytes_ = bytes;
+  device_ = device;
+}
+
+void DeviceArray::zero(cudaStream_t s) {
+  if (ptr_) {
+    DeviceGuard g(device_);
+    cu(cudaMemsetAsync(ptr_, 0, static_cast<size_t>(bytes_), s), "cudaMemsetAsync");
+  }
+}
+
+// --------------------------------------------------------------- partition
+std::vector<std::pair<int, int>> partition(int num_blocks, int stages) {
+  if (stages < 1) throw ConfigError("partition: need at least one stage");
+  if (num_blocks < 1 || num_blocks % stages != 0)
+    throw ConfigError("partition: " + std::to_string(stages) + " stages do not divide " + std::to_string(num_blocks) +
+                      " blocks evenly");
+  const int n = num_blocks / stages;
+  std::vector<std::pair<int, int>> r;
+  for (int k = 0; k < stages; ++k) r.emplace_back(k * n, (k + 1) * n);
+  return r;
+}
+
+// ---------------------------------------------------------- StageScheduler
+StageScheduler::StageScheduler(int stages, std::vector<int> devices) {
+  if (stages < 1) throw std::invalid_argument("StageScheduler: need at least one stage");
+  if (devices.empty()) {
+    int d = 0;
+    cu(cudaGetDevice(&d), "cudaGetDevice");
+    devices.push_back(d);
+  }
+  const int G = static_cast<int>(devices.size());
+  for (int k = 0; k < stages; ++k) devices_.push_back(devices[(int64_t)k * G / stages]);
+  streams_.resize(stages);
+  marks_.resize((size_t)stages * kNumMarks);
+  for (int k = 0; k < stages; ++k) {
+    DeviceGuard g(devices_[k]);
+    cu(cudaStreamCreateWithFlags(&streams_[k], cudaStreamNonBlocking), "cudaStreamCreate");
+    for (int m = 0; m < kNumMarks; ++m)
+      cu(cudaEventCreateWithFlags(&marks_[(size_t)k * kNumMarks + m], cudaEventDisableTiming), "cudaEventCreate");
+  }
+  DeviceGuard g(devices_[0]);
+  cu(cudaStreamCreateWithFlags(&ctl_, cudaStreamNonBlocking), "cudaStreamCreate");
+  cu(cudaEventCreate(&ev_begin_), "cudaEventCreate");
+  cu(cudaEventCreate(&ev_end_), "cudaEventCreate");
+  cu(cudaEventCreate(&ev_rb_), "cudaEventCreate");
+  cu(cudaEventCreate(&ev_re_), "cudaEventCreate");
+}
+
+StageScheduler::~StageScheduler() {
+  for (size_t k = 0; k < streams_.size(); ++k) {
+    cudaSetDevice(devices_[k]);
+    cudaStreamSynchronize(streams_[k]);
+    cudaStreamDestroy(streams_[k]);
+    for (int m = 0; m < kNumMarks; ++m) cudaEventDestroy(marks_[k * kNumMarks + m]);
+  }
+  cudaSetDevice(devices_[0]);
+  cudaStreamSynchronize(ctl_);
+  cudaStreamDestroy(ctl_);
+  cudaEventDestroy(ev_begin_);
+  cudaEventDestroy(ev_end_);
+  cudaEventDestroy(ev_rb_);
+  cudaEventDestroy(ev_re_);
+}
+
+void StageScheduler::region_begin() {
+  DeviceGuard g(devices_[0]);
+  cu(cudaEventRecord(ev_rb_, ctl_), "cudaEventRecord");
+}
+
+float StageScheduler::region_end() {
+  DeviceGuard g(devices_[0]);
+  cu(cudaEventRecord(ev_re_, ctl_), "cudaEventRecord");
+  cu(cudaEventSynchronize(ev_re_), "cudaEventSynchronize");
+  float ms = 0.f;
+  cu(cudaEventElapsedTime(&ms, ev_rb_, ev_re_), "cudaEventElapsedTime");
+  return ms;
+}
+
+void StageScheduler::begin() {
+  DeviceGuard g(devices_[0]);
+  cu(cudaEventRecord(ev_begin_, ctl_), "cudaEventRecord");
+  for (int k = 0; k < stages(); ++k) {
+    DeviceGuard gk(devices_[k]);
+    cu(cudaStreamWaitEvent(streams_[k], ev_begin_, 0), "cudaStreamWaitEvent");
+  }
+}
+
+void StageScheduler::end() {
+  for (int k = 0; k < stages(); ++k) {
+    record(k, kStageDone);
+    DeviceGuard g(devices_[0]);
+    cu(cudaStreamWaitEvent(ctl_, marks_[(size_t)k * kNumMarks + kStageDone], 0), "cudaStreamWaitEvent");
+  }
+  DeviceGuard g(devices_[0]);
+  cu(cudaEventRecord(ev_end_, ctl_), "cudaEventRecord");
+  timed_ = true;
+}
+
+void StageScheduler::record(int j, Mark what) {
+  DeviceGuard g(devices_[j]);
+  cu(cudaEventRecord(marks_[(size_t)j * kNumMarks + what], streams_[j]), "cudaEventRecord");
+}
+
+void StageScheduler::wait(int k, int j, Mark what) {
+  DeviceGuard g(devices_[k]);
+  cu(cudaStreamWaitEvent(streams_[k], marks_[(size_t)j * kNumMarks + what], 0), "cudaStreamWaitEvent");
+}
+
+float StageScheduler::last_ms() const {
+  if (!timed_) return 0.f;
+  float ms = 0.f;
+  cu(cudaEventSynchronize(ev_end_), "cudaEventSynchronize");
+  cu(cudaEventElapsedTime(&ms, ev_begin_, ev_end_), "cudaEventElapsedTime");
+  return ms;
+}
+
+void StageScheduler::sync() {
+  for (int k = 0; k < stages(); ++k) {
+    DeviceGuard g(devices_[k]);
+    cu(cudaStreamSynchronize(streams_[k]), "cudaStreamSynchronize");
+  }
+  DeviceGuard g(devices_[0]);
+  cu(cudaStreamSynchronize(ctl_), "cudaStreamSynchronize");
+}
+
+// --------------------------------------------------------- DecoupledTrainer
+DecoupledTrainer::DecoupledTrainer(const rp_geometry& g, int stages, TrainMode mode, PenaltyKind kind,
+                                   int num_samples, int math, std::vector<int> devices)
+    : geo_(g), mode_(mode), kind_(kind), num_samples_(num_samples), math_(math) {
+  if (rp_param_count(&g) < 0) check(RP_ERR_CONFIG);
+  if (num_samples < 1) throw ConfigError("DecoupledTrainer: need at least one sample");
+  const auto ranges = partition(g.blocks, stages);
+  blocks_per_stage_ = ranges[0].second - ranges[0].first;
+  sched_ = std::make_unique<StageScheduler>(stages, devices);
+  param_total_ = rp_param_count(&g);
+  for (int k = 0; k < stages; ++k) {
+    devices_.push_back(sched_->device_of(k));
+    if (std::find(unique_devices_.begin(), unique_devices_.end(), devices_[k]) == unique_devices_.end())
+      unique_devices_.push_back(devices_[k]);
+  }
+  params_.resize(unique_devices_.size());
+  grads_.resize(unique_devices_.size());
+  mom_.resize(unique_devices_.size());
+  for (size_t i = 0; i < unique_devices_.size(); ++i) {
+    params_[i].allocate(unique_devices_[i], param_total_ * 4);
+    grads_[i].allocate(unique_devices_[i], param_total_ * 4);
+    params_[i].zero(nullptr);
+    grads_[i].zero(nullptr);
+  }
+  stages_.resize(stages);
+  const int64_t state_bytes = (int64_t)num_samples * feat() * 4;
+  for (int k = 0; k < stages; ++k) {
+    Stage& st = stages_[k];
+    st.index = k;
+    st.begin = ranges[k].first;
+    st.end = ranges[k].second;
+    st.device = devices_[k];
+    if (k > 0) {
+      st.lam.allocate(st.device, state_bytes);
+      st.kappa.allocate(st.device, state_bytes);
+      st.lam.zero(nullptr);
+      st.kappa.zero(nullptr);
+    }
+    st.bout.allocate(st.device, state_bytes);
+    st.badj.allocate(st.device, state_bytes);
+    st.bout.zero(nullptr);
+    st.badj.zero(nullptr);
+    st.loss.allocate(st.device, 8);
+    st.loss.zero(nullptr);
+    st.red_ws.allocate(st.device, rp_op_reduce_workspace_bytes());
+  }
+  cu(cudaDeviceSynchronize(), "cudaDeviceSynchronize");
+}
+
+DecoupledTrainer::~DecoupledTrainer() {
+  if (sched_) sched_->sync();
+}
+
+static size_t dev_index(const std::vector<int>& u, int d) {
+  return static_cast<size_t>(std::find(u.begin(), u.end(), d) - u.begin());
+}
+
+const float* DecoupledTrainer::params_for(int k) const {
+  return params_[dev_index(unique_devices_, devices_[k])].get();
+}
+float* DecoupledTrainer::params_for(int k) { return params_[dev_index(unique_devices_, devices_[k])].get(); }
+float* DecoupledTrainer::grads_for(int k) { return grads_[dev_index(unique_devices_, devices_[k])].get(); }
+
+void DecoupledTrainer::init_params(uint64_t& rng_state) {
+  uint64_t s0 = rng_state;
+  for (size_t i = 0; i < unique_devices_.size(); ++i) {
+    DeviceGuard g(unique_devices_[i]);
+    uint64_t s = s0;
+    check(rp_op_init_params(&geo_, params_[i].get(), &s, nullptr));
+    rng_state = s;
+  }
+  cu(cudaDeviceSynchronize(), "cudaDeviceSynchronize");
+}
+
+void DecoupledTrainer::set_params(const float* host) {
+  sched_->sync();
+  for (size_t i = 0; i < unique_devices_.size(); ++i) {
+    DeviceGuard g(unique_devices_[i]);
+    cu(cudaMemcpy(params_[i].get(), host, param_total_ * 4, cudaMemcpyHostToDevice), "cudaMemcpy H2D");
+  }
+}
+
+void DecoupledTrainer::get_params(float* host) const {
+  sched_->sync();
+  // each stage's device owns its parameter slice (stage 0 owns S, stage K-1 owns T)
+  const Layout L(geo_);
+  for (int k = 0; k < stages(); ++k) {
+    const Stage& st = stages_[k];
+    int64_t beg = L.block0 + (int64_t)st.begin * L.block_stride;
+    int64_t end = L.block0 + (int64_t)st.end * L.block_stride;
+    if (k == 0) beg = 0;
+    if (k == stages() - 1) end = L.total;
+    DeviceGuard g(st.device);
+    cu(cudaMemcpy(host + beg, params_for(k) + beg, (end - beg) * 4, cudaMemcpyDeviceToHost), "cudaMemcpy D2H");
+  }
+}
+
+void DecoupledTrainer::get_grads(float* host) const {
+  sched_->sync();
+  const Layout L(geo_);
+  for (int k = 0; k < stages(); ++k) {
+    const Stage& st = stages_[k];
+    int64_t beg = L.block0 + (int64_t)st.begin * L.block_stride;
+    int64_t end = L.block0 + (int64_t)st.end * L.block_stride;
+    if (k == 0) beg = 0;
+    if (k == stages() - 1) end = L.total;
+    DeviceGuard g(st.device);
+    const float* src = grads_[dev_index(unique_devices_, st.device)].get();
+    cu(cudaMemcpy(host + beg, src + beg, (end - beg) * 4, cudaMemcpyDeviceToHost), "cudaMemcpy D2H");
+  }
+}
+
+void DecoupledTrainer::ensure_capacity(int nrows) {
+  for (int k = 0; k < stages(); ++k) {
+    Stage& st = stages_[k];
+    if (st.cap_rows >= nrows) continue;
+    const int n = st.end - st.begin;
+    st.xs.resize(n);
+    st.as.resize(n);
+    for (int i = 0; i < n; ++i) {
+      if (i > 0) st.xs[i].allocate(st.device, (int64_t)nrows * feat() * 4);
+      st.as[i].allocate(st.device, (int64_t)nrows * hid() * 4);
+    }
+    if (k == 0) st.x0.allocate(st.device, (int64_t)nrows * feat() * 4);
+    st.dpre.allocate(st.device, (int64_t)nrows * hid() * 4);
+    st.ws.allocate(st.device, rp_op_workspace_bytes(&geo_, nrows, math_));
+    if (k == stages() - 1) {
+      st.pooled.allocate(st.device, (int64_t)nrows * geo_.channels * 4);
+      st.logits.allocate(st.device, (int64_t)nrows * geo_.classes * 4);
+    }
+    st.cap_rows = nrows;
+  }
+}
+
+float* DecoupledTrainer::input_staging(int nrows) {
+  in_stage_.allocate(stages_[0].device, std::max<int64_t>(1, (int64_t)nrows * raw_feat() * 4));
+  return in_stage_.get();
+}
+
+int32_t* DecoupledTrainer::label_staging(int nrows) {
+  lab_stage_.allocate(stages_.back().device, std::max<int64_t>(4, (int64_t)nrows * 4));
+  return lab_stage_.get<int32_t>();
+}
+
+void DecoupledTrainer::check_rows(int row0, int nrows, const char* where) const {
+  if (row0 < 0 || nrows < 0 || (int64_t)row0 + nrows > num_samples_)
+    throw ShapeError(std::string(where) + ": rows [" + std::to_string(row0) + ", " + std::to_string(row0 + nrows) +
+                     ") out of " + std::to_string(num_samples_) + " samples");
+}
+
+// net_forward over the stage's block range (network.cpp:112-143).  The stage output
+// (X^k_end) is written to out_features; the tape keeps x_1..x_{n-1} and every a.
+void DecoupledTrainer::run_forward(Stage& st, const float* input, int nrows, float* out_features, cudaStream_t s) {
+  const Layout L(geo_);
+  const float* P = params_for(st.index);
+  const float* cur = input;
+  if (st.index == 0) {
+    check(rp_op_stem_fwd(&geo_, nrows, input, P, st.x0.get(), math_, st.ws.get(), st.ws.bytes(), s));
+    st.raw = input;
+    cur = st.x0.get();
+  }
+  st.input0 = cur;
+  const int n = st.end - st.begin;
+  for (int i = 0; i < n; ++i) {
+    const int l = st.begin + i;
+    float* out = i == n - 1 ? out_features : st.xs[i + 1].get();
+    check(rp_op_block_fwd(&geo_, nrows, cur, P + L.block0 + (int64_t)l * L.block_stride, st.as[i].get(), out, math_,
+                          st.ws.get(), st.ws.bytes(), s));
+    cur = out;
+  }
+  if (st.index == stages() - 1)
+    check(rp_op_head_fwd(&geo_, nrows, out_features, P + L.t_w, st.pooled.get(), st.logits.get(), s));
+}
+
+// stage_backward_update body (decoupled.cpp:85-115): upstream, net_vjp, apply_updates,
+// boundary_adjoint.  The cotangent lives in the boundary_adjoint rows and is updated
+// block by block in place, so p^k lands where correct_aux reads it.
+void DecoupledTrainer::run_backward(Stage& st, const int32_t* labels, int nrows, int row0, double beta, double lr,
+                                    double momentum, bool use_snapshot, cudaStream_t s) {
+  const Layout L(geo_);
+  const int k = st.index;
+  float* P = params_for(k);
+  float* G = grads_for(k);
+  float* g = st.badj.get() + (int64_t)row0 * feat();
+  const float* x_end = st.bout.get() + (int64_t)st.fwd_row0 * feat();
+  const int64_t n = (int64_t)nrows * feat();
+  if (k == stages() - 1) {
+    check(rp_op_head_loss_bwd(&geo_, nrows, st.pooled.get(), st.logits.get(), P + L.t_w, labels, st.loss.get<double>(),
+                              G + L.t_w, g, st.ws.get(), st.ws.bytes(), s));
+  } else {
+    const Stage& nx = stages_[k + 1];
+    const float* lam_next;
+    const float* kap_next;
+    if (use_snapshot) {
+      lam_next = st.snap_lam.get();
+      kap_next = st.snap_has_kappa ? st.snap_kappa.get() : nullptr;
+    } else {
+      lam_next = nx.lam.get() + (int64_t)row0 * feat();
+      kap_next = nx.kappa_zero ? nullptr : nx.kappa.get() + (int64_t)row0 * feat();
+    }
+    const double w = beta / static_cast<double>(normalizer(nrows, (int)feat()));
+    check(rp_op_synthetic_grad((int)kind_, lam_next, x_end, kap_next, n, w, g, st.red_ws.get(), s));
+  }
+  const int nb = st.end - st.begin;
+  for (int i = nb - 1; i >= 0; --i) {
+    const int l = st.begin + i;
+    const float* xin = i == 0 ? st.input0 : st.xs[i].get();
+    const int64_t off = L.block0 + (int64_t)l * L.block_stride;
+    check(rp_op_block_bwd(&geo_, nrows, xin, st.as[i].get(), P + off, g, st.dpre.get(), G + off, math_, st.ws.get(),
+                          st.ws.bytes(), s));
+  }
+  if (k == 0) check(rp_op_stem_bwd(&geo_, nrows, st.raw, g, G, st.ws.get(), st.ws.bytes(), s));
+  // apply_updates (network.cpp:174-191): the stage's parameter range is contiguous
+  int64_t beg = L.block0 + (int64_t)st.begin * L.block_stride;
+  int64_t end = L.block0 + (int64_t)st.end * L.block_stride;
+  if (k == 0) beg = 0;
+  if (k == stages() - 1) end = L.total;
+  float* v = nullptr;
+  if (momentum != 0.0) {
+    const size_t di = dev_index(unique_devices_, st.device);
+    if (mom_[di].bytes() == 0) {
+      mom_[di].allocate(st.device, param_total_ * 4);
+      mom_[di].zero(s);
+    }
+    v = mom_[di].get() + beg;
+  }
+  check(rp_op_sgd(P + beg, G + beg, v, end - beg, lr, momentum, s));
+}
+
+// correct_aux + correct_multiplier (decoupled.cpp:135-170) for boundary k.
+void DecoupledTrainer::run_correction(int k, const StepParams& p, int row0, int nrows, bool fuse_kappa,
+                                      cudaStream_t s) {
+  Stage& st = stages_[k];
+  const Stage& prev = stages_[k - 1];
+  const int64_t off = (int64_t)row0 * feat();
+  const int64_t n = (int64_t)nrows * feat();
+  const long norm = normalizer(nrows, (int)feat());
+  const double w = p.beta / static_cast<double>(norm);
+  float* lam = st.lam.get() + off;
+  const float* xp = prev.bout.get() + off;
+  const float* pk = st.badj.get() + off;
+  const bool alm = fuse_kappa && mode_ == TrainMode::Alm;
+  if (alm && kind_ != PenaltyKind::SquaredL2)
+    throw std::logic_error("correct_multiplier: the multiplier update is only derived for the squared_l2 penalty");
+  const double coef = kappa_rule_ == RP_KAPPA_RULE_TEXTBOOK ? -p.beta : p.kappa_lr * (double)norm / (2.0 * p.beta);
+  float* kap = (alm || !st.kappa_zero) ? st.kappa.get() + off : nullptr;
+  const bool single = p.max_corrections <= 1 || p.tau < 0.0;
+  if (single) {
+    check(rp_op_correct((int)kind_, lam, xp, pk, kap, n, w, p.lambda_lr, 1, coef, alm ? 1 : 0, st.red_ws.get(), s));
+  } else {
+    for (int pass = 0; pass < p.max_corrections; ++pass) {
+      if (pass >= 1) {
+        double v = 0.0;
+        check(rp_op_psi((int)kind_, lam, xp, n, &v, st.red_ws.get(), s));
+        if (v <= p.tau) break;
+      }
+      check(rp_op_correct((int)kind_, lam, xp, pk, kap, n, w, p.lambda_lr, 1, 0.0, 0, st.red_ws.get(), s));
+    }
+    if (alm) check(rp_op_correct((int)kind_, lam, xp, pk, kap, n, w, 0.0, 0, coef, 1, st.red_ws.get(), s));
+  }
+  if (alm) st.kappa_zero = false;
+}
+
+void DecoupledTrainer::reset_lambda_from_forward(const float* full_x) {
+  sched_->sync();
+  const int chunk = std::min(num_samples_, std::max(256, stages_[0].cap_rows));
+  ensure_capacity(chunk);
+  for (int r0 = 0; r0 < num_samples_; r0 += chunk) {
+    const int nr = std::min(chunk, num_samples_ - r0);
+    const float* in = full_x + (int64_t)r0 * raw_feat();
+    for (int k = 0; k < stages(); ++k) {
+      Stage& st = stages_[k];
+      DeviceGuard g(st.device);
+      cudaStream_t s = sched_->stream(k);
+      if (k > 0) {
+        // lambda_k := X_{kn} (the previous stage's output rows)
+        const Stage& pv = stages_[k - 1];
+        sched_->record(k - 1, StageScheduler::kStageDone);
+        sched_->wait(k, k - 1, StageScheduler::kStageDone);
+        cu(cudaMemcpyPeerAsync(st.lam.get() + (int64_t)r0 * feat(), st.device, pv.bout.get() + (int64_t)r0 * feat(),
+                               pv.device, (size_t)nr * feat() * 4, s),
+           "cudaMemcpyPeerAsync");
+        in = st.lam.get() + (int64_t)r0 * feat();
+      }
+      run_forward(st, in, nr, st.bout.get() + (int64_t)r0 * feat(), s);
+    }
+  }
+  for (int k = 0; k < stages(); ++k) {
+    Stage& st = stages_[k];
+    DeviceGuard g(st.device);
+    if (k > 0) st.kappa.zero(sched_->stream(k));
+    st.badj.zero(sched_->stream(k));
+    st.kappa_zero = true;
+    st.version = iteration_;
+    st.fwd_rows = 0;
+  }
+  sched_->sync();
+  has_forward_ = true;
+}
+
+double DecoupledTrainer::step(const float* batch_x, const int32_t* labels, int nrows, int row0, const StepParams& p,
+                              bool read_loss) {
+  check_rows(row0, nrows, "step");
+  if (nrows < 1) throw ShapeError("step: empty batch");
+  ensure_capacity(nrows);
+  ++iteration_;
+  sched_->begin();
+  // parallel phase: every stage's forward, synthetic/phi backward and update
+  // (pool.run_iteration, decoupled.cpp:184-187).  Stage k reads lambda_{k+1}/kappa_{k+1}
+  // directly: nothing writes them before the correction phase, so the iteration-start
+  // snapshot of decoupled.cpp:65-73 is implicit.
+  for (int k = 0; k < stages(); ++k) {
+    Stage& st = stages_[k];
+    DeviceGuard g(st.device);
+    cudaStream_t s = sched_->stream(k);
+    const float* in = k == 0 ? batch_x : st.lam.get() + (int64_t)row0 * feat();
+    run_forward(st, in, nrows, st.bout.get() + (int64_t)row0 * feat(), s);
+    st.version = iteration_;
+    st.fwd_rows = nrows;
+    st.fwd_row0 = row0;
+    run_backward(st, labels, nrows, row0, p.beta, p.lr, p.momentum, false, s);
+    sched_->record(k, StageScheduler::kBackwardDone);
+  }
+  has_forward_ = true;
+  // serial correction sweep (decoupled.cpp:189-192): boundaries are independent, so
+  // boundary k runs on stage k's stream once stage k-1 is done.
+  for (int k = 1; k < stages(); ++k) {
+    DeviceGuard g(stages_[k].device);
+    sched_->wait(k, k - 1, StageScheduler::kBackwardDone);
+    run_correction(k, p, row0, nrows, true, sched_->stream(k));
+  }
+  sched_->end();
+  if (!read_loss) return 0.0;
+  return last_loss();
+}
+
+double DecoupledTrainer::last_loss() const {
+  const Stage& st = stages_.back();
+  double v = 0.0;
+  DeviceGuard g(sched_->control_device());
+  cu(cudaMemcpyAsync(&v, st.loss.get(), 8, cudaMemcpyDeviceToHost, sched_->control()), "cudaMemcpyAsync D2H");
+  cu(cudaStreamSynchronize(sched_->control()), "cudaStreamSynchronize");
+  return v;
+}
+
+void DecoupledTrainer::take_snapshot(int k, int row0, int nrows) {
+  if (k < 0 || k >= stages() - 1)
+    throw std::invalid_argument("take_snapshot: stage " + std::to_string(k) + " has no downstream neighbour");
+  check_rows(row0, nrows, "take_snapshot");
+  Stage& st = stages_[k];
+  const Stage& nx = stages_[k + 1];
+  const int64_t bytes = std::max<int64_t>(4, (int64_t)nrows * feat() * 4);
+  st.snap_lam.allocate(st.device, bytes);
+  st.snap_kappa.allocate(st.device, bytes);
+  sched_->sync();
+  DeviceGuard g(st.device);
+  cu(cudaMemcpyPeer(st.snap_lam.get(), st.device, nx.lam.get() + (int64_t)row0 * feat(), nx.device,
+                    (size_t)nrows * feat() * 4),
+     "cudaMemcpyPeer");
+  cu(cudaMemcpyPeer(st.snap_kappa.get(), st.device, nx.kappa.get() + (int64_t)row0 * feat(), nx.device,
+                    (size_t)nrows * feat() * 4),
+     "cudaMemcpyPeer");
+  st.snap_has_kappa = !nx.kappa_zero;
+  st.snap_rows = nrows;
+}
+
+void DecoupledTrainer::stage_forward(int k, const float* batch_x, int nrows, int row0) {
+  if (k < 0 || k >= stages()) throw std::out_of_range("stage_forward: bad stage index");
+  check_rows(row0, nrows, "stage_forward");
+  ensure_capacity(std::max(nrows, 1));
+  Stage& st = stages_[k];
+  DeviceGuard g(st.device);
+  cudaStream_t s = sched_->stream(k);
+  const float* in = k == 0 ? batch_x : st.lam.get() + (int64_t)row0 * feat();
+  run_forward(st, in, nrows, st.bout.get() + (int64_t)row0 * feat(), s);
+  st.version = iteration_;
+  st.fwd_rows = nrows;
+  st.fwd_row0 = row0;
+  has_forward_ = true;
+  cu(cudaStreamSynchronize(s), "cudaStreamSynchronize");
+}
+
+void DecoupledTrainer::stage_backward_update(int k, const int32_t* labels, double beta, double lr, int row0,
+                                             double momentum) {
+  if (k < 0 || k >= stages()) throw std::out_of_range("stage_backward_update: bad stage index");
+  Stage& st = stages_[k];
+  if (st.version != iteration_ || st.fwd_rows == 0)
+    throw std::logic_error("stage_backward_update: stage " + std::to_string(k) +
+                           " has no forward pass for this iteration");
+  const int nrows = st.fwd_rows;
+  check_rows(row0, nrows, "stage_backward_update");
+  if (k < stages() - 1) {
+    if (st.snap_rows < 0)
+      throw std::invalid_argument("stage_backward_update: stage " + std::to_string(k) +
+                                  " needs the (lambda, kappa) snapshot of stage " + std::to_string(k + 1));
+    if (st.snap_rows != nrows) throw ShapeError("stage_backward_update: snapshot rows do not match the batch");
+  }
+  DeviceGuard g(st.device);
+  cudaStream_t s = sched_->stream(k);
+  run_backward(st, labels, nrows, row0, beta, lr, momentum, true, s);
+  cu(cudaStreamSynchronize(s), "cudaStreamSynchronize");
+}
+
+void DecoupledTrainer::correct_aux(int k, const StepParams& p, int row0, int nrows) {
+  if (k < 1 || k >= stages())
+    throw std::invalid_argument("correction: stage " + std::to_string(k) +
+                                " out of range (lambda_0 is fixed to the true input)");
+  if (!has_forward_) throw std::logic_error("correct_aux before any forward pass");
+  check_rows(row0, nrows, "correct_aux");
+  sched_->sync();
+  DeviceGuard g(stages_[k].device);
+  run_correction(k, p, row0, nrows, false, sched_->stream(k));
+  sched_->sync();
+}
+
+void DecoupledTrainer::correct_multiplier(int k, double beta, double kappa_lr, int row0, int nrows) {
+  if (k < 1 || k >= stages())
+    throw std::invalid_argument("correction: stage " + std::to_string(k) +
+                                " out of range (lambda_0 is fixed to the true input)");
+  if (kind_ != PenaltyKind::SquaredL2)
+    throw std::logic_error("correct_multiplier: the multiplier update is only derived for the squared_l2 penalty");
+  check_rows(row0, nrows, "correct_multiplier");
+  sched_->sync();
+  Stage& st = stages_[k];
+  const int64_t off = (int64_t)row0 * feat();
+  const long norm = normalizer(nrows, (int)feat());
+  const double coef = kappa_rule_ == RP_KAPPA_RULE_TEXTBOOK ? -beta : kappa_lr * (double)norm / (2.0 * beta);
+  DeviceGuard g(st.device);
+  check(rp_op_correct((int)kind_, st.lam.get() + off, stages_[k - 1].bout.get() + off, nullptr, st.kappa.get() + off,
+                      (int64_t)nrows * feat(), 0.0, 0.0, 0, coef, 1, st.red_ws.get(), sched_->stream(k)));
+  st.kappa_zero = false;
+  sched_->sync();
+}
+
+void DecoupledTrainer::correction_gradient(int k, double beta, int row0, int nrows, float* out) const {
+  if (k < 1 || k >= stages())
+    throw std::invalid_argument("correction: stage " + std::to_string(k) +
+                                " out of range (lambda_0 is fixed to the true input)");
+  check_rows(row0, nrows, "correction_gradient");
+  sched_->sync();
+  const Stage& st = stages_[k];
+  const int64_t off = (int64_t)row0 * feat();
+  const int64_t n = (int64_t)nrows * feat();
+  const double w = beta / static_cast<double>(normalizer(nrows, (int)feat()));
+  DeviceGuard g(st.device);
+  cudaStream_t s = sched_->stream(k);
+  // g = w d_lambda psi + p - kappa   (decoupled.cpp:124-133)
+  check(rp_op_psi_grad((int)kind_, st.lam.get() + off, stages_[k - 1].bout.get() + off, n, w, out, st.red_ws.get(), s));
+  check(rp_op_sgd(out, st.badj.get() + off, nullptr, n, -1.0, 0.0, s));   // out += p
+  check(rp_op_sgd(out, st.kappa.get() + off, nullptr, n, 1.0, 0.0, s));   // out -= kappa
+  cu(cudaStreamSynchronize(s), "cudaStreamSynchronize");
+}
+
+ViolationReport DecoupledTrainer::violation_report() const {
+  if (!has_forward_) throw std::logic_error("violation_report: no forward pass has cached boundary states yet");
+  sched_->sync();
+  ViolationReport r;
+  r.normalizer = normalizer(num_samples_, (int)feat());
+  r.per_stage.push_back(0.0);
+  for (int k = 1; k < stages(); ++k) {
+    const Stage& st = stages_[k];
+    DeviceGuard g(st.device);
+    double v = 0.0;
+    check(rp_op_psi((int)kind_, st.lam.get(), stages_[k - 1].bout.get(), (int64_t)num_samples_ * feat(), &v,
+                    st.red_ws.get(), sched_->stream(k)));
+    r.per_stage.push_back(v);
+  }
+  for (double v : r.per_stage) r.max_violation = std::max(r.max_violation, v);
+  return r;
+}
+
+void DecoupledTrainer::forward(const float* x, int nrows, float* logits) {
+  sched_->sync();
+  if (nrows <= 0) return;
+  const int chunk = std::max(1, std::min(nrows, std::max(256, stages_[0].cap_rows)));
+  ensure_capacity(chunk);
+  eval_a_.allocate(stages_[0].device, (int64_t)chunk * feat() * 4);
+  eval_b_.allocate(stages_[0].device, (int64_t)chunk * feat() * 4);
+  if (unique_devices_.size() > 1) throw std::logic_error("forward: eval on multi-device trainers is not supported");
+  cudaStream_t s = sched_->stream(0);
+  DeviceGuard g(stages_[0].device);
+  for (int r0 = 0; r0 < nrows; r0 += chunk) {
+    const int nr = std::min(chunk, nrows - r0);
+    const float* in = x + (int64_t)r0 * raw_feat();
+    float* bufs[2] = {eval_a_.get(), eval_b_.get()};
+    for (int k = 0; k < stages(); ++k) {
+      Stage& st = stages_[k];
+      float* out = bufs[k & 1];
+      // run_forward records tape pointers; eval does not touch trainer state otherwise
+      const float* saved_in0 = st.input0;
+      const float* saved_raw = st.raw;
+      run_forward(st, in, nr, out, s);
+      st.input0 = saved_in0;
+      st.raw = saved_raw;
+      in = out;
+    }
+    const Stage& last = stages_.back();
+    cu(cudaMemcpyAsync(logits + (int64_t)r0 * geo_.classes, last.logits.get(), (size_t)nr * geo_.classes * 4,
+                       cudaMemcpyDeviceToDevice, s),
+       "cudaMemcpyAsync");
+  }
+  cu(cudaStreamSynchronize(s), "cudaStreamSynchronize");
+  // eval clobbered the tapes: a following stage_backward_update needs a fresh forward
+  for (auto& st : stages_) st.version = -1;
+}
+
+int64_t DecoupledTrainer::state_elems(int k, int which) const {
+  if (k < 0 || k >= stages()) throw std::out_of_range("state: bad stage index");
+  if (which < 0 || which > 3) throw std::invalid_argument("state: which must be 0..3");
+  if (k == 0 && which < 2) return 0;
+  return (int64_t)num_samples_ * feat();
+}
+
+void DecoupledTrainer::get_state(int k, int which, float* host) const {
+  const int64_t n = state_elems(k, which);
+  if (n == 0) return;
+  sched_->sync();
+  const Stage& st = stages_[k];
+  const DeviceArray* arr[4] = {&st.lam, &st.kappa, &st.bout, &st.badj};
+  DeviceGuard g(st.device);
+  cu(cudaMemcpy(host, arr[which]->get(), n * 4, cudaMemcpyDeviceToHost), "cudaMemcpy D2H");
+}
+
+void DecoupledTrainer::set_state(int k, int which, const float* host) {
+  const int64_t n = state_elems(k, which);
+  if (n == 0) throw ShapeError("set_state: stage 0 has no lambda/kappa");
+  sched_->sync();
+  Stage& st = stages_[k];
+  DeviceArray* arr[4] = {&st.lam, &st.kappa, &st.bout, &st.badj};
+  DeviceGuard g(st.device);
+  cu(cudaMemcpy(arr[which]->get(), host, n * 4, cudaMemcpyHostToDevice), "cudaMemcpy H2D");
+  if (which == 1) st.kappa_zero = false;
+}
+
+}  // namespace respar::b200

@@ -1,0 +1,194 @@
+// Output map T and the task loss (network.cpp:108-110, 193-221), conv form:
+// global average pool -> affine C->classes -> mean softmax-CE, and its backward.
+// All reductions run in a fixed order (deterministic).
+#include <cfloat>
+
+#include "../common.cuh"
+#include "kernels.cuh"
+
+namespace rp::k {
+
+namespace {
+
+// pooled[b][c] = mean_p x[b][p][c]; one CTA per sample.
+__global__ __launch_bounds__(256) void gap_kernel(const float* __restrict__ x, int hw, int C,
+                                                 float* __restrict__ pooled) {
+  extern __shared__ float sh[];
+  const int b = blockIdx.x;
+  const float* xb = x + (int64_t)b * hw * C;
+  const int groups = C <= 256 ? max(1, 256 / C) : 1;
+  const float inv = 1.f / (float)hw;
+  for (int cbase = 0; cbase < C; cbase += 256) {
+    const int cw = min(256, C - cbase);
+    const int g = threadIdx.x / cw;
+    const int c = cbase + threadIdx.x % cw;
+    float acc = 0.f;
+    if (g < groups && threadIdx.x < groups * cw)
+      for (int p = g; p < hw; p += groups) acc += xb[(int64_t)p * C + c];
+    if (threadIdx.x < groups * cw) sh[g * cw + (c - cbase)] = acc;
+    __syncthreads();
+    if (threadIdx.x < cw) {
+      float s = 0.f;
+      for (int gg = 0; gg < groups; ++gg) s += sh[gg * cw + threadIdx.x];
+      pooled[(int64_t)b * C + cbase + threadIdx.x] = s * inv;
+    }
+    __syncthreads();
+  }
+}
+
+// logits[b][j] = sum_c pooled[b][c] t_w[c][j] + t_b[j]   (affine_forward)
+__global__ void fc_kernel(const float* __restrict__ pooled, const float* __restrict__ t_w,
+                          const float* __restrict__ t_b, int C, int classes, float* __restrict__ logits) {
+  const int b = blockIdx.x;
+  for (int j = threadIdx.x; j < classes; j += blockDim.x) {
+    float s = 0.f;
+    for (int c = 0; c < C; ++c) s = fmaf(pooled[(int64_t)b * C + c], t_w[(int64_t)c * classes + j], s);
+    logits[(int64_t)b * classes + j] = s + t_b[j];
+  }
+}
+
+// Per sample: softmax-CE (max-shifted, network.cpp:207-217) in fp64, grad_logits /B,
+// and the pooled-feature cotangent gpool = grad_logits . t_w^T.
+__global__ void loss_grad_kernel(const float* __restrict__ logits, const int32_t* __restrict__ labels,
+                                 const float* __restrict__ t_w, int nrows, int C, int classes,
+                                 float* __restrict__ glog, double* __restrict__ loss_b, float* __restrict__ gpool) {
+  const int b = blockIdx.x;
+  const float* l = logits + (int64_t)b * classes;
+  __shared__ double s_lse;
+  __shared__ float s_g[1024];
+  if (threadIdx.x == 0) {
+    double m = l[0];
+    for (int c = 1; c < classes; ++c) m = fmax(m, (double)l[c]);
+    double z = 0.0;
+    for (int c = 0; c < classes; ++c) z += exp((double)l[c] - m);
+    const double lse = m + log(z);
+    const int y = labels[b];
+    loss_b[b] = (y >= 0 && y < classes) ? lse - (double)l[y] : __longlong_as_double(0x7ff8000000000000LL);
+    s_lse = lse;
+  }
+  __syncthreads();
+  const int y = labels[b];
+  for (int c = threadIdx.x; c < classes; c += blockDim.x) {
+    const double sm = exp((double)l[c] - s_lse);
+    const float g = (float)((sm - (c == y ? 1.0 : 0.0)) / (double)nrows);
+    glog[(int64_t)b * classes + c] = g;
+    s_g[c] = g;
+  }
+  __syncthreads();
+  for (int c = threadIdx.x; c < C; c += blockDim.x) {
+    float s = 0.f;
+    for (int j = 0; j < classes; ++j) s = fmaf(s_g[j], t_w[(int64_t)c * classes + j], s);
+    gpool[(int64_t)b * C + c] = s;
+  }
+}
+
+// gt_w[c][j] = sum_b pooled[b][c] glog[b][j]; gt_b[j] = sum_b glog[b][j]; loss = mean loss_b.
+__global__ void head_param_grad_kernel(const float* __restrict__ pooled, const float* __restrict__ glog,
+                                       const double* __restrict__ loss_b, int nrows, int C, int classes,
+                                       float* __restrict__ gt_w, float* __restrict__ gt_b, double* __restrict__ loss) {
+  const int total = C * classes + classes;
+  for (int idx = blockIdx.x * blockDim.x + threadIdx.x; idx < total; idx += gridDim.x * blockDim.x) {
+    if (idx < C * classes) {
+      const int c = idx / classes, j = idx % classes;
+      float s = 0.f;
+      for (int b = 0; b < nrows; ++b) s = fmaf(pooled[(int64_t)b * C + c], glog[(int64_t)b * classes + j], s);
+      gt_w[idx] = s;
+    } else {
+      const int j = idx - C * classes;
+      float s = 0.f;
+      for (int b = 0; b < nrows; ++b) s += glog[(int64_t)b * classes + j];
+      gt_b[j] = s;
+    }
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0 && loss) {
+    double s = 0.0;
+    for (int b = 0; b < nrows; ++b) s += loss_b[b];
+    *loss = s / (double)nrows;
+  }
+}
+
+// g[b][p][c] = gpool[b][c] / hw  (d mean / d x)
+__global__ void broadcast_kernel(const float* __restrict__ gpool, int64_t hw, int C, int64_t total,
+                                 float inv_hw, float* __restrict__ g) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+    const int c = (int)(i % C);
+    const int64_t b = i / ((int64_t)C * hw);
+    g[i] = gpool[b * C + c] * inv_hw;
+  }
+}
+
+__global__ void broadcast_kernel_vec4(const float* __restrict__ gpool, int64_t hw, int C, int64_t total4,
+                                      float inv_hw, float4* __restrict__ g) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total4;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t e = i * 4;
+    const int c = (int)(e % C);
+    const int64_t b = e / ((int64_t)C * hw);
+    const float* gp = gpool + b * C + c;
+    g[i] = make_float4(gp[0] * inv_hw, gp[1] * inv_hw, gp[2] * inv_hw, gp[3] * inv_hw);
+  }
+}
+
+__global__ void argmax_hits_kernel(const float* __restrict__ logits, const int32_t* __restrict__ labels, int nrows,
+                                   int classes, unsigned long long* hits) {
+  for (int b = blockIdx.x * blockDim.x + threadIdx.x; b < nrows; b += gridDim.x * blockDim.x) {
+    const float* l = logits + (int64_t)b * classes;
+    int best = 0;
+    for (int c = 1; c < classes; ++c)
+      if (l[c] > l[best]) best = c;  // strict: ties -> lowest class (network.cpp:229)
+    if (best == labels[b]) atomicAdd(hits, 1ULL);  // integer: order-independent
+  }
+}
+
+int64_t align256(int64_t v) { return (v + 255) / 256 * 256; }
+
+}  // namespace
+
+int64_t head_ws_bytes(int nrows, int channels, int classes) {
+  return align256((int64_t)nrows * classes * 4) + align256((int64_t)nrows * 8) + align256((int64_t)nrows * channels * 4);
+}
+
+void head_forward(int nrows, int hw, int C, int classes, const float* x_end, const float* t_w, const float* t_b,
+                  float* pooled, float* logits, cudaStream_t st) {
+  if (nrows <= 0) return;
+  const int cw = C < 256 ? C : 256;
+  const int groups = C <= 256 ? (256 / C > 0 ? 256 / C : 1) : 1;
+  gap_kernel<<<nrows, 256, groups * cw * sizeof(float), st>>>(x_end, hw, C, pooled);
+  RP_LAUNCHED();
+  fc_kernel<<<nrows, 32, 0, st>>>(pooled, t_w, t_b, C, classes, logits);
+  RP_LAUNCHED();
+}
+
+void head_loss_backward(int nrows, int hw, int C, int classes, const float* pooled, const float* logits,
+                        const float* t_w, const int32_t* labels, double* loss_dev, float* gt_w, float* gt_b,
+                        float* g_out, void* ws, cudaStream_t st) {
+  if (nrows <= 0) return;
+  char* w = static_cast<char*>(ws);
+  float* glog = reinterpret_cast<float*>(w);
+  double* loss_b = reinterpret_cast<double*>(w + align256((int64_t)nrows * classes * 4));
+  float* gpool = reinterpret_cast<float*>(w + align256((int64_t)nrows * classes * 4) + align256((int64_t)nrows * 8));
+  loss_grad_kernel<<<nrows, 128, 0, st>>>(logits, labels, t_w, nrows, C, classes, glog, loss_b, gpool);
+  RP_LAUNCHED();
+  const int total = C * classes + classes;
+  head_param_grad_kernel<<<ceil_div(total, 128), 128, 0, st>>>(pooled, glog, loss_b, nrows, C, classes, gt_w, gt_b,
+                                                               loss_dev);
+  RP_LAUNCHED();
+  const int64_t n = (int64_t)nrows * hw * C;
+  const float inv = 1.f / (float)hw;
+  const int grid = (int)std::min<int64_t>((n / 4 + 255) / 256 + 1, 16 * kNumSMs);
+  if (C % 4 == 0 && (reinterpret_cast<uintptr_t>(g_out) & 15u) == 0)
+    broadcast_kernel_vec4<<<grid, 256, 0, st>>>(gpool, hw, C, n / 4, inv, reinterpret_cast<float4*>(g_out));
+  else
+    broadcast_kernel<<<grid, 256, 0, st>>>(gpool, hw, C, n, inv, g_out);
+  RP_LAUNCHED();
+}
+
+void argmax_hits(const float* logits, const int32_t* labels, int nrows, int classes, unsigned long long* hits_dev,
+                 cudaStream_t st) {
+  RP_CUDA(cudaMemsetAsync(hits_dev, 0, sizeof(unsigned long long), st));
+  if (nrows <= 0) return;
+  argmax_hits_kernel<<<ceil_div(nrows, 128), 128, 0, st>>>(logits, labels, nrows, classes, hits_dev);
+  RP_LAUNCHED();
+}
+
+}  // namespace rp::k

@@ -1,0 +1,63 @@
+// Internal launch API of the sm_100a kernels (namespace rp::k).  The C ABI
+// (capi.cpp) and the C++ host classes (host/) call these.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+namespace rp::k {
+
+// ---- elementwise / reductions (elementwise.cu) -----------------------------
+int64_t reduce_workspace_bytes();
+void fill_uniform(float* dst, int64_t n, uint64_t state, double lo, double hi, double scale, cudaStream_t s);
+void fill_normal(float* dst, int64_t n, uint64_t state, double mean, double sigma, bool accumulate,
+                 cudaStream_t s);
+void psi_device(int kind, const float* a, const float* b, int64_t n, void* ws, double* out_dev, cudaStream_t s);
+void psi_grad(int kind, const float* lam, const float* x, int64_t n, double scale, float* out, void* ws,
+              cudaStream_t s);
+void synthetic_grad(int kind, const float* lam_next, const float* x_end, const float* kappa, int64_t n, double w,
+                    float* g, void* ws, cudaStream_t s);
+void correct(int kind, float* lam, const float* x_prev, const float* p, float* kappa, int64_t n, double w,
+             double eta, bool update_lambda, double kappa_coef, bool update_kappa, void* ws, cudaStream_t s);
+void sgd(float* w, const float* g, float* v, int64_t n, double lr, double momentum, cudaStream_t s);
+
+// ---- 3x3 convolutions (conv_simt.cu, conv_tc.cu) ----------------------------
+// Epilogues fused into the implicit-GEMM store (network.cpp:82-106):
+enum Epilogue : int {
+  EPI_BIAS = 0,      // out = acc + bias                           (stem, identity conv1)
+  EPI_BIAS_TANH = 1, // out = tanh(acc + bias)                     (conv1: a)
+  EPI_RESID = 2,     // out = aux + h (acc + bias)                 (conv2: x' = x + h f)
+  EPI_TANH_BWD = 3,  // out = h acc (1 - aux^2)                    (dgrad2 -> dpre, aux = a)
+  EPI_ADD = 4,       // out = aux + acc   (in place allowed)       (dgrad1: g_prev = g + ...)
+  EPI_SCALE = 5      // out = h acc                                (identity dgrad2)
+};
+
+struct ConvShape {
+  int n, h, w;  // batch and spatial
+  int ci, co;   // channels
+  int64_t pixels() const { return (int64_t)n * h * w; }
+};
+
+// out = epilogue(conv3x3(in, w_hwio)) with zero padding 1, stride 1.  NHWC fp32.
+void conv3x3_fwd_simt(const ConvShape& s, const float* in, const float* w_hwio, const float* bias,
+                      const float* aux, float h, int epi, float* out, cudaStream_t st);
+// dgrad weight relayout: wd[ky][kx][co][ci] = w[2-ky][2-kx][ci][co]
+void conv3x3_dgrad_weights(const float* w_hwio, int ci, int co, float* wd, cudaStream_t st);
+// gw[tap][ci][co] = scale * sum_pix in(pix+tap)[ci] g(pix)[co], gb[co] = scale * sum_pix g(pix)[co]
+// (deterministic split-K over pixels; ws >= conv3x3_wgrad_ws_bytes).
+int64_t conv3x3_wgrad_ws_bytes(const ConvShape& s);
+void conv3x3_wgrad_simt(const ConvShape& s, const float* in, const float* g, float scale, float* gw, float* gb,
+                        void* ws, cudaStream_t st);
+
+// ---- head (head.cu) -------------------------------------------------------
+int64_t head_ws_bytes(int nrows, int channels, int classes);
+void head_forward(int nrows, int hw, int channels, int classes, const float* x_end, const float* t_w,
+                  const float* t_b, float* pooled, float* logits, cudaStream_t st);
+void head_loss_backward(int nrows, int hw, int channels, int classes, const float* pooled, const float* logits,
+                        const float* t_w, const int32_t* labels, double* loss_dev, float* gt_w, float* gt_b,
+                        float* g_out, void* ws, cudaStream_t st);
+void argmax_hits(const float* logits, const int32_t* labels, int nrows, int classes, unsigned long long* hits_dev,
+                 cudaStream_t st);
+
+}  // namespace rp::k
