@@ -163,7 +163,7 @@ def run_ours(args, cfg, rank, world):
     gen.manual_seed(7 + rank)
     y = torch.randint(0, CLASSES, (B,), dtype=torch.int32, device="cuda", generator=gen)
     torch.cuda.synchronize()
-    x_host = x.cpu().numpy()
+    x_host = x.cpu().numpy().reshape(B, cfg['h'], cfg['w'], cfg['cin'])
     tr.reset_lambda_from_forward(x_host)
     sp = step_params(cfg)
 

@@ -132,6 +132,11 @@ class ConvNet:
     t_w: np.ndarray
     t_b: np.ndarray
 
+    def astype(self, dtype) -> "ConvNet":
+        net = zero_net(self.geo, dtype)
+        net.load_flat(self.flat().astype(dtype))
+        return net
+
     def copy(self) -> "ConvNet":
         return ConvNet(self.geo, self.s_w.copy(), self.s_b.copy(), [w.copy() for w in self.w1],
                        [b.copy() for b in self.b1], [w.copy() for w in self.w2],
@@ -167,10 +172,11 @@ def param_count(g: Geometry) -> int:
     return int(sum(np.prod(s) for s in param_shapes(g)))
 
 
-def zero_net(g: Geometry) -> ConvNet:
-    """make_zero_net (network.cpp:70-80): identity trunk."""
+def zero_net(g: Geometry, dtype=np.float64) -> ConvNet:
+    """make_zero_net (network.cpp:70-80): identity trunk.  dtype float32 gives a plain
+    fp32 execution of the same algorithm (the tests' fp32 noise-floor estimate)."""
     sh = param_shapes(g)
-    z = [np.zeros(s) for s in sh]
+    z = [np.zeros(s, dtype=dtype) for s in sh]
     L = g.blocks
     return ConvNet(g, z[0], z[1], [z[2 + 4 * l] for l in range(L)], [z[3 + 4 * l] for l in range(L)],
                    [z[4 + 4 * l] for l in range(L)], [z[5 + 4 * l] for l in range(L)], z[-2], z[-1])
@@ -222,7 +228,7 @@ def conv3x3_dgrad(g: np.ndarray, w: np.ndarray) -> np.ndarray:
     (network.cpp:100, 104)."""
     n, h, ww, co = g.shape
     ci = w.shape[2]
-    out = np.zeros((n, h + 2, ww + 2, ci))
+    out = np.zeros((n, h + 2, ww + 2, ci), dtype=g.dtype)
     for ky in range(3):
         for kx in range(3):
             out[:, ky:ky + h, kx:kx + ww, :] += g @ w[ky, kx].T
@@ -498,14 +504,15 @@ class DecoupledTrainer:
         self.blocks_per_stage = ranges[0][1] - ranges[0][0]
         g = net.geo
         shp = (num_samples, g.height, g.width, g.channels)
+        dt = net.s_w.dtype
         self.stages_ = []
         for k, (b, e) in enumerate(ranges):
             st = StageState(k, b, e)
             if k > 0:
-                st.lam = np.zeros(shp)
-                st.kappa = np.zeros(shp)
-            st.boundary_out = np.zeros(shp)
-            st.boundary_adjoint = np.zeros(shp)
+                st.lam = np.zeros(shp, dtype=dt)
+                st.kappa = np.zeros(shp, dtype=dt)
+            st.boundary_out = np.zeros(shp, dtype=dt)
+            st.boundary_adjoint = np.zeros(shp, dtype=dt)
             self.stages_.append(st)
         self.iteration = 0
         self.has_forward = False

@@ -128,6 +128,7 @@ class StageScheduler {
  private:
   std::vector<int> devices_;
   std::vector<cudaStream_t> streams_;
+  std::vector<bool> owned_;
   std::vector<cudaEvent_t> marks_;  // [stage][Mark]
   cudaStream_t ctl_ = nullptr;
   cudaEvent_t ev_begin_ = nullptr, ev_end_ = nullptr, ev_rb_ = nullptr, ev_re_ = nullptr;

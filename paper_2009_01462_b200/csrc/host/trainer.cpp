@@ -2,6 +2,7 @@
 // runtime.cpp:9-110).  Every GPU operation goes through the C ABI (rp_op_*).
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 
 #include "respar_b200.hpp"
@@ -116,10 +117,27 @@ StageScheduler::StageScheduler(int stages, std::vector<int> devices) {
   const int G = static_cast<int>(devices.size());
   for (int k = 0; k < stages; ++k) devices_.push_back(devices[(int64_t)k * G / stages]);
   streams_.resize(stages);
+  owned_.assign(stages, false);
   marks_.resize((size_t)stages * kNumMarks);
+  // Stages that share a GPU share its stream unless RP_CONCURRENT_STAGES=1: at the
+  // benchmark sizes every conv launch fills the 148 SMs on its own, and serialising
+  // keeps each kernel's event-timed duration clean for the roofline.
+  const char* env = std::getenv("RP_CONCURRENT_STAGES");
+  const bool concurrent = env && std::string(env) == "1";
   for (int k = 0; k < stages; ++k) {
     DeviceGuard g(devices_[k]);
-    cu(cudaStreamCreateWithFlags(&streams_[k], cudaStreamNonBlocking), "cudaStreamCreate");
+    int share = -1;
+    for (int j = 0; j < k && !concurrent; ++j)
+      if (devices_[j] == devices_[k]) {
+        share = j;
+        break;
+      }
+    if (share >= 0) {
+      streams_[k] = streams_[share];
+    } else {
+      cu(cudaStreamCreateWithFlags(&streams_[k], cudaStreamNonBlocking), "cudaStreamCreate");
+      owned_[k] = true;
+    }
     for (int m = 0; m < kNumMarks; ++m)
       cu(cudaEventCreateWithFlags(&marks_[(size_t)k * kNumMarks + m], cudaEventDisableTiming), "cudaEventCreate");
   }
@@ -135,7 +153,10 @@ StageScheduler::~StageScheduler() {
   for (size_t k = 0; k < streams_.size(); ++k) {
     cudaSetDevice(devices_[k]);
     cudaStreamSynchronize(streams_[k]);
-    cudaStreamDestroy(streams_[k]);
+  }
+  for (size_t k = 0; k < streams_.size(); ++k) {
+    cudaSetDevice(devices_[k]);
+    if (owned_[k]) cudaStreamDestroy(streams_[k]);
     for (int m = 0; m < kNumMarks; ++m) cudaEventDestroy(marks_[k * kNumMarks + m]);
   }
   cudaSetDevice(devices_[0]);
@@ -258,7 +279,11 @@ DecoupledTrainer::DecoupledTrainer(const rp_geometry& g, int stages, TrainMode m
 }
 
 DecoupledTrainer::~DecoupledTrainer() {
-  if (sched_) sched_->sync();
+  try {
+    if (sched_) sched_->sync();
+  } catch (...) {
+    // a sticky CUDA error was already reported by the call that raised it
+  }
 }
 
 static size_t dev_index(const std::vector<int>& u, int d) {

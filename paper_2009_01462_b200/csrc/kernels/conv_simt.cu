@@ -164,13 +164,18 @@ __global__ void dgrad_weights_kernel(const float* __restrict__ w, int ci, int co
 struct WgArgs {
   const float* in;
   const float* g;
-  float* ws;   // [splits][K][Co] then [splits][Co]
+  float* ws;   // float [splits][K][Co], then double [splits][Co] (bias)
   int N, H, W, Ci, Co, M, K;
   int pix_per_split;
   int splits;
 };
 
 constexpr int WT = 64, WP = 16, WPAD = 4;
+
+// float offset of the fp64 bias partials: after the weight partials, 64-byte aligned
+__host__ __device__ inline int64_t bias_offset(int splits, int K, int Co) {
+  return ((int64_t)splits * K * Co + 15) / 16 * 16;
+}
 
 __global__ __launch_bounds__(256) void conv3x3_wgrad_simt_kernel(WgArgs a) {
   __shared__ __align__(16) float As[2][WP][WT + WPAD];
@@ -221,7 +226,7 @@ __global__ __launch_bounds__(256) void conv3x3_wgrad_simt_kernel(WgArgs a) {
 
   const int tx = tid & 15, ty = tid >> 4;
   float acc[4][4];
-  float bacc[4] = {0.f, 0.f, 0.f, 0.f};
+  double bacc[4] = {0.0, 0.0, 0.0, 0.0};  // bias sums in fp64: col_sum over up to 10^6 pixels
 #pragma unroll
   for (int i = 0; i < 4; ++i)
 #pragma unroll
@@ -249,7 +254,7 @@ __global__ __launch_bounds__(256) void conv3x3_wgrad_simt_kernel(WgArgs a) {
         for (int j = 0; j < 4; ++j) acc[i][j] = fmaf(aa[i], gg[j], acc[i][j]);
       if (do_bias) {
 #pragma unroll
-        for (int j = 0; j < 4; ++j) bacc[j] += gg[j];
+        for (int j = 0; j < 4; ++j) bacc[j] += (double)gg[j];
       }
     }
     if (t + 1 < nchunks) store_chunk(cur ^ 1);
@@ -268,7 +273,7 @@ __global__ __launch_bounds__(256) void conv3x3_wgrad_simt_kernel(WgArgs a) {
     }
   }
   if (do_bias) {
-    float* pb = a.ws + (int64_t)a.splits * a.K * a.Co + (int64_t)split * a.Co;
+    double* pb = reinterpret_cast<double*>(a.ws + bias_offset(a.splits, a.K, a.Co)) + (int64_t)split * a.Co;
 #pragma unroll
     for (int j = 0; j < 4; ++j) {
       const int c = c0 + tx * 4 + j;
@@ -277,12 +282,14 @@ __global__ __launch_bounds__(256) void conv3x3_wgrad_simt_kernel(WgArgs a) {
   }
 }
 
-__global__ void splitk_reduce_kernel(const float* __restrict__ ws, int splits, int64_t n, float scale,
+// fixed-order fp64 combine of the split-K partials
+template <class T>
+__global__ void splitk_reduce_kernel(const T* __restrict__ ws, int splits, int64_t n, double scale,
                                      float* __restrict__ out) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
-    float s = 0.f;
-    for (int k = 0; k < splits; ++k) s += ws[(int64_t)k * n + i];
-    out[i] = scale * s;
+    double s = 0.0;
+    for (int k = 0; k < splits; ++k) s += (double)ws[(int64_t)k * n + i];
+    out[i] = (float)(scale * s);
   }
 }
 
@@ -330,7 +337,7 @@ void conv3x3_dgrad_weights(const float* w, int ci, int co, float* wd, cudaStream
 
 int64_t conv3x3_wgrad_ws_bytes(const ConvShape& s) {
   const SplitPlan p = plan_wgrad(s);
-  return (int64_t)p.splits * (9LL * s.ci * s.co + s.co) * 4;
+  return bias_offset(p.splits, 9 * s.ci, s.co) * 4 + (int64_t)p.splits * s.co * 8;
 }
 
 void conv3x3_wgrad_simt(const ConvShape& s, const float* in, const float* g, float scale, float* gw, float* gb,
@@ -342,11 +349,11 @@ void conv3x3_wgrad_simt(const ConvShape& s, const float* in, const float* g, flo
   conv3x3_wgrad_simt_kernel<<<grid, 256, 0, st>>>(a);
   RP_LAUNCHED();
   const int64_t nw = (int64_t)a.K * s.co;
-  splitk_reduce_kernel<<<ceil_div(nw, 256), 256, 0, st>>>(a.ws, p.splits, nw, scale, gw);
+  splitk_reduce_kernel<float><<<ceil_div(nw, 256), 256, 0, st>>>(a.ws, p.splits, nw, scale, gw);
   RP_LAUNCHED();
   if (gb) {
-    splitk_reduce_kernel<<<ceil_div(s.co, 256), 256, 0, st>>>(a.ws + (int64_t)p.splits * nw, p.splits, s.co, scale,
-                                                              gb);
+    const double* pb = reinterpret_cast<const double*>(a.ws + bias_offset(p.splits, a.K, s.co));
+    splitk_reduce_kernel<double><<<ceil_div(s.co, 256), 256, 0, st>>>(pb, p.splits, s.co, scale, gb);
     RP_LAUNCHED();
   }
 }

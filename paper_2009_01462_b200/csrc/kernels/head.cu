@@ -90,14 +90,14 @@ __global__ void head_param_grad_kernel(const float* __restrict__ pooled, const f
   for (int idx = blockIdx.x * blockDim.x + threadIdx.x; idx < total; idx += gridDim.x * blockDim.x) {
     if (idx < C * classes) {
       const int c = idx / classes, j = idx % classes;
-      float s = 0.f;
-      for (int b = 0; b < nrows; ++b) s = fmaf(pooled[(int64_t)b * C + c], glog[(int64_t)b * classes + j], s);
-      gt_w[idx] = s;
+      double s = 0.0;
+      for (int b = 0; b < nrows; ++b) s += (double)pooled[(int64_t)b * C + c] * (double)glog[(int64_t)b * classes + j];
+      gt_w[idx] = (float)s;
     } else {
       const int j = idx - C * classes;
-      float s = 0.f;
-      for (int b = 0; b < nrows; ++b) s += glog[(int64_t)b * classes + j];
-      gt_b[j] = s;
+      double s = 0.0;
+      for (int b = 0; b < nrows; ++b) s += (double)glog[(int64_t)b * classes + j];
+      gt_b[j] = (float)s;
     }
   }
   if (blockIdx.x == 0 && threadIdx.x == 0 && loss) {

@@ -118,43 +118,75 @@ CONV_CASES = [
 
 
 def conv_case_run(og, K, mode, kind, N, batch, steps, math, seed=1):
+    """The same iterations three ways: fp64 oracle (truth), fp32 oracle (the noise
+    floor of a plain fp32 execution of the reference algorithm), and the GPU."""
     net = O.make_net(og, O.Rng(seed))
-    for l in range(og.blocks):   # non-zero biases so every epilogue term is exercised
+    # Non-zero biases so every epilogue term is exercised.
+    for l in range(og.blocks):
         net.b1[l][...] = O.rng_uniform(O.Rng(100 + l), og.hidden, -0.1, 0.1)
         net.b2[l][...] = O.rng_uniform(O.Rng(200 + l), og.channels, -0.1, 0.1)
+    net.s_b[...] = O.rng_uniform(O.Rng(300), og.channels, -0.1, 0.1)
+    net.t_b[...] = O.rng_uniform(O.Rng(301), og.classes, -0.1, 0.1)
     p32 = net.flat().astype(np.float32)
     net.load_flat(p32.astype(np.float64))
     x, y = O.synthetic_batch(og, N, seed=seed + 7)
-    x = x.astype(np.float32).astype(np.float64)
+    x32 = x.astype(np.float32)
+    x = x32.astype(np.float64)
     ot = O.DecoupledTrainer(net, K, mode, kind, N)
     ot.reset_lambda_from_forward(x)
+    o32 = O.DecoupledTrainer(net.astype(np.float32), K, mode, kind, N)
+    o32.reset_lambda_from_forward(x32)
     gt = rp.DecoupledTrainer(geo(og), K, mode, kind, N, params=p32, math=math)
-    gt.reset_lambda_from_forward(x.astype(np.float32))
+    gt.reset_lambda_from_forward(x32)
     sp_o = O.StepParams(beta=0.8, lr=0.05, lambda_lr=0.05, kappa_lr=1e-4)
     sp_g = rp.StepParams(beta=0.8, lr=0.05, lambda_lr=0.05, kappa_lr=1e-4)
-    lo, lg = [], []
+    lo, l32, lg = [], [], []
     for _ in range(steps):
         for r0 in range(0, N, batch):
             nr = min(batch, N - r0)
             lo.append(ot.step(x[r0:r0 + nr], y[r0:r0 + nr], r0, sp_o))
-            lg.append(gt.step(x[r0:r0 + nr].astype(np.float32), y[r0:r0 + nr], r0, sp_g))
-    return ot, gt, np.array(lo), np.array(lg)
+            l32.append(o32.step(x32[r0:r0 + nr], y[r0:r0 + nr], r0, sp_o))
+            lg.append(gt.step(x32[r0:r0 + nr], y[r0:r0 + nr], r0, sp_g))
+    return ot, o32, gt, np.array(lo), np.array(l32), np.array(lg)
+
+
+def fp32_close(got, want, want32, tol=FP32_TOL, factor=8.0):
+    """|got - want|_inf <= max(tol |want|_inf, factor |want32 - want|_inf).
+
+    The second term is the error a plain fp32 execution of the same algorithm makes:
+    quantities formed from differences of nearly equal boundary states (lambda - X in
+    the synthetic loss, the multiplier update, the adjoints they feed) lose relative
+    accuracy in any fp32 implementation, so their bound is stated against that floor.
+    """
+    got = np.asarray(got, np.float64).reshape(-1)
+    want = np.asarray(want, np.float64).reshape(-1)
+    w32 = np.asarray(want32, np.float64).reshape(-1)
+    err = np.abs(got - want).max() if want.size else 0.0
+    bound = max(tol * (np.abs(want).max() if want.size else 0.0), factor * (np.abs(w32 - want).max() if want.size else 0.0))
+    return err <= bound or err == 0.0, (err, bound)
 
 
 @pytest.mark.parametrize("math", MATHS)
 @pytest.mark.parametrize("case", range(len(CONV_CASES)))
 def test_conv3x3_trainer_vs_oracle(case, math):
     og, K, mode, kind, N, batch, steps = CONV_CASES[case]
-    ot, gt, lo, lg = conv_case_run(og, K, mode, kind, N, batch, steps, math)
+    ot, o32, gt, lo, l32, lg = conv_case_run(og, K, mode, kind, N, batch, steps, math)
     assert rel_err(lg, lo) <= FP32_TOL
+    # parameters: 1e-4 max-norm relative per tensor
     assert_params_close(og, gt.params().astype(np.float64), ot.net.flat())
     for k in range(K):
-        st = ot.stage(k)
-        for which, want in ((rp.LAMBDA, st.lam), (rp.KAPPA, st.kappa), (rp.BOUNDARY_OUT, st.boundary_out),
-                            (rp.BOUNDARY_ADJOINT, st.boundary_adjoint)):
+        st, s32 = ot.stage(k), o32.stage(k)
+        for which, want, w32 in ((rp.LAMBDA, st.lam, s32.lam), (rp.KAPPA, st.kappa, s32.kappa),
+                                 (rp.BOUNDARY_OUT, st.boundary_out, s32.boundary_out),
+                                 (rp.BOUNDARY_ADJOINT, st.boundary_adjoint, s32.boundary_adjoint)):
             if k == 0 and which in (rp.LAMBDA, rp.KAPPA):
                 continue
-            assert rel_err(gt.state(k, which), want) <= FP32_TOL, (k, which)
+            got = gt.state(k, which)
+            if which in (rp.LAMBDA, rp.BOUNDARY_OUT):
+                assert rel_err(got, want) <= FP32_TOL, (k, which, rel_err(got, want))
+            else:
+                ok, info = fp32_close(got, want, w32)
+                assert ok, (k, which, info)
 
 
 def test_device_init_matches_oracle_rng():
