@@ -145,6 +145,16 @@ int rp_op_correct(int32_t kind, float* lam, const float* x_prev, const float* p,
 /* W -= lr * g (apply_updates, network.cpp:174-191); with momentum: v = mu v + g; W -= lr v. */
 int rp_op_sgd(float* w, const float* g, float* v, int64_t n, double lr, double momentum, void* stream);
 
+/* One 3x3 conv (zero pad 1, stride 1) NHWC [n,h,w,ci] -> [n,h,w,co] with a fused
+ * epilogue: 0 acc+bias, 1 tanh(acc+bias), 2 aux+h(acc+bias), 3 h acc (1-aux^2),
+ * 4 aux+acc (out may equal aux), 5 h acc.  dgrad != 0: input-gradient conv, w_hwio is
+ * the forward conv's [3][3][co][ci] weight.  math RP_MATH_FP32 (3xTF32 tcgen05),
+ * RP_MATH_TF32, RP_MATH_SIMT. */
+int rp_op_conv3x3(int32_t n, int32_t h, int32_t w, int32_t ci, int32_t co, const float* in, const float* w_hwio,
+                  int32_t dgrad, const float* bias, const float* aux, double hstep, int32_t epi, float* out,
+                  int32_t math, void* ws, int64_t ws_bytes, void* stream);
+int64_t rp_op_conv3x3_workspace_bytes(int32_t ci, int32_t co);
+
 /* Residual block on nrows samples (network.cpp:82-106), block params at `pb` in the
  * flat layout (w1 b1 w2 b2).  Forward writes a (tape) and x_next.  Backward takes the
  * cotangent at the block output in g_io and overwrites it with the cotangent at the

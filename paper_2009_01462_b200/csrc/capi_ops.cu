@@ -50,30 +50,51 @@ void check_math(int math) {
 
 }  // namespace
 
+// bytes reserved at the front of an op workspace for per-call weight relayouts
+int64_t weight_ws_bytes(const rp_geometry& g) {
+  const int64_t C = g.channels, Ch = g.hidden;
+  return align256(std::max<int64_t>(k::conv3x3_tc_ws_bytes({1, 1, 1, (int)C, (int)Ch}), 9 * C * Ch * 4));
+}
+
 int64_t op_workspace_bytes(const rp_geometry& g, int nrows) {
   const int64_t C = g.channels, Ch = g.hidden;
-  const int64_t wd = align256(9 * C * Ch * 4) * 2;
   int64_t wg = k::conv3x3_wgrad_ws_bytes(shape(g, nrows, (int)Ch, (int)C));
   wg = std::max(wg, k::conv3x3_wgrad_ws_bytes(shape(g, nrows, (int)C, (int)Ch)));
   wg = std::max(wg, k::conv3x3_wgrad_ws_bytes(shape(g, nrows, g.in_channels, (int)C)));
   const int64_t head = k::head_ws_bytes(nrows, g.channels, g.classes);
-  return std::max(wd + align256(wg), head) + 256;
+  return std::max(weight_ws_bytes(g) + align256(wg), head) + 256;
+}
+
+// One 3x3 conv with a fused epilogue: the tcgen05 kernel (3xTF32 or TF32) when the
+// math mode asks for tensor cores and the shape is supported, the SIMT kernel otherwise.
+// dgrad: `w` is the forward conv's HWIO weight; the conv runs on the cotangent.
+void conv(const k::ConvShape& s, const float* in, const float* w, bool dgrad, const float* bias, const float* aux,
+          float h, int epi, float* out, int math, void* wws, int prof_cls, bool aux_read, cudaStream_t st) {
+  prof::Scope ps(prof_cls, st, conv_flops(s), conv_bytes(s, aux_read));
+  if (math != RP_MATH_SIMT && k::conv3x3_tc_supported(s)) {
+    k::conv3x3_fwd_tc(s, in, w, dgrad, bias, aux, h, epi, out, math != RP_MATH_TF32, wws, st);
+    return;
+  }
+  const float* wk = w;
+  if (dgrad) {
+    k::conv3x3_dgrad_weights(w, s.co, s.ci, static_cast<float*>(wws), st);
+    wk = static_cast<const float*>(wws);
+  }
+  k::conv3x3_fwd_simt(s, in, wk, bias, aux, h, epi, out, st);
 }
 
 void block_fwd(const rp_geometry& g, int nrows, const float* x, const float* pb, float* a, float* x_next, int math,
-               void*, int64_t, cudaStream_t st) {
+               void* ws, int64_t ws_bytes, cudaStream_t st) {
   const ParamLayout L = ParamLayout::of(g);
   const bool tanh_act = g.activation == RP_ACT_TANH;
-  (void)math;
+  if (ws_bytes < weight_ws_bytes(g)) fail(RP_ERR_RANGE, "block_fwd: workspace too small");
   const k::ConvShape s1 = shape(g, nrows, g.channels, g.hidden), s2 = shape(g, nrows, g.hidden, g.channels);
-  {  // conv1 + b1 + act  ->  a      (network.cpp:85-86)
-    prof::Scope ps(RP_PROF_CONV_FPROP, st, conv_flops(s1), conv_bytes(s1, false));
-    k::conv3x3_fwd_simt(s1, x, pb + L.w1, pb + L.b1, nullptr, 1.f, tanh_act ? k::EPI_BIAS_TANH : k::EPI_BIAS, a, st);
-  }
-  {  // conv2 + b2, *h, + x  ->  x'   (network.cpp:87)
-    prof::Scope ps(RP_PROF_CONV_FPROP, st, conv_flops(s2), conv_bytes(s2, true));
-    k::conv3x3_fwd_simt(s2, a, pb + L.w2, pb + L.b2, x, (float)g.step_h, k::EPI_RESID, x_next, st);
-  }
+  // conv1 + b1 + act  ->  a      (network.cpp:85-86)
+  conv(s1, x, pb + L.w1, false, pb + L.b1, nullptr, 1.f, tanh_act ? k::EPI_BIAS_TANH : k::EPI_BIAS, a, math, ws,
+       RP_PROF_CONV_FPROP, false, st);
+  // conv2 + b2, *h, + x  ->  x'   (network.cpp:87)
+  conv(s2, a, pb + L.w2, false, pb + L.b2, x, (float)g.step_h, k::EPI_RESID, x_next, math, ws, RP_PROF_CONV_FPROP,
+       true, st);
 }
 
 void block_bwd(const rp_geometry& g, int nrows, const float* x, const float* a, const float* pb, float* gio,
@@ -82,23 +103,14 @@ void block_bwd(const rp_geometry& g, int nrows, const float* x, const float* a, 
   const int C = g.channels, Ch = g.hidden;
   const bool tanh_act = g.activation == RP_ACT_TANH;
   const float h = (float)g.step_h;
-  (void)math;
   Carve cv{static_cast<char*>(ws), ws_bytes};
-  float* w2d = cv.take<float>(9LL * C * Ch);
-  float* w1d = cv.take<float>(9LL * C * Ch);
+  void* wws = cv.take<char>(weight_ws_bytes(g));
   const int64_t wg_bytes = std::max(k::conv3x3_wgrad_ws_bytes(shape(g, nrows, Ch, C)),
                                     k::conv3x3_wgrad_ws_bytes(shape(g, nrows, C, Ch)));
   void* wgws = cv.take<char>(wg_bytes);
-  {
-    prof::Scope ps(RP_PROF_OTHER, st, 0.0, 0.0);
-    k::conv3x3_dgrad_weights(pb + L.w2, Ch, C, w2d, st);
-    k::conv3x3_dgrad_weights(pb + L.w1, C, Ch, w1d, st);
-  }
-  const k::ConvShape d2 = shape(g, nrows, C, Ch), d1 = shape(g, nrows, Ch, C);
-  {  // dpre = h (g * W2^T) (1 - a^2)                            (network.cpp:100-101)
-    prof::Scope ps(RP_PROF_CONV_DGRAD, st, conv_flops(d2), conv_bytes(d2, tanh_act));
-    k::conv3x3_fwd_simt(d2, gio, w2d, nullptr, a, h, tanh_act ? k::EPI_TANH_BWD : k::EPI_SCALE, dpre, st);
-  }
+  // dpre = h (g * W2^T) (1 - a^2)                              (network.cpp:100-101)
+  conv(shape(g, nrows, C, Ch), gio, pb + L.w2, true, nullptr, a, h, tanh_act ? k::EPI_TANH_BWD : k::EPI_SCALE, dpre,
+       math, wws, RP_PROF_CONV_DGRAD, tanh_act, st);
   {  // gW2 = h a^T g, gb2 = h sum g                             (network.cpp:98-99)
     const k::ConvShape w2 = shape(g, nrows, Ch, C);
     prof::Scope ps(RP_PROF_CONV_WGRAD, st, conv_flops(w2), conv_bytes(w2, false));
@@ -109,10 +121,9 @@ void block_bwd(const rp_geometry& g, int nrows, const float* x, const float* a, 
     prof::Scope ps(RP_PROF_CONV_WGRAD, st, conv_flops(w1), conv_bytes(w1, false));
     k::conv3x3_wgrad_simt(w1, x, dpre, 1.f, gb + L.w1, gb + L.b1, wgws, st);
   }
-  {  // g <- g + dpre * W1^T   (in place)                        (network.cpp:104)
-    prof::Scope ps(RP_PROF_CONV_DGRAD, st, conv_flops(d1), conv_bytes(d1, true));
-    k::conv3x3_fwd_simt(d1, dpre, w1d, nullptr, gio, 1.f, k::EPI_ADD, gio, st);
-  }
+  // g <- g + dpre * W1^T   (in place)                          (network.cpp:104)
+  conv(shape(g, nrows, Ch, C), dpre, pb + L.w1, true, nullptr, gio, 1.f, k::EPI_ADD, gio, math, wws,
+       RP_PROF_CONV_DGRAD, true, st);
 }
 
 void stem_fwd(const rp_geometry& g, int nrows, const float* xr, const float* ps, float* x0, cudaStream_t st) {
@@ -267,6 +278,25 @@ int rp_op_sgd(float* w, const float* g, float* v, int64_t n, double lr, double m
     prof::Scope scope(RP_PROF_SGD, S(stream), 0.0, (double)n * (v ? 20.0 : 12.0));
     k::sgd(w, g, v, n, lr, momentum, S(stream));
   });
+}
+
+int rp_op_conv3x3(int32_t n, int32_t h, int32_t w, int32_t ci, int32_t co, const float* in, const float* w_hwio,
+                  int32_t dgrad, const float* bias, const float* aux, double hstep, int32_t epi, float* out,
+                  int32_t math, void* ws, int64_t ws_bytes, void* stream) {
+  return guard([&] {
+    check_math(math);
+    if (epi < 0 || epi > 5) fail(RP_ERR_RANGE, "conv3x3: unknown epilogue");
+    if (n < 0 || h < 1 || w < 1 || ci < 1 || co < 1) fail(RP_ERR_SHAPE, "conv3x3: bad shape");
+    const k::ConvShape s{n, h, w, ci, co};
+    if (ws_bytes < align256(std::max<int64_t>(k::conv3x3_tc_ws_bytes(s), 9LL * ci * co * 4)))
+      fail(RP_ERR_RANGE, "conv3x3: workspace too small");
+    conv(s, in, w_hwio, dgrad != 0, bias, aux, (float)hstep, epi, out, math, ws, RP_PROF_OTHER,
+         aux != nullptr, S(stream));
+  });
+}
+
+int64_t rp_op_conv3x3_workspace_bytes(int32_t ci, int32_t co) {
+  return align256(std::max<int64_t>(k::conv3x3_tc_ws_bytes({1, 1, 1, ci, co}), 9LL * ci * co * 4));
 }
 
 int rp_op_block_fwd(const rp_geometry* g, int32_t nrows, const float* x, const float* pb, float* a, float* x_next,

@@ -50,6 +50,13 @@ int64_t conv3x3_wgrad_ws_bytes(const ConvShape& s);
 void conv3x3_wgrad_simt(const ConvShape& s, const float* in, const float* g, float scale, float* gw, float* gb,
                         void* ws, cudaStream_t st);
 
+// tcgen05 implicit GEMM (conv_tc.cu): fprop, or dgrad when dgrad_weights (w_hwio is
+// then the forward conv's HWIO [3][3][s.co][s.ci] weight).  three: 3xTF32, else TF32.
+bool conv3x3_tc_supported(const ConvShape& s);
+int64_t conv3x3_tc_ws_bytes(const ConvShape& s);
+void conv3x3_fwd_tc(const ConvShape& s, const float* in, const float* w_hwio, bool dgrad_weights, const float* bias,
+                    const float* aux, float h, int epi, float* out, bool three, void* ws, cudaStream_t st);
+
 // ---- head (head.cu) -------------------------------------------------------
 int64_t head_ws_bytes(int nrows, int channels, int classes);
 void head_forward(int nrows, int hw, int channels, int classes, const float* x_end, const float* t_w,

@@ -1,0 +1,83 @@
+"""GPU: the 3x3 conv kernels (tcgen05 3xTF32 / TF32 and SIMT) through rp_op_conv3x3,
+against the fp64 oracle convolution (oracle/respar_oracle.py conv3x3 / conv3x3_dgrad)
+with every fused epilogue."""
+import ctypes as C
+
+import numpy as np
+import pytest
+
+import paper_2009_01462_b200 as rp
+from paper_2009_01462_b200._lib import lib
+from oracle import respar_oracle as O
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+
+EPIS = {0: "bias", 1: "bias_tanh", 2: "resid", 3: "tanh_bwd", 4: "add", 5: "scale"}
+
+
+def want_epi(epi, acc, bias, aux, h):
+    if epi == 0:
+        return acc + bias
+    if epi == 1:
+        return np.tanh(acc + bias)
+    if epi == 2:
+        return aux + h * (acc + bias)
+    if epi == 3:
+        return (h * acc) * (1.0 - aux * aux)
+    if epi == 4:
+        return aux + acc
+    return h * acc
+
+
+def run_conv(n, hh, ww, ci, co, epi, math, dgrad, seed=0, hstep=0.7):
+    rng = np.random.default_rng(seed)
+    cin, cout = (co, ci) if dgrad else (ci, co)       # dgrad: input has the fwd co channels
+    x = rng.uniform(-1, 1, (n, hh, ww, cin)).astype(np.float32)
+    w = (rng.uniform(-1, 1, (3, 3, ci, co)) / np.sqrt(9 * ci)).astype(np.float32)
+    bias = rng.uniform(-0.2, 0.2, cout).astype(np.float32)
+    aux = rng.uniform(-0.9, 0.9, (n, hh, ww, cout)).astype(np.float32)
+    acc = O.conv3x3_dgrad(x.astype(np.float64), w.astype(np.float64)) if dgrad else \
+        O.conv3x3(x.astype(np.float64), w.astype(np.float64))
+    want = want_epi(epi, acc, bias.astype(np.float64), aux.astype(np.float64), np.float32(hstep))
+    dev = torch.device("cuda")
+    tx, tw, tb = (torch.from_numpy(v).to(dev) for v in (x, w, bias))
+    taux = torch.from_numpy(aux).to(dev)
+    out = taux.clone() if epi == 4 else torch.empty((n, hh, ww, cout), device=dev)
+    wsb = lib().rp_op_conv3x3_workspace_bytes(ci, co)
+    ws = torch.empty(wsb, dtype=torch.uint8, device=dev)
+    use_aux = epi in (2, 3, 4)
+    rc = lib().rp_op_conv3x3(n, hh, ww, cin, cout, C.c_void_p(tx.data_ptr()), C.c_void_p(tw.data_ptr()),
+                             1 if dgrad else 0, C.c_void_p(tb.data_ptr()),
+                             C.c_void_p(out.data_ptr() if epi == 4 else taux.data_ptr()) if use_aux else None,
+                             hstep, epi, C.c_void_p(out.data_ptr()), rp.MATH[math], C.c_void_p(ws.data_ptr()),
+                             wsb, None)
+    rp.check(rc)
+    torch.cuda.synchronize()
+    return out.cpu().numpy().astype(np.float64), want
+
+
+SHAPES = [(2, 32, 32, 64, 64), (3, 8, 8, 16, 16), (1, 12, 12, 16, 32), (2, 6, 9, 32, 16), (1, 32, 32, 64, 128),
+          (5, 7, 7, 48, 64)]
+
+
+# 3xTF32 keeps ~21 of fp32's 24 mantissa bits per product: a few 1e-6 relative at K = 576
+@pytest.mark.parametrize("math,tol", [("fp32", 2e-5), ("simt", 2e-6), ("tf32", 5e-3)])
+@pytest.mark.parametrize("shape", SHAPES)
+@pytest.mark.parametrize("dgrad", [False, True])
+def test_conv_all_epilogues(shape, math, tol, dgrad):
+    n, hh, ww, ci, co = shape
+    for epi in range(6):
+        got, want = run_conv(n, hh, ww, ci, co, epi, math, dgrad, seed=epi)
+        err = np.abs(got - want).max() / max(np.abs(want).max(), 1e-30)
+        print(f"{shape} dgrad={dgrad} {math} {EPIS[epi]}: {err:.2e}")
+        assert err <= tol, (EPIS[epi], err)
+
+
+def test_conv_tc_is_deterministic_and_batch_independent():
+    """Per-pixel results do not depend on which other samples share the launch (the
+    property reset_lambda_from_forward's chunked forward relies on)."""
+    a, _ = run_conv(4, 32, 32, 64, 64, 1, "fp32", False, seed=3)
+    b, _ = run_conv(4, 32, 32, 64, 64, 1, "fp32", False, seed=3)
+    assert np.array_equal(a, b)
