@@ -3,7 +3,7 @@
  *
  * This is the drop-in boundary.  The reference (respar,
  * /root/reference/proj) has no FFI of its own: its boundary is the C++ library API
- * in include/respar/*.hpp, consumed by train(), the CLI and the pybind11 module.
+ * in include/respar/ (*.hpp), consumed by train(), the CLI and the pybind11 module.
  * The B200 build keeps that C++ surface (paper_2009_01462_b200/csrc/host/respar_b200.hpp,
  * namespace respar::b200) and puts this C ABI under it and beside it:
  *
@@ -154,6 +154,11 @@ int rp_op_conv3x3(int32_t n, int32_t h, int32_t w, int32_t ci, int32_t co, const
                   int32_t dgrad, const float* bias, const float* aux, double hstep, int32_t epi, float* out,
                   int32_t math, void* ws, int64_t ws_bytes, void* stream);
 int64_t rp_op_conv3x3_workspace_bytes(int32_t ci, int32_t co);
+/* Weight gradient of that conv: gw[3][3][ci][co] = scale sum_p in[p+tap][ci] gout[p][co],
+ * gb[co] = scale sum_p gout[p][co] (gb may be NULL).  Deterministic. */
+int rp_op_conv3x3_wgrad(int32_t n, int32_t h, int32_t w, int32_t ci, int32_t co, const float* in, const float* gout,
+                        double scale, float* gw, float* gb, int32_t math, void* ws, int64_t ws_bytes, void* stream);
+int64_t rp_op_conv3x3_wgrad_workspace_bytes(int32_t n, int32_t h, int32_t w, int32_t ci, int32_t co);
 
 /* Residual block on nrows samples (network.cpp:82-106), block params at `pb` in the
  * flat layout (w1 b1 w2 b2).  Forward writes a (tape) and x_next.  Backward takes the

@@ -1,6 +1,7 @@
 // C ABI, op layer (include/respar_b200.h "rp_op_*"): stream-ordered kernels on
 // caller-owned device buffers.  The C++ host classes (host/trainer.cpp) reach the GPU
 // only through these entry points.
+#include <algorithm>
 #include <cstring>
 #include <string>
 
@@ -56,11 +57,28 @@ int64_t weight_ws_bytes(const rp_geometry& g) {
   return align256(std::max<int64_t>(k::conv3x3_tc_ws_bytes({1, 1, 1, (int)C, (int)Ch}), 9 * C * Ch * 4));
 }
 
+int64_t wgrad_ws_bytes(const k::ConvShape& s) {
+  return std::max({k::conv3x3_wgrad_ws_bytes(s), k::conv3x3_wgrad_tc_ws_bytes(s, true),
+                   k::conv3x3_wgrad_tc_ws_bytes(s, false)});
+}
+
+// Weight gradient (+ bias sums): tcgen05 when the math mode and shape allow, SIMT otherwise.
+void wgrad(const k::ConvShape& s, const float* in, const float* gout, float scale, float* gw, float* gb, int math,
+           void* ws, cudaStream_t st) {
+  prof::Scope ps(RP_PROF_CONV_WGRAD, st, conv_flops(s), conv_bytes(s, false));
+  const bool three = math != RP_MATH_TF32;
+  if (math != RP_MATH_SIMT && k::conv3x3_wgrad_tc_supported(s, three)) {
+    k::conv3x3_wgrad_tc(s, in, gout, scale, gw, gb, three, ws, st);
+    return;
+  }
+  k::conv3x3_wgrad_simt(s, in, gout, scale, gw, gb, ws, st);
+}
+
 int64_t op_workspace_bytes(const rp_geometry& g, int nrows) {
   const int64_t C = g.channels, Ch = g.hidden;
-  int64_t wg = k::conv3x3_wgrad_ws_bytes(shape(g, nrows, (int)Ch, (int)C));
-  wg = std::max(wg, k::conv3x3_wgrad_ws_bytes(shape(g, nrows, (int)C, (int)Ch)));
-  wg = std::max(wg, k::conv3x3_wgrad_ws_bytes(shape(g, nrows, g.in_channels, (int)C)));
+  int64_t wg = wgrad_ws_bytes(shape(g, nrows, (int)Ch, (int)C));
+  wg = std::max(wg, wgrad_ws_bytes(shape(g, nrows, (int)C, (int)Ch)));
+  wg = std::max(wg, wgrad_ws_bytes(shape(g, nrows, g.in_channels, (int)C)));
   const int64_t head = k::head_ws_bytes(nrows, g.channels, g.classes);
   return std::max(weight_ws_bytes(g) + align256(wg), head) + 256;
 }
@@ -105,22 +123,15 @@ void block_bwd(const rp_geometry& g, int nrows, const float* x, const float* a, 
   const float h = (float)g.step_h;
   Carve cv{static_cast<char*>(ws), ws_bytes};
   void* wws = cv.take<char>(weight_ws_bytes(g));
-  const int64_t wg_bytes = std::max(k::conv3x3_wgrad_ws_bytes(shape(g, nrows, Ch, C)),
-                                    k::conv3x3_wgrad_ws_bytes(shape(g, nrows, C, Ch)));
+  const int64_t wg_bytes = std::max(wgrad_ws_bytes(shape(g, nrows, Ch, C)), wgrad_ws_bytes(shape(g, nrows, C, Ch)));
   void* wgws = cv.take<char>(wg_bytes);
   // dpre = h (g * W2^T) (1 - a^2)                              (network.cpp:100-101)
   conv(shape(g, nrows, C, Ch), gio, pb + L.w2, true, nullptr, a, h, tanh_act ? k::EPI_TANH_BWD : k::EPI_SCALE, dpre,
        math, wws, RP_PROF_CONV_DGRAD, tanh_act, st);
-  {  // gW2 = h a^T g, gb2 = h sum g                             (network.cpp:98-99)
-    const k::ConvShape w2 = shape(g, nrows, Ch, C);
-    prof::Scope ps(RP_PROF_CONV_WGRAD, st, conv_flops(w2), conv_bytes(w2, false));
-    k::conv3x3_wgrad_simt(w2, a, gio, h, gb + L.w2, gb + L.b2, wgws, st);
-  }
-  {  // gW1 = x^T dpre, gb1 = sum dpre                           (network.cpp:102-103)
-    const k::ConvShape w1 = shape(g, nrows, C, Ch);
-    prof::Scope ps(RP_PROF_CONV_WGRAD, st, conv_flops(w1), conv_bytes(w1, false));
-    k::conv3x3_wgrad_simt(w1, x, dpre, 1.f, gb + L.w1, gb + L.b1, wgws, st);
-  }
+  // gW2 = h a^T g, gb2 = h sum g                               (network.cpp:98-99)
+  wgrad(shape(g, nrows, Ch, C), a, gio, h, gb + L.w2, gb + L.b2, math, wgws, st);
+  // gW1 = x^T dpre, gb1 = sum dpre                             (network.cpp:102-103)
+  wgrad(shape(g, nrows, C, Ch), x, dpre, 1.f, gb + L.w1, gb + L.b1, math, wgws, st);
   // g <- g + dpre * W1^T   (in place)                          (network.cpp:104)
   conv(shape(g, nrows, Ch, C), dpre, pb + L.w1, true, nullptr, gio, 1.f, k::EPI_ADD, gio, math, wws,
        RP_PROF_CONV_DGRAD, true, st);
@@ -293,6 +304,21 @@ int rp_op_conv3x3(int32_t n, int32_t h, int32_t w, int32_t ci, int32_t co, const
     conv(s, in, w_hwio, dgrad != 0, bias, aux, (float)hstep, epi, out, math, ws, RP_PROF_OTHER,
          aux != nullptr, S(stream));
   });
+}
+
+int rp_op_conv3x3_wgrad(int32_t n, int32_t h, int32_t w, int32_t ci, int32_t co, const float* in, const float* gout,
+                        double scale, float* gw, float* gb, int32_t math, void* ws, int64_t ws_bytes, void* stream) {
+  return guard([&] {
+    check_math(math);
+    if (n < 1 || h < 1 || w < 1 || ci < 1 || co < 1) fail(RP_ERR_SHAPE, "conv3x3_wgrad: bad shape");
+    const k::ConvShape s{n, h, w, ci, co};
+    if (ws_bytes < wgrad_ws_bytes(s)) fail(RP_ERR_RANGE, "conv3x3_wgrad: workspace too small");
+    wgrad(s, in, gout, (float)scale, gw, gb, math, ws, S(stream));
+  });
+}
+
+int64_t rp_op_conv3x3_wgrad_workspace_bytes(int32_t n, int32_t h, int32_t w, int32_t ci, int32_t co) {
+  return wgrad_ws_bytes({n, h, w, ci, co});
 }
 
 int64_t rp_op_conv3x3_workspace_bytes(int32_t ci, int32_t co) {

@@ -57,6 +57,13 @@ int64_t conv3x3_tc_ws_bytes(const ConvShape& s);
 void conv3x3_fwd_tc(const ConvShape& s, const float* in, const float* w_hwio, bool dgrad_weights, const float* bias,
                     const float* aux, float h, int epi, float* out, bool three, void* ws, cudaStream_t st);
 
+// tcgen05 weight gradient (conv_wgrad_tc.cu): gw[tap][ci][co], gb[co] (may be null),
+// scaled; deterministic (per-CTA partials + fixed-order fp64 reduce).
+bool conv3x3_wgrad_tc_supported(const ConvShape& s, bool three);
+int64_t conv3x3_wgrad_tc_ws_bytes(const ConvShape& s, bool three);
+void conv3x3_wgrad_tc(const ConvShape& s, const float* in, const float* g, float scale, float* gw, float* gb,
+                      bool three, void* ws, cudaStream_t st);
+
 // ---- head (head.cu) -------------------------------------------------------
 int64_t head_ws_bytes(int nrows, int channels, int classes);
 void head_forward(int nrows, int hw, int channels, int classes, const float* x_end, const float* t_w,

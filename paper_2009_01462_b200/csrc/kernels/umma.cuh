@@ -90,6 +90,15 @@ __device__ __forceinline__ void tma_load_5d(const CUtensorMap* m, uint64_t* bar,
       : "memory");
 }
 
+__device__ __forceinline__ void tma_load_4d(const CUtensorMap* m, uint64_t* bar, void* dst, int c0, int c1, int c2,
+                                            int c3) {
+  asm volatile(
+      "cp.async.bulk.tensor.4d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%2, %3, %4, %5}], [%6];" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(m)), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(smem_u32(bar))
+      : "memory");
+}
+
 // Contiguous bulk copy global -> shared (bytes % 16 == 0, 16-byte aligned).
 __device__ __forceinline__ void bulk_load(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
   asm volatile(
@@ -172,14 +181,39 @@ __device__ __forceinline__ uint64_t desc_kmajor_interleave(uint32_t saddr, uint3
   return d;
 }
 
-// Instruction descriptor: fp32 accumulate, K-major A and B, M x N.
+// Instruction descriptor: fp32 accumulate, M x N; a_mn / b_mn select MN-major operands.
 // fmt: 0 = f16, 1 = bf16, 2 = tf32
-__host__ __device__ constexpr uint32_t idesc(int fmt, int M, int N) {
+__host__ __device__ constexpr uint32_t idesc(int fmt, int M, int N, int a_mn = 0, int b_mn = 0) {
   return (1u << 4)                           // c_format = F32
          | ((uint32_t)fmt << 7)              // a_format
          | ((uint32_t)fmt << 10)             // b_format
+         | ((uint32_t)a_mn << 15)            // a_major
+         | ((uint32_t)b_mn << 16)            // b_major
          | ((uint32_t)(N >> 3) << 17)        // n_dim
          | ((uint32_t)(M >> 4) << 24);       // m_dim
 }
 
+// MN-major, no swizzle: a core matrix is 8 K-rows x 16 B (4 tf32 MN-elements), 128
+// contiguous bytes; lbo = byte distance between K-adjacent core matrices, sbo = byte
+// distance between MN-adjacent core matrices.  Same bit packing as the K-major form.
+__device__ __forceinline__ uint64_t desc_mnmajor_interleave(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
+  return desc_kmajor_interleave(saddr, lbo, sbo);
+}
+
+}  // namespace rp::umma
+
+namespace rp::umma {
+// General form: layout_type 0 none, 1 SW128 with 32 B atoms (MN-major tf32), 2 SW128,
+// 4 SW64, 6 SW32; base_offset = pattern phase of the start address.
+__device__ __forceinline__ uint64_t desc_general(uint32_t saddr, uint32_t lbo, uint32_t sbo, uint32_t layout,
+                                                 uint32_t base_offset) {
+  uint64_t d = 0;
+  d |= (uint64_t)((saddr >> 4) & 0x3FFF);
+  d |= (uint64_t)((lbo >> 4) & 0x3FFF) << 16;
+  d |= (uint64_t)((sbo >> 4) & 0x3FFF) << 32;
+  d |= (uint64_t)1 << 46;
+  d |= (uint64_t)(base_offset & 7) << 49;
+  d |= (uint64_t)(layout & 7) << 61;
+  return d;
+}
 }  // namespace rp::umma

@@ -81,3 +81,42 @@ def test_conv_tc_is_deterministic_and_batch_independent():
     a, _ = run_conv(4, 32, 32, 64, 64, 1, "fp32", False, seed=3)
     b, _ = run_conv(4, 32, 32, 64, 64, 1, "fp32", False, seed=3)
     assert np.array_equal(a, b)
+
+
+def run_wgrad(n, hh, ww, ci, co, math, seed=0, scale=0.8):
+    rng = np.random.default_rng(seed)
+    x = rng.uniform(-1, 1, (n, hh, ww, ci)).astype(np.float32)
+    g = rng.uniform(-1, 1, (n, hh, ww, co)).astype(np.float32)
+    want_w = scale * O.conv3x3_wgrad(x.astype(np.float64), g.astype(np.float64))
+    want_b = scale * g.astype(np.float64).reshape(-1, co).sum(axis=0)
+    dev = torch.device("cuda")
+    tx, tg = torch.from_numpy(x).to(dev), torch.from_numpy(g).to(dev)
+    gw = torch.full((3, 3, ci, co), float("nan"), device=dev)
+    gb = torch.full((co,), float("nan"), device=dev)
+    wsb = lib().rp_op_conv3x3_wgrad_workspace_bytes(n, hh, ww, ci, co)
+    ws = torch.empty(wsb, dtype=torch.uint8, device=dev)
+    rp.check(lib().rp_op_conv3x3_wgrad(n, hh, ww, ci, co, C.c_void_p(tx.data_ptr()), C.c_void_p(tg.data_ptr()),
+                                       scale, C.c_void_p(gw.data_ptr()), C.c_void_p(gb.data_ptr()), rp.MATH[math],
+                                       C.c_void_p(ws.data_ptr()), wsb, None))
+    torch.cuda.synchronize()
+    return gw.cpu().numpy().astype(np.float64), gb.cpu().numpy().astype(np.float64), want_w, want_b
+
+
+WG_SHAPES = [(2, 32, 32, 64, 64), (3, 8, 8, 16, 64), (4, 16, 16, 32, 64), (1, 12, 10, 64, 64), (2, 32, 32, 64, 128),
+             (3, 7, 7, 16, 16)]
+
+
+@pytest.mark.parametrize("math,tol", [("fp32", 2e-5), ("simt", 2e-6), ("tf32", 5e-3)])
+@pytest.mark.parametrize("shape", WG_SHAPES)
+def test_wgrad(shape, math, tol):
+    gw, gb, ww_, wb = run_wgrad(*shape, math=math)
+    ew = np.abs(gw - ww_).max() / np.abs(ww_).max()
+    eb = np.abs(gb - wb).max() / np.abs(wb).max()
+    print(f"wgrad {shape} {math}: w {ew:.2e} b {eb:.2e}")
+    assert ew <= tol and eb <= max(tol, 1e-6), (ew, eb)
+
+
+def test_wgrad_deterministic():
+    a = run_wgrad(2, 32, 32, 64, 64, "fp32", seed=5)
+    b = run_wgrad(2, 32, 32, 64, 64, "fp32", seed=5)
+    assert np.array_equal(a[0], b[0]) and np.array_equal(a[1], b[1])
