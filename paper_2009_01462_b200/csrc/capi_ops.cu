@@ -54,7 +54,8 @@ void check_math(int math) {
 // bytes reserved at the front of an op workspace for per-call weight relayouts
 int64_t weight_ws_bytes(const rp_geometry& g) {
   const int64_t C = g.channels, Ch = g.hidden;
-  return align256(std::max<int64_t>(k::conv3x3_tc_ws_bytes({1, 1, 1, (int)C, (int)Ch}), 9 * C * Ch * 4));
+  return align256(std::max({k::conv3x3_tc_ws_bytes({1, 1, 1, (int)C, (int)Ch}),
+                            k::conv3x3_tc_ws_bytes({1, 1, 1, (int)Ch, (int)C}), (int64_t)(9 * C * Ch * 4)}));
 }
 
 int64_t wgrad_ws_bytes(const k::ConvShape& s) {
@@ -291,6 +292,8 @@ int rp_op_sgd(float* w, const float* g, float* v, int64_t n, double lr, double m
   });
 }
 
+int64_t rp_op_conv3x3_workspace_bytes(int32_t ci, int32_t co);
+
 int rp_op_conv3x3(int32_t n, int32_t h, int32_t w, int32_t ci, int32_t co, const float* in, const float* w_hwio,
                   int32_t dgrad, const float* bias, const float* aux, double hstep, int32_t epi, float* out,
                   int32_t math, void* ws, int64_t ws_bytes, void* stream) {
@@ -299,7 +302,7 @@ int rp_op_conv3x3(int32_t n, int32_t h, int32_t w, int32_t ci, int32_t co, const
     if (epi < 0 || epi > 5) fail(RP_ERR_RANGE, "conv3x3: unknown epilogue");
     if (n < 0 || h < 1 || w < 1 || ci < 1 || co < 1) fail(RP_ERR_SHAPE, "conv3x3: bad shape");
     const k::ConvShape s{n, h, w, ci, co};
-    if (ws_bytes < align256(std::max<int64_t>(k::conv3x3_tc_ws_bytes(s), 9LL * ci * co * 4)))
+    if (ws_bytes < rp_op_conv3x3_workspace_bytes(std::min(ci, co), std::max(ci, co)))
       fail(RP_ERR_RANGE, "conv3x3: workspace too small");
     conv(s, in, w_hwio, dgrad != 0, bias, aux, (float)hstep, epi, out, math, ws, RP_PROF_OTHER,
          aux != nullptr, S(stream));
@@ -322,7 +325,9 @@ int64_t rp_op_conv3x3_wgrad_workspace_bytes(int32_t n, int32_t h, int32_t w, int
 }
 
 int64_t rp_op_conv3x3_workspace_bytes(int32_t ci, int32_t co) {
-  return align256(std::max<int64_t>(k::conv3x3_tc_ws_bytes({1, 1, 1, ci, co}), 9LL * ci * co * 4));
+  // either orientation (fprop ci -> co, or its dgrad co -> ci)
+  return align256(std::max({k::conv3x3_tc_ws_bytes({1, 1, 1, ci, co}), k::conv3x3_tc_ws_bytes({1, 1, 1, co, ci}),
+                            (int64_t)9 * ci * co * 4}));
 }
 
 int rp_op_block_fwd(const rp_geometry* g, int32_t nrows, const float* x, const float* pb, float* a, float* x_next,

@@ -6,27 +6,33 @@
 // W2^T) / matmul(dpre, W1^T), network.cpp:85-104, generalised to 3x3 taps.)
 //
 // Design:
-//  * M = output positions in the zero-padded "interior frame" of one image (H rows x
-//    (W+2) columns, flattened): tap (dy,dx) is then a constant shift of
-//    dy*(W+2)+dx positions, so one halo slab per 16-channel chunk, loaded once by TMA
-//    (out-of-bounds rows/columns zero-filled by the TMA unit), serves all 9 taps as 9
-//    shifted UMMA descriptors.  The 2 padding columns per row are computed and
-//    discarded (6% of the MMA work at W = 32).
-//  * operands are K-major "interleaved" (no swizzle): for each group of 4 channels
-//    every position is 16 contiguous bytes, so a shift by one position is +16 B of
-//    descriptor start address.  The TMA box is (4 ch, W+2, rows, 4 kgroups, 1) over a
-//    5-D view of NHWC whose 4th dim is the channel group (stride 16 B).
-//  * a unit = S consecutive 128-position tiles sharing one weight pass (S
-//    accumulators of 128 x Co fp32 in TMEM, double-buffered across units).
-//  * fp32 accuracy with tensor cores: 3xTF32.  Each operand v = hi + lo with
-//    hi = rna_tf32(v) and lo = v - hi (exact); D += Ahi Bhi + Ahi Blo + Alo Bhi.
-//    Weights are split once per call into global memory; the activation halo is split
-//    in shared memory by 4 converter warps.  RP_MATH_TF32 issues only Ahi Bhi.
+//  * Output positions live in the zero-padded "interior frame" of one image (H rows x
+//    (W+2) columns, flattened): tap (dy,dx) is then a constant shift of dy*(W+2)+dx
+//    positions, so one halo slab per 16-channel chunk, loaded once by TMA (out-of-bounds
+//    rows/columns zero-filled), serves all 9 taps as 9 shifted UMMA descriptors.  The 2
+//    padding columns per row are computed and discarded.
+//  * D^T = W^T x: the MMA's A operand is the (tiny) weight tile, M = 128 rows = the output
+//    channels stacked twice, [W_hi ; W_lo]; B is the shifted halo view, N = 128 positions.
+//    Consecutive MMAs share A (both operand splits of x, both tiles of a unit), which is
+//    what lets tcgen05 run at its full rate (tools/umma_bench.py: a new A every MMA
+//    costs ~40% through shared-memory operand bandwidth).
+//  * fp32 accuracy (RP_MATH_FP32, "3xTF32+"): v = hi + lo, hi = rna_tf32(v), lo = v - hi
+//    (exact).  MMA(A = [W_hi; W_lo], B = x_hi) and MMA(A, B = x_lo) accumulate all four
+//    products; the epilogue adds the hi-row and lo-row halves.  RP_MATH_TF32 drops the
+//    x_lo MMA (x enters truncated).
+//  * operands are K-major "interleaved" (no swizzle): for each group of 4 channels every
+//    position is 16 contiguous bytes, so a shift by one position is +16 B of descriptor
+//    start address.  The TMA box is (4 ch, W+2, rows, 4 kgroups, 1) over a 5-D view of
+//    NHWC whose 4th dim is the channel group (stride 16 B).
+//  * a unit = up to S = 2 consecutive 128-position tiles (accumulators 128 x 128 fp32 in
+//    TMEM, double-buffered across units); tiles past the image end are skipped.
 //  * warp roles (320 threads, persistent, 1 CTA/SM): w0 TMA producer, w1 MMA issuer
-//    (one thread), w2-5 converters, w6-9 epilogue (TMEM -> registers -> fused
-//    bias / tanh / skip / step-size -> global).
+//    (whole warp walks the loop so descriptors stay warp-uniform; one elected lane
+//    issues), w2-5 converters (halo hi/lo split), w6-9 epilogue (TMEM -> registers ->
+//    hi+lo sum -> fused bias / tanh / skip / step-size -> coalesced NHWC stores).
 #include <cuda.h>
 
+#include <cstdlib>
 #include <map>
 #include <mutex>
 #include <tuple>
@@ -42,23 +48,22 @@ namespace {
 using namespace rp::umma;
 
 constexpr int kThreads = 320;
-constexpr int kWStages = 4;
+constexpr int kWStages = 3;          // one weight stage = one filter row (3 taps) of one chunk
 constexpr int kChunk = 16;           // input channels per halo chunk
+constexpr int kS = 2;                // 128-position tiles per unit
 constexpr int kMaxSmem = 220 * 1024;
 
 struct TcArgs {
-  int N, H, W, Ci, Co, Wp, rows_h, S, units_per_img, num_units, halo_pos, nchunks;
+  int N, H, W, Ci, Co, Wp, rows_h, T, units_per_img, num_units, halo_pos, nchunks;
   uint32_t halo_bytes;  // one raw (or lo) halo buffer
-  uint32_t w_bytes;     // one hi (or lo) weight stage
-  uint32_t halo_stride; // bytes per halo stage slot (raw + lo + pads)
-  int three;            // 1: 3xTF32, 0: plain TF32
-  int epi;
+  uint32_t halo_stride; // bytes per halo slot (raw + lo + pads)
+  uint32_t w_tap;       // bytes of one tap's A operand (128 rows x 16 channels x 4 B)
   float h;
-  const float* w_hi;    // [tap][chunk][kg][co][4]
-  const float* w_lo;
+  const float* w;       // prepped [chunk][tap][kg][128 rows][4]
   const float* bias;
   const float* aux;
   float* out;
+  unsigned long long* trace;   // diagnostics (tools/trace_conv.py): per-unit timestamps, null = off
 };
 
 __device__ __forceinline__ float rna_tf32(float v) {
@@ -68,10 +73,10 @@ __device__ __forceinline__ float rna_tf32(float v) {
 }
 
 template <int EPI>
-__device__ __forceinline__ float epi_value(float acc, int co, int64_t idx, const TcArgs& a) {
-  if constexpr (EPI == EPI_BIAS) return acc + __ldg(a.bias + co);
-  if constexpr (EPI == EPI_BIAS_TANH) return tanhf(acc + __ldg(a.bias + co));
-  if constexpr (EPI == EPI_RESID) return __ldg(a.aux + idx) + a.h * (acc + __ldg(a.bias + co));
+__device__ __forceinline__ float epi_value(float acc, float bias, int64_t idx, const TcArgs& a) {
+  if constexpr (EPI == EPI_BIAS) return acc + bias;
+  if constexpr (EPI == EPI_BIAS_TANH) return tanhf(acc + bias);
+  if constexpr (EPI == EPI_RESID) return __ldg(a.aux + idx) + a.h * (acc + bias);
   if constexpr (EPI == EPI_TANH_BWD) {
     const float t = __ldg(a.aux + idx);
     return (a.h * acc) * (1.f - t * t);
@@ -80,17 +85,19 @@ __device__ __forceinline__ float epi_value(float acc, int co, int64_t idx, const
   return a.h * acc;
 }
 
-template <int EPI>
+template <int EPI, bool THREE>
 __global__ void __launch_bounds__(kThreads, 1)
-    conv3x3_tc_kernel(const __grid_constant__ CUtensorMap tmap, const TcArgs a, int tmem_cols) {
+    conv3x3_tc_kernel(const __grid_constant__ CUtensorMap tmap, const TcArgs a) {
   extern __shared__ __align__(1024) uint8_t smem[];
-  const int warp = threadIdx.x >> 5;
+  const int warp = __shfl_sync(0xffffffffu, (int)threadIdx.x / 32, 0);   // warp-uniform role index
   const int lane = threadIdx.x & 31;
 
   // ---- shared memory carve-up
-  uint8_t* halo_base = smem;                                      // 2 slots
-  uint8_t* w_base = smem + 2 * a.halo_stride;                     // kWStages x (hi, lo)
-  uint64_t* bars = reinterpret_cast<uint64_t*>(w_base + kWStages * 2 * a.w_bytes);
+  const uint32_t w_stage = 3 * a.w_tap;
+  uint8_t* halo_base = smem;                                  // 2 slots
+  uint8_t* w_base = smem + 2 * a.halo_stride;                 // kWStages stages
+  float* xchg = reinterpret_cast<float*>(w_base + kWStages * w_stage);   // [2 buf][2 pairs][2 sides][32][32]
+  uint64_t* bars = reinterpret_cast<uint64_t*>(xchg + 2 * 2 * 2 * 32 * 32);
   uint64_t* halo_full = bars;        // [2]
   uint64_t* halo_conv = bars + 2;    // [2]
   uint64_t* halo_empty = bars + 4;   // [2]
@@ -101,9 +108,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 10 + 2 * kWStages);
 
   auto halo_raw = [&](int s) { return halo_base + s * a.halo_stride + 128; };
-  auto halo_lo = [&](int s) { return halo_base + s * a.halo_stride + 128 + a.halo_bytes + 128; };
-  auto w_hi_s = [&](int s) { return w_base + s * 2 * a.w_bytes; };
-  auto w_lo_s = [&](int s) { return w_base + s * 2 * a.w_bytes + a.w_bytes; };
+  auto halo_lo = [&](int s) { return halo_base + s * a.halo_stride + 256 + a.halo_bytes; };
+  auto w_s = [&](int s) { return w_base + s * w_stage; };
 
   if (threadIdx.x == 0) {
     for (int i = 0; i < 2; ++i) {
@@ -120,8 +126,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     fence_barrier_init();
     prefetch_tmap(&tmap);
   }
-  if (warp == 1) tmem_alloc<512>(tmem_slot);  // column count fixed at the max; see host
-  // zero the 128-byte pads around the halo buffers (read only by discarded rows)
+  if (warp == 1) tmem_alloc<512>(tmem_slot);
+  // zero the 128-byte pads around the halo buffers (read only for discarded positions)
   for (int i = threadIdx.x; i < 2 * 3 * 32; i += blockDim.x) {
     const int s = i / 96, part = (i / 32) % 3, w = i % 32;
     uint8_t* base = halo_base + s * a.halo_stride +
@@ -131,102 +137,117 @@ __global__ void __launch_bounds__(kThreads, 1)
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
-  const uint32_t tmem_base = *tmem_slot;
-  (void)tmem_cols;
+  const uint32_t tmem_base = __shfl_sync(0xffffffffu, *tmem_slot, 0);
 
   const int Wp = a.Wp;
-  const uint32_t kg_stride_a = (uint32_t)a.halo_pos * 16u;     // bytes between channel groups (halo)
-  const uint32_t kg_stride_b = (uint32_t)a.Co * 16u;           // bytes between channel groups (weights)
 
   if (warp == 0) {
     // ===================== TMA producer =====================
-    if (lane == 0) {
-      int hs = 0, ws = 0;
-      uint32_t hph = 0, wph = 0;
-      for (int u = blockIdx.x; u < a.num_units; u += gridDim.x) {
-        const int n = u / a.units_per_img;
-        const int f0 = (u % a.units_per_img) * a.S * 128;
-        const int y0 = f0 / Wp;
-        for (int c = 0; c < a.nchunks; ++c) {
-          mbar_wait(&halo_empty[hs], hph ^ 1);
+    int hs = 0, ws = 0;
+    uint32_t hph = 0, wph = 0;
+    const uint32_t wbytes = 3 * a.w_tap;
+    for (int u = blockIdx.x; u < a.num_units; u += gridDim.x) {
+      const int n = u / a.units_per_img;
+      const int f0 = (u - n * a.units_per_img) * kS * 128;
+      const int y0 = f0 / Wp;
+      for (int c = 0; c < a.nchunks; ++c) {
+        mbar_wait(&halo_empty[hs], hph ^ 1);
+        if (elect_one()) {
           mbar_arrive_expect_tx(&halo_full[hs], a.halo_bytes);
           tma_load_5d(&tmap, &halo_full[hs], halo_raw(hs), 0, -1, y0 - 1, 4 * c, n);
-          if (++hs == 2) hs = 0, hph ^= 1;
-          for (int t = 0; t < 9; ++t) {
-            mbar_wait(&w_empty[ws], wph ^ 1);
-            mbar_arrive_expect_tx(&w_full[ws], a.three ? 2 * a.w_bytes : a.w_bytes);
-            const int64_t off = ((int64_t)t * a.nchunks + c) * (a.w_bytes / 4);
-            bulk_load(w_hi_s(ws), a.w_hi + off, a.w_bytes, &w_full[ws]);
-            if (a.three) bulk_load(w_lo_s(ws), a.w_lo + off, a.w_bytes, &w_full[ws]);
-            if (++ws == kWStages) ws = 0, wph ^= 1;
+        }
+        __syncwarp();
+        if (++hs == 2) hs = 0, hph ^= 1;
+        for (int dy = 0; dy < 3; ++dy) {
+          mbar_wait(&w_empty[ws], wph ^ 1);
+          if (elect_one()) {
+            mbar_arrive_expect_tx(&w_full[ws], wbytes);
+            bulk_load(w_s(ws), a.w + ((int64_t)c * 9 + 3 * dy) * (a.w_tap / 4), wbytes, &w_full[ws]);
           }
+          __syncwarp();
+          if (++ws == kWStages) ws = 0, wph ^= 1;
         }
       }
     }
   } else if (warp == 1) {
     // ===================== MMA issuer =====================
-    if (lane == 0) {
-      const uint32_t id = idesc(2, 128, a.Co);
-      int hs = 0, ws = 0, ab = 0;
-      uint32_t hph = 0, wph = 0, aph = 0;
-      for (int u = blockIdx.x; u < a.num_units; u += gridDim.x) {
-        const int f0 = (u % a.units_per_img) * a.S * 128;
-        const int c0 = f0 % Wp;
-        mbar_wait(&acc_empty[ab], aph ^ 1);
+    const uint32_t id = idesc(2, 128, 128);
+    const uint32_t kg_x = (uint32_t)a.halo_pos * 16u;     // bytes between channel groups (halo)
+    const uint32_t kg_w = 128u * 16u;                     // bytes between channel groups (weights)
+    const uint64_t xj = (uint64_t)((2 * kg_x) >> 4);      // K-step (8 channels) of B, 16-byte units
+    const uint64_t wj = (uint64_t)((2 * kg_w) >> 4);
+    const uint64_t wtap = (uint64_t)(a.w_tap >> 4);
+    int hs = 0, ws = 0, ab = 0;
+    uint32_t hph = 0, wph = 0, aph = 0;
+    for (int u = blockIdx.x; u < a.num_units; u += gridDim.x) {
+      const int n = u / a.units_per_img;
+      const int tile0 = (u - n * a.units_per_img) * kS;
+      const int ntiles = min(kS, a.T - tile0);               // warp-uniform
+      const int f0 = tile0 * 128;
+      const int c0 = f0 - (f0 / Wp) * Wp;
+      mbar_wait(&acc_empty[ab], aph ^ 1);
+      tc_fence_after();
+      if (a.trace && blockIdx.x < 2 && lane == 0) a.trace[(blockIdx.x * 64 + (u / gridDim.x)) * 8 + 0] = globaltimer_ns();
+      const uint32_t d0 = tmem_base + (uint32_t)(ab * kS * 128);
+      for (int c = 0; c < a.nchunks; ++c) {
+        mbar_wait(THREE ? &halo_conv[hs] : &halo_full[hs], hph);
         tc_fence_after();
-        for (int c = 0; c < a.nchunks; ++c) {
-          mbar_wait(a.three ? &halo_conv[hs] : &halo_full[hs], hph);
+        if (a.trace && blockIdx.x < 2 && lane == 0) a.trace[(blockIdx.x * 64 + (u / gridDim.x)) * 8 + 4 + (c < 3 ? c : 3)] = globaltimer_ns();
+        const uint64_t dxh0 = desc_kmajor_interleave(smem_u32(halo_raw(hs)), kg_x, 128);
+        const uint64_t dxl0 = desc_kmajor_interleave(smem_u32(halo_lo(hs)), kg_x, 128);
+        for (int dy = 0; dy < 3; ++dy) {
+          mbar_wait(&w_full[ws], wph);
           tc_fence_after();
-          const uint32_t raw = smem_u32(halo_raw(hs));
-          const uint32_t lo = smem_u32(halo_lo(hs));
-          for (int t = 0; t < 9; ++t) {
-            mbar_wait(&w_full[ws], wph);
-            tc_fence_after();
-            const int shift = c0 + (t / 3) * Wp + (t % 3) - 1;
-            const uint32_t bh = smem_u32(w_hi_s(ws));
-            const uint32_t bl = smem_u32(w_lo_s(ws));
+          const uint64_t dw0 = desc_kmajor_interleave(smem_u32(w_s(ws)), kg_w, 128);
+          const int64_t row = c0 + dy * Wp - 1;              // positions; >= -1
+          const uint64_t bh = dxh0 + (uint64_t)row;          // 16-byte units: one position = 1
+          const uint64_t bl = dxl0 + (uint64_t)row;
+          const bool first = (c == 0 && dy == 0);
+          if (elect_one()) {
 #pragma unroll
-            for (int j = 0; j < 2; ++j) {
-              const uint64_t db_hi = desc_kmajor_interleave(bh + 2 * j * kg_stride_b, kg_stride_b, 128);
-              const uint64_t db_lo = desc_kmajor_interleave(bl + 2 * j * kg_stride_b, kg_stride_b, 128);
-              for (int s = 0; s < a.S; ++s) {
-                const uint32_t pos = (uint32_t)(shift + s * 128);
-                const uint32_t aoff = 2 * j * kg_stride_a + pos * 16u;
-                const uint64_t da_hi = desc_kmajor_interleave(raw + aoff, kg_stride_a, 128);
-                const uint32_t d = tmem_base + (uint32_t)((ab * a.S + s) * a.Co);
-                const uint32_t accum = (c | t | j) ? 1u : 0u;
-                mma_tf32(d, da_hi, db_hi, id, accum);
-                if (a.three) {
-                  const uint64_t da_lo = desc_kmajor_interleave(lo + aoff, kg_stride_a, 128);
-                  mma_tf32(d, da_hi, db_lo, id, 1u);
-                  mma_tf32(d, da_lo, db_hi, id, 1u);
+            for (int dx = 0; dx < 3; ++dx) {
+#pragma unroll
+              for (int j = 0; j < 2; ++j) {
+                const uint64_t da = dw0 + dx * wtap + j * wj;   // A: weights, shared by the next MMAs
+                const uint32_t accum = (first && dx == 0 && j == 0) ? 0u : 1u;
+#pragma unroll
+                for (int s = 0; s < kS; ++s) {
+                  if (s < ntiles) {
+                    const uint64_t boff = (uint64_t)(dx + 128 * s) + j * xj;
+                    mma_tf32(d0 + s * 128, da, bh + boff, id, accum);
+                    if (THREE) mma_tf32(d0 + s * 128, da, bl + boff, id, 1u);
+                  }
                 }
               }
             }
             mma_commit(&w_empty[ws]);
-            if (++ws == kWStages) ws = 0, wph ^= 1;
           }
-          mma_commit(&halo_empty[hs]);
-          if (++hs == 2) hs = 0, hph ^= 1;
+          __syncwarp();
+          if (++ws == kWStages) ws = 0, wph ^= 1;
         }
-        mma_commit(&acc_full[ab]);
-        if (++ab == 2) ab = 0, aph ^= 1;
+        if (elect_one()) mma_commit(&halo_empty[hs]);
+        __syncwarp();
+        if (++hs == 2) hs = 0, hph ^= 1;
       }
+      if (elect_one()) mma_commit(&acc_full[ab]);
+      __syncwarp();
+      if (a.trace && blockIdx.x < 2 && lane == 0) a.trace[(blockIdx.x * 64 + (u / gridDim.x)) * 8 + 1] = globaltimer_ns();
+      if (++ab == 2) ab = 0, aph ^= 1;
     }
   } else if (warp < 6) {
-    // ===================== converters (3xTF32 split of the halo) =====================
-    if (a.three) {
+    // ===================== converters (hi/lo split of the halo) =====================
+    if (THREE) {
       const int tid = threadIdx.x - 64;
       int hs = 0;
       uint32_t hph = 0;
+      const int n16 = (int)(a.halo_bytes / 16);
       for (int u = blockIdx.x; u < a.num_units; u += gridDim.x) {
         for (int c = 0; c < a.nchunks; ++c) {
           mbar_wait(&halo_full[hs], hph);
           float4* raw = reinterpret_cast<float4*>(halo_raw(hs));
           float4* lo = reinterpret_cast<float4*>(halo_lo(hs));
-          const int n16 = (int)(a.halo_bytes / 16);
           for (int i = tid; i < n16; i += 128) {
-            float4 v = raw[i];
+            const float4 v = raw[i];
             float4 hi, l;
             hi.x = rna_tf32(v.x); hi.y = rna_tf32(v.y); hi.z = rna_tf32(v.z); hi.w = rna_tf32(v.w);
             l.x = v.x - hi.x; l.y = v.y - hi.y; l.z = v.z - hi.z; l.w = v.w - hi.w;
@@ -241,38 +262,77 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
   } else {
     // ===================== epilogue =====================
-    const int q = warp & 3;         // TMEM lane quadrant this warp may access
-    const int m = q * 32 + lane;    // accumulator row == position within the tile
-    int ab = 0;
+    // D row r: r < 64 -> W_hi products for co = r, r >= 64 -> W_lo products for co = r - 64.
+    // The warp pair holding the hi and lo rows of the same 32 channels swaps half of each
+    // 16-position chunk through shared memory; each warp then finishes 8 positions
+    // (hi + lo, fused epilogue) and stores 32 consecutive channels of a position per
+    // instruction (coalesced NHWC).
+    const int q = warp & 3;                 // TMEM lane quadrant this warp may access
+    const bool hi_warp = q < 2;
+    const int co = (q & 1) * 32 + lane;     // output channel of this lane
+    const float bias = (EPI == EPI_BIAS || EPI == EPI_BIAS_TANH || EPI == EPI_RESID) ? __ldg(a.bias + co) : 0.f;
+    const int own0 = hi_warp ? 0 : 32;      // positions [own0, own0 + 32) of each 64-batch are ours
+    int ab = 0, xb = 0;
     uint32_t aph = 0;
     for (int u = blockIdx.x; u < a.num_units; u += gridDim.x) {
       const int n = u / a.units_per_img;
-      const int f0 = (u % a.units_per_img) * a.S * 128;
+      const int tile0 = (u - n * a.units_per_img) * kS;
+      const int ntiles = min(kS, a.T - tile0);
+      const int64_t img = (int64_t)n * a.H * a.W;
       mbar_wait(&acc_full[ab], aph);
       tc_fence_after();
-      for (int s = 0; s < a.S; ++s) {
-        const int f = f0 + s * 128 + m;
-        const int y = f / Wp, X = f - (f / Wp) * Wp;
-        const bool valid = y < a.H && X >= 1 && X <= a.W;
-        const int64_t base = valid ? ((((int64_t)n * a.H + y) * a.W) + (X - 1)) * a.Co : 0;
-        for (int cc = 0; cc < a.Co; cc += 16) {
-          uint32_t r[16];
-          tmem_ld16(tmem_base + ((uint32_t)(q * 32) << 16) + (uint32_t)((ab * a.S + s) * a.Co + cc), r);
+      if (a.trace && blockIdx.x < 2 && threadIdx.x == 192) a.trace[(blockIdx.x * 64 + (u / gridDim.x)) * 8 + 2] = globaltimer_ns();
+      for (int s = 0; s < ntiles; ++s) {
+        const uint32_t tcol = tmem_base + ((uint32_t)(q * 32) << 16) + (uint32_t)((ab * kS + s) * 128);
+        for (int p0 = 0; p0 < 128; p0 += 64) {
+          uint32_t r[64];
+          tmem_ld16(tcol + (uint32_t)p0, *reinterpret_cast<uint32_t(*)[16]>(&r[0]));
+          tmem_ld16(tcol + (uint32_t)p0 + 16, *reinterpret_cast<uint32_t(*)[16]>(&r[16]));
+          tmem_ld16(tcol + (uint32_t)p0 + 32, *reinterpret_cast<uint32_t(*)[16]>(&r[32]));
+          tmem_ld16(tcol + (uint32_t)p0 + 48, *reinterpret_cast<uint32_t(*)[16]>(&r[48]));
           tmem_wait_ld();
-          if (valid) {
-            float4* dst = reinterpret_cast<float4*>(a.out + base + cc);
+          float* mine = xchg + ((xb * 2 + (q & 1)) * 2 + (hi_warp ? 0 : 1)) * 32 * 32;
+          float* theirs = xchg + ((xb * 2 + (q & 1)) * 2 + (hi_warp ? 1 : 0)) * 32 * 32;
+          // static register indices only (a runtime offset into r[] would spill it to local memory)
 #pragma unroll
-            for (int v = 0; v < 4; ++v) {
-              float4 o;
-              o.x = epi_value<EPI>(__uint_as_float(r[4 * v + 0]), cc + 4 * v + 0, base + cc + 4 * v + 0, a);
-              o.y = epi_value<EPI>(__uint_as_float(r[4 * v + 1]), cc + 4 * v + 1, base + cc + 4 * v + 1, a);
-              o.z = epi_value<EPI>(__uint_as_float(r[4 * v + 2]), cc + 4 * v + 2, base + cc + 4 * v + 2, a);
-              o.w = epi_value<EPI>(__uint_as_float(r[4 * v + 3]), cc + 4 * v + 3, base + cc + 4 * v + 3, a);
-              dst[v] = o;
+          for (int e = 0; e < 32; ++e) mine[e * 32 + lane] = __uint_as_float(hi_warp ? r[32 + e] : r[e]);
+          asm volatile("bar.sync 2, 128;" ::: "memory");
+          // positions own0 .. own0+31 of this batch: frame coordinates without divisions
+          const int f = (tile0 + s) * 128 + p0 + own0;
+          int y = f / Wp, X = f - (f / Wp) * Wp;
+#pragma unroll
+          for (int e0 = 0; e0 < 32; e0 += 8) {
+            float v[8], auxv[8];
+            int64_t idx[8];
+            bool ok[8];
+#pragma unroll
+            for (int e = 0; e < 8; ++e) {
+              ok[e] = y < a.H && X >= 1 && X <= a.W;
+              idx[e] = (img + (int64_t)y * a.W + (X - 1)) * a.Co + co;
+              v[e] = __uint_as_float(hi_warp ? r[e0 + e] : r[32 + e0 + e]) + theirs[(e0 + e) * 32 + lane];
+              if (++X == Wp) X = 0, ++y;
+            }
+            if (EPI == EPI_RESID || EPI == EPI_TANH_BWD || EPI == EPI_ADD) {
+#pragma unroll
+              for (int e = 0; e < 8; ++e) auxv[e] = ok[e] ? a.aux[idx[e]] : 0.f;
+            }
+#pragma unroll
+            for (int e = 0; e < 8; ++e) {
+              if (!ok[e]) continue;                           // warp-uniform
+              float o;
+              if constexpr (EPI == EPI_BIAS) o = v[e] + bias;
+              else if constexpr (EPI == EPI_BIAS_TANH) o = tanhf(v[e] + bias);
+              else if constexpr (EPI == EPI_RESID) o = auxv[e] + a.h * (v[e] + bias);
+              else if constexpr (EPI == EPI_TANH_BWD) o = (a.h * v[e]) * (1.f - auxv[e] * auxv[e]);
+              else if constexpr (EPI == EPI_ADD) o = auxv[e] + v[e];
+              else o = a.h * v[e];
+              a.out[idx[e]] = o;
             }
           }
+          xb ^= 1;
         }
       }
+      if (a.trace && blockIdx.x < 2 && threadIdx.x == 192) a.trace[(blockIdx.x * 64 + (u / gridDim.x)) * 8 + 3] = globaltimer_ns();
       tc_fence_before();
       mbar_arrive(&acc_empty[ab]);
       if (++ab == 2) ab = 0, aph ^= 1;
@@ -287,38 +347,36 @@ __global__ void __launch_bounds__(kThreads, 1)
   }
 }
 
-// weights HWIO src[tap][ci][co] -> prepped [tap'][chunk][kg][co'][4] (hi, lo) for an
-// fprop (flip = 0: ci' = ci, co' = co) or dgrad (flip = 1: tap' = 8 - tap, ci' = co, co' = ci)
-__global__ void prep_weights_kernel(const float* __restrict__ w, int ci_src, int co_src, int flip, int three,
-                                    float* __restrict__ hi, float* __restrict__ lo) {
+// weights HWIO src[tap][ci][co] -> prepped A operand [chunk][tap'][kg][128 rows][4]: row
+// r < 64 holds w_hi[co = r], r >= 64 holds w_lo[co = r - 64] (TF32 mode: the same
+// split; x enters truncated).  fprop (flip = 0) or dgrad (flip = 1: tap' = 8 - tap,
+// ci' = co, co' = ci).
+__global__ void prep_weights_kernel(const float* __restrict__ w, int ci_src, int co_src, int flip,
+                                    float* __restrict__ out) {
   const int Ci = flip ? co_src : ci_src;
-  const int Co = flip ? ci_src : co_src;
-  const int nchunks = Ci / kChunk;
-  const int total = 9 * Ci * Co;
+  const int Co = flip ? ci_src : co_src;   // == 64
+  const int total = 9 * Ci * 128;
   for (int idx = blockIdx.x * blockDim.x + threadIdx.x; idx < total; idx += gridDim.x * blockDim.x) {
     const int e = idx & 3;
-    const int co = (idx >> 2) % Co;
-    const int rest = (idx >> 2) / Co;        // (tap, chunk, kg)
+    const int r = (idx >> 2) & 127;
+    const int rest = idx >> 9;                   // (chunk, tap, kg)
     const int kg = rest % 4;
-    const int chunk = (rest / 4) % nchunks;
-    const int tap = rest / (4 * nchunks);
+    const int tap = (rest / 4) % 9;
+    const int chunk = rest / 36;
     const int ci = chunk * kChunk + kg * 4 + e;
+    const int co = r < Co ? r : r - Co;
     float v;
     if (!flip)
       v = w[((int64_t)tap * ci_src + ci) * co_src + co];
     else
       v = w[((int64_t)(8 - tap) * ci_src + co) * co_src + ci];
-    if (three) {
-      const float h = rna_tf32(v);
-      hi[idx] = h;
-      lo[idx] = v - h;
-    } else {
-      hi[idx] = v;
-    }
+    const float h = rna_tf32(v);
+    out[idx] = r < Co ? h : v - h;
   }
 }
 
 // ---------------------------------------------------------------- host side
+unsigned long long* g_trace = nullptr;
 typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
                                   const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
                                   CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
@@ -352,35 +410,27 @@ CUtensorMap make_halo_map(const float* in, const ConvShape& s, int Wp, int rows_
 }
 
 struct Plan {
-  int S, Wp, rows_h, halo_pos, T, units_per_img;
-  uint32_t halo_bytes, w_bytes, halo_stride;
+  bool ok = false;
+  int Wp, rows_h, halo_pos, T, units_per_img;
+  uint32_t halo_bytes, w_tap, halo_stride;
   size_t smem;
 };
 
 Plan plan_for(const ConvShape& s) {
-  Plan best{};
-  double best_eff = -1.0;
-  for (int S = 4; S >= 1; --S) {
-    if (2 * S * s.co > 512) continue;
-    Plan p{};
-    p.S = S;
-    p.Wp = s.w + 2;
-    p.rows_h = (3 * p.Wp + 128 * S + p.Wp - 1) / p.Wp;
-    p.halo_pos = p.rows_h * p.Wp;
-    p.T = (s.h * p.Wp + 127) / 128;
-    p.units_per_img = (p.T + S - 1) / S;
-    p.halo_bytes = (uint32_t)p.halo_pos * 64u;
-    p.w_bytes = (uint32_t)s.co * kChunk * 4u;
-    p.halo_stride = (128 + p.halo_bytes + 128 + p.halo_bytes + 128 + 1023) / 1024 * 1024;
-    p.smem = 2 * (size_t)p.halo_stride + kWStages * 2 * (size_t)p.w_bytes + 256 + 1024;
-    if (p.smem > (size_t)kMaxSmem || p.rows_h > 256) continue;
-    const double eff = (double)p.T / (double)(p.units_per_img * S);
-    if (eff > best_eff + 1e-9) {
-      best_eff = eff;
-      best = p;
-    }
-  }
-  return best;
+  Plan p;
+  if (s.co != 64 || s.ci % kChunk != 0 || s.w + 2 > 256) return p;
+  p.Wp = s.w + 2;
+  p.rows_h = (3 * p.Wp + 128 * kS + p.Wp - 1) / p.Wp;
+  if (p.rows_h > 256) return p;
+  p.halo_pos = p.rows_h * p.Wp;
+  p.T = (s.h * p.Wp + 127) / 128;
+  p.units_per_img = (p.T + kS - 1) / kS;
+  p.halo_bytes = (uint32_t)p.halo_pos * 64u;
+  p.w_tap = 128u * kChunk * 4u;
+  p.halo_stride = (128 + p.halo_bytes + 128 + p.halo_bytes + 128 + 1023) / 1024 * 1024;
+  p.smem = 2 * (size_t)p.halo_stride + kWStages * 3 * (size_t)p.w_tap + 2 * 2 * 2 * 32 * 32 * 4 + 256 + 1024;
+  p.ok = p.smem <= (size_t)kMaxSmem;
+  return p;
 }
 
 std::mutex g_map_mu;
@@ -397,40 +447,45 @@ const CUtensorMap& cached_map(const float* in, const ConvShape& s, int Wp, int r
   return it->second;
 }
 
-template <int EPI>
-void launch_epi(const CUtensorMap& m, const TcArgs& a, size_t smem, int grid, cudaStream_t st) {
+template <int EPI, bool THREE>
+void launch_cfg(const CUtensorMap& m, const TcArgs& a, size_t smem, int grid, cudaStream_t st) {
   static bool configured = false;
   if (!configured) {
-    RP_CUDA(cudaFuncSetAttribute(conv3x3_tc_kernel<EPI>, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxSmem));
+    RP_CUDA(cudaFuncSetAttribute(conv3x3_tc_kernel<EPI, THREE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 kMaxSmem));
     configured = true;
   }
-  conv3x3_tc_kernel<EPI><<<grid, kThreads, smem, st>>>(m, a, 512);
+  conv3x3_tc_kernel<EPI, THREE><<<grid, kThreads, smem, st>>>(m, a);
+}
+
+template <int EPI>
+void launch_epi(const CUtensorMap& m, const TcArgs& a, bool three, size_t smem, int grid, cudaStream_t st) {
+  if (three)
+    launch_cfg<EPI, true>(m, a, smem, grid, st);
+  else
+    launch_cfg<EPI, false>(m, a, smem, grid, st);
 }
 
 }  // namespace
 
-bool conv3x3_tc_supported(const ConvShape& s) {
-  if (s.ci % kChunk != 0 || s.co % 16 != 0 || s.co > 256 || s.co < 16) return false;
-  if (s.w + 2 > 256) return false;
-  return plan_for(s).S > 0;
-}
+bool conv3x3_tc_supported(const ConvShape& s) { return plan_for(s).ok; }
 
-int64_t conv3x3_tc_ws_bytes(const ConvShape& s) { return 2 * (9LL * s.ci * s.co * 4 + 256); }
+void conv3x3_tc_set_trace(unsigned long long* p) { g_trace = p; }
+
+int64_t conv3x3_tc_ws_bytes(const ConvShape& s) { return 9LL * s.ci * 128 * 4 + 256; }
 
 void conv3x3_fwd_tc(const ConvShape& s, const float* in, const float* w_hwio, bool dgrad_weights, const float* bias,
                     const float* aux, float h, int epi, float* out, bool three, void* ws, cudaStream_t st) {
   if (s.pixels() == 0) return;
   const Plan p = plan_for(s);
-  if (p.S == 0) fail(RP_ERR_INTERNAL, "conv3x3_fwd_tc: unsupported shape");
-  float* w_hi = static_cast<float*>(ws);
-  float* w_lo = w_hi + (9LL * s.ci * s.co + 63) / 64 * 64;
+  if (!p.ok) fail(RP_ERR_INTERNAL, "conv3x3_fwd_tc: unsupported shape");
+  float* wp = static_cast<float*>(ws);
   // the weight tensor handed in is HWIO of the *forward* conv; for dgrad it has
   // (ci_src, co_src) = (s.co, s.ci)
   const int ci_src = dgrad_weights ? s.co : s.ci;
   const int co_src = dgrad_weights ? s.ci : s.co;
-  const int total = 9 * s.ci * s.co;
-  prep_weights_kernel<<<ceil_div(total, 256), 256, 0, st>>>(w_hwio, ci_src, co_src, dgrad_weights ? 1 : 0,
-                                                             three ? 1 : 0, w_hi, w_lo);
+  const int total = 9 * s.ci * 128;
+  prep_weights_kernel<<<ceil_div(total, 256), 256, 0, st>>>(w_hwio, ci_src, co_src, dgrad_weights ? 1 : 0, wp);
   RP_LAUNCHED();
   TcArgs a{};
   a.N = s.n;
@@ -440,31 +495,29 @@ void conv3x3_fwd_tc(const ConvShape& s, const float* in, const float* w_hwio, bo
   a.Co = s.co;
   a.Wp = p.Wp;
   a.rows_h = p.rows_h;
-  a.S = p.S;
+  a.T = p.T;
   a.units_per_img = p.units_per_img;
   a.num_units = s.n * p.units_per_img;
   a.halo_pos = p.halo_pos;
   a.nchunks = s.ci / kChunk;
   a.halo_bytes = p.halo_bytes;
-  a.w_bytes = p.w_bytes;
   a.halo_stride = p.halo_stride;
-  a.three = three ? 1 : 0;
-  a.epi = epi;
+  a.w_tap = p.w_tap;
   a.h = h;
-  a.w_hi = w_hi;
-  a.w_lo = w_lo;
+  a.w = wp;
   a.bias = bias;
   a.aux = aux;
   a.out = out;
+  a.trace = g_trace;
   const CUtensorMap& m = cached_map(in, s, p.Wp, p.rows_h);
   const int grid = std::min(a.num_units, kNumSMs);
   switch (epi) {
-    case EPI_BIAS: launch_epi<EPI_BIAS>(m, a, p.smem, grid, st); break;
-    case EPI_BIAS_TANH: launch_epi<EPI_BIAS_TANH>(m, a, p.smem, grid, st); break;
-    case EPI_RESID: launch_epi<EPI_RESID>(m, a, p.smem, grid, st); break;
-    case EPI_TANH_BWD: launch_epi<EPI_TANH_BWD>(m, a, p.smem, grid, st); break;
-    case EPI_ADD: launch_epi<EPI_ADD>(m, a, p.smem, grid, st); break;
-    default: launch_epi<EPI_SCALE>(m, a, p.smem, grid, st); break;
+    case EPI_BIAS: launch_epi<EPI_BIAS>(m, a, three, p.smem, grid, st); break;
+    case EPI_BIAS_TANH: launch_epi<EPI_BIAS_TANH>(m, a, three, p.smem, grid, st); break;
+    case EPI_RESID: launch_epi<EPI_RESID>(m, a, three, p.smem, grid, st); break;
+    case EPI_TANH_BWD: launch_epi<EPI_TANH_BWD>(m, a, three, p.smem, grid, st); break;
+    case EPI_ADD: launch_epi<EPI_ADD>(m, a, three, p.smem, grid, st); break;
+    default: launch_epi<EPI_SCALE>(m, a, three, p.smem, grid, st); break;
   }
   RP_LAUNCHED();
 }

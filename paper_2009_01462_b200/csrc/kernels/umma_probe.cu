@@ -162,3 +162,133 @@ extern "C" int rp_debug_umma_probe(const float* a, const float* b, int mode, uin
     return e.code;
   }
 }
+
+// ---------------------------------------------------------------------------
+// MMA throughput microbenchmark: every CTA issues `reps` back-to-back tcgen05.mma of
+// one configuration on fixed smem operands; cycles per MMA -> out[blockIdx.x].
+// cfg: fmt (0 f16, 1 bf16, 2 tf32), N, layout (0 interleave, 2 SW128), a/b major.
+namespace rp::k {
+namespace {
+__global__ void __launch_bounds__(128, 1) umma_bench_kernel(int fmt, int N, int layout, int a_mn, int b_mn, int reps,
+                                                            int nacc, int nops, int chain, float* out) {
+  extern __shared__ __align__(1024) uint8_t sm[];
+  __shared__ uint64_t bar;
+  __shared__ uint32_t slot;
+  const int tid = threadIdx.x;
+  for (int i = tid; i < 64 * 1024 / 4; i += 128) reinterpret_cast<uint32_t*>(sm)[i] = 0x3c003c00u;
+  if (tid == 0) {
+    umma::mbar_init(&bar, 1);
+    umma::fence_barrier_init();
+  }
+  if (tid < 32) umma::tmem_alloc<512>(&slot);
+  umma::fence_proxy_async_smem();
+  umma::tc_fence_before();
+  __syncthreads();
+  umma::tc_fence_after();
+  const uint32_t tmem = slot;
+  const int warp_u = __shfl_sync(0xffffffffu, tid / 32, 0);   // warp-uniform for the compiler
+  if (warp_u == 0) {   // whole warp runs the issue loop; one elected lane issues
+    const uint32_t a0 = umma::smem_u32(sm), b0 = umma::smem_u32(sm + 32 * 1024);
+    uint64_t da, db;
+    if (layout == 0) {  // interleave: K-major lbo = rows*16, sbo = 128
+      da = umma::desc_general(a0, 128 * 16, 128, 0, 0);
+      db = umma::desc_general(b0, N * 16, 128, 0, 0);
+    } else {            // SW128 K-major: sbo = 1024
+      da = umma::desc_general(a0, 16, 1024, layout, 0);
+      db = umma::desc_general(b0, 16, 1024, layout, 0);
+    }
+    const uint32_t id = umma::idesc(fmt, 128, N, a_mn, b_mn);
+    const uint32_t tm = __shfl_sync(0xffffffffu, tmem, 0);
+    const long long t0 = clock64();
+    if (nops == 98) {
+      // A reused by 4 MMAs (collector fill/use/use/lastuse), B rotating over 4 regions
+      for (int r = 0; r < reps; r += 4) {
+        if (umma::elect_one()) {
+          umma::mma_tf32_c<1>(tm, da, db, id, r > 0);
+          umma::mma_tf32_c<2>(tm + N, da, db + 256, id, r > 0);
+          umma::mma_tf32_c<2>(tm, da, db + 512, id, 1);
+          umma::mma_tf32_c<3>(tm + N, da, db + 768, id, 1);
+        }
+        __syncwarp();
+      }
+    } else if (nops == 97) {
+      // same pattern without the collector
+      for (int r = 0; r < reps; r += 4) {
+        if (umma::elect_one()) {
+          umma::mma_tf32(tm, da, db, id, r > 0);
+          umma::mma_tf32(tm + N, da, db + 256, id, r > 0);
+          umma::mma_tf32(tm, da, db + 512, id, 1);
+          umma::mma_tf32(tm + N, da, db + 768, id, 1);
+        }
+        __syncwarp();
+      }
+    } else if (nops == 99) {
+      // unrolled: 4 accumulators, compile-time offsets
+      for (int r = 0; r < reps; r += 4) {
+        if (umma::elect_one()) {
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            const uint32_t dq = tm + (uint32_t)((q % nacc) * N);
+            if (fmt == 2)
+              umma::mma_tf32(dq, da + q * 256, db, id, r > 0);
+            else
+              umma::mma_f16(dq, da + q * 256, db, id, r > 0);
+          }
+        }
+        __syncwarp();
+      }
+    } else {
+      int g = 0, gi = 0, op = 0;
+      for (int r = 0; r < reps; ++r) {
+        const uint32_t d = tm + (uint32_t)(g * N);
+        const uint64_t aoff = (uint64_t)(op * 256);
+        if (umma::elect_one()) {
+          if (fmt == 2)
+            umma::mma_tf32(d, da + aoff, db, id, r >= nacc * chain);
+          else
+            umma::mma_f16(d, da + aoff, db, id, r >= nacc * chain);
+        }
+        __syncwarp();
+        if (++op == nops) op = 0;
+        if (++gi == chain) {
+          gi = 0;
+          if (++g == nacc) g = 0;
+        }
+      }
+    }
+    if (umma::elect_one()) umma::mma_commit(&bar);
+    __syncwarp();
+    umma::mbar_wait(&bar, 0);
+    const long long t1 = clock64();
+    if (tid == 0) out[blockIdx.x] = (float)(t1 - t0) / reps;
+  }
+  umma::tc_fence_before();
+  __syncthreads();
+  if (tid < 32) {
+    umma::tc_fence_after();
+    umma::tmem_dealloc<512>(tmem);
+  }
+}
+}  // namespace
+}  // namespace rp::k
+
+extern "C" int rp_debug_umma_bench(int fmt, int N, int layout, int a_mn, int b_mn, int reps, int nacc, int nops,
+                                   int chain, int grid, float* out) {
+  try {
+    RP_CUDA(cudaFuncSetAttribute(rp::k::umma_bench_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024));
+    rp::k::umma_bench_kernel<<<grid, 128, 96 * 1024>>>(fmt, N, layout, a_mn, b_mn, reps, nacc, nops, chain, out);
+    RP_LAUNCHED();
+    RP_CUDA(cudaDeviceSynchronize());
+    return 0;
+  } catch (const rp::Error& e) {
+    return e.code;
+  }
+}
+
+namespace rp::k {
+void conv3x3_tc_set_trace(unsigned long long* p);
+}
+extern "C" int rp_debug_set_trace(unsigned long long* p) {
+  rp::k::conv3x3_tc_set_trace(p);
+  return 0;
+}
