@@ -16,8 +16,8 @@
 //    Consecutive MMAs share A (both operand splits of x, both tiles of a unit), which is
 //    what lets tcgen05 run at its full rate (tools/umma_bench.py: a new A every MMA
 //    costs ~40% through shared-memory operand bandwidth).
-//  * fp32 accuracy (RP_MATH_FP32, "3xTF32+"): v = hi + lo, hi = rna_tf32(v), lo = v - hi
-//    (exact).  MMA(A = [W_hi; W_lo], B = x_hi) and MMA(A, B = x_lo) accumulate all four
+//  * fp32 accuracy (RP_MATH_FP32, "3xTF32+"): v = hi + lo, hi = the tf32 truncation the
+//    tensor core applies to the raw fp32 halo, lo = v - hi (exact, written by converters).  MMA(A = [W_hi; W_lo], B = x_hi) and MMA(A, B = x_lo) accumulate all four
 //    products; the epilogue adds the hi-row and lo-row halves.  RP_MATH_TF32 drops the
 //    x_lo MMA (x enters truncated).
 //  * operands are K-major "interleaved" (no swizzle): for each group of 4 channels every
@@ -28,7 +28,7 @@
 //    TMEM, double-buffered across units); tiles past the image end are skipped.
 //  * warp roles (320 threads, persistent, 1 CTA/SM): w0 TMA producer, w1 MMA issuer
 //    (whole warp walks the loop so descriptors stay warp-uniform; one elected lane
-//    issues), w2-5 converters (halo hi/lo split), w6-9 epilogue (TMEM -> registers ->
+//    issues), w2-5 converters (halo lo part), w6-9 epilogue (TMEM -> registers ->
 //    hi+lo sum -> fused bias / tanh / skip / step-size -> coalesced NHWC stores).
 #include <cuda.h>
 
@@ -71,6 +71,11 @@ __device__ __forceinline__ float rna_tf32(float v) {
   asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(v));
   return __uint_as_float(r);
 }
+
+// The tensor core reads an fp32 operand as tf32 by dropping the low 13 mantissa bits
+// (measured: 1 + 2^-11 + 2^-12 enters as 1.0), so the raw halo already is x_hi and only
+// x_lo = x - trunc(x) (exact in fp32) has to be written.
+__device__ __forceinline__ float trunc_tf32(float v) { return __uint_as_float(__float_as_uint(v) & 0xffffe000u); }
 
 template <int EPI>
 __device__ __forceinline__ float epi_value(float acc, float bias, int64_t idx, const TcArgs& a) {
@@ -248,10 +253,9 @@ __global__ void __launch_bounds__(kThreads, 1)
           float4* lo = reinterpret_cast<float4*>(halo_lo(hs));
           for (int i = tid; i < n16; i += 128) {
             const float4 v = raw[i];
-            float4 hi, l;
-            hi.x = rna_tf32(v.x); hi.y = rna_tf32(v.y); hi.z = rna_tf32(v.z); hi.w = rna_tf32(v.w);
-            l.x = v.x - hi.x; l.y = v.y - hi.y; l.z = v.z - hi.z; l.w = v.w - hi.w;
-            raw[i] = hi;
+            float4 l;
+            l.x = v.x - trunc_tf32(v.x); l.y = v.y - trunc_tf32(v.y);
+            l.z = v.z - trunc_tf32(v.z); l.w = v.w - trunc_tf32(v.w);
             lo[i] = l;
           }
           fence_proxy_async_smem();

@@ -14,16 +14,22 @@
 // address bits (verified on device by rp_debug_umma_probe_sw32), so a tap shift of s
 // positions is simply +128*s bytes of descriptor start address with base_offset 0.
 //
-//   D[r][(tap, ci)] += sum_p A[r][p] * X_tap[ci][p]
-//     3xTF32: A = [g_hi ; g_lo] stacked along M (M = 128 for Co = 64) so one MMA per split
-//     of x (hi, lo) yields hi*hi, lo*hi, hi*lo (and lo*lo); the reduce sums the row halves.
-//     N = 32 channels of x per MMA; 9 taps in two tap groups (TMEM: 5 x 64 fp32 columns).
-//
-// Persistent CTAs (1/SM) are split between the tap groups; each accumulates a contiguous
-// range of pixel blocks in TMEM and writes one fp32 partial; a fixed-order fp64 reduce
-// combines them (deterministic: no atomics).
+// 3xTF32 by stacking both operands (the tensor core truncates fp32 to tf32, so the raw
+// tile is the hi part and only lo = v - trunc(v) is written):
+//   A = [g_hi ; g_lo]   (M = 2 Co = 128: four 32-channel slabs at a uniform stride)
+//   B = [x_hi ; x_lo]   (N = 2 Ci: 2 Ci / 32 slabs at a uniform stride)
+// so ONE M=128 x N=2Ci x K=8 MMA per (k-step, tap) yields all four products in the
+// four quadrants of D; the epilogue adds the quadrants.  The tap loop is innermost, so
+// consecutive MMAs share A (the tensor core then runs at full rate, umma_bench).
+// TMEM holds 512 fp32 columns = 512 / (2 Ci) taps, so the 9 taps are split into tap
+// groups (Ci = 64: 3 groups of 3 taps) and the persistent CTAs (1/SM) into matching CTA
+// groups; each CTA accumulates a contiguous range of pixel blocks in TMEM and writes one
+// fp32 partial [tap ci][co]; a fixed-order fp64 reduce combines them (deterministic).
+// RP_MATH_TF32 skips the lo writes (the lo slabs stay zero).
 #include <cuda.h>
 
+#include <cstdio>
+#include <cstdlib>
 #include <map>
 #include <mutex>
 #include <tuple>
@@ -39,85 +45,87 @@ namespace {
 using namespace rp::umma;
 
 constexpr int kThreads = 320;
-constexpr int kXStages = 2;
-constexpr int kMaxSmem = 220 * 1024;
-constexpr int kPad = 1024;          // zero rows around every x slab (shifted reads)
+constexpr int kMaxStages = 4;
+constexpr int kMaxSmem = 227 * 1024;
+constexpr int kLead = 128;          // zero row in front of the x slabs (tap shift -1)
+constexpr int kTrail = 1024;        // zero rows behind them (K padding reads)
+constexpr int kMaxGroups = 4;
+constexpr int kMaxTaps = 5;         // taps per group (Ci = 32: 5 + 4)
+constexpr int kConvThreads = 256;   // warps 2..9 split the lo parts / bias sums
 
 struct WgArgs {
-  int N, H, W, Ci, Co, Wp, rg, P, Pp, nchunks, rowsA, three;
-  int tg;                        // taps per group (group 1 holds the rest)
-  int ctas_g0;                   // CTAs assigned to tap group 0
+  int N, H, W, Ci, Co, Wp, rg, P, Pp, three, nstages;
+  int n2;                        // B columns per tap (2 Ci)
+  int tg;                        // taps per group (the last group may hold fewer)
+  int grp_cta[kMaxGroups + 1];   // CTA range of tap group i: [grp_cta[i], grp_cta[i+1])
   int blocks_per_img, num_blocks;
-  uint32_t slab;                 // bytes per 32-channel g slab (Pp rows of 128 B, 1 KB aligned)
-  uint32_t xb;                   // bytes per x slab body ((rg+2)*Wp rows, 1 KB aligned)
-  uint32_t g_stride;             // bytes per g slot (rowsA/32 slabs)
-  uint32_t x_stride;             // bytes per x stage (pad hi pad pad lo pad)
-  float* part;                   // [grid][rowsA][tg * Ci]
+  uint32_t g_slab;               // bytes per 32-channel g slab (Pp rows of 128 B; rows >= P stay 0)
+  uint32_t x_slab;               // bytes per x slab ((rg+2)*Wp rows of 128 B, packed)
+  uint32_t x_off;                // byte offset of x slab 0 in a stage
+  uint32_t stage;                // bytes per stage
+  float* part;                   // [grid][tg * Ci][Co]
   double* part_bias;             // [grid][Co]
+  unsigned long long* trace;     // diagnostics (tools/trace_wgrad.py), null = off
 };
 
-__device__ __forceinline__ float rna_tf32(float v) {
-  uint32_t r;
-  asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(v));
-  return __uint_as_float(r);
+// per-block timestamps of CTAs 0/1, first 64 blocks: [0] TMA issue, [1] converters see the
+// data, [2] converters done, [3] MMA warp starts the block, [4] block's MMAs issued
+#define WG_TRACE(slot, b)                                                                      \
+  do {                                                                                         \
+    if (a.trace && blockIdx.x < 2 && (b) - blk_beg < 64)                                       \
+      a.trace[(blockIdx.x * 64 + ((b) - blk_beg)) * 8 + (slot)] = globaltimer_ns();            \
+  } while (0)
+
+__device__ __forceinline__ float trunc_tf32(float v) { return __uint_as_float(__float_as_uint(v) & 0xffffe000u); }
+
+__device__ __forceinline__ float4 lo_part(float4 v) {
+  return make_float4(v.x - trunc_tf32(v.x), v.y - trunc_tf32(v.y), v.z - trunc_tf32(v.z), v.w - trunc_tf32(v.w));
 }
 
-__device__ __forceinline__ void split_inplace(float4* hi, float4* lo, int n16, int tid) {
-  for (int i = tid; i < n16; i += 128) {
-    const float4 v = hi[i];
-    float4 h, l;
-    h.x = rna_tf32(v.x); h.y = rna_tf32(v.y); h.z = rna_tf32(v.z); h.w = rna_tf32(v.w);
-    l.x = v.x - h.x; l.y = v.y - h.y; l.z = v.z - h.z; l.w = v.w - h.w;
-    hi[i] = h;
-    lo[i] = l;
-  }
-}
-
+// Shared-memory stage: [g_hi 0..1 | g_lo 0..1] (Pp rows each, 1 KB aligned) then a
+// 128-byte zero row, the x slabs [x_hi 0..nx-1 | x_lo 0..nx-1] packed back to back (a tap
+// shift reads at most one row before / seven rows after a slab; those positions meet
+// g == 0, so the neighbour slab's finite data is harmless) and a 1 KB zero tail.  TMA
+// and UMMA apply the 128B swizzle on absolute address bits, so the x slabs need only
+// 128-byte alignment.
 __global__ void __launch_bounds__(kThreads, 1)
     wgrad_tc_kernel(const __grid_constant__ CUtensorMap tmap_g, const __grid_constant__ CUtensorMap tmap_x,
                     const WgArgs a) {
   extern __shared__ __align__(1024) uint8_t smem[];
-  const int warp = threadIdx.x >> 5;
+  const int warp = __shfl_sync(0xffffffffu, (int)threadIdx.x / 32, 0);   // warp-uniform role index
   const int lane = threadIdx.x & 31;
-  const int nslab = a.rowsA / 32;
-  const int nslab_hi = a.Co / 32;
+  const int nx = a.Ci / 32;                       // x_hi slabs (as many x_lo slabs follow)
+  const int S = a.nstages;
 
-  uint8_t* g_base = smem;
-  uint8_t* x_base = smem + 2 * a.g_stride;
-  uint64_t* bars = reinterpret_cast<uint64_t*>(x_base + kXStages * a.x_stride);
-  uint64_t* g_full = bars;                // [2]
-  uint64_t* g_conv = bars + 2;            // [2]
-  uint64_t* g_empty = bars + 4;           // [2]
-  uint64_t* x_full = bars + 6;            // [kXStages]
-  uint64_t* x_conv = bars + 6 + kXStages;
-  uint64_t* x_empty = bars + 6 + 2 * kXStages;
-  uint64_t* acc_full = bars + 6 + 3 * kXStages;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 8 + 3 * kXStages);
-  double* bsum = reinterpret_cast<double*>(bars + 10 + 3 * kXStages);   // [128]
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + S * a.stage);
+  uint64_t* full = bars;                       // [S]
+  uint64_t* conv = bars + kMaxStages;
+  uint64_t* empty = bars + 2 * kMaxStages;
+  uint64_t* acc_full = bars + 3 * kMaxStages;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 3 * kMaxStages + 1);
+  double* bsum = reinterpret_cast<double*>(bars + 3 * kMaxStages + 2);   // [8 warps][64]
 
-  auto g_slab = [&](int s, int j) { return g_base + s * a.g_stride + j * a.slab; };
-  auto x_hi = [&](int s) { return x_base + s * a.x_stride + kPad; };
-  auto x_lo = [&](int s) { return x_base + s * a.x_stride + 3 * kPad + a.xb; };
+  auto g_slab = [&](int s, int j) { return smem + s * a.stage + j * a.g_slab; };
+  auto x_slab = [&](int s, int j) { return smem + s * a.stage + a.x_off + j * a.x_slab; };
 
   // CTA -> (tap group, contiguous block range)
-  const bool g0 = (int)blockIdx.x < a.ctas_g0;
-  const int jg = g0 ? blockIdx.x : blockIdx.x - a.ctas_g0;
-  const int ng = g0 ? a.ctas_g0 : gridDim.x - a.ctas_g0;
+  int gi = 0, c_lo = a.grp_cta[0], c_hi = a.grp_cta[1];
+#pragma unroll
+  for (int i = 1; i < kMaxGroups; ++i)   // static indices: no local copy of the parameter array
+    if ((int)blockIdx.x >= a.grp_cta[i] && a.grp_cta[i] < a.grp_cta[i + 1])
+      gi = i, c_lo = a.grp_cta[i], c_hi = a.grp_cta[i + 1];
+  const int jg = blockIdx.x - c_lo;
+  const int ng = c_hi - c_lo;
   const int blk_beg = (int)((int64_t)jg * a.num_blocks / ng);
   const int blk_end = (int)((int64_t)(jg + 1) * a.num_blocks / ng);
-  const int t0 = g0 ? 0 : a.tg;
-  const int ntaps = g0 ? min(a.tg, 9) : 9 - a.tg;
+  const int t0 = gi * a.tg;
+  const int ntaps = min(a.tg, 9 - t0);
 
   if (threadIdx.x == 0) {
-    for (int i = 0; i < 2; ++i) {
-      mbar_init(&g_full[i], 1);
-      mbar_init(&g_conv[i], 128);
-      mbar_init(&g_empty[i], 1);
-    }
-    for (int i = 0; i < kXStages; ++i) {
-      mbar_init(&x_full[i], 1);
-      mbar_init(&x_conv[i], 128);
-      mbar_init(&x_empty[i], 1);
+    for (int i = 0; i < S; ++i) {
+      mbar_init(&full[i], 1);
+      mbar_init(&conv[i], kConvThreads);
+      mbar_init(&empty[i], 1);
     }
     mbar_init(acc_full, 1);
     fence_barrier_init();
@@ -125,145 +133,228 @@ __global__ void __launch_bounds__(kThreads, 1)
     prefetch_tmap(&tmap_x);
   }
   if (warp == 1) tmem_alloc<512>(tmem_slot);
-  // Zero everything once: the x pads and the g rows P..Pp-1 are read (against zero g)
-  // but never written, so they must hold finite values.
+  // Zero the stages once: pads, g rows P..Pp-1 and (TF32) the lo slabs are read by the
+  // MMA but never written.
   {
     uint4* z = reinterpret_cast<uint4*>(smem);
-    const int n16 = (int)((2 * (size_t)a.g_stride + kXStages * (size_t)a.x_stride) / 16);
+    const int n16 = (int)((size_t)S * a.stage / 16);
     for (int i = threadIdx.x; i < n16; i += blockDim.x) z[i] = make_uint4(0u, 0u, 0u, 0u);
   }
   fence_proxy_async_smem();
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
-  const uint32_t tmem_base = *tmem_slot;
+  const uint32_t tmem_base = __shfl_sync(0xffffffffu, *tmem_slot, 0);
   const int Wp = a.Wp;
+  const uint32_t xrows = (uint32_t)(a.rg + 2) * Wp;
 
   if (warp == 0) {
     // ===================== TMA producer =====================
-    if (lane == 0) {
-      int gs = 0, xs = 0;
-      uint32_t gph = 0, xph = 0;
-      for (int b = blk_beg; b < blk_end; ++b) {
-        const int n = b / a.blocks_per_img;
-        const int y0 = (b % a.blocks_per_img) * a.rg;
-        mbar_wait(&g_empty[gs], gph ^ 1);
-        mbar_arrive_expect_tx(&g_full[gs], (uint32_t)nslab_hi * a.P * 128u);
-        for (int j = 0; j < nslab_hi; ++j) tma_load_4d(&tmap_g, &g_full[gs], g_slab(gs, j), 32 * j, -1, y0, n);
-        if (++gs == 2) gs = 0, gph ^= 1;
-        for (int c = 0; c < a.nchunks; ++c) {
-          mbar_wait(&x_empty[xs], xph ^ 1);
-          mbar_arrive_expect_tx(&x_full[xs], (uint32_t)(a.rg + 2) * Wp * 128u);
-          tma_load_4d(&tmap_x, &x_full[xs], x_hi(xs), 32 * c, -1, y0 - 1, n);
-          if (++xs == kXStages) xs = 0, xph ^= 1;
-        }
+    int s = 0;
+    uint32_t ph = 0;
+    const uint32_t bytes = 2u * a.P * 128u + (uint32_t)nx * xrows * 128u;
+    for (int b = blk_beg; b < blk_end; ++b) {
+      const int n = b / a.blocks_per_img;
+      const int y0 = (b - n * a.blocks_per_img) * a.rg;
+      mbar_wait(&empty[s], ph ^ 1);
+      if (elect_one()) {
+        WG_TRACE(0, b);
+        mbar_arrive_expect_tx(&full[s], bytes);
+        for (int j = 0; j < 2; ++j) tma_load_4d(&tmap_g, &full[s], g_slab(s, j), 32 * j, -1, y0, n);
+        for (int j = 0; j < nx; ++j) tma_load_4d(&tmap_x, &full[s], x_slab(s, j), 32 * j, -1, y0 - 1, n);
       }
+      __syncwarp();
+      if (++s == S) s = 0, ph ^= 1;
     }
   } else if (warp == 1) {
     // ===================== MMA issuer =====================
-    if (lane == 0) {
-      const uint32_t id = idesc(2, 128, 32, 1, 1);
-      int gs = 0, xs = 0;
-      uint32_t gph = 0, xph = 0;
-      const int ksteps = a.Pp / 8;
-      for (int b = blk_beg; b < blk_end; ++b) {
-        mbar_wait(&g_conv[gs], gph);
-        tc_fence_after();
-        const uint64_t da0 = desc_general(smem_u32(g_slab(gs, 0)), a.slab, 512, 1, 0);
-        for (int c = 0; c < a.nchunks; ++c) {
-          mbar_wait(a.three ? &x_conv[xs] : &x_full[xs], xph);
-          tc_fence_after();
-          const uint32_t xh = smem_u32(x_hi(xs)), xl = smem_u32(x_lo(xs));
-          for (int ti = 0; ti < ntaps; ++ti) {
-            const int t = t0 + ti;
-            const int shift = (t / 3) * Wp + (t % 3) - 1;
-            const uint64_t dbh0 = desc_general(xh + (uint32_t)(shift * 128), a.xb, 512, 1, 0);
-            const uint64_t dbl0 = desc_general(xl + (uint32_t)(shift * 128), a.xb, 512, 1, 0);
-            const uint32_t d = tmem_base + (uint32_t)(ti * a.Ci + c * 32);
-            for (int k = 0; k < ksteps; ++k) {
-              const uint64_t kadv = (uint64_t)(k * 64);     // 8 rows x 128 B, in 16-byte units
-              const uint32_t accum = (b > blk_beg || k > 0) ? 1u : 0u;
-              mma_tf32(d, da0 + kadv, dbh0 + kadv, id, accum);
-              if (a.three) mma_tf32(d, da0 + kadv, dbl0 + kadv, id, 1u);
+    // All offsets precomputed: the issue loop is descriptor adds + UTCHMMA only.
+    const uint32_t id = idesc(2, 128, a.n2, 1, 1);
+    const int ksteps = a.Pp / 8;
+    uint64_t boff[kMaxTaps];
+    uint32_t dcol[kMaxTaps];
+#pragma unroll
+    for (int ti = 0; ti < kMaxTaps; ++ti) {
+      const int t = min(t0 + ti, 8);
+      boff[ti] = (uint64_t)(int64_t)(((t / 3) * Wp + (t % 3) - 1) * 8);   // shift rows x 128 B / 16
+      dcol[ti] = tmem_base + (uint32_t)(ti * a.n2);
+    }
+    int s = 0;
+    uint32_t ph = 0;
+    for (int b = blk_beg; b < blk_end; ++b) {
+      mbar_wait(&conv[s], ph);
+      tc_fence_after();
+      if (lane == 0) WG_TRACE(3, b);
+      uint64_t da = desc_general(smem_u32(g_slab(s, 0)), a.g_slab, 512, 1, 0);
+      uint64_t db = desc_general(smem_u32(x_slab(s, 0)), a.x_slab, 512, 1, 0);
+      if (elect_one()) {
+        {
+          for (int k = 0; k < ksteps; ++k) {
+            const uint32_t accum = (b > blk_beg || k > 0) ? 1u : 0u;
+            // A (this k-step's g) is read into the collector once and reused by every tap
+            if (ntaps == 1) {
+              mma_tf32(dcol[0], da, db + boff[0], id, accum);
+            } else {
+              mma_tf32_c<1>(dcol[0], da, db + boff[0], id, accum);
+#pragma unroll
+              for (int ti = 1; ti < kMaxTaps; ++ti) {
+                if (ti + 1 < ntaps)
+                  mma_tf32_c<2>(dcol[ti], da, db + boff[ti], id, accum);
+                else if (ti + 1 == ntaps)
+                  mma_tf32_c<3>(dcol[ti], da, db + boff[ti], id, accum);
+              }
+            }
+            da += 64;   // next 8 positions: 8 rows x 128 B, in 16-byte units
+            db += 64;
+          }
+        }
+        mma_commit(&empty[s]);
+        WG_TRACE(4, b);
+      }
+      __syncwarp();
+      if (++s == S) s = 0, ph ^= 1;
+    }
+    if (elect_one()) mma_commit(acc_full);
+    __syncwarp();
+  } else {
+    // ===================== converters (warps 2..9): lo parts + bias sums =====================
+    const int tid = threadIdx.x - 64;
+    // float4 i = tid + 256 m of the g slabs sits in row p = i / 8 (mod Pp) with
+    // p & 3 == (tid / 8) & 3 (Pp % 8 == 0), so a thread always meets the same 4 channels of
+    // a slab (32-byte granules XOR (p & 3)); slab 0 / 1 decide which accumulator.
+    const int cb = ((((tid & 7) >> 1) ^ ((tid >> 3) & 3)) << 3) + ((tid & 1) << 2);
+    // bias: per-block fp32 sums folded into Kahan-compensated fp32 running sums (fp64
+    // arithmetic runs at a few ops/clk/SM on this part - too slow for the block loop)
+    float bs[8] = {0, 0, 0, 0, 0, 0, 0, 0}, bc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    const bool do_bias = gi == 0;
+    const bool do_lo = a.three != 0;
+    const int ng4 = a.Pp * 8;            // float4 per g slab
+    const int nx4 = nx * (int)xrows * 8; // float4 over all x_hi slabs
+    int s = 0;
+    uint32_t ph = 0;
+    for (int b = blk_beg; b < blk_end; ++b) {
+      mbar_wait(&full[s], ph);
+      if (tid == 0) WG_TRACE(1, b);
+      if (do_bias || do_lo) {
+        const float4* hi = reinterpret_cast<const float4*>(g_slab(s, 0));
+        float4* lo = reinterpret_cast<float4*>(g_slab(s, 2));
+        float bf[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+        for (int i0 = tid; i0 < 2 * ng4; i0 += 4 * kConvThreads) {
+          float4 v[4];
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            const int i = i0 + u * kConvThreads;
+            v[u] = i < 2 * ng4 ? hi[i] : make_float4(0.f, 0.f, 0.f, 0.f);
+          }
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            const int i = i0 + u * kConvThreads;
+            if (i < 2 * ng4) {
+              if (do_lo) lo[i] = lo_part(v[u]);
+              const bool s1 = i >= ng4;
+              bf[0] += s1 ? 0.f : v[u].x; bf[1] += s1 ? 0.f : v[u].y;
+              bf[2] += s1 ? 0.f : v[u].z; bf[3] += s1 ? 0.f : v[u].w;
+              bf[4] += s1 ? v[u].x : 0.f; bf[5] += s1 ? v[u].y : 0.f;
+              bf[6] += s1 ? v[u].z : 0.f; bf[7] += s1 ? v[u].w : 0.f;
             }
           }
-          mma_commit(&x_empty[xs]);
-          if (++xs == kXStages) xs = 0, xph ^= 1;
         }
-        mma_commit(&g_empty[gs]);
-        if (++gs == 2) gs = 0, gph ^= 1;
-      }
-      mma_commit(acc_full);
-    }
-  } else if (warp < 6) {
-    // ===================== converters: bias sums + 3xTF32 split =====================
-    const int tid = threadIdx.x - 64;
-    const int npar = 128 / a.Co;               // threads per bias channel (Co <= 128)
-    const int bco = tid % a.Co, bpar = tid / a.Co;
-    double bacc = 0.0;
-    int gs = 0, xs = 0;
-    uint32_t gph = 0, xph = 0;
-    for (int b = blk_beg; b < blk_end; ++b) {
-      mbar_wait(&g_full[gs], gph);
-      if (g0) {
-        // raw g element (p, co): slab co/32, row p, 32-byte granule swizzled by (p & 3)
-        const uint8_t* sl = g_slab(gs, bco / 32);
-        const int c = bco % 32;
-        for (int p = bpar; p < a.P; p += npar) {
-          const int gran = (c >> 3) ^ (p & 3);
-          bacc += (double)*reinterpret_cast<const float*>(sl + p * 128 + gran * 32 + (c & 7) * 4);
-        }
-      }
-      asm volatile("bar.sync 1, 128;" ::: "memory");   // bias reads finish before hi overwrites
-      if (a.three)
-        for (int j = 0; j < nslab_hi; ++j)
-          split_inplace(reinterpret_cast<float4*>(g_slab(gs, j)), reinterpret_cast<float4*>(g_slab(gs, nslab_hi + j)),
-                        a.P * 8, tid);
-      fence_proxy_async_smem();
-      mbar_arrive(&g_conv[gs]);
-      if (++gs == 2) gs = 0, gph ^= 1;
-      if (a.three) {
-        for (int c = 0; c < a.nchunks; ++c) {
-          mbar_wait(&x_full[xs], xph);
-          split_inplace(reinterpret_cast<float4*>(x_hi(xs)), reinterpret_cast<float4*>(x_lo(xs)),
-                        (a.rg + 2) * Wp * 8, tid);
-          fence_proxy_async_smem();
-          mbar_arrive(&x_conv[xs]);
-          if (++xs == kXStages) xs = 0, xph ^= 1;
-        }
-      }
-    }
-    if (g0) {
-      bsum[tid] = bacc;
-      asm volatile("bar.sync 1, 128;" ::: "memory");
-      if (tid < a.Co) {
-        double s = 0.0;
-        for (int k = 0; k < npar; ++k) s += bsum[tid + k * a.Co];
-        a.part_bias[(size_t)blockIdx.x * a.Co + tid] = s;
-      }
-    }
-    (void)nslab;
-  } else {
-    // ===================== epilogue: TMEM accumulator -> fp32 partial =====================
-    const int q = warp & 3;
-    const int row = q * 32 + lane;
-    const int cols = ntaps * a.Ci;
-    float* dst = a.part + ((size_t)blockIdx.x * a.rowsA + row) * (size_t)(a.tg * a.Ci);
-    const bool any = blk_end > blk_beg;
-    if (any) {
-      mbar_wait(acc_full, 0);
-      tc_fence_after();
-    }
-    for (int cc = 0; cc < cols; cc += 16) {
-      uint32_t r[16];
-      tmem_ld16(tmem_base + ((uint32_t)(q * 32) << 16) + (uint32_t)cc, r);
-      tmem_wait_ld();
-      float4* d4 = reinterpret_cast<float4*>(dst + cc);
+        if (do_bias) {
 #pragma unroll
-      for (int v = 0; v < 4; ++v)
-        d4[v] = any ? make_float4(__uint_as_float(r[4 * v]), __uint_as_float(r[4 * v + 1]),
-                                  __uint_as_float(r[4 * v + 2]), __uint_as_float(r[4 * v + 3]))
-                    : make_float4(0.f, 0.f, 0.f, 0.f);
+          for (int e = 0; e < 8; ++e) {
+            const float y = bf[e] - bc[e];
+            const float t = bs[e] + y;
+            bc[e] = (t - bs[e]) - y;
+            bs[e] = t;
+          }
+        }
+      }
+      if (do_lo) {
+        const float4* hi = reinterpret_cast<const float4*>(x_slab(s, 0));
+        float4* lo = reinterpret_cast<float4*>(x_slab(s, nx));
+        for (int i0 = tid; i0 < nx4; i0 += 4 * kConvThreads) {
+          float4 v[4];
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            const int i = i0 + u * kConvThreads;
+            if (i < nx4) v[u] = hi[i];
+          }
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            const int i = i0 + u * kConvThreads;
+            if (i < nx4) lo[i] = lo_part(v[u]);
+          }
+        }
+      }
+      fence_proxy_async_smem();
+      if (tid == 0) WG_TRACE(2, b);
+      mbar_arrive(&conv[s]);
+      if (++s == S) s = 0, ph ^= 1;
+    }
+    const int cw = tid / 32;   // converter warp 0..7
+    if (gi == 0) {
+      // lanes l, l^10, l^20, l^30 hold the same channels: fixed-order butterfly, then lanes
+      // 0..7 (rows p & 3 == 0) publish the warp's 64 sums.
+      double bd[8];
+#pragma unroll
+      for (int e = 0; e < 8; ++e) {
+        bd[e] = (double)bs[e] - (double)bc[e];
+        bd[e] += __shfl_xor_sync(0xffffffffu, bd[e], 10);
+        bd[e] += __shfl_xor_sync(0xffffffffu, bd[e], 20);
+      }
+      if (lane < 8) {
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          bsum[cw * 64 + cb + e] = bd[e];
+          bsum[cw * 64 + 32 + cb + e] = bd[4 + e];
+        }
+      }
+      asm volatile("bar.sync 1, 256;" ::: "memory");
+      if (tid < 64) {
+        double t = 0.0;
+        for (int w = 0; w < 8; ++w) t += bsum[w * 64 + tid];
+        a.part_bias[(size_t)blockIdx.x * 64 + tid] = t;
+      }
+    }
+    if (warp >= 6) {
+      // ===================== epilogue: D quadrants -> fp32 partial [tap ci][co] =====================
+      // TMEM lane r: r < 64 -> g_hi row co = r, r >= 64 -> g_lo row co = r - 64; columns
+      // [ti n2, ti n2 + Ci) x_hi, [ti n2 + Ci, (ti+1) n2) x_lo.  Warps on lanes 64..127 park
+      // their (hi + lo column) sums in the drained stage memory; the other two add theirs
+      // and store coalesced rows of 64 output channels.
+      const int q = warp & 3;
+      const int co = (q & 1) * 32 + lane;
+      float* xbuf = reinterpret_cast<float*>(smem);     // [tg * Ci][64], reuses stage memory
+      float* dst = a.part + (size_t)blockIdx.x * a.tg * a.Ci * 64;
+      const bool any = blk_end > blk_beg;
+      if (any) {
+        mbar_wait(acc_full, 0);
+        tc_fence_after();
+      }
+      const uint32_t trow = tmem_base + ((uint32_t)(q * 32) << 16);
+      for (int pass = 0; pass < 2; ++pass) {
+        const bool mine = (pass == 0) == (q >= 2);
+        if (mine) {
+          for (int ti = 0; ti < ntaps; ++ti) {
+            for (int c = 0; c < a.Ci; c += 16) {
+              uint32_t rh[16], rl[16];
+              tmem_ld16(trow + (uint32_t)(ti * a.n2 + c), rh);
+              tmem_ld16(trow + (uint32_t)(ti * a.n2 + a.Ci + c), rl);
+              tmem_wait_ld();
+              const int col0 = ti * a.Ci + c;
+#pragma unroll
+              for (int e = 0; e < 16; ++e) {
+                const float v = any ? __uint_as_float(rh[e]) + __uint_as_float(rl[e]) : 0.f;
+                if (q >= 2)
+                  xbuf[(col0 + e) * 64 + co] = v;
+                else
+                  dst[(size_t)(col0 + e) * 64 + co] = v + xbuf[(col0 + e) * 64 + co];
+              }
+            }
+          }
+        }
+        asm volatile("bar.sync 2, 128;" ::: "memory");
+      }
     }
   }
 
@@ -275,33 +366,30 @@ __global__ void __launch_bounds__(kThreads, 1)
   }
 }
 
-// gW[tap][ci][co] (HWIO) = scale * sum over the tap group's CTAs of D[co][col] (+ D[Co+co][col])
-__global__ void wgrad_reduce_kernel(const float* __restrict__ part, const double* __restrict__ part_bias, int grid,
-                                    int ctas_g0, int tg, int Ci, int Co, int rowsA, int three, double scale,
-                                    float* __restrict__ gw, float* __restrict__ gb) {
+// gW[tap][ci][co] (HWIO) = scale * sum over the tap group's CTAs of part[cta][ti ci][co]
+__global__ void wgrad_reduce_kernel(const float* __restrict__ part, const double* __restrict__ part_bias,
+                                    const WgArgs a, double scale, float* __restrict__ gw, float* __restrict__ gb) {
+  const int Ci = a.Ci, Co = 64;
   const int total = 9 * Ci * Co;
-  const int64_t pstride = (int64_t)rowsA * tg * Ci;
+  const int64_t pstride = (int64_t)a.tg * Ci * Co;
   for (int idx = blockIdx.x * blockDim.x + threadIdx.x; idx < total + Co; idx += gridDim.x * blockDim.x) {
     if (idx < total) {
       const int co = idx % Co;
       const int ci = (idx / Co) % Ci;
       const int tap = idx / (Co * Ci);
-      const bool grp0 = tap < tg;
-      const int ti = grp0 ? tap : tap - tg;
-      const int b0 = grp0 ? 0 : ctas_g0;
-      const int b1 = grp0 ? ctas_g0 : grid;
-      const int64_t col = (int64_t)ti * Ci + ci;
+      const int gi = tap / a.tg;
+      int c_lo = a.grp_cta[0], c_hi = a.grp_cta[1];
+#pragma unroll
+      for (int i = 1; i < kMaxGroups; ++i)
+        if (gi == i) c_lo = a.grp_cta[i], c_hi = a.grp_cta[i + 1];
+      const int64_t off = ((int64_t)(tap - gi * a.tg) * Ci + ci) * Co + co;
       double s = 0.0;
-      for (int b = b0; b < b1; ++b) {
-        const float* p = part + b * pstride;
-        s += (double)p[(int64_t)co * tg * Ci + col];
-        if (three) s += (double)p[(int64_t)(Co + co) * tg * Ci + col];
-      }
+      for (int b = c_lo; b < c_hi; ++b) s += (double)part[b * pstride + off];
       gw[idx] = (float)(scale * s);
     } else if (gb) {
       const int co = idx - total;
       double s = 0.0;
-      for (int b = 0; b < ctas_g0; ++b) s += part_bias[(int64_t)b * Co + co];
+      for (int b = a.grp_cta[0]; b < a.grp_cta[1]; ++b) s += part_bias[(int64_t)b * Co + co];
       gb[co] = (float)(scale * s);
     }
   }
@@ -358,47 +446,64 @@ uint32_t round1k(uint64_t v) { return (uint32_t)((v + 1023) / 1024 * 1024); }
 
 struct WgPlan {
   bool ok = false;
-  int rg, P, Pp, tg, ctas_g0, grid, rowsA;
-  uint32_t slab, xb, g_stride, x_stride;
+  int rg, P, Pp, tg, ngroups, grid, nstages;
+  uint32_t g_slab, x_slab, x_off, stage;
   size_t smem;
 };
 
 WgPlan plan(const ConvShape& s, bool three) {
+  (void)three;
   WgPlan p;
-  p.rowsA = (three ? 2 : 1) * s.co;
-  if (p.rowsA != 128 || s.ci % 32 != 0 || s.co % 32 != 0 || s.w + 2 > 256) return p;
+  if (s.co != 64 || (s.ci != 32 && s.ci != 64) || s.w + 2 > 256) return p;
   const int Wp = s.w + 2;
-  const int ngroups = (9 * s.ci + 511) / 512;
-  if (ngroups > 2) return p;
-  p.tg = (9 + ngroups - 1) / ngroups;
-  // largest block (whole padded rows) whose double-buffered g and x stages fit
-  for (int rg = std::min(s.h, 8); rg >= 1; --rg) {
+  const int n2 = 2 * s.ci;
+  const int tg_max = 512 / n2;
+  p.ngroups = (9 + tg_max - 1) / tg_max;
+  p.tg = (9 + p.ngroups - 1) / p.ngroups;
+  // (rows per block, stages) in order of preference; RP_WGRAD_CFG="rg,stages" overrides
+  int cand[6][2] = {{2, 2}, {1, 3}, {1, 2}, {0, 0}, {0, 0}, {0, 0}};
+  if (const char* e = getenv("RP_WGRAD_CFG")) {
+    int r = 0, st = 0;
+    if (sscanf(e, "%d,%d", &r, &st) == 2) cand[0][0] = r, cand[0][1] = st;
+  }
+  for (auto& c : cand) {
+    const int rg = std::min(c[0], s.h), st = c[1];
+    if (rg < 1 || st < 2 || st > kMaxStages) continue;
     WgPlan q = p;
     q.rg = rg;
+    q.nstages = st;
     q.P = rg * Wp;
     q.Pp = (q.P + 7) / 8 * 8;
-    q.slab = round1k((uint64_t)q.Pp * 128);
-    q.xb = round1k((uint64_t)(rg + 2) * Wp * 128 + (q.Pp - q.P) * 128);
-    q.g_stride = (uint32_t)(q.rowsA / 32) * q.slab;
-    q.x_stride = 2 * (kPad + q.xb + kPad);
-    q.smem = 2 * (size_t)q.g_stride + kXStages * (size_t)q.x_stride + 2048 + 1024;
-    if (q.smem > (size_t)kMaxSmem || q.rg + 2 > 256) continue;
+    q.g_slab = (uint32_t)q.Pp * 128u;
+    q.x_slab = (uint32_t)(rg + 2) * Wp * 128u;
+    q.x_off = 4 * q.g_slab + kLead;
+    q.stage = round1k((uint64_t)q.x_off + (uint64_t)(n2 / 32) * q.x_slab + kTrail);
+    q.smem = st * (size_t)q.stage + (3 * kMaxStages + 2) * 8 + 8 * 64 * 8;
+    if (q.smem > (size_t)kMaxSmem) continue;
+    if ((size_t)q.tg * s.ci * 64 * 4 > st * (size_t)q.stage) continue;   // epilogue exchange
     q.grid = kNumSMs;
-    q.ctas_g0 = ngroups == 1 ? q.grid : (int)((int64_t)q.grid * q.tg / 9);
     q.ok = true;
     return q;
   }
   return p;
 }
 
+unsigned long long* g_trace = nullptr;
+
+int64_t part_bytes(const WgPlan& p, const ConvShape& s) {
+  return ((int64_t)p.grid * p.tg * s.ci * 64 * 4 + 255) / 256 * 256;
+}
+
 }  // namespace
+
+void conv3x3_wgrad_tc_set_trace(unsigned long long* p) { g_trace = p; }
 
 bool conv3x3_wgrad_tc_supported(const ConvShape& s, bool three) { return plan(s, three).ok; }
 
 int64_t conv3x3_wgrad_tc_ws_bytes(const ConvShape& s, bool three) {
   const WgPlan p = plan(s, three);
   if (!p.ok) return 0;
-  return ((int64_t)p.grid * p.rowsA * p.tg * s.ci * 4 + 255) / 256 * 256 + (int64_t)p.grid * s.co * 8 + 256;
+  return part_bytes(p, s) + (int64_t)p.grid * 64 * 8 + 256;
 }
 
 void conv3x3_wgrad_tc(const ConvShape& s, const float* in, const float* g, float scale, float* gw, float* gb,
@@ -415,20 +520,24 @@ void conv3x3_wgrad_tc(const ConvShape& s, const float* in, const float* g, float
   a.rg = p.rg;
   a.P = p.P;
   a.Pp = p.Pp;
-  a.nchunks = s.ci / 32;
-  a.rowsA = p.rowsA;
   a.three = three ? 1 : 0;
+  a.n2 = 2 * s.ci;
   a.tg = p.tg;
-  a.ctas_g0 = p.ctas_g0;
+  int taps_before = 0;
+  for (int i = 0; i <= kMaxGroups; ++i) {
+    a.grp_cta[i] = (int)((int64_t)p.grid * taps_before / 9);
+    taps_before = std::min(9, taps_before + (i < p.ngroups ? p.tg : 0));
+  }
   a.blocks_per_img = (s.h + p.rg - 1) / p.rg;
   a.num_blocks = s.n * a.blocks_per_img;
-  a.slab = p.slab;
-  a.xb = p.xb;
-  a.g_stride = p.g_stride;
-  a.x_stride = p.x_stride;
+  a.nstages = p.nstages;
+  a.g_slab = p.g_slab;
+  a.x_slab = p.x_slab;
+  a.x_off = p.x_off;
+  a.stage = p.stage;
+  a.trace = g_trace;
   a.part = static_cast<float*>(ws);
-  a.part_bias = reinterpret_cast<double*>(static_cast<char*>(ws) +
-                                          ((int64_t)p.grid * p.rowsA * p.tg * s.ci * 4 + 255) / 256 * 256);
+  a.part_bias = reinterpret_cast<double*>(static_cast<char*>(ws) + part_bytes(p, s));
   const CUtensorMap& mg = cached(g, s.n, s.h, s.w, s.co, p.rg);
   const CUtensorMap& mx = cached(in, s.n, s.h, s.w, s.ci, p.rg + 2);
   static bool configured = false;
@@ -439,8 +548,7 @@ void conv3x3_wgrad_tc(const ConvShape& s, const float* in, const float* g, float
   wgrad_tc_kernel<<<p.grid, kThreads, p.smem, st>>>(mg, mx, a);
   RP_LAUNCHED();
   const int total = 9 * s.ci * s.co + s.co;
-  wgrad_reduce_kernel<<<ceil_div(total, 256), 256, 0, st>>>(a.part, a.part_bias, p.grid, p.ctas_g0, p.tg, s.ci,
-                                                            s.co, p.rowsA, a.three, (double)scale, gw, gb);
+  wgrad_reduce_kernel<<<ceil_div(total, 256), 256, 0, st>>>(a.part, a.part_bias, a, (double)scale, gw, gb);
   RP_LAUNCHED();
 }
 

@@ -175,7 +175,17 @@ __global__ void __launch_bounds__(128, 1) umma_bench_kernel(int fmt, int N, int 
   __shared__ uint64_t bar;
   __shared__ uint32_t slot;
   const int tid = threadIdx.x;
-  for (int i = tid; i < 64 * 1024 / 4; i += 128) reinterpret_cast<uint32_t*>(sm)[i] = 0x3c003c00u;
+  for (int i = tid; i < 192 * 1024 / 4; i += 128) {
+    uint32_t v = 0x3c003c00u;
+    if (b_mn == 2) {   // pseudo-random finite fp32 in [1, 2) with random sign / mantissa
+      uint32_t h = (uint32_t)i * 2654435761u;
+      h ^= h >> 15;
+      h *= 2246822519u;
+      h ^= h >> 13;
+      v = 0x3f800000u | (h & 0x807fffffu);
+    }
+    reinterpret_cast<uint32_t*>(sm)[i] = v;
+  }
   if (tid == 0) {
     umma::mbar_init(&bar, 1);
     umma::fence_barrier_init();
@@ -193,6 +203,12 @@ __global__ void __launch_bounds__(128, 1) umma_bench_kernel(int fmt, int N, int 
     if (layout == 0) {  // interleave: K-major lbo = rows*16, sbo = 128
       da = umma::desc_general(a0, 128 * 16, 128, 0, 0);
       db = umma::desc_general(b0, N * 16, 128, 0, 0);
+    } else if (layout == 1 && a_mn) {   // SW128_32B MN-major: 32-element groups 8 KB apart
+      da = umma::desc_general(a0, 8192, 512, 1, 0);
+      db = umma::desc_general(b0, 8192, 512, 1, 0);
+    } else if (layout == 3) {            // as layout 1 with the wgrad kernel's slab strides
+      da = umma::desc_general(a0, 9216, 512, 1, 0);
+      db = umma::desc_general(umma::smem_u32(sm + 40 * 1024) + 1024, 18432, 512, 1, 0);
     } else {            // SW128 K-major: sbo = 1024
       da = umma::desc_general(a0, 16, 1024, layout, 0);
       db = umma::desc_general(b0, 16, 1024, layout, 0);
@@ -208,6 +224,80 @@ __global__ void __launch_bounds__(128, 1) umma_bench_kernel(int fmt, int N, int 
           umma::mma_tf32_c<2>(tm + N, da, db + 256, id, r > 0);
           umma::mma_tf32_c<2>(tm, da, db + 512, id, 1);
           umma::mma_tf32_c<3>(tm + N, da, db + 768, id, 1);
+        }
+        __syncwarp();
+      }
+    } else if (nops == 93) {
+      // 94 without the k-step advance (B offsets fixed per tap)
+      for (int r = 0; r < reps; r += nacc) {
+        if (umma::elect_one()) {
+          for (int t = 0; t < nacc; ++t)
+            umma::mma_tf32(tm + (uint32_t)(t * N), da, db + (uint64_t)(t * chain * 8), id, r > 0);
+        }
+        __syncwarp();
+      }
+    } else if (nops == 92) {
+      // 95 with the whole loop inside one elected lane (as wgrad issues)
+      if (umma::elect_one()) {
+        int k = 0;
+        for (int r = 0; r < reps; r += nacc) {
+          const uint64_t kadv = (uint64_t)(k * 64);
+          for (int t = 0; t < nacc; ++t)
+            umma::mma_tf32(tm + (uint32_t)(t * N), da + kadv, db + kadv + (uint64_t)(t * chain * 8), id, r > 0);
+          if (++k == 3) k = 0;
+        }
+      }
+      __syncwarp();
+    } else if (nops == 90) {
+      // 92 with the A collector: fill on the first tap of a k-step, use, lastuse on the last
+      if (umma::elect_one()) {
+        int k = 0;
+        for (int r = 0; r < reps; r += nacc) {
+          const uint64_t kadv = (uint64_t)(k * 64);
+          const uint64_t a_k = da + kadv;
+          umma::mma_tf32_c<1>(tm, a_k, db + kadv, id, r > 0);
+          for (int t = 1; t + 1 < nacc; ++t)
+            umma::mma_tf32_c<2>(tm + (uint32_t)(t * N), a_k, db + kadv + (uint64_t)(t * chain * 8), id, r > 0);
+          umma::mma_tf32_c<3>(tm + (uint32_t)((nacc - 1) * N), a_k, db + kadv + (uint64_t)((nacc - 1) * chain * 8),
+                              id, r > 0);
+          if (++k == 3) k = 0;
+        }
+      }
+      __syncwarp();
+    } else if (nops == 91) {
+      // 95 with the k-step advance applied to A only
+      int k = 0;
+      for (int r = 0; r < reps; r += nacc) {
+        const uint64_t kadv = (uint64_t)(k * 64);
+        if (umma::elect_one()) {
+          for (int t = 0; t < nacc; ++t)
+            umma::mma_tf32(tm + (uint32_t)(t * N), da + kadv, db + (uint64_t)(t * chain * 8), id, r > 0);
+        }
+        __syncwarp();
+        if (++k == 3) k = 0;
+      }
+    } else if (nops == 95 || nops == 94) {
+      // wgrad pattern: per k-step (A advances 8 rows = 64 units; 94: A fixed) nacc taps,
+      // B = k-step + tap shift of t * chain rows, accumulator t
+      int k = 0;
+      for (int r = 0; r < reps; r += nacc) {
+        const uint64_t kadv = (uint64_t)(k * 64);
+        if (umma::elect_one()) {
+          for (int t = 0; t < nacc; ++t)
+            umma::mma_tf32(tm + (uint32_t)(t * N), nops == 95 ? da + kadv : da, db + kadv + (uint64_t)(t * chain * 8),
+                           id, r > 0);
+        }
+        __syncwarp();
+        if (++k == 3) k = 0;
+      }
+    } else if (nops == 96) {
+      // A same, B rotating over start offsets 0, chain, 2 chain, 3 chain (16-byte units)
+      for (int r = 0; r < reps; r += 4) {
+        if (umma::elect_one()) {
+          umma::mma_tf32(tm, da, db, id, r > 0);
+          umma::mma_tf32(tm + N, da, db + (uint64_t)chain, id, r > 0);
+          umma::mma_tf32(tm + 2 * N, da, db + (uint64_t)(2 * chain), id, r > 0);
+          umma::mma_tf32(tm, da, db + (uint64_t)(3 * chain), id, 1);
         }
         __syncwarp();
       }
@@ -275,8 +365,8 @@ __global__ void __launch_bounds__(128, 1) umma_bench_kernel(int fmt, int N, int 
 extern "C" int rp_debug_umma_bench(int fmt, int N, int layout, int a_mn, int b_mn, int reps, int nacc, int nops,
                                    int chain, int grid, float* out) {
   try {
-    RP_CUDA(cudaFuncSetAttribute(rp::k::umma_bench_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024));
-    rp::k::umma_bench_kernel<<<grid, 128, 96 * 1024>>>(fmt, N, layout, a_mn, b_mn, reps, nacc, nops, chain, out);
+    RP_CUDA(cudaFuncSetAttribute(rp::k::umma_bench_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 192 * 1024));
+    rp::k::umma_bench_kernel<<<grid, 128, 192 * 1024>>>(fmt, N, layout, a_mn, b_mn, reps, nacc, nops, chain, out);
     RP_LAUNCHED();
     RP_CUDA(cudaDeviceSynchronize());
     return 0;
@@ -287,8 +377,10 @@ extern "C" int rp_debug_umma_bench(int fmt, int N, int layout, int a_mn, int b_m
 
 namespace rp::k {
 void conv3x3_tc_set_trace(unsigned long long* p);
+void conv3x3_wgrad_tc_set_trace(unsigned long long* p);
 }
 extern "C" int rp_debug_set_trace(unsigned long long* p) {
   rp::k::conv3x3_tc_set_trace(p);
+  rp::k::conv3x3_wgrad_tc_set_trace(p);
   return 0;
 }
