@@ -216,6 +216,82 @@ def run_ours(args, cfg, rank, world):
                 B=B, K=K, g=g)
 
 
+def run_ours_distributed(args, cfg, rank, world):
+    """N > 1: one process per GPU, stage k of the K-stage pipeline on rank floor(k G / K)
+    (paper_2009_01462_b200/distributed.py); N > K runs N / K pipeline replicas, each on
+    its own synthetic batch.  Neighbour exchange over NCCL point-to-point."""
+    import torch
+    import torch.distributed as dist
+    import paper_2009_01462_b200 as rp
+    from paper_2009_01462_b200._lib import lib
+    from paper_2009_01462_b200.distributed import CudaStageEngine, DistributedDecoupledTrainer, placement
+
+    dev = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(dev)
+    g = rp.Geometry(cfg["cin"], cfg["h"], cfg["w"], cfg["c"], cfg["ch"], cfg["L"], CLASSES)
+    B, K = cfg["B"], cfg["K"]
+    if cfg["mode"] == "serial":
+        raise SystemExit("bench: the serial config runs on one GPU (K = 1)")
+    mode = {"alm": rp.ALM, "penalty": rp.PENALTY}[cfg["mode"]]
+    plc = placement(K, world, rank)
+    eng = CudaStageEngine(g, K, mode, rp.SQUARED_L2, B, plc.lo, plc.hi, dev, seed_state=_splitmix(1),
+                          math=args.math or cfg["math"])
+    tr = DistributedDecoupledTrainer(eng, plc)
+    x = torch.empty(B * g.raw_size, dtype=torch.float32, device="cuda")
+    st = C.c_uint64(1000 + plc.replica)
+    rp.check(lib().rp_op_fill_uniform(C.c_void_p(x.data_ptr()), x.numel(), C.byref(st), -1.0, 1.0, 1.0, None))
+    gen = torch.Generator(device="cuda")
+    gen.manual_seed(7 + plc.replica)
+    y = torch.randint(0, CLASSES, (B,), dtype=torch.int32, device="cuda", generator=gen)
+    torch.cuda.synchronize()
+    tr.reset_lambda_from_forward(x.data_ptr(), B)
+    sp = step_params(cfg)
+    xp = x.data_ptr() if plc.first else None
+    yp = y.data_ptr() if plc.last else None
+    for _ in range(args.warmup):
+        tr.step(xp, yp, B, 0, sp)
+    torch.cuda.synchronize()
+    dist.barrier()
+    torch.cuda.synchronize()
+    clocks = ClockSampler(dev)
+    clocks.start()
+    lib().rp_profile_enable(1)
+    profile_classes()
+    n0 = rp.launch_count()
+    eng.region(0)
+    for _ in range(args.steps):
+        tr.step(xp, yp, B, 0, sp)
+    total_ms = eng.region(1)
+    torch.cuda.synchronize()
+    launches = rp.launch_count() - n0
+    lib().rp_profile_enable(0)
+    prof = profile_classes()
+    clk = clocks.stop()
+    t = torch.tensor([total_ms], device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    total_ms = float(t.item())
+    loss = tr.loss()
+
+    # e2e: pinned host batch -> device (stage 0 rank: pixels, last-stage rank: labels), the
+    # step, the loss read back on every rank; wall clock, max over ranks
+    x_host = x.cpu().pin_memory()
+    y_host = y.cpu().pin_memory()
+    e2e_steps = max(1, min(args.steps, 10))
+    dist.barrier()
+    t0 = time.perf_counter()
+    for _ in range(e2e_steps):
+        if plc.first:
+            x.copy_(x_host, non_blocking=True)
+        if plc.last:
+            y.copy_(y_host, non_blocking=True)
+        torch.cuda.current_stream().synchronize()
+        tr.step(xp, yp, B, 0, sp, read_loss=True)
+    e2e_s = torch.tensor([(time.perf_counter() - t0) / e2e_steps], device="cuda")
+    dist.all_reduce(e2e_s, op=dist.ReduceOp.MAX)
+    return dict(tr=tr, total_ms=total_ms, prof=prof, clocks=clk, launches=launches, loss=loss,
+                e2e_s=float(e2e_s.item()), B=B, K=K, g=g, replicas=plc.replicas, plc=plc)
+
+
 def _splitmix(seed):
     """Rng(seed).split().state == Rng(seed).next_u64() (tensor.cpp:163-175)."""
     M = (1 << 64) - 1
@@ -295,6 +371,8 @@ def main():
     ap.add_argument("--ref-images", type=int, default=2)
     ap.add_argument("--cpu-images", type=int, default=4)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--dist-path", action="store_true",
+                    help="run the one-process-per-GPU stage-sharded path even at N=1 (smoke of the N>1 code)")
     args = ap.parse_args()
     cfg = dict(CONFIGS[args.config])
     if args.math:
@@ -306,18 +384,23 @@ def main():
         run_reference(args, cfg, rank, world)
         return
 
-    if world > 1:
+    distributed = world > 1 or args.dist_path
+    if distributed:
         import torch
         import torch.distributed as dist
         torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", "0")))
-        dist.init_process_group("nccl")
+        if not dist.is_initialized():
+            os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+            os.environ.setdefault("MASTER_PORT", "29517")
+            dist.init_process_group("nccl", rank=rank, world_size=world)
 
-    r = run_ours(args, cfg, rank, world)
+    r = run_ours_distributed(args, cfg, rank, world) if distributed else run_ours(args, cfg, rank, world)
     if rank != 0:
         return
     B, K = r["B"], r["K"]
+    replicas = r.get("replicas", 1)
     total_s = r["total_ms"] / 1e3
-    value = world * B * args.steps / total_s   # replicas: every rank ran B images per step
+    value = replicas * B * args.steps / total_s   # every pipeline replica ran B images per step
     peaks, peaks_kind = measured_peaks()
     prof = r["prof"]
     convs = {k: v for k, v in prof.items() if k.startswith("conv_")}
@@ -347,15 +430,18 @@ def main():
     line = {
         "metric": METRIC, "value": value, "unit": "images/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": r["total_ms"] / args.steps, "higher_is_better": True,
-        "scaling": "weak" if world > 1 else "strong", "vs_baseline": None,
+        # N <= K: one pipeline, the same batch spread over more GPUs; N > K: replicas
+        "scaling": "weak" if world > K else "strong", "vs_baseline": None,
         "dtype": "bf16" if cfg["math"] == "bf16" else "f32", "data": "synthetic",
         "config": {"workload": f"{args.config}: ODE-ResNet {cfg['cin']}x{cfg['h']}x{cfg['w']}, batch {B}, "
                                f"C={cfg['c']}, L={cfg['L']}, K={K} stages, {cfg['mode']}, math {cfg['math']}",
-                   **_cfg_json(cfg), "parallelism": f"{K} stages on {world} GPU(s)"
-                   + (" (replicas per GPU)" if world > 1 else ""),
+                   **_cfg_json(cfg),
+                   "parallelism": f"{K} stages on {min(world, K)} GPU(s) (stage k on rank floor(k G / K), NCCL "
+                                  f"point-to-point neighbour exchange)" + (f" x {replicas} replicas" if replicas > 1
+                                                                           else ""),
                    "l2": "inputs larger than L2 (per-iteration working set > 2 GB)",
                    "model_flops_per_iter": flops_iter,
-                   "model_tflops": flops_iter * args.steps / total_s / 1e12 / world},
+                   "model_tflops": flops_iter * replicas * args.steps / total_s / 1e12},
         # the reference's ALM update (kappa_lr 1e-9, lambda_lr 0.1) diverges on this synthetic
         # batch after ~10 iterations - the reference itself does the same (tools/ref_loss_curve.py);
         # a non-finite value is reported as null so the line stays valid JSON
@@ -363,8 +449,9 @@ def main():
         "clocks": r["clocks"],
         "gpu_launches": r["launches"],
         "roofline": roof,
-        "e2e": {"value": B / r["e2e_s"], "unit": "images/s",
-                "h2d_bytes_per_step": B * r["g"].raw_size * 4 + B * 4, "d2h_bytes_per_step": 8},
+        "e2e": {"value": replicas * B / r["e2e_s"], "unit": "images/s",
+                "h2d_bytes_per_step": replicas * (B * r["g"].raw_size * 4 + B * 4),
+                "d2h_bytes_per_step": 8 * world},
     }
     if not args.no_cpu_baseline:
         try:
@@ -381,5 +468,17 @@ def main():
     print(json.dumps(line))
 
 
+def _shutdown():
+    try:
+        import torch.distributed as dist
+        if dist.is_available() and dist.is_initialized():
+            dist.destroy_process_group()
+    except Exception:
+        pass
+
+
 if __name__ == "__main__":
-    main()
+    try:
+        main()
+    finally:
+        _shutdown()

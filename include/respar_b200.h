@@ -203,6 +203,34 @@ int rp_trainer_create(const rp_geometry* g, int32_t stages, int32_t mode, int32_
                       int32_t num_samples, const float* params_host, uint64_t* seed_state,
                       int32_t math, const int32_t* devices, int32_t ndev, rp_trainer** out);
 int rp_trainer_destroy(rp_trainer* t);
+
+/* ---- stage-sharded trainer (one process per GPU) -----------------
+ * Holds stages [stage_lo, stage_hi) of the K-stage net on `device`, plus -- when
+ * stage_hi < K -- a ghost of stage stage_hi (lambda, kappa, received p) because the
+ * holder of stage k-1 corrects boundary k.  One iteration on rank r
+ * (paper_2009_01462_b200/distributed.py):
+ *   rp_trainer_step_local            parallel phase + inner-boundary corrections
+ *   send p_{stage_lo} to rank r-1 || receive p_{stage_hi} into the ghost's adjoint
+ *   rp_trainer_correct_ghost         correct_aux / correct_multiplier of boundary stage_hi
+ *   send the ghost's lambda to rank r+1 || receive lambda_{stage_lo} from rank r-1
+ * The exchanges are NCCL point-to-point on rp_trainer_stage_stream(k) streams; no
+ * collective touches the data path (the parameters are disjoint per stage).
+ * Replaces the in-process StagePool (runtime.hpp:33-67) for multi-GPU runs. */
+int rp_trainer_create_local(const rp_geometry* g, int32_t stages, int32_t mode, int32_t penalty, int32_t num_samples,
+                            const float* params_host, uint64_t* seed_state, int32_t math, int32_t device,
+                            int32_t stage_lo, int32_t stage_hi, rp_trainer** out);
+int rp_trainer_local_range(rp_trainer* t, int32_t* stage_lo, int32_t* stage_hi);
+/* reset_lambda_from_forward over the local stages: x_dev = raw inputs of all samples
+ * (stage_lo == 0) or NULL (stage_lo's lambda already holds the upstream boundary). */
+int rp_trainer_reset_local(rp_trainer* t, const float* x_dev);
+int rp_trainer_step_local(rp_trainer* t, const float* x_dev, const int32_t* labels_dev, int32_t nrows, int32_t row0,
+                          const rp_step_params* p);
+int rp_trainer_correct_ghost(rp_trainer* t, const rp_step_params* p, int32_t row0, int32_t nrows);
+/* device pointer of a state buffer ([num_samples][H W C] fp32) of a local or ghost stage;
+ * which: RP_STATE_LAMBDA 0, KAPPA 1, BOUNDARY_OUT 2, BOUNDARY_ADJOINT 3 */
+int rp_trainer_state_device(rp_trainer* t, int32_t k, int32_t which, float** ptr);
+int rp_trainer_stage_stream(rp_trainer* t, int32_t k, void** stream);
+int rp_trainer_loss_device(rp_trainer* t, double** ptr);
 int rp_trainer_set_kappa_rule(rp_trainer* t, int32_t rule);
 int rp_trainer_get_params(rp_trainer* t, float* host);
 int rp_trainer_set_params(rp_trainer* t, const float* host);

@@ -69,6 +69,15 @@ SIGNATURES = {
     "rp_trainer_create": (C.c_int, [_G, C.c_int32, C.c_int32, C.c_int32, C.c_int32, _F, _U64P, C.c_int32,
                                     _I32, C.c_int32, C.POINTER(_P)]),
     "rp_trainer_destroy": (C.c_int, [_P]),
+    "rp_trainer_create_local": (C.c_int, [_G, C.c_int32, C.c_int32, C.c_int32, C.c_int32, _F, _U64P, C.c_int32,
+                                          C.c_int32, C.c_int32, C.c_int32, C.POINTER(_P)]),
+    "rp_trainer_local_range": (C.c_int, [_P, _I32, _I32]),
+    "rp_trainer_reset_local": (C.c_int, [_P, _P]),
+    "rp_trainer_step_local": (C.c_int, [_P, _P, _P, C.c_int32, C.c_int32, _SP]),
+    "rp_trainer_correct_ghost": (C.c_int, [_P, _SP, C.c_int32, C.c_int32]),
+    "rp_trainer_state_device": (C.c_int, [_P, C.c_int32, C.c_int32, C.POINTER(_P)]),
+    "rp_trainer_stage_stream": (C.c_int, [_P, C.c_int32, C.POINTER(_P)]),
+    "rp_trainer_loss_device": (C.c_int, [_P, C.POINTER(_P)]),
     "rp_trainer_set_kappa_rule": (C.c_int, [_P, C.c_int32]),
     "rp_trainer_get_params": (C.c_int, [_P, _F]),
     "rp_trainer_set_params": (C.c_int, [_P, _F]),

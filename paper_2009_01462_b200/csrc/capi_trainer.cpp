@@ -168,6 +168,91 @@ int rp_trainer_create(const rp_geometry* g, int32_t stages, int32_t mode, int32_
   });
 }
 
+int rp_trainer_create_local(const rp_geometry* g, int32_t stages, int32_t mode, int32_t penalty, int32_t num_samples,
+                            const float* params_host, uint64_t* seed_state, int32_t math, int32_t device,
+                            int32_t stage_lo, int32_t stage_hi, rp_trainer** out) {
+  return tguard([&] {
+    need(g, "geometry");
+    need(out, "out");
+    *out = nullptr;
+    if (rp_param_count(g) < 0) throw respar::b200::ConfigError(rp_last_error());
+    if (mode != RP_MODE_PENALTY && mode != RP_MODE_ALM)
+      throw respar::b200::ConfigError("stage-sharded trainers run the penalty or ALM mode");
+    if (penalty < 0 || penalty > 2) throw respar::b200::ConfigError("unknown penalty kind");
+    if (math < RP_MATH_FP32 || math > RP_MATH_SIMT) throw respar::b200::ConfigError("unknown math mode");
+    auto h = std::make_unique<rp_trainer>();
+    h->tr = std::make_unique<DecoupledTrainer>(
+        *g, stages, mode == RP_MODE_ALM ? respar::b200::TrainMode::Alm : respar::b200::TrainMode::Penalty,
+        static_cast<respar::b200::PenaltyKind>(penalty), num_samples, math, std::vector<int>{device}, stage_lo,
+        stage_hi);
+    if (params_host) {
+      h->tr->set_params(params_host);
+    } else {
+      need(seed_state, "seed_state");
+      h->tr->init_params(*seed_state);
+    }
+    *out = h.release();
+  });
+}
+
+int rp_trainer_local_range(rp_trainer* t, int32_t* stage_lo, int32_t* stage_hi) {
+  return tguard([&] {
+    need(t, "trainer");
+    if (stage_lo) *stage_lo = t->tr->stage_lo();
+    if (stage_hi) *stage_hi = t->tr->stage_hi();
+  });
+}
+
+int rp_trainer_reset_local(rp_trainer* t, const float* x_dev) {
+  return tguard([&] {
+    need(t, "trainer");
+    t->tr->reset_lambda_from_forward(x_dev);
+  });
+}
+
+int rp_trainer_step_local(rp_trainer* t, const float* x_dev, const int32_t* labels_dev, int32_t nrows, int32_t row0,
+                          const rp_step_params* p) {
+  return tguard([&] {
+    need(t, "trainer");
+    DecoupledTrainer& tr = *t->tr;
+    if (tr.stage_lo() == 0) need(x_dev, "x");
+    if (tr.stage_hi() == tr.stages()) need(labels_dev, "labels");
+    tr.step_local(x_dev, labels_dev, nrows, row0, to_params(p));
+  });
+}
+
+int rp_trainer_correct_ghost(rp_trainer* t, const rp_step_params* p, int32_t row0, int32_t nrows) {
+  return tguard([&] {
+    need(t, "trainer");
+    t->tr->correct_ghost(to_params(p), row0, nrows);
+  });
+}
+
+int rp_trainer_state_device(rp_trainer* t, int32_t k, int32_t which, float** ptr) {
+  return tguard([&] {
+    need(t, "trainer");
+    need(ptr, "ptr");
+    *ptr = t->tr->state_device(k, which);
+  });
+}
+
+int rp_trainer_stage_stream(rp_trainer* t, int32_t k, void** stream) {
+  return tguard([&] {
+    need(t, "trainer");
+    need(stream, "stream");
+    if (k < 0 || k >= t->tr->stages()) throw std::out_of_range("stage_stream: bad stage index");
+    *stream = static_cast<void*>(t->tr->scheduler().stream(k));
+  });
+}
+
+int rp_trainer_loss_device(rp_trainer* t, double** ptr) {
+  return tguard([&] {
+    need(t, "trainer");
+    need(ptr, "ptr");
+    *ptr = t->tr->loss_device();
+  });
+}
+
 int rp_trainer_destroy(rp_trainer* t) {
   return tguard([&] { delete t; });
 }

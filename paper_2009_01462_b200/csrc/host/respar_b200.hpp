@@ -137,10 +137,18 @@ class StageScheduler {
 
 // DecoupledTrainer (decoupled.hpp:56-120) on device.  Parameters are fp32 in the flat
 // layout of include/respar_b200.h; lambda/kappa/boundary state is N_train x (H W C) fp32.
+//
+// Stage-sharded form (one process per GPU): a trainer may materialise only
+// the stages [stage_lo, stage_hi) of the K-stage net.  When stage_hi < K it also holds a
+// "ghost" of stage stage_hi -- lambda, kappa and the received boundary adjoint p of the
+// boundary it corrects -- because boundary k is corrected by the owner of stage k-1
+// (which holds X^{k-1}_end and, for its own backward, lambda_k / kappa_k).  The neighbour
+// exchange (p_k upstream, the corrected lambda_k downstream) is done by the caller
+// (paper_2009_01462_b200/distributed.py) on the stage streams.
 class DecoupledTrainer {
  public:
   DecoupledTrainer(const rp_geometry& g, int stages, TrainMode mode, PenaltyKind kind, int num_samples,
-                   int math = RP_MATH_FP32, std::vector<int> devices = {});
+                   int math = RP_MATH_FP32, std::vector<int> devices = {}, int stage_lo = 0, int stage_hi = -1);
   ~DecoupledTrainer();
 
   // ---- parameters (ResidualNet, network.hpp:29-41) ----
@@ -151,6 +159,8 @@ class DecoupledTrainer {
   int64_t param_count() const { return param_total_; }
 
   // ---- reference methods; x / labels are device pointers ----
+  // full_x: raw inputs of all num_samples rows (stage_lo == 0); ignored when stage_lo > 0
+  // (stage_lo's lambda must already hold the upstream rank's boundary output).
   void reset_lambda_from_forward(const float* full_x);
   double step(const float* batch_x, const int32_t* labels, int nrows, int row0, const StepParams& p,
               bool read_loss = true);
@@ -160,6 +170,18 @@ class DecoupledTrainer {
   void correct_aux(int k, const StepParams& p, int row0, int nrows);
   void correct_multiplier(int k, double beta, double kappa_lr, int row0, int nrows);
   void correction_gradient(int k, double beta, int row0, int nrows, float* out) const;
+  // ---- stage-sharded iteration: the parallel phase of the local stages plus the
+  // corrections of the boundaries inside [stage_lo, stage_hi) (step() == this + the loss
+  // read on a trainer that owns every stage); then, once the downstream rank's p has been
+  // received into the ghost's boundary adjoint, the ghost boundary's correction.
+  void step_local(const float* batch_x, const int32_t* labels, int nrows, int row0, const StepParams& p);
+  void correct_ghost(const StepParams& p, int row0, int nrows);
+  int stage_lo() const { return stage_lo_; }
+  int stage_hi() const { return stage_hi_; }
+  bool is_local(int k) const { return k >= stage_lo_ && k < stage_hi_; }
+  bool has_ghost() const { return stage_hi_ < static_cast<int>(stages_.size()); }
+  float* state_device(int k, int which);     // start of the [num_samples][feat] buffer
+  double* loss_device();                      // last stage's loss (device fp64)
   ViolationReport violation_report() const;
   double last_loss() const;
   // full serial forward of the current net (eval): logits [nrows, classes] device
@@ -214,6 +236,8 @@ class DecoupledTrainer {
                     bool use_snapshot, cudaStream_t s);
   void run_correction(int k, const StepParams& p, int row0, int nrows, bool fuse_kappa, cudaStream_t s);
   void check_rows(int row0, int nrows, const char* where) const;
+  void need_local(int k, const char* where) const;
+  bool owns_state(int k) const { return is_local(k) || k == stage_hi_; }
   int64_t feat() const { return (int64_t)geo_.height * geo_.width * geo_.channels; }
   int64_t hid() const { return (int64_t)geo_.height * geo_.width * geo_.hidden; }
   int64_t raw_feat() const { return (int64_t)geo_.height * geo_.width * geo_.in_channels; }
@@ -234,6 +258,7 @@ class DecoupledTrainer {
   DeviceArray in_stage_, lab_stage_, eval_a_, eval_b_;
   long iteration_ = 0;
   bool has_forward_ = false;
+  int stage_lo_ = 0, stage_hi_ = 0;
 };
 
 }  // namespace respar::b200

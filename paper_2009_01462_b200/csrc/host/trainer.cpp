@@ -174,6 +174,13 @@ void StageScheduler::region_begin() {
 }
 
 float StageScheduler::region_end() {
+  // join every stage stream (work enqueued after end(), e.g. the neighbour exchange and
+  // the ghost correction of a stage-sharded step, belongs to the region)
+  for (int k = 0; k < stages(); ++k) {
+    record(k, kStageDone);
+    DeviceGuard g(devices_[0]);
+    cu(cudaStreamWaitEvent(ctl_, marks_[(size_t)k * kNumMarks + kStageDone], 0), "cudaStreamWaitEvent");
+  }
   DeviceGuard g(devices_[0]);
   cu(cudaEventRecord(ev_re_, ctl_), "cudaEventRecord");
   cu(cudaEventSynchronize(ev_re_), "cudaEventSynchronize");
@@ -231,11 +238,16 @@ void StageScheduler::sync() {
 
 // --------------------------------------------------------- DecoupledTrainer
 DecoupledTrainer::DecoupledTrainer(const rp_geometry& g, int stages, TrainMode mode, PenaltyKind kind,
-                                   int num_samples, int math, std::vector<int> devices)
+                                   int num_samples, int math, std::vector<int> devices, int stage_lo, int stage_hi)
     : geo_(g), mode_(mode), kind_(kind), num_samples_(num_samples), math_(math) {
   if (rp_param_count(&g) < 0) check(RP_ERR_CONFIG);
   if (num_samples < 1) throw ConfigError("DecoupledTrainer: need at least one sample");
   const auto ranges = partition(g.blocks, stages);
+  stage_lo_ = stage_lo;
+  stage_hi_ = stage_hi < 0 ? stages : stage_hi;
+  if (stage_lo_ < 0 || stage_lo_ >= stage_hi_ || stage_hi_ > stages)
+    throw std::invalid_argument("DecoupledTrainer: local stage range [" + std::to_string(stage_lo_) + ", " +
+                                std::to_string(stage_hi_) + ") is not inside [0, " + std::to_string(stages) + ")");
   blocks_per_stage_ = ranges[0].second - ranges[0].first;
   sched_ = std::make_unique<StageScheduler>(stages, devices);
   param_total_ = rp_param_count(&g);
@@ -261,16 +273,20 @@ DecoupledTrainer::DecoupledTrainer(const rp_geometry& g, int stages, TrainMode m
     st.begin = ranges[k].first;
     st.end = ranges[k].second;
     st.device = devices_[k];
+    if (!owns_state(k)) continue;               // another rank's stage
+    const bool ghost = !is_local(k);
+    if (ghost) st.device = devices_[k - 1];     // lives with the stage that corrects it
     if (k > 0) {
       st.lam.allocate(st.device, state_bytes);
       st.kappa.allocate(st.device, state_bytes);
       st.lam.zero(nullptr);
       st.kappa.zero(nullptr);
     }
-    st.bout.allocate(st.device, state_bytes);
     st.badj.allocate(st.device, state_bytes);
-    st.bout.zero(nullptr);
     st.badj.zero(nullptr);
+    if (ghost) continue;
+    st.bout.allocate(st.device, state_bytes);
+    st.bout.zero(nullptr);
     st.loss.allocate(st.device, 8);
     st.loss.zero(nullptr);
     st.red_ws.allocate(st.device, rp_op_reduce_workspace_bytes());
@@ -319,7 +335,7 @@ void DecoupledTrainer::get_params(float* host) const {
   sched_->sync();
   // each stage's device owns its parameter slice (stage 0 owns S, stage K-1 owns T)
   const Layout L(geo_);
-  for (int k = 0; k < stages(); ++k) {
+  for (int k = stage_lo_; k < stage_hi_; ++k) {
     const Stage& st = stages_[k];
     int64_t beg = L.block0 + (int64_t)st.begin * L.block_stride;
     int64_t end = L.block0 + (int64_t)st.end * L.block_stride;
@@ -333,7 +349,7 @@ void DecoupledTrainer::get_params(float* host) const {
 void DecoupledTrainer::get_grads(float* host) const {
   sched_->sync();
   const Layout L(geo_);
-  for (int k = 0; k < stages(); ++k) {
+  for (int k = stage_lo_; k < stage_hi_; ++k) {
     const Stage& st = stages_[k];
     int64_t beg = L.block0 + (int64_t)st.begin * L.block_stride;
     int64_t end = L.block0 + (int64_t)st.end * L.block_stride;
@@ -346,7 +362,7 @@ void DecoupledTrainer::get_grads(float* host) const {
 }
 
 void DecoupledTrainer::ensure_capacity(int nrows) {
-  for (int k = 0; k < stages(); ++k) {
+  for (int k = stage_lo_; k < stage_hi_; ++k) {
     Stage& st = stages_[k];
     if (st.cap_rows >= nrows) continue;
     const int n = st.end - st.begin;
@@ -368,13 +384,18 @@ void DecoupledTrainer::ensure_capacity(int nrows) {
 }
 
 float* DecoupledTrainer::input_staging(int nrows) {
-  in_stage_.allocate(stages_[0].device, std::max<int64_t>(1, (int64_t)nrows * raw_feat() * 4));
+  in_stage_.allocate(stages_[stage_lo_].device, std::max<int64_t>(1, (int64_t)nrows * raw_feat() * 4));
   return in_stage_.get();
 }
 
 int32_t* DecoupledTrainer::label_staging(int nrows) {
-  lab_stage_.allocate(stages_.back().device, std::max<int64_t>(4, (int64_t)nrows * 4));
+  lab_stage_.allocate(stages_[stage_hi_ - 1].device, std::max<int64_t>(4, (int64_t)nrows * 4));
   return lab_stage_.get<int32_t>();
+}
+
+void DecoupledTrainer::need_local(int k, const char* where) const {
+  if (k >= 0 && k < stages() && !is_local(k))
+    throw std::invalid_argument(std::string(where) + ": stage " + std::to_string(k) + " is not local to this rank");
 }
 
 void DecoupledTrainer::check_rows(int row0, int nrows, const char* where) const {
@@ -498,16 +519,18 @@ void DecoupledTrainer::run_correction(int k, const StepParams& p, int row0, int 
 
 void DecoupledTrainer::reset_lambda_from_forward(const float* full_x) {
   sched_->sync();
-  const int chunk = std::min(num_samples_, std::max(256, stages_[0].cap_rows));
+  if (stage_lo_ == 0 && !full_x) throw std::invalid_argument("reset_lambda_from_forward: null input");
+  const int chunk = std::min(num_samples_, std::max(256, stages_[stage_lo_].cap_rows));
   ensure_capacity(chunk);
   for (int r0 = 0; r0 < num_samples_; r0 += chunk) {
     const int nr = std::min(chunk, num_samples_ - r0);
-    const float* in = full_x + (int64_t)r0 * raw_feat();
-    for (int k = 0; k < stages(); ++k) {
+    const float* in = stage_lo_ == 0 ? full_x + (int64_t)r0 * raw_feat()
+                                     : stages_[stage_lo_].lam.get() + (int64_t)r0 * feat();
+    for (int k = stage_lo_; k < stage_hi_; ++k) {
       Stage& st = stages_[k];
       DeviceGuard g(st.device);
       cudaStream_t s = sched_->stream(k);
-      if (k > 0) {
+      if (k > stage_lo_) {
         // lambda_k := X_{kn} (the previous stage's output rows)
         const Stage& pv = stages_[k - 1];
         sched_->record(k - 1, StageScheduler::kStageDone);
@@ -520,7 +543,20 @@ void DecoupledTrainer::reset_lambda_from_forward(const float* full_x) {
       run_forward(st, in, nr, st.bout.get() + (int64_t)r0 * feat(), s);
     }
   }
-  for (int k = 0; k < stages(); ++k) {
+  if (has_ghost()) {
+    // the ghost's lambda starts as this rank's boundary output (the downstream rank
+    // receives the same rows as its stage input)
+    Stage& gh = stages_[stage_hi_];
+    const Stage& pv = stages_[stage_hi_ - 1];
+    DeviceGuard g(gh.device);
+    cudaStream_t s = sched_->stream(stage_hi_ - 1);
+    cu(cudaMemcpyAsync(gh.lam.get(), pv.bout.get(), (size_t)num_samples_ * feat() * 4, cudaMemcpyDeviceToDevice, s),
+       "cudaMemcpyAsync");
+    gh.kappa.zero(s);
+    gh.badj.zero(s);
+    gh.kappa_zero = true;
+  }
+  for (int k = stage_lo_; k < stage_hi_; ++k) {
     Stage& st = stages_[k];
     DeviceGuard g(st.device);
     if (k > 0) st.kappa.zero(sched_->stream(k));
@@ -535,6 +571,16 @@ void DecoupledTrainer::reset_lambda_from_forward(const float* full_x) {
 
 double DecoupledTrainer::step(const float* batch_x, const int32_t* labels, int nrows, int row0, const StepParams& p,
                               bool read_loss) {
+  if (has_ghost() || stage_lo_ > 0)
+    throw std::logic_error("step: this trainer holds stages [" + std::to_string(stage_lo_) + ", " +
+                           std::to_string(stage_hi_) + ") only; use the distributed step");
+  step_local(batch_x, labels, nrows, row0, p);
+  if (!read_loss) return 0.0;
+  return last_loss();
+}
+
+void DecoupledTrainer::step_local(const float* batch_x, const int32_t* labels, int nrows, int row0,
+                                  const StepParams& p) {
   check_rows(row0, nrows, "step");
   if (nrows < 1) throw ShapeError("step: empty batch");
   ensure_capacity(nrows);
@@ -544,7 +590,7 @@ double DecoupledTrainer::step(const float* batch_x, const int32_t* labels, int n
   // (pool.run_iteration, decoupled.cpp:184-187).  Stage k reads lambda_{k+1}/kappa_{k+1}
   // directly: nothing writes them before the correction phase, so the iteration-start
   // snapshot of decoupled.cpp:65-73 is implicit.
-  for (int k = 0; k < stages(); ++k) {
+  for (int k = stage_lo_; k < stage_hi_; ++k) {
     Stage& st = stages_[k];
     DeviceGuard g(st.device);
     cudaStream_t s = sched_->stream(k);
@@ -559,17 +605,39 @@ double DecoupledTrainer::step(const float* batch_x, const int32_t* labels, int n
   has_forward_ = true;
   // serial correction sweep (decoupled.cpp:189-192): boundaries are independent, so
   // boundary k runs on stage k's stream once stage k-1 is done.
-  for (int k = 1; k < stages(); ++k) {
+  for (int k = stage_lo_ + 1; k < stage_hi_; ++k) {
     DeviceGuard g(stages_[k].device);
     sched_->wait(k, k - 1, StageScheduler::kBackwardDone);
     run_correction(k, p, row0, nrows, true, sched_->stream(k));
   }
   sched_->end();
-  if (!read_loss) return 0.0;
-  return last_loss();
+}
+
+void DecoupledTrainer::correct_ghost(const StepParams& p, int row0, int nrows) {
+  if (!has_ghost()) throw std::logic_error("correct_ghost: this trainer owns the last stage");
+  check_rows(row0, nrows, "correct_ghost");
+  // runs on the stream of stage_hi - 1, after its backward and the receive of p
+  DeviceGuard g(stages_[stage_hi_ - 1].device);
+  run_correction(stage_hi_, p, row0, nrows, true, sched_->stream(stage_hi_ - 1));
+}
+
+float* DecoupledTrainer::state_device(int k, int which) {
+  if (k < 0 || k >= stages()) throw std::out_of_range("state: bad stage index");
+  if (which < 0 || which > 3) throw std::invalid_argument("state: which must be 0..3");
+  if (!owns_state(k)) throw std::invalid_argument("state: stage " + std::to_string(k) + " is not held by this rank");
+  Stage& st = stages_[k];
+  DeviceArray* arr[4] = {&st.lam, &st.kappa, &st.bout, &st.badj};
+  if (arr[which]->bytes() == 0) throw std::invalid_argument("state: stage " + std::to_string(k) + " has no such buffer");
+  return arr[which]->get();
+}
+
+double* DecoupledTrainer::loss_device() {
+  if (stage_hi_ != stages()) throw std::logic_error("loss: the last stage is not local");
+  return stages_.back().loss.get<double>();
 }
 
 double DecoupledTrainer::last_loss() const {
+  if (stage_hi_ != stages()) throw std::logic_error("last_loss: the last stage is not local");
   const Stage& st = stages_.back();
   double v = 0.0;
   DeviceGuard g(sched_->control_device());
@@ -581,6 +649,7 @@ double DecoupledTrainer::last_loss() const {
 void DecoupledTrainer::take_snapshot(int k, int row0, int nrows) {
   if (k < 0 || k >= stages() - 1)
     throw std::invalid_argument("take_snapshot: stage " + std::to_string(k) + " has no downstream neighbour");
+  need_local(k, "take_snapshot");
   check_rows(row0, nrows, "take_snapshot");
   Stage& st = stages_[k];
   const Stage& nx = stages_[k + 1];
@@ -601,6 +670,7 @@ void DecoupledTrainer::take_snapshot(int k, int row0, int nrows) {
 
 void DecoupledTrainer::stage_forward(int k, const float* batch_x, int nrows, int row0) {
   if (k < 0 || k >= stages()) throw std::out_of_range("stage_forward: bad stage index");
+  need_local(k, "stage_forward");
   check_rows(row0, nrows, "stage_forward");
   ensure_capacity(std::max(nrows, 1));
   Stage& st = stages_[k];
@@ -618,6 +688,7 @@ void DecoupledTrainer::stage_forward(int k, const float* batch_x, int nrows, int
 void DecoupledTrainer::stage_backward_update(int k, const int32_t* labels, double beta, double lr, int row0,
                                              double momentum) {
   if (k < 0 || k >= stages()) throw std::out_of_range("stage_backward_update: bad stage index");
+  need_local(k, "stage_backward_update");
   Stage& st = stages_[k];
   if (st.version != iteration_ || st.fwd_rows == 0)
     throw std::logic_error("stage_backward_update: stage " + std::to_string(k) +
@@ -641,6 +712,7 @@ void DecoupledTrainer::correct_aux(int k, const StepParams& p, int row0, int nro
     throw std::invalid_argument("correction: stage " + std::to_string(k) +
                                 " out of range (lambda_0 is fixed to the true input)");
   if (!has_forward_) throw std::logic_error("correct_aux before any forward pass");
+  need_local(k - 1, "correct_aux");
   check_rows(row0, nrows, "correct_aux");
   sched_->sync();
   DeviceGuard g(stages_[k].device);
@@ -654,6 +726,7 @@ void DecoupledTrainer::correct_multiplier(int k, double beta, double kappa_lr, i
                                 " out of range (lambda_0 is fixed to the true input)");
   if (kind_ != PenaltyKind::SquaredL2)
     throw std::logic_error("correct_multiplier: the multiplier update is only derived for the squared_l2 penalty");
+  need_local(k - 1, "correct_multiplier");
   check_rows(row0, nrows, "correct_multiplier");
   sched_->sync();
   Stage& st = stages_[k];
@@ -671,6 +744,7 @@ void DecoupledTrainer::correction_gradient(int k, double beta, int row0, int nro
   if (k < 1 || k >= stages())
     throw std::invalid_argument("correction: stage " + std::to_string(k) +
                                 " out of range (lambda_0 is fixed to the true input)");
+  need_local(k - 1, "correction_gradient");
   check_rows(row0, nrows, "correction_gradient");
   sched_->sync();
   const Stage& st = stages_[k];
@@ -693,6 +767,11 @@ ViolationReport DecoupledTrainer::violation_report() const {
   r.normalizer = normalizer(num_samples_, (int)feat());
   r.per_stage.push_back(0.0);
   for (int k = 1; k < stages(); ++k) {
+    // boundary k is reported by the holder of stage k-1 (0 for the other ranks' boundaries)
+    if (!is_local(k - 1)) {
+      r.per_stage.push_back(0.0);
+      continue;
+    }
     const Stage& st = stages_[k];
     DeviceGuard g(st.device);
     double v = 0.0;
@@ -712,6 +791,7 @@ void DecoupledTrainer::forward(const float* x, int nrows, float* logits) {
   eval_a_.allocate(stages_[0].device, (int64_t)chunk * feat() * 4);
   eval_b_.allocate(stages_[0].device, (int64_t)chunk * feat() * 4);
   if (unique_devices_.size() > 1) throw std::logic_error("forward: eval on multi-device trainers is not supported");
+  if (stage_lo_ != 0 || stage_hi_ != stages()) throw std::logic_error("forward: needs every stage on this trainer");
   cudaStream_t s = sched_->stream(0);
   DeviceGuard g(stages_[0].device);
   for (int r0 = 0; r0 < nrows; r0 += chunk) {
@@ -743,6 +823,8 @@ int64_t DecoupledTrainer::state_elems(int k, int which) const {
   if (k < 0 || k >= stages()) throw std::out_of_range("state: bad stage index");
   if (which < 0 || which > 3) throw std::invalid_argument("state: which must be 0..3");
   if (k == 0 && which < 2) return 0;
+  if (!owns_state(k)) throw std::invalid_argument("state: stage " + std::to_string(k) + " is not held by this rank");
+  if (!is_local(k) && which == 2) throw std::invalid_argument("state: the ghost stage has no boundary_out");
   return (int64_t)num_samples_ * feat();
 }
 

@@ -1,0 +1,278 @@
+"""Stage-sharded layer-parallel training, one process per GPU.
+
+The reference runs every stage of ``DecoupledTrainer::step`` (decoupled.cpp:172-194) on
+one ``StagePool`` of threads (runtime.cpp:41-88).  Here stage k of K lives on rank
+``floor(k * R / K)`` of an R-process job (``torch.distributed``; NCCL between B200s,
+gloo in the CPU tests), and the only data the ranks exchange per iteration is the
+neighbour traffic of the decoupled algorithm itself -- no collective touches the data
+path, because the parameters of different stages are disjoint (network.cpp:174-191).
+
+Ownership of boundary k (between stage k-1 on rank a and stage k on rank b):
+
+* rank a holds the *master* lambda_k and kappa_k: its stage k-1 backward reads them as
+  the iteration-start snapshot (decoupled.cpp:65-73, 105-110), and it runs the boundary's
+  correction (correct_aux / correct_multiplier, decoupled.cpp:135-170), which also needs
+  its own X^{k-1}_end;
+* rank b holds a copy of lambda_k as stage k's forward input (decoupled.cpp:75-83) and
+  produces p_k, the cotangent at that input (decoupled.cpp:111-113).
+
+One iteration on every rank, with one pair of point-to-point exchanges per boundary::
+
+    engine.step_local          stages [lo, hi): forward, synthetic / phi backward, SGD;
+                               corrections of the boundaries inside [lo, hi)
+    exchange A                 p_lo -> rank-1            ||  p_hi <- rank+1 (ghost adjoint)
+    engine.correct_ghost       boundary hi (lambda_hi, kappa_hi updated in place)
+    exchange B                 lambda_hi -> rank+1       ||  lambda_lo <- rank-1
+
+Every correction of the reference's serial sweep (decoupled.cpp:189-192) reads only its
+own boundary's state, so running them on different ranks reproduces the reference's
+result bit for bit (tests/test_distributed.py checks this against the single-process
+trainer).  The engine is the CUDA trainer (``CudaStageEngine``) on B200; the transport
+ops run on the owning stage's CUDA stream, so NCCL overlaps nothing it must not.
+
+When R > K the job runs R / K independent replicas of the K-stage pipeline ("replicas
+only": the reference has no data-parallel gradient exchange, so none is invented).
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass
+from typing import Optional
+
+import numpy as np
+
+from ._lib import lib
+from .trainer import (BOUNDARY_ADJOINT, LAMBDA, MATH, ConfigError, Geometry, StepParams, _kind, _mode, check,
+                      param_count)
+
+__all__ = ["StagePlacement", "placement", "CudaStageEngine", "DistributedDecoupledTrainer"]
+
+
+@dataclass(frozen=True)
+class StagePlacement:
+    """Where the stages of one K-stage pipeline live in an R-process job."""
+    stages: int          # K
+    world: int           # R
+    rank: int
+    group_size: int      # ranks per pipeline replica (min(R, K))
+    replica: int         # which replica this rank belongs to
+    replicas: int
+    lo: int              # local stages [lo, hi)
+    hi: int
+    prev_rank: Optional[int]   # global rank holding stage lo-1 (None if lo == 0)
+    next_rank: Optional[int]   # global rank holding stage hi (None if hi == K)
+
+    @property
+    def first(self) -> bool:
+        return self.lo == 0
+
+    @property
+    def last(self) -> bool:
+        return self.hi == self.stages
+
+    def rank_of_stage(self, k: int) -> int:
+        """floor(k * G / K) inside this replica."""
+        return self.replica * self.group_size + (k * self.group_size) // self.stages
+
+
+def placement(stages: int, world: int, rank: int) -> StagePlacement:
+    """Stage k -> rank floor(k * G / K) with G = min(R, K) ranks per pipeline; R > K
+    runs R / K replicas (R must then be a multiple of K; K < R needs no extra ranks)."""
+    if stages < 1 or world < 1 or not 0 <= rank < world:
+        raise ConfigError(f"placement: bad (stages={stages}, world={world}, rank={rank})")
+    G = min(world, stages)
+    if world % G != 0:
+        raise ConfigError(f"placement: {world} ranks cannot hold whole {stages}-stage pipelines")
+    replica, r = divmod(rank, G)
+    owned = [k for k in range(stages) if (k * G) // stages == r]
+    if not owned:
+        raise ConfigError(f"placement: rank {rank} owns no stage")
+    lo, hi = owned[0], owned[-1] + 1
+    base = replica * G
+    return StagePlacement(stages=stages, world=world, rank=rank, group_size=G, replica=replica,
+                          replicas=world // G, lo=lo, hi=hi,
+                          prev_rank=None if lo == 0 else base + ((lo - 1) * G) // stages,
+                          next_rank=None if hi == stages else base + (hi * G) // stages)
+
+
+class _DeviceArray:
+    """__cuda_array_interface__ view of trainer-owned device memory (no copy)."""
+
+    def __init__(self, ptr: int, shape, typestr: str):
+        self.__cuda_array_interface__ = {"shape": tuple(shape), "typestr": typestr, "data": (ptr, False),
+                                         "version": 3, "strides": None}
+
+
+class CudaStageEngine:
+    """The B200 trainer for the local stages of one rank (rp_trainer_create_local)."""
+
+    def __init__(self, geometry: Geometry, stages: int, mode, penalty, num_samples: int, lo: int, hi: int,
+                 device: int, params: Optional[np.ndarray] = None, seed_state: int = 0, math: str = "fp32"):
+        import torch
+        self.torch = torch
+        self.geometry = geometry
+        self.stages = stages
+        self.lo, self.hi = lo, hi
+        self.num_samples = num_samples
+        self.device = device
+        self._g = geometry.c()
+        self._h = C.c_void_p()
+        st = C.c_uint64(seed_state)
+        p = None
+        if params is not None:
+            p = np.ascontiguousarray(params, dtype=np.float32)
+        check(lib().rp_trainer_create_local(C.byref(self._g), stages, _mode(mode), _kind(penalty), num_samples,
+                                            p.ctypes.data_as(C.POINTER(C.c_float)) if p is not None else None,
+                                            C.byref(st), MATH[math], device, lo, hi, C.byref(self._h)))
+        self.seed_state = st.value
+        self.nparams = param_count(geometry)
+
+    def close(self):
+        if getattr(self, "_h", None) and self._h.value:
+            lib().rp_trainer_destroy(self._h)
+            self._h = C.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    # -- state views (torch tensors aliasing the trainer's device buffers) --
+    def view(self, k: int, which: int, row0: int, nrows: int):
+        ptr = C.c_void_p()
+        check(lib().rp_trainer_state_device(self._h, k, which, C.byref(ptr)))
+        fs = self.geometry.feature_size
+        t = self.torch.as_tensor(_DeviceArray(ptr.value, (self.num_samples * fs,), "<f4"),
+                                 device=f"cuda:{self.device}")
+        return t[row0 * fs:(row0 + nrows) * fs]
+
+    def loss_tensor(self):
+        ptr = C.c_void_p()
+        check(lib().rp_trainer_loss_device(self._h, C.byref(ptr)))
+        return self.torch.as_tensor(_DeviceArray(ptr.value, (1,), "<f8"), device=f"cuda:{self.device}")
+
+    def stream(self, k: int):
+        """Context manager making stage k's CUDA stream torch's current stream, so the
+        NCCL transfers are ordered after the kernels that produce / consume them."""
+        s = C.c_void_p()
+        check(lib().rp_trainer_stage_stream(self._h, k, C.byref(s)))
+        ext = self.torch.cuda.ExternalStream(s.value, device=f"cuda:{self.device}")
+        return self.torch.cuda.stream(ext)
+
+    # -- algorithm --
+    def reset(self, x_ptr: Optional[int]) -> None:
+        check(lib().rp_trainer_reset_local(self._h, C.c_void_p(x_ptr) if x_ptr else None))
+
+    def step_local(self, x_ptr: Optional[int], labels_ptr: Optional[int], nrows: int, row0: int,
+                   p: StepParams) -> None:
+        check(lib().rp_trainer_step_local(self._h, C.c_void_p(x_ptr) if x_ptr else None,
+                                          C.c_void_p(labels_ptr) if labels_ptr else None, nrows, row0,
+                                          C.byref(p.c())))
+
+    def correct_ghost(self, p: StepParams, row0: int, nrows: int) -> None:
+        check(lib().rp_trainer_correct_ghost(self._h, C.byref(p.c()), row0, nrows))
+
+    def region(self, which: int) -> float:
+        ms = C.c_float()
+        check(lib().rp_trainer_region(self._h, which, C.byref(ms)))
+        return ms.value
+
+    def params(self) -> np.ndarray:
+        """Local stages' slices of the flat parameters (other entries 0)."""
+        out = np.zeros(self.nparams, np.float32)
+        check(lib().rp_trainer_get_params(self._h, out.ctypes.data_as(C.POINTER(C.c_float))))
+        return out
+
+    def state(self, k: int, which: int) -> np.ndarray:
+        g = self.geometry
+        out = np.empty((self.num_samples, g.height, g.width, g.channels), np.float32)
+        check(lib().rp_trainer_get_state(self._h, k, which, out.ctypes.data_as(C.POINTER(C.c_float))))
+        return out
+
+
+class DistributedDecoupledTrainer:
+    """``DecoupledTrainer::step`` across processes: the local stages run on ``engine``;
+    the boundary traffic goes over ``torch.distributed`` point-to-point.
+
+    ``engine`` provides ``lo, hi, stages`` and ``view / stream / reset / step_local /
+    correct_ghost / loss_tensor`` (``CudaStageEngine``; the CPU tests plug in the oracle)."""
+
+    def __init__(self, engine, plc: StagePlacement, group=None):
+        if (engine.lo, engine.hi, engine.stages) != (plc.lo, plc.hi, plc.stages):
+            raise ConfigError("DistributedDecoupledTrainer: engine stages do not match the placement")
+        self.engine = engine
+        self.plc = plc
+        self.group = group
+        self.iteration = 0
+
+    # -- transport --
+    def _exchange(self, sends, recvs, k_stream: int) -> None:
+        """Post the sends and receives of one exchange phase together (no ordering
+        deadlock between the two neighbours) on stage k_stream's stream and make that
+        stream wait for them."""
+        import torch.distributed as dist
+        ops = [dist.P2POp(dist.isend, t, peer, self.group) for t, peer in sends] + \
+              [dist.P2POp(dist.irecv, t, peer, self.group) for t, peer in recvs]
+        if not ops:
+            return
+        with self.engine.stream(k_stream):
+            for req in dist.batch_isend_irecv(ops):
+                req.wait()
+
+    def reset_lambda_from_forward(self, x_ptr: Optional[int], nrows: int) -> None:
+        """decoupled.cpp:44-63 as a chained forward: rank r waits for the boundary rows
+        of rank r-1, runs its stages, hands its last boundary to rank r+1."""
+        e, p = self.engine, self.plc
+        if p.prev_rank is not None:
+            self._exchange([], [(e.view(p.lo, LAMBDA, 0, nrows), p.prev_rank)], p.lo)
+        e.reset(x_ptr if p.first else None)
+        if p.next_rank is not None:
+            self._exchange([(e.view(p.hi, LAMBDA, 0, nrows), p.next_rank)], [], p.hi - 1)
+
+    def step(self, x_ptr: Optional[int], labels_ptr: Optional[int], nrows: int, row0: int, sp: StepParams,
+             read_loss: bool = False) -> Optional[float]:
+        e, p = self.engine, self.plc
+        self.iteration += 1
+        e.step_local(x_ptr, labels_ptr, nrows, row0, sp)
+        # exchange A: p_lo upstream, p_hi from downstream into the ghost's adjoint rows
+        sends = [(e.view(p.lo, BOUNDARY_ADJOINT, row0, nrows), p.prev_rank)] if p.prev_rank is not None else []
+        recvs = [(e.view(p.hi, BOUNDARY_ADJOINT, row0, nrows), p.next_rank)] if p.next_rank is not None else []
+        self._exchange(sends, recvs, p.hi - 1 if recvs else p.lo)
+        if p.next_rank is not None:
+            e.correct_ghost(sp, row0, nrows)
+        # exchange B: the corrected lambda_hi downstream, lambda_lo from upstream
+        sends = [(e.view(p.hi, LAMBDA, row0, nrows), p.next_rank)] if p.next_rank is not None else []
+        recvs = [(e.view(p.lo, LAMBDA, row0, nrows), p.prev_rank)] if p.prev_rank is not None else []
+        self._exchange(sends, recvs, p.lo if recvs else p.hi - 1)
+        if not read_loss:
+            return None
+        return self.loss()
+
+    def loss(self) -> float:
+        """The last stage's pre-update loss (decoupled.cpp:193), on every rank of the replica."""
+        import torch.distributed as dist
+        p = self.plc
+        last = p.rank_of_stage(p.stages - 1)
+        t = self.engine.loss_tensor().clone() if p.last else None
+        if p.group_size == 1:
+            return float(t.item())
+        if t is None:
+            t = self._zeros_like_loss()
+        with self.engine.stream(p.hi - 1):
+            if p.last:
+                ops = [dist.P2POp(dist.isend, t, r, self.group)
+                       for r in range(p.replica * p.group_size, (p.replica + 1) * p.group_size) if r != p.rank]
+            else:
+                ops = [dist.P2POp(dist.irecv, t, last, self.group)]
+            for req in dist.batch_isend_irecv(ops):
+                req.wait()
+        return float(t.item())
+
+    def _zeros_like_loss(self):
+        lt = getattr(self.engine, "loss_like", None)
+        if lt is not None:
+            return lt()
+        import torch
+        return torch.zeros(1, dtype=torch.float64, device=f"cuda:{self.engine.device}")
+
