@@ -63,6 +63,8 @@ enum { RP_MATH_FP32 = 0, RP_MATH_TF32 = 1, RP_MATH_BF16 = 2, RP_MATH_SIMT = 3 };
 /* multiplier rule: the reference's (decoupled.cpp:157-170) or the textbook one
  * kappa += beta (lambda - X) (north_star wording; opt-in only). */
 enum { RP_KAPPA_RULE_REFERENCE = 0, RP_KAPPA_RULE_TEXTBOOK = 1 };
+/* per-stage state buffers (StageState, decoupled.hpp:29-32) for get/set_state & co. */
+enum { RP_STATE_LAMBDA = 0, RP_STATE_KAPPA = 1, RP_STATE_BOUNDARY_OUT = 2, RP_STATE_BOUNDARY_ADJOINT = 3 };
 
 /* ResidualNet geometry (network.hpp:29-41 + conv geometry). */
 typedef struct rp_geometry {
