@@ -80,6 +80,7 @@ int64_t op_workspace_bytes(const rp_geometry& g, int nrows) {
   int64_t wg = wgrad_ws_bytes(shape(g, nrows, (int)Ch, (int)C));
   wg = std::max(wg, wgrad_ws_bytes(shape(g, nrows, (int)C, (int)Ch)));
   wg = std::max(wg, wgrad_ws_bytes(shape(g, nrows, g.in_channels, (int)C)));
+  wg = std::max(wg, k::stem_wgrad_ws_bytes(shape(g, nrows, g.in_channels, (int)C)));
   const int64_t head = k::head_ws_bytes(nrows, g.channels, g.classes);
   return std::max(weight_ws_bytes(g) + align256(wg), head) + 256;
 }
@@ -142,15 +143,23 @@ void stem_fwd(const rp_geometry& g, int nrows, const float* xr, const float* ps,
   const ParamLayout L = ParamLayout::of(g);
   const k::ConvShape sh = shape(g, nrows, g.in_channels, g.channels);
   prof::Scope scope(RP_PROF_STEM, st, conv_flops(sh), conv_bytes(sh, false));
-  k::conv3x3_fwd_simt(sh, xr, ps + L.s_w, ps + L.s_b, nullptr, 1.f, k::EPI_BIAS, x0, st);
+  if (k::stem_supported(sh))
+    k::stem_fwd(sh, xr, ps + L.s_w, ps + L.s_b, x0, st);
+  else
+    k::conv3x3_fwd_simt(sh, xr, ps + L.s_w, ps + L.s_b, nullptr, 1.f, k::EPI_BIAS, x0, st);
 }
 
 void stem_bwd(const rp_geometry& g, int nrows, const float* xr, const float* g0, float* gs, void* ws,
               int64_t ws_bytes, cudaStream_t st) {
   const ParamLayout L = ParamLayout::of(g);
   const k::ConvShape sh = shape(g, nrows, g.in_channels, g.channels);
-  if (k::conv3x3_wgrad_ws_bytes(sh) > ws_bytes) fail(RP_ERR_RANGE, "stem_bwd: workspace too small");
   prof::Scope scope(RP_PROF_STEM, st, conv_flops(sh), conv_bytes(sh, false));
+  if (k::stem_supported(sh)) {
+    if (k::stem_wgrad_ws_bytes(sh) > ws_bytes) fail(RP_ERR_RANGE, "stem_bwd: workspace too small");
+    k::stem_wgrad(sh, xr, g0, 1.f, gs + L.s_w, gs + L.s_b, ws, st);
+    return;
+  }
+  if (k::conv3x3_wgrad_ws_bytes(sh) > ws_bytes) fail(RP_ERR_RANGE, "stem_bwd: workspace too small");
   k::conv3x3_wgrad_simt(sh, xr, g0, 1.f, gs + L.s_w, gs + L.s_b, ws, st);
 }
 

@@ -50,11 +50,12 @@ using namespace rp::umma;
 constexpr int kThreads = 320;
 constexpr int kWStages = 3;          // one weight stage = one filter row (3 taps) of one chunk
 constexpr int kChunk = 16;           // input channels per halo chunk
+constexpr bool kUseCollector = false;  // A-operand collector reuse (measured: no gain here)
 constexpr int kS = 2;                // 128-position tiles per unit
 constexpr int kMaxSmem = 220 * 1024;
 
 struct TcArgs {
-  int N, H, W, Ci, Co, Wp, rows_h, T, units_per_img, num_units, halo_pos, nchunks;
+  int N, H, W, Ci, Co, Wp, rows_h, T, num_tiles, halo_pos, nchunks;
   uint32_t halo_bytes;  // one raw (or lo) halo buffer
   uint32_t halo_stride; // bytes per halo slot (raw + lo + pads)
   uint32_t w_tap;       // bytes of one tap's A operand (128 rows x 16 channels x 4 B)
@@ -64,6 +65,7 @@ struct TcArgs {
   const float* aux;
   float* out;
   unsigned long long* trace;   // diagnostics (tools/trace_conv.py): per-unit timestamps, null = off
+  int dbg;                     // experiment bits (RP_CONV_DBG): 1 no epilogue, 2 no converters
 };
 
 __device__ __forceinline__ float rna_tf32(float v) {
@@ -76,6 +78,26 @@ __device__ __forceinline__ float rna_tf32(float v) {
 // (measured: 1 + 2^-11 + 2^-12 enters as 1.0), so the raw halo already is x_hi and only
 // x_lo = x - trunc(x) (exact in fp32) has to be written.
 __device__ __forceinline__ float trunc_tf32(float v) { return __uint_as_float(__float_as_uint(v) & 0xffffe000u); }
+
+// Work split: CTA b owns the contiguous range [b*N*T/G, (b+1)*N*T/G) of the global tile
+// index n*T + t (tile = 128 frame positions of image n), walked in units of up to kS
+// tiles of one image.  Every CTA gets floor or ceil of the mean tile count (the old
+// round-robin over fixed 2-tile units left the busiest CTA 9% above the mean).
+struct UnitIter {
+  int t, t_end, T;
+  __device__ UnitIter(int total, int T_) : T(T_) {
+    t = (int)((int64_t)blockIdx.x * total / gridDim.x);
+    t_end = (int)((int64_t)(blockIdx.x + 1) * total / gridDim.x);
+  }
+  __device__ bool next(int& n, int& tile0, int& ntiles) {
+    if (t >= t_end) return false;
+    n = t / T;
+    tile0 = t - n * T;
+    ntiles = min(kS, min(T - tile0, t_end - t));
+    t += ntiles;
+    return true;
+  }
+};
 
 template <int EPI>
 __device__ __forceinline__ float epi_value(float acc, float bias, int64_t idx, const TcArgs& a) {
@@ -151,9 +173,10 @@ __global__ void __launch_bounds__(kThreads, 1)
     int hs = 0, ws = 0;
     uint32_t hph = 0, wph = 0;
     const uint32_t wbytes = 3 * a.w_tap;
-    for (int u = blockIdx.x; u < a.num_units; u += gridDim.x) {
-      const int n = u / a.units_per_img;
-      const int f0 = (u - n * a.units_per_img) * kS * 128;
+    UnitIter it(a.num_tiles, a.T);
+    int n, tile0, ntiles;
+    while (it.next(n, tile0, ntiles)) {
+      const int f0 = tile0 * 128;
       const int y0 = f0 / Wp;
       for (int c = 0; c < a.nchunks; ++c) {
         mbar_wait(&halo_empty[hs], hph ^ 1);
@@ -184,24 +207,29 @@ __global__ void __launch_bounds__(kThreads, 1)
     const uint64_t wtap = (uint64_t)(a.w_tap >> 4);
     int hs = 0, ws = 0, ab = 0;
     uint32_t hph = 0, wph = 0, aph = 0;
-    for (int u = blockIdx.x; u < a.num_units; u += gridDim.x) {
-      const int n = u / a.units_per_img;
-      const int tile0 = (u - n * a.units_per_img) * kS;
-      const int ntiles = min(kS, a.T - tile0);               // warp-uniform
+    UnitIter it(a.num_tiles, a.T);
+    int n, tile0, ntiles, ui = 0;
+    while (it.next(n, tile0, ntiles)) {                       // warp-uniform
+      const int u = ui++;
       const int f0 = tile0 * 128;
       const int c0 = f0 - (f0 / Wp) * Wp;
       mbar_wait(&acc_empty[ab], aph ^ 1);
       tc_fence_after();
-      if (a.trace && blockIdx.x < 2 && lane == 0) a.trace[(blockIdx.x * 64 + (u / gridDim.x)) * 8 + 0] = globaltimer_ns();
+      if (a.trace && blockIdx.x < 2 && lane == 0 && u < 64) a.trace[(blockIdx.x * 64 + u) * 8 + 0] = globaltimer_ns();
       const uint32_t d0 = tmem_base + (uint32_t)(ab * kS * 128);
+      long long wait_h = 0, wait_w = 0;
       for (int c = 0; c < a.nchunks; ++c) {
+        long long tw = a.trace ? clock64() : 0;
         mbar_wait(THREE ? &halo_conv[hs] : &halo_full[hs], hph);
+        if (a.trace) wait_h += clock64() - tw;
         tc_fence_after();
-        if (a.trace && blockIdx.x < 2 && lane == 0) a.trace[(blockIdx.x * 64 + (u / gridDim.x)) * 8 + 4 + (c < 3 ? c : 3)] = globaltimer_ns();
+        if (a.trace && blockIdx.x < 2 && lane == 0 && u < 64 && c == 0) a.trace[(blockIdx.x * 64 + u) * 8 + 4] = globaltimer_ns();
         const uint64_t dxh0 = desc_kmajor_interleave(smem_u32(halo_raw(hs)), kg_x, 128);
         const uint64_t dxl0 = desc_kmajor_interleave(smem_u32(halo_lo(hs)), kg_x, 128);
         for (int dy = 0; dy < 3; ++dy) {
+          long long tw2 = a.trace ? clock64() : 0;
           mbar_wait(&w_full[ws], wph);
+          if (a.trace) wait_w += clock64() - tw2;
           tc_fence_after();
           const uint64_t dw0 = desc_kmajor_interleave(smem_u32(w_s(ws)), kg_w, 128);
           const int64_t row = c0 + dy * Wp - 1;              // positions; >= -1
@@ -215,12 +243,25 @@ __global__ void __launch_bounds__(kThreads, 1)
               for (int j = 0; j < 2; ++j) {
                 const uint64_t da = dw0 + dx * wtap + j * wj;   // A: weights, shared by the next MMAs
                 const uint32_t accum = (first && dx == 0 && j == 0) ? 0u : 1u;
+                // the 2 ntiles MMAs (tiles x {x_hi, x_lo}) may read A through the collector
+                if (THREE && kUseCollector) {
+                  const uint64_t b0 = (uint64_t)dx + j * xj;
+                  mma_tf32_c<1>(d0, da, bh + b0, id, accum);
+                  if (ntiles > 1) {
+                    mma_tf32_c<2>(d0, da, bl + b0, id, 1u);
+                    mma_tf32_c<2>(d0 + 128, da, bh + b0 + 128, id, accum);
+                    mma_tf32_c<3>(d0 + 128, da, bl + b0 + 128, id, 1u);
+                  } else {
+                    mma_tf32_c<3>(d0, da, bl + b0, id, 1u);
+                  }
+                } else {
 #pragma unroll
-                for (int s = 0; s < kS; ++s) {
-                  if (s < ntiles) {
-                    const uint64_t boff = (uint64_t)(dx + 128 * s) + j * xj;
-                    mma_tf32(d0 + s * 128, da, bh + boff, id, accum);
-                    if (THREE) mma_tf32(d0 + s * 128, da, bl + boff, id, 1u);
+                  for (int s = 0; s < kS; ++s) {
+                    if (s < ntiles) {
+                      const uint64_t boff = (uint64_t)(dx + 128 * s) + j * xj;
+                      mma_tf32(d0 + s * 128, da, bh + boff, id, accum);
+                      if (THREE) mma_tf32(d0 + s * 128, da, bl + boff, id, 1u);
+                    }
                   }
                 }
               }
@@ -236,7 +277,11 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
       if (elect_one()) mma_commit(&acc_full[ab]);
       __syncwarp();
-      if (a.trace && blockIdx.x < 2 && lane == 0) a.trace[(blockIdx.x * 64 + (u / gridDim.x)) * 8 + 1] = globaltimer_ns();
+      if (a.trace && blockIdx.x < 2 && lane == 0 && u < 64) {
+        a.trace[(blockIdx.x * 64 + u) * 8 + 1] = globaltimer_ns();
+        a.trace[(blockIdx.x * 64 + u) * 8 + 5] = (unsigned long long)wait_h;   // cycles waiting for the halo
+        a.trace[(blockIdx.x * 64 + u) * 8 + 6] = (unsigned long long)wait_w;   // cycles waiting for weights
+      }
       if (++ab == 2) ab = 0, aph ^= 1;
     }
   } else if (warp < 6) {
@@ -246,12 +291,14 @@ __global__ void __launch_bounds__(kThreads, 1)
       int hs = 0;
       uint32_t hph = 0;
       const int n16 = (int)(a.halo_bytes / 16);
-      for (int u = blockIdx.x; u < a.num_units; u += gridDim.x) {
+      UnitIter it(a.num_tiles, a.T);
+      int n, tile0, ntiles;
+      while (it.next(n, tile0, ntiles)) {
         for (int c = 0; c < a.nchunks; ++c) {
           mbar_wait(&halo_full[hs], hph);
           float4* raw = reinterpret_cast<float4*>(halo_raw(hs));
           float4* lo = reinterpret_cast<float4*>(halo_lo(hs));
-          for (int i = tid; i < n16; i += 128) {
+          for (int i = tid; i < ((a.dbg & 2) ? 0 : n16); i += 128) {
             const float4 v = raw[i];
             float4 l;
             l.x = v.x - trunc_tf32(v.x); l.y = v.y - trunc_tf32(v.y);
@@ -278,15 +325,15 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int own0 = hi_warp ? 0 : 32;      // positions [own0, own0 + 32) of each 64-batch are ours
     int ab = 0, xb = 0;
     uint32_t aph = 0;
-    for (int u = blockIdx.x; u < a.num_units; u += gridDim.x) {
-      const int n = u / a.units_per_img;
-      const int tile0 = (u - n * a.units_per_img) * kS;
-      const int ntiles = min(kS, a.T - tile0);
+    UnitIter it(a.num_tiles, a.T);
+    int n, tile0, ntiles, ui = 0;
+    while (it.next(n, tile0, ntiles)) {
+      const int u = ui++;
       const int64_t img = (int64_t)n * a.H * a.W;
       mbar_wait(&acc_full[ab], aph);
       tc_fence_after();
-      if (a.trace && blockIdx.x < 2 && threadIdx.x == 192) a.trace[(blockIdx.x * 64 + (u / gridDim.x)) * 8 + 2] = globaltimer_ns();
-      for (int s = 0; s < ntiles; ++s) {
+      if (a.trace && blockIdx.x < 2 && threadIdx.x == 192) a.trace[(blockIdx.x * 64 + min(u, 63)) * 8 + 2] = globaltimer_ns();
+      for (int s = 0; s < ((a.dbg & 1) ? 0 : ntiles); ++s) {
         const uint32_t tcol = tmem_base + ((uint32_t)(q * 32) << 16) + (uint32_t)((ab * kS + s) * 128);
         for (int p0 = 0; p0 < 128; p0 += 64) {
           uint32_t r[64];
@@ -336,7 +383,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           xb ^= 1;
         }
       }
-      if (a.trace && blockIdx.x < 2 && threadIdx.x == 192) a.trace[(blockIdx.x * 64 + (u / gridDim.x)) * 8 + 3] = globaltimer_ns();
+      if (a.trace && blockIdx.x < 2 && threadIdx.x == 192) a.trace[(blockIdx.x * 64 + min(u, 63)) * 8 + 3] = globaltimer_ns();
       tc_fence_before();
       mbar_arrive(&acc_empty[ab]);
       if (++ab == 2) ab = 0, aph ^= 1;
@@ -500,8 +547,7 @@ void conv3x3_fwd_tc(const ConvShape& s, const float* in, const float* w_hwio, bo
   a.Wp = p.Wp;
   a.rows_h = p.rows_h;
   a.T = p.T;
-  a.units_per_img = p.units_per_img;
-  a.num_units = s.n * p.units_per_img;
+  a.num_tiles = s.n * p.T;
   a.halo_pos = p.halo_pos;
   a.nchunks = s.ci / kChunk;
   a.halo_bytes = p.halo_bytes;
@@ -513,8 +559,9 @@ void conv3x3_fwd_tc(const ConvShape& s, const float* in, const float* w_hwio, bo
   a.aux = aux;
   a.out = out;
   a.trace = g_trace;
+  a.dbg = getenv("RP_CONV_DBG") ? atoi(getenv("RP_CONV_DBG")) : 0;
   const CUtensorMap& m = cached_map(in, s, p.Wp, p.rows_h);
-  const int grid = std::min(a.num_units, kNumSMs);
+  const int grid = std::min(a.num_tiles, kNumSMs);
   switch (epi) {
     case EPI_BIAS: launch_epi<EPI_BIAS>(m, a, three, p.smem, grid, st); break;
     case EPI_BIAS_TANH: launch_epi<EPI_BIAS_TANH>(m, a, three, p.smem, grid, st); break;

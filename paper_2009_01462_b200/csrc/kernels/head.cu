@@ -11,6 +11,43 @@ namespace rp::k {
 namespace {
 
 // pooled[b][c] = mean_p x[b][p][c]; one CTA per sample.
+// pooled[b][c] = mean_p x[b][p][c].  One CTA per image; thread (group g, float4 lane q)
+// sums positions g, g + G, ... (8 loads in flight), groups combined in fixed order.
+constexpr int kGapThreads = 512;
+__global__ __launch_bounds__(kGapThreads) void gap_kernel_vec4(const float4* __restrict__ x, int hw, int C4,
+                                                              float* __restrict__ pooled) {
+  extern __shared__ float4 sh4[];
+  const int b = blockIdx.x;
+  const float4* xb = x + (int64_t)b * hw * C4;
+  const int groups = kGapThreads / C4;     // C4 divides kGapThreads (host check)
+  const int g = threadIdx.x / C4, q = threadIdx.x % C4;
+  float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+  int p = g;
+  for (; p + 7 * groups < hw; p += 8 * groups) {
+    float4 v[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) v[u] = __ldg(xb + (int64_t)(p + u * groups) * C4 + q);
+#pragma unroll
+    for (int u = 0; u < 8; ++u) acc.x += v[u].x, acc.y += v[u].y, acc.z += v[u].z, acc.w += v[u].w;
+  }
+  for (; p < hw; p += groups) {
+    const float4 v = __ldg(xb + (int64_t)p * C4 + q);
+    acc.x += v.x, acc.y += v.y, acc.z += v.z, acc.w += v.w;
+  }
+  sh4[threadIdx.x] = acc;
+  __syncthreads();
+  if (threadIdx.x < C4) {
+    float4 s = make_float4(0.f, 0.f, 0.f, 0.f);
+    for (int gg = 0; gg < groups; ++gg) {
+      const float4 v = sh4[gg * C4 + threadIdx.x];
+      s.x += v.x, s.y += v.y, s.z += v.z, s.w += v.w;
+    }
+    const float inv = 1.f / (float)hw;
+    reinterpret_cast<float4*>(pooled)[(int64_t)b * C4 + threadIdx.x] =
+        make_float4(s.x * inv, s.y * inv, s.z * inv, s.w * inv);
+  }
+}
+
 __global__ __launch_bounds__(256) void gap_kernel(const float* __restrict__ x, int hw, int C,
                                                  float* __restrict__ pooled) {
   extern __shared__ float sh[];
@@ -83,28 +120,33 @@ __global__ void loss_grad_kernel(const float* __restrict__ logits, const int32_t
 }
 
 // gt_w[c][j] = sum_b pooled[b][c] glog[b][j]; gt_b[j] = sum_b glog[b][j]; loss = mean loss_b.
+// gt_w[c][j] = sum_b pooled[b][c] glog[b][j], gt_b[j] = sum_b glog[b][j], loss = mean_b
+// loss_b: one warp per output, lanes stride the rows, fixed shuffle order (fp64).
 __global__ void head_param_grad_kernel(const float* __restrict__ pooled, const float* __restrict__ glog,
                                        const double* __restrict__ loss_b, int nrows, int C, int classes,
                                        float* __restrict__ gt_w, float* __restrict__ gt_b, double* __restrict__ loss) {
-  const int total = C * classes + classes;
-  for (int idx = blockIdx.x * blockDim.x + threadIdx.x; idx < total; idx += gridDim.x * blockDim.x) {
-    if (idx < C * classes) {
-      const int c = idx / classes, j = idx % classes;
-      double s = 0.0;
-      for (int b = 0; b < nrows; ++b) s += (double)pooled[(int64_t)b * C + c] * (double)glog[(int64_t)b * classes + j];
-      gt_w[idx] = (float)s;
-    } else {
-      const int j = idx - C * classes;
-      double s = 0.0;
-      for (int b = 0; b < nrows; ++b) s += (double)glog[(int64_t)b * classes + j];
-      gt_b[j] = (float)s;
-    }
+  const int total = C * classes + classes + 1;
+  const int w = (blockIdx.x * blockDim.x + threadIdx.x) / 32, lane = threadIdx.x & 31;
+  if (w >= total) return;
+  double s = 0.0;
+  if (w < C * classes) {
+    const int c = w / classes, j = w % classes;
+    for (int b = lane; b < nrows; b += 32) s += (double)pooled[(int64_t)b * C + c] * (double)glog[(int64_t)b * classes + j];
+  } else if (w < C * classes + classes) {
+    const int j = w - C * classes;
+    for (int b = lane; b < nrows; b += 32) s += (double)glog[(int64_t)b * classes + j];
+  } else {
+    for (int b = lane; b < nrows; b += 32) s += loss_b[b];
   }
-  if (blockIdx.x == 0 && threadIdx.x == 0 && loss) {
-    double s = 0.0;
-    for (int b = 0; b < nrows; ++b) s += loss_b[b];
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+  if (lane != 0) return;
+  if (w < C * classes)
+    gt_w[w] = (float)s;
+  else if (w < C * classes + classes)
+    gt_b[w - C * classes] = (float)s;
+  else if (loss)
     *loss = s / (double)nrows;
-  }
 }
 
 // g[b][p][c] = gpool[b][c] / hw  (d mean / d x)
@@ -153,7 +195,12 @@ void head_forward(int nrows, int hw, int C, int classes, const float* x_end, con
   if (nrows <= 0) return;
   const int cw = C < 256 ? C : 256;
   const int groups = C <= 256 ? (256 / C > 0 ? 256 / C : 1) : 1;
-  gap_kernel<<<nrows, 256, groups * cw * sizeof(float), st>>>(x_end, hw, C, pooled);
+  if (C % 4 == 0 && kGapThreads % (C / 4) == 0 && (reinterpret_cast<uintptr_t>(x_end) & 15u) == 0) {
+    gap_kernel_vec4<<<nrows, kGapThreads, kGapThreads * sizeof(float4), st>>>(
+        reinterpret_cast<const float4*>(x_end), hw, C / 4, pooled);
+  } else {
+    gap_kernel<<<nrows, 256, groups * cw * sizeof(float), st>>>(x_end, hw, C, pooled);
+  }
   RP_LAUNCHED();
   fc_kernel<<<nrows, 32, 0, st>>>(pooled, t_w, t_b, C, classes, logits);
   RP_LAUNCHED();
@@ -169,9 +216,9 @@ void head_loss_backward(int nrows, int hw, int C, int classes, const float* pool
   float* gpool = reinterpret_cast<float*>(w + align256((int64_t)nrows * classes * 4) + align256((int64_t)nrows * 8));
   loss_grad_kernel<<<nrows, 128, 0, st>>>(logits, labels, t_w, nrows, C, classes, glog, loss_b, gpool);
   RP_LAUNCHED();
-  const int total = C * classes + classes;
-  head_param_grad_kernel<<<ceil_div(total, 128), 128, 0, st>>>(pooled, glog, loss_b, nrows, C, classes, gt_w, gt_b,
-                                                               loss_dev);
+  const int total = C * classes + classes + 1;
+  head_param_grad_kernel<<<ceil_div((int64_t)total * 32, 256), 256, 0, st>>>(pooled, glog, loss_b, nrows, C, classes,
+                                                                            gt_w, gt_b, loss_dev);
   RP_LAUNCHED();
   const int64_t n = (int64_t)nrows * hw * C;
   const float inv = 1.f / (float)hw;

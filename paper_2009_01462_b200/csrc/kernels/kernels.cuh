@@ -64,6 +64,13 @@ int64_t conv3x3_wgrad_tc_ws_bytes(const ConvShape& s, bool three);
 void conv3x3_wgrad_tc(const ConvShape& s, const float* in, const float* g, float scale, float* gw, float* gb,
                       bool three, void* ws, cudaStream_t st);
 
+// ---- stem S (stem.cu): Cin <= 4 streaming kernels (SIMT conv path otherwise)
+bool stem_supported(const ConvShape& s);
+int64_t stem_wgrad_ws_bytes(const ConvShape& s);
+void stem_fwd(const ConvShape& s, const float* x, const float* w, const float* b, float* out, cudaStream_t st);
+void stem_wgrad(const ConvShape& s, const float* x, const float* g, float scale, float* gw, float* gb, void* ws,
+                cudaStream_t st);
+
 // ---- head (head.cu) -------------------------------------------------------
 int64_t head_ws_bytes(int nrows, int channels, int classes);
 void head_forward(int nrows, int hw, int channels, int classes, const float* x_end, const float* t_w,

@@ -1,0 +1,298 @@
+// The stem S: a 3x3 conv from the raw image channels (Cin <= 4) to C channels
+// (affine_forward S, network.cpp:108-110, as a conv) and its weight gradient
+// (net_vjp's S grads, network.cpp:165-170).  With Cin = 3 the conv is 27 MACs per
+// output: the cost is writing / reading the C-channel activation, so these kernels
+// are plain CUDA-core streaming kernels sized for HBM, not implicit GEMMs.
+//
+//   fwd  : x0[p][co] = s_b[co] + sum_{tap, ci} x[p + off(tap)][ci] * s_w[tap][ci][co]
+//   wgrad: gw[tap][ci][co] = scale * sum_p x[p + off(tap)][ci] * g[p][co],
+//          gb[co] = scale * sum_p g[p][co]   (deterministic: fixed position ranges per
+//          CTA, fixed-order lane / CTA reductions)
+#include "../common.cuh"
+#include "kernels.cuh"
+
+namespace rp::k {
+
+namespace {
+
+constexpr int kStemMaxCin = 4;
+constexpr int kStemGrid = 8 * kNumSMs;   // wgrad partials (8 CTAs / SM hide the gather latency)
+
+template <int Cin>
+__global__ __launch_bounds__(256) void stem_fwd_kernel(const float* __restrict__ x, const float* __restrict__ w,
+                                                       const float* __restrict__ b, int N, int H, int W, int C,
+                                                       float* __restrict__ out) {
+  extern __shared__ float ws[];   // [9 * Cin * C] weights then [C] bias
+  const int nw = 9 * Cin * C;
+  for (int i = threadIdx.x; i < nw + C; i += blockDim.x) ws[i] = i < nw ? w[i] : b[i - nw];
+  __syncthreads();
+  const int groups = C / 16;
+  const int64_t items = (int64_t)N * H * W * groups;
+  for (int64_t it = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; it < items;
+       it += (int64_t)gridDim.x * blockDim.x) {
+    const int cg = (int)(it % groups);
+    const int64_t p = it / groups;
+    const int xq = (int)(p % W);
+    const int yq = (int)((p / W) % H);
+    const int64_t n = p / ((int64_t)W * H);
+    const int c0 = cg * 16;
+    float acc[16];
+#pragma unroll
+    for (int j = 0; j < 16; ++j) acc[j] = ws[nw + c0 + j];
+#pragma unroll
+    for (int tap = 0; tap < 9; ++tap) {
+      const int yy = yq + tap / 3 - 1, xx = xq + tap % 3 - 1;
+      if (yy < 0 || yy >= H || xx < 0 || xx >= W) continue;
+      const float* xp = x + ((n * H + yy) * W + xx) * Cin;
+#pragma unroll
+      for (int ci = 0; ci < Cin; ++ci) {
+        const float v = __ldg(xp + ci);
+        const float4* wr = reinterpret_cast<const float4*>(ws + (tap * Cin + ci) * C + c0);
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const float4 wv = wr[q];
+          acc[4 * q + 0] = fmaf(v, wv.x, acc[4 * q + 0]);
+          acc[4 * q + 1] = fmaf(v, wv.y, acc[4 * q + 1]);
+          acc[4 * q + 2] = fmaf(v, wv.z, acc[4 * q + 2]);
+          acc[4 * q + 3] = fmaf(v, wv.w, acc[4 * q + 3]);
+        }
+      }
+    }
+    float4* o = reinterpret_cast<float4*>(out + p * C + c0);
+#pragma unroll
+    for (int q = 0; q < 4; ++q) o[q] = make_float4(acc[4 * q], acc[4 * q + 1], acc[4 * q + 2], acc[4 * q + 3]);
+  }
+}
+
+// Register-blocked variant for W % 4 == 0: a thread computes 4 consecutive positions
+// of one row x 16 channels, so every weight float4 read from smem feeds 16 FMAs.
+template <int Cin>
+__global__ __launch_bounds__(256, 2) void stem_fwd4_kernel(const float* __restrict__ x, const float* __restrict__ w,
+                                                        const float* __restrict__ b, int N, int H, int W, int C,
+                                                        float* __restrict__ out) {
+  extern __shared__ float ws[];
+  const int nw = 9 * Cin * C;
+  for (int i = threadIdx.x; i < nw + C; i += blockDim.x) ws[i] = i < nw ? w[i] : b[i - nw];
+  __syncthreads();
+  const int groups = C / 16;
+  const int64_t items = (int64_t)N * H * (W / 4) * groups;
+  for (int64_t it = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; it < items;
+       it += (int64_t)gridDim.x * blockDim.x) {
+    const int cg = (int)(it % groups);
+    const int64_t q = it / groups;                     // quad of positions
+    const int x0 = (int)(q % (W / 4)) * 4;
+    const int yq = (int)((q / (W / 4)) % H);
+    const int64_t n = q / ((int64_t)(W / 4) * H);
+    const int c0 = cg * 16;
+    float acc[4][16];
+#pragma unroll
+    for (int j = 0; j < 16; ++j) {
+      const float bj = ws[nw + c0 + j];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) acc[i][j] = bj;
+    }
+#pragma unroll
+    for (int dy = 0; dy < 3; ++dy) {
+      const int yy = yq + dy - 1;
+      if (yy < 0 || yy >= H) continue;
+      const float* row = x + (n * H + yy) * (int64_t)W * Cin;
+      // the 6 input columns x0-1 .. x0+4 of this row (zero outside)
+      float xv[6][Cin];
+#pragma unroll
+      for (int k = 0; k < 6; ++k) {
+        const int xx = x0 + k - 1;
+#pragma unroll
+        for (int ci = 0; ci < Cin; ++ci) xv[k][ci] = (xx >= 0 && xx < W) ? __ldg(row + (int64_t)xx * Cin + ci) : 0.f;
+      }
+#pragma unroll
+      for (int dx = 0; dx < 3; ++dx) {
+#pragma unroll
+        for (int ci = 0; ci < Cin; ++ci) {
+          const float4* wr = reinterpret_cast<const float4*>(ws + ((dy * 3 + dx) * Cin + ci) * C + c0);
+#pragma unroll
+          for (int qq = 0; qq < 4; ++qq) {
+            const float4 wv = wr[qq];
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+              const float v = xv[i + dx][ci];
+              acc[i][4 * qq + 0] = fmaf(v, wv.x, acc[i][4 * qq + 0]);
+              acc[i][4 * qq + 1] = fmaf(v, wv.y, acc[i][4 * qq + 1]);
+              acc[i][4 * qq + 2] = fmaf(v, wv.z, acc[i][4 * qq + 2]);
+              acc[i][4 * qq + 3] = fmaf(v, wv.w, acc[i][4 * qq + 3]);
+            }
+          }
+        }
+      }
+    }
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      float4* o = reinterpret_cast<float4*>(out + ((n * H + yq) * (int64_t)W + x0 + i) * C + c0);
+#pragma unroll
+      for (int qq = 0; qq < 4; ++qq)
+        o[qq] = make_float4(acc[i][4 * qq], acc[i][4 * qq + 1], acc[i][4 * qq + 2], acc[i][4 * qq + 3]);
+    }
+  }
+}
+
+// Weight gradient as a small GEMM gW[r][co] = sum_p X[p][r] g[p][co] over the im2col
+// rows r = (tap, ci) plus a ones row (r = 9 Cin: the bias).  CTA b owns positions
+// [b P / G, (b+1) P / G), staged PC at a time into smem; thread (half h, row quad rb,
+// channel quad cb) accumulates a 4 x 4 register tile over the positions pp = h mod halves.
+template <int Cin>
+__global__ __launch_bounds__(256) void stem_wgrad_gemm_kernel(const float* __restrict__ x,
+                                                              const float* __restrict__ g, int N, int H, int W,
+                                                              int C, int PC, float* __restrict__ part) {
+  constexpr int R = 9 * Cin + 1;
+  constexpr int RP = (R + 3) / 4 * 4;
+  extern __shared__ __align__(16) float sm[];
+  float* X = sm;                   // [PC][RP]
+  float* G = sm + PC * RP;         // [PC][C]
+  const int C4 = C / 4, nt = (RP / 4) * C4;
+  const int halves = max(1, 256 / nt);
+  const int t = threadIdx.x;
+  const int h = t / nt, rb = (t % nt) / C4, cb = t % C4;
+  const bool active = h < halves;
+  const int64_t P = (int64_t)N * H * W;
+  const int64_t p0 = blockIdx.x * P / gridDim.x, p1 = (blockIdx.x + 1) * P / gridDim.x;
+  float acc[4][4] = {};
+  for (int64_t c0 = p0; c0 < p1; c0 += PC) {
+    const int np = (int)(p1 - c0 < (int64_t)PC ? p1 - c0 : (int64_t)PC);
+    __syncthreads();
+#pragma unroll 4
+    for (int i = t; i < PC * RP; i += blockDim.x) {
+      const int pp = i / RP, r = i % RP;
+      float v = 0.f;
+      if (pp < np) {
+        if (r < 9 * Cin) {
+          const int64_t p = c0 + pp;
+          const int xq = (int)(p % W), yq = (int)((p / W) % H);
+          const int64_t n = p / ((int64_t)W * H);
+          const int tap = r / Cin, ci = r % Cin;
+          const int yy = yq + tap / 3 - 1, xx = xq + tap % 3 - 1;
+          if (yy >= 0 && yy < H && xx >= 0 && xx < W) v = __ldg(x + ((n * H + yy) * W + xx) * Cin + ci);
+        } else if (r == 9 * Cin) {
+          v = 1.f;
+        }
+      }
+      X[i] = v;
+    }
+    const float4* g4 = reinterpret_cast<const float4*>(g + c0 * C);
+    float4* G4 = reinterpret_cast<float4*>(G);
+#pragma unroll 4
+    for (int i = t; i < PC * C4; i += blockDim.x)
+      G4[i] = i < np * C4 ? __ldg(g4 + i) : make_float4(0.f, 0.f, 0.f, 0.f);
+    __syncthreads();
+    if (active) {
+      const float4* X4 = reinterpret_cast<const float4*>(X);
+      for (int pp = h; pp < np; pp += halves) {
+        const float4 xv = X4[pp * (RP / 4) + rb];
+        const float4 gv = G4[pp * C4 + cb];
+        const float xa[4] = {xv.x, xv.y, xv.z, xv.w};
+        const float ga[4] = {gv.x, gv.y, gv.z, gv.w};
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+#pragma unroll
+          for (int j = 0; j < 4; ++j) acc[i][j] = fmaf(xa[i], ga[j], acc[i][j]);
+      }
+    }
+  }
+  // fixed-order combine of the halves, then the CTA partial [RP][C]
+  __syncthreads();
+  float* red = sm;                 // [halves][RP][C]
+  if (active)
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+      for (int j = 0; j < 4; ++j) red[((size_t)h * RP + rb * 4 + i) * C + cb * 4 + j] = acc[i][j];
+  __syncthreads();
+  for (int i = t; i < RP * C; i += blockDim.x) {
+    float s = 0.f;
+    for (int hh = 0; hh < halves; ++hh) s += red[(size_t)hh * RP * C + i];
+    part[(int64_t)blockIdx.x * RP * C + i] = s;
+  }
+}
+
+// out[i] = scale * sum_b part[b][i], one warp per output, fixed lane striding and
+// shuffle order.  i < 9 Cin C -> gw (HWIO == [tap][ci][co]); the next C -> gb.
+// Partials have `rows` rows of C per CTA (rows >= 9 Cin + 1; padding rows ignored).
+__global__ void stem_wgrad_reduce_kernel(const float* __restrict__ part, int grid, int Cin, int C, int rows,
+                                         double scale, float* __restrict__ gw, float* __restrict__ gb) {
+  const int R = 9 * Cin + 1;
+  const int warp = (blockIdx.x * blockDim.x + threadIdx.x) / 32, lane = threadIdx.x & 31;
+  if (warp >= R * C) return;
+  double s = 0.0;
+  for (int b = lane; b < grid; b += 32) s += (double)part[(int64_t)b * rows * C + warp];
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+  if (lane == 0) {
+    const int r = warp / C;
+    if (r < 9 * Cin)
+      gw[warp] = (float)(scale * s);
+    else if (gb)
+      gb[warp - 9 * Cin * C] = (float)(scale * s);
+  }
+}
+
+}  // namespace
+
+bool stem_supported(const ConvShape& s) {
+  return s.ci >= 1 && s.ci <= kStemMaxCin && s.co % 16 == 0 && s.co <= 256 && 256 % s.co == 0;
+}
+
+int64_t stem_wgrad_ws_bytes(const ConvShape& s) {
+  return (int64_t)kStemGrid * ((9 * s.ci + 1 + 3) / 4 * 4) * s.co * 4 + 256;
+}
+
+void stem_fwd(const ConvShape& s, const float* x, const float* w, const float* b, float* out, cudaStream_t st) {
+  const int64_t items = s.pixels() * (s.co / 16);
+  const int grid = (int)std::min<int64_t>((items + 255) / 256, 32 * kNumSMs);
+  const size_t smem = (size_t)(9 * s.ci * s.co + s.co) * 4;
+  const dim3 gr(std::max(grid, 1));
+  if (s.w % 4 == 0) {
+    const int64_t items4 = s.pixels() / 4 * (s.co / 16);
+    const dim3 gr4((unsigned)std::max<int64_t>(1, std::min<int64_t>((items4 + 255) / 256, 32 * kNumSMs)));
+    switch (s.ci) {
+      case 1: stem_fwd4_kernel<1><<<gr4, 256, smem, st>>>(x, w, b, s.n, s.h, s.w, s.co, out); break;
+      case 2: stem_fwd4_kernel<2><<<gr4, 256, smem, st>>>(x, w, b, s.n, s.h, s.w, s.co, out); break;
+      case 3: stem_fwd4_kernel<3><<<gr4, 256, smem, st>>>(x, w, b, s.n, s.h, s.w, s.co, out); break;
+      default: stem_fwd4_kernel<4><<<gr4, 256, smem, st>>>(x, w, b, s.n, s.h, s.w, s.co, out); break;
+    }
+    RP_LAUNCHED();
+    return;
+  }
+  switch (s.ci) {
+    case 1: stem_fwd_kernel<1><<<gr, 256, smem, st>>>(x, w, b, s.n, s.h, s.w, s.co, out); break;
+    case 2: stem_fwd_kernel<2><<<gr, 256, smem, st>>>(x, w, b, s.n, s.h, s.w, s.co, out); break;
+    case 3: stem_fwd_kernel<3><<<gr, 256, smem, st>>>(x, w, b, s.n, s.h, s.w, s.co, out); break;
+    default: stem_fwd_kernel<4><<<gr, 256, smem, st>>>(x, w, b, s.n, s.h, s.w, s.co, out); break;
+  }
+  RP_LAUNCHED();
+}
+
+template <int Cin>
+void launch_wgrad_gemm(const ConvShape& s, const float* x, const float* g, float* part, cudaStream_t st) {
+  constexpr int RP = (9 * Cin + 1 + 3) / 4 * 4;
+  const int PC = std::max(16, std::min(64, 24 * 1024 / ((RP + s.co) * 4)));
+  const size_t smem = std::max<size_t>((size_t)PC * (RP + s.co) * 4,
+                                       (size_t)std::max(1, 256 / ((RP / 4) * (s.co / 4))) * RP * s.co * 4);
+  stem_wgrad_gemm_kernel<Cin><<<kStemGrid, 256, smem, st>>>(x, g, s.n, s.h, s.w, s.co, PC, part);
+}
+
+void stem_wgrad(const ConvShape& s, const float* x, const float* g, float scale, float* gw, float* gb, void* ws,
+                cudaStream_t st) {
+  float* part = static_cast<float*>(ws);
+  switch (s.ci) {
+    case 1: launch_wgrad_gemm<1>(s, x, g, part, st); break;
+    case 2: launch_wgrad_gemm<2>(s, x, g, part, st); break;
+    case 3: launch_wgrad_gemm<3>(s, x, g, part, st); break;
+    default: launch_wgrad_gemm<4>(s, x, g, part, st); break;
+  }
+  RP_LAUNCHED();
+  const int rows = (9 * s.ci + 1 + 3) / 4 * 4;
+  const int outs = (9 * s.ci + 1) * s.co;
+  stem_wgrad_reduce_kernel<<<ceil_div((int64_t)outs * 32, 256), 256, 0, st>>>(part, kStemGrid, s.ci, s.co, rows,
+                                                                              (double)scale, gw, gb);
+  RP_LAUNCHED();
+}
+
+}  // namespace rp::k

@@ -173,8 +173,10 @@ __global__ void __launch_bounds__(128, 1) umma_bench_kernel(int fmt, int N, int 
                                                             int nacc, int nops, int chain, float* out) {
   extern __shared__ __align__(1024) uint8_t sm[];
   __shared__ uint64_t bar;
+  __shared__ uint64_t bar2;
   __shared__ uint32_t slot;
   const int tid = threadIdx.x;
+  if (tid == 0) umma::mbar_init(&bar2, 1);
   for (int i = tid; i < 192 * 1024 / 4; i += 128) {
     uint32_t v = 0x3c003c00u;
     if (b_mn == 2) {   // pseudo-random finite fp32 in [1, 2) with random sign / mantissa
@@ -200,7 +202,7 @@ __global__ void __launch_bounds__(128, 1) umma_bench_kernel(int fmt, int N, int 
   if (warp_u == 0) {   // whole warp runs the issue loop; one elected lane issues
     const uint32_t a0 = umma::smem_u32(sm), b0 = umma::smem_u32(sm + 32 * 1024);
     uint64_t da, db;
-    if (layout == 0) {  // interleave: K-major lbo = rows*16, sbo = 128
+    if (layout == 0 || layout == 4) {  // interleave: K-major lbo = rows*16, sbo = 128 (4: M = 64)
       da = umma::desc_general(a0, 128 * 16, 128, 0, 0);
       db = umma::desc_general(b0, N * 16, 128, 0, 0);
     } else if (layout == 1 && a_mn) {   // SW128_32B MN-major: 32-element groups 8 KB apart
@@ -213,7 +215,7 @@ __global__ void __launch_bounds__(128, 1) umma_bench_kernel(int fmt, int N, int 
       da = umma::desc_general(a0, 16, 1024, layout, 0);
       db = umma::desc_general(b0, 16, 1024, layout, 0);
     }
-    const uint32_t id = umma::idesc(fmt, 128, N, a_mn, b_mn);
+    const uint32_t id = umma::idesc(fmt, layout == 4 ? 64 : 128, N, a_mn, b_mn);
     const uint32_t tm = __shfl_sync(0xffffffffu, tmem, 0);
     const long long t0 = clock64();
     if (nops == 98) {
@@ -226,6 +228,45 @@ __global__ void __launch_bounds__(128, 1) umma_bench_kernel(int fmt, int N, int 
           umma::mma_tf32_c<3>(tm + N, da, db + 768, id, 1);
         }
         __syncwarp();
+      }
+    } else if (nops == 89 || nops == 88 || nops == 87) {
+      // conv_tc fprop pattern (88: without the collector): A = weights [kg][128][4] (LBO
+      // 2 KB), 3 taps x 2 k-steps per stage; B = halo K-major interleave with LBO =
+      // chain*16 (halo positions), x_hi at 64 KB, x_lo at 96 KB, 2 tiles of 128 positions
+      const uint32_t w0 = umma::smem_u32(sm), xh = umma::smem_u32(sm + 64 * 1024), xl = umma::smem_u32(sm + 96 * 1024);
+      const uint32_t kgx = (uint32_t)chain * 16u;
+      const uint64_t dw = umma::desc_kmajor_interleave(w0, 2048, 128);
+      const uint64_t bh = umma::desc_kmajor_interleave(xh, kgx, 128);
+      const uint64_t bl = umma::desc_kmajor_interleave(xl, kgx, 128);
+      const uint32_t idn = umma::idesc(2, 128, 128);
+      const uint64_t xj = (uint64_t)((2 * kgx) >> 4);
+      int dy = 0;
+      for (int r = 0; r < reps; r += 24) {
+        const uint64_t row = (uint64_t)(dy * 34 + 5);
+        if (umma::elect_one()) {
+#pragma unroll
+          for (int dx = 0; dx < 3; ++dx) {
+#pragma unroll
+            for (int j = 0; j < 2; ++j) {
+              const uint64_t da = dw + dx * 512 + j * 256;
+              const uint64_t b0 = row + dx + j * xj;
+              if (nops != 88) {
+                umma::mma_tf32_c<1>(tm, da, bh + b0, idn, 1u);
+                umma::mma_tf32_c<2>(tm, da, bl + b0, idn, 1u);
+                umma::mma_tf32_c<2>(tm + 128, da, bh + b0 + 128, idn, 1u);
+                umma::mma_tf32_c<3>(tm + 128, da, bl + b0 + 128, idn, 1u);
+              } else {
+                umma::mma_tf32(tm, da, bh + b0, idn, 1u);
+                umma::mma_tf32(tm, da, bl + b0, idn, 1u);
+                umma::mma_tf32(tm + 128, da, bh + b0 + 128, idn, 1u);
+                umma::mma_tf32(tm + 128, da, bl + b0 + 128, idn, 1u);
+              }
+            }
+          }
+          if (nops == 87) umma::mma_commit(&bar2);   // 87: commit after every stage (as conv_tc)
+        }
+        __syncwarp();
+        if (++dy == 3) dy = 0;
       }
     } else if (nops == 93) {
       // 94 without the k-step advance (B offsets fixed per tap)

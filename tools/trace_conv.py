@@ -27,7 +27,7 @@ for math in ("fp32", "tf32"):
             row = t[cta, u]
             if row[0] == 0:
                 break
-            print(f" cta{cta} u{u}: mma_start {(row[0]-t0)/1e3:7.2f} halo_c0..3 " +
-                  " ".join(f"{(v-t0)/1e3:7.2f}" for v in row[4:8]) +
-                  f" mma_end {(row[1]-t0)/1e3:7.2f} epi_start {(row[2]-t0)/1e3:7.2f} epi_end {(row[3]-t0)/1e3:7.2f}")
+            print(f" cta{cta} u{u}: mma_start {(row[0]-t0)/1e3:7.2f} halo_c0 {(row[4]-t0)/1e3:7.2f}"
+                  f" mma_end {(row[1]-t0)/1e3:7.2f} epi_start {(row[2]-t0)/1e3:7.2f} epi_end {(row[3]-t0)/1e3:7.2f}"
+                  f"  wait_halo {row[5]/1965:6.2f}us wait_w {row[6]/1965:6.2f}us")
     tr.zero_()
