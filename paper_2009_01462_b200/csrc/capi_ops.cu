@@ -47,6 +47,7 @@ double conv_bytes(const k::ConvShape& s, bool aux) {
 
 void check_math(int math) {
   if (math < RP_MATH_FP32 || math > RP_MATH_SIMT) fail(RP_ERR_CONFIG, "unknown math mode");
+  if (math == RP_MATH_BF16) fail(RP_ERR_CONFIG, "RP_MATH_BF16: the bf16 conv kernels are not built yet");
 }
 
 }  // namespace

@@ -79,23 +79,43 @@ __device__ __forceinline__ float rna_tf32(float v) {
 // x_lo = x - trunc(x) (exact in fp32) has to be written.
 __device__ __forceinline__ float trunc_tf32(float v) { return __uint_as_float(__float_as_uint(v) & 0xffffe000u); }
 
-// Work split: CTA b owns the contiguous range [b*N*T/G, (b+1)*N*T/G) of the global tile
-// index n*T + t (tile = 128 frame positions of image n), walked in units of up to kS
-// tiles of one image.  Every CTA gets floor or ceil of the mean tile count (the old
-// round-robin over fixed 2-tile units left the busiest CTA 9% above the mean).
+// Work split.  A unit is kS tiles (128 frame positions each) of one image and one
+// 64-channel output block cb; T = ceil(frame / 128) tiles per image leaves one shorter
+// "tail" unit per image when kS does not divide T.  Full units go round-robin from CTA
+// 0 upwards, tail units round-robin from CTA G-1 downwards, so the CTAs that get one
+// full unit less get the extra tail: every CTA ends within one tile of the mean (plain
+// round-robin over mixed units left the busiest CTA 9% above it).  cb is the outermost
+// index, so CTAs working on the same images at the same time share the halo in L2.
 struct UnitIter {
-  int t, t_end, T;
-  __device__ UnitIter(int total, int T_) : T(T_) {
-    t = (int)((int64_t)blockIdx.x * total / gridDim.x);
-    t_end = (int)((int64_t)(blockIdx.x + 1) * total / gridDim.x);
+  int f, tl, nf, ntail, fu, T, NT, G;
+  __device__ UnitIter(int mtiles, int N, int T_) : T(T_) {
+    G = gridDim.x;
+    fu = T / kS;                              // full units per image
+    nf = mtiles * N * fu;
+    ntail = (T % kS) ? mtiles * N : 0;
+    NT = N;
+    f = blockIdx.x;
+    tl = G - 1 - (int)blockIdx.x;
   }
-  __device__ bool next(int& n, int& tile0, int& ntiles) {
-    if (t >= t_end) return false;
-    n = t / T;
-    tile0 = t - n * T;
-    ntiles = min(kS, min(T - tile0, t_end - t));
-    t += ntiles;
-    return true;
+  __device__ bool next(int& cb, int& n, int& tile0, int& ntiles) {
+    if (f < nf) {
+      cb = f / (NT * fu);
+      const int r = f - cb * NT * fu;
+      n = r / fu;
+      tile0 = (r - n * fu) * kS;
+      ntiles = kS;
+      f += G;
+      return true;
+    }
+    if (tl < ntail) {
+      cb = tl / NT;
+      n = tl - cb * NT;
+      tile0 = fu * kS;
+      ntiles = T - tile0;
+      tl += G;
+      return true;
+    }
+    return false;
   }
 };
 
@@ -173,9 +193,10 @@ __global__ void __launch_bounds__(kThreads, 1)
     int hs = 0, ws = 0;
     uint32_t hph = 0, wph = 0;
     const uint32_t wbytes = 3 * a.w_tap;
-    UnitIter it(a.num_tiles, a.T);
-    int n, tile0, ntiles;
-    while (it.next(n, tile0, ntiles)) {
+    UnitIter it(a.Co / 64, a.N, a.T);
+    int cb, n, tile0, ntiles;
+    while (it.next(cb, n, tile0, ntiles)) {
+      const float* wcb = a.w + (int64_t)cb * a.nchunks * 9 * (a.w_tap / 4);
       const int f0 = tile0 * 128;
       const int y0 = f0 / Wp;
       for (int c = 0; c < a.nchunks; ++c) {
@@ -190,7 +211,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           mbar_wait(&w_empty[ws], wph ^ 1);
           if (elect_one()) {
             mbar_arrive_expect_tx(&w_full[ws], wbytes);
-            bulk_load(w_s(ws), a.w + ((int64_t)c * 9 + 3 * dy) * (a.w_tap / 4), wbytes, &w_full[ws]);
+            bulk_load(w_s(ws), wcb + ((int64_t)c * 9 + 3 * dy) * (a.w_tap / 4), wbytes, &w_full[ws]);
           }
           __syncwarp();
           if (++ws == kWStages) ws = 0, wph ^= 1;
@@ -207,9 +228,9 @@ __global__ void __launch_bounds__(kThreads, 1)
     const uint64_t wtap = (uint64_t)(a.w_tap >> 4);
     int hs = 0, ws = 0, ab = 0;
     uint32_t hph = 0, wph = 0, aph = 0;
-    UnitIter it(a.num_tiles, a.T);
-    int n, tile0, ntiles, ui = 0;
-    while (it.next(n, tile0, ntiles)) {                       // warp-uniform
+    UnitIter it(a.Co / 64, a.N, a.T);
+    int cb, n, tile0, ntiles, ui = 0;
+    while (it.next(cb, n, tile0, ntiles)) {                   // warp-uniform
       const int u = ui++;
       const int f0 = tile0 * 128;
       const int c0 = f0 - (f0 / Wp) * Wp;
@@ -291,9 +312,9 @@ __global__ void __launch_bounds__(kThreads, 1)
       int hs = 0;
       uint32_t hph = 0;
       const int n16 = (int)(a.halo_bytes / 16);
-      UnitIter it(a.num_tiles, a.T);
-      int n, tile0, ntiles;
-      while (it.next(n, tile0, ntiles)) {
+      UnitIter it(a.Co / 64, a.N, a.T);
+      int cb, n, tile0, ntiles;
+      while (it.next(cb, n, tile0, ntiles)) {
         for (int c = 0; c < a.nchunks; ++c) {
           mbar_wait(&halo_full[hs], hph);
           float4* raw = reinterpret_cast<float4*>(halo_raw(hs));
@@ -320,16 +341,18 @@ __global__ void __launch_bounds__(kThreads, 1)
     // instruction (coalesced NHWC).
     const int q = warp & 3;                 // TMEM lane quadrant this warp may access
     const bool hi_warp = q < 2;
-    const int co = (q & 1) * 32 + lane;     // output channel of this lane
-    const float bias = (EPI == EPI_BIAS || EPI == EPI_BIAS_TANH || EPI == EPI_RESID) ? __ldg(a.bias + co) : 0.f;
+    const int co_l = (q & 1) * 32 + lane;   // output channel of this lane within the co block
+    constexpr bool kBias = EPI == EPI_BIAS || EPI == EPI_BIAS_TANH || EPI == EPI_RESID;
     const int own0 = hi_warp ? 0 : 32;      // positions [own0, own0 + 32) of each 64-batch are ours
     int ab = 0, xb = 0;
     uint32_t aph = 0;
-    UnitIter it(a.num_tiles, a.T);
-    int n, tile0, ntiles, ui = 0;
-    while (it.next(n, tile0, ntiles)) {
+    UnitIter it(a.Co / 64, a.N, a.T);
+    int cb, n, tile0, ntiles, ui = 0;
+    while (it.next(cb, n, tile0, ntiles)) {
       const int u = ui++;
       const int64_t img = (int64_t)n * a.H * a.W;
+      const int co = cb * 64 + co_l;
+      const float bias = kBias ? __ldg(a.bias + co) : 0.f;
       mbar_wait(&acc_full[ab], aph);
       tc_fence_after();
       if (a.trace && blockIdx.x < 2 && threadIdx.x == 192) a.trace[(blockIdx.x * 64 + min(u, 63)) * 8 + 2] = globaltimer_ns();
@@ -398,31 +421,35 @@ __global__ void __launch_bounds__(kThreads, 1)
   }
 }
 
-// weights HWIO src[tap][ci][co] -> prepped A operand [chunk][tap'][kg][128 rows][4]: row
-// r < 64 holds w_hi[co = r], r >= 64 holds w_lo[co = r - 64] (TF32 mode: the same
-// split; x enters truncated).  fprop (flip = 0) or dgrad (flip = 1: tap' = 8 - tap,
-// ci' = co, co' = ci).
+// weights HWIO src[tap][ci][co] -> prepped A operand [cb][chunk][tap'][kg][128 rows][4]
+// per 64-channel output block cb: row r < 64 holds w_hi[co = 64 cb + r], r >= 64 holds
+// w_lo[co = 64 cb + r - 64] (TF32 mode: the same split; x enters truncated).  fprop
+// (flip = 0) or dgrad (flip = 1: tap' = 8 - tap, ci' = co, co' = ci).
 __global__ void prep_weights_kernel(const float* __restrict__ w, int ci_src, int co_src, int flip,
                                     float* __restrict__ out) {
   const int Ci = flip ? co_src : ci_src;
-  const int Co = flip ? ci_src : co_src;   // == 64
-  const int total = 9 * Ci * 128;
-  for (int idx = blockIdx.x * blockDim.x + threadIdx.x; idx < total; idx += gridDim.x * blockDim.x) {
-    const int e = idx & 3;
-    const int r = (idx >> 2) & 127;
-    const int rest = idx >> 9;                   // (chunk, tap, kg)
-    const int kg = rest % 4;
-    const int tap = (rest / 4) % 9;
-    const int chunk = rest / 36;
+  const int Co = flip ? ci_src : co_src;   // multiple of 64
+  const int64_t per_cb = 9LL * Ci * 128;
+  const int64_t total = per_cb * (Co / 64);
+  for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total;
+       idx += (int64_t)gridDim.x * blockDim.x) {
+    const int cb = (int)(idx / per_cb);
+    const int64_t li = idx - cb * per_cb;
+    const int e = (int)(li & 3);
+    const int r = (int)((li >> 2) & 127);
+    const int64_t rest = li >> 9;               // (chunk, tap, kg)
+    const int kg = (int)(rest % 4);
+    const int tap = (int)((rest / 4) % 9);
+    const int chunk = (int)(rest / 36);
     const int ci = chunk * kChunk + kg * 4 + e;
-    const int co = r < Co ? r : r - Co;
+    const int co = cb * 64 + (r < 64 ? r : r - 64);
     float v;
     if (!flip)
       v = w[((int64_t)tap * ci_src + ci) * co_src + co];
     else
       v = w[((int64_t)(8 - tap) * ci_src + co) * co_src + ci];
     const float h = rna_tf32(v);
-    out[idx] = r < Co ? h : v - h;
+    out[idx] = r < 64 ? h : v - h;
   }
 }
 
@@ -469,7 +496,7 @@ struct Plan {
 
 Plan plan_for(const ConvShape& s) {
   Plan p;
-  if (s.co != 64 || s.ci % kChunk != 0 || s.w + 2 > 256) return p;
+  if (s.co % 64 != 0 || s.ci % kChunk != 0 || s.w + 2 > 256) return p;
   p.Wp = s.w + 2;
   p.rows_h = (3 * p.Wp + 128 * kS + p.Wp - 1) / p.Wp;
   if (p.rows_h > 256) return p;
@@ -523,7 +550,7 @@ bool conv3x3_tc_supported(const ConvShape& s) { return plan_for(s).ok; }
 
 void conv3x3_tc_set_trace(unsigned long long* p) { g_trace = p; }
 
-int64_t conv3x3_tc_ws_bytes(const ConvShape& s) { return 9LL * s.ci * 128 * 4 + 256; }
+int64_t conv3x3_tc_ws_bytes(const ConvShape& s) { return 9LL * s.ci * 2 * s.co * 4 + 256; }
 
 void conv3x3_fwd_tc(const ConvShape& s, const float* in, const float* w_hwio, bool dgrad_weights, const float* bias,
                     const float* aux, float h, int epi, float* out, bool three, void* ws, cudaStream_t st) {
@@ -535,8 +562,9 @@ void conv3x3_fwd_tc(const ConvShape& s, const float* in, const float* w_hwio, bo
   // (ci_src, co_src) = (s.co, s.ci)
   const int ci_src = dgrad_weights ? s.co : s.ci;
   const int co_src = dgrad_weights ? s.ci : s.co;
-  const int total = 9 * s.ci * 128;
-  prep_weights_kernel<<<ceil_div(total, 256), 256, 0, st>>>(w_hwio, ci_src, co_src, dgrad_weights ? 1 : 0, wp);
+  const int64_t total = 9LL * s.ci * 2 * s.co;
+  prep_weights_kernel<<<(int)std::min<int64_t>(ceil_div(total, 256), 16 * kNumSMs), 256, 0, st>>>(
+      w_hwio, ci_src, co_src, dgrad_weights ? 1 : 0, wp);
   RP_LAUNCHED();
   TcArgs a{};
   a.N = s.n;
@@ -547,7 +575,7 @@ void conv3x3_fwd_tc(const ConvShape& s, const float* in, const float* w_hwio, bo
   a.Wp = p.Wp;
   a.rows_h = p.rows_h;
   a.T = p.T;
-  a.num_tiles = s.n * p.T;
+  a.num_tiles = (s.co / 64) * s.n * p.T;
   a.halo_pos = p.halo_pos;
   a.nchunks = s.ci / kChunk;
   a.halo_bytes = p.halo_bytes;

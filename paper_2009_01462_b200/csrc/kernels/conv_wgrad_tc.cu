@@ -49,15 +49,15 @@ constexpr int kMaxStages = 4;
 constexpr int kMaxSmem = 227 * 1024;
 constexpr int kLead = 128;          // zero row in front of the x slabs (tap shift -1)
 constexpr int kTrail = 1024;        // zero rows behind them (K padding reads)
-constexpr int kMaxGroups = 4;
 constexpr int kMaxTaps = 5;         // taps per group (Ci = 32: 5 + 4)
 constexpr int kConvThreads = 256;   // warps 2..9 split the lo parts / bias sums
 
 struct WgArgs {
   int N, H, W, Ci, Co, Wp, rg, P, Pp, three, nstages;
-  int n2;                        // B columns per tap (2 Ci)
-  int tg;                        // taps per group (the last group may hold fewer)
-  int grp_cta[kMaxGroups + 1];   // CTA range of tap group i: [grp_cta[i], grp_cta[i+1])
+  int CiB;                       // input channels per ci block (Ci == 32: 32, else 64)
+  int mo, mi;                    // 64-channel co blocks, CiB-channel ci blocks
+  int n2;                        // B columns per tap (2 CiB)
+  int tg, ngroups;               // taps per tap group (the last may hold fewer), tap groups
   int blocks_per_img, num_blocks;
   uint32_t g_slab;               // bytes per 32-channel g slab (Pp rows of 128 B; rows >= P stay 0)
   uint32_t x_slab;               // bytes per x slab ((rg+2)*Wp rows of 128 B, packed)
@@ -75,6 +75,14 @@ struct WgArgs {
     if (a.trace && blockIdx.x < 2 && (b) - blk_beg < 64)                                       \
       a.trace[(blockIdx.x * 64 + ((b) - blk_beg)) * 8 + (slot)] = globaltimer_ns();            \
   } while (0)
+
+// Work groups gid = ((cob * mi + cib) * ngroups + gi) get CTAs in proportion to their
+// taps: group gid owns CTAs [grp_start(gid), grp_start(gid + 1)) of a `grid`-CTA launch.
+__device__ __forceinline__ int grp_start(int gid, int grid, const WgArgs& a) {
+  const int pair = gid / a.ngroups, gi = gid - pair * a.ngroups;
+  const int taps = pair * 9 + min(9, gi * a.tg);
+  return (int)((int64_t)grid * taps / (9 * a.mo * a.mi));
+}
 
 __device__ __forceinline__ float trunc_tf32(float v) { return __uint_as_float(__float_as_uint(v) & 0xffffe000u); }
 
@@ -94,7 +102,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   extern __shared__ __align__(1024) uint8_t smem[];
   const int warp = __shfl_sync(0xffffffffu, (int)threadIdx.x / 32, 0);   // warp-uniform role index
   const int lane = threadIdx.x & 31;
-  const int nx = a.Ci / 32;                       // x_hi slabs (as many x_lo slabs follow)
+  const int nx = a.CiB / 32;                      // x_hi slabs (as many x_lo slabs follow)
   const int S = a.nstages;
 
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + S * a.stage);
@@ -109,11 +117,12 @@ __global__ void __launch_bounds__(kThreads, 1)
   auto x_slab = [&](int s, int j) { return smem + s * a.stage + a.x_off + j * a.x_slab; };
 
   // CTA -> (tap group, contiguous block range)
-  int gi = 0, c_lo = a.grp_cta[0], c_hi = a.grp_cta[1];
-#pragma unroll
-  for (int i = 1; i < kMaxGroups; ++i)   // static indices: no local copy of the parameter array
-    if ((int)blockIdx.x >= a.grp_cta[i] && a.grp_cta[i] < a.grp_cta[i + 1])
-      gi = i, c_lo = a.grp_cta[i], c_hi = a.grp_cta[i + 1];
+  const int NG = a.mo * a.mi * a.ngroups;
+  int gid = 0;
+  while (gid + 1 < NG && grp_start(gid + 1, gridDim.x, a) <= (int)blockIdx.x) ++gid;
+  const int c_lo = grp_start(gid, gridDim.x, a), c_hi = grp_start(gid + 1, gridDim.x, a);
+  const int gi = gid % a.ngroups;
+  const int cib = (gid / a.ngroups) % a.mi, cob = gid / (a.ngroups * a.mi);
   const int jg = blockIdx.x - c_lo;
   const int ng = c_hi - c_lo;
   const int blk_beg = (int)((int64_t)jg * a.num_blocks / ng);
@@ -160,8 +169,9 @@ __global__ void __launch_bounds__(kThreads, 1)
       if (elect_one()) {
         WG_TRACE(0, b);
         mbar_arrive_expect_tx(&full[s], bytes);
-        for (int j = 0; j < 2; ++j) tma_load_4d(&tmap_g, &full[s], g_slab(s, j), 32 * j, -1, y0, n);
-        for (int j = 0; j < nx; ++j) tma_load_4d(&tmap_x, &full[s], x_slab(s, j), 32 * j, -1, y0 - 1, n);
+        for (int j = 0; j < 2; ++j) tma_load_4d(&tmap_g, &full[s], g_slab(s, j), 64 * cob + 32 * j, -1, y0, n);
+        for (int j = 0; j < nx; ++j)
+          tma_load_4d(&tmap_x, &full[s], x_slab(s, j), a.CiB * cib + 32 * j, -1, y0 - 1, n);
       }
       __syncwarp();
       if (++s == S) s = 0, ph ^= 1;
@@ -226,7 +236,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     // bias: per-block fp32 sums folded into Kahan-compensated fp32 running sums (fp64
     // arithmetic runs at a few ops/clk/SM on this part - too slow for the block loop)
     float bs[8] = {0, 0, 0, 0, 0, 0, 0, 0}, bc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-    const bool do_bias = gi == 0;
+    const bool do_bias = gi == 0 && cib == 0;
     const bool do_lo = a.three != 0;
     const int ng4 = a.Pp * 8;            // float4 per g slab
     const int nx4 = nx * (int)xrows * 8; // float4 over all x_hi slabs
@@ -292,7 +302,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       if (++s == S) s = 0, ph ^= 1;
     }
     const int cw = tid / 32;   // converter warp 0..7
-    if (gi == 0) {
+    if (do_bias) {
       // lanes l, l^10, l^20, l^30 hold the same channels: fixed-order butterfly, then lanes
       // 0..7 (rows p & 3 == 0) publish the warp's 64 sums.
       double bd[8];
@@ -325,7 +335,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       const int q = warp & 3;
       const int co = (q & 1) * 32 + lane;
       float* xbuf = reinterpret_cast<float*>(smem);     // [tg * Ci][64], reuses stage memory
-      float* dst = a.part + (size_t)blockIdx.x * a.tg * a.Ci * 64;
+      float* dst = a.part + (size_t)blockIdx.x * a.tg * a.CiB * 64;
       const bool any = blk_end > blk_beg;
       if (any) {
         mbar_wait(acc_full, 0);
@@ -336,12 +346,12 @@ __global__ void __launch_bounds__(kThreads, 1)
         const bool mine = (pass == 0) == (q >= 2);
         if (mine) {
           for (int ti = 0; ti < ntaps; ++ti) {
-            for (int c = 0; c < a.Ci; c += 16) {
+            for (int c = 0; c < a.CiB; c += 16) {
               uint32_t rh[16], rl[16];
               tmem_ld16(trow + (uint32_t)(ti * a.n2 + c), rh);
-              tmem_ld16(trow + (uint32_t)(ti * a.n2 + a.Ci + c), rl);
+              tmem_ld16(trow + (uint32_t)(ti * a.n2 + a.CiB + c), rl);
               tmem_wait_ld();
-              const int col0 = ti * a.Ci + c;
+              const int col0 = ti * a.CiB + c;
 #pragma unroll
               for (int e = 0; e < 16; ++e) {
                 const float v = any ? __uint_as_float(rh[e]) + __uint_as_float(rl[e]) : 0.f;
@@ -366,30 +376,31 @@ __global__ void __launch_bounds__(kThreads, 1)
   }
 }
 
-// gW[tap][ci][co] (HWIO) = scale * sum over the tap group's CTAs of part[cta][ti ci][co]
+// gW[tap][ci][co] (HWIO) = scale * sum over the work group's CTAs of part[cta][ti ci'][co']
 __global__ void wgrad_reduce_kernel(const float* __restrict__ part, const double* __restrict__ part_bias,
-                                    const WgArgs a, double scale, float* __restrict__ gw, float* __restrict__ gb) {
-  const int Ci = a.Ci, Co = 64;
+                                    const WgArgs a, int grid, double scale, float* __restrict__ gw,
+                                    float* __restrict__ gb) {
+  const int Ci = a.Ci, Co = a.Co;
   const int total = 9 * Ci * Co;
-  const int64_t pstride = (int64_t)a.tg * Ci * Co;
+  const int64_t pstride = (int64_t)a.tg * a.CiB * 64;
   for (int idx = blockIdx.x * blockDim.x + threadIdx.x; idx < total + Co; idx += gridDim.x * blockDim.x) {
     if (idx < total) {
       const int co = idx % Co;
       const int ci = (idx / Co) % Ci;
       const int tap = idx / (Co * Ci);
-      const int gi = tap / a.tg;
-      int c_lo = a.grp_cta[0], c_hi = a.grp_cta[1];
-#pragma unroll
-      for (int i = 1; i < kMaxGroups; ++i)
-        if (gi == i) c_lo = a.grp_cta[i], c_hi = a.grp_cta[i + 1];
-      const int64_t off = ((int64_t)(tap - gi * a.tg) * Ci + ci) * Co + co;
+      const int gi = tap / a.tg, cob = co / 64, cib = ci / a.CiB;
+      const int gid = (cob * a.mi + cib) * a.ngroups + gi;
+      const int c_lo = grp_start(gid, grid, a), c_hi = grp_start(gid + 1, grid, a);
+      const int64_t off = ((int64_t)(tap - gi * a.tg) * a.CiB + (ci - cib * a.CiB)) * 64 + (co - cob * 64);
       double s = 0.0;
       for (int b = c_lo; b < c_hi; ++b) s += (double)part[b * pstride + off];
       gw[idx] = (float)(scale * s);
     } else if (gb) {
-      const int co = idx - total;
+      const int co = idx - total, cob = co / 64;
+      const int gid = cob * a.mi * a.ngroups;
+      const int c_lo = grp_start(gid, grid, a), c_hi = grp_start(gid + 1, grid, a);
       double s = 0.0;
-      for (int b = a.grp_cta[0]; b < a.grp_cta[1]; ++b) s += part_bias[(int64_t)b * Co + co];
+      for (int b = c_lo; b < c_hi; ++b) s += part_bias[(int64_t)b * 64 + (co - cob * 64)];
       gb[co] = (float)(scale * s);
     }
   }
@@ -446,7 +457,7 @@ uint32_t round1k(uint64_t v) { return (uint32_t)((v + 1023) / 1024 * 1024); }
 
 struct WgPlan {
   bool ok = false;
-  int rg, P, Pp, tg, ngroups, grid, nstages;
+  int rg, P, Pp, tg, ngroups, grid, nstages, CiB;
   uint32_t g_slab, x_slab, x_off, stage;
   size_t smem;
 };
@@ -454,12 +465,14 @@ struct WgPlan {
 WgPlan plan(const ConvShape& s, bool three) {
   (void)three;
   WgPlan p;
-  if (s.co != 64 || (s.ci != 32 && s.ci != 64) || s.w + 2 > 256) return p;
+  if (s.co % 64 != 0 || (s.ci != 32 && s.ci % 64 != 0) || s.w + 2 > 256) return p;
   const int Wp = s.w + 2;
-  const int n2 = 2 * s.ci;
+  p.CiB = s.ci == 32 ? 32 : 64;
+  const int n2 = 2 * p.CiB;
   const int tg_max = 512 / n2;
   p.ngroups = (9 + tg_max - 1) / tg_max;
   p.tg = (9 + p.ngroups - 1) / p.ngroups;
+  if ((s.co / 64) * (s.ci / p.CiB) * p.ngroups > kNumSMs) return p;   // every work group needs a CTA
   // (rows per block, stages) in order of preference; RP_WGRAD_CFG="rg,stages" overrides
   int cand[6][2] = {{2, 2}, {1, 3}, {1, 2}, {0, 0}, {0, 0}, {0, 0}};
   if (const char* e = getenv("RP_WGRAD_CFG")) {
@@ -478,9 +491,10 @@ WgPlan plan(const ConvShape& s, bool three) {
     q.x_slab = (uint32_t)(rg + 2) * Wp * 128u;
     q.x_off = 4 * q.g_slab + kLead;
     q.stage = round1k((uint64_t)q.x_off + (uint64_t)(n2 / 32) * q.x_slab + kTrail);
+    (void)s;
     q.smem = st * (size_t)q.stage + (3 * kMaxStages + 2) * 8 + 8 * 64 * 8;
     if (q.smem > (size_t)kMaxSmem) continue;
-    if ((size_t)q.tg * s.ci * 64 * 4 > st * (size_t)q.stage) continue;   // epilogue exchange
+    if ((size_t)q.tg * q.CiB * 64 * 4 > st * (size_t)q.stage) continue;   // epilogue exchange
     q.grid = kNumSMs;
     q.ok = true;
     return q;
@@ -491,7 +505,8 @@ WgPlan plan(const ConvShape& s, bool three) {
 unsigned long long* g_trace = nullptr;
 
 int64_t part_bytes(const WgPlan& p, const ConvShape& s) {
-  return ((int64_t)p.grid * p.tg * s.ci * 64 * 4 + 255) / 256 * 256;
+  (void)s;
+  return ((int64_t)p.grid * p.tg * p.CiB * 64 * 4 + 255) / 256 * 256;
 }
 
 }  // namespace
@@ -521,13 +536,12 @@ void conv3x3_wgrad_tc(const ConvShape& s, const float* in, const float* g, float
   a.P = p.P;
   a.Pp = p.Pp;
   a.three = three ? 1 : 0;
-  a.n2 = 2 * s.ci;
+  a.CiB = p.CiB;
+  a.mo = s.co / 64;
+  a.mi = s.ci / p.CiB;
+  a.n2 = 2 * p.CiB;
   a.tg = p.tg;
-  int taps_before = 0;
-  for (int i = 0; i <= kMaxGroups; ++i) {
-    a.grp_cta[i] = (int)((int64_t)p.grid * taps_before / 9);
-    taps_before = std::min(9, taps_before + (i < p.ngroups ? p.tg : 0));
-  }
+  a.ngroups = p.ngroups;
   a.blocks_per_img = (s.h + p.rg - 1) / p.rg;
   a.num_blocks = s.n * a.blocks_per_img;
   a.nstages = p.nstages;
@@ -548,7 +562,7 @@ void conv3x3_wgrad_tc(const ConvShape& s, const float* in, const float* g, float
   wgrad_tc_kernel<<<p.grid, kThreads, p.smem, st>>>(mg, mx, a);
   RP_LAUNCHED();
   const int total = 9 * s.ci * s.co + s.co;
-  wgrad_reduce_kernel<<<ceil_div(total, 256), 256, 0, st>>>(a.part, a.part_bias, a, (double)scale, gw, gb);
+  wgrad_reduce_kernel<<<ceil_div(total, 256), 256, 0, st>>>(a.part, a.part_bias, a, p.grid, (double)scale, gw, gb);
   RP_LAUNCHED();
 }
 

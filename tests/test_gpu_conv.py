@@ -59,11 +59,13 @@ def run_conv(n, hh, ww, ci, co, epi, math, dgrad, seed=0, hstep=0.7):
 
 
 SHAPES = [(2, 32, 32, 64, 64), (3, 8, 8, 16, 16), (1, 12, 12, 16, 32), (2, 6, 9, 32, 16), (1, 32, 32, 64, 128),
-          (5, 7, 7, 48, 64)]
+          (5, 7, 7, 48, 64),
+          # wide channels (C5 uses C = 256): several 64-channel output blocks per launch
+          (2, 16, 16, 128, 128), (1, 16, 16, 256, 256), (2, 8, 8, 64, 192), (1, 9, 11, 256, 64)]
 
 
 # 3xTF32 keeps ~21 of fp32's 24 mantissa bits per product: a few 1e-6 relative at K = 576
-@pytest.mark.parametrize("math,tol", [("fp32", 2e-5), ("simt", 2e-6), ("tf32", 5e-3)])
+@pytest.mark.parametrize("math,tol", [("fp32", 2e-5), ("simt", 4e-6), ("tf32", 5e-3)])
 @pytest.mark.parametrize("shape", SHAPES)
 @pytest.mark.parametrize("dgrad", [False, True])
 def test_conv_all_epilogues(shape, math, tol, dgrad):
@@ -103,10 +105,13 @@ def run_wgrad(n, hh, ww, ci, co, math, seed=0, scale=0.8):
 
 
 WG_SHAPES = [(2, 32, 32, 64, 64), (3, 8, 8, 16, 64), (4, 16, 16, 32, 64), (1, 12, 10, 64, 64), (2, 32, 32, 64, 128),
-             (3, 7, 7, 16, 16)]
+             (3, 7, 7, 16, 16),
+             # ci / co blocks (C5: 256 x 256)
+             (2, 16, 16, 128, 128), (1, 16, 16, 256, 256), (2, 8, 8, 192, 64), (2, 8, 8, 64, 256),
+             (2, 8, 8, 32, 128)]
 
 
-@pytest.mark.parametrize("math,tol", [("fp32", 2e-5), ("simt", 2e-6), ("tf32", 5e-3)])
+@pytest.mark.parametrize("math,tol", [("fp32", 2e-5), ("simt", 4e-6), ("tf32", 5e-3)])
 @pytest.mark.parametrize("shape", WG_SHAPES)
 def test_wgrad(shape, math, tol):
     gw, gb, ww_, wb = run_wgrad(*shape, math=math)
