@@ -233,6 +233,10 @@ int rp_trainer_correct_ghost(rp_trainer* t, const rp_step_params* p, int32_t row
 int rp_trainer_state_device(rp_trainer* t, int32_t k, int32_t which, float** ptr);
 int rp_trainer_stage_stream(rp_trainer* t, int32_t k, void** stream);
 int rp_trainer_loss_device(rp_trainer* t, double** ptr);
+/* Evaluation forward of the local stages (decoupled.cpp:332-347 split across ranks): in =
+ * raw inputs (stage_lo == 0) or the upstream boundary features [nrows][H W C]; out = the
+ * features after stage_hi - 1, or logits [nrows][classes] when the last stage is local. */
+int rp_trainer_forward_local(rp_trainer* t, const float* in_dev, int32_t nrows, float* out_dev);
 int rp_trainer_set_kappa_rule(rp_trainer* t, int32_t rule);
 int rp_trainer_get_params(rp_trainer* t, float* host);
 int rp_trainer_set_params(rp_trainer* t, const float* host);

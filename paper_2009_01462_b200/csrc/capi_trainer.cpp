@@ -247,6 +247,17 @@ int rp_trainer_stage_stream(rp_trainer* t, int32_t k, void** stream) {
   });
 }
 
+int rp_trainer_forward_local(rp_trainer* t, const float* in_dev, int32_t nrows, float* out_dev) {
+  return tguard([&] {
+    need(t, "trainer");
+    if (nrows > 0) {
+      need(in_dev, "in");
+      need(out_dev, "out");
+    }
+    t->tr->forward_local(in_dev, nrows, out_dev);
+  });
+}
+
 int rp_trainer_loss_device(rp_trainer* t, double** ptr) {
   return tguard([&] {
     need(t, "trainer");

@@ -186,6 +186,10 @@ class DecoupledTrainer {
   double last_loss() const;
   // full serial forward of the current net (eval): logits [nrows, classes] device
   void forward(const float* x, int nrows, float* logits);
+  // evaluation forward of the local stages [stage_lo, stage_hi) only (no tape kept):
+  // `in` = raw inputs (stage_lo == 0) or the upstream boundary features; `out` = the
+  // boundary features after stage_hi - 1, or the logits when the last stage is local.
+  void forward_local(const float* in, int nrows, float* out);
 
   static long normalizer(int nrows, int feature_size) { return static_cast<long>(nrows) * feature_size; }
 

@@ -284,12 +284,12 @@ DecoupledTrainer::DecoupledTrainer(const rp_geometry& g, int stages, TrainMode m
     }
     st.badj.allocate(st.device, state_bytes);
     st.badj.zero(nullptr);
+    st.red_ws.allocate(st.device, rp_op_reduce_workspace_bytes());   // psi / correction reductions
     if (ghost) continue;
     st.bout.allocate(st.device, state_bytes);
     st.bout.zero(nullptr);
     st.loss.allocate(st.device, 8);
     st.loss.zero(nullptr);
-    st.red_ws.allocate(st.device, rp_op_reduce_workspace_bytes());
   }
   cu(cudaDeviceSynchronize(), "cudaDeviceSynchronize");
 }
@@ -784,39 +784,47 @@ ViolationReport DecoupledTrainer::violation_report() const {
 }
 
 void DecoupledTrainer::forward(const float* x, int nrows, float* logits) {
+  if (stage_lo_ != 0 || stage_hi_ != stages()) throw std::logic_error("forward: needs every stage on this trainer");
+  forward_local(x, nrows, logits);
+}
+
+void DecoupledTrainer::forward_local(const float* x, int nrows, float* out) {
   sched_->sync();
   if (nrows <= 0) return;
-  const int chunk = std::max(1, std::min(nrows, std::max(256, stages_[0].cap_rows)));
-  ensure_capacity(chunk);
-  eval_a_.allocate(stages_[0].device, (int64_t)chunk * feat() * 4);
-  eval_b_.allocate(stages_[0].device, (int64_t)chunk * feat() * 4);
   if (unique_devices_.size() > 1) throw std::logic_error("forward: eval on multi-device trainers is not supported");
-  if (stage_lo_ != 0 || stage_hi_ != stages()) throw std::logic_error("forward: needs every stage on this trainer");
-  cudaStream_t s = sched_->stream(0);
-  DeviceGuard g(stages_[0].device);
+  const int chunk = std::max(1, std::min(nrows, std::max(256, stages_[stage_lo_].cap_rows)));
+  ensure_capacity(chunk);
+  eval_a_.allocate(stages_[stage_lo_].device, (int64_t)chunk * feat() * 4);
+  eval_b_.allocate(stages_[stage_lo_].device, (int64_t)chunk * feat() * 4);
+  cudaStream_t s = sched_->stream(stage_lo_);
+  DeviceGuard g(stages_[stage_lo_].device);
+  const bool last = stage_hi_ == stages();
+  const int64_t in_stride = stage_lo_ == 0 ? raw_feat() : feat();
   for (int r0 = 0; r0 < nrows; r0 += chunk) {
     const int nr = std::min(chunk, nrows - r0);
-    const float* in = x + (int64_t)r0 * raw_feat();
+    const float* in = x + (int64_t)r0 * in_stride;
     float* bufs[2] = {eval_a_.get(), eval_b_.get()};
-    for (int k = 0; k < stages(); ++k) {
+    for (int k = stage_lo_; k < stage_hi_; ++k) {
       Stage& st = stages_[k];
-      float* out = bufs[k & 1];
+      float* o = (!last && k == stage_hi_ - 1) ? out + (int64_t)r0 * feat() : bufs[(k - stage_lo_) & 1];
       // run_forward records tape pointers; eval does not touch trainer state otherwise
       const float* saved_in0 = st.input0;
       const float* saved_raw = st.raw;
-      run_forward(st, in, nr, out, s);
+      run_forward(st, in, nr, o, s);
       st.input0 = saved_in0;
       st.raw = saved_raw;
-      in = out;
+      in = o;
     }
-    const Stage& last = stages_.back();
-    cu(cudaMemcpyAsync(logits + (int64_t)r0 * geo_.classes, last.logits.get(), (size_t)nr * geo_.classes * 4,
-                       cudaMemcpyDeviceToDevice, s),
-       "cudaMemcpyAsync");
+    if (last) {
+      const Stage& lst = stages_.back();
+      cu(cudaMemcpyAsync(out + (int64_t)r0 * geo_.classes, lst.logits.get(), (size_t)nr * geo_.classes * 4,
+                         cudaMemcpyDeviceToDevice, s),
+         "cudaMemcpyAsync");
+    }
   }
   cu(cudaStreamSynchronize(s), "cudaStreamSynchronize");
   // eval clobbered the tapes: a following stage_backward_update needs a fresh forward
-  for (auto& st : stages_) st.version = -1;
+  for (int k = stage_lo_; k < stage_hi_; ++k) stages_[k].version = -1;
 }
 
 int64_t DecoupledTrainer::state_elems(int k, int which) const {

@@ -173,6 +173,27 @@ class CudaStageEngine:
     def correct_ghost(self, p: StepParams, row0: int, nrows: int) -> None:
         check(lib().rp_trainer_correct_ghost(self._h, C.byref(p.c()), row0, nrows))
 
+    def forward_local(self, in_tensor, nrows: int, out_tensor) -> None:
+        check(lib().rp_trainer_forward_local(self._h, C.c_void_p(in_tensor.data_ptr()) if nrows else None, nrows,
+                                             C.c_void_p(out_tensor.data_ptr()) if nrows else None))
+
+    def buffer(self, numel: int):
+        return self.torch.empty(numel, dtype=self.torch.float32, device=f"cuda:{self.device}")
+
+    def input_tensor(self, x_ptr: int, nrows: int):
+        g = self.geometry
+        return self.torch.as_tensor(_DeviceArray(x_ptr, (nrows * g.height * g.width * g.in_channels,), "<f4"),
+                                    device=f"cuda:{self.device}")
+
+    def violation(self):
+        """psi of the boundaries this rank corrects (0 elsewhere), length K."""
+        per = np.zeros(self.stages)
+        mx = C.c_double()
+        norm = C.c_int64()
+        check(lib().rp_trainer_violation_report(self._h, per.ctypes.data_as(C.POINTER(C.c_double)), C.byref(mx),
+                                                C.byref(norm)))
+        return per, norm.value
+
     def region(self, which: int) -> float:
         ms = C.c_float()
         check(lib().rp_trainer_region(self._h, which, C.byref(ms)))
@@ -205,6 +226,15 @@ class DistributedDecoupledTrainer:
         self.plc = plc
         self.group = group
         self.iteration = 0
+        self._replica_group = None
+        if plc.group_size > 1:
+            import torch.distributed as dist
+            # every rank creates every replica's group, in the same order (dist.new_group rule)
+            for r in range(plc.replicas):
+                ranks = list(range(r * plc.group_size, (r + 1) * plc.group_size))
+                g = dist.new_group(ranks)
+                if r == plc.replica:
+                    self._replica_group = g
 
     # -- transport --
     def _exchange(self, sends, recvs, k_stream: int) -> None:
@@ -248,6 +278,52 @@ class DistributedDecoupledTrainer:
         if not read_loss:
             return None
         return self.loss()
+
+    # -- evaluation (decoupled.cpp:332-347): a chained forward across the ranks --
+    def evaluate(self, x_ptr: Optional[int], labels: Optional[np.ndarray], nrows: int):
+        """Full serial forward of the current net on nrows inputs (rank 0 of the replica
+        passes x_ptr, the last passes the labels): returns (loss_phi, accuracy) on every
+        rank of the replica (network.cpp:193-234: mean softmax-CE, argmax ties to the
+        lowest class)."""
+        e, p = self.engine, self.plc
+        fs = e.geometry.feature_size
+        inp = e.input_tensor(x_ptr, nrows) if p.first else e.buffer(nrows * fs)
+        if p.prev_rank is not None:
+            self._exchange([], [(inp, p.prev_rank)], p.lo)
+        out = e.buffer(nrows * (e.geometry.classes if p.last else fs))
+        e.forward_local(inp, nrows, out)
+        if p.next_rank is not None:
+            self._exchange([(out, p.next_rank)], [], p.hi - 1)
+        res = self._zeros_like_loss().new_zeros(2)
+        if p.last:
+            logits = out.detach().to("cpu").double().numpy().reshape(nrows, e.geometry.classes)
+            y = np.asarray(labels).reshape(-1)
+            m = logits.max(axis=1, keepdims=True)
+            lse = m[:, 0] + np.log(np.exp(logits - m).sum(axis=1))
+            loss = float((lse - logits[np.arange(nrows), y]).mean()) if nrows else 0.0
+            acc = float((np.argmax(logits, axis=1) == y).mean()) if nrows else 0.0
+            res[0], res[1] = loss, acc
+        if self._replica_group is not None:
+            import torch.distributed as dist
+            last = p.rank_of_stage(p.stages - 1)
+            with e.stream(p.hi - 1):
+                dist.broadcast(res, last, group=self._replica_group)
+        return float(res[0].item()), float(res[1].item())
+
+    def violation_report(self):
+        """violation_report (decoupled.cpp:196-205): psi(lambda_k, X^{k-1}_end) per
+        boundary over all N_train rows; each boundary is computed by the rank that
+        corrects it and the K-vector is summed over the replica (a scalar collective, off
+        the data path)."""
+        per, norm = self.engine.violation()
+        if self._replica_group is not None:
+            import torch.distributed as dist
+            t = self._zeros_like_loss().new_tensor(per)
+            with self.engine.stream(self.plc.hi - 1):
+                dist.all_reduce(t, group=self._replica_group)
+            per = t.cpu().numpy()
+        per = [float(v) for v in per]
+        return per, max(per), norm
 
     def loss(self) -> float:
         """The last stage's pre-update loss (decoupled.cpp:193), on every rank of the replica."""

@@ -87,6 +87,32 @@ class OracleStageEngine:
     def correct_ghost(self, sp, row0, nrows):
         self._correct(self.hi, sp, row0, nrows)
 
+    def buffer(self, numel):
+        return torch.zeros(numel, dtype=torch.float64)
+
+    def input_tensor(self, x, nrows):
+        return torch.from_numpy(np.ascontiguousarray(x).reshape(-1))
+
+    def forward_local(self, inp, nrows, out):
+        g = self.tr.net.geo
+        shape = (nrows, g.height, g.width, g.in_channels if self.lo == 0 else g.channels)
+        cur = inp.numpy().reshape(shape)
+        for k in range(self.lo, self.hi):
+            st = self.tr.stage(k)
+            tape = O.net_forward(self.tr.net, cur, st.begin, st.end)
+            cur = tape.logits if (k == self.stages - 1) else tape.features
+        out.copy_(torch.from_numpy(np.ascontiguousarray(cur).reshape(-1)))
+
+    def violation(self):
+        per = np.zeros(self.stages)
+        for k in range(max(self.lo + 1, 1), min(self.hi + 1, self.stages)):
+            per[k] = O.psi(O.SQUARED_L2, self.tr.stage(k).lam, self.tr.stage(k - 1).boundary_out)
+        return per, self.tr.normalizer(NROWS)
+
+    @property
+    def geometry(self):
+        return self.tr.net.geo
+
     def loss_tensor(self):
         return torch.tensor([self.tr.last_stage_loss], dtype=torch.float64)
 
@@ -125,7 +151,10 @@ def _worker(rank, world, port, stages, mode, outdir):
         losses = []
         for _ in range(STEPS):
             losses.append(tr.step(x, y, NROWS, 0, sp, read_loss=True))
-        out = {"losses": np.array(losses), "params": eng.tr.net.flat(), "lo": plc.lo, "hi": plc.hi}
+        ev = tr.evaluate(x if plc.first else None, y if plc.last else None, NROWS)
+        per, mx, norm = tr.violation_report()
+        out = {"losses": np.array(losses), "params": eng.tr.net.flat(), "lo": plc.lo, "hi": plc.hi,
+               "eval": np.array(ev), "viol": np.array(per)}
         for k in range(max(plc.lo, 1), min(plc.hi + 1, stages)):
             out[f"lam{k}"] = eng.tr.stage(k).lam
             out[f"kap{k}"] = eng.tr.stage(k).kappa
@@ -170,11 +199,17 @@ def test_sharded_step_matches_single_process(world, stages, mode):
                            start_method="spawn")
         ranks = [dict(np.load(os.path.join(d, f"rank{r}.npz"))) for r in range(world)]
     ref, ref_losses = _single(stages, mode)
+    _, x, y = _problem()
+    logits = O.net_forward(ref.net, x, 0, GEO.blocks).logits
+    ref_eval = (O.loss_phi(logits, y)[0], float((O.argmax_lowest(logits) == y).mean()))
+    ref_viol = ref.violation_report()[0]
     ref_params = ref.net.flat()
     slices = _layout_slices(stages)
     for r, res in enumerate(ranks):
-        # every rank of a replica reports the last stage's loss
+        # every rank of a replica reports the last stage's loss, the evaluation and the violations
         np.testing.assert_array_equal(res["losses"], ref_losses)
+        np.testing.assert_allclose(res["eval"], ref_eval, rtol=1e-12, atol=0)
+        np.testing.assert_allclose(res["viol"], ref_viol, rtol=1e-12, atol=0)
         for k in range(int(res["lo"]), int(res["hi"])):
             a, b = slices[k]
             np.testing.assert_array_equal(res["params"][a:b], ref_params[a:b], err_msg=f"rank {r} stage {k}")

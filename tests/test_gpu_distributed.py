@@ -76,6 +76,21 @@ def test_two_local_trainers_equal_full_trainer(stages, mode):
         np.testing.assert_array_equal(src.state(k, rp.KAPPA), full.state(k, rp.KAPPA), err_msg=f"kappa {k}")
     np.testing.assert_array_equal(e1.state(half, rp.LAMBDA), full.state(half, rp.LAMBDA))
 
+    # violation report: each boundary from the rank that corrects it
+    per_full, _, _ = full.violation_report()
+    v0, _ = e0.violation()
+    v1, _ = e1.violation()
+    np.testing.assert_array_equal(v0 + v1, np.array(per_full))
+
+    # chained evaluation forward: rank 0's boundary features feed rank 1's stages
+    feats = e0.buffer(N * GEO.feature_size)
+    e0.forward_local(x, N, feats)
+    logits = e1.buffer(N * GEO.classes)
+    e1.forward_local(feats, N, logits)
+    torch.cuda.synchronize()
+    want = full.forward(x.cpu().numpy())
+    np.testing.assert_array_equal(logits.cpu().numpy().reshape(N, GEO.classes), want)
+
 
 def test_local_trainer_protocol_errors():
     e = CudaStageEngine(GEO, 4, rp.ALM, rp.SQUARED_L2, N, 2, 4, 0, seed_state=1)
