@@ -176,10 +176,9 @@ def run_ours(args, cfg, rank, world):
         dist.barrier()
     torch.cuda.synchronize()
 
+    # timed region: no per-kernel event records inside it
     clocks = ClockSampler(dev)
     clocks.start()
-    lib().rp_profile_enable(1)
-    profile_classes()  # clear
     n0 = rp.launch_count()
     h = tr._h
     rp.check(lib().rp_trainer_region(h, 0, None))
@@ -189,10 +188,17 @@ def run_ours(args, cfg, rank, world):
     rp.check(lib().rp_trainer_region(h, 1, C.byref(ms)))
     torch.cuda.synchronize()
     launches = rp.launch_count() - n0
-    lib().rp_profile_enable(0)
-    prof = profile_classes()
     clk = clocks.stop()
     total_ms = ms.value
+    # a second, profiled pass of the same steps: per-kernel-class CUDA-event times for the
+    # roofline (event records on the launching streams; not part of the timed value)
+    lib().rp_profile_enable(1)
+    profile_classes()  # clear
+    for _ in range(args.steps):
+        tr.step_device(x.data_ptr(), y.data_ptr(), B, 0, sp, read_loss=False)
+    torch.cuda.synchronize()
+    lib().rp_profile_enable(0)
+    prof = profile_classes()
     if world > 1:
         import torch.distributed as dist
         t = torch.tensor([total_ms], device="cuda")
@@ -255,8 +261,6 @@ def run_ours_distributed(args, cfg, rank, world):
     torch.cuda.synchronize()
     clocks = ClockSampler(dev)
     clocks.start()
-    lib().rp_profile_enable(1)
-    profile_classes()
     n0 = rp.launch_count()
     eng.region(0)
     for _ in range(args.steps):
@@ -264,9 +268,14 @@ def run_ours_distributed(args, cfg, rank, world):
     total_ms = eng.region(1)
     torch.cuda.synchronize()
     launches = rp.launch_count() - n0
+    clk = clocks.stop()
+    lib().rp_profile_enable(1)       # profiled pass for the roofline classes (untimed)
+    profile_classes()
+    for _ in range(args.steps):
+        tr.step(xp, yp, B, 0, sp)
+    torch.cuda.synchronize()
     lib().rp_profile_enable(0)
     prof = profile_classes()
-    clk = clocks.stop()
     t = torch.tensor([total_ms], device="cuda")
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     total_ms = float(t.item())

@@ -359,48 +359,63 @@ __global__ void __launch_bounds__(kThreads, 1)
       for (int s = 0; s < ((a.dbg & 1) ? 0 : ntiles); ++s) {
         const uint32_t tcol = tmem_base + ((uint32_t)(q * 32) << 16) + (uint32_t)((ab * kS + s) * 128);
         for (int p0 = 0; p0 < 128; p0 += 64) {
-          uint32_t r[64];
-          tmem_ld16(tcol + (uint32_t)p0, *reinterpret_cast<uint32_t(*)[16]>(&r[0]));
-          tmem_ld16(tcol + (uint32_t)p0 + 16, *reinterpret_cast<uint32_t(*)[16]>(&r[16]));
-          tmem_ld16(tcol + (uint32_t)p0 + 32, *reinterpret_cast<uint32_t(*)[16]>(&r[32]));
-          tmem_ld16(tcol + (uint32_t)p0 + 48, *reinterpret_cast<uint32_t(*)[16]>(&r[48]));
-          tmem_wait_ld();
+          constexpr bool kAux = EPI == EPI_RESID || EPI == EPI_TANH_BWD || EPI == EPI_ADD;
           float* mine = xchg + ((xb * 2 + (q & 1)) * 2 + (hi_warp ? 0 : 1)) * 32 * 32;
           float* theirs = xchg + ((xb * 2 + (q & 1)) * 2 + (hi_warp ? 1 : 0)) * 32 * 32;
-          // static register indices only (a runtime offset into r[] would spill it to local memory)
+          // 1) the 32 columns the partner warp finishes: TMEM -> smem
+          {
+            uint32_t rr[32];
+            const uint32_t c_give = tcol + (uint32_t)p0 + (hi_warp ? 32u : 0u);
+            tmem_ld16(c_give, *reinterpret_cast<uint32_t(*)[16]>(&rr[0]));
+            tmem_ld16(c_give + 16, *reinterpret_cast<uint32_t(*)[16]>(&rr[16]));
+            tmem_wait_ld();
 #pragma unroll
-          for (int e = 0; e < 32; ++e) mine[e * 32 + lane] = __uint_as_float(hi_warp ? r[32 + e] : r[e]);
+            for (int e = 0; e < 32; ++e) mine[e * 32 + lane] = __uint_as_float(rr[e]);
+          }
+          // 3) our own 32 columns
+          uint32_t r[32];
+          {
+            const uint32_t c_own = tcol + (uint32_t)p0 + (uint32_t)own0;
+            tmem_ld16(c_own, *reinterpret_cast<uint32_t(*)[16]>(&r[0]));
+            tmem_ld16(c_own + 16, *reinterpret_cast<uint32_t(*)[16]>(&r[16]));
+            tmem_wait_ld();
+          }
           asm volatile("bar.sync 2, 128;" ::: "memory");
-          // positions own0 .. own0+31 of this batch: frame coordinates without divisions
+          // positions own0 .. own0+31 of this batch, 16 at a time: the aux operand (skip /
+          // tape / cotangent input) of all 16 is loaded before any is used, so the
+          // epilogue pays two memory latencies per 64 positions instead of four.
+          // NHWC offsets are 32-bit relative to the image (H W Co < 2^31).
+          const float* auxb = kAux ? a.aux + img * a.Co + co : nullptr;
+          float* outb = a.out + img * a.Co + co;
           const int f = (tile0 + s) * 128 + p0 + own0;
           int y = f / Wp, X = f - (f / Wp) * Wp;
 #pragma unroll
-          for (int e0 = 0; e0 < 32; e0 += 8) {
-            float v[8], auxv[8];
-            int64_t idx[8];
-            bool ok[8];
+          for (int h16 = 0; h16 < 32; h16 += 16) {
+            int off[16];
+            bool ok[16];
+            float ax[16];
 #pragma unroll
-            for (int e = 0; e < 8; ++e) {
+            for (int e = 0; e < 16; ++e) {
               ok[e] = y < a.H && X >= 1 && X <= a.W;
-              idx[e] = (img + (int64_t)y * a.W + (X - 1)) * a.Co + co;
-              v[e] = __uint_as_float(hi_warp ? r[e0 + e] : r[32 + e0 + e]) + theirs[(e0 + e) * 32 + lane];
+              off[e] = ok[e] ? (y * a.W + (X - 1)) * a.Co : 0;
               if (++X == Wp) X = 0, ++y;
             }
-            if (EPI == EPI_RESID || EPI == EPI_TANH_BWD || EPI == EPI_ADD) {
+            if constexpr (kAux) {
 #pragma unroll
-              for (int e = 0; e < 8; ++e) auxv[e] = ok[e] ? a.aux[idx[e]] : 0.f;
+              for (int e = 0; e < 16; ++e) ax[e] = auxb[off[e]];
             }
 #pragma unroll
-            for (int e = 0; e < 8; ++e) {
+            for (int e = 0; e < 16; ++e) {
               if (!ok[e]) continue;                           // warp-uniform
+              const float v = __uint_as_float(r[h16 + e]) + theirs[(h16 + e) * 32 + lane];
               float o;
-              if constexpr (EPI == EPI_BIAS) o = v[e] + bias;
-              else if constexpr (EPI == EPI_BIAS_TANH) o = tanhf(v[e] + bias);
-              else if constexpr (EPI == EPI_RESID) o = auxv[e] + a.h * (v[e] + bias);
-              else if constexpr (EPI == EPI_TANH_BWD) o = (a.h * v[e]) * (1.f - auxv[e] * auxv[e]);
-              else if constexpr (EPI == EPI_ADD) o = auxv[e] + v[e];
-              else o = a.h * v[e];
-              a.out[idx[e]] = o;
+              if constexpr (EPI == EPI_BIAS) o = v + bias;
+              else if constexpr (EPI == EPI_BIAS_TANH) o = tanhf(v + bias);
+              else if constexpr (EPI == EPI_RESID) o = ax[e] + a.h * (v + bias);
+              else if constexpr (EPI == EPI_TANH_BWD) o = (a.h * v) * (1.f - ax[e] * ax[e]);
+              else if constexpr (EPI == EPI_ADD) o = ax[e] + v;
+              else o = a.h * v;
+              outb[off[e]] = o;
             }
           }
           xb ^= 1;
