@@ -161,6 +161,35 @@ int ref_serial_train_step(int in_dim, int d, int h, int L, int classes, int act,
     net_to_flat(n, params);
   });
 }
+// build_initial_net (decoupled.cpp:207-245).  mode: TrainMode (0 serial, 1 penalty, 2 alm);
+// init: InitScheme (0 multilevel, 1 warmstart, 2 random), config.hpp:17-18.  The reference
+// hard-codes in_dim = 2 (the toy input).  lr schedule = (epoch, value) steps.
+int ref_build_initial_net(int mode, int init, int d, int h, int L, int K, int classes, int coarse_epochs,
+                          int warm_epochs, const int* lr_epochs, const double* lr_values, int n_lr,
+                          const double* x, const int* labels, int rows, uint64_t* state, double* params) {
+  return guard([&] {
+    TrainConfig cfg;
+    cfg.mode = static_cast<TrainMode>(mode);
+    cfg.init = static_cast<InitScheme>(init);
+    cfg.feature_dim = d;
+    cfg.hidden_dim = h;
+    cfg.num_blocks = L;
+    cfg.stages = K;
+    cfg.classes = classes;
+    cfg.coarse_epochs = coarse_epochs;
+    cfg.warmstart_epochs = warm_epochs;
+    cfg.schedules.lr_steps.clear();
+    for (int i = 0; i < n_lr; ++i) cfg.schedules.lr_steps.emplace_back(lr_epochs[i], lr_values[i]);
+    Tensor xt(rows, 2);
+    copy_in(xt, x);
+    std::vector<int> y(labels, labels + rows);
+    Rng r(*state);
+    ResidualNet n = build_initial_net(cfg, xt, y, r);
+    net_to_flat(n, params);
+    *state = r.state;
+  });
+}
+
 int ref_loss_phi(const double* logits, const int* labels, int rows, int classes, double* value,
                  double* grad) {
   return guard([&] {

@@ -50,6 +50,7 @@ def lib():
         L.ref_trainer_iteration.argtypes = [C.c_void_p]
         L.ref_rng_next_u64.restype = C.c_uint64
         L.ref_rng_split.restype = C.c_uint64
+        L.ref_build_initial_net.restype = C.c_int
         for name in ("ref_trainer_get_params", "ref_trainer_set_params", "ref_trainer_reset_lambda",
                      "ref_trainer_get_state", "ref_trainer_set_state", "ref_trainer_step",
                      "ref_trainer_take_snapshot", "ref_trainer_stage_forward",
@@ -241,3 +242,22 @@ class RefTrainer:
         norm = C.c_long()
         _check(lib().ref_trainer_violation_report(C.c_void_p(self.h), _p(per), C.byref(mx), C.byref(norm)))
         return list(per), mx.value, norm.value
+
+
+def build_initial_net(mode, init, d, h, L, K, classes, coarse_epochs, warm_epochs, lr_steps, x, labels, state):
+    """The reference's build_initial_net (decoupled.cpp:207-245); in_dim is 2 there.
+    Returns (flat params, advanced rng state)."""
+    Lb = lib()
+    n = len(lr_steps)
+    ep = (C.c_int * max(n, 1))(*[int(e) for e, _ in lr_steps])
+    va = (C.c_double * max(n, 1))(*[float(v) for _, v in lr_steps])
+    x = np.ascontiguousarray(x, np.float64)
+    y = np.ascontiguousarray(labels, np.int32)
+    st = C.c_uint64(state)
+    out = np.empty(param_count(2, d, h, L, classes), np.float64)
+    rc = Lb.ref_build_initial_net(mode, init, d, h, L, K, classes, coarse_epochs, warm_epochs, ep, va, n,
+                                  x.ctypes.data_as(_D), y.ctypes.data_as(_I), x.shape[0], C.byref(st),
+                                  out.ctypes.data_as(_D))
+    if rc != 0:
+        raise RefError(rc, Lb.ref_last_error().decode())
+    return out, st.value

@@ -696,3 +696,60 @@ def extract_dense_params(g: Geometry, conv_flat: np.ndarray) -> np.ndarray:
         parts += [net.w1[l][1, 1].reshape(-1), net.b1[l], net.w2[l][1, 1].reshape(-1), net.b2[l]]
     parts += [net.t_w.reshape(-1), net.t_b]
     return np.concatenate(parts)
+
+
+# ------------------------------------------------------------- initialisation
+MULTILEVEL, WARMSTART, RANDOM = 0, 1, 2        # InitScheme (config.hpp:18)
+
+
+def lr_value_at(steps, epoch: int, fallback: float = 0.1) -> float:
+    """Schedules::value_at (config.cpp:72-80): the entry with the largest epoch <= e."""
+    v = fallback
+    for e, val in steps:
+        if e > epoch:
+            break
+        v = val
+    return v
+
+
+def build_initial_net(g: Geometry, stages: int, mode: int, init: int, train_x, labels, rng: Rng,
+                      coarse_epochs: int = 50, warmstart_epochs: int = 10, lr_steps=()) -> ConvNet:
+    """build_initial_net (decoupled.cpp:207-245): random init (serial mode or Random);
+    Warmstart = warmstart_epochs full-batch serial steps of the deep net; Multilevel =
+    train a `stages`-block coarse net for coarse_epochs, then replicate coarse block k
+    into the n = L / K blocks of stage k with W2, b2 scaled by 1 / n."""
+    lr_at = lambda e: lr_value_at(lr_steps, e, 0.1)  # noqa: E731
+    if mode == SERIAL or init == RANDOM:
+        return make_net(g, rng)
+    if init == WARMSTART:
+        net = make_net(g, rng)
+        for e in range(warmstart_epochs):
+            serial_train_step(net, train_x, labels, lr_at(e))
+        return net
+    coarse = make_net(coarse_geometry(g, stages), rng)
+    for e in range(coarse_epochs):
+        serial_train_step(coarse, train_x, labels, lr_at(e))
+    return replicate_coarse(g, stages, coarse)
+
+
+def coarse_geometry(g: Geometry, stages: int) -> Geometry:
+    """The K-block coarse net of the multilevel init (decoupled.cpp:226)."""
+    return Geometry(in_channels=g.in_channels, height=g.height, width=g.width, channels=g.channels, hidden=g.hidden,
+                    blocks=stages, classes=g.classes, activation=g.activation, step_h=g.step_h)
+
+
+def replicate_coarse(g: Geometry, stages: int, coarse: ConvNet) -> ConvNet:
+    """decoupled.cpp:228-244: S, T from the coarse net; coarse block k copied into the
+    n = L / K blocks of stage k with W2, b2 scaled by 1 / n."""
+    n = g.blocks // stages
+    net = zero_net(g, coarse.s_w.dtype)
+    net.s_w[...], net.s_b[...] = coarse.s_w, coarse.s_b
+    net.t_w[...], net.t_b[...] = coarse.t_w, coarse.t_b
+    for k in range(stages):
+        for i in range(n):
+            l = k * n + i
+            net.w1[l][...] = coarse.w1[k]
+            net.b1[l][...] = coarse.b1[k]
+            net.w2[l][...] = coarse.w2[k] * (1.0 / n)
+            net.b2[l][...] = coarse.b2[k] * (1.0 / n)
+    return net
