@@ -10,3 +10,8 @@ from .trainer import (  # noqa: F401
     LINF, MATH, PENALTY, SERIAL, SQUARED_L2, TANH, ConfigError, DecoupledTrainer, DeviceError, DivergedError,
     Geometry, InvalidArgument, LogicError, SerialTrainer, ShapeError, StageError, StepParams, check, launch_count,
     normalizer, param_count, partition, serial_train_step)
+from . import harness, init  # noqa: E402,F401  (train / configs / metrics; build_initial_net)
+from .harness import (  # noqa: E402,F401
+    Dataset, ExperimentSummary, MetricsRow, Schedules, TrainConfig, default_config, gen_circles, load_config_file,
+    parse_config_json, run_experiment, train)
+from .init import build_initial_net  # noqa: E402,F401
