@@ -47,7 +47,6 @@ double conv_bytes(const k::ConvShape& s, bool aux) {
 
 void check_math(int math) {
   if (math < RP_MATH_FP32 || math > RP_MATH_SIMT) fail(RP_ERR_CONFIG, "unknown math mode");
-  if (math == RP_MATH_BF16) fail(RP_ERR_CONFIG, "RP_MATH_BF16: the bf16 conv kernels are not built yet");
 }
 
 }  // namespace
@@ -92,6 +91,12 @@ int64_t op_workspace_bytes(const rp_geometry& g, int nrows) {
 void conv(const k::ConvShape& s, const float* in, const float* w, bool dgrad, const float* bias, const float* aux,
           float h, int epi, float* out, int math, void* wws, int prof_cls, bool aux_read, cudaStream_t st) {
   prof::Scope ps(prof_cls, st, conv_flops(s), conv_bytes(s, aux_read));
+  // RP_MATH_BF16: bf16 operands where the bf16 kernel tiles the shape (Co % 128, Ci % 32),
+  // the fp32-accurate 3xTF32 kernel elsewhere (never less precise than asked for)
+  if (math == RP_MATH_BF16 && k::conv3x3_bf16_supported(s)) {
+    k::conv3x3_fwd_bf16(s, in, w, dgrad, bias, aux, h, epi, out, wws, st);
+    return;
+  }
   if (math != RP_MATH_SIMT && k::conv3x3_tc_supported(s)) {
     k::conv3x3_fwd_tc(s, in, w, dgrad, bias, aux, h, epi, out, math != RP_MATH_TF32, wws, st);
     return;

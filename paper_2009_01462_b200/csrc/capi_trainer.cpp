@@ -150,7 +150,6 @@ int rp_trainer_create(const rp_geometry* g, int32_t stages, int32_t mode, int32_
     if (mode < RP_MODE_SERIAL || mode > RP_MODE_ALM) throw respar::b200::ConfigError("unknown train mode");
     if (penalty < 0 || penalty > 2) throw respar::b200::ConfigError("unknown penalty kind");
     if (math < RP_MATH_FP32 || math > RP_MATH_SIMT) throw respar::b200::ConfigError("unknown math mode");
-    if (math == RP_MATH_BF16) throw respar::b200::ConfigError("RP_MATH_BF16: the bf16 conv kernels are not built yet");
     if (mode == RP_MODE_SERIAL && stages != 1) throw respar::b200::ConfigError("serial mode runs exactly one stage");
     std::vector<int> devs;
     for (int i = 0; i < ndev; ++i) devs.push_back(devices[i]);
@@ -181,7 +180,6 @@ int rp_trainer_create_local(const rp_geometry* g, int32_t stages, int32_t mode, 
       throw respar::b200::ConfigError("stage-sharded trainers run the penalty or ALM mode");
     if (penalty < 0 || penalty > 2) throw respar::b200::ConfigError("unknown penalty kind");
     if (math < RP_MATH_FP32 || math > RP_MATH_SIMT) throw respar::b200::ConfigError("unknown math mode");
-    if (math == RP_MATH_BF16) throw respar::b200::ConfigError("RP_MATH_BF16: the bf16 conv kernels are not built yet");
     auto h = std::make_unique<rp_trainer>();
     h->tr = std::make_unique<DecoupledTrainer>(
         *g, stages, mode == RP_MODE_ALM ? respar::b200::TrainMode::Alm : respar::b200::TrainMode::Penalty,

@@ -1,0 +1,490 @@
+// tcgen05 implicit-GEMM 3x3 convolution with bf16 operands and fp32 accumulation
+// (RP_MATH_BF16, config C5: "BF16 tensor-core conv path with fp32 accumulation").
+//
+//   out[p][co] = epi( sum_{tap, ci} bf16(in[p + off(tap)][ci]) * bf16(w[tap][ci][co]) )
+//
+// Same structure as conv_tc.cu (interior-frame halo, taps as shifted UMMA descriptors,
+// weights as the shared A operand, persistent warp-specialised CTAs), re-tiled for
+// kind::f16: M = 128 output channels per block (no hi / lo stacking), K = 16 channels
+// per MMA, 32-channel halo chunks.  Activations stay fp32 in HBM: TMA brings the fp32
+// halo, converter warps round it to bf16 (RNE) into the K-major interleaved layout the
+// MMA reads, the epilogue reads fp32 accumulators from TMEM and applies the same fused
+// bias / tanh / skip / (1 - a^2) / step-size as the fp32 kernel.
+//
+// Shared memory: 2 fp32 halo slots (TMA), 2 bf16 halo slots (MMA operand), 3 weight
+// stages (one filter row of one chunk).  TMEM: 2 units x 2 tiles x 128 columns.
+#include <cuda.h>
+#include <cuda_bf16.h>
+
+#include <map>
+#include <mutex>
+#include <tuple>
+
+#include "../common.cuh"
+#include "kernels.cuh"
+#include "umma.cuh"
+
+namespace rp::k {
+
+namespace {
+
+using namespace rp::umma;
+
+constexpr int kThreads = 320;
+constexpr int kWStages = 3;
+constexpr int kChunk = 32;           // input channels per halo chunk
+constexpr int kS = 2;                // 128-position tiles per unit
+constexpr int kMaxSmem = 227 * 1024;
+
+struct BfArgs {
+  int N, H, W, Ci, Co, Wp, rows_h, T, halo_pos, nchunks;
+  uint32_t raw_bytes;   // fp32 halo chunk: [8 groups][positions][4 ch]
+  uint32_t raw_stride;  // bytes per fp32 slot
+  uint32_t bf_bytes;    // bf16 halo chunk: [4 kg][positions][8 ch]
+  uint32_t bf_stride;   // bytes per bf16 slot (with zero pads before / after)
+  uint32_t w_tap;       // bytes of one tap's A operand: 4 kg x 128 rows x 16 B
+  float h;
+  const __nv_bfloat16* w;   // prepped [cb][chunk][tap][kg][128 rows][8]
+  const float* bias;
+  const float* aux;
+  float* out;
+};
+
+// Work split as in conv_tc.cu: full kS-tile units round-robin from CTA 0, the per-image
+// tail units from CTA G-1 downwards; the 128-channel output block cb is outermost.
+struct UnitIter {
+  int f, tl, nf, ntail, fu, T, NT, G;
+  __device__ UnitIter(int mtiles, int N, int T_) : T(T_) {
+    G = gridDim.x;
+    fu = T / kS;
+    nf = mtiles * N * fu;
+    ntail = (T % kS) ? mtiles * N : 0;
+    NT = N;
+    f = blockIdx.x;
+    tl = G - 1 - (int)blockIdx.x;
+  }
+  __device__ bool next(int& cb, int& n, int& tile0, int& ntiles) {
+    if (f < nf) {
+      cb = f / (NT * fu);
+      const int r = f - cb * NT * fu;
+      n = r / fu;
+      tile0 = (r - n * fu) * kS;
+      ntiles = kS;
+      f += G;
+      return true;
+    }
+    if (tl < ntail) {
+      cb = tl / NT;
+      n = tl - cb * NT;
+      tile0 = fu * kS;
+      ntiles = T - tile0;
+      tl += G;
+      return true;
+    }
+    return false;
+  }
+};
+
+__device__ __forceinline__ uint32_t pack_bf16(float a, float b) {
+  const __nv_bfloat162 v = __floats2bfloat162_rn(a, b);   // .x = a (low half), RNE
+  return *reinterpret_cast<const uint32_t*>(&v);
+}
+
+template <int EPI>
+__global__ void __launch_bounds__(kThreads, 1)
+    conv3x3_bf16_kernel(const __grid_constant__ CUtensorMap tmap, const BfArgs a) {
+  extern __shared__ __align__(1024) uint8_t smem[];
+  const int warp = __shfl_sync(0xffffffffu, (int)threadIdx.x / 32, 0);
+  const int lane = threadIdx.x & 31;
+
+  const uint32_t w_stage = 3 * a.w_tap;
+  uint8_t* raw_base = smem;                                    // 2 fp32 slots
+  uint8_t* bf_base = smem + 2 * a.raw_stride;                  // 2 bf16 slots
+  uint8_t* w_base = bf_base + 2 * a.bf_stride;                 // kWStages stages
+  uint64_t* bars = reinterpret_cast<uint64_t*>(w_base + kWStages * w_stage);
+  uint64_t* raw_full = bars;           // [2] TMA -> converters
+  uint64_t* raw_empty = bars + 2;      // [2] converters -> TMA
+  uint64_t* bf_full = bars + 4;        // [2] converters -> MMA
+  uint64_t* bf_empty = bars + 6;       // [2] MMA -> converters
+  uint64_t* w_full = bars + 8;         // [kWStages]
+  uint64_t* w_empty = bars + 8 + kWStages;
+  uint64_t* acc_full = bars + 8 + 2 * kWStages;    // [2]
+  uint64_t* acc_empty = bars + 10 + 2 * kWStages;  // [2]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 12 + 2 * kWStages);
+
+  auto raw_s = [&](int s) { return raw_base + s * a.raw_stride; };
+  auto bf_s = [&](int s) { return bf_base + s * a.bf_stride + 128; };
+  auto w_s = [&](int s) { return w_base + s * w_stage; };
+
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&raw_full[i], 1);
+      mbar_init(&raw_empty[i], 128);
+      mbar_init(&bf_full[i], 128);
+      mbar_init(&bf_empty[i], 1);
+      mbar_init(&acc_full[i], 1);
+      mbar_init(&acc_empty[i], 128);
+    }
+    for (int i = 0; i < kWStages; ++i) {
+      mbar_init(&w_full[i], 1);
+      mbar_init(&w_empty[i], 1);
+    }
+    fence_barrier_init();
+    prefetch_tmap(&tmap);
+  }
+  if (warp == 1) tmem_alloc<512>(tmem_slot);
+  // zero the 128-byte pads around the bf16 halo (read only for discarded positions)
+  for (int i = threadIdx.x; i < 2 * 2 * 32; i += blockDim.x) {
+    const int s = i / 64, part = (i / 32) & 1, w = i % 32;
+    uint8_t* base = bf_base + s * a.bf_stride + (part == 0 ? 0 : 128 + a.bf_bytes);
+    reinterpret_cast<uint32_t*>(base)[w] = 0u;
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = __shfl_sync(0xffffffffu, *tmem_slot, 0);
+  const int Wp = a.Wp;
+
+  if (warp == 0) {
+    // ===================== TMA producer =====================
+    int rs = 0, ws = 0;
+    uint32_t rph = 0, wph = 0;
+    const uint32_t wbytes = 3 * a.w_tap;
+    UnitIter it(a.Co / 128, a.N, a.T);
+    int cb, n, tile0, ntiles;
+    while (it.next(cb, n, tile0, ntiles)) {
+      const __nv_bfloat16* wcb = a.w + (int64_t)cb * a.nchunks * 9 * (a.w_tap / 2);
+      const int y0 = (tile0 * 128) / Wp;
+      for (int c = 0; c < a.nchunks; ++c) {
+        mbar_wait(&raw_empty[rs], rph ^ 1);
+        if (elect_one()) {
+          mbar_arrive_expect_tx(&raw_full[rs], a.raw_bytes);
+          tma_load_5d(&tmap, &raw_full[rs], raw_s(rs), 0, -1, y0 - 1, 8 * c, n);
+        }
+        __syncwarp();
+        if (++rs == 2) rs = 0, rph ^= 1;
+        for (int dy = 0; dy < 3; ++dy) {
+          mbar_wait(&w_empty[ws], wph ^ 1);
+          if (elect_one()) {
+            mbar_arrive_expect_tx(&w_full[ws], wbytes);
+            bulk_load(w_s(ws), wcb + ((int64_t)c * 9 + 3 * dy) * (a.w_tap / 2), wbytes, &w_full[ws]);
+          }
+          __syncwarp();
+          if (++ws == kWStages) ws = 0, wph ^= 1;
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ===================== MMA issuer =====================
+    const uint32_t id = idesc(1, 128, 128);                 // bf16 x bf16 -> fp32, M 128, N 128
+    const uint32_t kg_x = (uint32_t)a.halo_pos * 16u;     // bytes between 8-channel groups (halo)
+    const uint32_t kg_w = 128u * 16u;                     // bytes between 8-channel groups (weights)
+    const uint64_t xj = (uint64_t)((2 * kg_x) >> 4);      // one K = 16 step of B, 16-byte units
+    const uint64_t wj = (uint64_t)((2 * kg_w) >> 4);
+    const uint64_t wtap = (uint64_t)(a.w_tap >> 4);
+    int bs = 0, ws = 0, ab = 0;
+    uint32_t bph = 0, wph = 0, aph = 0;
+    UnitIter it(a.Co / 128, a.N, a.T);
+    int cb, n, tile0, ntiles;
+    while (it.next(cb, n, tile0, ntiles)) {
+      const int f0 = tile0 * 128;
+      const int c0 = f0 - (f0 / Wp) * Wp;
+      mbar_wait(&acc_empty[ab], aph ^ 1);
+      tc_fence_after();
+      const uint32_t d0 = tmem_base + (uint32_t)(ab * kS * 128);
+      for (int c = 0; c < a.nchunks; ++c) {
+        mbar_wait(&bf_full[bs], bph);
+        tc_fence_after();
+        const uint64_t dx0 = desc_kmajor_interleave(smem_u32(bf_s(bs)), kg_x, 128);
+        for (int dy = 0; dy < 3; ++dy) {
+          mbar_wait(&w_full[ws], wph);
+          tc_fence_after();
+          const uint64_t dw0 = desc_kmajor_interleave(smem_u32(w_s(ws)), kg_w, 128);
+          const uint64_t bb = dx0 + (uint64_t)(int64_t)(c0 + dy * Wp - 1);   // one position = 16 B
+          const bool first = (c == 0 && dy == 0);
+          if (elect_one()) {
+#pragma unroll
+            for (int dx = 0; dx < 3; ++dx) {
+#pragma unroll
+              for (int j = 0; j < 2; ++j) {
+                const uint64_t da = dw0 + dx * wtap + j * wj;
+                const uint32_t accum = (first && dx == 0 && j == 0) ? 0u : 1u;
+#pragma unroll
+                for (int s = 0; s < kS; ++s)
+                  if (s < ntiles) mma_f16(d0 + s * 128, da, bb + (uint64_t)(dx + 128 * s) + j * xj, id, accum);
+              }
+            }
+            mma_commit(&w_empty[ws]);
+          }
+          __syncwarp();
+          if (++ws == kWStages) ws = 0, wph ^= 1;
+        }
+        if (elect_one()) mma_commit(&bf_empty[bs]);
+        __syncwarp();
+        if (++bs == 2) bs = 0, bph ^= 1;
+      }
+      if (elect_one()) mma_commit(&acc_full[ab]);
+      __syncwarp();
+      if (++ab == 2) ab = 0, aph ^= 1;
+    }
+  } else if (warp < 6) {
+    // ===================== converters: fp32 halo -> bf16 K-major interleave =====================
+    // raw [g = 8 groups of 4 ch][pos][4 floats]  ->  bf16 [k = 4 groups of 8 ch][pos][8 bf16]
+    const int tid = threadIdx.x - 64;
+    int rs = 0, bs = 0;
+    uint32_t rph = 0, bph = 0;
+    const int hp = a.halo_pos;
+    UnitIter it(a.Co / 128, a.N, a.T);
+    int cb, n, tile0, ntiles;
+    while (it.next(cb, n, tile0, ntiles)) {
+      for (int c = 0; c < a.nchunks; ++c) {
+        mbar_wait(&raw_full[rs], rph);
+        mbar_wait(&bf_empty[bs], bph ^ 1);
+        const float4* raw = reinterpret_cast<const float4*>(raw_s(rs));
+        uint4* bf = reinterpret_cast<uint4*>(bf_s(bs));
+        for (int i = tid; i < 4 * hp; i += 128) {
+          const int k = i / hp, p = i - k * hp;
+          const float4 u = raw[(2 * k) * hp + p];
+          const float4 v = raw[(2 * k + 1) * hp + p];
+          bf[i] = make_uint4(pack_bf16(u.x, u.y), pack_bf16(u.z, u.w), pack_bf16(v.x, v.y), pack_bf16(v.z, v.w));
+        }
+        fence_proxy_async_smem();
+        mbar_arrive(&bf_full[bs]);
+        mbar_arrive(&raw_empty[rs]);
+        if (++rs == 2) rs = 0, rph ^= 1;
+        if (++bs == 2) bs = 0, bph ^= 1;
+      }
+    }
+  } else {
+    // ===================== epilogue =====================
+    // TMEM lane r = output channel cb*128 + r; a warp owns lanes 32q..32q+31 and walks
+    // the positions 16 columns at a time: one 128-byte store per position (NHWC).
+    const int q = warp & 3;
+    constexpr bool kBias = EPI == EPI_BIAS || EPI == EPI_BIAS_TANH || EPI == EPI_RESID;
+    constexpr bool kAux = EPI == EPI_RESID || EPI == EPI_TANH_BWD || EPI == EPI_ADD;
+    int ab = 0;
+    uint32_t aph = 0;
+    UnitIter it(a.Co / 128, a.N, a.T);
+    int cb, n, tile0, ntiles;
+    while (it.next(cb, n, tile0, ntiles)) {
+      const int64_t img = (int64_t)n * a.H * a.W;
+      const int co = cb * 128 + q * 32 + lane;
+      const float bias = kBias ? __ldg(a.bias + co) : 0.f;
+      const float* auxb = kAux ? a.aux + img * a.Co + co : nullptr;
+      float* outb = a.out + img * a.Co + co;
+      mbar_wait(&acc_full[ab], aph);
+      tc_fence_after();
+      for (int s = 0; s < ntiles; ++s) {
+        const uint32_t tcol = tmem_base + ((uint32_t)(q * 32) << 16) + (uint32_t)((ab * kS + s) * 128);
+        const int fb = (tile0 + s) * 128;
+        int y = fb / Wp, X = fb - (fb / Wp) * Wp;
+        for (int p0 = 0; p0 < 128; p0 += 16) {
+          int off[16];
+          bool ok[16];
+          float ax[16];
+#pragma unroll
+          for (int e = 0; e < 16; ++e) {
+            ok[e] = y < a.H && X >= 1 && X <= a.W;
+            off[e] = ok[e] ? (y * a.W + (X - 1)) * a.Co : 0;
+            if (++X == Wp) X = 0, ++y;
+          }
+          if constexpr (kAux) {
+#pragma unroll
+            for (int e = 0; e < 16; ++e) ax[e] = auxb[off[e]];
+          }
+          uint32_t r[16];
+          tmem_ld16(tcol + (uint32_t)p0, r);
+          tmem_wait_ld();
+#pragma unroll
+          for (int e = 0; e < 16; ++e) {
+            if (!ok[e]) continue;                               // warp-uniform
+            const float v = __uint_as_float(r[e]);
+            float o;
+            if constexpr (EPI == EPI_BIAS) o = v + bias;
+            else if constexpr (EPI == EPI_BIAS_TANH) o = tanhf(v + bias);
+            else if constexpr (EPI == EPI_RESID) o = ax[e] + a.h * (v + bias);
+            else if constexpr (EPI == EPI_TANH_BWD) o = (a.h * v) * (1.f - ax[e] * ax[e]);
+            else if constexpr (EPI == EPI_ADD) o = ax[e] + v;
+            else o = a.h * v;
+            outb[off[e]] = o;
+          }
+        }
+      }
+      tc_fence_before();
+      mbar_arrive(&acc_empty[ab]);
+      if (++ab == 2) ab = 0, aph ^= 1;
+    }
+  }
+
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_dealloc<512>(tmem_base);
+  }
+}
+
+// HWIO fp32 -> bf16 A operand [cb][chunk][tap'][kg][128 rows][8]: row r = output channel
+// 128 cb + r, element e = input channel 32 chunk + 8 kg + e.  flip = dgrad (tap' = 8 - tap,
+// ci' = co, co' = ci).
+__global__ void prep_weights_bf16_kernel(const float* __restrict__ w, int ci_src, int co_src, int flip,
+                                         __nv_bfloat16* __restrict__ out) {
+  const int Ci = flip ? co_src : ci_src;
+  const int Co = flip ? ci_src : co_src;
+  const int64_t per_cb = 9LL * Ci * 128;
+  const int64_t total = per_cb * (Co / 128);
+  for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total;
+       idx += (int64_t)gridDim.x * blockDim.x) {
+    const int cb = (int)(idx / per_cb);
+    const int64_t li = idx - cb * per_cb;
+    const int e = (int)(li & 7);
+    const int r = (int)((li >> 3) & 127);
+    const int64_t rest = li >> 10;              // (chunk, tap, kg)
+    const int kg = (int)(rest % 4);
+    const int tap = (int)((rest / 4) % 9);
+    const int chunk = (int)(rest / 36);
+    const int ci = chunk * kChunk + kg * 8 + e;
+    const int co = cb * 128 + r;
+    const float v = !flip ? w[((int64_t)tap * ci_src + ci) * co_src + co]
+                          : w[((int64_t)(8 - tap) * ci_src + co) * co_src + ci];
+    out[idx] = __float2bfloat16_rn(v);
+  }
+}
+
+// ---------------------------------------------------------------- host side
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                  const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+EncodeTiledFn encode_fn() {
+  static EncodeTiledFn fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<EncodeTiledFn>(p);
+  });
+  if (!fn) fail(RP_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
+  return fn;
+}
+
+// NHWC fp32 as 5-D (4 ch, W, H, C/4 groups, N); box (4, W+2 from x = -1, rows, 8 groups, 1)
+CUtensorMap make_halo_map(const float* in, const ConvShape& s, int Wp, int rows_h) {
+  CUtensorMap m;
+  const cuuint64_t dims[5] = {4, (cuuint64_t)s.w, (cuuint64_t)s.h, (cuuint64_t)(s.ci / 4), (cuuint64_t)s.n};
+  const cuuint64_t strides[4] = {(cuuint64_t)s.ci * 4, (cuuint64_t)s.w * s.ci * 4, 16,
+                                 (cuuint64_t)s.h * s.w * s.ci * 4};
+  const cuuint32_t box[5] = {4, (cuuint32_t)Wp, (cuuint32_t)rows_h, 8, 1};
+  const cuuint32_t estr[5] = {1, 1, 1, 1, 1};
+  CUresult r = encode_fn()(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 5, const_cast<float*>(in), dims, strides, box, estr,
+                           CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                           CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) fail(RP_ERR_CUDA, "cuTensorMapEncodeTiled (bf16 conv) failed (" + std::to_string((int)r) + ")");
+  return m;
+}
+
+struct Plan {
+  bool ok = false;
+  int Wp, rows_h, halo_pos, T;
+  uint32_t raw_bytes, raw_stride, bf_bytes, bf_stride, w_tap;
+  size_t smem;
+};
+
+Plan plan_for(const ConvShape& s) {
+  Plan p;
+  if (s.co % 128 != 0 || s.ci % kChunk != 0 || s.w + 2 > 256) return p;
+  p.Wp = s.w + 2;
+  p.rows_h = (3 * p.Wp + 128 * kS + p.Wp - 1) / p.Wp;
+  if (p.rows_h > 256) return p;
+  p.halo_pos = p.rows_h * p.Wp;
+  p.T = (s.h * p.Wp + 127) / 128;
+  p.raw_bytes = (uint32_t)p.halo_pos * kChunk * 4u;
+  p.raw_stride = (p.raw_bytes + 1023) / 1024 * 1024;
+  p.bf_bytes = (uint32_t)p.halo_pos * kChunk * 2u;
+  p.bf_stride = (128 + p.bf_bytes + 128 + 1023) / 1024 * 1024;
+  p.w_tap = 4u * 128u * 16u;
+  p.smem = 2 * (size_t)p.raw_stride + 2 * (size_t)p.bf_stride + kWStages * 3 * (size_t)p.w_tap + 512 + 1024;
+  p.ok = p.smem <= (size_t)kMaxSmem;
+  return p;
+}
+
+std::mutex g_map_mu;
+std::map<std::tuple<const void*, int, int, int, int, int>, CUtensorMap> g_maps;
+
+const CUtensorMap& cached_map(const float* in, const ConvShape& s, int Wp, int rows_h) {
+  std::lock_guard<std::mutex> lk(g_map_mu);
+  auto key = std::make_tuple((const void*)in, s.n, s.h, s.w, s.ci, rows_h);
+  auto it = g_maps.find(key);
+  if (it == g_maps.end()) {
+    if (g_maps.size() > 4096) g_maps.clear();
+    it = g_maps.emplace(key, make_halo_map(in, s, Wp, rows_h)).first;
+  }
+  return it->second;
+}
+
+template <int EPI>
+void launch(const CUtensorMap& m, const BfArgs& a, size_t smem, int grid, cudaStream_t st) {
+  static bool configured = false;
+  if (!configured) {
+    RP_CUDA(cudaFuncSetAttribute(conv3x3_bf16_kernel<EPI>, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxSmem));
+    configured = true;
+  }
+  conv3x3_bf16_kernel<EPI><<<grid, kThreads, smem, st>>>(m, a);
+}
+
+}  // namespace
+
+bool conv3x3_bf16_supported(const ConvShape& s) { return plan_for(s).ok; }
+
+int64_t conv3x3_bf16_ws_bytes(const ConvShape& s) { return 9LL * s.ci * s.co * 2 + 256; }
+
+void conv3x3_fwd_bf16(const ConvShape& s, const float* in, const float* w_hwio, bool dgrad_weights, const float* bias,
+                      const float* aux, float h, int epi, float* out, void* ws, cudaStream_t st) {
+  if (s.pixels() == 0) return;
+  const Plan p = plan_for(s);
+  if (!p.ok) fail(RP_ERR_INTERNAL, "conv3x3_fwd_bf16: unsupported shape");
+  __nv_bfloat16* wp = static_cast<__nv_bfloat16*>(ws);
+  const int ci_src = dgrad_weights ? s.co : s.ci;
+  const int co_src = dgrad_weights ? s.ci : s.co;
+  const int64_t total = 9LL * s.ci * s.co;
+  prep_weights_bf16_kernel<<<(int)std::min<int64_t>(ceil_div(total, 256), 16 * kNumSMs), 256, 0, st>>>(
+      w_hwio, ci_src, co_src, dgrad_weights ? 1 : 0, wp);
+  RP_LAUNCHED();
+  BfArgs a{};
+  a.N = s.n;
+  a.H = s.h;
+  a.W = s.w;
+  a.Ci = s.ci;
+  a.Co = s.co;
+  a.Wp = p.Wp;
+  a.rows_h = p.rows_h;
+  a.T = p.T;
+  a.halo_pos = p.halo_pos;
+  a.nchunks = s.ci / kChunk;
+  a.raw_bytes = p.raw_bytes;
+  a.raw_stride = p.raw_stride;
+  a.bf_bytes = p.bf_bytes;
+  a.bf_stride = p.bf_stride;
+  a.w_tap = p.w_tap;
+  a.h = h;
+  a.w = wp;
+  a.bias = bias;
+  a.aux = aux;
+  a.out = out;
+  const CUtensorMap& m = cached_map(in, s, p.Wp, p.rows_h);
+  const int units = (s.co / 128) * s.n * ((p.T + kS - 1) / kS);
+  const int grid = std::min(units, kNumSMs);
+  switch (epi) {
+    case EPI_BIAS: launch<EPI_BIAS>(m, a, p.smem, grid, st); break;
+    case EPI_BIAS_TANH: launch<EPI_BIAS_TANH>(m, a, p.smem, grid, st); break;
+    case EPI_RESID: launch<EPI_RESID>(m, a, p.smem, grid, st); break;
+    case EPI_TANH_BWD: launch<EPI_TANH_BWD>(m, a, p.smem, grid, st); break;
+    case EPI_ADD: launch<EPI_ADD>(m, a, p.smem, grid, st); break;
+    default: launch<EPI_SCALE>(m, a, p.smem, grid, st); break;
+  }
+  RP_LAUNCHED();
+}
+
+}  // namespace rp::k

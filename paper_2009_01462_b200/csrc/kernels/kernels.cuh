@@ -57,6 +57,12 @@ int64_t conv3x3_tc_ws_bytes(const ConvShape& s);
 void conv3x3_fwd_tc(const ConvShape& s, const float* in, const float* w_hwio, bool dgrad_weights, const float* bias,
                     const float* aux, float h, int epi, float* out, bool three, void* ws, cudaStream_t st);
 
+// tcgen05 bf16-operand conv, fp32 accumulate (conv_bf16.cu): Co % 128 == 0, Ci % 32 == 0.
+bool conv3x3_bf16_supported(const ConvShape& s);
+int64_t conv3x3_bf16_ws_bytes(const ConvShape& s);
+void conv3x3_fwd_bf16(const ConvShape& s, const float* in, const float* w_hwio, bool dgrad_weights, const float* bias,
+                      const float* aux, float h, int epi, float* out, void* ws, cudaStream_t st);
+
 // tcgen05 weight gradient (conv_wgrad_tc.cu): gw[tap][ci][co], gb[co] (may be null),
 // scaled; deterministic (per-CTA partials + fixed-order fp64 reduce).
 bool conv3x3_wgrad_tc_supported(const ConvShape& s, bool three);

@@ -77,6 +77,22 @@ def test_conv_all_epilogues(shape, math, tol, dgrad):
         assert err <= tol, (EPIS[epi], err)
 
 
+BF16_SHAPES = [(2, 16, 16, 128, 128), (1, 16, 16, 256, 256), (2, 9, 11, 64, 128), (1, 32, 32, 128, 256),
+               (2, 8, 8, 64, 64)]   # the last falls back to 3xTF32 (Co % 128 != 0)
+
+
+# bf16 operands (8-bit mantissa), fp32 accumulation: ~2^-9 relative per product
+@pytest.mark.parametrize("shape", BF16_SHAPES)
+@pytest.mark.parametrize("dgrad", [False, True])
+@pytest.mark.parametrize("epi", [1, 2, 3, 4])
+def test_conv_bf16(shape, dgrad, epi):
+    n, hh, ww, ci, co = shape
+    got, want = run_conv(n, hh, ww, ci, co, epi, "bf16", dgrad, seed=3)
+    err = np.abs(got - want).max() / np.abs(want).max()
+    print(f"bf16 {shape} dgrad={dgrad} {EPIS[epi]}: {err:.2e}")
+    assert err <= 1e-2, err
+
+
 def test_conv_tc_is_deterministic_and_batch_independent():
     """Per-pixel results do not depend on which other samples share the launch (the
     property reset_lambda_from_forward's chunked forward relies on)."""
