@@ -60,7 +60,7 @@ int64_t weight_ws_bytes(const rp_geometry& g) {
 
 int64_t wgrad_ws_bytes(const k::ConvShape& s) {
   return std::max({k::conv3x3_wgrad_ws_bytes(s), k::conv3x3_wgrad_tc_ws_bytes(s, true),
-                   k::conv3x3_wgrad_tc_ws_bytes(s, false)});
+                   k::conv3x3_wgrad_tc_ws_bytes(s, false), k::conv3x3_wgrad_bf16_ws_bytes(s)});
 }
 
 // Weight gradient (+ bias sums): tcgen05 when the math mode and shape allow, SIMT otherwise.
@@ -68,6 +68,10 @@ void wgrad(const k::ConvShape& s, const float* in, const float* gout, float scal
            void* ws, cudaStream_t st) {
   prof::Scope ps(RP_PROF_CONV_WGRAD, st, conv_flops(s), conv_bytes(s, false));
   const bool three = math != RP_MATH_TF32;
+  if (math == RP_MATH_BF16 && k::conv3x3_wgrad_bf16_supported(s)) {
+    k::conv3x3_wgrad_bf16(s, in, gout, scale, gw, gb, ws, st);
+    return;
+  }
   if (math != RP_MATH_SIMT && k::conv3x3_wgrad_tc_supported(s, three)) {
     k::conv3x3_wgrad_tc(s, in, gout, scale, gw, gb, three, ws, st);
     return;

@@ -70,6 +70,12 @@ int64_t conv3x3_wgrad_tc_ws_bytes(const ConvShape& s, bool three);
 void conv3x3_wgrad_tc(const ConvShape& s, const float* in, const float* g, float scale, float* gw, float* gb,
                       bool three, void* ws, cudaStream_t st);
 
+// tcgen05 bf16-operand weight gradient (conv_wgrad_bf16.cu): Ci, Co % 128 == 0.
+bool conv3x3_wgrad_bf16_supported(const ConvShape& s);
+int64_t conv3x3_wgrad_bf16_ws_bytes(const ConvShape& s);
+void conv3x3_wgrad_bf16(const ConvShape& s, const float* in, const float* g, float scale, float* gw, float* gb,
+                        void* ws, cudaStream_t st);
+
 // ---- stem S (stem.cu): Cin <= 4 streaming kernels (SIMT conv path otherwise)
 bool stem_supported(const ConvShape& s);
 int64_t stem_wgrad_ws_bytes(const ConvShape& s);

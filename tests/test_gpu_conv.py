@@ -137,6 +137,16 @@ def test_wgrad(shape, math, tol):
     assert ew <= tol and eb <= max(tol, 1e-6), (ew, eb)
 
 
+@pytest.mark.parametrize("shape", [(2, 16, 16, 128, 128), (1, 16, 16, 256, 256), (2, 8, 8, 128, 256),
+                                   (2, 8, 8, 256, 128), (3, 7, 9, 128, 128)])
+def test_wgrad_bf16(shape):
+    gw, gb, ww_, wb = run_wgrad(*shape, math="bf16")
+    ew = np.abs(gw - ww_).max() / np.abs(ww_).max()
+    eb = np.abs(gb - wb).max() / np.abs(wb).max()
+    print(f"wgrad bf16 {shape}: w {ew:.2e} b {eb:.2e}")
+    assert ew <= 1e-2 and eb <= 1e-5, (ew, eb)     # bf16 operands; the bias sums fp32 values
+
+
 def test_wgrad_deterministic():
     a = run_wgrad(2, 32, 32, 64, 64, "fp32", seed=5)
     b = run_wgrad(2, 32, 32, 64, 64, "fp32", seed=5)
