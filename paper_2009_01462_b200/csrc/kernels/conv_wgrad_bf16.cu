@@ -37,7 +37,9 @@ constexpr int kLead = 128;          // zero row before the x slabs (tap shift -1
 constexpr int kTrail = 2048;        // zero rows after them (K padding reads up to 15 rows)
 constexpr int kTg = 3;              // taps per group (3 x 128 TMEM columns)
 constexpr int kConvThreads = 256;   // warps 2..9
-constexpr int kPiece = 32;          // channels per TMA piece
+constexpr int kPiece = 64;          // channels per TMA piece (one bf16 slab row: 256-byte fp32 rows)
+constexpr int kPieces = 128 / kPiece; // pieces per operand per block
+constexpr int kMaxSlots = 8;        // fp32 staging ring depth (as many as shared memory allows)
 
 struct BwArgs {
   int N, H, W, Ci, Co, Wp, rg, P, Pp;
@@ -48,6 +50,8 @@ struct BwArgs {
   uint32_t x_off;                // offset of x slab 0 in a stage
   uint32_t stage;                // bytes per operand stage
   uint32_t piece;                // bytes per staging slot (largest fp32 piece)
+  int nslots;                    // staging ring depth
+  unsigned long long* trace;     // per-block timestamps (tools/trace_wgrad.py), null = off
   float* part;                   // [grid][kTg * 128 (ci)][128 (co)]
   double* part_bias;             // [grid][128]
 };
@@ -56,6 +60,12 @@ __device__ __forceinline__ int grp_start(int gid, int grid, const BwArgs& a) {
   // 3 tap groups of 3 taps per (co block, ci block) pair: CTAs split evenly
   return (int)((int64_t)grid * gid / (3 * a.mo * a.mi));
 }
+
+#define BW_TRACE(slot_, b)                                                                     \
+  do {                                                                                         \
+    if (a.trace && blockIdx.x < 2 && (b) - blk_beg < 64)                                       \
+      a.trace[(blockIdx.x * 64 + ((b) - blk_beg)) * 8 + (slot_)] = globaltimer_ns();           \
+  } while (0)
 
 __device__ __forceinline__ uint32_t pack_bf16(float a, float b) {
   const __nv_bfloat162 v = __floats2bfloat162_rn(a, b);
@@ -70,15 +80,15 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int lane = threadIdx.x & 31;
 
   uint8_t* stage_base = smem;                                  // kStages operand stages
-  uint8_t* ring = smem + kStages * a.stage;                    // 2 fp32 staging slots
-  uint64_t* bars = reinterpret_cast<uint64_t*>(ring + 2 * a.piece);
-  uint64_t* p_full = bars;          // [2] TMA -> converters (per piece)
-  uint64_t* p_empty = bars + 2;     // [2] converters -> TMA
-  uint64_t* full = bars + 4;        // [kStages] converters -> MMA
-  uint64_t* empty = bars + 6;       // [kStages] MMA -> converters
-  uint64_t* acc_full = bars + 8;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 9);
-  double* bsum = reinterpret_cast<double*>(bars + 10);       // [8 warps][128]
+  uint8_t* ring = smem + kStages * a.stage;                    // nslots fp32 staging slots
+  uint64_t* bars = reinterpret_cast<uint64_t*>(ring + a.nslots * a.piece);
+  uint64_t* p_full = bars;                       // [kMaxSlots] TMA -> converters (per piece)
+  uint64_t* p_empty = bars + kMaxSlots;          // [kMaxSlots] converters -> TMA
+  uint64_t* full = bars + 2 * kMaxSlots;         // [kStages] converters -> MMA
+  uint64_t* empty = bars + 2 * kMaxSlots + 2;    // [kStages] MMA -> converters
+  uint64_t* acc_full = bars + 2 * kMaxSlots + 4;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * kMaxSlots + 5);
+  double* bsum = reinterpret_cast<double*>(bars + 2 * kMaxSlots + 6);   // [8 warps][128]
 
   auto g_slab = [&](int s, int j) { return stage_base + s * a.stage + j * a.g_slab; };
   auto x_slab = [&](int s, int j) { return stage_base + s * a.stage + a.x_off + j * a.x_slab; };
@@ -97,9 +107,11 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int xrows = (a.rg + 2) * Wp;
 
   if (threadIdx.x == 0) {
-    for (int i = 0; i < 2; ++i) {
+    for (int i = 0; i < a.nslots; ++i) {
       mbar_init(&p_full[i], 1);
       mbar_init(&p_empty[i], kConvThreads);
+    }
+    for (int i = 0; i < kStages; ++i) {
       mbar_init(&full[i], kConvThreads);
       mbar_init(&empty[i], 1);
     }
@@ -128,19 +140,20 @@ __global__ void __launch_bounds__(kThreads, 1)
     for (int b = blk_beg; b < blk_end; ++b) {
       const int n = b / a.blocks_per_img;
       const int y0 = (b - n * a.blocks_per_img) * a.rg;
-      for (int pc = 0; pc < 8; ++pc) {
+      for (int pc = 0; pc < 2 * kPieces; ++pc) {
         mbar_wait(&p_empty[r], rph ^ 1);
         if (elect_one()) {
-          if (pc < 4) {
-            mbar_arrive_expect_tx(&p_full[r], (uint32_t)a.P * 128u);
+          if (pc == 0) BW_TRACE(0, b);
+          if (pc < kPieces) {
+            mbar_arrive_expect_tx(&p_full[r], (uint32_t)a.P * kPiece * 4u);
             tma_load_4d(&tmap_g, &p_full[r], slot(r), 128 * cob + kPiece * pc, -1, y0, n);
           } else {
-            mbar_arrive_expect_tx(&p_full[r], (uint32_t)xrows * 128u);
-            tma_load_4d(&tmap_x, &p_full[r], slot(r), 128 * cib + kPiece * (pc - 4), -1, y0 - 1, n);
+            mbar_arrive_expect_tx(&p_full[r], (uint32_t)xrows * kPiece * 4u);
+            tma_load_4d(&tmap_x, &p_full[r], slot(r), 128 * cib + kPiece * (pc - kPieces), -1, y0 - 1, n);
           }
         }
         __syncwarp();
-        if (++r == 2) r = 0, rph ^= 1;
+        if (++r == a.nslots) r = 0, rph ^= 1;
       }
     }
   } else if (warp == 1) {
@@ -158,6 +171,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     for (int b = blk_beg; b < blk_end; ++b) {
       mbar_wait(&full[s], ph);
       tc_fence_after();
+      if (lane == 0) BW_TRACE(3, b);
       uint64_t da = desc_general(smem_u32(g_slab(s, 0)), a.g_slab, 1024, 2, 0);
       uint64_t db = desc_general(smem_u32(x_slab(s, 0)), a.x_slab, 1024, 2, 0);
       if (elect_one()) {
@@ -170,6 +184,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           db += 128;
         }
         mma_commit(&empty[s]);
+        BW_TRACE(4, b);
       }
       __syncwarp();
       if (++s == kStages) s = 0, ph ^= 1;
@@ -178,31 +193,44 @@ __global__ void __launch_bounds__(kThreads, 1)
     __syncwarp();
   } else {
     // ===================== converters (warps 2..9): fp32 pieces -> swizzled bf16 =====================
-    // A piece is `rows` rows of 32 fp32 channels (128 B, unswizzled); it fills 4 of the 8
-    // 16-byte chunks (8 channels each) of the 64-channel bf16 rows of slab (piece / 2).
-    // Item i = tid + 256 m: row i / 4, chunk q = i % 4 == tid % 4 (fixed per thread), so a
-    // thread sums the same 8 g channels of each of the 4 g pieces: 4 x 8 bias sums.
+    // A piece is `rows` rows of 64 fp32 channels (256 B, unswizzled) = one bf16 slab row of
+    // 8 16-byte chunks.  Thread t converts float4 f = t + 256 m (contiguous 16-byte loads,
+    // no bank conflicts): row f / 16, channels 4 (f % 16) .. +3 -> 8 bytes of bf16 at chunk
+    // (f % 16) / 2 (swizzled: chunk ^ (absolute row & 7)), half (f % 2).  f % 16 == t % 16
+    // for every m, so a thread sums the same 4 g channels of each g piece for the bias.
+    // 4 float4 in flight per thread (loads first).
     const int tid = threadIdx.x - 64;
-    const int q = tid & 3;
+    const int c4 = tid & 15, q = c4 >> 1, half = c4 & 1;
     const bool do_bias = gi == 0 && cib == 0;
-    float bs[4][8], bk[4][8];
+    float bs[kPieces][4], bk[kPieces][4];
 #pragma unroll
-    for (int pc = 0; pc < 4; ++pc)
+    for (int pc = 0; pc < kPieces; ++pc)
 #pragma unroll
-      for (int e = 0; e < 8; ++e) bs[pc][e] = bk[pc][e] = 0.f;
-    auto convert = [&](int r, uint8_t* dst, int cbase, int rows, float* bf) {
+      for (int e = 0; e < 4; ++e) bs[pc][e] = bk[pc][e] = 0.f;
+    auto convert = [&](int r, uint8_t* dst, int rows, float* bf) {
       const float4* src = reinterpret_cast<const float4*>(slot(r));
-      for (int i = tid; i < rows * 4; i += kConvThreads) {
-        const int row = i >> 2;
-        const float4 u = src[row * 8 + 2 * q];
-        const float4 v = src[row * 8 + 2 * q + 1];
-        const uint32_t raddr = smem_u32(dst) + (uint32_t)row * 128u;
-        const int phys = (cbase + q) ^ (int)((raddr >> 7) & 7u);
-        *reinterpret_cast<uint4*>(dst + (size_t)row * 128 + phys * 16) =
-            make_uint4(pack_bf16(u.x, u.y), pack_bf16(u.z, u.w), pack_bf16(v.x, v.y), pack_bf16(v.z, v.w));
-        if (bf) {
-          bf[0] += u.x; bf[1] += u.y; bf[2] += u.z; bf[3] += u.w;
-          bf[4] += v.x; bf[5] += v.y; bf[6] += v.z; bf[7] += v.w;
+      const uint32_t dbase = smem_u32(dst);
+      const int n4 = rows * 16;
+      for (int f0 = tid; f0 < n4; f0 += 4 * kConvThreads) {
+        float4 u[4];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          const int f = f0 + k * kConvThreads;
+          u[k] = f < n4 ? src[f] : make_float4(0.f, 0.f, 0.f, 0.f);
+        }
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          const int f = f0 + k * kConvThreads;
+          if (f < n4) {
+            const int row = f >> 4;
+            const uint32_t raddr = dbase + (uint32_t)row * 128u;
+            const int phys = q ^ (int)((raddr >> 7) & 7u);
+            *reinterpret_cast<uint2*>(dst + (size_t)row * 128 + phys * 16 + half * 8) =
+                make_uint2(pack_bf16(u[k].x, u[k].y), pack_bf16(u[k].z, u[k].w));
+          }
+          if (bf) {
+            bf[0] += u[k].x; bf[1] += u[k].y; bf[2] += u[k].z; bf[3] += u[k].w;
+          }
         }
       }
     };
@@ -210,14 +238,19 @@ __global__ void __launch_bounds__(kThreads, 1)
     uint32_t rph = 0, ph = 0;
     for (int b = blk_beg; b < blk_end; ++b) {
       mbar_wait(&empty[s], ph ^ 1);
+      if (tid == 0) BW_TRACE(1, b);
+      long long wt = 0;
 #pragma unroll
-      for (int pc = 0; pc < 4; ++pc) {                           // g pieces: co 32 pc .. 32 pc + 31
+      for (int pc = 0; pc < kPieces; ++pc) {                     // g pieces: co 64 pc .. 64 pc + 63
+        long long t0w = a.trace ? clock64() : 0;
         mbar_wait(&p_full[r], rph);
-        float bf[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-        convert(r, g_slab(s, pc / 2), (pc % 2) * 4, a.P, do_bias ? bf : nullptr);
+        if (a.trace) wt += clock64() - t0w;
+        if (tid == 0 && pc == 0) BW_TRACE(5, b);
+        float bf[4] = {0, 0, 0, 0};
+        convert(r, g_slab(s, pc), a.P, do_bias ? bf : nullptr);
         if (do_bias) {
 #pragma unroll
-          for (int e = 0; e < 8; ++e) {                          // Kahan fold of the block sum
+          for (int e = 0; e < 4; ++e) {                          // Kahan fold of the block sum
             const float y = bf[e] - bk[pc][e];
             const float t = bs[pc][e] + y;
             bk[pc][e] = (t - bs[pc][e]) - y;
@@ -226,31 +259,34 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         fence_proxy_async_smem();
         mbar_arrive(&p_empty[r]);
-        if (++r == 2) r = 0, rph ^= 1;
+        if (++r == a.nslots) r = 0, rph ^= 1;
       }
-      for (int pc = 0; pc < 4; ++pc) {                           // x pieces: ci 32 pc .. 32 pc + 31
+      for (int pc = 0; pc < kPieces; ++pc) {                     // x pieces: ci 64 pc .. 64 pc + 63
+        long long t0w = a.trace ? clock64() : 0;
         mbar_wait(&p_full[r], rph);
-        convert(r, x_slab(s, pc / 2), (pc % 2) * 4, xrows, nullptr);
+        if (a.trace) wt += clock64() - t0w;
+        convert(r, x_slab(s, pc), xrows, nullptr);
         fence_proxy_async_smem();
         mbar_arrive(&p_empty[r]);
-        if (++r == 2) r = 0, rph ^= 1;
+        if (++r == a.nslots) r = 0, rph ^= 1;
       }
+      if (tid == 0) BW_TRACE(2, b);
+      if (tid == 0 && a.trace && blockIdx.x < 2 && b - blk_beg < 64)
+        a.trace[(blockIdx.x * 64 + (b - blk_beg)) * 8 + 6] = (unsigned long long)wt;
       mbar_arrive(&full[s]);
       if (++s == kStages) s = 0, ph ^= 1;
     }
     if (do_bias) {
-      // lanes sharing q = lane & 3 combine in fixed order (xor 4, 8, 16), lanes 0..3
-      // publish the warp's 128 channel sums, warps are summed in order by 128 threads
+      // lanes sharing c4 = lane & 15 combine in fixed order (xor 16), lanes 0..15 publish
+      // the warp's 128 channel sums, warps are summed in order by 128 threads
       const int cw = tid / 32;
 #pragma unroll
-      for (int pc = 0; pc < 4; ++pc) {
+      for (int pc = 0; pc < kPieces; ++pc) {
 #pragma unroll
-        for (int e = 0; e < 8; ++e) {
+        for (int e = 0; e < 4; ++e) {
           double d = (double)bs[pc][e] - (double)bk[pc][e];
-          d += __shfl_xor_sync(0xffffffffu, d, 4);
-          d += __shfl_xor_sync(0xffffffffu, d, 8);
           d += __shfl_xor_sync(0xffffffffu, d, 16);
-          if (lane < 4) bsum[cw * 128 + pc * 32 + 8 * q + e] = d;
+          if (lane < 16) bsum[cw * 128 + pc * 64 + 4 * c4 + e] = d;
         }
       }
       asm volatile("bar.sync 1, 256;" ::: "memory");
@@ -347,7 +383,7 @@ CUtensorMap make_map(const float* t, int n, int h, int w, int c, int rows) {
   CUtensorMap m;
   const cuuint64_t dims[4] = {(cuuint64_t)c, (cuuint64_t)w, (cuuint64_t)h, (cuuint64_t)n};
   const cuuint64_t strides[3] = {(cuuint64_t)c * 4, (cuuint64_t)w * c * 4, (cuuint64_t)h * w * c * 4};
-  const cuuint32_t box[4] = {(cuuint32_t)kPiece, (cuuint32_t)(w + 2), (cuuint32_t)rows, 1};
+  const cuuint32_t box[4] = {(cuuint32_t)kPiece, (cuuint32_t)(w + 2), (cuuint32_t)rows, 1};   // 256 B rows
   const cuuint32_t estr[4] = {1, 1, 1, 1};
   CUresult r = encode_fn()(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, const_cast<float*>(t), dims, strides, box, estr,
                            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
@@ -374,7 +410,7 @@ uint32_t round1k(uint64_t v) { return (uint32_t)((v + 1023) / 1024 * 1024); }
 
 struct BwPlan {
   bool ok = false;
-  int rg, P, Pp, grid;
+  int rg, P, Pp, grid, nslots;
   uint32_t g_slab, x_slab, x_off, stage, piece;
   size_t smem;
 };
@@ -393,9 +429,12 @@ BwPlan plan(const ConvShape& s) {
     q.x_slab = (uint32_t)(rg + 2) * Wp * 128u;
     q.x_off = 2 * q.g_slab + kLead;
     q.stage = round1k((uint64_t)q.x_off + 2ull * q.x_slab + kTrail);
-    q.piece = round1k((uint64_t)std::max(q.P, (rg + 2) * Wp) * 128);
-    q.smem = kStages * (size_t)q.stage + 2 * (size_t)q.piece + 12 * 8 + 8 * 128 * 8 + 256;
-    if (q.smem > (size_t)kMaxSmem) continue;
+    q.piece = round1k((uint64_t)std::max(q.P, (rg + 2) * Wp) * kPiece * 4);
+    const size_t fixed = kStages * (size_t)q.stage + (2 * kMaxSlots + 8) * 8 + 8 * 128 * 8 + 256;
+    if (fixed + 2 * (size_t)q.piece > (size_t)kMaxSmem) continue;
+    q.nslots = (int)std::min<size_t>(kMaxSlots, ((size_t)kMaxSmem - fixed) / q.piece);
+    if (q.nslots < 3 && rg > 2) continue;   // prefer a smaller block with a deeper TMA ring
+    q.smem = fixed + (size_t)q.nslots * q.piece;
     if ((size_t)kTg * 128 * 128 * 4 > 0 && q.Pp - q.P > 15) continue;
     q.grid = kNumSMs;
     q.ok = true;
@@ -407,6 +446,9 @@ BwPlan plan(const ConvShape& s) {
 int64_t part_bytes(const BwPlan& p) { return ((int64_t)p.grid * kTg * 128 * 128 * 4 + 255) / 256 * 256; }
 
 }  // namespace
+
+unsigned long long* g_bw_trace = nullptr;
+void conv3x3_wgrad_bf16_set_trace(unsigned long long* p) { g_bw_trace = p; }
 
 bool conv3x3_wgrad_bf16_supported(const ConvShape& s) { return plan(s).ok; }
 
@@ -439,6 +481,8 @@ void conv3x3_wgrad_bf16(const ConvShape& s, const float* in, const float* g, flo
   a.x_off = p.x_off;
   a.stage = p.stage;
   a.piece = p.piece;
+  a.nslots = p.nslots;
+  a.trace = g_bw_trace;
   a.part = static_cast<float*>(ws);
   a.part_bias = reinterpret_cast<double*>(static_cast<char*>(ws) + part_bytes(p));
   const CUtensorMap& mg = cached(g, s.n, s.h, s.w, s.co, p.rg);

@@ -419,9 +419,11 @@ extern "C" int rp_debug_umma_bench(int fmt, int N, int layout, int a_mn, int b_m
 namespace rp::k {
 void conv3x3_tc_set_trace(unsigned long long* p);
 void conv3x3_wgrad_tc_set_trace(unsigned long long* p);
+void conv3x3_wgrad_bf16_set_trace(unsigned long long* p);
 }
 extern "C" int rp_debug_set_trace(unsigned long long* p) {
   rp::k::conv3x3_tc_set_trace(p);
   rp::k::conv3x3_wgrad_tc_set_trace(p);
+  rp::k::conv3x3_wgrad_bf16_set_trace(p);
   return 0;
 }
