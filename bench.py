@@ -167,6 +167,7 @@ def run_ours(args, cfg, rank, world):
     x_host = x.cpu().numpy().reshape(B, cfg['h'], cfg['w'], cfg['cin'])
     tr.reset_lambda_from_forward(x_host)
     sp = step_params(cfg)
+    tr.use_cuda_graphs(not args.no_graphs)   # the step is captured once and replayed
 
     for _ in range(args.warmup):
         tr.step_device(x.data_ptr(), y.data_ptr(), B, 0, sp, read_loss=False)
@@ -192,6 +193,7 @@ def run_ours(args, cfg, rank, world):
     total_ms = ms.value
     # a second, profiled pass of the same steps: per-kernel-class CUDA-event times for the
     # roofline (event records on the launching streams; not part of the timed value)
+    tr.use_cuda_graphs(False)                # per-kernel events need eager launches
     lib().rp_profile_enable(1)
     profile_classes()  # clear
     for _ in range(args.steps):
@@ -199,6 +201,7 @@ def run_ours(args, cfg, rank, world):
     torch.cuda.synchronize()
     lib().rp_profile_enable(0)
     prof = profile_classes()
+    tr.use_cuda_graphs(not args.no_graphs)
     if world > 1:
         import torch.distributed as dist
         t = torch.tensor([total_ms], device="cuda")
@@ -380,6 +383,7 @@ def main():
     ap.add_argument("--ref-images", type=int, default=2)
     ap.add_argument("--cpu-images", type=int, default=4)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-graphs", action="store_true", help="launch every kernel eagerly (no CUDA graph replay)")
     ap.add_argument("--dist-path", action="store_true",
                     help="run the one-process-per-GPU stage-sharded path even at N=1 (smoke of the N>1 code)")
     args = ap.parse_args()

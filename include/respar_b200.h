@@ -238,6 +238,10 @@ int rp_trainer_loss_device(rp_trainer* t, double** ptr);
  * features after stage_hi - 1, or logits [nrows][classes] when the last stage is local. */
 int rp_trainer_forward_local(rp_trainer* t, const float* in_dev, int32_t nrows, float* out_dev);
 int rp_trainer_set_kappa_rule(rp_trainer* t, int32_t rule);
+/* CUDA graphs for step / step_device (on != 0): the iteration is captured once per
+ * (inputs, rows, StepParams, multiplier state) and replayed; single-pass corrections
+ * (tau < 0 or max_corrections == 1) only, others run eagerly.  Off by default. */
+int rp_trainer_set_graphs(rp_trainer* t, int32_t on);
 int rp_trainer_get_params(rp_trainer* t, float* host);
 int rp_trainer_set_params(rp_trainer* t, const float* host);
 /* Gradients of the last stage_backward_update / step (flat layout, host). */

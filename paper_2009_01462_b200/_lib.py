@@ -80,6 +80,7 @@ SIGNATURES = {
     "rp_trainer_loss_device": (C.c_int, [_P, C.POINTER(_P)]),
     "rp_trainer_forward_local": (C.c_int, [_P, _P, C.c_int32, _P]),
     "rp_trainer_set_kappa_rule": (C.c_int, [_P, C.c_int32]),
+    "rp_trainer_set_graphs": (C.c_int, [_P, C.c_int32]),
     "rp_trainer_get_params": (C.c_int, [_P, _F]),
     "rp_trainer_set_params": (C.c_int, [_P, _F]),
     "rp_trainer_get_grads": (C.c_int, [_P, _F]),

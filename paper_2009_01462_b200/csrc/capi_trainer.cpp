@@ -21,6 +21,7 @@ std::atomic<uint64_t> g_launches{0};
 
 void set_last_error(const std::string& msg) { g_last_error = msg; }
 void note_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
+void note_launches(uint64_t n) { g_launches.fetch_add(n, std::memory_order_relaxed); }
 
 }  // namespace rp
 
@@ -261,6 +262,13 @@ int rp_trainer_loss_device(rp_trainer* t, double** ptr) {
     need(t, "trainer");
     need(ptr, "ptr");
     *ptr = t->tr->loss_device();
+  });
+}
+
+int rp_trainer_set_graphs(rp_trainer* t, int32_t on) {
+  return tguard([&] {
+    need(t, "trainer");
+    t->tr->set_graphs(on != 0);
   });
 }
 

@@ -35,6 +35,7 @@ inline void cuda_check(cudaError_t e, const char* what, const char* file, int li
   } while (0)
 
 void note_launch();
+void note_launches(uint64_t n);   // kernels launched through a CUDA graph replay
 
 inline int ceil_div(int64_t a, int64_t b) { return static_cast<int>((a + b - 1) / b); }
 

@@ -175,6 +175,11 @@ class DecoupledTrainer {
   // read on a trainer that owns every stage); then, once the downstream rank's p has been
   // received into the ghost's boundary adjoint, the ghost boundary's correction.
   void step_local(const float* batch_x, const int32_t* labels, int nrows, int row0, const StepParams& p);
+  // CUDA graphs: step() captures the iteration (all stage streams) into one graph the first
+  // time it sees a (pointers, rows, StepParams, multiplier state) key and replays it after
+  // that.  Only for trainers that own every stage and single-pass corrections (tau < 0).
+  void set_graphs(bool on);
+  bool graphs() const { return graphs_; }
   void correct_ghost(const StepParams& p, int row0, int nrows);
   int stage_lo() const { return stage_lo_; }
   int stage_hi() const { return stage_hi_; }
@@ -263,6 +268,27 @@ class DecoupledTrainer {
   long iteration_ = 0;
   bool has_forward_ = false;
   int stage_lo_ = 0, stage_hi_ = 0;
+
+  struct GraphKey {
+    const void* x = nullptr;
+    const void* y = nullptr;
+    int nrows = -1, row0 = -1;
+    double beta = 0, tau = 0, lr = 0, lambda_lr = 0, kappa_lr = 0, momentum = 0;
+    int max_corrections = 0;
+    uint64_t kappa_zero_mask = 0;
+    bool operator==(const GraphKey& o) const {
+      return x == o.x && y == o.y && nrows == o.nrows && row0 == o.row0 && beta == o.beta && tau == o.tau &&
+             lr == o.lr && lambda_lr == o.lambda_lr && kappa_lr == o.kappa_lr && momentum == o.momentum &&
+             max_corrections == o.max_corrections && kappa_zero_mask == o.kappa_zero_mask;
+    }
+  };
+  bool graphs_ = false;
+  bool graph_valid_ = false;
+  GraphKey graph_key_;
+  cudaGraphExec_t graph_exec_ = nullptr;
+  uint64_t graph_kernels_ = 0;   // kernel nodes of the captured iteration (launch accounting)
+  void step_graphed(const float* batch_x, const int32_t* labels, int nrows, int row0, const StepParams& p);
+  uint64_t kappa_zero_mask() const;
 };
 
 }  // namespace respar::b200

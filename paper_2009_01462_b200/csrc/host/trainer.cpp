@@ -7,6 +7,10 @@
 
 #include "respar_b200.hpp"
 
+namespace rp {
+void note_launches(uint64_t n);   // capi_trainer.cpp: kernels launched through a graph replay
+}
+
 namespace respar::b200 {
 
 namespace {
@@ -300,6 +304,7 @@ DecoupledTrainer::~DecoupledTrainer() {
   } catch (...) {
     // a sticky CUDA error was already reported by the call that raised it
   }
+  if (graph_exec_) cudaGraphExecDestroy(graph_exec_);
 }
 
 static size_t dev_index(const std::vector<int>& u, int d) {
@@ -574,7 +579,11 @@ double DecoupledTrainer::step(const float* batch_x, const int32_t* labels, int n
   if (has_ghost() || stage_lo_ > 0)
     throw std::logic_error("step: this trainer holds stages [" + std::to_string(stage_lo_) + ", " +
                            std::to_string(stage_hi_) + ") only; use the distributed step");
-  step_local(batch_x, labels, nrows, row0, p);
+  const bool single_pass = p.max_corrections <= 1 || p.tau < 0.0;   // no host-side psi test
+  if (graphs_ && single_pass)
+    step_graphed(batch_x, labels, nrows, row0, p);
+  else
+    step_local(batch_x, labels, nrows, row0, p);
   if (!read_loss) return 0.0;
   return last_loss();
 }
@@ -611,6 +620,102 @@ void DecoupledTrainer::step_local(const float* batch_x, const int32_t* labels, i
     run_correction(k, p, row0, nrows, true, sched_->stream(k));
   }
   sched_->end();
+}
+
+void DecoupledTrainer::set_graphs(bool on) {
+  graphs_ = on;
+  if (!on && graph_exec_) {
+    sched_->sync();
+    cudaGraphExecDestroy(graph_exec_);
+    graph_exec_ = nullptr;
+    graph_valid_ = false;
+  }
+}
+
+uint64_t DecoupledTrainer::kappa_zero_mask() const {
+  uint64_t m = 0;
+  for (int k = 0; k < stages() && k < 64; ++k)
+    if (owns_state(k) && stages_[k].kappa_zero) m |= 1ull << k;
+  return m;
+}
+
+// One CUDA graph per iteration shape.  Capturing runs step_local's host logic (so the host
+// bookkeeping -- iteration, versions, multiplier flags -- advances exactly as for an eager
+// step) while the device work is recorded instead of executed; the graph is then launched
+// once for this step.  Replays repeat the bookkeeping by hand and launch the graph.
+void DecoupledTrainer::step_graphed(const float* batch_x, const int32_t* labels, int nrows, int row0,
+                                    const StepParams& p) {
+  check_rows(row0, nrows, "step");
+  if (nrows < 1) throw ShapeError("step: empty batch");
+  if (unique_devices_.size() > 1) {   // multi-device capture is not attempted
+    step_local(batch_x, labels, nrows, row0, p);
+    return;
+  }
+  ensure_capacity(nrows);
+  GraphKey key;
+  key.x = batch_x;
+  key.y = labels;
+  key.nrows = nrows;
+  key.row0 = row0;
+  key.beta = p.beta;
+  key.tau = p.tau;
+  key.lr = p.lr;
+  key.lambda_lr = p.lambda_lr;
+  key.kappa_lr = p.kappa_lr;
+  key.momentum = p.momentum;
+  key.max_corrections = p.max_corrections;
+  key.kappa_zero_mask = kappa_zero_mask();
+  cudaStream_t ctl = sched_->control();
+  DeviceGuard g(sched_->control_device());
+  if (graph_valid_ && key == graph_key_) {
+    ++iteration_;
+    for (int k = stage_lo_; k < stage_hi_; ++k) {
+      Stage& st = stages_[k];
+      st.version = iteration_;
+      st.fwd_rows = nrows;
+      st.fwd_row0 = row0;
+    }
+    has_forward_ = true;
+    cu(cudaGraphLaunch(graph_exec_, ctl), "cudaGraphLaunch");
+    rp::note_launches(graph_kernels_);
+    return;
+  }
+  if (graph_exec_) {
+    cu(cudaStreamSynchronize(ctl), "cudaStreamSynchronize");
+    cudaGraphExecDestroy(graph_exec_);
+    graph_exec_ = nullptr;
+  }
+  graph_valid_ = false;
+  cudaGraph_t graph = nullptr;
+  cu(cudaStreamBeginCapture(ctl, cudaStreamCaptureModeThreadLocal), "cudaStreamBeginCapture");
+  try {
+    step_local(batch_x, labels, nrows, row0, p);
+  } catch (...) {
+    cudaStreamEndCapture(ctl, &graph);
+    if (graph) cudaGraphDestroy(graph);
+    throw;
+  }
+  cu(cudaStreamEndCapture(ctl, &graph), "cudaStreamEndCapture");
+  size_t nnodes = 0;
+  cu(cudaGraphGetNodes(graph, nullptr, &nnodes), "cudaGraphGetNodes");
+  std::vector<cudaGraphNode_t> nodes(nnodes);
+  if (nnodes) cu(cudaGraphGetNodes(graph, nodes.data(), &nnodes), "cudaGraphGetNodes");
+  graph_kernels_ = 0;
+  for (cudaGraphNode_t n : nodes) {
+    cudaGraphNodeType t;
+    cu(cudaGraphNodeGetType(n, &t), "cudaGraphNodeGetType");
+    if (t == cudaGraphNodeTypeKernel) ++graph_kernels_;
+  }
+  cudaGraphExec_t exec = nullptr;
+  const cudaError_t e = cudaGraphInstantiate(&exec, graph, 0);
+  cudaGraphDestroy(graph);
+  cu(e, "cudaGraphInstantiate");
+  graph_exec_ = exec;
+  // the key is taken after the captured step: its multiplier flags are the replay's
+  graph_key_ = key;
+  graph_key_.kappa_zero_mask = kappa_zero_mask();
+  graph_valid_ = graph_key_.kappa_zero_mask == key.kappa_zero_mask;   // replayable as is
+  cu(cudaGraphLaunch(graph_exec_, ctl), "cudaGraphLaunch");
 }
 
 void DecoupledTrainer::correct_ghost(const StepParams& p, int row0, int nrows) {

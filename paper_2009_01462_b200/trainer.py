@@ -203,6 +203,10 @@ class DecoupledTrainer:
     def set_kappa_rule(self, rule: int) -> None:
         check(lib().rp_trainer_set_kappa_rule(self._h, rule))
 
+    def use_cuda_graphs(self, on: bool = True) -> None:
+        """Capture the iteration into a CUDA graph and replay it (rp_trainer_set_graphs)."""
+        check(lib().rp_trainer_set_graphs(self._h, 1 if on else 0))
+
     # ---- parameters ----
     def params(self) -> np.ndarray:
         out = np.empty(self.nparams, np.float32)

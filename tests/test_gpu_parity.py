@@ -300,3 +300,29 @@ def test_zero_lr_and_zero_lambda_lr_leave_state():
     before = tr.state(1, rp.LAMBDA)
     tr.correct_aux(1, sp, 0, 5)
     assert np.array_equal(tr.state(1, rp.LAMBDA), before)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("mode", [rp.ALM, rp.PENALTY])
+def test_cuda_graph_steps_equal_eager(mode):
+    """rp_trainer_set_graphs: captured + replayed iterations are bitwise the eager ones,
+    across the first ALM step (multiplier state changes -> recapture) and a schedule change."""
+    import torch
+    g = rp.Geometry(3, 8, 8, 64, 64, 4, 10)
+    x, y = O.synthetic_batch(O.Geometry(3, 8, 8, 64, 64, 4, 10), 6, 5)
+    xs = np.ascontiguousarray(x, np.float32)
+    res = []
+    for graphs in (False, True):
+        tr = rp.DecoupledTrainer(g, 2, mode, rp.SQUARED_L2, 6, seed_state=9)
+        tr.reset_lambda_from_forward(xs)
+        tr.use_cuda_graphs(graphs)
+        xd = torch.from_numpy(xs).cuda()
+        yd = torch.from_numpy(y.astype(np.int32)).cuda()
+        losses = []
+        for i in range(6):
+            sp = rp.StepParams(beta=0.1, lr=0.05 if i < 4 else 0.02, lambda_lr=0.05, kappa_lr=1e-6)
+            losses.append(tr.step_device(xd.data_ptr(), yd.data_ptr(), 6, 0, sp, read_loss=True))
+        res.append((losses, tr.params(), tr.state(1, rp.LAMBDA), tr.state(1, rp.KAPPA)))
+    assert res[0][0] == res[1][0]
+    for a, b in zip(res[0][1:], res[1][1:]):
+        np.testing.assert_array_equal(a, b)
