@@ -227,6 +227,11 @@ class DistributedDecoupledTrainer:
         self.group = group
         self.iteration = 0
         self._replica_group = None
+        if plc.world > 1:
+            import torch.distributed as dist
+            # a collective first: NCCL wants every rank in the first call on a group, and the
+            # pipeline's first point-to-point exchanges involve only neighbour pairs
+            dist.barrier(group=group)
         if plc.group_size > 1:
             import torch.distributed as dist
             # every rank creates every replica's group, in the same order (dist.new_group rule)
