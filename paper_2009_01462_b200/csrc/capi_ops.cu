@@ -1,6 +1,8 @@
 // C ABI, op layer (include/respar_b200.h "rp_op_*"): stream-ordered kernels on
 // caller-owned device buffers.  The C++ host classes (host/trainer.cpp) reach the GPU
 // only through these entry points.
+#include <cstdlib>
+#include <string>
 #include <algorithm>
 #include <cstring>
 #include <string>
@@ -43,6 +45,17 @@ double conv_flops(const k::ConvShape& s) { return 2.0 * 9.0 * s.ci * s.co * (dou
 // the epilogue's aux tensor when it has one (weights are negligible)
 double conv_bytes(const k::ConvShape& s, bool aux) {
   return 4.0 * (double)s.pixels() * (s.ci + s.co + (aux ? s.co : 0));
+}
+
+// fp32-accurate conv operand split for the fprop / dgrad kernel: 3xBF16 (default: 3 K=16
+// MMAs per 16 channels instead of 4 K=8 ones; measured 2-5 % faster, ~4e-6 relative) or
+// 3xTF32 (RP_FP32_SPLIT=tf32x3, ~1e-6 relative), read once.
+int fp32_split() {
+  static const int m = [] {
+    const char* e = std::getenv("RP_FP32_SPLIT");
+    return (e && std::string(e) == "tf32x3") ? (int)k::TC_MODE_X3TF32 : (int)k::TC_MODE_X3BF16;
+  }();
+  return m;
 }
 
 void check_math(int math) {
@@ -102,7 +115,8 @@ void conv(const k::ConvShape& s, const float* in, const float* w, bool dgrad, co
     return;
   }
   if (math != RP_MATH_SIMT && k::conv3x3_tc_supported(s)) {
-    k::conv3x3_fwd_tc(s, in, w, dgrad, bias, aux, h, epi, out, math != RP_MATH_TF32, wws, st);
+    k::conv3x3_fwd_tc(s, in, w, dgrad, bias, aux, h, epi, out, math == RP_MATH_TF32 ? k::TC_MODE_TF32 : fp32_split(),
+                      wws, st);
     return;
   }
   const float* wk = w;

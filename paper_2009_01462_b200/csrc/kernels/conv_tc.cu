@@ -31,6 +31,7 @@
 //    issues), w2-5 converters (halo lo part), w6-9 epilogue (TMEM -> registers ->
 //    hi+lo sum -> fused bias / tanh / skip / step-size -> coalesced NHWC stores).
 #include <cuda.h>
+#include <cuda_bf16.h>
 
 #include <cstdlib>
 #include <map>
@@ -54,11 +55,18 @@ constexpr bool kUseCollector = false;  // A-operand collector reuse (measured: n
 constexpr int kS = 2;                // 128-position tiles per unit
 constexpr int kMaxSmem = 220 * 1024;
 
+// Operand modes: TF32 (x and W truncated to tf32), X3TF32 ([W_hi; W_lo] x {x_hi, x_lo}) and
+// X3BF16 (the default fp32-accurate path, capi_ops.cu fp32_split) ([W0; W1] x {x0, x1, x2} with bf16 splits: W to
+// 16 significant bits, x to 24; products W0x0 .. W1x2 cover everything above 2^-18 of |W x|,
+// in 3 MMAs of K = 16 per 16 channels instead of 4 of K = 8).
+enum { MODE_TF32 = 0, MODE_X3TF32 = 1, MODE_X3BF16 = 2 };
+
 struct TcArgs {
   int N, H, W, Ci, Co, Wp, rows_h, T, num_tiles, halo_pos, nchunks;
   uint32_t halo_bytes;  // one raw (or lo) halo buffer
   uint32_t halo_stride; // bytes per halo slot (raw + lo + pads)
-  uint32_t w_tap;       // bytes of one tap's A operand (128 rows x 16 channels x 4 B)
+  uint32_t w_tap;       // bytes of one tap's A operand (128 rows x 16 channels x 4 B; bf16: x 2 B)
+  uint32_t plane_bytes; // X3BF16: one bf16 plane of the halo chunk (halo_pos x 32 B)
   float h;
   const float* w;       // prepped [chunk][tap][kg][128 rows][4]
   const float* bias;
@@ -132,7 +140,33 @@ __device__ __forceinline__ float epi_value(float acc, float bias, int64_t idx, c
   return a.h * acc;
 }
 
-template <int EPI, bool THREE>
+__device__ __forceinline__ uint32_t pack_bf16x2(float a, float b) {
+  const __nv_bfloat162 v = __floats2bfloat162_rn(a, b);
+  return *reinterpret_cast<const uint32_t*>(&v);
+}
+
+// v = p0 + p1 + p2 in bf16 (RNE at each step); returns the three packed planes
+__device__ __forceinline__ void split3_bf16(const float (&v)[8], uint4& p0, uint4& p1, uint4& p2) {
+  float r1[8], r2[8];
+  uint32_t a[4], b[4], c[4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const __nv_bfloat162 h = __floats2bfloat162_rn(v[2 * i], v[2 * i + 1]);
+    a[i] = *reinterpret_cast<const uint32_t*>(&h);
+    r1[2 * i] = v[2 * i] - __low2float(h);
+    r1[2 * i + 1] = v[2 * i + 1] - __high2float(h);
+    const __nv_bfloat162 m = __floats2bfloat162_rn(r1[2 * i], r1[2 * i + 1]);
+    b[i] = *reinterpret_cast<const uint32_t*>(&m);
+    r2[2 * i] = r1[2 * i] - __low2float(m);
+    r2[2 * i + 1] = r1[2 * i + 1] - __high2float(m);
+    c[i] = pack_bf16x2(r2[2 * i], r2[2 * i + 1]);
+  }
+  p0 = make_uint4(a[0], a[1], a[2], a[3]);
+  p1 = make_uint4(b[0], b[1], b[2], b[3]);
+  p2 = make_uint4(c[0], c[1], c[2], c[3]);
+}
+
+template <int EPI, int MODE>
 __global__ void __launch_bounds__(kThreads, 1)
     conv3x3_tc_kernel(const __grid_constant__ CUtensorMap tmap, const TcArgs a) {
   extern __shared__ __align__(1024) uint8_t smem[];
@@ -154,8 +188,12 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint64_t* acc_empty = bars + 8 + 2 * kWStages;  // [2]
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 10 + 2 * kWStages);
 
+  constexpr bool THREE = MODE != MODE_TF32;
+  constexpr bool BF = MODE == MODE_X3BF16;
   auto halo_raw = [&](int s) { return halo_base + s * a.halo_stride + 128; };
   auto halo_lo = [&](int s) { return halo_base + s * a.halo_stride + 256 + a.halo_bytes; };
+  // X3BF16: planes p = 0..2 of bf16 [2 kg][positions][8], each behind a 128-byte zero pad
+  auto plane = [&](int s, int p) { return halo_base + s * a.halo_stride + 256 + a.halo_bytes + p * (a.plane_bytes + 128); };
   auto w_s = [&](int s) { return w_base + s * w_stage; };
 
   if (threadIdx.x == 0) {
@@ -175,11 +213,21 @@ __global__ void __launch_bounds__(kThreads, 1)
   }
   if (warp == 1) tmem_alloc<512>(tmem_slot);
   // zero the 128-byte pads around the halo buffers (read only for discarded positions)
-  for (int i = threadIdx.x; i < 2 * 3 * 32; i += blockDim.x) {
-    const int s = i / 96, part = (i / 32) % 3, w = i % 32;
-    uint8_t* base = halo_base + s * a.halo_stride +
-                    (part == 0 ? 0 : part == 1 ? 128 + a.halo_bytes : 256 + 2 * a.halo_bytes);
-    reinterpret_cast<uint32_t*>(base)[w] = 0u;
+  if constexpr (BF) {
+    for (int i = threadIdx.x; i < 2 * 5 * 32; i += blockDim.x) {
+      const int s = i / 160, part = (i / 32) % 5, w = i % 32;
+      uint8_t* base = part == 0 ? halo_base + s * a.halo_stride
+                    : part == 1 ? halo_base + s * a.halo_stride + 128 + a.halo_bytes
+                                : plane(s, part - 2) + a.plane_bytes;
+      reinterpret_cast<uint32_t*>(base)[w] = 0u;
+    }
+  } else {
+    for (int i = threadIdx.x; i < 2 * 3 * 32; i += blockDim.x) {
+      const int s = i / 96, part = (i / 32) % 3, w = i % 32;
+      uint8_t* base = halo_base + s * a.halo_stride +
+                      (part == 0 ? 0 : part == 1 ? 128 + a.halo_bytes : 256 + 2 * a.halo_bytes);
+      reinterpret_cast<uint32_t*>(base)[w] = 0u;
+    }
   }
   tc_fence_before();
   __syncthreads();
@@ -196,7 +244,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     UnitIter it(a.Co / 64, a.N, a.T);
     int cb, n, tile0, ntiles;
     while (it.next(cb, n, tile0, ntiles)) {
-      const float* wcb = a.w + (int64_t)cb * a.nchunks * 9 * (a.w_tap / 4);
+      const uint8_t* wcb = reinterpret_cast<const uint8_t*>(a.w) + (int64_t)cb * a.nchunks * 9 * a.w_tap;
       const int f0 = tile0 * 128;
       const int y0 = f0 / Wp;
       for (int c = 0; c < a.nchunks; ++c) {
@@ -211,7 +259,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           mbar_wait(&w_empty[ws], wph ^ 1);
           if (elect_one()) {
             mbar_arrive_expect_tx(&w_full[ws], wbytes);
-            bulk_load(w_s(ws), wcb + ((int64_t)c * 9 + 3 * dy) * (a.w_tap / 4), wbytes, &w_full[ws]);
+            bulk_load(w_s(ws), wcb + ((int64_t)c * 9 + 3 * dy) * a.w_tap, wbytes, &w_full[ws]);
           }
           __syncwarp();
           if (++ws == kWStages) ws = 0, wph ^= 1;
@@ -220,7 +268,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
   } else if (warp == 1) {
     // ===================== MMA issuer =====================
-    const uint32_t id = idesc(2, 128, 128);
+    const uint32_t id = BF ? idesc(1, 128, 128) : idesc(2, 128, 128);
     const uint32_t kg_x = (uint32_t)a.halo_pos * 16u;     // bytes between channel groups (halo)
     const uint32_t kg_w = 128u * 16u;                     // bytes between channel groups (weights)
     const uint64_t xj = (uint64_t)((2 * kg_x) >> 4);      // K-step (8 channels) of B, 16-byte units
@@ -245,8 +293,9 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (a.trace) wait_h += clock64() - tw;
         tc_fence_after();
         if (a.trace && blockIdx.x < 2 && lane == 0 && u < 64 && c == 0) a.trace[(blockIdx.x * 64 + u) * 8 + 4] = globaltimer_ns();
-        const uint64_t dxh0 = desc_kmajor_interleave(smem_u32(halo_raw(hs)), kg_x, 128);
-        const uint64_t dxl0 = desc_kmajor_interleave(smem_u32(halo_lo(hs)), kg_x, 128);
+        const uint64_t dxh0 = desc_kmajor_interleave(smem_u32(BF ? plane(hs, 0) : halo_raw(hs)), kg_x, 128);
+        const uint64_t dxl0 = desc_kmajor_interleave(smem_u32(BF ? plane(hs, 1) : halo_lo(hs)), kg_x, 128);
+        const uint64_t dxq0 = desc_kmajor_interleave(smem_u32(plane(hs, BF ? 2 : 0)), kg_x, 128);
         for (int dy = 0; dy < 3; ++dy) {
           long long tw2 = a.trace ? clock64() : 0;
           mbar_wait(&w_full[ws], wph);
@@ -256,8 +305,28 @@ __global__ void __launch_bounds__(kThreads, 1)
           const int64_t row = c0 + dy * Wp - 1;              // positions; >= -1
           const uint64_t bh = dxh0 + (uint64_t)row;          // 16-byte units: one position = 1
           const uint64_t bl = dxl0 + (uint64_t)row;
+          const uint64_t bq = dxq0 + (uint64_t)row;
           const bool first = (c == 0 && dy == 0);
-          if (elect_one()) {
+          if (BF) {
+            // 16 channels = one K = 16 step; A = [W0; W1] (bf16), B = planes x0, x1, x2
+            if (elect_one()) {
+#pragma unroll
+              for (int dx = 0; dx < 3; ++dx) {
+                const uint64_t da = dw0 + dx * wtap;
+                const uint32_t accum = (first && dx == 0) ? 0u : 1u;
+#pragma unroll
+                for (int s = 0; s < kS; ++s) {
+                  if (s < ntiles) {
+                    const uint64_t boff = (uint64_t)(dx + 128 * s);
+                    mma_f16(d0 + s * 128, da, bh + boff, id, accum);
+                    mma_f16(d0 + s * 128, da, bl + boff, id, 1u);
+                    mma_f16(d0 + s * 128, da, bq + boff, id, 1u);
+                  }
+                }
+              }
+              mma_commit(&w_empty[ws]);
+            }
+          } else if (elect_one()) {
 #pragma unroll
             for (int dx = 0; dx < 3; ++dx) {
 #pragma unroll
@@ -318,13 +387,32 @@ __global__ void __launch_bounds__(kThreads, 1)
         for (int c = 0; c < a.nchunks; ++c) {
           mbar_wait(&halo_full[hs], hph);
           float4* raw = reinterpret_cast<float4*>(halo_raw(hs));
-          float4* lo = reinterpret_cast<float4*>(halo_lo(hs));
-          for (int i = tid; i < ((a.dbg & 2) ? 0 : n16); i += 128) {
-            const float4 v = raw[i];
-            float4 l;
-            l.x = v.x - trunc_tf32(v.x); l.y = v.y - trunc_tf32(v.y);
-            l.z = v.z - trunc_tf32(v.z); l.w = v.w - trunc_tf32(v.w);
-            lo[i] = l;
+          if constexpr (BF) {
+            // raw [4 groups of 4 ch][pos][4 floats] -> planes [2 kg of 8 ch][pos][8 bf16]
+            const int hp = a.halo_pos;
+            uint4* p0 = reinterpret_cast<uint4*>(plane(hs, 0));
+            uint4* p1 = reinterpret_cast<uint4*>(plane(hs, 1));
+            uint4* p2 = reinterpret_cast<uint4*>(plane(hs, 2));
+            for (int i = tid; i < 2 * hp; i += 128) {
+              const int k = i / hp, p = i - k * hp;
+              const float4 u = raw[(2 * k) * hp + p];
+              const float4 v = raw[(2 * k + 1) * hp + p];
+              const float vv[8] = {u.x, u.y, u.z, u.w, v.x, v.y, v.z, v.w};
+              uint4 q0, q1, q2;
+              split3_bf16(vv, q0, q1, q2);
+              p0[i] = q0;
+              p1[i] = q1;
+              p2[i] = q2;
+            }
+          } else {
+            float4* lo = reinterpret_cast<float4*>(halo_lo(hs));
+            for (int i = tid; i < ((a.dbg & 2) ? 0 : n16); i += 128) {
+              const float4 v = raw[i];
+              float4 l;
+              l.x = v.x - trunc_tf32(v.x); l.y = v.y - trunc_tf32(v.y);
+              l.z = v.z - trunc_tf32(v.z); l.w = v.w - trunc_tf32(v.w);
+              lo[i] = l;
+            }
           }
           fence_proxy_async_smem();
           mbar_arrive(&halo_conv[hs]);
@@ -468,6 +556,33 @@ __global__ void prep_weights_kernel(const float* __restrict__ w, int ci_src, int
   }
 }
 
+// X3BF16 weights: [cb][chunk][tap'][kg (2)][128 rows][8 bf16]: row r < 64 holds
+// W0 = bf16(w[co = 64 cb + r]), r >= 64 holds W1 = bf16(w - W0) for co = 64 cb + r - 64.
+__global__ void prep_weights_bf16x2_kernel(const float* __restrict__ w, int ci_src, int co_src, int flip,
+                                           __nv_bfloat16* __restrict__ out) {
+  const int Ci = flip ? co_src : ci_src;
+  const int Co = flip ? ci_src : co_src;
+  const int64_t per_cb = 9LL * Ci * 128;
+  const int64_t total = per_cb * (Co / 64);
+  for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total;
+       idx += (int64_t)gridDim.x * blockDim.x) {
+    const int cb = (int)(idx / per_cb);
+    const int64_t li = idx - cb * per_cb;
+    const int e = (int)(li & 7);
+    const int r = (int)((li >> 3) & 127);
+    const int64_t rest = li >> 10;              // (chunk, tap, kg)
+    const int kg = (int)(rest % 2);
+    const int tap = (int)((rest / 2) % 9);
+    const int chunk = (int)(rest / 18);
+    const int ci = chunk * kChunk + kg * 8 + e;
+    const int co = cb * 64 + (r < 64 ? r : r - 64);
+    const float v = !flip ? w[((int64_t)tap * ci_src + ci) * co_src + co]
+                          : w[((int64_t)(8 - tap) * ci_src + co) * co_src + ci];
+    const __nv_bfloat16 h = __float2bfloat16_rn(v);
+    out[idx] = r < 64 ? h : __float2bfloat16_rn(v - __bfloat162float(h));
+  }
+}
+
 // ---------------------------------------------------------------- host side
 unsigned long long* g_trace = nullptr;
 typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
@@ -505,11 +620,11 @@ CUtensorMap make_halo_map(const float* in, const ConvShape& s, int Wp, int rows_
 struct Plan {
   bool ok = false;
   int Wp, rows_h, halo_pos, T, units_per_img;
-  uint32_t halo_bytes, w_tap, halo_stride;
+  uint32_t halo_bytes, w_tap, halo_stride, plane_bytes;
   size_t smem;
 };
 
-Plan plan_for(const ConvShape& s) {
+Plan plan_for(const ConvShape& s, int mode = MODE_X3TF32) {
   Plan p;
   if (s.co % 64 != 0 || s.ci % kChunk != 0 || s.w + 2 > 256) return p;
   p.Wp = s.w + 2;
@@ -519,8 +634,14 @@ Plan plan_for(const ConvShape& s) {
   p.T = (s.h * p.Wp + 127) / 128;
   p.units_per_img = (p.T + kS - 1) / kS;
   p.halo_bytes = (uint32_t)p.halo_pos * 64u;
-  p.w_tap = 128u * kChunk * 4u;
-  p.halo_stride = (128 + p.halo_bytes + 128 + p.halo_bytes + 128 + 1023) / 1024 * 1024;
+  p.plane_bytes = (uint32_t)p.halo_pos * 32u;
+  if (mode == MODE_X3BF16) {
+    p.w_tap = 128u * kChunk * 2u;
+    p.halo_stride = (128 + p.halo_bytes + 128 + 3 * (p.plane_bytes + 128) + 1023) / 1024 * 1024;
+  } else {
+    p.w_tap = 128u * kChunk * 4u;
+    p.halo_stride = (128 + p.halo_bytes + 128 + p.halo_bytes + 128 + 1023) / 1024 * 1024;
+  }
   p.smem = 2 * (size_t)p.halo_stride + kWStages * 3 * (size_t)p.w_tap + 2 * 2 * 2 * 32 * 32 * 4 + 256 + 1024;
   p.ok = p.smem <= (size_t)kMaxSmem;
   return p;
@@ -540,23 +661,25 @@ const CUtensorMap& cached_map(const float* in, const ConvShape& s, int Wp, int r
   return it->second;
 }
 
-template <int EPI, bool THREE>
+template <int EPI, int MODE>
 void launch_cfg(const CUtensorMap& m, const TcArgs& a, size_t smem, int grid, cudaStream_t st) {
   static bool configured = false;
   if (!configured) {
-    RP_CUDA(cudaFuncSetAttribute(conv3x3_tc_kernel<EPI, THREE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    RP_CUDA(cudaFuncSetAttribute(conv3x3_tc_kernel<EPI, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  kMaxSmem));
     configured = true;
   }
-  conv3x3_tc_kernel<EPI, THREE><<<grid, kThreads, smem, st>>>(m, a);
+  conv3x3_tc_kernel<EPI, MODE><<<grid, kThreads, smem, st>>>(m, a);
 }
 
 template <int EPI>
-void launch_epi(const CUtensorMap& m, const TcArgs& a, bool three, size_t smem, int grid, cudaStream_t st) {
-  if (three)
-    launch_cfg<EPI, true>(m, a, smem, grid, st);
+void launch_epi(const CUtensorMap& m, const TcArgs& a, int mode, size_t smem, int grid, cudaStream_t st) {
+  if (mode == MODE_X3BF16)
+    launch_cfg<EPI, MODE_X3BF16>(m, a, smem, grid, st);
+  else if (mode == MODE_X3TF32)
+    launch_cfg<EPI, MODE_X3TF32>(m, a, smem, grid, st);
   else
-    launch_cfg<EPI, false>(m, a, smem, grid, st);
+    launch_cfg<EPI, MODE_TF32>(m, a, smem, grid, st);
 }
 
 }  // namespace
@@ -568,19 +691,24 @@ void conv3x3_tc_set_trace(unsigned long long* p) { g_trace = p; }
 int64_t conv3x3_tc_ws_bytes(const ConvShape& s) { return 9LL * s.ci * 2 * s.co * 4 + 256; }
 
 void conv3x3_fwd_tc(const ConvShape& s, const float* in, const float* w_hwio, bool dgrad_weights, const float* bias,
-                    const float* aux, float h, int epi, float* out, bool three, void* ws, cudaStream_t st) {
+                    const float* aux, float h, int epi, float* out, int mode, void* ws, cudaStream_t st) {
   if (s.pixels() == 0) return;
-  const Plan p = plan_for(s);
+  const Plan p = plan_for(s, mode);
   if (!p.ok) fail(RP_ERR_INTERNAL, "conv3x3_fwd_tc: unsupported shape");
-  float* wp = static_cast<float*>(ws);
   // the weight tensor handed in is HWIO of the *forward* conv; for dgrad it has
   // (ci_src, co_src) = (s.co, s.ci)
   const int ci_src = dgrad_weights ? s.co : s.ci;
   const int co_src = dgrad_weights ? s.ci : s.co;
   const int64_t total = 9LL * s.ci * 2 * s.co;
-  prep_weights_kernel<<<(int)std::min<int64_t>(ceil_div(total, 256), 16 * kNumSMs), 256, 0, st>>>(
-      w_hwio, ci_src, co_src, dgrad_weights ? 1 : 0, wp);
+  const int pgrid = (int)std::min<int64_t>(ceil_div(total, 256), 16 * kNumSMs);
+  if (mode == MODE_X3BF16)
+    prep_weights_bf16x2_kernel<<<pgrid, 256, 0, st>>>(w_hwio, ci_src, co_src, dgrad_weights ? 1 : 0,
+                                                      static_cast<__nv_bfloat16*>(ws));
+  else
+    prep_weights_kernel<<<pgrid, 256, 0, st>>>(w_hwio, ci_src, co_src, dgrad_weights ? 1 : 0,
+                                               static_cast<float*>(ws));
   RP_LAUNCHED();
+  const float* wp = static_cast<const float*>(ws);
   TcArgs a{};
   a.N = s.n;
   a.H = s.h;
@@ -596,6 +724,7 @@ void conv3x3_fwd_tc(const ConvShape& s, const float* in, const float* w_hwio, bo
   a.halo_bytes = p.halo_bytes;
   a.halo_stride = p.halo_stride;
   a.w_tap = p.w_tap;
+  a.plane_bytes = p.plane_bytes;
   a.h = h;
   a.w = wp;
   a.bias = bias;
@@ -606,12 +735,12 @@ void conv3x3_fwd_tc(const ConvShape& s, const float* in, const float* w_hwio, bo
   const CUtensorMap& m = cached_map(in, s, p.Wp, p.rows_h);
   const int grid = std::min(a.num_tiles, kNumSMs);
   switch (epi) {
-    case EPI_BIAS: launch_epi<EPI_BIAS>(m, a, three, p.smem, grid, st); break;
-    case EPI_BIAS_TANH: launch_epi<EPI_BIAS_TANH>(m, a, three, p.smem, grid, st); break;
-    case EPI_RESID: launch_epi<EPI_RESID>(m, a, three, p.smem, grid, st); break;
-    case EPI_TANH_BWD: launch_epi<EPI_TANH_BWD>(m, a, three, p.smem, grid, st); break;
-    case EPI_ADD: launch_epi<EPI_ADD>(m, a, three, p.smem, grid, st); break;
-    default: launch_epi<EPI_SCALE>(m, a, three, p.smem, grid, st); break;
+    case EPI_BIAS: launch_epi<EPI_BIAS>(m, a, mode, p.smem, grid, st); break;
+    case EPI_BIAS_TANH: launch_epi<EPI_BIAS_TANH>(m, a, mode, p.smem, grid, st); break;
+    case EPI_RESID: launch_epi<EPI_RESID>(m, a, mode, p.smem, grid, st); break;
+    case EPI_TANH_BWD: launch_epi<EPI_TANH_BWD>(m, a, mode, p.smem, grid, st); break;
+    case EPI_ADD: launch_epi<EPI_ADD>(m, a, mode, p.smem, grid, st); break;
+    default: launch_epi<EPI_SCALE>(m, a, mode, p.smem, grid, st); break;
   }
   RP_LAUNCHED();
 }

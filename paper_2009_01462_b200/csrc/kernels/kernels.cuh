@@ -51,11 +51,13 @@ void conv3x3_wgrad_simt(const ConvShape& s, const float* in, const float* g, flo
                         void* ws, cudaStream_t st);
 
 // tcgen05 implicit GEMM (conv_tc.cu): fprop, or dgrad when dgrad_weights (w_hwio is
-// then the forward conv's HWIO [3][3][s.co][s.ci] weight).  three: 3xTF32, else TF32.
+// then the forward conv's HWIO [3][3][s.co][s.ci] weight).  mode: 0 TF32, 1 3xTF32 (fp32-
+// accurate, default), 2 3xBF16 (fp32-accurate through bf16 splits; RP_FP32_SPLIT=bf16x3).
+enum { TC_MODE_TF32 = 0, TC_MODE_X3TF32 = 1, TC_MODE_X3BF16 = 2 };
 bool conv3x3_tc_supported(const ConvShape& s);
 int64_t conv3x3_tc_ws_bytes(const ConvShape& s);
 void conv3x3_fwd_tc(const ConvShape& s, const float* in, const float* w_hwio, bool dgrad_weights, const float* bias,
-                    const float* aux, float h, int epi, float* out, bool three, void* ws, cudaStream_t st);
+                    const float* aux, float h, int epi, float* out, int mode, void* ws, cudaStream_t st);
 
 // tcgen05 bf16-operand conv, fp32 accumulate (conv_bf16.cu): Co % 128 == 0, Ci % 32 == 0.
 bool conv3x3_bf16_supported(const ConvShape& s);
