@@ -257,8 +257,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             bs[pc][e] = t;
           }
         }
-        fence_proxy_async_smem();
-        mbar_arrive(&p_empty[r]);
+        mbar_arrive(&p_empty[r]);                                // slot read: TMA may refill it
         if (++r == a.nslots) r = 0, rph ^= 1;
       }
       for (int pc = 0; pc < kPieces; ++pc) {                     // x pieces: ci 64 pc .. 64 pc + 63
@@ -266,10 +265,10 @@ __global__ void __launch_bounds__(kThreads, 1)
         mbar_wait(&p_full[r], rph);
         if (a.trace) wt += clock64() - t0w;
         convert(r, x_slab(s, pc), xrows, nullptr);
-        fence_proxy_async_smem();
         mbar_arrive(&p_empty[r]);
         if (++r == a.nslots) r = 0, rph ^= 1;
       }
+      fence_proxy_async_smem();                                  // bf16 stage -> tensor core (async proxy)
       if (tid == 0) BW_TRACE(2, b);
       if (tid == 0 && a.trace && blockIdx.x < 2 && b - blk_beg < 64)
         a.trace[(blockIdx.x * 64 + (b - blk_beg)) * 8 + 6] = (unsigned long long)wt;
