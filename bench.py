@@ -428,10 +428,18 @@ def main():
         with open(tpath) as f:
             t = json.load(f).get(dom)
         traffic = t["bytes_per_launch"] if t else None
+    # the fp32-accurate kernels run every fp32 MAC as 3-4 reduced-precision tensor products
+    # (3xTF32 / 3xBF16 stacking): their own ceiling is a fraction of the bf16
+    # peak, reported beside the prescribed bf16-peak fraction
+    split = {"fp32": 8.0, "tf32": 2.0, "bf16": 1.0, "simt": None}.get(cfg["math"])
+    ceiling = peaks["bf16_tflops_sustained"] / split if split else None
     roof = {"bound": "tensor", "kernel": dom, "achieved": achieved_tf,
             "peak": peaks["bf16_tflops_sustained"], "unit": "TFLOP/s",
             "frac": achieved_tf / peaks["bf16_tflops_sustained"], "traffic": traffic,
             "traffic_unit": "bytes per launch (ncu --set full, profiles/traffic.json)",
+            "math_ceiling": {"tflops": ceiling, "frac": achieved_tf / ceiling if ceiling else None,
+                             "note": "bf16 sustained peak / products per fp32-equivalent MAC "
+                                     "(fp32: 4 tf32 products at half the bf16 rate)"},
             "peak_source": f"{peaks_kind} bf16 dense sustained (MEASURED_PEAKS.json)",
             "avg_launch_ms": avg_ms, "launches": d["launches"],
             "share_of_step": d["ms"] / args.steps / step_prof_ms if step_prof_ms else None,

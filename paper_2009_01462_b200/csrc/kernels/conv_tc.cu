@@ -73,7 +73,6 @@ struct TcArgs {
   const float* aux;
   float* out;
   unsigned long long* trace;   // diagnostics (tools/trace_conv.py): per-unit timestamps, null = off
-  int dbg;                     // experiment bits (RP_CONV_DBG): 1 no epilogue, 2 no converters
 };
 
 __device__ __forceinline__ float rna_tf32(float v) {
@@ -406,7 +405,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             }
           } else {
             float4* lo = reinterpret_cast<float4*>(halo_lo(hs));
-            for (int i = tid; i < ((a.dbg & 2) ? 0 : n16); i += 128) {
+            for (int i = tid; i < n16; i += 128) {
               const float4 v = raw[i];
               float4 l;
               l.x = v.x - trunc_tf32(v.x); l.y = v.y - trunc_tf32(v.y);
@@ -444,7 +443,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_wait(&acc_full[ab], aph);
       tc_fence_after();
       if (a.trace && blockIdx.x < 2 && threadIdx.x == 192) a.trace[(blockIdx.x * 64 + min(u, 63)) * 8 + 2] = globaltimer_ns();
-      for (int s = 0; s < ((a.dbg & 1) ? 0 : ntiles); ++s) {
+      for (int s = 0; s < ntiles; ++s) {
         const uint32_t tcol = tmem_base + ((uint32_t)(q * 32) << 16) + (uint32_t)((ab * kS + s) * 128);
         for (int p0 = 0; p0 < 128; p0 += 64) {
           constexpr bool kAux = EPI == EPI_RESID || EPI == EPI_TANH_BWD || EPI == EPI_ADD;
@@ -731,7 +730,6 @@ void conv3x3_fwd_tc(const ConvShape& s, const float* in, const float* w_hwio, bo
   a.aux = aux;
   a.out = out;
   a.trace = g_trace;
-  a.dbg = getenv("RP_CONV_DBG") ? atoi(getenv("RP_CONV_DBG")) : 0;
   const CUtensorMap& m = cached_map(in, s, p.Wp, p.rows_h);
   const int grid = std::min(a.num_tiles, kNumSMs);
   switch (epi) {
