@@ -162,6 +162,15 @@ int rp_op_conv3x3_wgrad(int32_t n, int32_t h, int32_t w, int32_t ci, int32_t co,
                         double scale, float* gw, float* gb, int32_t math, void* ws, int64_t ws_bytes, void* stream);
 int64_t rp_op_conv3x3_wgrad_workspace_bytes(int32_t n, int32_t h, int32_t w, int32_t ci, int32_t co);
 
+/* bf16 plane pairs of an fp32 tensor: p0 = bf16(v), p1 = bf16(v - p0) (n % 4 == 0). */
+int rp_op_split_planes(const float* in, int64_t n, void* p0, void* p1, void* stream);
+/* Weight gradient from plane pairs (x = x0 + x1, gout = g0 + g1; bf16 NHWC planes), Ci and
+ * Co multiples of 64: the fp32-accurate (~1e-5) tcgen05 wgrad fed by TMA alone. */
+int rp_op_conv3x3_wgrad_planes(int32_t n, int32_t h, int32_t w, int32_t ci, int32_t co, const void* x0, const void* x1,
+                               const void* g0, const void* g1, double scale, float* gw, float* gb, void* ws,
+                               int64_t ws_bytes, void* stream);
+int64_t rp_op_conv3x3_wgrad_planes_workspace_bytes(int32_t n, int32_t h, int32_t w, int32_t ci, int32_t co);
+
 /* Residual block on nrows samples (network.cpp:82-106), block params at `pb` in the
  * flat layout (w1 b1 w2 b2).  Forward writes a (tape) and x_next.  Backward takes the
  * cotangent at the block output in g_io and overwrites it with the cotangent at the

@@ -386,6 +386,38 @@ int rp_op_block_bwd(const rp_geometry* g, int32_t nrows, const float* x, const f
   });
 }
 
+int rp_op_split_planes(const float* in, int64_t n, void* p0, void* p1, void* stream) {
+  return guard([&] {
+    if (n > 0) {
+      need(in, "in");
+      need(p0, "p0");
+      need(p1, "p1");
+    }
+    k::split_planes(in, n, p0, p1, S(stream));
+  });
+}
+
+int64_t rp_op_conv3x3_wgrad_planes_workspace_bytes(int32_t n, int32_t h, int32_t w, int32_t ci, int32_t co) {
+  return k::conv3x3_wgrad_planes_ws_bytes(k::ConvShape{n, h, w, ci, co});
+}
+
+int rp_op_conv3x3_wgrad_planes(int32_t n, int32_t h, int32_t w, int32_t ci, int32_t co, const void* x0, const void* x1,
+                               const void* g0, const void* g1, double scale, float* gw, float* gb, void* ws,
+                               int64_t ws_bytes, void* stream) {
+  return guard([&] {
+    const k::ConvShape s{n, h, w, ci, co};
+    if (!k::conv3x3_wgrad_planes_supported(s)) fail(RP_ERR_SHAPE, "conv3x3_wgrad_planes: unsupported shape");
+    if (ws_bytes < k::conv3x3_wgrad_planes_ws_bytes(s)) fail(RP_ERR_RANGE, "conv3x3_wgrad_planes: workspace too small");
+    need(x0, "x0");
+    need(x1, "x1");
+    need(g0, "g0");
+    need(g1, "g1");
+    need(gw, "gw");
+    prof::Scope ps(RP_PROF_CONV_WGRAD, S(stream), conv_flops(s), 2.0 * (double)s.pixels() * (s.ci + s.co));
+    k::conv3x3_wgrad_planes(s, x0, x1, g0, g1, (float)scale, gw, gb, ws, S(stream));
+  });
+}
+
 int rp_op_stem_fwd(const rp_geometry* g, int32_t nrows, const float* x_raw, const float* ps, float* x0, int32_t math,
                    void*, int64_t, void* stream) {
   return guard([&] {

@@ -72,6 +72,8 @@ struct TcArgs {
   const float* bias;
   const float* aux;
   float* out;
+  __nv_bfloat16* p0;           // optional bf16 plane pair of out: p0 = bf16(o), p1 = bf16(o - p0)
+  __nv_bfloat16* p1;
   unsigned long long* trace;   // diagnostics (tools/trace_conv.py): per-unit timestamps, null = off
 };
 
@@ -474,6 +476,9 @@ __global__ void __launch_bounds__(kThreads, 1)
           // NHWC offsets are 32-bit relative to the image (H W Co < 2^31).
           const float* auxb = kAux ? a.aux + img * a.Co + co : nullptr;
           float* outb = a.out + img * a.Co + co;
+          const bool planes = a.p0 != nullptr;
+          __nv_bfloat16* p0b = planes ? a.p0 + img * a.Co + co : nullptr;
+          __nv_bfloat16* p1b = planes ? a.p1 + img * a.Co + co : nullptr;
           const int f = (tile0 + s) * 128 + p0 + own0;
           int y = f / Wp, X = f - (f / Wp) * Wp;
 #pragma unroll
@@ -503,6 +508,11 @@ __global__ void __launch_bounds__(kThreads, 1)
               else if constexpr (EPI == EPI_ADD) o = ax[e] + v;
               else o = a.h * v;
               outb[off[e]] = o;
+              if (planes) {
+                const __nv_bfloat16 h0 = __float2bfloat16_rn(o);
+                p0b[off[e]] = h0;
+                p1b[off[e]] = __float2bfloat16_rn(o - __bfloat162float(h0));
+              }
             }
           }
           xb ^= 1;
@@ -690,7 +700,8 @@ void conv3x3_tc_set_trace(unsigned long long* p) { g_trace = p; }
 int64_t conv3x3_tc_ws_bytes(const ConvShape& s) { return 9LL * s.ci * 2 * s.co * 4 + 256; }
 
 void conv3x3_fwd_tc(const ConvShape& s, const float* in, const float* w_hwio, bool dgrad_weights, const float* bias,
-                    const float* aux, float h, int epi, float* out, int mode, void* ws, cudaStream_t st) {
+                    const float* aux, float h, int epi, float* out, int mode, void* ws, cudaStream_t st,
+                    void* out_planes) {
   if (s.pixels() == 0) return;
   const Plan p = plan_for(s, mode);
   if (!p.ok) fail(RP_ERR_INTERNAL, "conv3x3_fwd_tc: unsupported shape");
@@ -729,6 +740,8 @@ void conv3x3_fwd_tc(const ConvShape& s, const float* in, const float* w_hwio, bo
   a.bias = bias;
   a.aux = aux;
   a.out = out;
+  a.p0 = static_cast<__nv_bfloat16*>(out_planes);
+  a.p1 = out_planes ? a.p0 + s.pixels() * s.co : nullptr;
   a.trace = g_trace;
   const CUtensorMap& m = cached_map(in, s, p.Wp, p.rows_h);
   const int grid = std::min(a.num_tiles, kNumSMs);

@@ -1,0 +1,464 @@
+// tcgen05 weight gradient from bf16 *plane pairs* (fp32-accurate path, RP_MATH_FP32):
+//
+//   gW[tap][ci][co] = scale * sum_p x[p + off(tap)][ci] * g[p][co],  gb[co] = scale * sum_p g[p][co]
+//
+// with x = x0 + x1 and g = g0 + g1, x0 = bf16(x), x1 = bf16(x - x0) (16 significant bits; the
+// producing epilogues write the planes next to the fp32 tensor).  Operands go from HBM to the
+// MMA by TMA alone -- no fp32 staging, no converter pass -- which is what bounded the fp32
+// wgrad kernels (conv_wgrad_tc.cu, conv_wgrad_bf16.cu: three shared-memory passes per block):
+//   A = [g0 ; g1]  (M = 128 for a 64-channel co block, MN-major bf16, 128B swizzle)
+//   B = [x0 ; x1]  (N = 128 for a 64-channel ci block)
+// one M128 x N128 x K16 MMA per (16 positions, tap) yields g0x0 + g1x0 + g0x1 + g1x1 in the
+// four quadrants of D (everything above 2^-17 |g x|); the epilogue adds the quadrants.
+// Positions are the padded interior frame (rows x (W+2)), taps are shifted B descriptors,
+// 3 taps per tap group (TMEM 3 x 128 columns), (co block, ci block, tap group) work groups,
+// per-CTA partials and a fixed-order fp64 reduce, as in conv_wgrad_tc.cu.  The bias sums
+// g0 + g1 from the staged planes (bias warps, Kahan-compensated fp32).
+#include <cuda.h>
+#include <cuda_bf16.h>
+
+#include <map>
+#include <mutex>
+#include <tuple>
+
+#include "../common.cuh"
+#include "kernels.cuh"
+#include "umma.cuh"
+
+namespace rp::k {
+
+namespace {
+
+using namespace rp::umma;
+
+constexpr int kThreads = 320;
+constexpr int kMaxStages = 4;
+constexpr int kMaxSmem = 227 * 1024;
+constexpr int kLead = 128;          // zero row before the x slabs (tap shift -1)
+constexpr int kTrail = 2048;        // zero rows after them (K padding reads up to 15 rows)
+constexpr int kTg = 3;              // taps per group
+
+struct PwArgs {
+  int N, H, W, Ci, Co, Wp, rg, P, Pp, nstages;
+  int mo, mi;                    // 64-channel co / ci blocks
+  int blocks_per_img, num_blocks;
+  uint32_t g_slab;               // bytes per bf16 g plane slab (Pp rows x 128 B, 1 KB aligned)
+  uint32_t x_slab;               // bytes per bf16 x plane slab ((rg+2)*Wp rows, packed)
+  uint32_t x_off;
+  uint32_t stage;
+  float* part;                   // [grid][kTg * 64 (ci)][64 (co)]
+  double* part_bias;             // [grid][64]
+};
+
+__device__ __forceinline__ int grp_start(int gid, int grid, const PwArgs& a) {
+  return (int)((int64_t)grid * gid / (3 * a.mo * a.mi));
+}
+
+__global__ void __launch_bounds__(kThreads, 1)
+    wgrad_planes_kernel(const __grid_constant__ CUtensorMap tg0, const __grid_constant__ CUtensorMap tg1,
+                        const __grid_constant__ CUtensorMap tx0, const __grid_constant__ CUtensorMap tx1,
+                        const PwArgs a) {
+  extern __shared__ __align__(1024) uint8_t smem[];
+  const int warp = __shfl_sync(0xffffffffu, (int)threadIdx.x / 32, 0);
+  const int lane = threadIdx.x & 31;
+  const int S = a.nstages;
+
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + S * a.stage);
+  uint64_t* full = bars;                        // [S] TMA -> MMA / bias warps
+  uint64_t* empty = bars + kMaxStages;          // [S] MMA -> TMA
+  uint64_t* bias_free = bars + 2 * kMaxStages;  // [S] bias warps -> TMA
+  uint64_t* acc_full = bars + 3 * kMaxStages;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 3 * kMaxStages + 1);
+  double* bsum = reinterpret_cast<double*>(bars + 3 * kMaxStages + 2);   // [4 warps][64]
+
+  auto g_slab = [&](int s, int j) { return smem + s * a.stage + j * a.g_slab; };
+  auto x_slab = [&](int s, int j) { return smem + s * a.stage + a.x_off + j * a.x_slab; };
+
+  const int NG = 3 * a.mo * a.mi;
+  int gid = 0;
+  while (gid + 1 < NG && grp_start(gid + 1, gridDim.x, a) <= (int)blockIdx.x) ++gid;
+  const int c_lo = grp_start(gid, gridDim.x, a), c_hi = grp_start(gid + 1, gridDim.x, a);
+  const int gi = gid % 3, cib = (gid / 3) % a.mi, cob = gid / (3 * a.mi);
+  const int jg = blockIdx.x - c_lo, ng = c_hi - c_lo;
+  const int blk_beg = (int)((int64_t)jg * a.num_blocks / ng);
+  const int blk_end = (int)((int64_t)(jg + 1) * a.num_blocks / ng);
+  const int t0 = gi * kTg;
+  const int Wp = a.Wp;
+  const int xrows = (a.rg + 2) * Wp;
+  const bool do_bias = gi == 0 && cib == 0;
+
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < S; ++i) {
+      mbar_init(&full[i], 1);
+      mbar_init(&empty[i], 1);
+      mbar_init(&bias_free[i], 128);
+    }
+    mbar_init(acc_full, 1);
+    fence_barrier_init();
+    prefetch_tmap(&tg0);
+    prefetch_tmap(&tg1);
+    prefetch_tmap(&tx0);
+    prefetch_tmap(&tx1);
+  }
+  if (warp == 1) tmem_alloc<512>(tmem_slot);
+  {
+    uint4* z = reinterpret_cast<uint4*>(smem);
+    const int n16 = (int)((size_t)S * a.stage / 16);
+    for (int i = threadIdx.x; i < n16; i += blockDim.x) z[i] = make_uint4(0u, 0u, 0u, 0u);
+  }
+  fence_proxy_async_smem();
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = __shfl_sync(0xffffffffu, *tmem_slot, 0);
+
+  if (warp == 0) {
+    // ===================== TMA producer: 4 plane loads per block =====================
+    int s = 0;
+    uint32_t ph = 0;
+    const uint32_t bytes = 2u * a.P * 128u + 2u * xrows * 128u;
+    for (int b = blk_beg; b < blk_end; ++b) {
+      const int n = b / a.blocks_per_img;
+      const int y0 = (b - n * a.blocks_per_img) * a.rg;
+      mbar_wait(&empty[s], ph ^ 1);
+      if (do_bias) mbar_wait(&bias_free[s], ph ^ 1);
+      if (elect_one()) {
+        mbar_arrive_expect_tx(&full[s], bytes);
+        tma_load_4d(&tg0, &full[s], g_slab(s, 0), 64 * cob, -1, y0, n);
+        tma_load_4d(&tg1, &full[s], g_slab(s, 1), 64 * cob, -1, y0, n);
+        tma_load_4d(&tx0, &full[s], x_slab(s, 0), 64 * cib, -1, y0 - 1, n);
+        tma_load_4d(&tx1, &full[s], x_slab(s, 1), 64 * cib, -1, y0 - 1, n);
+      }
+      __syncwarp();
+      if (++s == S) s = 0, ph ^= 1;
+    }
+  } else if (warp == 1) {
+    // ===================== MMA issuer =====================
+    const uint32_t id = idesc(1, 128, 128, 1, 1);
+    const int ksteps = a.Pp / 16;
+    uint64_t boff[kTg];
+#pragma unroll
+    for (int ti = 0; ti < kTg; ++ti) {
+      const int t = t0 + ti;
+      boff[ti] = (uint64_t)(int64_t)(((t / 3) * Wp + (t % 3) - 1) * 8);   // shift rows x 128 B / 16
+    }
+    int s = 0;
+    uint32_t ph = 0;
+    for (int b = blk_beg; b < blk_end; ++b) {
+      mbar_wait(&full[s], ph);
+      tc_fence_after();
+      uint64_t da = desc_general(smem_u32(g_slab(s, 0)), a.g_slab, 1024, 2, 0);
+      uint64_t db = desc_general(smem_u32(x_slab(s, 0)), a.x_slab, 1024, 2, 0);
+      if (elect_one()) {
+        for (int k = 0; k < ksteps; ++k) {
+          const uint32_t accum = (b > blk_beg || k > 0) ? 1u : 0u;
+#pragma unroll
+          for (int ti = 0; ti < kTg; ++ti)
+            mma_f16(tmem_base + (uint32_t)(ti * 128), da, db + boff[ti], id, accum);
+          da += 128;   // 16 positions = 16 rows x 128 B, in 16-byte units
+          db += 128;
+        }
+        mma_commit(&empty[s]);
+      }
+      __syncwarp();
+      if (++s == S) s = 0, ph ^= 1;
+    }
+    if (elect_one()) mma_commit(acc_full);
+    __syncwarp();
+  } else if (warp < 6) {
+    // ===================== bias warps: sum g0 + g1 over the block's positions =====================
+    // thread t: logical 16-byte chunk cq = t % 8 (channels 8 cq .. 8 cq + 7) of rows
+    // p = t / 8 + 16 k; the chunk sits at (cq ^ (absolute row & 7)) in the swizzled row.
+    if (do_bias) {
+      const int tid = threadIdx.x - 64;
+      const int cq = tid & 7, r0 = tid >> 3;
+      float bs[8] = {0, 0, 0, 0, 0, 0, 0, 0}, bk[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+      int s = 0;
+      uint32_t ph = 0;
+      for (int b = blk_beg; b < blk_end; ++b) {
+        mbar_wait(&full[s], ph);
+        float bf[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+        const uint8_t* p0 = g_slab(s, 0);
+        const uint8_t* p1 = g_slab(s, 1);
+        const uint32_t base0 = smem_u32(p0), base1 = smem_u32(p1);
+        for (int p = r0; p < a.P; p += 16) {
+          const int ph0 = (int)(((base0 >> 7) + p) & 7), ph1 = (int)(((base1 >> 7) + p) & 7);
+          const uint4 u = *reinterpret_cast<const uint4*>(p0 + (size_t)p * 128 + ((cq ^ ph0) << 4));
+          const uint4 v = *reinterpret_cast<const uint4*>(p1 + (size_t)p * 128 + ((cq ^ ph1) << 4));
+          const __nv_bfloat162* uh = reinterpret_cast<const __nv_bfloat162*>(&u);
+          const __nv_bfloat162* vh = reinterpret_cast<const __nv_bfloat162*>(&v);
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            bf[2 * e] += __low2float(uh[e]) + __low2float(vh[e]);
+            bf[2 * e + 1] += __high2float(uh[e]) + __high2float(vh[e]);
+          }
+        }
+#pragma unroll
+        for (int e = 0; e < 8; ++e) {
+          const float y = bf[e] - bk[e];
+          const float t = bs[e] + y;
+          bk[e] = (t - bs[e]) - y;
+          bs[e] = t;
+        }
+        mbar_arrive(&bias_free[s]);
+        if (++s == S) s = 0, ph ^= 1;
+      }
+      // threads t, t + 8, ... (same cq) combine in fixed order: lanes xor 8, 16, then warps
+      const int cw = tid / 32;
+#pragma unroll
+      for (int e = 0; e < 8; ++e) {
+        double d = (double)bs[e] - (double)bk[e];
+        d += __shfl_xor_sync(0xffffffffu, d, 8);
+        d += __shfl_xor_sync(0xffffffffu, d, 16);
+        if (lane < 8) bsum[cw * 64 + 8 * cq + e] = d;
+      }
+      asm volatile("bar.sync 1, 128;" ::: "memory");
+      if (tid < 64) {
+        double t = 0.0;
+        for (int w = 0; w < 4; ++w) t += bsum[w * 64 + tid];
+        a.part_bias[(size_t)blockIdx.x * 64 + tid] = t;
+      }
+    }
+  } else {
+    // ===================== epilogue: D quadrants -> fp32 partial [tap ci][co] =====================
+    // TMEM lane r: r < 64 -> g0 row co = r, r >= 64 -> g1 row co = r - 64; columns
+    // [ti 128, ti 128 + 64) x0, [ti 128 + 64, (ti + 1) 128) x1.  Warps on lanes 64..127
+    // park their (x0 + x1 column) sums in the drained stage memory; the other two add
+    // theirs and store coalesced rows of 64 output channels.
+    const int q = warp & 3;
+    const int co = (q & 1) * 32 + lane;
+    float* xbuf = reinterpret_cast<float*>(smem);     // [kTg * 64][64], reuses stage memory
+    float* dst = a.part + (size_t)blockIdx.x * kTg * 64 * 64;
+    const bool any = blk_end > blk_beg;
+    if (any) {
+      mbar_wait(acc_full, 0);
+      tc_fence_after();
+    }
+    // stage memory is drained once the last MMAs completed and the bias warps let go
+    if (do_bias) asm volatile("bar.sync 3, 256;" ::: "memory");
+    const uint32_t trow = tmem_base + ((uint32_t)(q * 32) << 16);
+    for (int pass = 0; pass < 2; ++pass) {
+      const bool mine = (pass == 0) == (q >= 2);
+      if (mine) {
+        for (int ti = 0; ti < kTg; ++ti) {
+          for (int c = 0; c < 64; c += 16) {
+            uint32_t rh[16], rl[16];
+            tmem_ld16(trow + (uint32_t)(ti * 128 + c), rh);
+            tmem_ld16(trow + (uint32_t)(ti * 128 + 64 + c), rl);
+            tmem_wait_ld();
+            const int col0 = ti * 64 + c;
+#pragma unroll
+            for (int e = 0; e < 16; ++e) {
+              const float v = any ? __uint_as_float(rh[e]) + __uint_as_float(rl[e]) : 0.f;
+              if (q >= 2)
+                xbuf[(col0 + e) * 64 + co] = v;
+              else
+                dst[(size_t)(col0 + e) * 64 + co] = v + xbuf[(col0 + e) * 64 + co];
+            }
+          }
+        }
+      }
+      asm volatile("bar.sync 2, 128;" ::: "memory");
+    }
+  }
+  if (do_bias && warp >= 2 && warp < 6) asm volatile("bar.sync 3, 256;" ::: "memory");
+
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_dealloc<512>(tmem_base);
+  }
+}
+
+__global__ void wgrad_planes_reduce_kernel(const float* __restrict__ part, const double* __restrict__ part_bias,
+                                           const PwArgs a, int grid, double scale, float* __restrict__ gw,
+                                           float* __restrict__ gb) {
+  const int Ci = a.Ci, Co = a.Co;
+  const int total = 9 * Ci * Co;
+  const int64_t pstride = (int64_t)kTg * 64 * 64;
+  for (int idx = blockIdx.x * blockDim.x + threadIdx.x; idx < total + Co; idx += gridDim.x * blockDim.x) {
+    if (idx < total) {
+      const int co = idx % Co;
+      const int ci = (idx / Co) % Ci;
+      const int tap = idx / (Co * Ci);
+      const int gi = tap / kTg, cob = co / 64, cib = ci / 64;
+      const int gid = (cob * a.mi + cib) * 3 + gi;
+      const int c_lo = grp_start(gid, grid, a), c_hi = grp_start(gid + 1, grid, a);
+      const int64_t off = ((int64_t)(tap - gi * kTg) * 64 + (ci - cib * 64)) * 64 + (co - cob * 64);
+      double s = 0.0;
+      for (int b = c_lo; b < c_hi; ++b) s += (double)part[b * pstride + off];
+      gw[idx] = (float)(scale * s);
+    } else if (gb) {
+      const int co = idx - total, cob = co / 64;
+      const int gid = cob * a.mi * 3;
+      const int c_lo = grp_start(gid, grid, a), c_hi = grp_start(gid + 1, grid, a);
+      double s = 0.0;
+      for (int b = c_lo; b < c_hi; ++b) s += part_bias[(int64_t)b * 64 + (co - cob * 64)];
+      gb[co] = (float)(scale * s);
+    }
+  }
+}
+
+// fp32 -> (bf16(v), bf16(v - bf16(v))) planes, for tensors not written by a conv epilogue
+__global__ void split_planes_kernel(const float4* __restrict__ in, int64_t n4, uint2* __restrict__ p0,
+                                    uint2* __restrict__ p1) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n4; i += (int64_t)gridDim.x * blockDim.x) {
+    const float4 v = in[i];
+    const __nv_bfloat162 a = __floats2bfloat162_rn(v.x, v.y), b = __floats2bfloat162_rn(v.z, v.w);
+    const __nv_bfloat162 c = __floats2bfloat162_rn(v.x - __low2float(a), v.y - __high2float(a));
+    const __nv_bfloat162 d = __floats2bfloat162_rn(v.z - __low2float(b), v.w - __high2float(b));
+    p0[i] = make_uint2(*reinterpret_cast<const uint32_t*>(&a), *reinterpret_cast<const uint32_t*>(&b));
+    p1[i] = make_uint2(*reinterpret_cast<const uint32_t*>(&c), *reinterpret_cast<const uint32_t*>(&d));
+  }
+}
+
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                  const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+EncodeTiledFn encode_fn() {
+  static EncodeTiledFn fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<EncodeTiledFn>(p);
+  });
+  if (!fn) fail(RP_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
+  return fn;
+}
+
+// bf16 NHWC plane as (C, W, H, N); box = 64 channels (128 B) x (W+2) columns from x = -1 x
+// rows, 128-byte swizzle (the MMA's MN-major layout)
+CUtensorMap make_map(const void* t, int n, int h, int w, int c, int rows) {
+  CUtensorMap m;
+  const cuuint64_t dims[4] = {(cuuint64_t)c, (cuuint64_t)w, (cuuint64_t)h, (cuuint64_t)n};
+  const cuuint64_t strides[3] = {(cuuint64_t)c * 2, (cuuint64_t)w * c * 2, (cuuint64_t)h * w * c * 2};
+  const cuuint32_t box[4] = {64, (cuuint32_t)(w + 2), (cuuint32_t)rows, 1};
+  const cuuint32_t estr[4] = {1, 1, 1, 1};
+  CUresult r = encode_fn()(&m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<void*>(t), dims, strides, box, estr,
+                           CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                           CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) fail(RP_ERR_CUDA, "cuTensorMapEncodeTiled (planes) failed (" + std::to_string((int)r) + ")");
+  return m;
+}
+
+std::mutex g_mu;
+std::map<std::tuple<const void*, int, int, int, int, int>, CUtensorMap> g_maps;
+
+const CUtensorMap& cached(const void* t, int n, int h, int w, int c, int rows) {
+  std::lock_guard<std::mutex> lk(g_mu);
+  auto key = std::make_tuple(t, n, h, w, c, rows);
+  auto it = g_maps.find(key);
+  if (it == g_maps.end()) {
+    if (g_maps.size() > 4096) g_maps.clear();
+    it = g_maps.emplace(key, make_map(t, n, h, w, c, rows)).first;
+  }
+  return it->second;
+}
+
+uint32_t round1k(uint64_t v) { return (uint32_t)((v + 1023) / 1024 * 1024); }
+
+struct PwPlan {
+  bool ok = false;
+  int rg, P, Pp, grid, nstages;
+  uint32_t g_slab, x_slab, x_off, stage;
+  size_t smem;
+};
+
+PwPlan plan(const ConvShape& s) {
+  PwPlan p;
+  if (s.co % 64 != 0 || s.ci % 64 != 0 || s.w + 2 > 256) return p;
+  if (3 * (s.co / 64) * (s.ci / 64) > kNumSMs) return p;
+  const int Wp = s.w + 2;
+  // (rows per block, stages) in order of preference
+  const int cand[][2] = {{4, 3}, {3, 3}, {2, 3}, {4, 2}, {2, 2}, {1, 2}};
+  for (const auto& c : cand) {
+    const int rg = std::min(c[0], s.h), st = c[1];
+    PwPlan q;
+    q.rg = rg;
+    q.nstages = st;
+    q.P = rg * Wp;
+    q.Pp = (q.P + 15) / 16 * 16;
+    q.g_slab = round1k((uint64_t)q.Pp * 128);
+    q.x_slab = (uint32_t)(rg + 2) * Wp * 128u;
+    q.x_off = 2 * q.g_slab + kLead;
+    q.stage = round1k((uint64_t)q.x_off + 2ull * q.x_slab + kTrail);
+    q.smem = st * (size_t)q.stage + (3 * kMaxStages + 2) * 8 + 4 * 64 * 8 + 256;
+    if (q.smem > (size_t)kMaxSmem) continue;
+    if ((size_t)kTg * 64 * 64 * 4 > st * (size_t)q.stage) continue;
+    q.grid = kNumSMs;
+    q.ok = true;
+    return q;
+  }
+  return p;
+}
+
+int64_t part_bytes(const PwPlan& p) { return ((int64_t)p.grid * kTg * 64 * 64 * 4 + 255) / 256 * 256; }
+
+}  // namespace
+
+bool conv3x3_wgrad_planes_supported(const ConvShape& s) { return plan(s).ok; }
+
+int64_t conv3x3_wgrad_planes_ws_bytes(const ConvShape& s) {
+  const PwPlan p = plan(s);
+  if (!p.ok) return 0;
+  return part_bytes(p) + (int64_t)p.grid * 64 * 8 + 256;
+}
+
+void split_planes(const float* in, int64_t n, void* p0, void* p1, cudaStream_t st) {
+  if (n <= 0) return;
+  if (n % 4) fail(RP_ERR_SHAPE, "split_planes: element count must be a multiple of 4");
+  const int64_t n4 = n / 4;
+  const int grid = (int)std::min<int64_t>((n4 + 255) / 256, 16 * kNumSMs);
+  split_planes_kernel<<<grid, 256, 0, st>>>(reinterpret_cast<const float4*>(in), n4, static_cast<uint2*>(p0),
+                                           static_cast<uint2*>(p1));
+  RP_LAUNCHED();
+}
+
+void conv3x3_wgrad_planes(const ConvShape& s, const void* x0, const void* x1, const void* g0, const void* g1,
+                          float scale, float* gw, float* gb, void* ws, cudaStream_t st) {
+  const PwPlan p = plan(s);
+  if (!p.ok) fail(RP_ERR_INTERNAL, "conv3x3_wgrad_planes: unsupported shape");
+  PwArgs a{};
+  a.N = s.n;
+  a.H = s.h;
+  a.W = s.w;
+  a.Ci = s.ci;
+  a.Co = s.co;
+  a.Wp = s.w + 2;
+  a.rg = p.rg;
+  a.P = p.P;
+  a.Pp = p.Pp;
+  a.nstages = p.nstages;
+  a.mo = s.co / 64;
+  a.mi = s.ci / 64;
+  a.blocks_per_img = (s.h + p.rg - 1) / p.rg;
+  a.num_blocks = s.n * a.blocks_per_img;
+  a.g_slab = p.g_slab;
+  a.x_slab = p.x_slab;
+  a.x_off = p.x_off;
+  a.stage = p.stage;
+  a.part = static_cast<float*>(ws);
+  a.part_bias = reinterpret_cast<double*>(static_cast<char*>(ws) + part_bytes(p));
+  const CUtensorMap& mg0 = cached(g0, s.n, s.h, s.w, s.co, p.rg);
+  const CUtensorMap& mg1 = cached(g1, s.n, s.h, s.w, s.co, p.rg);
+  const CUtensorMap& mx0 = cached(x0, s.n, s.h, s.w, s.ci, p.rg + 2);
+  const CUtensorMap& mx1 = cached(x1, s.n, s.h, s.w, s.ci, p.rg + 2);
+  static bool configured = false;
+  if (!configured) {
+    RP_CUDA(cudaFuncSetAttribute(wgrad_planes_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxSmem));
+    configured = true;
+  }
+  wgrad_planes_kernel<<<p.grid, kThreads, p.smem, st>>>(mg0, mg1, mx0, mx1, a);
+  RP_LAUNCHED();
+  const int total = 9 * s.ci * s.co + s.co;
+  wgrad_planes_reduce_kernel<<<ceil_div(total, 256), 256, 0, st>>>(a.part, a.part_bias, a, p.grid, (double)scale,
+                                                                   gw, gb);
+  RP_LAUNCHED();
+}
+
+}  // namespace rp::k

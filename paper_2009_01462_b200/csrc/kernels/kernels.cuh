@@ -56,8 +56,10 @@ void conv3x3_wgrad_simt(const ConvShape& s, const float* in, const float* g, flo
 enum { TC_MODE_TF32 = 0, TC_MODE_X3TF32 = 1, TC_MODE_X3BF16 = 2 };
 bool conv3x3_tc_supported(const ConvShape& s);
 int64_t conv3x3_tc_ws_bytes(const ConvShape& s);
+// out_planes (optional): bf16 [2][pixels * co] receives the plane pair of out.
 void conv3x3_fwd_tc(const ConvShape& s, const float* in, const float* w_hwio, bool dgrad_weights, const float* bias,
-                    const float* aux, float h, int epi, float* out, int mode, void* ws, cudaStream_t st);
+                    const float* aux, float h, int epi, float* out, int mode, void* ws, cudaStream_t st,
+                    void* out_planes = nullptr);
 
 // tcgen05 bf16-operand conv, fp32 accumulate (conv_bf16.cu): Co % 128 == 0, Ci % 32 == 0.
 bool conv3x3_bf16_supported(const ConvShape& s);
@@ -77,6 +79,15 @@ bool conv3x3_wgrad_bf16_supported(const ConvShape& s);
 int64_t conv3x3_wgrad_bf16_ws_bytes(const ConvShape& s);
 void conv3x3_wgrad_bf16(const ConvShape& s, const float* in, const float* g, float scale, float* gw, float* gb,
                         void* ws, cudaStream_t st);
+
+// tcgen05 weight gradient from bf16 plane pairs x = x0 + x1, g = g0 + g1 (conv_wgrad_planes.cu):
+// the fp32-accurate wgrad when the producers wrote the planes; Ci, Co % 64 == 0.
+bool conv3x3_wgrad_planes_supported(const ConvShape& s);
+int64_t conv3x3_wgrad_planes_ws_bytes(const ConvShape& s);
+void conv3x3_wgrad_planes(const ConvShape& s, const void* x0, const void* x1, const void* g0, const void* g1,
+                          float scale, float* gw, float* gb, void* ws, cudaStream_t st);
+// fp32 [n] -> bf16 planes p0 = bf16(v), p1 = bf16(v - p0)   (n % 4 == 0)
+void split_planes(const float* in, int64_t n, void* p0, void* p1, cudaStream_t st);
 
 // ---- stem S (stem.cu): Cin <= 4 streaming kernels (SIMT conv path otherwise)
 bool stem_supported(const ConvShape& s);

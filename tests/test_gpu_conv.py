@@ -147,6 +147,41 @@ def test_wgrad_bf16(shape):
     assert ew <= 1e-2 and eb <= 1e-5, (ew, eb)     # bf16 operands; the bias sums fp32 values
 
 
+def run_wgrad_planes(n, hh, ww, ci, co, seed=0, scale=0.37):
+    rng = np.random.default_rng(seed)
+    x = rng.uniform(-1, 1, (n, hh, ww, ci)).astype(np.float32)
+    g = rng.uniform(-1, 1, (n, hh, ww, co)).astype(np.float32)
+    want_w = scale * O.conv3x3_wgrad(x.astype(np.float64), g.astype(np.float64))
+    want_b = scale * g.astype(np.float64).reshape(-1, co).sum(axis=0)
+    dev = torch.device("cuda")
+    tx, tg = torch.from_numpy(x).to(dev), torch.from_numpy(g).to(dev)
+    planes = [torch.empty(t.numel(), dtype=torch.bfloat16, device=dev) for t in (tx, tx, tg, tg)]
+    rp.check(lib().rp_op_split_planes(C.c_void_p(tx.data_ptr()), tx.numel(), C.c_void_p(planes[0].data_ptr()),
+                                      C.c_void_p(planes[1].data_ptr()), None))
+    rp.check(lib().rp_op_split_planes(C.c_void_p(tg.data_ptr()), tg.numel(), C.c_void_p(planes[2].data_ptr()),
+                                      C.c_void_p(planes[3].data_ptr()), None))
+    gw = torch.full((3, 3, ci, co), float("nan"), device=dev)
+    gb = torch.full((co,), float("nan"), device=dev)
+    wsb = lib().rp_op_conv3x3_wgrad_planes_workspace_bytes(n, hh, ww, ci, co)
+    ws = torch.empty(wsb, dtype=torch.uint8, device=dev)
+    rp.check(lib().rp_op_conv3x3_wgrad_planes(n, hh, ww, ci, co, *[C.c_void_p(t.data_ptr()) for t in planes], scale,
+                                              C.c_void_p(gw.data_ptr()), C.c_void_p(gb.data_ptr()),
+                                              C.c_void_p(ws.data_ptr()), wsb, None))
+    torch.cuda.synchronize()
+    return gw.cpu().numpy().astype(np.float64), gb.cpu().numpy().astype(np.float64), want_w, want_b
+
+
+# x, g as 16-bit-mantissa plane pairs: ~2^-17 relative per product
+@pytest.mark.parametrize("shape", [(2, 32, 32, 64, 64), (3, 8, 8, 64, 64), (1, 12, 10, 64, 64), (2, 16, 16, 128, 64),
+                                   (2, 8, 8, 64, 128), (1, 16, 16, 256, 256), (2, 7, 9, 64, 64)])
+def test_wgrad_planes(shape):
+    gw, gb, ww_, wb = run_wgrad_planes(*shape)
+    ew = np.abs(gw - ww_).max() / np.abs(ww_).max()
+    eb = np.abs(gb - wb).max() / np.abs(wb).max()
+    print(f"wgrad planes {shape}: w {ew:.2e} b {eb:.2e}")
+    assert ew <= 3e-5 and eb <= 3e-5, (ew, eb)
+
+
 def test_wgrad_deterministic():
     a = run_wgrad(2, 32, 32, 64, 64, "fp32", seed=5)
     b = run_wgrad(2, 32, 32, 64, 64, "fp32", seed=5)

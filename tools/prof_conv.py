@@ -32,6 +32,13 @@ ws_b = max(lib().rp_op_conv3x3_workspace_bytes(c, c), lib().rp_op_conv3x3_wgrad_
 ws = torch.empty(ws_b, dtype=torch.uint8, device=dev)
 gw = torch.empty(3, 3, c, c, device=dev)
 gb = torch.empty(c, device=dev)
+planes = [torch.empty(n * h * w * c, dtype=torch.bfloat16, device=dev) for _ in range(4)]
+for src, (p0, p1) in ((x, planes[:2]), (g, planes[2:])):
+    rp.check(lib().rp_op_split_planes(C.c_void_p(src.data_ptr()), src.numel(), C.c_void_p(p0.data_ptr()),
+                                      C.c_void_p(p1.data_ptr()), None))
+ws_p = lib().rp_op_conv3x3_wgrad_planes_workspace_bytes(n, h, w, c, c)
+ws_b = max(ws_b, ws_p)
+ws = torch.empty(ws_b, dtype=torch.uint8, device=dev)
 P = C.c_void_p
 m = rp.MATH[a.math]
 flops = 2 * 9 * c * c * n * h * w
@@ -47,6 +54,10 @@ for which in a.which.split(","):
         elif which == "dgrad":
             rp.check(lib().rp_op_conv3x3(n, h, w, c, c, P(g.data_ptr()), P(wt.data_ptr()), 1, None, P(x.data_ptr()),
                                          1.0, 3, P(out.data_ptr()), m, P(ws.data_ptr()), ws_b, None))
+        elif which == "wgrad_planes":
+            rp.check(lib().rp_op_conv3x3_wgrad_planes(n, h, w, c, c, *[C.c_void_p(t.data_ptr()) for t in planes], 1.0,
+                                                      P(gw.data_ptr()), P(gb.data_ptr()), P(ws.data_ptr()), ws_b,
+                                                      None))
         else:
             rp.check(lib().rp_op_conv3x3_wgrad(n, h, w, c, c, P(x.data_ptr()), P(g.data_ptr()), 1.0,
                                                P(gw.data_ptr()), P(gb.data_ptr()), m, P(ws.data_ptr()), ws_b, None))
