@@ -73,7 +73,24 @@ int64_t weight_ws_bytes(const rp_geometry& g) {
 
 int64_t wgrad_ws_bytes(const k::ConvShape& s) {
   return std::max({k::conv3x3_wgrad_ws_bytes(s), k::conv3x3_wgrad_tc_ws_bytes(s, true),
-                   k::conv3x3_wgrad_tc_ws_bytes(s, false), k::conv3x3_wgrad_bf16_ws_bytes(s)});
+                   k::conv3x3_wgrad_tc_ws_bytes(s, false), k::conv3x3_wgrad_bf16_ws_bytes(s),
+                   k::conv3x3_wgrad_planes_ws_bytes(s)});
+}
+
+// The plane-pair block path (fp32 math): every conv of the block on the tcgen05 kernel, whose
+// epilogue also writes the bf16 plane pair (v = p0 + p1) of its output, so both weight
+// gradients run on the TMA-fed plane wgrad (conv_wgrad_planes.cu). RP_WGRAD_PLANES=0 turns
+// it off (the fp32-operand 3xTF32 wgrad then runs).
+bool planes_path(const rp_geometry& g, int nrows, int math) {
+  static const bool enabled = [] {
+    const char* e = std::getenv("RP_WGRAD_PLANES");
+    return !(e && std::string(e) == "0");
+  }();
+  if (!enabled || math != RP_MATH_FP32 || nrows <= 0) return false;
+  const k::ConvShape s1{nrows, g.height, g.width, g.channels, g.hidden};
+  const k::ConvShape s2{nrows, g.height, g.width, g.hidden, g.channels};
+  return k::conv3x3_tc_supported(s1) && k::conv3x3_tc_supported(s2) && k::conv3x3_wgrad_planes_supported(s1) &&
+         k::conv3x3_wgrad_planes_supported(s2);
 }
 
 // Weight gradient (+ bias sums): tcgen05 when the math mode and shape allow, SIMT otherwise.
@@ -106,8 +123,14 @@ int64_t op_workspace_bytes(const rp_geometry& g, int nrows) {
 // math mode asks for tensor cores and the shape is supported, the SIMT kernel otherwise.
 // dgrad: `w` is the forward conv's HWIO weight; the conv runs on the cotangent.
 void conv(const k::ConvShape& s, const float* in, const float* w, bool dgrad, const float* bias, const float* aux,
-          float h, int epi, float* out, int math, void* wws, int prof_cls, bool aux_read, cudaStream_t st) {
-  prof::Scope ps(prof_cls, st, conv_flops(s), conv_bytes(s, aux_read));
+          float h, int epi, float* out, int math, void* wws, int prof_cls, bool aux_read, cudaStream_t st,
+          void* out_planes = nullptr) {
+  prof::Scope ps(prof_cls, st, conv_flops(s), conv_bytes(s, aux_read) + (out_planes ? 4.0 * s.pixels() * s.co : 0.0));
+  if (out_planes) {   // only the fp32 tcgen05 kernel writes plane pairs (planes_path() checked the shape)
+    if (math != RP_MATH_FP32 || !k::conv3x3_tc_supported(s)) fail(RP_ERR_INTERNAL, "conv: plane output needs fp32 tcgen05");
+    k::conv3x3_fwd_tc(s, in, w, dgrad, bias, aux, h, epi, out, fp32_split(), wws, st, out_planes);
+    return;
+  }
   // RP_MATH_BF16: bf16 operands where the bf16 kernel tiles the shape (Co % 128, Ci % 32),
   // the fp32-accurate 3xTF32 kernel elsewhere (never less precise than asked for)
   if (math == RP_MATH_BF16 && k::conv3x3_bf16_supported(s)) {
@@ -161,6 +184,50 @@ void block_bwd(const rp_geometry& g, int nrows, const float* x, const float* a, 
   // g <- g + dpre * W1^T   (in place)                          (network.cpp:104)
   conv(shape(g, nrows, Ch, C), dpre, pb + L.w1, true, nullptr, gio, 1.f, k::EPI_ADD, gio, math, wws,
        RP_PROF_CONV_DGRAD, true, st);
+}
+
+// Plane-pair variants: a_p / x_next_p / x_p / g_p / dpre_p are bf16 [2][elements] pairs.
+void block_fwd_planes(const rp_geometry& g, int nrows, const float* x, const float* pb, float* a, float* x_next,
+                      void* a_p, void* x_next_p, void* ws, int64_t ws_bytes, cudaStream_t st) {
+  const ParamLayout L = ParamLayout::of(g);
+  const bool tanh_act = g.activation == RP_ACT_TANH;
+  if (ws_bytes < weight_ws_bytes(g)) fail(RP_ERR_RANGE, "block_fwd: workspace too small");
+  const k::ConvShape s1 = shape(g, nrows, g.channels, g.hidden), s2 = shape(g, nrows, g.hidden, g.channels);
+  conv(s1, x, pb + L.w1, false, pb + L.b1, nullptr, 1.f, tanh_act ? k::EPI_BIAS_TANH : k::EPI_BIAS, a, RP_MATH_FP32,
+       ws, RP_PROF_CONV_FPROP, false, st, a_p);
+  conv(s2, a, pb + L.w2, false, pb + L.b2, x, (float)g.step_h, k::EPI_RESID, x_next, RP_MATH_FP32, ws,
+       RP_PROF_CONV_FPROP, true, st, x_next_p);
+}
+
+void wgrad_planes(const k::ConvShape& s, const void* xp, const void* gp, float scale, float* gw, float* gb, void* ws,
+                  cudaStream_t st) {
+  prof::Scope ps(RP_PROF_CONV_WGRAD, st, conv_flops(s), 4.0 * (double)s.pixels() * (s.ci + s.co));
+  const auto* x0 = static_cast<const uint16_t*>(xp);   // bf16 bits
+  const auto* g0 = static_cast<const uint16_t*>(gp);
+  k::conv3x3_wgrad_planes(s, x0, x0 + s.pixels() * s.ci, g0, g0 + s.pixels() * s.co, scale, gw, gb, ws, st);
+}
+
+void block_bwd_planes(const rp_geometry& g, int nrows, const void* x_p, const float* a, const void* a_p,
+                      const float* pb, float* gio, void* g_p, float* dpre, void* dpre_p, float* gb, void* ws,
+                      int64_t ws_bytes, cudaStream_t st) {
+  const ParamLayout L = ParamLayout::of(g);
+  const int C = g.channels, Ch = g.hidden;
+  const bool tanh_act = g.activation == RP_ACT_TANH;
+  const float h = (float)g.step_h;
+  Carve cv{static_cast<char*>(ws), ws_bytes};
+  void* wws = cv.take<char>(weight_ws_bytes(g));
+  const int64_t wg_bytes = std::max(wgrad_ws_bytes(shape(g, nrows, Ch, C)), wgrad_ws_bytes(shape(g, nrows, C, Ch)));
+  void* wgws = cv.take<char>(wg_bytes);
+  // dpre = h (g * W2^T) (1 - a^2), and its planes                (network.cpp:100-101)
+  conv(shape(g, nrows, C, Ch), gio, pb + L.w2, true, nullptr, a, h, tanh_act ? k::EPI_TANH_BWD : k::EPI_SCALE, dpre,
+       RP_MATH_FP32, wws, RP_PROF_CONV_DGRAD, tanh_act, st, dpre_p);
+  // gW2 = h a^T g, gb2 = h sum g                                  (network.cpp:98-99)
+  wgrad_planes(shape(g, nrows, Ch, C), a_p, g_p, h, gb + L.w2, gb + L.b2, wgws, st);
+  // gW1 = x^T dpre, gb1 = sum dpre                                (network.cpp:102-103)
+  wgrad_planes(shape(g, nrows, C, Ch), x_p, dpre_p, 1.f, gb + L.w1, gb + L.b1, wgws, st);
+  // g <- g + dpre * W1^T in place, and the planes of the new g   (network.cpp:104)
+  conv(shape(g, nrows, Ch, C), dpre, pb + L.w1, true, nullptr, gio, 1.f, k::EPI_ADD, gio, RP_MATH_FP32, wws,
+       RP_PROF_CONV_DGRAD, true, st, g_p);
 }
 
 void stem_fwd(const rp_geometry& g, int nrows, const float* xr, const float* ps, float* x0, cudaStream_t st) {
@@ -383,6 +450,47 @@ int rp_op_block_bwd(const rp_geometry* g, int32_t nrows, const float* x, const f
     if (nrows <= 0) return;
     need(ws, "ws");
     block_bwd(*g, nrows, x, a, pb, g_io, dpre, gb, math, ws, ws_bytes, S(stream));
+  });
+}
+
+int32_t rp_op_block_planes_supported(const rp_geometry* g, int32_t nrows, int32_t math) {
+  if (!g || nrows <= 0) return 0;
+  return planes_path(*g, nrows, math) ? 1 : 0;
+}
+
+int rp_op_block_fwd_planes(const rp_geometry* g, int32_t nrows, const float* x, const float* pb, float* a,
+                           float* x_next, void* a_planes, void* x_next_planes, void* ws, int64_t ws_bytes,
+                           void* stream) {
+  return guard([&] {
+    need(g, "geometry");
+    if (!planes_path(*g, nrows, RP_MATH_FP32)) fail(RP_ERR_SHAPE, "block_fwd_planes: geometry not on the plane path");
+    need(x, "x");
+    need(pb, "pb");
+    need(a, "a");
+    need(x_next, "x_next");
+    need(a_planes, "a_planes");
+    block_fwd_planes(*g, nrows, x, pb, a, x_next, a_planes, x_next_planes, ws, ws_bytes, S(stream));
+  });
+}
+
+int rp_op_block_bwd_planes(const rp_geometry* g, int32_t nrows, const void* x_planes, const float* a,
+                           const void* a_planes, const float* pb, float* g_io, void* g_planes, float* dpre,
+                           void* dpre_planes, float* gb, void* ws, int64_t ws_bytes, void* stream) {
+  return guard([&] {
+    need(g, "geometry");
+    if (!planes_path(*g, nrows, RP_MATH_FP32)) fail(RP_ERR_SHAPE, "block_bwd_planes: geometry not on the plane path");
+    if (ws_bytes < op_workspace_bytes(*g, nrows)) fail(RP_ERR_RANGE, "block_bwd_planes: workspace too small");
+    need(x_planes, "x_planes");
+    need(a, "a");
+    need(a_planes, "a_planes");
+    need(pb, "pb");
+    need(g_io, "g_io");
+    need(g_planes, "g_planes");
+    need(dpre, "dpre");
+    need(dpre_planes, "dpre_planes");
+    need(gb, "gb");
+    block_bwd_planes(*g, nrows, x_planes, a, a_planes, pb, g_io, g_planes, dpre, dpre_planes, gb, ws, ws_bytes,
+                     S(stream));
   });
 }
 

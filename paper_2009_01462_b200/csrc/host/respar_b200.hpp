@@ -225,6 +225,11 @@ class DecoupledTrainer {
     bool kappa_zero = true;
     std::vector<DeviceArray> xs;  // tape inputs x_1..x_{n-1}
     std::vector<DeviceArray> as;  // tape activations a_0..a_{n-1}
+    // plane-pair tape (fp32 math on tcgen05 shapes): bf16 [2][elements] pairs of the block
+    // inputs x_0..x_{n-1} and of a_0..a_{n-1}; dpre_p / g_p are backward scratch
+    std::vector<DeviceArray> xps, aps;
+    DeviceArray dpre_p, g_p;
+    bool tape_planes = false;
     DeviceArray x0, dpre, ws, red_ws, pooled, logits, loss;
     DeviceArray snap_lam, snap_kappa;
     int snap_rows = -1;

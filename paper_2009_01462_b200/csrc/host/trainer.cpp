@@ -379,6 +379,16 @@ void DecoupledTrainer::ensure_capacity(int nrows) {
     }
     if (k == 0) st.x0.allocate(st.device, (int64_t)nrows * feat() * 4);
     st.dpre.allocate(st.device, (int64_t)nrows * hid() * 4);
+    if (rp_op_block_planes_supported(&geo_, nrows, math_)) {
+      st.xps.resize(n);
+      st.aps.resize(n);
+      for (int i = 0; i < n; ++i) {
+        st.xps[i].allocate(st.device, (int64_t)nrows * feat() * 4);
+        st.aps[i].allocate(st.device, (int64_t)nrows * hid() * 4);
+      }
+      st.dpre_p.allocate(st.device, (int64_t)nrows * hid() * 4);
+      st.g_p.allocate(st.device, (int64_t)nrows * feat() * 4);
+    }
     st.ws.allocate(st.device, rp_op_workspace_bytes(&geo_, nrows, math_));
     if (k == stages() - 1) {
       st.pooled.allocate(st.device, (int64_t)nrows * geo_.channels * 4);
@@ -422,6 +432,23 @@ void DecoupledTrainer::run_forward(Stage& st, const float* input, int nrows, flo
   }
   st.input0 = cur;
   const int n = st.end - st.begin;
+  st.tape_planes = n > 0 && rp_op_block_planes_supported(&geo_, nrows, math_);
+  if (st.tape_planes) {
+    const int64_t e = (int64_t)nrows * feat();
+    auto* p = st.xps[0].get<uint16_t>();
+    check(rp_op_split_planes(cur, e, p, p + e, s));
+    for (int i = 0; i < n; ++i) {
+      const int l = st.begin + i;
+      float* out = i == n - 1 ? out_features : st.xs[i + 1].get();
+      check(rp_op_block_fwd_planes(&geo_, nrows, cur, P + L.block0 + (int64_t)l * L.block_stride, st.as[i].get(), out,
+                                   st.aps[i].get(), i == n - 1 ? nullptr : st.xps[i + 1].get(), st.ws.get(),
+                                   st.ws.bytes(), s));
+      cur = out;
+    }
+    if (st.index == stages() - 1)
+      check(rp_op_head_fwd(&geo_, nrows, out_features, P + L.t_w, st.pooled.get(), st.logits.get(), s));
+    return;
+  }
   for (int i = 0; i < n; ++i) {
     const int l = st.begin + i;
     float* out = i == n - 1 ? out_features : st.xs[i + 1].get();
@@ -463,6 +490,16 @@ void DecoupledTrainer::run_backward(Stage& st, const int32_t* labels, int nrows,
     check(rp_op_synthetic_grad((int)kind_, lam_next, x_end, kap_next, n, w, g, st.red_ws.get(), s));
   }
   const int nb = st.end - st.begin;
+  if (st.tape_planes && st.fwd_rows == nrows) {
+    auto* gp = st.g_p.get<uint16_t>();
+    check(rp_op_split_planes(g, n, gp, gp + n, s));
+    for (int i = nb - 1; i >= 0; --i) {
+      const int l = st.begin + i;
+      const int64_t off = L.block0 + (int64_t)l * L.block_stride;
+      check(rp_op_block_bwd_planes(&geo_, nrows, st.xps[i].get(), st.as[i].get(), st.aps[i].get(), P + off, g, gp,
+                                   st.dpre.get(), st.dpre_p.get(), G + off, st.ws.get(), st.ws.bytes(), s));
+    }
+  } else
   for (int i = nb - 1; i >= 0; --i) {
     const int l = st.begin + i;
     const float* xin = i == 0 ? st.input0 : st.xs[i].get();

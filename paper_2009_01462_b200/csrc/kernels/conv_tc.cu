@@ -48,7 +48,7 @@ namespace {
 
 using namespace rp::umma;
 
-constexpr int kThreads = 320;
+constexpr int kThreads = 480;       // w0 halo TMA, w1 MMA, w2-5 converters, w6-13 epilogue, w14 weight TMA
 constexpr int kWStages = 3;          // one weight stage = one filter row (3 taps) of one chunk
 constexpr int kChunk = 16;           // input channels per halo chunk
 constexpr bool kUseCollector = false;  // A-operand collector reuse (measured: no gain here)
@@ -67,6 +67,8 @@ struct TcArgs {
   uint32_t halo_stride; // bytes per halo slot (raw + lo + pads)
   uint32_t w_tap;       // bytes of one tap's A operand (128 rows x 16 channels x 4 B; bf16: x 2 B)
   uint32_t plane_bytes; // X3BF16: one bf16 plane of the halo chunk (halo_pos x 32 B)
+  uint32_t raw_stride;  // X3BF16: bytes per raw fp32 halo slot ([pos][16 ch], TMA target)
+  int raw_slots;        // X3BF16: depth of the raw ring (2 or 3)
   float h;
   const float* w;       // prepped [chunk][tap][kg][128 rows][4]
   const float* bias;
@@ -167,6 +169,23 @@ __device__ __forceinline__ void split3_bf16(const float (&v)[8], uint4& p0, uint
   p2 = make_uint4(c[0], c[1], c[2], c[3]);
 }
 
+// the same for 4 values: three packed bf16x4 planes
+__device__ __forceinline__ void split3_bf16_4(const float (&v)[4], uint2& p0, uint2& p1, uint2& p2) {
+  uint32_t a[2], b[2], c[2];
+#pragma unroll
+  for (int i = 0; i < 2; ++i) {
+    const __nv_bfloat162 h = __floats2bfloat162_rn(v[2 * i], v[2 * i + 1]);
+    a[i] = *reinterpret_cast<const uint32_t*>(&h);
+    const float r0 = v[2 * i] - __low2float(h), r1 = v[2 * i + 1] - __high2float(h);
+    const __nv_bfloat162 m = __floats2bfloat162_rn(r0, r1);
+    b[i] = *reinterpret_cast<const uint32_t*>(&m);
+    c[i] = pack_bf16x2(r0 - __low2float(m), r1 - __high2float(m));
+  }
+  p0 = make_uint2(a[0], a[1]);
+  p1 = make_uint2(b[0], b[1]);
+  p2 = make_uint2(c[0], c[1]);
+}
+
 template <int EPI, int MODE>
 __global__ void __launch_bounds__(kThreads, 1)
     conv3x3_tc_kernel(const __grid_constant__ CUtensorMap tmap, const TcArgs a) {
@@ -176,9 +195,12 @@ __global__ void __launch_bounds__(kThreads, 1)
 
   // ---- shared memory carve-up
   const uint32_t w_stage = 3 * a.w_tap;
+  constexpr bool BF = MODE == MODE_X3BF16;
+  // X3BF16: [2 plane slots][raw_slots raw slots][weights]...; else [2 halo slots][weights]...
   uint8_t* halo_base = smem;                                  // 2 slots
-  uint8_t* w_base = smem + 2 * a.halo_stride;                 // kWStages stages
-  float* xchg = reinterpret_cast<float*>(w_base + kWStages * w_stage);   // [2 buf][2 pairs][2 sides][32][32]
+  uint8_t* raw_base = smem + 2 * a.halo_stride;               // X3BF16 only
+  uint8_t* w_base = smem + 2 * a.halo_stride + (BF ? a.raw_slots * a.raw_stride : 0u);   // kWStages stages
+  float* xchg = reinterpret_cast<float*>(w_base + kWStages * w_stage);   // [2 groups][2 pairs][2 sides][32][32]
   uint64_t* bars = reinterpret_cast<uint64_t*>(xchg + 2 * 2 * 2 * 32 * 32);
   uint64_t* halo_full = bars;        // [2]
   uint64_t* halo_conv = bars + 2;    // [2]
@@ -187,14 +209,17 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint64_t* w_empty = bars + 6 + kWStages;
   uint64_t* acc_full = bars + 6 + 2 * kWStages;   // [2]
   uint64_t* acc_empty = bars + 8 + 2 * kWStages;  // [2]
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 10 + 2 * kWStages);
+  uint64_t* raw_full = bars + 10 + 2 * kWStages;  // [3] X3BF16: TMA -> converters
+  uint64_t* raw_empty = bars + 13 + 2 * kWStages; // [3] X3BF16: converters -> TMA
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 16 + 2 * kWStages);
+  int* pos_tab = reinterpret_cast<int*>(bars + 32);   // [2 groups][128] epilogue position -> NHWC offset
 
   constexpr bool THREE = MODE != MODE_TF32;
-  constexpr bool BF = MODE == MODE_X3BF16;
   auto halo_raw = [&](int s) { return halo_base + s * a.halo_stride + 128; };
   auto halo_lo = [&](int s) { return halo_base + s * a.halo_stride + 256 + a.halo_bytes; };
-  // X3BF16: planes p = 0..2 of bf16 [2 kg][positions][8], each behind a 128-byte zero pad
-  auto plane = [&](int s, int p) { return halo_base + s * a.halo_stride + 256 + a.halo_bytes + p * (a.plane_bytes + 128); };
+  // X3BF16: planes p = 0..2 of bf16 [2 kg][positions][8], each between 128-byte zero pads
+  auto plane = [&](int s, int p) { return halo_base + s * a.halo_stride + 128 + p * (a.plane_bytes + 128); };
+  auto raw_slot = [&](int r) { return raw_base + r * a.raw_stride; };
   auto w_s = [&](int s) { return w_base + s * w_stage; };
 
   if (threadIdx.x == 0) {
@@ -203,11 +228,15 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_init(&halo_conv[i], 128);
       mbar_init(&halo_empty[i], 1);
       mbar_init(&acc_full[i], 1);
-      mbar_init(&acc_empty[i], 128);
+      mbar_init(&acc_empty[i], 256);
     }
     for (int i = 0; i < kWStages; ++i) {
       mbar_init(&w_full[i], 1);
       mbar_init(&w_empty[i], 1);
+    }
+    for (int i = 0; i < 3; ++i) {
+      mbar_init(&raw_full[i], 1);
+      mbar_init(&raw_empty[i], 128);
     }
     fence_barrier_init();
     prefetch_tmap(&tmap);
@@ -215,11 +244,9 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (warp == 1) tmem_alloc<512>(tmem_slot);
   // zero the 128-byte pads around the halo buffers (read only for discarded positions)
   if constexpr (BF) {
-    for (int i = threadIdx.x; i < 2 * 5 * 32; i += blockDim.x) {
-      const int s = i / 160, part = (i / 32) % 5, w = i % 32;
-      uint8_t* base = part == 0 ? halo_base + s * a.halo_stride
-                    : part == 1 ? halo_base + s * a.halo_stride + 128 + a.halo_bytes
-                                : plane(s, part - 2) + a.plane_bytes;
+    for (int i = threadIdx.x; i < 2 * 4 * 32; i += blockDim.x) {
+      const int s = i / 128, part = (i / 32) % 4, w = i % 32;
+      uint8_t* base = part == 0 ? halo_base + s * a.halo_stride : plane(s, part - 1) + a.plane_bytes;
       reinterpret_cast<uint32_t*>(base)[w] = 0u;
     }
   } else {
@@ -238,24 +265,43 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int Wp = a.Wp;
 
   if (warp == 0) {
-    // ===================== TMA producer =====================
-    int hs = 0, ws = 0;
-    uint32_t hph = 0, wph = 0;
+    // ===================== halo TMA producer =====================
+    // X3BF16: into the raw ring, released by the converters (runs up to raw_slots chunks
+    // ahead of the converters, independent of the MMA); else into the halo slot the MMA
+    // releases.
+    int hs = 0;
+    uint32_t hph = 0;
+    const int nslots = BF ? a.raw_slots : 2;
+    UnitIter it(a.Co / 64, a.N, a.T);
+    int cb, n, tile0, ntiles;
+    while (it.next(cb, n, tile0, ntiles)) {
+      const int f0 = tile0 * 128;
+      const int y0 = f0 / Wp;
+      for (int c = 0; c < a.nchunks; ++c) {
+        mbar_wait(BF ? &raw_empty[hs] : &halo_empty[hs], hph ^ 1);
+        if (elect_one()) {
+          if constexpr (BF) {
+            mbar_arrive_expect_tx(&raw_full[hs], a.halo_bytes);
+            tma_load_4d(&tmap, &raw_full[hs], raw_slot(hs), kChunk * c, -1, y0 - 1, n);
+          } else {
+            mbar_arrive_expect_tx(&halo_full[hs], a.halo_bytes);
+            tma_load_5d(&tmap, &halo_full[hs], halo_raw(hs), 0, -1, y0 - 1, 4 * c, n);
+          }
+        }
+        __syncwarp();
+        if (++hs == nslots) hs = 0, hph ^= 1;
+      }
+    }
+  } else if (warp == 14) {
+    // ===================== weight TMA producer =====================
+    int ws = 0;
+    uint32_t wph = 0;
     const uint32_t wbytes = 3 * a.w_tap;
     UnitIter it(a.Co / 64, a.N, a.T);
     int cb, n, tile0, ntiles;
     while (it.next(cb, n, tile0, ntiles)) {
       const uint8_t* wcb = reinterpret_cast<const uint8_t*>(a.w) + (int64_t)cb * a.nchunks * 9 * a.w_tap;
-      const int f0 = tile0 * 128;
-      const int y0 = f0 / Wp;
       for (int c = 0; c < a.nchunks; ++c) {
-        mbar_wait(&halo_empty[hs], hph ^ 1);
-        if (elect_one()) {
-          mbar_arrive_expect_tx(&halo_full[hs], a.halo_bytes);
-          tma_load_5d(&tmap, &halo_full[hs], halo_raw(hs), 0, -1, y0 - 1, 4 * c, n);
-        }
-        __syncwarp();
-        if (++hs == 2) hs = 0, hph ^= 1;
         for (int dy = 0; dy < 3; ++dy) {
           mbar_wait(&w_empty[ws], wph ^ 1);
           if (elect_one()) {
@@ -377,8 +423,39 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
   } else if (warp < 6) {
     // ===================== converters (hi/lo split of the halo) =====================
-    if (THREE) {
-      const int tid = threadIdx.x - 64;
+    const int tid = threadIdx.x - 64;
+    if constexpr (BF) {
+      // raw [pos][16 ch] fp32 (raw ring) -> planes [2 kg of 8 ch][pos][8 bf16] (plane slot);
+      // one float4 (4 channels of one position) per thread and step: conflict-free LDS.128,
+      // three STS.64
+      const int hp = a.halo_pos;
+      int rs = 0, hs = 0;
+      uint32_t rph = 0, hph = 0;
+      UnitIter it(a.Co / 64, a.N, a.T);
+      int cb, n, tile0, ntiles;
+      while (it.next(cb, n, tile0, ntiles)) {
+        for (int c = 0; c < a.nchunks; ++c) {
+          mbar_wait(&raw_full[rs], rph);
+          mbar_wait(&halo_empty[hs], hph ^ 1);      // the MMA is done with this plane slot
+          const float4* raw = reinterpret_cast<const float4*>(raw_slot(rs));
+          uint2* p0 = reinterpret_cast<uint2*>(plane(hs, 0));
+          uint2* p1 = reinterpret_cast<uint2*>(plane(hs, 1));
+          uint2* p2 = reinterpret_cast<uint2*>(plane(hs, 2));
+          for (int i = tid; i < 4 * hp; i += 128) {
+            const float4 v = raw[i];
+            const int pos = i >> 2, q = i & 3;
+            const int o = ((q >> 1) * hp + pos) * 2 + (q & 1);
+            const float vv[4] = {v.x, v.y, v.z, v.w};
+            split3_bf16_4(vv, p0[o], p1[o], p2[o]);
+          }
+          mbar_arrive(&raw_empty[rs]);
+          fence_proxy_async_smem();
+          mbar_arrive(&halo_conv[hs]);
+          if (++rs == a.raw_slots) rs = 0, rph ^= 1;
+          if (++hs == 2) hs = 0, hph ^= 1;
+        }
+      }
+    } else if (THREE) {
       int hs = 0;
       uint32_t hph = 0;
       const int n16 = (int)(a.halo_bytes / 16);
@@ -388,32 +465,13 @@ __global__ void __launch_bounds__(kThreads, 1)
         for (int c = 0; c < a.nchunks; ++c) {
           mbar_wait(&halo_full[hs], hph);
           float4* raw = reinterpret_cast<float4*>(halo_raw(hs));
-          if constexpr (BF) {
-            // raw [4 groups of 4 ch][pos][4 floats] -> planes [2 kg of 8 ch][pos][8 bf16]
-            const int hp = a.halo_pos;
-            uint4* p0 = reinterpret_cast<uint4*>(plane(hs, 0));
-            uint4* p1 = reinterpret_cast<uint4*>(plane(hs, 1));
-            uint4* p2 = reinterpret_cast<uint4*>(plane(hs, 2));
-            for (int i = tid; i < 2 * hp; i += 128) {
-              const int k = i / hp, p = i - k * hp;
-              const float4 u = raw[(2 * k) * hp + p];
-              const float4 v = raw[(2 * k + 1) * hp + p];
-              const float vv[8] = {u.x, u.y, u.z, u.w, v.x, v.y, v.z, v.w};
-              uint4 q0, q1, q2;
-              split3_bf16(vv, q0, q1, q2);
-              p0[i] = q0;
-              p1[i] = q1;
-              p2[i] = q2;
-            }
-          } else {
-            float4* lo = reinterpret_cast<float4*>(halo_lo(hs));
-            for (int i = tid; i < n16; i += 128) {
-              const float4 v = raw[i];
-              float4 l;
-              l.x = v.x - trunc_tf32(v.x); l.y = v.y - trunc_tf32(v.y);
-              l.z = v.z - trunc_tf32(v.z); l.w = v.w - trunc_tf32(v.w);
-              lo[i] = l;
-            }
+          float4* lo = reinterpret_cast<float4*>(halo_lo(hs));
+          for (int i = tid; i < n16; i += 128) {
+            const float4 v = raw[i];
+            float4 l;
+            l.x = v.x - trunc_tf32(v.x); l.y = v.y - trunc_tf32(v.y);
+            l.z = v.z - trunc_tf32(v.z); l.w = v.w - trunc_tf32(v.w);
+            lo[i] = l;
           }
           fence_proxy_async_smem();
           mbar_arrive(&halo_conv[hs]);
@@ -421,19 +479,29 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
       }
     }
-  } else {
+  } else if (warp < 14) {
     // ===================== epilogue =====================
-    // D row r: r < 64 -> W_hi products for co = r, r >= 64 -> W_lo products for co = r - 64.
-    // The warp pair holding the hi and lo rows of the same 32 channels swaps half of each
-    // 16-position chunk through shared memory; each warp then finishes 8 positions
-    // (hi + lo, fused epilogue) and stores 32 consecutive channels of a position per
-    // instruction (coalesced NHWC).
+    // Two groups of 4 warps; group g finishes tile s = g of every unit (both tiles of a
+    // unit drain in parallel).  D row r: r < 64 -> W_hi (W0) products for co = r, r >= 64 ->
+    // W_lo (W1) products for co = r - 64.  The warp pair holding the hi and lo rows of the
+    // same 32 channels swaps half of each 64-position batch through shared memory; each
+    // warp then finishes 32 positions (hi + lo, fused epilogue) and stores 32 consecutive
+    // channels of a position per instruction (coalesced NHWC).  Frame position -> NHWC
+    // offset comes from a per-tile table (one LDS broadcast per position).
     const int q = warp & 3;                 // TMEM lane quadrant this warp may access
+    const int grp = (warp - 6) >> 2;        // tile of the unit this warp drains
     const bool hi_warp = q < 2;
     const int co_l = (q & 1) * 32 + lane;   // output channel of this lane within the co block
+    const int gtid = (int)threadIdx.x - 192 - grp * 128;
     constexpr bool kBias = EPI == EPI_BIAS || EPI == EPI_BIAS_TANH || EPI == EPI_RESID;
+    constexpr bool kAux = EPI == EPI_RESID || EPI == EPI_TANH_BWD || EPI == EPI_ADD;
     const int own0 = hi_warp ? 0 : 32;      // positions [own0, own0 + 32) of each 64-batch are ours
-    int ab = 0, xb = 0;
+    float* mine = xchg + ((grp * 2 + (q & 1)) * 2 + (hi_warp ? 0 : 1)) * 32 * 32;
+    const float* theirs = xchg + ((grp * 2 + (q & 1)) * 2 + (hi_warp ? 1 : 0)) * 32 * 32;
+    int* tab = pos_tab + grp * 128;
+    const uint32_t pair_bar = 2 + grp * 2 + (q & 1);   // this warp and its partner (64 threads)
+    const uint32_t grp_bar = 6 + grp;                  // the group (128 threads)
+    int ab = 0;
     uint32_t aph = 0;
     UnitIter it(a.Co / 64, a.N, a.T);
     int cb, n, tile0, ntiles, ui = 0;
@@ -445,14 +513,22 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_wait(&acc_full[ab], aph);
       tc_fence_after();
       if (a.trace && blockIdx.x < 2 && threadIdx.x == 192) a.trace[(blockIdx.x * 64 + min(u, 63)) * 8 + 2] = globaltimer_ns();
-      for (int s = 0; s < ntiles; ++s) {
-        const uint32_t tcol = tmem_base + ((uint32_t)(q * 32) << 16) + (uint32_t)((ab * kS + s) * 128);
+      if (grp < ntiles) {
+        {
+          const int f = (tile0 + grp) * 128 + gtid;
+          const int y = f / Wp, X = f - y * Wp;
+          asm volatile("bar.sync %0, 128;" ::"r"(grp_bar) : "memory");   // last tile's readers are done
+          tab[gtid] = (y < a.H && X >= 1 && X <= a.W) ? (y * a.W + (X - 1)) * a.Co : -1;
+          asm volatile("bar.sync %0, 128;" ::"r"(grp_bar) : "memory");
+        }
+        const uint32_t tcol = tmem_base + ((uint32_t)(q * 32) << 16) + (uint32_t)((ab * kS + grp) * 128);
+        const float* auxb = kAux ? a.aux + img * a.Co + co : nullptr;
+        float* outb = a.out + img * a.Co + co;
+        const bool planes = a.p0 != nullptr;
+        __nv_bfloat16* p0b = planes ? a.p0 + img * a.Co + co : nullptr;
+        __nv_bfloat16* p1b = planes ? a.p1 + img * a.Co + co : nullptr;
         for (int p0 = 0; p0 < 128; p0 += 64) {
-          constexpr bool kAux = EPI == EPI_RESID || EPI == EPI_TANH_BWD || EPI == EPI_ADD;
-          float* mine = xchg + ((xb * 2 + (q & 1)) * 2 + (hi_warp ? 0 : 1)) * 32 * 32;
-          float* theirs = xchg + ((xb * 2 + (q & 1)) * 2 + (hi_warp ? 1 : 0)) * 32 * 32;
-          // 1) the 32 columns the partner warp finishes: TMEM -> smem
-          {
+          {   // the 32 columns the partner warp finishes: TMEM -> smem
             uint32_t rr[32];
             const uint32_t c_give = tcol + (uint32_t)p0 + (hi_warp ? 32u : 0u);
             tmem_ld16(c_give, *reinterpret_cast<uint32_t(*)[16]>(&rr[0]));
@@ -461,45 +537,29 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
             for (int e = 0; e < 32; ++e) mine[e * 32 + lane] = __uint_as_float(rr[e]);
           }
-          // 3) our own 32 columns
-          uint32_t r[32];
+          uint32_t r[32];   // our own 32 columns
           {
             const uint32_t c_own = tcol + (uint32_t)p0 + (uint32_t)own0;
             tmem_ld16(c_own, *reinterpret_cast<uint32_t(*)[16]>(&r[0]));
             tmem_ld16(c_own + 16, *reinterpret_cast<uint32_t(*)[16]>(&r[16]));
             tmem_wait_ld();
           }
-          asm volatile("bar.sync 2, 128;" ::: "memory");
-          // positions own0 .. own0+31 of this batch, 16 at a time: the aux operand (skip /
-          // tape / cotangent input) of all 16 is loaded before any is used, so the
-          // epilogue pays two memory latencies per 64 positions instead of four.
-          // NHWC offsets are 32-bit relative to the image (H W Co < 2^31).
-          const float* auxb = kAux ? a.aux + img * a.Co + co : nullptr;
-          float* outb = a.out + img * a.Co + co;
-          const bool planes = a.p0 != nullptr;
-          __nv_bfloat16* p0b = planes ? a.p0 + img * a.Co + co : nullptr;
-          __nv_bfloat16* p1b = planes ? a.p1 + img * a.Co + co : nullptr;
-          const int f = (tile0 + s) * 128 + p0 + own0;
-          int y = f / Wp, X = f - (f / Wp) * Wp;
+          asm volatile("bar.sync %0, 64;" ::"r"(pair_bar) : "memory");
+          const int* tb = tab + p0 + own0;
 #pragma unroll
-          for (int h16 = 0; h16 < 32; h16 += 16) {
-            int off[16];
-            bool ok[16];
-            float ax[16];
+          for (int h8 = 0; h8 < 32; h8 += 8) {
+            int off[8];
+            float ax[8];
 #pragma unroll
-            for (int e = 0; e < 16; ++e) {
-              ok[e] = y < a.H && X >= 1 && X <= a.W;
-              off[e] = ok[e] ? (y * a.W + (X - 1)) * a.Co : 0;
-              if (++X == Wp) X = 0, ++y;
-            }
+            for (int e = 0; e < 8; ++e) off[e] = tb[h8 + e];
             if constexpr (kAux) {
 #pragma unroll
-              for (int e = 0; e < 16; ++e) ax[e] = auxb[off[e]];
+              for (int e = 0; e < 8; ++e) ax[e] = off[e] >= 0 ? auxb[off[e]] : 0.f;
             }
 #pragma unroll
-            for (int e = 0; e < 16; ++e) {
-              if (!ok[e]) continue;                           // warp-uniform
-              const float v = __uint_as_float(r[h16 + e]) + theirs[(h16 + e) * 32 + lane];
+            for (int e = 0; e < 8; ++e) {
+              if (off[e] < 0) continue;                       // warp-uniform
+              const float v = __uint_as_float(r[h8 + e]) + theirs[(h8 + e) * 32 + lane];
               float o;
               if constexpr (EPI == EPI_BIAS) o = v + bias;
               else if constexpr (EPI == EPI_BIAS_TANH) o = tanhf(v + bias);
@@ -515,7 +575,7 @@ __global__ void __launch_bounds__(kThreads, 1)
               }
             }
           }
-          xb ^= 1;
+          asm volatile("bar.sync %0, 64;" ::"r"(pair_bar) : "memory");   // partner done with `mine`
         }
       }
       if (a.trace && blockIdx.x < 2 && threadIdx.x == 192) a.trace[(blockIdx.x * 64 + min(u, 63)) * 8 + 3] = globaltimer_ns();
@@ -612,6 +672,21 @@ EncodeTiledFn encode_fn() {
   return fn;
 }
 
+// X3BF16 raw halo: plain NHWC box {16 ch, W + 2, rows, 1} (64-byte rows), zero fill
+// outside the image
+CUtensorMap make_raw_map(const float* in, const ConvShape& s, int Wp, int rows_h) {
+  CUtensorMap m;
+  const cuuint64_t dims[4] = {(cuuint64_t)s.ci, (cuuint64_t)s.w, (cuuint64_t)s.h, (cuuint64_t)s.n};
+  const cuuint64_t strides[3] = {(cuuint64_t)s.ci * 4, (cuuint64_t)s.w * s.ci * 4, (cuuint64_t)s.h * s.w * s.ci * 4};
+  const cuuint32_t box[4] = {(cuuint32_t)kChunk, (cuuint32_t)Wp, (cuuint32_t)rows_h, 1};
+  const cuuint32_t estr[4] = {1, 1, 1, 1};
+  CUresult r = encode_fn()(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, const_cast<float*>(in), dims, strides, box, estr,
+                           CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                           CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) fail(RP_ERR_CUDA, "cuTensorMapEncodeTiled failed (" + std::to_string((int)r) + ")");
+  return m;
+}
+
 CUtensorMap make_halo_map(const float* in, const ConvShape& s, int Wp, int rows_h) {
   CUtensorMap m;
   const cuuint64_t dims[5] = {4, (cuuint64_t)s.w, (cuuint64_t)s.h, (cuuint64_t)(s.ci / 4), (cuuint64_t)s.n};
@@ -629,7 +704,8 @@ CUtensorMap make_halo_map(const float* in, const ConvShape& s, int Wp, int rows_
 struct Plan {
   bool ok = false;
   int Wp, rows_h, halo_pos, T, units_per_img;
-  uint32_t halo_bytes, w_tap, halo_stride, plane_bytes;
+  uint32_t halo_bytes, w_tap, halo_stride, plane_bytes, raw_stride = 0;
+  int raw_slots = 0;
   size_t smem;
 };
 
@@ -644,28 +720,33 @@ Plan plan_for(const ConvShape& s, int mode = MODE_X3TF32) {
   p.units_per_img = (p.T + kS - 1) / kS;
   p.halo_bytes = (uint32_t)p.halo_pos * 64u;
   p.plane_bytes = (uint32_t)p.halo_pos * 32u;
+  const size_t fixed_bytes = 2 * 2 * 2 * 32 * 32 * 4 + 256 + 1024 + 1024;   // xchg + barriers + table + alignment
   if (mode == MODE_X3BF16) {
     p.w_tap = 128u * kChunk * 2u;
-    p.halo_stride = (128 + p.halo_bytes + 128 + 3 * (p.plane_bytes + 128) + 1023) / 1024 * 1024;
+    p.halo_stride = (128 + 3 * (p.plane_bytes + 128) + 1023) / 1024 * 1024;   // plane slot
+    p.raw_stride = (p.halo_bytes + 1023) / 1024 * 1024;
+    const size_t base = 2 * (size_t)p.halo_stride + kWStages * 3 * (size_t)p.w_tap + fixed_bytes;
+    p.raw_slots = base + 3 * (size_t)p.raw_stride <= (size_t)kMaxSmem ? 3 : 2;
+    p.smem = base + p.raw_slots * (size_t)p.raw_stride;
   } else {
     p.w_tap = 128u * kChunk * 4u;
     p.halo_stride = (128 + p.halo_bytes + 128 + p.halo_bytes + 128 + 1023) / 1024 * 1024;
+    p.smem = 2 * (size_t)p.halo_stride + kWStages * 3 * (size_t)p.w_tap + fixed_bytes;
   }
-  p.smem = 2 * (size_t)p.halo_stride + kWStages * 3 * (size_t)p.w_tap + 2 * 2 * 2 * 32 * 32 * 4 + 256 + 1024;
   p.ok = p.smem <= (size_t)kMaxSmem;
   return p;
 }
 
 std::mutex g_map_mu;
-std::map<std::tuple<const void*, int, int, int, int, int>, CUtensorMap> g_maps;
+std::map<std::tuple<const void*, int, int, int, int, int, bool>, CUtensorMap> g_maps;
 
-const CUtensorMap& cached_map(const float* in, const ConvShape& s, int Wp, int rows_h) {
+const CUtensorMap& cached_map(const float* in, const ConvShape& s, int Wp, int rows_h, bool raw) {
   std::lock_guard<std::mutex> lk(g_map_mu);
-  auto key = std::make_tuple((const void*)in, s.n, s.h, s.w, s.ci, rows_h);
+  auto key = std::make_tuple((const void*)in, s.n, s.h, s.w, s.ci, rows_h, raw);
   auto it = g_maps.find(key);
   if (it == g_maps.end()) {
     if (g_maps.size() > 4096) g_maps.clear();
-    it = g_maps.emplace(key, make_halo_map(in, s, Wp, rows_h)).first;
+    it = g_maps.emplace(key, raw ? make_raw_map(in, s, Wp, rows_h) : make_halo_map(in, s, Wp, rows_h)).first;
   }
   return it->second;
 }
@@ -735,6 +816,8 @@ void conv3x3_fwd_tc(const ConvShape& s, const float* in, const float* w_hwio, bo
   a.halo_stride = p.halo_stride;
   a.w_tap = p.w_tap;
   a.plane_bytes = p.plane_bytes;
+  a.raw_stride = p.raw_stride;
+  a.raw_slots = p.raw_slots;
   a.h = h;
   a.w = wp;
   a.bias = bias;
@@ -743,7 +826,7 @@ void conv3x3_fwd_tc(const ConvShape& s, const float* in, const float* w_hwio, bo
   a.p0 = static_cast<__nv_bfloat16*>(out_planes);
   a.p1 = out_planes ? a.p0 + s.pixels() * s.co : nullptr;
   a.trace = g_trace;
-  const CUtensorMap& m = cached_map(in, s, p.Wp, p.rows_h);
+  const CUtensorMap& m = cached_map(in, s, p.Wp, p.rows_h, mode == MODE_X3BF16);
   const int grid = std::min(a.num_tiles, kNumSMs);
   switch (epi) {
     case EPI_BIAS: launch_epi<EPI_BIAS>(m, a, mode, p.smem, grid, st); break;

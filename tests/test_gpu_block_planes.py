@@ -1,0 +1,113 @@
+"""GPU: the plane-pair residual block (rp_op_block_fwd_planes / rp_op_block_bwd_planes) that
+the fp32 trainer runs on tcgen05 shapes, against the fp64 oracle block (block_forward /
+block_vjp, network.cpp:82-106) and against the fp32-operand block path.
+
+The forward convs are the same kernel as rp_op_block_fwd, so a and x_next must match it bit
+for bit; the planes must reconstruct them to bf16-pair precision (|v - p0 - p1| <= 2^-16 |v|).
+The weight gradients differ from the fp32-operand path only by the plane split (~1e-5)."""
+import ctypes as C
+
+import numpy as np
+import pytest
+
+import paper_2009_01462_b200 as rp
+from paper_2009_01462_b200._lib import lib, rp_geometry
+from oracle import respar_oracle as O
+
+pytestmark = pytest.mark.gpu
+torch = pytest.importorskip("torch")
+
+GW_TOL = 5e-5    # weight / bias gradients, relative to the tensor's max |value|
+FWD_TOL = 2e-5   # a, x_next, input cotangent (3xBF16 convs)
+
+
+def _p(t):
+    return C.c_void_p(t.data_ptr())
+
+
+def _planes_to_f64(t, n):
+    b = t.view(torch.bfloat16).float().cpu().numpy().astype(np.float64)
+    return b[:n] + b[n:2 * n]
+
+
+def _rel(got, want):
+    return np.abs(got - want).max() / max(np.abs(want).max(), 1e-30)
+
+
+@pytest.mark.parametrize("n,hw,c,ch", [(4, 16, 64, 64), (2, 32, 64, 128), (3, 8, 128, 64)])
+def test_block_planes(n, hw, c, ch):
+    og = O.Geometry(in_channels=3, height=hw, width=hw, channels=c, hidden=ch, blocks=1, classes=10,
+                    activation=O.TANH, step_h=0.5)
+    net = O.make_net(og, O.Rng(11))
+    net.b1[0][...] = O.rng_uniform(O.Rng(12), ch, -0.1, 0.1)
+    net.b2[0][...] = O.rng_uniform(O.Rng(13), c, -0.1, 0.1)
+    flat = net.flat().astype(np.float32)
+    net32 = net.astype(np.float32).astype(np.float64)
+    geo = rp_geometry(3, hw, hw, c, ch, 1, 10, 0, 0.5)
+    assert lib().rp_op_block_planes_supported(C.byref(geo), n, rp.MATH["fp32"]) == 1
+    assert lib().rp_op_block_planes_supported(C.byref(geo), n, rp.MATH["bf16"]) == 0
+
+    rng = np.random.default_rng(5)
+    x = rng.uniform(-1, 1, (n, hw, hw, c)).astype(np.float32)
+    up = rng.uniform(-1, 1, (n, hw, hw, c)).astype(np.float32)
+    dev = torch.device("cuda")
+    tx, tup, tp = (torch.from_numpy(v).to(dev) for v in (x, up, flat))
+    off = lib().rp_param_offset_block(C.byref(geo), 0)
+    pb = C.c_void_p(tp.data_ptr() + 4 * off)
+    wsb = lib().rp_op_workspace_bytes(C.byref(geo), n, rp.MATH["fp32"])
+    ws = torch.empty(wsb, dtype=torch.uint8, device=dev)
+    ne, nh = n * hw * hw * c, n * hw * hw * ch
+
+    # fp32-operand reference path
+    a_ref = torch.empty(nh, device=dev)
+    xn_ref = torch.empty(ne, device=dev)
+    rp.check(lib().rp_op_block_fwd(C.byref(geo), n, _p(tx), pb, _p(a_ref), _p(xn_ref), rp.MATH["fp32"], _p(ws), wsb,
+                                   None))
+    # plane path
+    a = torch.empty(nh, device=dev)
+    xn = torch.empty(ne, device=dev)
+    a_p = torch.empty(2 * nh, dtype=torch.int16, device=dev)
+    xn_p = torch.empty(2 * ne, dtype=torch.int16, device=dev)
+    rp.check(lib().rp_op_block_fwd_planes(C.byref(geo), n, _p(tx), pb, _p(a), _p(xn), _p(a_p), _p(xn_p), _p(ws), wsb,
+                                          None))
+    torch.cuda.synchronize()
+    assert torch.equal(a, a_ref) and torch.equal(xn, xn_ref)
+    a64, xn64 = a.cpu().numpy().astype(np.float64), xn.cpu().numpy().astype(np.float64)
+    assert np.all(np.abs(_planes_to_f64(a_p, nh) - a64) <= 2.0 ** -16 * np.abs(a64))
+    assert np.all(np.abs(_planes_to_f64(xn_p, ne) - xn64) <= 2.0 ** -16 * np.abs(xn64))
+    want_xn, cache = O.block_forward(net32, 0, x.astype(np.float64))
+    assert _rel(xn64.reshape(want_xn.shape), want_xn) < FWD_TOL
+
+    # backward: plane path vs oracle and vs fp32-operand path
+    x_p = torch.empty(2 * ne, dtype=torch.int16, device=dev)
+    rp.check(lib().rp_op_split_planes(_p(tx), ne, _p(x_p), C.c_void_p(x_p.data_ptr() + 2 * ne), None))
+    g_io = tup.clone().reshape(-1)
+    g_p = torch.empty(2 * ne, dtype=torch.int16, device=dev)
+    rp.check(lib().rp_op_split_planes(_p(g_io), ne, _p(g_p), C.c_void_p(g_p.data_ptr() + 2 * ne), None))
+    dpre = torch.empty(nh, device=dev)
+    dpre_p = torch.empty(2 * nh, dtype=torch.int16, device=dev)
+    gb = torch.zeros_like(tp)
+    gbp = C.c_void_p(gb.data_ptr() + 4 * off)
+    rp.check(lib().rp_op_block_bwd_planes(C.byref(geo), n, _p(x_p), _p(a), _p(a_p), pb, _p(g_io), _p(g_p), _p(dpre),
+                                          _p(dpre_p), gbp, _p(ws), wsb, None))
+    g_ref = tup.clone().reshape(-1)
+    gb_ref = torch.zeros_like(tp)
+    rp.check(lib().rp_op_block_bwd(C.byref(geo), n, _p(tx), _p(a_ref), pb, _p(g_ref), _p(dpre),
+                                   C.c_void_p(gb_ref.data_ptr() + 4 * off), rp.MATH["fp32"], _p(ws), wsb, None))
+    torch.cuda.synchronize()
+    assert torch.equal(g_io, g_ref)        # dgrads: same kernels, same inputs
+    g64 = g_io.cpu().numpy().astype(np.float64)
+    assert np.all(np.abs(_planes_to_f64(g_p, ne) - g64) <= 2.0 ** -16 * np.abs(g64))
+
+    p_prev, (gw1, gb1, gw2, gb2) = O.block_vjp(net32, 0, O.BlockCache(x.astype(np.float64), a64.reshape(
+        n, hw, hw, ch)), up.astype(np.float64))
+    assert _rel(g64.reshape(p_prev.shape), p_prev) < FWD_TOL
+    got = O.zero_net(og)
+    got.load_flat(gb.cpu().numpy().astype(np.float64))
+    ref = O.zero_net(og)
+    ref.load_flat(gb_ref.cpu().numpy().astype(np.float64))
+    for name, want in (("w1", gw1), ("b1", gb1), ("w2", gw2), ("b2", gb2)):
+        gv = np.asarray(getattr(got, name)[0])
+        rv = np.asarray(getattr(ref, name)[0])
+        assert _rel(gv, want) < GW_TOL, name
+        assert _rel(gv, rv) < GW_TOL, name
