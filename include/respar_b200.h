@@ -181,16 +181,17 @@ int rp_op_block_fwd(const rp_geometry* g, int32_t nrows, const float* x, const f
 int rp_op_block_bwd(const rp_geometry* g, int32_t nrows, const float* x, const float* a, const float* pb,
                     float* g_io, float* dpre, float* gb, int32_t math, void* ws, int64_t ws_bytes,
                     void* stream);
-/* Plane-pair block path (RP_MATH_FP32 only): the convs also write the bf16 plane pair
- * (v = p0 + p1, each a [2][elements] bf16 buffer: p0 then p1) of a, x_next, dpre and the
- * updated cotangent, and both weight gradients run on rp_op_conv3x3_wgrad_planes.  Same
- * arithmetic contract as rp_op_block_fwd / _bwd (~1e-5 relative on the weight gradient).
+/* Plane-pair block path (RP_MATH_FP32 only): every conv reads its input as a bf16 plane
+ * pair (v = p0 + p1, each a [2][elements] bf16 buffer: p0 then p1) and writes the plane
+ * pair of its output (a, x_next, dpre, the updated cotangent) next to the fp32 tensor; both
+ * weight gradients run on rp_op_conv3x3_wgrad_planes.  ~1e-5 relative (2^-17 operand
+ * splits) where rp_op_block_fwd / _bwd are ~4e-6.
  * x_next_planes may be NULL (a stage's last block).  Backward reads g_planes as the planes
  * of g_io on entry and leaves the planes of the new g_io there. */
 int32_t rp_op_block_planes_supported(const rp_geometry* g, int32_t nrows, int32_t math);
-int rp_op_block_fwd_planes(const rp_geometry* g, int32_t nrows, const float* x, const float* pb, float* a,
-                           float* x_next, void* a_planes, void* x_next_planes, void* ws, int64_t ws_bytes,
-                           void* stream);
+int rp_op_block_fwd_planes(const rp_geometry* g, int32_t nrows, const float* x, const void* x_planes,
+                           const float* pb, float* a, float* x_next, void* a_planes, void* x_next_planes, void* ws,
+                           int64_t ws_bytes, void* stream);
 int rp_op_block_bwd_planes(const rp_geometry* g, int32_t nrows, const void* x_planes, const float* a,
                            const void* a_planes, const float* pb, float* g_io, void* g_planes, float* dpre,
                            void* dpre_planes, float* gb, void* ws, int64_t ws_bytes, void* stream);

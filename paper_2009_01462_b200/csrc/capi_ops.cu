@@ -124,11 +124,11 @@ int64_t op_workspace_bytes(const rp_geometry& g, int nrows) {
 // dgrad: `w` is the forward conv's HWIO weight; the conv runs on the cotangent.
 void conv(const k::ConvShape& s, const float* in, const float* w, bool dgrad, const float* bias, const float* aux,
           float h, int epi, float* out, int math, void* wws, int prof_cls, bool aux_read, cudaStream_t st,
-          void* out_planes = nullptr) {
+          void* out_planes = nullptr, const void* in_planes = nullptr) {
   prof::Scope ps(prof_cls, st, conv_flops(s), conv_bytes(s, aux_read) + (out_planes ? 4.0 * s.pixels() * s.co : 0.0));
-  if (out_planes) {   // only the fp32 tcgen05 kernel writes plane pairs (planes_path() checked the shape)
-    if (math != RP_MATH_FP32 || !k::conv3x3_tc_supported(s)) fail(RP_ERR_INTERNAL, "conv: plane output needs fp32 tcgen05");
-    k::conv3x3_fwd_tc(s, in, w, dgrad, bias, aux, h, epi, out, fp32_split(), wws, st, out_planes);
+  if (out_planes || in_planes) {   // only the fp32 tcgen05 kernel reads / writes plane pairs (planes_path())
+    if (math != RP_MATH_FP32 || !k::conv3x3_tc_supported(s)) fail(RP_ERR_INTERNAL, "conv: plane i/o needs fp32 tcgen05");
+    k::conv3x3_fwd_tc(s, in, w, dgrad, bias, aux, h, epi, out, fp32_split(), wws, st, out_planes, in_planes);
     return;
   }
   // RP_MATH_BF16: bf16 operands where the bf16 kernel tiles the shape (Co % 128, Ci % 32),
@@ -187,16 +187,16 @@ void block_bwd(const rp_geometry& g, int nrows, const float* x, const float* a, 
 }
 
 // Plane-pair variants: a_p / x_next_p / x_p / g_p / dpre_p are bf16 [2][elements] pairs.
-void block_fwd_planes(const rp_geometry& g, int nrows, const float* x, const float* pb, float* a, float* x_next,
-                      void* a_p, void* x_next_p, void* ws, int64_t ws_bytes, cudaStream_t st) {
+void block_fwd_planes(const rp_geometry& g, int nrows, const float* x, const void* x_p, const float* pb, float* a,
+                      float* x_next, void* a_p, void* x_next_p, void* ws, int64_t ws_bytes, cudaStream_t st) {
   const ParamLayout L = ParamLayout::of(g);
   const bool tanh_act = g.activation == RP_ACT_TANH;
   if (ws_bytes < weight_ws_bytes(g)) fail(RP_ERR_RANGE, "block_fwd: workspace too small");
   const k::ConvShape s1 = shape(g, nrows, g.channels, g.hidden), s2 = shape(g, nrows, g.hidden, g.channels);
   conv(s1, x, pb + L.w1, false, pb + L.b1, nullptr, 1.f, tanh_act ? k::EPI_BIAS_TANH : k::EPI_BIAS, a, RP_MATH_FP32,
-       ws, RP_PROF_CONV_FPROP, false, st, a_p);
+       ws, RP_PROF_CONV_FPROP, false, st, a_p, x_p);
   conv(s2, a, pb + L.w2, false, pb + L.b2, x, (float)g.step_h, k::EPI_RESID, x_next, RP_MATH_FP32, ws,
-       RP_PROF_CONV_FPROP, true, st, x_next_p);
+       RP_PROF_CONV_FPROP, true, st, x_next_p, a_p);
 }
 
 void wgrad_planes(const k::ConvShape& s, const void* xp, const void* gp, float scale, float* gw, float* gb, void* ws,
@@ -220,14 +220,14 @@ void block_bwd_planes(const rp_geometry& g, int nrows, const void* x_p, const fl
   void* wgws = cv.take<char>(wg_bytes);
   // dpre = h (g * W2^T) (1 - a^2), and its planes                (network.cpp:100-101)
   conv(shape(g, nrows, C, Ch), gio, pb + L.w2, true, nullptr, a, h, tanh_act ? k::EPI_TANH_BWD : k::EPI_SCALE, dpre,
-       RP_MATH_FP32, wws, RP_PROF_CONV_DGRAD, tanh_act, st, dpre_p);
+       RP_MATH_FP32, wws, RP_PROF_CONV_DGRAD, tanh_act, st, dpre_p, g_p);
   // gW2 = h a^T g, gb2 = h sum g                                  (network.cpp:98-99)
   wgrad_planes(shape(g, nrows, Ch, C), a_p, g_p, h, gb + L.w2, gb + L.b2, wgws, st);
   // gW1 = x^T dpre, gb1 = sum dpre                                (network.cpp:102-103)
   wgrad_planes(shape(g, nrows, C, Ch), x_p, dpre_p, 1.f, gb + L.w1, gb + L.b1, wgws, st);
   // g <- g + dpre * W1^T in place, and the planes of the new g   (network.cpp:104)
   conv(shape(g, nrows, Ch, C), dpre, pb + L.w1, true, nullptr, gio, 1.f, k::EPI_ADD, gio, RP_MATH_FP32, wws,
-       RP_PROF_CONV_DGRAD, true, st, g_p);
+       RP_PROF_CONV_DGRAD, true, st, g_p, dpre_p);
 }
 
 void stem_fwd(const rp_geometry& g, int nrows, const float* xr, const float* ps, float* x0, cudaStream_t st) {
@@ -458,18 +458,19 @@ int32_t rp_op_block_planes_supported(const rp_geometry* g, int32_t nrows, int32_
   return planes_path(*g, nrows, math) ? 1 : 0;
 }
 
-int rp_op_block_fwd_planes(const rp_geometry* g, int32_t nrows, const float* x, const float* pb, float* a,
-                           float* x_next, void* a_planes, void* x_next_planes, void* ws, int64_t ws_bytes,
-                           void* stream) {
+int rp_op_block_fwd_planes(const rp_geometry* g, int32_t nrows, const float* x, const void* x_planes,
+                           const float* pb, float* a, float* x_next, void* a_planes, void* x_next_planes, void* ws,
+                           int64_t ws_bytes, void* stream) {
   return guard([&] {
     need(g, "geometry");
     if (!planes_path(*g, nrows, RP_MATH_FP32)) fail(RP_ERR_SHAPE, "block_fwd_planes: geometry not on the plane path");
     need(x, "x");
+    need(x_planes, "x_planes");
     need(pb, "pb");
     need(a, "a");
     need(x_next, "x_next");
     need(a_planes, "a_planes");
-    block_fwd_planes(*g, nrows, x, pb, a, x_next, a_planes, x_next_planes, ws, ws_bytes, S(stream));
+    block_fwd_planes(*g, nrows, x, x_planes, pb, a, x_next, a_planes, x_next_planes, ws, ws_bytes, S(stream));
   });
 }
 

@@ -440,9 +440,9 @@ void DecoupledTrainer::run_forward(Stage& st, const float* input, int nrows, flo
     for (int i = 0; i < n; ++i) {
       const int l = st.begin + i;
       float* out = i == n - 1 ? out_features : st.xs[i + 1].get();
-      check(rp_op_block_fwd_planes(&geo_, nrows, cur, P + L.block0 + (int64_t)l * L.block_stride, st.as[i].get(), out,
-                                   st.aps[i].get(), i == n - 1 ? nullptr : st.xps[i + 1].get(), st.ws.get(),
-                                   st.ws.bytes(), s));
+      check(rp_op_block_fwd_planes(&geo_, nrows, cur, st.xps[i].get(), P + L.block0 + (int64_t)l * L.block_stride,
+                                   st.as[i].get(), out, st.aps[i].get(), i == n - 1 ? nullptr : st.xps[i + 1].get(),
+                                   st.ws.get(), st.ws.bytes(), s));
       cur = out;
     }
     if (st.index == stages() - 1)

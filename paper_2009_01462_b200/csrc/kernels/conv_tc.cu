@@ -51,7 +51,11 @@ using namespace rp::umma;
 constexpr int kThreads = 480;       // w0 halo TMA, w1 MMA, w2-5 converters, w6-13 epilogue, w14 weight TMA
 constexpr int kWStages = 3;          // one weight stage = one filter row (3 taps) of one chunk
 constexpr int kChunk = 16;           // input channels per halo chunk
-constexpr bool kUseCollector = false;  // A-operand collector reuse (measured: no gain here)
+constexpr bool kUseCollector = false;  // A-operand collector reuse, tf32 modes (measured: no gain)
+#ifndef RP_CONV_COLLECTOR_BF
+#define RP_CONV_COLLECTOR_BF 1
+#endif
+constexpr bool kUseCollectorBF = RP_CONV_COLLECTOR_BF;   // X3BF16: A reuse across the 6 MMAs of a tap
 constexpr int kS = 2;                // 128-position tiles per unit
 constexpr int kMaxSmem = 220 * 1024;
 
@@ -59,7 +63,10 @@ constexpr int kMaxSmem = 220 * 1024;
 // X3BF16 (the default fp32-accurate path, capi_ops.cu fp32_split) ([W0; W1] x {x0, x1, x2} with bf16 splits: W to
 // 16 significant bits, x to 24; products W0x0 .. W1x2 cover everything above 2^-18 of |W x|,
 // in 3 MMAs of K = 16 per 16 channels instead of 4 of K = 8).
-enum { MODE_TF32 = 0, MODE_X3TF32 = 1, MODE_X3BF16 = 2 };
+// MODE_PLANES: the input arrives as a bf16 plane pair (x = x0 + x1, written by the
+// producing conv's epilogue): TMA loads both planes straight into the MMA layout (no
+// converters) and [W0; W1] x {x0, x1} is 2 MMAs per 16 channels (~2^-17 relative).
+enum { MODE_TF32 = 0, MODE_X3TF32 = 1, MODE_X3BF16 = 2, MODE_PLANES = 3 };
 
 struct TcArgs {
   int N, H, W, Ci, Co, Wp, rows_h, T, num_tiles, halo_pos, nchunks;
@@ -68,7 +75,7 @@ struct TcArgs {
   uint32_t w_tap;       // bytes of one tap's A operand (128 rows x 16 channels x 4 B; bf16: x 2 B)
   uint32_t plane_bytes; // X3BF16: one bf16 plane of the halo chunk (halo_pos x 32 B)
   uint32_t raw_stride;  // X3BF16: bytes per raw fp32 halo slot ([pos][16 ch], TMA target)
-  int raw_slots;        // X3BF16: depth of the raw ring (2 or 3)
+  int raw_slots;        // X3BF16: depth of the raw ring (2 or 3); PLANES: halo slots (2..4)
   float h;
   const float* w;       // prepped [chunk][tap][kg][128 rows][4]
   const float* bias;
@@ -196,37 +203,45 @@ __global__ void __launch_bounds__(kThreads, 1)
   // ---- shared memory carve-up
   const uint32_t w_stage = 3 * a.w_tap;
   constexpr bool BF = MODE == MODE_X3BF16;
-  // X3BF16: [2 plane slots][raw_slots raw slots][weights]...; else [2 halo slots][weights]...
-  uint8_t* halo_base = smem;                                  // 2 slots
+  constexpr bool PL = MODE == MODE_PLANES;
+  constexpr bool BFL = BF || PL;                              // bf16 plane layout in the halo slots
+  // X3BF16: [2 plane slots][raw_slots raw slots][weights]...; PLANES: [raw_slots plane
+  // slots][weights]...; else [2 halo slots][weights]...
+  const int hslots = PL ? a.raw_slots : 2;
+  uint8_t* halo_base = smem;
   uint8_t* raw_base = smem + 2 * a.halo_stride;               // X3BF16 only
-  uint8_t* w_base = smem + 2 * a.halo_stride + (BF ? a.raw_slots * a.raw_stride : 0u);   // kWStages stages
+  uint8_t* w_base = smem + hslots * a.halo_stride + (BF ? a.raw_slots * a.raw_stride : 0u);   // kWStages stages
   float* xchg = reinterpret_cast<float*>(w_base + kWStages * w_stage);   // [2 groups][2 pairs][2 sides][32][32]
   uint64_t* bars = reinterpret_cast<uint64_t*>(xchg + 2 * 2 * 2 * 32 * 32);
-  uint64_t* halo_full = bars;        // [2]
-  uint64_t* halo_conv = bars + 2;    // [2]
-  uint64_t* halo_empty = bars + 4;   // [2]
-  uint64_t* w_full = bars + 6;       // [kWStages]
-  uint64_t* w_empty = bars + 6 + kWStages;
-  uint64_t* acc_full = bars + 6 + 2 * kWStages;   // [2]
-  uint64_t* acc_empty = bars + 8 + 2 * kWStages;  // [2]
-  uint64_t* raw_full = bars + 10 + 2 * kWStages;  // [3] X3BF16: TMA -> converters
-  uint64_t* raw_empty = bars + 13 + 2 * kWStages; // [3] X3BF16: converters -> TMA
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 16 + 2 * kWStages);
+  uint64_t* halo_full = bars;        // [4]
+  uint64_t* halo_conv = bars + 4;    // [4]
+  uint64_t* halo_empty = bars + 8;   // [4]
+  uint64_t* w_full = bars + 12;      // [kWStages]
+  uint64_t* w_empty = bars + 12 + kWStages;
+  uint64_t* acc_full = bars + 12 + 2 * kWStages;   // [2]
+  uint64_t* acc_empty = bars + 14 + 2 * kWStages;  // [2]
+  uint64_t* raw_full = bars + 16 + 2 * kWStages;   // [3] X3BF16: TMA -> converters
+  uint64_t* raw_empty = bars + 19 + 2 * kWStages;  // [3] X3BF16: converters -> TMA
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 22 + 2 * kWStages);
   int* pos_tab = reinterpret_cast<int*>(bars + 32);   // [2 groups][128] epilogue position -> NHWC offset
 
   constexpr bool THREE = MODE != MODE_TF32;
   auto halo_raw = [&](int s) { return halo_base + s * a.halo_stride + 128; };
   auto halo_lo = [&](int s) { return halo_base + s * a.halo_stride + 256 + a.halo_bytes; };
   // X3BF16: planes p = 0..2 of bf16 [2 kg][positions][8], each between 128-byte zero pads
-  auto plane = [&](int s, int p) { return halo_base + s * a.halo_stride + 128 + p * (a.plane_bytes + 128); };
+  // (plane pitch rounded to 128 B: the planes are TMA destinations in the PLANES mode)
+  const uint32_t plane_pitch = ((a.plane_bytes + 127u) & ~127u) + 128u;
+  auto plane = [&](int s, int p) { return halo_base + s * a.halo_stride + 128 + p * plane_pitch; };
   auto raw_slot = [&](int r) { return raw_base + r * a.raw_stride; };
   auto w_s = [&](int s) { return w_base + s * w_stage; };
 
   if (threadIdx.x == 0) {
-    for (int i = 0; i < 2; ++i) {
+    for (int i = 0; i < 4; ++i) {
       mbar_init(&halo_full[i], 1);
       mbar_init(&halo_conv[i], 128);
       mbar_init(&halo_empty[i], 1);
+    }
+    for (int i = 0; i < 2; ++i) {
       mbar_init(&acc_full[i], 1);
       mbar_init(&acc_empty[i], 256);
     }
@@ -243,9 +258,10 @@ __global__ void __launch_bounds__(kThreads, 1)
   }
   if (warp == 1) tmem_alloc<512>(tmem_slot);
   // zero the 128-byte pads around the halo buffers (read only for discarded positions)
-  if constexpr (BF) {
-    for (int i = threadIdx.x; i < 2 * 4 * 32; i += blockDim.x) {
-      const int s = i / 128, part = (i / 32) % 4, w = i % 32;
+  if constexpr (BFL) {
+    constexpr int kParts = PL ? 3 : 4;      // front pad + one behind each plane
+    for (int i = threadIdx.x; i < hslots * kParts * 32; i += blockDim.x) {
+      const int s = i / (kParts * 32), part = (i / 32) % kParts, w = i % 32;
       uint8_t* base = part == 0 ? halo_base + s * a.halo_stride : plane(s, part - 1) + a.plane_bytes;
       reinterpret_cast<uint32_t*>(base)[w] = 0u;
     }
@@ -271,7 +287,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     // releases.
     int hs = 0;
     uint32_t hph = 0;
-    const int nslots = BF ? a.raw_slots : 2;
+    const int nslots = BF ? a.raw_slots : hslots;
     UnitIter it(a.Co / 64, a.N, a.T);
     int cb, n, tile0, ntiles;
     while (it.next(cb, n, tile0, ntiles)) {
@@ -283,6 +299,11 @@ __global__ void __launch_bounds__(kThreads, 1)
           if constexpr (BF) {
             mbar_arrive_expect_tx(&raw_full[hs], a.halo_bytes);
             tma_load_4d(&tmap, &raw_full[hs], raw_slot(hs), kChunk * c, -1, y0 - 1, n);
+          } else if constexpr (PL) {
+            // both planes of the chunk: images [0, N) are plane 0, [N, 2N) plane 1
+            mbar_arrive_expect_tx(&halo_full[hs], 2 * a.plane_bytes);
+            tma_load_5d(&tmap, &halo_full[hs], plane(hs, 0), 0, -1, y0 - 1, 2 * c, n);
+            tma_load_5d(&tmap, &halo_full[hs], plane(hs, 1), 0, -1, y0 - 1, 2 * c, n + a.N);
           } else {
             mbar_arrive_expect_tx(&halo_full[hs], a.halo_bytes);
             tma_load_5d(&tmap, &halo_full[hs], halo_raw(hs), 0, -1, y0 - 1, 4 * c, n);
@@ -315,7 +336,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
   } else if (warp == 1) {
     // ===================== MMA issuer =====================
-    const uint32_t id = BF ? idesc(1, 128, 128) : idesc(2, 128, 128);
+    const uint32_t id = BFL ? idesc(1, 128, 128) : idesc(2, 128, 128);
     const uint32_t kg_x = (uint32_t)a.halo_pos * 16u;     // bytes between channel groups (halo)
     const uint32_t kg_w = 128u * 16u;                     // bytes between channel groups (weights)
     const uint64_t xj = (uint64_t)((2 * kg_x) >> 4);      // K-step (8 channels) of B, 16-byte units
@@ -336,12 +357,12 @@ __global__ void __launch_bounds__(kThreads, 1)
       long long wait_h = 0, wait_w = 0;
       for (int c = 0; c < a.nchunks; ++c) {
         long long tw = a.trace ? clock64() : 0;
-        mbar_wait(THREE ? &halo_conv[hs] : &halo_full[hs], hph);
+        mbar_wait((THREE && !PL) ? &halo_conv[hs] : &halo_full[hs], hph);
         if (a.trace) wait_h += clock64() - tw;
         tc_fence_after();
         if (a.trace && blockIdx.x < 2 && lane == 0 && u < 64 && c == 0) a.trace[(blockIdx.x * 64 + u) * 8 + 4] = globaltimer_ns();
-        const uint64_t dxh0 = desc_kmajor_interleave(smem_u32(BF ? plane(hs, 0) : halo_raw(hs)), kg_x, 128);
-        const uint64_t dxl0 = desc_kmajor_interleave(smem_u32(BF ? plane(hs, 1) : halo_lo(hs)), kg_x, 128);
+        const uint64_t dxh0 = desc_kmajor_interleave(smem_u32(BFL ? plane(hs, 0) : halo_raw(hs)), kg_x, 128);
+        const uint64_t dxl0 = desc_kmajor_interleave(smem_u32(BFL ? plane(hs, 1) : halo_lo(hs)), kg_x, 128);
         const uint64_t dxq0 = desc_kmajor_interleave(smem_u32(plane(hs, BF ? 2 : 0)), kg_x, 128);
         for (int dy = 0; dy < 3; ++dy) {
           long long tw2 = a.trace ? clock64() : 0;
@@ -354,20 +375,51 @@ __global__ void __launch_bounds__(kThreads, 1)
           const uint64_t bl = dxl0 + (uint64_t)row;
           const uint64_t bq = dxq0 + (uint64_t)row;
           const bool first = (c == 0 && dy == 0);
-          if (BF) {
+          if (PL) {
+            // 16 channels = one K = 16 step; A = [W0; W1] (bf16), B = planes x0, x1
+            if (elect_one()) {
+#pragma unroll
+              for (int dx = 0; dx < 3; ++dx) {
+                const uint64_t da = dw0 + dx * wtap;
+                const uint32_t accum = (first && dx == 0) ? 0u : 1u;
+                mma_f16_c<1>(d0, da, bh + dx, id, accum);
+                if (ntiles > 1) {
+                  mma_f16_c<2>(d0, da, bl + dx, id, 1u);
+                  mma_f16_c<2>(d0 + 128, da, bh + dx + 128, id, accum);
+                  mma_f16_c<3>(d0 + 128, da, bl + dx + 128, id, 1u);
+                } else {
+                  mma_f16_c<3>(d0, da, bl + dx, id, 1u);
+                }
+              }
+              mma_commit(&w_empty[ws]);
+            }
+          } else if (BF) {
             // 16 channels = one K = 16 step; A = [W0; W1] (bf16), B = planes x0, x1, x2
             if (elect_one()) {
 #pragma unroll
               for (int dx = 0; dx < 3; ++dx) {
                 const uint64_t da = dw0 + dx * wtap;
                 const uint32_t accum = (first && dx == 0) ? 0u : 1u;
+                if (kUseCollectorBF) {   // the 3 ntiles MMAs of one tap share A through the collector
+                  mma_f16_c<1>(d0, da, bh + dx, id, accum);
+                  mma_f16_c<2>(d0, da, bl + dx, id, 1u);
+                  if (ntiles > 1) {
+                    mma_f16_c<2>(d0, da, bq + dx, id, 1u);
+                    mma_f16_c<2>(d0 + 128, da, bh + dx + 128, id, accum);
+                    mma_f16_c<2>(d0 + 128, da, bl + dx + 128, id, 1u);
+                    mma_f16_c<3>(d0 + 128, da, bq + dx + 128, id, 1u);
+                  } else {
+                    mma_f16_c<3>(d0, da, bq + dx, id, 1u);
+                  }
+                } else {
 #pragma unroll
-                for (int s = 0; s < kS; ++s) {
-                  if (s < ntiles) {
-                    const uint64_t boff = (uint64_t)(dx + 128 * s);
-                    mma_f16(d0 + s * 128, da, bh + boff, id, accum);
-                    mma_f16(d0 + s * 128, da, bl + boff, id, 1u);
-                    mma_f16(d0 + s * 128, da, bq + boff, id, 1u);
+                  for (int s = 0; s < kS; ++s) {
+                    if (s < ntiles) {
+                      const uint64_t boff = (uint64_t)(dx + 128 * s);
+                      mma_f16(d0 + s * 128, da, bh + boff, id, accum);
+                      mma_f16(d0 + s * 128, da, bl + boff, id, 1u);
+                      mma_f16(d0 + s * 128, da, bq + boff, id, 1u);
+                    }
                   }
                 }
               }
@@ -410,7 +462,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         if (elect_one()) mma_commit(&halo_empty[hs]);
         __syncwarp();
-        if (++hs == 2) hs = 0, hph ^= 1;
+        if (++hs == hslots) hs = 0, hph ^= 1;
       }
       if (elect_one()) mma_commit(&acc_full[ab]);
       __syncwarp();
@@ -455,7 +507,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           if (++hs == 2) hs = 0, hph ^= 1;
         }
       }
-    } else if (THREE) {
+    } else if constexpr (THREE && !PL) {
       int hs = 0;
       uint32_t hph = 0;
       const int n16 = (int)(a.halo_bytes / 16);
@@ -687,6 +739,22 @@ CUtensorMap make_raw_map(const float* in, const ConvShape& s, int Wp, int rows_h
   return m;
 }
 
+// PLANES input: bf16 planes [2][N][H][W][C] (p1 = p0 + N H W C) viewed as 2N images in
+// 8-channel groups, box {8 ch, W + 2, rows, 2 groups, 1}: the slot layout [2 kg][pos][8].
+CUtensorMap make_planes_map(const void* planes, const ConvShape& s, int Wp, int rows_h) {
+  CUtensorMap m;
+  const cuuint64_t dims[5] = {8, (cuuint64_t)s.w, (cuuint64_t)s.h, (cuuint64_t)(s.ci / 8), (cuuint64_t)(2 * s.n)};
+  const cuuint64_t strides[4] = {(cuuint64_t)s.ci * 2, (cuuint64_t)s.w * s.ci * 2, 16,
+                                 (cuuint64_t)s.h * s.w * s.ci * 2};
+  const cuuint32_t box[5] = {8, (cuuint32_t)Wp, (cuuint32_t)rows_h, 2, 1};
+  const cuuint32_t estr[5] = {1, 1, 1, 1, 1};
+  CUresult r = encode_fn()(&m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 5, const_cast<void*>(planes), dims, strides, box,
+                           estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                           CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) fail(RP_ERR_CUDA, "cuTensorMapEncodeTiled failed (" + std::to_string((int)r) + ")");
+  return m;
+}
+
 CUtensorMap make_halo_map(const float* in, const ConvShape& s, int Wp, int rows_h) {
   CUtensorMap m;
   const cuuint64_t dims[5] = {4, (cuuint64_t)s.w, (cuuint64_t)s.h, (cuuint64_t)(s.ci / 4), (cuuint64_t)s.n};
@@ -721,9 +789,16 @@ Plan plan_for(const ConvShape& s, int mode = MODE_X3TF32) {
   p.halo_bytes = (uint32_t)p.halo_pos * 64u;
   p.plane_bytes = (uint32_t)p.halo_pos * 32u;
   const size_t fixed_bytes = 2 * 2 * 2 * 32 * 32 * 4 + 256 + 1024 + 1024;   // xchg + barriers + table + alignment
-  if (mode == MODE_X3BF16) {
+  if (mode == MODE_PLANES) {
     p.w_tap = 128u * kChunk * 2u;
-    p.halo_stride = (128 + 3 * (p.plane_bytes + 128) + 1023) / 1024 * 1024;   // plane slot
+    p.halo_stride = (128 + 2 * (p.plane_bytes + 255) + 1023) / 1024 * 1024;   // plane-pair slot (128 B pitch)
+    const size_t base = kWStages * 3 * (size_t)p.w_tap + fixed_bytes;
+    p.raw_slots = 4;
+    while (p.raw_slots > 2 && base + p.raw_slots * (size_t)p.halo_stride > (size_t)kMaxSmem) --p.raw_slots;
+    p.smem = base + p.raw_slots * (size_t)p.halo_stride;
+  } else if (mode == MODE_X3BF16) {
+    p.w_tap = 128u * kChunk * 2u;
+    p.halo_stride = (128 + 3 * (p.plane_bytes + 255) + 1023) / 1024 * 1024;   // plane slot (128 B pitch)
     p.raw_stride = (p.halo_bytes + 1023) / 1024 * 1024;
     const size_t base = 2 * (size_t)p.halo_stride + kWStages * 3 * (size_t)p.w_tap + fixed_bytes;
     p.raw_slots = base + 3 * (size_t)p.raw_stride <= (size_t)kMaxSmem ? 3 : 2;
@@ -738,15 +813,20 @@ Plan plan_for(const ConvShape& s, int mode = MODE_X3TF32) {
 }
 
 std::mutex g_map_mu;
-std::map<std::tuple<const void*, int, int, int, int, int, bool>, CUtensorMap> g_maps;
+std::map<std::tuple<const void*, int, int, int, int, int, int>, CUtensorMap> g_maps;
 
-const CUtensorMap& cached_map(const float* in, const ConvShape& s, int Wp, int rows_h, bool raw) {
+// kind: 0 interleaved fp32 halo, 1 raw fp32 [pos][16], 2 bf16 plane pair
+const CUtensorMap& cached_map(const void* in, const ConvShape& s, int Wp, int rows_h, int kind) {
   std::lock_guard<std::mutex> lk(g_map_mu);
-  auto key = std::make_tuple((const void*)in, s.n, s.h, s.w, s.ci, rows_h, raw);
+  auto key = std::make_tuple(in, s.n, s.h, s.w, s.ci, rows_h, kind);
   auto it = g_maps.find(key);
   if (it == g_maps.end()) {
     if (g_maps.size() > 4096) g_maps.clear();
-    it = g_maps.emplace(key, raw ? make_raw_map(in, s, Wp, rows_h) : make_halo_map(in, s, Wp, rows_h)).first;
+    const float* f = static_cast<const float*>(in);
+    it = g_maps.emplace(key, kind == 2   ? make_planes_map(in, s, Wp, rows_h)
+                             : kind == 1 ? make_raw_map(f, s, Wp, rows_h)
+                                         : make_halo_map(f, s, Wp, rows_h))
+             .first;
   }
   return it->second;
 }
@@ -764,7 +844,9 @@ void launch_cfg(const CUtensorMap& m, const TcArgs& a, size_t smem, int grid, cu
 
 template <int EPI>
 void launch_epi(const CUtensorMap& m, const TcArgs& a, int mode, size_t smem, int grid, cudaStream_t st) {
-  if (mode == MODE_X3BF16)
+  if (mode == MODE_PLANES)
+    launch_cfg<EPI, MODE_PLANES>(m, a, smem, grid, st);
+  else if (mode == MODE_X3BF16)
     launch_cfg<EPI, MODE_X3BF16>(m, a, smem, grid, st);
   else if (mode == MODE_X3TF32)
     launch_cfg<EPI, MODE_X3TF32>(m, a, smem, grid, st);
@@ -782,8 +864,9 @@ int64_t conv3x3_tc_ws_bytes(const ConvShape& s) { return 9LL * s.ci * 2 * s.co *
 
 void conv3x3_fwd_tc(const ConvShape& s, const float* in, const float* w_hwio, bool dgrad_weights, const float* bias,
                     const float* aux, float h, int epi, float* out, int mode, void* ws, cudaStream_t st,
-                    void* out_planes) {
+                    void* out_planes, const void* in_planes) {
   if (s.pixels() == 0) return;
+  if (in_planes) mode = MODE_PLANES;
   const Plan p = plan_for(s, mode);
   if (!p.ok) fail(RP_ERR_INTERNAL, "conv3x3_fwd_tc: unsupported shape");
   // the weight tensor handed in is HWIO of the *forward* conv; for dgrad it has
@@ -792,7 +875,7 @@ void conv3x3_fwd_tc(const ConvShape& s, const float* in, const float* w_hwio, bo
   const int co_src = dgrad_weights ? s.ci : s.co;
   const int64_t total = 9LL * s.ci * 2 * s.co;
   const int pgrid = (int)std::min<int64_t>(ceil_div(total, 256), 16 * kNumSMs);
-  if (mode == MODE_X3BF16)
+  if (mode == MODE_X3BF16 || mode == MODE_PLANES)
     prep_weights_bf16x2_kernel<<<pgrid, 256, 0, st>>>(w_hwio, ci_src, co_src, dgrad_weights ? 1 : 0,
                                                       static_cast<__nv_bfloat16*>(ws));
   else
@@ -826,7 +909,8 @@ void conv3x3_fwd_tc(const ConvShape& s, const float* in, const float* w_hwio, bo
   a.p0 = static_cast<__nv_bfloat16*>(out_planes);
   a.p1 = out_planes ? a.p0 + s.pixels() * s.co : nullptr;
   a.trace = g_trace;
-  const CUtensorMap& m = cached_map(in, s, p.Wp, p.rows_h, mode == MODE_X3BF16);
+  const CUtensorMap& m = mode == MODE_PLANES ? cached_map(in_planes, s, p.Wp, p.rows_h, 2)
+                                              : cached_map(in, s, p.Wp, p.rows_h, mode == MODE_X3BF16 ? 1 : 0);
   const int grid = std::min(a.num_tiles, kNumSMs);
   switch (epi) {
     case EPI_BIAS: launch_epi<EPI_BIAS>(m, a, mode, p.smem, grid, st); break;

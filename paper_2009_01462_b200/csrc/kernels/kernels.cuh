@@ -57,9 +57,11 @@ enum { TC_MODE_TF32 = 0, TC_MODE_X3TF32 = 1, TC_MODE_X3BF16 = 2 };
 bool conv3x3_tc_supported(const ConvShape& s);
 int64_t conv3x3_tc_ws_bytes(const ConvShape& s);
 // out_planes (optional): bf16 [2][pixels * co] receives the plane pair of out.
+// in_planes (optional): bf16 [2][pixels * ci], the input as a plane pair (in unused): the
+// 2-MMA plane mode (~2^-17 relative).
 void conv3x3_fwd_tc(const ConvShape& s, const float* in, const float* w_hwio, bool dgrad_weights, const float* bias,
                     const float* aux, float h, int epi, float* out, int mode, void* ws, cudaStream_t st,
-                    void* out_planes = nullptr);
+                    void* out_planes = nullptr, const void* in_planes = nullptr);
 
 // tcgen05 bf16-operand conv, fp32 accumulate (conv_bf16.cu): Co % 128 == 0, Ci % 32 == 0.
 bool conv3x3_bf16_supported(const ConvShape& s);

@@ -2,9 +2,10 @@
 the fp32 trainer runs on tcgen05 shapes, against the fp64 oracle block (block_forward /
 block_vjp, network.cpp:82-106) and against the fp32-operand block path.
 
-The forward convs are the same kernel as rp_op_block_fwd, so a and x_next must match it bit
-for bit; the planes must reconstruct them to bf16-pair precision (|v - p0 - p1| <= 2^-16 |v|).
-The weight gradients differ from the fp32-operand path only by the plane split (~1e-5)."""
+Every conv of the plane path reads its input as a bf16 plane pair (2^-17 relative split) and
+writes the plane pair of its output, which must reconstruct the fp32 output to bf16-pair
+precision (|v - p0 - p1| <= 2^-16 |v|).  Tolerances: 2e-5 of the tensor's max |value| against
+the fp64 oracle for activations / cotangents, 5e-5 for the weight gradients."""
 import ctypes as C
 
 import numpy as np
@@ -18,7 +19,7 @@ pytestmark = pytest.mark.gpu
 torch = pytest.importorskip("torch")
 
 GW_TOL = 5e-5    # weight / bias gradients, relative to the tensor's max |value|
-FWD_TOL = 2e-5   # a, x_next, input cotangent (3xBF16 convs)
+FWD_TOL = 2e-5   # a, x_next, input cotangent
 
 
 def _p(t):
@@ -68,19 +69,20 @@ def test_block_planes(n, hw, c, ch):
     xn = torch.empty(ne, device=dev)
     a_p = torch.empty(2 * nh, dtype=torch.int16, device=dev)
     xn_p = torch.empty(2 * ne, dtype=torch.int16, device=dev)
-    rp.check(lib().rp_op_block_fwd_planes(C.byref(geo), n, _p(tx), pb, _p(a), _p(xn), _p(a_p), _p(xn_p), _p(ws), wsb,
-                                          None))
+    x_p = torch.empty(2 * ne, dtype=torch.int16, device=dev)
+    rp.check(lib().rp_op_split_planes(_p(tx), ne, _p(x_p), C.c_void_p(x_p.data_ptr() + 2 * ne), None))
+    rp.check(lib().rp_op_block_fwd_planes(C.byref(geo), n, _p(tx), _p(x_p), pb, _p(a), _p(xn), _p(a_p), _p(xn_p),
+                                          _p(ws), wsb, None))
     torch.cuda.synchronize()
-    assert torch.equal(a, a_ref) and torch.equal(xn, xn_ref)
     a64, xn64 = a.cpu().numpy().astype(np.float64), xn.cpu().numpy().astype(np.float64)
+    assert _rel(a64, a_ref.cpu().numpy().astype(np.float64)) < FWD_TOL
+    assert _rel(xn64, xn_ref.cpu().numpy().astype(np.float64)) < FWD_TOL
     assert np.all(np.abs(_planes_to_f64(a_p, nh) - a64) <= 2.0 ** -16 * np.abs(a64))
     assert np.all(np.abs(_planes_to_f64(xn_p, ne) - xn64) <= 2.0 ** -16 * np.abs(xn64))
     want_xn, cache = O.block_forward(net32, 0, x.astype(np.float64))
     assert _rel(xn64.reshape(want_xn.shape), want_xn) < FWD_TOL
 
     # backward: plane path vs oracle and vs fp32-operand path
-    x_p = torch.empty(2 * ne, dtype=torch.int16, device=dev)
-    rp.check(lib().rp_op_split_planes(_p(tx), ne, _p(x_p), C.c_void_p(x_p.data_ptr() + 2 * ne), None))
     g_io = tup.clone().reshape(-1)
     g_p = torch.empty(2 * ne, dtype=torch.int16, device=dev)
     rp.check(lib().rp_op_split_planes(_p(g_io), ne, _p(g_p), C.c_void_p(g_p.data_ptr() + 2 * ne), None))
@@ -95,8 +97,8 @@ def test_block_planes(n, hw, c, ch):
     rp.check(lib().rp_op_block_bwd(C.byref(geo), n, _p(tx), _p(a_ref), pb, _p(g_ref), _p(dpre),
                                    C.c_void_p(gb_ref.data_ptr() + 4 * off), rp.MATH["fp32"], _p(ws), wsb, None))
     torch.cuda.synchronize()
-    assert torch.equal(g_io, g_ref)        # dgrads: same kernels, same inputs
     g64 = g_io.cpu().numpy().astype(np.float64)
+    assert _rel(g64, g_ref.cpu().numpy().astype(np.float64)) < FWD_TOL
     assert np.all(np.abs(_planes_to_f64(g_p, ne) - g64) <= 2.0 ** -16 * np.abs(g64))
 
     p_prev, (gw1, gb1, gw2, gb2) = O.block_vjp(net32, 0, O.BlockCache(x.astype(np.float64), a64.reshape(
