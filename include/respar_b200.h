@@ -156,6 +156,12 @@ int rp_op_conv3x3(int32_t n, int32_t h, int32_t w, int32_t ci, int32_t co, const
                   int32_t dgrad, const float* bias, const float* aux, double hstep, int32_t epi, float* out,
                   int32_t math, void* ws, int64_t ws_bytes, void* stream);
 int64_t rp_op_conv3x3_workspace_bytes(int32_t ci, int32_t co);
+/* The same conv reading its input as a bf16 plane pair (in_planes = [2][n h w ci]: x = p0 + p1)
+ * on the tcgen05 plane mode (Co % 64 == 0, Ci % 16 == 0; ~2^-17 relative); out_planes
+ * (optional, [2][n h w co] bf16) receives the plane pair of out. */
+int rp_op_conv3x3_planes(int32_t n, int32_t h, int32_t w, int32_t ci, int32_t co, const void* in_planes,
+                         const float* w_hwio, int32_t dgrad, const float* bias, const float* aux, double hstep,
+                         int32_t epi, float* out, void* out_planes, void* ws, int64_t ws_bytes, void* stream);
 /* Weight gradient of that conv: gw[3][3][ci][co] = scale sum_p in[p+tap][ci] gout[p][co],
  * gb[co] = scale sum_p gout[p][co] (gb may be NULL).  Deterministic. */
 int rp_op_conv3x3_wgrad(int32_t n, int32_t h, int32_t w, int32_t ci, int32_t co, const float* in, const float* gout,

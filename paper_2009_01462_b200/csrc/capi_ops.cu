@@ -420,6 +420,22 @@ int rp_op_conv3x3_wgrad(int32_t n, int32_t h, int32_t w, int32_t ci, int32_t co,
   });
 }
 
+int rp_op_conv3x3_planes(int32_t n, int32_t h, int32_t w, int32_t ci, int32_t co, const void* in_planes,
+                         const float* w_hwio, int32_t dgrad, const float* bias, const float* aux, double hstep,
+                         int32_t epi, float* out, void* out_planes, void* ws, int64_t ws_bytes, void* stream) {
+  return guard([&] {
+    if (epi < 0 || epi > 5) fail(RP_ERR_RANGE, "conv3x3_planes: unknown epilogue");
+    if (n < 0 || h < 1 || w < 1 || ci < 1 || co < 1) fail(RP_ERR_SHAPE, "conv3x3_planes: bad shape");
+    const k::ConvShape s{n, h, w, ci, co};
+    if (!k::conv3x3_tc_supported(s)) fail(RP_ERR_SHAPE, "conv3x3_planes: unsupported shape (Co % 64, Ci % 16)");
+    if (ws_bytes < rp_op_conv3x3_workspace_bytes(std::min(ci, co), std::max(ci, co)))
+      fail(RP_ERR_RANGE, "conv3x3_planes: workspace too small");
+    if (n > 0) need(in_planes, "in_planes");
+    conv(s, nullptr, w_hwio, dgrad != 0, bias, aux, (float)hstep, epi, out, RP_MATH_FP32, ws, RP_PROF_OTHER,
+         aux != nullptr, S(stream), out_planes, in_planes);
+  });
+}
+
 int64_t rp_op_conv3x3_wgrad_workspace_bytes(int32_t n, int32_t h, int32_t w, int32_t ci, int32_t co) {
   return wgrad_ws_bytes({n, h, w, ci, co});
 }

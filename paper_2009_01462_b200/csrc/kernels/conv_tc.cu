@@ -211,7 +211,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint8_t* halo_base = smem;
   uint8_t* raw_base = smem + 2 * a.halo_stride;               // X3BF16 only
   uint8_t* w_base = smem + hslots * a.halo_stride + (BF ? a.raw_slots * a.raw_stride : 0u);   // kWStages stages
-  float* xchg = reinterpret_cast<float*>(w_base + kWStages * w_stage);   // [2 groups][2 pairs][2 sides][32][32]
+  float* xchg = reinterpret_cast<float*>(w_base + kWStages * w_stage);   // [2 groups][hi, lo][32 pos][64 ch]
   uint64_t* bars = reinterpret_cast<uint64_t*>(xchg + 2 * 2 * 2 * 32 * 32);
   uint64_t* halo_full = bars;        // [4]
   uint64_t* halo_conv = bars + 4;    // [4]
@@ -533,26 +533,24 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
   } else if (warp < 14) {
     // ===================== epilogue =====================
-    // Two groups of 4 warps; group g finishes tile s = g of every unit (both tiles of a
-    // unit drain in parallel).  D row r: r < 64 -> W_hi (W0) products for co = r, r >= 64 ->
-    // W_lo (W1) products for co = r - 64.  The warp pair holding the hi and lo rows of the
-    // same 32 channels swaps half of each 64-position batch through shared memory; each
-    // warp then finishes 32 positions (hi + lo, fused epilogue) and stores 32 consecutive
-    // channels of a position per instruction (coalesced NHWC).  Frame position -> NHWC
-    // offset comes from a per-tile table (one LDS broadcast per position).
+    // Two groups of 4 warps; group g finishes tile s = g of every unit (both tiles of a unit
+    // drain in parallel).  D row r: r < 64 -> W_hi (W0) products for co = r, r >= 64 ->
+    // W_lo (W1) products for co = r - 64.  Per batch of 32 positions every warp moves its
+    // 32 rows (TMEM lane quadrant) to shared memory as [hi|lo][position][64 ch]; the group
+    // then reads it back transposed -- a thread owns 4 consecutive channels of a position --
+    // and finishes hi + lo, the fused epilogue and the stores with 16-byte vectors
+    // (coalesced NHWC rows).  Frame position -> NHWC offset comes from a per-tile table.
     const int q = warp & 3;                 // TMEM lane quadrant this warp may access
     const int grp = (warp - 6) >> 2;        // tile of the unit this warp drains
-    const bool hi_warp = q < 2;
-    const int co_l = (q & 1) * 32 + lane;   // output channel of this lane within the co block
     const int gtid = (int)threadIdx.x - 192 - grp * 128;
     constexpr bool kBias = EPI == EPI_BIAS || EPI == EPI_BIAS_TANH || EPI == EPI_RESID;
     constexpr bool kAux = EPI == EPI_RESID || EPI == EPI_TANH_BWD || EPI == EPI_ADD;
-    const int own0 = hi_warp ? 0 : 32;      // positions [own0, own0 + 32) of each 64-batch are ours
-    float* mine = xchg + ((grp * 2 + (q & 1)) * 2 + (hi_warp ? 0 : 1)) * 32 * 32;
-    const float* theirs = xchg + ((grp * 2 + (q & 1)) * 2 + (hi_warp ? 1 : 0)) * 32 * 32;
+    float* buf = xchg + grp * 2 * 32 * 64;                // [2: hi, lo][32 positions][64 ch]
+    float* wrow = buf + (q >> 1) * 32 * 64 + (q & 1) * 32 + lane;   // this lane's channel column
+    const int c4 = gtid & 15;                             // channels 4 c4 .. 4 c4 + 3 (read-back)
+    const int prow = gtid >> 4;                           // positions prow + 8 j (read-back)
     int* tab = pos_tab + grp * 128;
-    const uint32_t pair_bar = 2 + grp * 2 + (q & 1);   // this warp and its partner (64 threads)
-    const uint32_t grp_bar = 6 + grp;                  // the group (128 threads)
+    const uint32_t grp_bar = 6 + grp;                     // the group (128 threads)
     int ab = 0;
     uint32_t aph = 0;
     UnitIter it(a.Co / 64, a.N, a.T);
@@ -560,8 +558,9 @@ __global__ void __launch_bounds__(kThreads, 1)
     while (it.next(cb, n, tile0, ntiles)) {
       const int u = ui++;
       const int64_t img = (int64_t)n * a.H * a.W;
-      const int co = cb * 64 + co_l;
-      const float bias = kBias ? __ldg(a.bias + co) : 0.f;
+      const int co = cb * 64 + 4 * c4;
+      float4 bias = make_float4(0.f, 0.f, 0.f, 0.f);
+      if (kBias) bias = make_float4(__ldg(a.bias + co), __ldg(a.bias + co + 1), __ldg(a.bias + co + 2), __ldg(a.bias + co + 3));
       mbar_wait(&acc_full[ab], aph);
       tc_fence_after();
       if (a.trace && blockIdx.x < 2 && threadIdx.x == 192) a.trace[(blockIdx.x * 64 + min(u, 63)) * 8 + 2] = globaltimer_ns();
@@ -569,9 +568,8 @@ __global__ void __launch_bounds__(kThreads, 1)
         {
           const int f = (tile0 + grp) * 128 + gtid;
           const int y = f / Wp, X = f - y * Wp;
-          asm volatile("bar.sync %0, 128;" ::"r"(grp_bar) : "memory");   // last tile's readers are done
+          asm volatile("bar.sync %0, 128;" ::"r"(grp_bar) : "memory");   // the last tile's readers are done
           tab[gtid] = (y < a.H && X >= 1 && X <= a.W) ? (y * a.W + (X - 1)) * a.Co : -1;
-          asm volatile("bar.sync %0, 128;" ::"r"(grp_bar) : "memory");
         }
         const uint32_t tcol = tmem_base + ((uint32_t)(q * 32) << 16) + (uint32_t)((ab * kS + grp) * 128);
         const float* auxb = kAux ? a.aux + img * a.Co + co : nullptr;
@@ -579,55 +577,56 @@ __global__ void __launch_bounds__(kThreads, 1)
         const bool planes = a.p0 != nullptr;
         __nv_bfloat16* p0b = planes ? a.p0 + img * a.Co + co : nullptr;
         __nv_bfloat16* p1b = planes ? a.p1 + img * a.Co + co : nullptr;
-        for (int p0 = 0; p0 < 128; p0 += 64) {
-          {   // the 32 columns the partner warp finishes: TMEM -> smem
-            uint32_t rr[32];
-            const uint32_t c_give = tcol + (uint32_t)p0 + (hi_warp ? 32u : 0u);
-            tmem_ld16(c_give, *reinterpret_cast<uint32_t(*)[16]>(&rr[0]));
-            tmem_ld16(c_give + 16, *reinterpret_cast<uint32_t(*)[16]>(&rr[16]));
-            tmem_wait_ld();
+        for (int pb = 0; pb < 128; pb += 32) {
+          uint32_t r[32];
+          tmem_ld16(tcol + (uint32_t)pb, *reinterpret_cast<uint32_t(*)[16]>(&r[0]));
+          tmem_ld16(tcol + (uint32_t)pb + 16, *reinterpret_cast<uint32_t(*)[16]>(&r[16]));
+          tmem_wait_ld();
+          asm volatile("bar.sync %0, 128;" ::"r"(grp_bar) : "memory");   // buf free (and tab written)
 #pragma unroll
-            for (int e = 0; e < 32; ++e) mine[e * 32 + lane] = __uint_as_float(rr[e]);
+          for (int e = 0; e < 32; ++e) wrow[e * 64] = __uint_as_float(r[e]);
+          asm volatile("bar.sync %0, 128;" ::"r"(grp_bar) : "memory");
+          int off[4];
+          float4 ax[4];
+#pragma unroll
+          for (int j = 0; j < 4; ++j) off[j] = tab[pb + prow + 8 * j];
+          if constexpr (kAux) {
+#pragma unroll
+            for (int j = 0; j < 4; ++j)
+              ax[j] = off[j] >= 0 ? *reinterpret_cast<const float4*>(auxb + off[j]) : make_float4(0.f, 0.f, 0.f, 0.f);
           }
-          uint32_t r[32];   // our own 32 columns
-          {
-            const uint32_t c_own = tcol + (uint32_t)p0 + (uint32_t)own0;
-            tmem_ld16(c_own, *reinterpret_cast<uint32_t(*)[16]>(&r[0]));
-            tmem_ld16(c_own + 16, *reinterpret_cast<uint32_t(*)[16]>(&r[16]));
-            tmem_wait_ld();
-          }
-          asm volatile("bar.sync %0, 64;" ::"r"(pair_bar) : "memory");
-          const int* tb = tab + p0 + own0;
 #pragma unroll
-          for (int h8 = 0; h8 < 32; h8 += 8) {
-            int off[8];
-            float ax[8];
+          for (int j = 0; j < 4; ++j) {
+            if (off[j] < 0) continue;
+            const int pr = prow + 8 * j;
+            const float4 hv = *reinterpret_cast<const float4*>(buf + pr * 64 + 4 * c4);
+            const float4 lv = *reinterpret_cast<const float4*>(buf + 32 * 64 + pr * 64 + 4 * c4);
+            const float v[4] = {hv.x + lv.x, hv.y + lv.y, hv.z + lv.z, hv.w + lv.w};
+            const float bb[4] = {bias.x, bias.y, bias.z, bias.w};
+            const float xa[4] = {ax[j].x, ax[j].y, ax[j].z, ax[j].w};
+            float o[4];
 #pragma unroll
-            for (int e = 0; e < 8; ++e) off[e] = tb[h8 + e];
-            if constexpr (kAux) {
-#pragma unroll
-              for (int e = 0; e < 8; ++e) ax[e] = off[e] >= 0 ? auxb[off[e]] : 0.f;
+            for (int i = 0; i < 4; ++i) {
+              if constexpr (EPI == EPI_BIAS) o[i] = v[i] + bb[i];
+              else if constexpr (EPI == EPI_BIAS_TANH) o[i] = tanhf(v[i] + bb[i]);
+              else if constexpr (EPI == EPI_RESID) o[i] = xa[i] + a.h * (v[i] + bb[i]);
+              else if constexpr (EPI == EPI_TANH_BWD) o[i] = (a.h * v[i]) * (1.f - xa[i] * xa[i]);
+              else if constexpr (EPI == EPI_ADD) o[i] = xa[i] + v[i];
+              else o[i] = a.h * v[i];
             }
+            *reinterpret_cast<float4*>(outb + off[j]) = make_float4(o[0], o[1], o[2], o[3]);
+            if (planes) {
+              uint32_t h[2], l[2];
 #pragma unroll
-            for (int e = 0; e < 8; ++e) {
-              if (off[e] < 0) continue;                       // warp-uniform
-              const float v = __uint_as_float(r[h8 + e]) + theirs[(h8 + e) * 32 + lane];
-              float o;
-              if constexpr (EPI == EPI_BIAS) o = v + bias;
-              else if constexpr (EPI == EPI_BIAS_TANH) o = tanhf(v + bias);
-              else if constexpr (EPI == EPI_RESID) o = ax[e] + a.h * (v + bias);
-              else if constexpr (EPI == EPI_TANH_BWD) o = (a.h * v) * (1.f - ax[e] * ax[e]);
-              else if constexpr (EPI == EPI_ADD) o = ax[e] + v;
-              else o = a.h * v;
-              outb[off[e]] = o;
-              if (planes) {
-                const __nv_bfloat16 h0 = __float2bfloat16_rn(o);
-                p0b[off[e]] = h0;
-                p1b[off[e]] = __float2bfloat16_rn(o - __bfloat162float(h0));
+              for (int i = 0; i < 2; ++i) {
+                const __nv_bfloat162 hh = __floats2bfloat162_rn(o[2 * i], o[2 * i + 1]);
+                h[i] = *reinterpret_cast<const uint32_t*>(&hh);
+                l[i] = pack_bf16x2(o[2 * i] - __low2float(hh), o[2 * i + 1] - __high2float(hh));
               }
+              *reinterpret_cast<uint2*>(p0b + off[j]) = make_uint2(h[0], h[1]);
+              *reinterpret_cast<uint2*>(p1b + off[j]) = make_uint2(l[0], l[1]);
             }
           }
-          asm volatile("bar.sync %0, 64;" ::"r"(pair_bar) : "memory");   // partner done with `mine`
         }
       }
       if (a.trace && blockIdx.x < 2 && threadIdx.x == 192) a.trace[(blockIdx.x * 64 + min(u, 63)) * 8 + 3] = globaltimer_ns();

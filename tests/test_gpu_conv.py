@@ -77,6 +77,51 @@ def test_conv_all_epilogues(shape, math, tol, dgrad):
         assert err <= tol, (EPIS[epi], err)
 
 
+PLANE_SHAPES = [(2, 32, 32, 64, 64), (1, 32, 32, 64, 128), (2, 32, 32, 128, 64), (5, 7, 7, 48, 64),
+                (1, 12, 10, 16, 64), (2, 16, 16, 128, 128), (1, 16, 16, 256, 256), (1, 9, 11, 256, 64)]
+
+
+# plane mode: the input enters as a bf16 pair (2^-17 relative), W as [W0; W1] (2^-17)
+@pytest.mark.parametrize("shape", PLANE_SHAPES)
+@pytest.mark.parametrize("dgrad", [False, True])
+def test_conv_planes(shape, dgrad):
+    n, hh, ww, ci, co = shape
+    if dgrad and ci % 64:
+        pytest.skip("dgrad output channels (the forward ci) must be a multiple of 64")
+    dev = torch.device("cuda")
+    for epi in range(6):
+        rng = np.random.default_rng(epi)
+        cin, cout = (co, ci) if dgrad else (ci, co)
+        x = rng.uniform(-1, 1, (n, hh, ww, cin)).astype(np.float32)
+        w = (rng.uniform(-1, 1, (3, 3, ci, co)) / np.sqrt(9 * ci)).astype(np.float32)
+        bias = rng.uniform(-0.2, 0.2, cout).astype(np.float32)
+        aux = rng.uniform(-0.9, 0.9, (n, hh, ww, cout)).astype(np.float32)
+        acc = O.conv3x3_dgrad(x.astype(np.float64), w.astype(np.float64)) if dgrad else \
+            O.conv3x3(x.astype(np.float64), w.astype(np.float64))
+        want = want_epi(epi, acc, bias.astype(np.float64), aux.astype(np.float64), np.float32(0.7))
+        tx, tw, tb, taux = (torch.from_numpy(v).to(dev) for v in (x, w, bias, aux))
+        xp = torch.empty(2 * tx.numel(), dtype=torch.bfloat16, device=dev)
+        rp.check(lib().rp_op_split_planes(C.c_void_p(tx.data_ptr()), tx.numel(), C.c_void_p(xp.data_ptr()),
+                                          C.c_void_p(xp.data_ptr() + 2 * tx.numel()), None))
+        out = taux.clone() if epi == 4 else torch.empty((n, hh, ww, cout), device=dev)
+        op = torch.empty(2 * out.numel(), dtype=torch.bfloat16, device=dev)
+        wsb = lib().rp_op_conv3x3_workspace_bytes(ci, co)
+        ws = torch.empty(wsb, dtype=torch.uint8, device=dev)
+        use_aux = epi in (2, 3, 4)
+        rp.check(lib().rp_op_conv3x3_planes(
+            n, hh, ww, cin, cout, C.c_void_p(xp.data_ptr()), C.c_void_p(tw.data_ptr()), 1 if dgrad else 0,
+            C.c_void_p(tb.data_ptr()), C.c_void_p(out.data_ptr() if epi == 4 else taux.data_ptr()) if use_aux else None,
+            0.7, epi, C.c_void_p(out.data_ptr()), C.c_void_p(op.data_ptr()), C.c_void_p(ws.data_ptr()), wsb, None))
+        torch.cuda.synchronize()
+        got = out.cpu().numpy().astype(np.float64)
+        err = np.abs(got - want).max() / max(np.abs(want).max(), 1e-30)
+        print(f"planes {shape} dgrad={dgrad} {EPIS[epi]}: {err:.2e}")
+        assert err <= 2e-5, (EPIS[epi], err)
+        pl = op.float().cpu().numpy().astype(np.float64)
+        rec = (pl[:out.numel()] + pl[out.numel():]).reshape(got.shape)
+        assert np.all(np.abs(rec - got) <= 2.0 ** -16 * np.abs(got)), EPIS[epi]
+
+
 BF16_SHAPES = [(2, 16, 16, 128, 128), (1, 16, 16, 256, 256), (2, 9, 11, 64, 128), (1, 32, 32, 128, 256),
                (2, 8, 8, 64, 64)]   # the last falls back to 3xTF32 (Co % 128 != 0)
 

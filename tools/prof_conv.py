@@ -32,7 +32,10 @@ ws_b = max(lib().rp_op_conv3x3_workspace_bytes(c, c), lib().rp_op_conv3x3_wgrad_
 ws = torch.empty(ws_b, dtype=torch.uint8, device=dev)
 gw = torch.empty(3, 3, c, c, device=dev)
 gb = torch.empty(c, device=dev)
-planes = [torch.empty(n * h * w * c, dtype=torch.bfloat16, device=dev) for _ in range(4)]
+ne = n * h * w * c
+xp = torch.empty(2 * ne, dtype=torch.bfloat16, device=dev)   # plane pairs: p1 = p0 + ne
+gp = torch.empty(2 * ne, dtype=torch.bfloat16, device=dev)
+planes = [xp[:ne], xp[ne:], gp[:ne], gp[ne:]]
 for src, (p0, p1) in ((x, planes[:2]), (g, planes[2:])):
     rp.check(lib().rp_op_split_planes(C.c_void_p(src.data_ptr()), src.numel(), C.c_void_p(p0.data_ptr()),
                                       C.c_void_p(p1.data_ptr()), None))
@@ -54,6 +57,12 @@ for which in a.which.split(","):
         elif which == "dgrad":
             rp.check(lib().rp_op_conv3x3(n, h, w, c, c, P(g.data_ptr()), P(wt.data_ptr()), 1, None, P(x.data_ptr()),
                                          1.0, 3, P(out.data_ptr()), m, P(ws.data_ptr()), ws_b, None))
+        elif which in ("fprop_planes", "dgrad_planes"):
+            d = which == "dgrad_planes"
+            rp.check(lib().rp_op_conv3x3_planes(n, h, w, c, c, P(planes[0].data_ptr()), P(wt.data_ptr()), int(d),
+                                                P(b.data_ptr()), P(x.data_ptr()) if d else None, 1.0, 3 if d else 1,
+                                                P(out.data_ptr()), P(planes[2].data_ptr()), P(ws.data_ptr()), ws_b,
+                                                None))
         elif which == "wgrad_planes":
             rp.check(lib().rp_op_conv3x3_wgrad_planes(n, h, w, c, c, *[C.c_void_p(t.data_ptr()) for t in planes], 1.0,
                                                       P(gw.data_ptr()), P(gb.data_ptr()), P(ws.data_ptr()), ws_b,

@@ -11,12 +11,20 @@ x = torch.randn(n, h, w, c, device="cuda"); out = torch.empty_like(x)
 wt = torch.randn(3, 3, c, c, device="cuda") * 0.05; b = torch.zeros(c, device="cuda")
 wsb = lib().rp_op_conv3x3_workspace_bytes(c, c); ws = torch.empty(wsb, dtype=torch.uint8, device="cuda")
 P = C.c_void_p
-for math in ("fp32", "tf32"):
+xp = torch.empty(2 * x.numel(), dtype=torch.bfloat16, device="cuda")
+op = torch.empty_like(xp)
+rp.check(lib().rp_op_split_planes(P(x.data_ptr()), x.numel(), P(xp.data_ptr()), P(xp.data_ptr() + 2 * x.numel()), None))
+for math in sys.argv[1:] or ("planes", "fp32"):
     for it in range(3):
         if it == 2:
             L.rp_debug_set_trace(P(tr.data_ptr()))
-        rp.check(lib().rp_op_conv3x3(n, h, w, c, c, P(x.data_ptr()), P(wt.data_ptr()), 0, P(b.data_ptr()), None, 1.0, 1,
-                                     P(out.data_ptr()), rp.MATH[math], P(ws.data_ptr()), wsb, None))
+        if math == "planes":
+            rp.check(lib().rp_op_conv3x3_planes(n, h, w, c, c, P(xp.data_ptr()), P(wt.data_ptr()), 0, P(b.data_ptr()),
+                                                None, 1.0, 1, P(out.data_ptr()), P(op.data_ptr()), P(ws.data_ptr()),
+                                                wsb, None))
+        else:
+            rp.check(lib().rp_op_conv3x3(n, h, w, c, c, P(x.data_ptr()), P(wt.data_ptr()), 0, P(b.data_ptr()), None,
+                                         1.0, 1, P(out.data_ptr()), rp.MATH[math], P(ws.data_ptr()), wsb, None))
         torch.cuda.synchronize()
     L.rp_debug_set_trace(None)
     t = tr.cpu().numpy().reshape(2, 64, 8)
