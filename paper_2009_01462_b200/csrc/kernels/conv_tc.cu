@@ -50,6 +50,7 @@ using namespace rp::umma;
 
 constexpr int kThreads = 480;       // w0 halo TMA, w1 MMA, w2-5 converters, w6-13 epilogue, w14 weight TMA
 constexpr int kWStages = 3;          // one weight stage = one filter row (3 taps) of one chunk
+constexpr int kWMax = 8;             // barrier slots for the weight ring (PLANES: up to 8 stages)
 constexpr int kChunk = 16;           // input channels per halo chunk
 constexpr bool kUseCollector = false;  // A-operand collector reuse, tf32 modes (measured: no gain)
 #ifndef RP_CONV_COLLECTOR_BF
@@ -76,6 +77,7 @@ struct TcArgs {
   uint32_t plane_bytes; // X3BF16: one bf16 plane of the halo chunk (halo_pos x 32 B)
   uint32_t raw_stride;  // X3BF16: bytes per raw fp32 halo slot ([pos][16 ch], TMA target)
   int raw_slots;        // X3BF16: depth of the raw ring (2 or 3); PLANES: halo slots (2..4)
+  int wstages;          // depth of the weight ring (<= kWMax)
   float h;
   const float* w;       // prepped [chunk][tap][kg][128 rows][4]
   const float* bias;
@@ -84,6 +86,7 @@ struct TcArgs {
   __nv_bfloat16* p0;           // optional bf16 plane pair of out: p0 = bf16(o), p1 = bf16(o - p0)
   __nv_bfloat16* p1;
   unsigned long long* trace;   // diagnostics (tools/trace_conv.py): per-unit timestamps, null = off
+  int dbg;                     // diagnostics (RP_CONV_DBG): 1 no epilogue, 2 no halo TMA, 4 no weight TMA, 8 no MMA
 };
 
 __device__ __forceinline__ float rna_tf32(float v) {
@@ -211,19 +214,20 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint8_t* halo_base = smem;
   uint8_t* raw_base = smem + 2 * a.halo_stride;               // X3BF16 only
   uint8_t* w_base = smem + hslots * a.halo_stride + (BF ? a.raw_slots * a.raw_stride : 0u);   // kWStages stages
-  float* xchg = reinterpret_cast<float*>(w_base + kWStages * w_stage);   // [2 groups][hi, lo][32 pos][64 ch]
+  const int wst = a.wstages;
+  float* xchg = reinterpret_cast<float*>(w_base + wst * w_stage);   // [2 groups][hi, lo][32 pos][64 ch]
   uint64_t* bars = reinterpret_cast<uint64_t*>(xchg + 2 * 2 * 2 * 32 * 32);
   uint64_t* halo_full = bars;        // [4]
   uint64_t* halo_conv = bars + 4;    // [4]
   uint64_t* halo_empty = bars + 8;   // [4]
-  uint64_t* w_full = bars + 12;      // [kWStages]
-  uint64_t* w_empty = bars + 12 + kWStages;
-  uint64_t* acc_full = bars + 12 + 2 * kWStages;   // [2]
-  uint64_t* acc_empty = bars + 14 + 2 * kWStages;  // [2]
-  uint64_t* raw_full = bars + 16 + 2 * kWStages;   // [3] X3BF16: TMA -> converters
-  uint64_t* raw_empty = bars + 19 + 2 * kWStages;  // [3] X3BF16: converters -> TMA
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 22 + 2 * kWStages);
-  int* pos_tab = reinterpret_cast<int*>(bars + 32);   // [2 groups][128] epilogue position -> NHWC offset
+  uint64_t* w_full = bars + 12;      // [kWMax]
+  uint64_t* w_empty = bars + 12 + kWMax;
+  uint64_t* acc_full = bars + 12 + 2 * kWMax;   // [2]
+  uint64_t* acc_empty = bars + 14 + 2 * kWMax;  // [2]
+  uint64_t* raw_full = bars + 16 + 2 * kWMax;   // [3] X3BF16: TMA -> converters
+  uint64_t* raw_empty = bars + 19 + 2 * kWMax;  // [3] X3BF16: converters -> TMA
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 22 + 2 * kWMax);
+  int* pos_tab = reinterpret_cast<int*>(bars + 64);   // [2 groups][128] epilogue position -> NHWC offset
 
   constexpr bool THREE = MODE != MODE_TF32;
   auto halo_raw = [&](int s) { return halo_base + s * a.halo_stride + 128; };
@@ -245,7 +249,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_init(&acc_full[i], 1);
       mbar_init(&acc_empty[i], 256);
     }
-    for (int i = 0; i < kWStages; ++i) {
+    for (int i = 0; i < kWMax; ++i) {
       mbar_init(&w_full[i], 1);
       mbar_init(&w_empty[i], 1);
     }
@@ -301,9 +305,11 @@ __global__ void __launch_bounds__(kThreads, 1)
             tma_load_4d(&tmap, &raw_full[hs], raw_slot(hs), kChunk * c, -1, y0 - 1, n);
           } else if constexpr (PL) {
             // both planes of the chunk: images [0, N) are plane 0, [N, 2N) plane 1
+            if (a.dbg & 2) { mbar_arrive(&halo_full[hs]); } else {
             mbar_arrive_expect_tx(&halo_full[hs], 2 * a.plane_bytes);
             tma_load_5d(&tmap, &halo_full[hs], plane(hs, 0), 0, -1, y0 - 1, 2 * c, n);
             tma_load_5d(&tmap, &halo_full[hs], plane(hs, 1), 0, -1, y0 - 1, 2 * c, n + a.N);
+            }
           } else {
             mbar_arrive_expect_tx(&halo_full[hs], a.halo_bytes);
             tma_load_5d(&tmap, &halo_full[hs], halo_raw(hs), 0, -1, y0 - 1, 4 * c, n);
@@ -326,17 +332,20 @@ __global__ void __launch_bounds__(kThreads, 1)
         for (int dy = 0; dy < 3; ++dy) {
           mbar_wait(&w_empty[ws], wph ^ 1);
           if (elect_one()) {
+            if (a.dbg & 4) { mbar_arrive(&w_full[ws]); } else {
             mbar_arrive_expect_tx(&w_full[ws], wbytes);
             bulk_load(w_s(ws), wcb + ((int64_t)c * 9 + 3 * dy) * a.w_tap, wbytes, &w_full[ws]);
+            }
           }
           __syncwarp();
-          if (++ws == kWStages) ws = 0, wph ^= 1;
+          if (++ws == wst) ws = 0, wph ^= 1;
         }
       }
     }
   } else if (warp == 1) {
     // ===================== MMA issuer =====================
     const uint32_t id = BFL ? idesc(1, 128, 128) : idesc(2, 128, 128);
+    const uint32_t id256 = idesc(1, 128, 256);
     const uint32_t kg_x = (uint32_t)a.halo_pos * 16u;     // bytes between channel groups (halo)
     const uint32_t kg_w = 128u * 16u;                     // bytes between channel groups (weights)
     const uint64_t xj = (uint64_t)((2 * kg_x) >> 4);      // K-step (8 channels) of B, 16-byte units
@@ -378,16 +387,16 @@ __global__ void __launch_bounds__(kThreads, 1)
           if (PL) {
             // 16 channels = one K = 16 step; A = [W0; W1] (bf16), B = planes x0, x1
             if (elect_one()) {
+              if (!(a.dbg & 8))
 #pragma unroll
               for (int dx = 0; dx < 3; ++dx) {
                 const uint64_t da = dw0 + dx * wtap;
                 const uint32_t accum = (first && dx == 0) ? 0u : 1u;
-                mma_f16_c<1>(d0, da, bh + dx, id, accum);
-                if (ntiles > 1) {
-                  mma_f16_c<2>(d0, da, bl + dx, id, 1u);
-                  mma_f16_c<2>(d0 + 128, da, bh + dx + 128, id, accum);
-                  mma_f16_c<3>(d0 + 128, da, bl + dx + 128, id, 1u);
+                if (ntiles > 1) {   // both tiles (256 consecutive positions) in one N = 256 MMA
+                  mma_f16_c<1>(d0, da, bh + dx, id256, accum);
+                  mma_f16_c<3>(d0, da, bl + dx, id256, 1u);
                 } else {
+                  mma_f16_c<1>(d0, da, bh + dx, id, accum);
                   mma_f16_c<3>(d0, da, bl + dx, id, 1u);
                 }
               }
@@ -458,7 +467,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             mma_commit(&w_empty[ws]);
           }
           __syncwarp();
-          if (++ws == kWStages) ws = 0, wph ^= 1;
+          if (++ws == wst) ws = 0, wph ^= 1;
         }
         if (elect_one()) mma_commit(&halo_empty[hs]);
         __syncwarp();
@@ -564,7 +573,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_wait(&acc_full[ab], aph);
       tc_fence_after();
       if (a.trace && blockIdx.x < 2 && threadIdx.x == 192) a.trace[(blockIdx.x * 64 + min(u, 63)) * 8 + 2] = globaltimer_ns();
-      if (grp < ntiles) {
+      if (grp < ntiles && !(a.dbg & 1)) {
         {
           const int f = (tile0 + grp) * 128 + gtid;
           const int y = f / Wp, X = f - y * Wp;
@@ -772,7 +781,7 @@ struct Plan {
   bool ok = false;
   int Wp, rows_h, halo_pos, T, units_per_img;
   uint32_t halo_bytes, w_tap, halo_stride, plane_bytes, raw_stride = 0;
-  int raw_slots = 0;
+  int raw_slots = 0, wstages = kWStages;
   size_t smem;
 };
 
@@ -787,14 +796,19 @@ Plan plan_for(const ConvShape& s, int mode = MODE_X3TF32) {
   p.units_per_img = (p.T + kS - 1) / kS;
   p.halo_bytes = (uint32_t)p.halo_pos * 64u;
   p.plane_bytes = (uint32_t)p.halo_pos * 32u;
-  const size_t fixed_bytes = 2 * 2 * 2 * 32 * 32 * 4 + 256 + 1024 + 1024;   // xchg + barriers + table + alignment
+  const size_t fixed_bytes = 2 * 2 * 2 * 32 * 32 * 4 + 512 + 1024 + 1024;   // xchg + barriers + table + alignment
   if (mode == MODE_PLANES) {
     p.w_tap = 128u * kChunk * 2u;
     p.halo_stride = (128 + 2 * (p.plane_bytes + 255) + 1023) / 1024 * 1024;   // plane-pair slot (128 B pitch)
-    const size_t base = kWStages * 3 * (size_t)p.w_tap + fixed_bytes;
-    p.raw_slots = 4;
-    while (p.raw_slots > 2 && base + p.raw_slots * (size_t)p.halo_stride > (size_t)kMaxSmem) --p.raw_slots;
-    p.smem = base + p.raw_slots * (size_t)p.halo_stride;
+    // deepest weight ring first (the weight stream is the one the MMA waits on), then the
+    // most halo slots that still fit
+    p.ok = false;
+    for (int wst = 6; wst >= kWStages && !p.ok; --wst)
+      for (int hs = 4; hs >= 2 && !p.ok; --hs) {
+        const size_t need = wst * 3 * (size_t)p.w_tap + fixed_bytes + hs * (size_t)p.halo_stride;
+        if (need <= (size_t)kMaxSmem) p.wstages = wst, p.raw_slots = hs, p.smem = need, p.ok = true;
+      }
+    if (!p.ok) return p;
   } else if (mode == MODE_X3BF16) {
     p.w_tap = 128u * kChunk * 2u;
     p.halo_stride = (128 + 3 * (p.plane_bytes + 255) + 1023) / 1024 * 1024;   // plane slot (128 B pitch)
@@ -900,6 +914,7 @@ void conv3x3_fwd_tc(const ConvShape& s, const float* in, const float* w_hwio, bo
   a.plane_bytes = p.plane_bytes;
   a.raw_stride = p.raw_stride;
   a.raw_slots = p.raw_slots;
+  a.wstages = p.wstages;
   a.h = h;
   a.w = wp;
   a.bias = bias;
@@ -908,6 +923,11 @@ void conv3x3_fwd_tc(const ConvShape& s, const float* in, const float* w_hwio, bo
   a.p0 = static_cast<__nv_bfloat16*>(out_planes);
   a.p1 = out_planes ? a.p0 + s.pixels() * s.co : nullptr;
   a.trace = g_trace;
+  static const int dbg = [] {
+    const char* e = std::getenv("RP_CONV_DBG");
+    return e ? std::atoi(e) : 0;
+  }();
+  a.dbg = dbg;
   const CUtensorMap& m = mode == MODE_PLANES ? cached_map(in_planes, s, p.Wp, p.rows_h, 2)
                                               : cached_map(in, s, p.Wp, p.rows_h, mode == MODE_X3BF16 ? 1 : 0);
   const int grid = std::min(a.num_tiles, kNumSMs);

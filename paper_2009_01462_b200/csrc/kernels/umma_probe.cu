@@ -211,6 +211,9 @@ __global__ void __launch_bounds__(128, 1) umma_bench_kernel(int fmt, int N, int 
     } else if (layout == 3) {            // as layout 1 with the wgrad kernel's slab strides
       da = umma::desc_general(a0, 9216, 512, 1, 0);
       db = umma::desc_general(umma::smem_u32(sm + 40 * 1024) + 1024, 18432, 512, 1, 0);
+    } else if (layout == 6) {            // SW32 K-major: 8 rows x 32 B atoms, sbo = 256
+      da = umma::desc_general(a0, 16, 256, 6, 0);
+      db = umma::desc_general(b0, 16, 256, 6, 0);
     } else {            // SW128 K-major: sbo = 1024
       da = umma::desc_general(a0, 16, 1024, layout, 0);
       db = umma::desc_general(b0, 16, 1024, layout, 0);
@@ -218,7 +221,25 @@ __global__ void __launch_bounds__(128, 1) umma_bench_kernel(int fmt, int N, int 
     const uint32_t id = umma::idesc(fmt, layout == 4 ? 64 : 128, N, a_mn, b_mn);
     const uint32_t tm = __shfl_sync(0xffffffffu, tmem, 0);
     const long long t0 = clock64();
-    if (nops == 98) {
+    if (nops == 86 || nops == 85) {
+      // bf16: A reused by 4 MMAs (86: collector fill/use/use/lastuse, 85: plain), B rotating
+      for (int r = 0; r < reps; r += 4) {
+        if (umma::elect_one()) {
+          if (nops == 86) {
+            umma::mma_f16_c<1>(tm, da, db, id, r > 0);
+            umma::mma_f16_c<2>(tm + N, da, db + 256, id, r > 0);
+            umma::mma_f16_c<2>(tm, da, db + 512, id, 1);
+            umma::mma_f16_c<3>(tm + N, da, db + 768, id, 1);
+          } else {
+            umma::mma_f16(tm, da, db, id, r > 0);
+            umma::mma_f16(tm + N, da, db + 256, id, r > 0);
+            umma::mma_f16(tm, da, db + 512, id, 1);
+            umma::mma_f16(tm + N, da, db + 768, id, 1);
+          }
+        }
+        __syncwarp();
+      }
+    } else if (nops == 98) {
       // A reused by 4 MMAs (collector fill/use/use/lastuse), B rotating over 4 regions
       for (int r = 0; r < reps; r += 4) {
         if (umma::elect_one()) {
