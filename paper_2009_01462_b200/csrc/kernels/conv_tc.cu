@@ -58,7 +58,10 @@ constexpr bool kUseCollector = false;  // A-operand collector reuse, tf32 modes 
 #endif
 constexpr bool kUseCollectorBF = RP_CONV_COLLECTOR_BF;   // X3BF16: A reuse across the 6 MMAs of a tap
 constexpr int kS = 2;                // 128-position tiles per unit
-constexpr int kMaxSmem = 220 * 1024;
+constexpr int kEpiB = 8;             // epilogue batch (positions per TMEM load / exchange)
+constexpr int kMaxSmem = 220 * 1024;      // streaming plans
+constexpr int kMaxSmemRes = 227 * 1024;   // resident-weight plan (the sm_100 per-CTA maximum)
+constexpr int kWResMax = 12;              // resident weight stages (Ci = 64: 4 chunks x 3 filter rows)
 
 // Operand modes: TF32 (x and W truncated to tf32), X3TF32 ([W_hi; W_lo] x {x_hi, x_lo}) and
 // X3BF16 (the default fp32-accurate path, capi_ops.cu fp32_split) ([W0; W1] x {x0, x1, x2} with bf16 splits: W to
@@ -77,7 +80,8 @@ struct TcArgs {
   uint32_t plane_bytes; // X3BF16: one bf16 plane of the halo chunk (halo_pos x 32 B)
   uint32_t raw_stride;  // X3BF16: bytes per raw fp32 halo slot ([pos][16 ch], TMA target)
   int raw_slots;        // X3BF16: depth of the raw ring (2 or 3); PLANES: halo slots (2..4)
-  int wstages;          // depth of the weight ring (<= kWMax)
+  int wstages;          // depth of the weight ring (<= kWMax); resident: stages of the whole filter
+  int resident;         // PLANES, Co = 64: the co block's whole prepped filter stays in shared memory
   float h;
   const float* w;       // prepped [chunk][tap][kg][128 rows][4]
   const float* bias;
@@ -215,8 +219,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint8_t* raw_base = smem + 2 * a.halo_stride;               // X3BF16 only
   uint8_t* w_base = smem + hslots * a.halo_stride + (BF ? a.raw_slots * a.raw_stride : 0u);   // kWStages stages
   const int wst = a.wstages;
-  float* xchg = reinterpret_cast<float*>(w_base + wst * w_stage);   // [2 groups][hi, lo][32 pos][64 ch]
-  uint64_t* bars = reinterpret_cast<uint64_t*>(xchg + 2 * 2 * 2 * 32 * 32);
+  float* xchg = reinterpret_cast<float*>(w_base + wst * w_stage);   // [2 groups][hi, lo][kEpiB pos][64 ch]
+  uint64_t* bars = reinterpret_cast<uint64_t*>(xchg + 2 * 2 * kEpiB * 64);
   uint64_t* halo_full = bars;        // [4]
   uint64_t* halo_conv = bars + 4;    // [4]
   uint64_t* halo_empty = bars + 8;   // [4]
@@ -324,9 +328,19 @@ __global__ void __launch_bounds__(kThreads, 1)
     int ws = 0;
     uint32_t wph = 0;
     const uint32_t wbytes = 3 * a.w_tap;
+    if (a.resident) {
+      // the whole filter of the single co block, once per launch (stage c * 3 + dy = slot c * 3 + dy):
+      // the per-unit weight stream was ~16 B/clk/SM of L2 traffic on top of the halo and the epilogue
+      if (elect_one()) {
+        mbar_arrive_expect_tx(&w_full[0], (uint32_t)wst * wbytes);
+        for (int i = 0; i < wst; ++i)
+          bulk_load(w_s(i), reinterpret_cast<const uint8_t*>(a.w) + (int64_t)i * wbytes, wbytes, &w_full[0]);
+      }
+      __syncwarp();
+    }
     UnitIter it(a.Co / 64, a.N, a.T);
     int cb, n, tile0, ntiles;
-    while (it.next(cb, n, tile0, ntiles)) {
+    while (!a.resident && it.next(cb, n, tile0, ntiles)) {
       const uint8_t* wcb = reinterpret_cast<const uint8_t*>(a.w) + (int64_t)cb * a.nchunks * 9 * a.w_tap;
       for (int c = 0; c < a.nchunks; ++c) {
         for (int dy = 0; dy < 3; ++dy) {
@@ -345,7 +359,6 @@ __global__ void __launch_bounds__(kThreads, 1)
   } else if (warp == 1) {
     // ===================== MMA issuer =====================
     const uint32_t id = BFL ? idesc(1, 128, 128) : idesc(2, 128, 128);
-    const uint32_t id256 = idesc(1, 128, 256);
     const uint32_t kg_x = (uint32_t)a.halo_pos * 16u;     // bytes between channel groups (halo)
     const uint32_t kg_w = 128u * 16u;                     // bytes between channel groups (weights)
     const uint64_t xj = (uint64_t)((2 * kg_x) >> 4);      // K-step (8 channels) of B, 16-byte units
@@ -355,10 +368,16 @@ __global__ void __launch_bounds__(kThreads, 1)
     uint32_t hph = 0, wph = 0, aph = 0;
     UnitIter it(a.Co / 64, a.N, a.T);
     int cb, n, tile0, ntiles, ui = 0;
+    if (a.resident) {   // unconditionally: a CTA without units must not exit with the load in flight
+      mbar_wait(&w_full[0], 0);
+      tc_fence_after();
+    }
     while (it.next(cb, n, tile0, ntiles)) {                   // warp-uniform
       const int u = ui++;
       const int f0 = tile0 * 128;
       const int c0 = f0 - (f0 / Wp) * Wp;
+      const int nvalid = min(ntiles * 128, a.H * Wp - f0);              // frame positions of the unit
+      const uint32_t id_unit = idesc(1, 128, (nvalid + 15) / 16 * 16);  // PLANES: N = 16 .. 256
       mbar_wait(&acc_empty[ab], aph ^ 1);
       tc_fence_after();
       if (a.trace && blockIdx.x < 2 && lane == 0 && u < 64) a.trace[(blockIdx.x * 64 + u) * 8 + 0] = globaltimer_ns();
@@ -375,7 +394,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         const uint64_t dxq0 = desc_kmajor_interleave(smem_u32(plane(hs, BF ? 2 : 0)), kg_x, 128);
         for (int dy = 0; dy < 3; ++dy) {
           long long tw2 = a.trace ? clock64() : 0;
-          mbar_wait(&w_full[ws], wph);
+          if (!a.resident) mbar_wait(&w_full[ws], wph);
           if (a.trace) wait_w += clock64() - tw2;
           tc_fence_after();
           const uint64_t dw0 = desc_kmajor_interleave(smem_u32(w_s(ws)), kg_w, 128);
@@ -385,22 +404,19 @@ __global__ void __launch_bounds__(kThreads, 1)
           const uint64_t bq = dxq0 + (uint64_t)row;
           const bool first = (c == 0 && dy == 0);
           if (PL) {
-            // 16 channels = one K = 16 step; A = [W0; W1] (bf16), B = planes x0, x1
+            // 16 channels = one K = 16 step; A = [W0; W1] (bf16), B = planes x0, x1.  One MMA
+            // spans the unit's frame positions (N = 256 for two tiles; the image's last tile
+            // only as far as the frame goes, e.g. 64 of 128 positions at 32x32)
             if (elect_one()) {
               if (!(a.dbg & 8))
 #pragma unroll
               for (int dx = 0; dx < 3; ++dx) {
                 const uint64_t da = dw0 + dx * wtap;
                 const uint32_t accum = (first && dx == 0) ? 0u : 1u;
-                if (ntiles > 1) {   // both tiles (256 consecutive positions) in one N = 256 MMA
-                  mma_f16_c<1>(d0, da, bh + dx, id256, accum);
-                  mma_f16_c<3>(d0, da, bl + dx, id256, 1u);
-                } else {
-                  mma_f16_c<1>(d0, da, bh + dx, id, accum);
-                  mma_f16_c<3>(d0, da, bl + dx, id, 1u);
-                }
+                mma_f16_c<1>(d0, da, bh + dx, id_unit, accum);
+                mma_f16_c<3>(d0, da, bl + dx, id_unit, 1u);
               }
-              mma_commit(&w_empty[ws]);
+              if (!a.resident) mma_commit(&w_empty[ws]);
             }
           } else if (BF) {
             // 16 channels = one K = 16 step; A = [W0; W1] (bf16), B = planes x0, x1, x2
@@ -544,20 +560,23 @@ __global__ void __launch_bounds__(kThreads, 1)
     // ===================== epilogue =====================
     // Two groups of 4 warps; group g finishes tile s = g of every unit (both tiles of a unit
     // drain in parallel).  D row r: r < 64 -> W_hi (W0) products for co = r, r >= 64 ->
-    // W_lo (W1) products for co = r - 64.  Per batch of 32 positions every warp moves its
-    // 32 rows (TMEM lane quadrant) to shared memory as [hi|lo][position][64 ch]; the group
-    // then reads it back transposed -- a thread owns 4 consecutive channels of a position --
-    // and finishes hi + lo, the fused epilogue and the stores with 16-byte vectors
-    // (coalesced NHWC rows).  Frame position -> NHWC offset comes from a per-tile table.
+    // W_lo (W1) products for co = r - 64.  Batches of 8 positions: every warp moves its 32
+    // rows (TMEM lane quadrant) to shared memory as [hi|lo][position][64 ch]; the group then
+    // reads it back transposed -- thread t owns channels 4 (t & 15) .. +3 of position t >> 4
+    // -- and finishes hi + lo, the fused epilogue and the stores with 16-byte vectors
+    // (coalesced NHWC rows).  The small exchange buffer (8 KB for both groups) is what lets
+    // the resident-weight plan keep three halo slots; the tile's aux operand (16 float4 per
+    // thread) is loaded before the first batch, so a tile pays one memory latency.  Frame
+    // position -> NHWC offset comes from a per-tile table.
     const int q = warp & 3;                 // TMEM lane quadrant this warp may access
     const int grp = (warp - 6) >> 2;        // tile of the unit this warp drains
     const int gtid = (int)threadIdx.x - 192 - grp * 128;
     constexpr bool kBias = EPI == EPI_BIAS || EPI == EPI_BIAS_TANH || EPI == EPI_RESID;
     constexpr bool kAux = EPI == EPI_RESID || EPI == EPI_TANH_BWD || EPI == EPI_ADD;
-    float* buf = xchg + grp * 2 * 32 * 64;                // [2: hi, lo][32 positions][64 ch]
-    float* wrow = buf + (q >> 1) * 32 * 64 + (q & 1) * 32 + lane;   // this lane's channel column
+    float* buf = xchg + grp * 2 * kEpiB * 64;                  // [2: hi, lo][kEpiB positions][64 ch]
+    float* wrow = buf + (q >> 1) * kEpiB * 64 + (q & 1) * 32 + lane;   // this lane's channel column
     const int c4 = gtid & 15;                             // channels 4 c4 .. 4 c4 + 3 (read-back)
-    const int prow = gtid >> 4;                           // positions prow + 8 j (read-back)
+    const int prow = gtid >> 4;                           // position prow of each batch
     int* tab = pos_tab + grp * 128;
     const uint32_t grp_bar = 6 + grp;                     // the group (128 threads)
     int ab = 0;
@@ -579,6 +598,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           const int y = f / Wp, X = f - y * Wp;
           asm volatile("bar.sync %0, 128;" ::"r"(grp_bar) : "memory");   // the last tile's readers are done
           tab[gtid] = (y < a.H && X >= 1 && X <= a.W) ? (y * a.W + (X - 1)) * a.Co : -1;
+          asm volatile("bar.sync %0, 128;" ::"r"(grp_bar) : "memory");   // table visible
         }
         const uint32_t tcol = tmem_base + ((uint32_t)(q * 32) << 16) + (uint32_t)((ab * kS + grp) * 128);
         const float* auxb = kAux ? a.aux + img * a.Co + co : nullptr;
@@ -586,54 +606,55 @@ __global__ void __launch_bounds__(kThreads, 1)
         const bool planes = a.p0 != nullptr;
         __nv_bfloat16* p0b = planes ? a.p0 + img * a.Co + co : nullptr;
         __nv_bfloat16* p1b = planes ? a.p1 + img * a.Co + co : nullptr;
-        for (int pb = 0; pb < 128; pb += 32) {
-          uint32_t r[32];
-          tmem_ld16(tcol + (uint32_t)pb, *reinterpret_cast<uint32_t(*)[16]>(&r[0]));
-          tmem_ld16(tcol + (uint32_t)pb + 16, *reinterpret_cast<uint32_t(*)[16]>(&r[16]));
-          tmem_wait_ld();
-          asm volatile("bar.sync %0, 128;" ::"r"(grp_bar) : "memory");   // buf free (and tab written)
+        const int fvalid = a.H * Wp - (tile0 + grp) * 128;   // frame positions left in this tile
+        const int nb = min(128 / kEpiB, (fvalid + kEpiB - 1) / kEpiB);   // batches with frame positions
+        float4 ax[128 / kEpiB];
+        if constexpr (kAux) {
 #pragma unroll
-          for (int e = 0; e < 32; ++e) wrow[e * 64] = __uint_as_float(r[e]);
-          asm volatile("bar.sync %0, 128;" ::"r"(grp_bar) : "memory");
-          int off[4];
-          float4 ax[4];
-#pragma unroll
-          for (int j = 0; j < 4; ++j) off[j] = tab[pb + prow + 8 * j];
-          if constexpr (kAux) {
-#pragma unroll
-            for (int j = 0; j < 4; ++j)
-              ax[j] = off[j] >= 0 ? *reinterpret_cast<const float4*>(auxb + off[j]) : make_float4(0.f, 0.f, 0.f, 0.f);
+          for (int b = 0; b < 128 / kEpiB; ++b) {
+            const int o = b < nb ? tab[b * kEpiB + prow] : -1;
+            ax[b] = o >= 0 ? __ldg(reinterpret_cast<const float4*>(auxb + o)) : make_float4(0.f, 0.f, 0.f, 0.f);
           }
+        }
 #pragma unroll
-          for (int j = 0; j < 4; ++j) {
-            if (off[j] < 0) continue;
-            const int pr = prow + 8 * j;
-            const float4 hv = *reinterpret_cast<const float4*>(buf + pr * 64 + 4 * c4);
-            const float4 lv = *reinterpret_cast<const float4*>(buf + 32 * 64 + pr * 64 + 4 * c4);
-            const float v[4] = {hv.x + lv.x, hv.y + lv.y, hv.z + lv.z, hv.w + lv.w};
-            const float bb[4] = {bias.x, bias.y, bias.z, bias.w};
-            const float xa[4] = {ax[j].x, ax[j].y, ax[j].z, ax[j].w};
-            float o[4];
+        for (int b = 0; b < 128 / kEpiB; ++b) {
+          if (b < nb) {   // group-uniform
+            uint32_t r[kEpiB];
+            tmem_ld8(tcol + (uint32_t)(b * kEpiB), r);
+            tmem_wait_ld();
+            asm volatile("bar.sync %0, 128;" ::"r"(grp_bar) : "memory");   // buf free
 #pragma unroll
-            for (int i = 0; i < 4; ++i) {
-              if constexpr (EPI == EPI_BIAS) o[i] = v[i] + bb[i];
-              else if constexpr (EPI == EPI_BIAS_TANH) o[i] = tanhf(v[i] + bb[i]);
-              else if constexpr (EPI == EPI_RESID) o[i] = xa[i] + a.h * (v[i] + bb[i]);
-              else if constexpr (EPI == EPI_TANH_BWD) o[i] = (a.h * v[i]) * (1.f - xa[i] * xa[i]);
-              else if constexpr (EPI == EPI_ADD) o[i] = xa[i] + v[i];
-              else o[i] = a.h * v[i];
-            }
-            *reinterpret_cast<float4*>(outb + off[j]) = make_float4(o[0], o[1], o[2], o[3]);
-            if (planes) {
-              uint32_t h[2], l[2];
+            for (int e = 0; e < kEpiB; ++e) wrow[e * 64] = __uint_as_float(r[e]);
+            asm volatile("bar.sync %0, 128;" ::"r"(grp_bar) : "memory");
+            const int off = tab[b * kEpiB + prow];
+            if (off >= 0) {
+              const float4 hv = *reinterpret_cast<const float4*>(buf + prow * 64 + 4 * c4);
+              const float4 lv = *reinterpret_cast<const float4*>(buf + kEpiB * 64 + prow * 64 + 4 * c4);
+              const float v[4] = {hv.x + lv.x, hv.y + lv.y, hv.z + lv.z, hv.w + lv.w};
+              const float bb[4] = {bias.x, bias.y, bias.z, bias.w};
+              const float xa[4] = {ax[b].x, ax[b].y, ax[b].z, ax[b].w};
+              float o[4];
 #pragma unroll
-              for (int i = 0; i < 2; ++i) {
-                const __nv_bfloat162 hh = __floats2bfloat162_rn(o[2 * i], o[2 * i + 1]);
-                h[i] = *reinterpret_cast<const uint32_t*>(&hh);
-                l[i] = pack_bf16x2(o[2 * i] - __low2float(hh), o[2 * i + 1] - __high2float(hh));
+              for (int i = 0; i < 4; ++i) {
+                if constexpr (EPI == EPI_BIAS) o[i] = v[i] + bb[i];
+                else if constexpr (EPI == EPI_BIAS_TANH) o[i] = tanhf(v[i] + bb[i]);
+                else if constexpr (EPI == EPI_RESID) o[i] = xa[i] + a.h * (v[i] + bb[i]);
+                else if constexpr (EPI == EPI_TANH_BWD) o[i] = (a.h * v[i]) * (1.f - xa[i] * xa[i]);
+                else if constexpr (EPI == EPI_ADD) o[i] = xa[i] + v[i];
+                else o[i] = a.h * v[i];
               }
-              *reinterpret_cast<uint2*>(p0b + off[j]) = make_uint2(h[0], h[1]);
-              *reinterpret_cast<uint2*>(p1b + off[j]) = make_uint2(l[0], l[1]);
+              *reinterpret_cast<float4*>(outb + off) = make_float4(o[0], o[1], o[2], o[3]);
+              if (planes) {
+                uint32_t h[2], l[2];
+#pragma unroll
+                for (int i = 0; i < 2; ++i) {
+                  const __nv_bfloat162 hh = __floats2bfloat162_rn(o[2 * i], o[2 * i + 1]);
+                  h[i] = *reinterpret_cast<const uint32_t*>(&hh);
+                  l[i] = pack_bf16x2(o[2 * i] - __low2float(hh), o[2 * i + 1] - __high2float(hh));
+                }
+                *reinterpret_cast<uint2*>(p0b + off) = make_uint2(h[0], h[1]);
+                *reinterpret_cast<uint2*>(p1b + off) = make_uint2(l[0], l[1]);
+              }
             }
           }
         }
@@ -644,7 +665,6 @@ __global__ void __launch_bounds__(kThreads, 1)
       if (++ab == 2) ab = 0, aph ^= 1;
     }
   }
-
   tc_fence_before();
   __syncthreads();
   if (warp == 1) {
@@ -782,6 +802,7 @@ struct Plan {
   int Wp, rows_h, halo_pos, T, units_per_img;
   uint32_t halo_bytes, w_tap, halo_stride, plane_bytes, raw_stride = 0;
   int raw_slots = 0, wstages = kWStages;
+  bool resident = false;
   size_t smem;
 };
 
@@ -796,10 +817,26 @@ Plan plan_for(const ConvShape& s, int mode = MODE_X3TF32) {
   p.units_per_img = (p.T + kS - 1) / kS;
   p.halo_bytes = (uint32_t)p.halo_pos * 64u;
   p.plane_bytes = (uint32_t)p.halo_pos * 32u;
-  const size_t fixed_bytes = 2 * 2 * 2 * 32 * 32 * 4 + 512 + 1024 + 1024;   // xchg + barriers + table + alignment
+  const size_t fixed_bytes = 2 * 2 * kEpiB * 64 * 4 + 512 + 1024;   // xchg + barriers + table
   if (mode == MODE_PLANES) {
     p.w_tap = 128u * kChunk * 2u;
     p.halo_stride = (128 + 2 * (p.plane_bytes + 255) + 1023) / 1024 * 1024;   // plane-pair slot (128 B pitch)
+    // resident filter (one co block, every (chunk, filter row) stage) + 3 halo slots (2 if short)
+    const int nst = 3 * (s.ci / kChunk);
+    const int res_slots = nst * 3 * (size_t)p.w_tap + fixed_bytes + 3 * (size_t)p.halo_stride <= (size_t)kMaxSmemRes ? 3 : 2;
+    const size_t need_res = nst * 3 * (size_t)p.w_tap + fixed_bytes + res_slots * (size_t)p.halo_stride;
+    static const bool res_off = [] {
+      const char* e = std::getenv("RP_CONV_RESIDENT");
+      return e && e[0] == '0';
+    }();
+    if (!res_off && s.co == 64 && nst <= kWResMax && need_res <= (size_t)kMaxSmemRes) {
+      p.resident = true;
+      p.wstages = nst;
+      p.raw_slots = res_slots;
+      p.smem = need_res;
+      p.ok = true;
+      return p;
+    }
     // deepest weight ring first (the weight stream is the one the MMA waits on), then the
     // most halo slots that still fit
     p.ok = false;
@@ -849,7 +886,7 @@ void launch_cfg(const CUtensorMap& m, const TcArgs& a, size_t smem, int grid, cu
   static bool configured = false;
   if (!configured) {
     RP_CUDA(cudaFuncSetAttribute(conv3x3_tc_kernel<EPI, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 kMaxSmem));
+                                 kMaxSmemRes));
     configured = true;
   }
   conv3x3_tc_kernel<EPI, MODE><<<grid, kThreads, smem, st>>>(m, a);
@@ -915,6 +952,7 @@ void conv3x3_fwd_tc(const ConvShape& s, const float* in, const float* w_hwio, bo
   a.raw_stride = p.raw_stride;
   a.raw_slots = p.raw_slots;
   a.wstages = p.wstages;
+  a.resident = p.resident ? 1 : 0;
   a.h = h;
   a.w = wp;
   a.bias = bias;

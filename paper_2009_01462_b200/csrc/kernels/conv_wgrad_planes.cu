@@ -43,7 +43,7 @@ struct PwArgs {
   int mo, mi;                    // 64-channel co / ci blocks
   int blocks_per_img, num_blocks;
   uint32_t g_slab;               // bytes per bf16 g plane slab (Pp rows x 128 B, 1 KB aligned)
-  uint32_t x_slab;               // bytes per bf16 x plane slab ((rg+2)*Wp rows, packed)
+  uint32_t x_slab;               // bytes per bf16 x plane slab (rg * Wp rows of one filter row, packed)
   uint32_t x_off;
   uint32_t stage;
   float* part;                   // [grid][kTg * 64 (ci)][64 (co)]
@@ -84,7 +84,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int blk_end = (int)((int64_t)(jg + 1) * a.num_blocks / ng);
   const int t0 = gi * kTg;
   const int Wp = a.Wp;
-  const int xrows = (a.rg + 2) * Wp;
+  const int xrows = a.rg * Wp;   // x rows of this tap group's filter row only (y0 - 1 + gi ..)
   const bool do_bias = gi == 0 && cib == 0;
 
   if (threadIdx.x == 0) {
@@ -126,8 +126,8 @@ __global__ void __launch_bounds__(kThreads, 1)
         mbar_arrive_expect_tx(&full[s], bytes);
         tma_load_4d(&tg0, &full[s], g_slab(s, 0), 64 * cob, -1, y0, n);
         tma_load_4d(&tg1, &full[s], g_slab(s, 1), 64 * cob, -1, y0, n);
-        tma_load_4d(&tx0, &full[s], x_slab(s, 0), 64 * cib, -1, y0 - 1, n);
-        tma_load_4d(&tx1, &full[s], x_slab(s, 1), 64 * cib, -1, y0 - 1, n);
+        tma_load_4d(&tx0, &full[s], x_slab(s, 0), 64 * cib, -1, y0 - 1 + gi, n);
+        tma_load_4d(&tx1, &full[s], x_slab(s, 1), 64 * cib, -1, y0 - 1 + gi, n);
       }
       __syncwarp();
       if (++s == S) s = 0, ph ^= 1;
@@ -140,7 +140,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
     for (int ti = 0; ti < kTg; ++ti) {
       const int t = t0 + ti;
-      boff[ti] = (uint64_t)(int64_t)(((t / 3) * Wp + (t % 3) - 1) * 8);   // shift rows x 128 B / 16
+      boff[ti] = (uint64_t)(int64_t)(((t % 3) - 1) * 8);   // dx shift (x slab starts at row y0 - 1 + dy); 128 B / 16
     }
     int s = 0;
     uint32_t ph = 0;
@@ -152,9 +152,11 @@ __global__ void __launch_bounds__(kThreads, 1)
       if (elect_one()) {
         for (int k = 0; k < ksteps; ++k) {
           const uint32_t accum = (b > blk_beg || k > 0) ? 1u : 0u;
-#pragma unroll
-          for (int ti = 0; ti < kTg; ++ti)
-            mma_f16(tmem_base + (uint32_t)(ti * 128), da, db + boff[ti], id, accum);
+          // the 3 taps share A (the g rows of these 16 positions): read it once through the
+          // A collector instead of once per MMA (shared-memory operand bandwidth)
+          mma_f16_c<1>(tmem_base, da, db + boff[0], id, accum);
+          mma_f16_c<2>(tmem_base + 128u, da, db + boff[1], id, accum);
+          mma_f16_c<3>(tmem_base + 256u, da, db + boff[2], id, accum);
           da += 128;   // 16 positions = 16 rows x 128 B, in 16-byte units
           db += 128;
         }
@@ -384,7 +386,7 @@ PwPlan plan(const ConvShape& s) {
     q.P = rg * Wp;
     q.Pp = (q.P + 15) / 16 * 16;
     q.g_slab = round1k((uint64_t)q.Pp * 128);
-    q.x_slab = (uint32_t)(rg + 2) * Wp * 128u;
+    q.x_slab = (uint32_t)rg * Wp * 128u;   // one filter row's x rows per tap group
     q.x_off = 2 * q.g_slab + kLead;
     q.stage = round1k((uint64_t)q.x_off + 2ull * q.x_slab + kTrail);
     q.smem = st * (size_t)q.stage + (3 * kMaxStages + 2) * 8 + 4 * 64 * 8 + 256;
@@ -446,8 +448,8 @@ void conv3x3_wgrad_planes(const ConvShape& s, const void* x0, const void* x1, co
   a.part_bias = reinterpret_cast<double*>(static_cast<char*>(ws) + part_bytes(p));
   const CUtensorMap& mg0 = cached(g0, s.n, s.h, s.w, s.co, p.rg);
   const CUtensorMap& mg1 = cached(g1, s.n, s.h, s.w, s.co, p.rg);
-  const CUtensorMap& mx0 = cached(x0, s.n, s.h, s.w, s.ci, p.rg + 2);
-  const CUtensorMap& mx1 = cached(x1, s.n, s.h, s.w, s.ci, p.rg + 2);
+  const CUtensorMap& mx0 = cached(x0, s.n, s.h, s.w, s.ci, p.rg);
+  const CUtensorMap& mx1 = cached(x1, s.n, s.h, s.w, s.ci, p.rg);
   static bool configured = false;
   if (!configured) {
     RP_CUDA(cudaFuncSetAttribute(wgrad_planes_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxSmem));

@@ -289,6 +289,38 @@ __global__ void __launch_bounds__(128, 1) umma_bench_kernel(int fmt, int N, int 
         __syncwarp();
         if (++dy == 3) dy = 0;
       }
+    } else if (nops == 80 || nops == 81 || nops == 82) {
+      // conv_tc PLANES pattern (bf16): A = weights [kg 2][128][8] (LBO 2 KB) per tap, B = plane
+      // pair (x0 at 64 KB, x1 at 96 KB), K-major interleave with LBO = chain * 16 (halo
+      // positions), N = 256; per filter row 3 taps x {x0 fill, x1 lastuse}.  80: B shifted by
+      // dy * 34 + dx - 1 positions as in the kernel; 81: no shifts (B 128 B aligned); 82: as 80
+      // without the collector
+      const uint32_t w0 = umma::smem_u32(sm), xh = umma::smem_u32(sm + 64 * 1024), xl = umma::smem_u32(sm + 96 * 1024);
+      const uint32_t kgx = (uint32_t)chain * 16u;
+      const uint64_t dw = umma::desc_kmajor_interleave(w0, 2048, 128);
+      const uint64_t bh = umma::desc_kmajor_interleave(xh, kgx, 128);
+      const uint64_t bl = umma::desc_kmajor_interleave(xl, kgx, 128);
+      const uint32_t idn = umma::idesc(1, 128, 256);
+      int dy = 0;
+      for (int r = 0; r < reps; r += 6) {
+        const uint64_t row = nops == 81 ? 0 : (uint64_t)(dy * 34 + 1);
+        if (umma::elect_one()) {
+#pragma unroll
+          for (int dx = 0; dx < 3; ++dx) {
+            const uint64_t da = dw + dx * 256;
+            const uint64_t b0 = row + (nops == 81 ? 0 : dx);
+            if (nops == 82) {
+              umma::mma_f16(tm, da, bh + b0, idn, 1u);
+              umma::mma_f16(tm, da, bl + b0, idn, 1u);
+            } else {
+              umma::mma_f16_c<1>(tm, da, bh + b0, idn, 1u);
+              umma::mma_f16_c<3>(tm, da, bl + b0, idn, 1u);
+            }
+          }
+        }
+        __syncwarp();
+        if (++dy == 3) dy = 0;
+      }
     } else if (nops == 93) {
       // 94 without the k-step advance (B offsets fixed per tap)
       for (int r = 0; r < reps; r += nacc) {

@@ -1,0 +1,6 @@
+P="python tools/prof_conv.py --iters 20"
+$P --which fprop_planes,dgrad_planes,wgrad_planes,fprop,dgrad
+RP_CONV_RESIDENT=0 $P --which fprop_planes,dgrad_planes
+python tools/trace_conv.py planes | head -9
+timeout 600 python -m pytest tests -m gpu -x -q 2>&1 | tail -3
+python bench.py --no-cpu-baseline 2>&1 | tail -1 | cut -c1-300
