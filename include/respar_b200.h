@@ -196,11 +196,21 @@ int rp_op_block_bwd(const rp_geometry* g, int32_t nrows, const float* x, const f
  * of g_io on entry and leaves the planes of the new g_io there. */
 int32_t rp_op_block_planes_supported(const rp_geometry* g, int32_t nrows, int32_t math);
 int rp_op_block_fwd_planes(const rp_geometry* g, int32_t nrows, const float* x, const void* x_planes,
-                           const float* pb, float* a, float* x_next, void* a_planes, void* x_next_planes, void* ws,
-                           int64_t ws_bytes, void* stream);
+                           const float* pb, float* a, float* x_next, void* a_planes, void* x_next_planes,
+                           const void* filters, void* ws, int64_t ws_bytes, void* stream);
 int rp_op_block_bwd_planes(const rp_geometry* g, int32_t nrows, const void* x_planes, const float* a,
                            const void* a_planes, const float* pb, float* g_io, void* g_planes, float* dpre,
-                           void* dpre_planes, float* gb, void* ws, int64_t ws_bytes, void* stream);
+                           void* dpre_planes, float* gb, const void* filters, void* ws, int64_t ws_bytes,
+                           void* stream);
+/* The plane path's tcgen05 filter operands for nblocks consecutive blocks (pb = the first
+ * block's parameters) in one launch: dgrad = 0 the forward filters (W1, W2), 1 the
+ * input-gradient filters (W2, W1 flipped and transposed), one pair per block, each pair
+ * rp_op_planes_filters_bytes(g, 1) bytes.  Passing a block's pair as `filters` to the two ops
+ * above skips their per-conv preparation (nullable: each conv then prepares its own).  The
+ * pair reflects the parameters at preparation time. */
+int64_t rp_op_planes_filters_bytes(const rp_geometry* g, int32_t nblocks);
+int rp_op_prep_planes_filters(const rp_geometry* g, const float* pb, int32_t nblocks, int32_t dgrad, void* out,
+                              void* stream);
 /* Device workspace the block/stem/head ops need for nrows samples (weight relayouts,
  * deterministic split-K partials). */
 int64_t rp_op_workspace_bytes(const rp_geometry* g, int32_t nrows, int32_t math);

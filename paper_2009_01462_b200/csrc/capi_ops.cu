@@ -124,11 +124,12 @@ int64_t op_workspace_bytes(const rp_geometry& g, int nrows) {
 // dgrad: `w` is the forward conv's HWIO weight; the conv runs on the cotangent.
 void conv(const k::ConvShape& s, const float* in, const float* w, bool dgrad, const float* bias, const float* aux,
           float h, int epi, float* out, int math, void* wws, int prof_cls, bool aux_read, cudaStream_t st,
-          void* out_planes = nullptr, const void* in_planes = nullptr) {
+          void* out_planes = nullptr, const void* in_planes = nullptr, const void* wprep = nullptr) {
   prof::Scope ps(prof_cls, st, conv_flops(s), conv_bytes(s, aux_read) + (out_planes ? 4.0 * s.pixels() * s.co : 0.0));
   if (out_planes || in_planes) {   // only the fp32 tcgen05 kernel reads / writes plane pairs (planes_path())
     if (math != RP_MATH_FP32 || !k::conv3x3_tc_supported(s)) fail(RP_ERR_INTERNAL, "conv: plane i/o needs fp32 tcgen05");
-    k::conv3x3_fwd_tc(s, in, w, dgrad, bias, aux, h, epi, out, fp32_split(), wws, st, out_planes, in_planes);
+    k::conv3x3_fwd_tc(s, in, w, dgrad, bias, aux, h, epi, out, fp32_split(), wws, st, out_planes, in_planes,
+                      in_planes ? wprep : nullptr);
     return;
   }
   // RP_MATH_BF16: bf16 operands where the bf16 kernel tiles the shape (Co % 128, Ci % 32),
@@ -187,16 +188,34 @@ void block_bwd(const rp_geometry& g, int nrows, const float* x, const float* a, 
 }
 
 // Plane-pair variants: a_p / x_next_p / x_p / g_p / dpre_p are bf16 [2][elements] pairs.
+// filters (nullable): the block's two prepared plane-mode filters (prep_planes_filters), else
+// each conv prepares its own.
+int64_t planes_filter_bytes(const rp_geometry& g) { return 9LL * g.channels * g.hidden * 2 * 2; }
+
+void prep_planes_filters(const rp_geometry& g, const float* pb, int nblocks, bool dgrad, void* out, cudaStream_t st) {
+  const ParamLayout L = ParamLayout::of(g);
+  const int C = g.channels, Ch = g.hidden;
+  // forward: conv1 (W1: C -> Ch), conv2 (W2: Ch -> C); input gradient in block_bwd order:
+  // dgrad2 (W2 flipped), dgrad1 (W1 flipped)
+  const int64_t off[2] = {dgrad ? L.w2 : L.w1, dgrad ? L.w1 : L.w2};
+  const int ci_src[2] = {dgrad ? Ch : C, dgrad ? C : Ch};
+  const int co_src[2] = {dgrad ? C : Ch, dgrad ? Ch : C};
+  k::prep_filters_planes(pb, L.block_stride, nblocks, off, ci_src, co_src, dgrad, out, st);
+}
+
 void block_fwd_planes(const rp_geometry& g, int nrows, const float* x, const void* x_p, const float* pb, float* a,
-                      float* x_next, void* a_p, void* x_next_p, void* ws, int64_t ws_bytes, cudaStream_t st) {
+                      float* x_next, void* a_p, void* x_next_p, const void* filters, void* ws, int64_t ws_bytes,
+                      cudaStream_t st) {
   const ParamLayout L = ParamLayout::of(g);
   const bool tanh_act = g.activation == RP_ACT_TANH;
   if (ws_bytes < weight_ws_bytes(g)) fail(RP_ERR_RANGE, "block_fwd: workspace too small");
   const k::ConvShape s1 = shape(g, nrows, g.channels, g.hidden), s2 = shape(g, nrows, g.hidden, g.channels);
+  const char* f = static_cast<const char*>(filters);
+  const int64_t fb = planes_filter_bytes(g);
   conv(s1, x, pb + L.w1, false, pb + L.b1, nullptr, 1.f, tanh_act ? k::EPI_BIAS_TANH : k::EPI_BIAS, a, RP_MATH_FP32,
-       ws, RP_PROF_CONV_FPROP, false, st, a_p, x_p);
+       ws, RP_PROF_CONV_FPROP, false, st, a_p, x_p, f);
   conv(s2, a, pb + L.w2, false, pb + L.b2, x, (float)g.step_h, k::EPI_RESID, x_next, RP_MATH_FP32, ws,
-       RP_PROF_CONV_FPROP, true, st, x_next_p, a_p);
+       RP_PROF_CONV_FPROP, true, st, x_next_p, a_p, f ? f + fb : nullptr);
 }
 
 void wgrad_planes(const k::ConvShape& s, const void* xp, const void* gp, float scale, float* gw, float* gb, void* ws,
@@ -208,8 +227,8 @@ void wgrad_planes(const k::ConvShape& s, const void* xp, const void* gp, float s
 }
 
 void block_bwd_planes(const rp_geometry& g, int nrows, const void* x_p, const float* a, const void* a_p,
-                      const float* pb, float* gio, void* g_p, float* dpre, void* dpre_p, float* gb, void* ws,
-                      int64_t ws_bytes, cudaStream_t st) {
+                      const float* pb, float* gio, void* g_p, float* dpre, void* dpre_p, float* gb,
+                      const void* filters, void* ws, int64_t ws_bytes, cudaStream_t st) {
   const ParamLayout L = ParamLayout::of(g);
   const int C = g.channels, Ch = g.hidden;
   const bool tanh_act = g.activation == RP_ACT_TANH;
@@ -219,15 +238,17 @@ void block_bwd_planes(const rp_geometry& g, int nrows, const void* x_p, const fl
   const int64_t wg_bytes = std::max(wgrad_ws_bytes(shape(g, nrows, Ch, C)), wgrad_ws_bytes(shape(g, nrows, C, Ch)));
   void* wgws = cv.take<char>(wg_bytes);
   // dpre = h (g * W2^T) (1 - a^2), and its planes                (network.cpp:100-101)
+  const char* f = static_cast<const char*>(filters);
+  const int64_t fb = planes_filter_bytes(g);
   conv(shape(g, nrows, C, Ch), gio, pb + L.w2, true, nullptr, a, h, tanh_act ? k::EPI_TANH_BWD : k::EPI_SCALE, dpre,
-       RP_MATH_FP32, wws, RP_PROF_CONV_DGRAD, tanh_act, st, dpre_p, g_p);
+       RP_MATH_FP32, wws, RP_PROF_CONV_DGRAD, tanh_act, st, dpre_p, g_p, f);
   // gW2 = h a^T g, gb2 = h sum g                                  (network.cpp:98-99)
   wgrad_planes(shape(g, nrows, Ch, C), a_p, g_p, h, gb + L.w2, gb + L.b2, wgws, st);
   // gW1 = x^T dpre, gb1 = sum dpre                                (network.cpp:102-103)
   wgrad_planes(shape(g, nrows, C, Ch), x_p, dpre_p, 1.f, gb + L.w1, gb + L.b1, wgws, st);
   // g <- g + dpre * W1^T in place, and the planes of the new g   (network.cpp:104)
   conv(shape(g, nrows, Ch, C), dpre, pb + L.w1, true, nullptr, gio, 1.f, k::EPI_ADD, gio, RP_MATH_FP32, wws,
-       RP_PROF_CONV_DGRAD, true, st, g_p, dpre_p);
+       RP_PROF_CONV_DGRAD, true, st, g_p, dpre_p, f ? f + fb : nullptr);
 }
 
 void stem_fwd(const rp_geometry& g, int nrows, const float* xr, const float* ps, float* x0, cudaStream_t st) {
@@ -475,8 +496,8 @@ int32_t rp_op_block_planes_supported(const rp_geometry* g, int32_t nrows, int32_
 }
 
 int rp_op_block_fwd_planes(const rp_geometry* g, int32_t nrows, const float* x, const void* x_planes,
-                           const float* pb, float* a, float* x_next, void* a_planes, void* x_next_planes, void* ws,
-                           int64_t ws_bytes, void* stream) {
+                           const float* pb, float* a, float* x_next, void* a_planes, void* x_next_planes,
+                           const void* filters, void* ws, int64_t ws_bytes, void* stream) {
   return guard([&] {
     need(g, "geometry");
     if (!planes_path(*g, nrows, RP_MATH_FP32)) fail(RP_ERR_SHAPE, "block_fwd_planes: geometry not on the plane path");
@@ -486,13 +507,32 @@ int rp_op_block_fwd_planes(const rp_geometry* g, int32_t nrows, const float* x, 
     need(a, "a");
     need(x_next, "x_next");
     need(a_planes, "a_planes");
-    block_fwd_planes(*g, nrows, x, x_planes, pb, a, x_next, a_planes, x_next_planes, ws, ws_bytes, S(stream));
+    block_fwd_planes(*g, nrows, x, x_planes, pb, a, x_next, a_planes, x_next_planes, filters, ws, ws_bytes,
+                     S(stream));
+  });
+}
+
+int64_t rp_op_planes_filters_bytes(const rp_geometry* g, int32_t nblocks) {
+  if (!g || nblocks <= 0) return 0;
+  return (int64_t)nblocks * 2 * planes_filter_bytes(*g);
+}
+
+int rp_op_prep_planes_filters(const rp_geometry* g, const float* pb, int32_t nblocks, int32_t dgrad, void* out,
+                              void* stream) {
+  return guard([&] {
+    need(g, "geometry");
+    validate_geometry(*g);
+    if (nblocks <= 0) return;
+    need(pb, "pb");
+    need(out, "out");
+    prep_planes_filters(*g, pb, nblocks, dgrad != 0, out, S(stream));
   });
 }
 
 int rp_op_block_bwd_planes(const rp_geometry* g, int32_t nrows, const void* x_planes, const float* a,
                            const void* a_planes, const float* pb, float* g_io, void* g_planes, float* dpre,
-                           void* dpre_planes, float* gb, void* ws, int64_t ws_bytes, void* stream) {
+                           void* dpre_planes, float* gb, const void* filters, void* ws, int64_t ws_bytes,
+                           void* stream) {
   return guard([&] {
     need(g, "geometry");
     if (!planes_path(*g, nrows, RP_MATH_FP32)) fail(RP_ERR_SHAPE, "block_bwd_planes: geometry not on the plane path");
@@ -506,8 +546,8 @@ int rp_op_block_bwd_planes(const rp_geometry* g, int32_t nrows, const void* x_pl
     need(dpre, "dpre");
     need(dpre_planes, "dpre_planes");
     need(gb, "gb");
-    block_bwd_planes(*g, nrows, x_planes, a, a_planes, pb, g_io, g_planes, dpre, dpre_planes, gb, ws, ws_bytes,
-                     S(stream));
+    block_bwd_planes(*g, nrows, x_planes, a, a_planes, pb, g_io, g_planes, dpre, dpre_planes, gb, filters, ws,
+                     ws_bytes, S(stream));
   });
 }
 

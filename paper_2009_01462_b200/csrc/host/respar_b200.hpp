@@ -229,6 +229,7 @@ class DecoupledTrainer {
     // inputs x_0..x_{n-1} and of a_0..a_{n-1}; dpre_p / g_p are backward scratch
     std::vector<DeviceArray> xps, aps;
     DeviceArray dpre_p, g_p;
+    DeviceArray filters;  // plane path: the blocks' prepared filter pairs (forward, then reused for dgrad)
     bool tape_planes = false;
     DeviceArray x0, dpre, ws, red_ws, pooled, logits, loss;
     DeviceArray snap_lam, snap_kappa;

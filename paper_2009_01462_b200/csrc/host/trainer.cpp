@@ -388,6 +388,7 @@ void DecoupledTrainer::ensure_capacity(int nrows) {
       }
       st.dpre_p.allocate(st.device, (int64_t)nrows * hid() * 4);
       st.g_p.allocate(st.device, (int64_t)nrows * feat() * 4);
+      st.filters.allocate(st.device, std::max<int64_t>(256, rp_op_planes_filters_bytes(&geo_, n)));
     }
     st.ws.allocate(st.device, rp_op_workspace_bytes(&geo_, nrows, math_));
     if (k == stages() - 1) {
@@ -437,12 +438,16 @@ void DecoupledTrainer::run_forward(Stage& st, const float* input, int nrows, flo
     const int64_t e = (int64_t)nrows * feat();
     auto* p = st.xps[0].get<uint16_t>();
     check(rp_op_split_planes(cur, e, p, p + e, s));
+    // every block's forward filters in one launch (not one per conv)
+    const int64_t fpair = rp_op_planes_filters_bytes(&geo_, 1);
+    check(rp_op_prep_planes_filters(&geo_, P + L.block0 + (int64_t)st.begin * L.block_stride, n, 0,
+                                    st.filters.get(), s));
     for (int i = 0; i < n; ++i) {
       const int l = st.begin + i;
       float* out = i == n - 1 ? out_features : st.xs[i + 1].get();
       check(rp_op_block_fwd_planes(&geo_, nrows, cur, st.xps[i].get(), P + L.block0 + (int64_t)l * L.block_stride,
                                    st.as[i].get(), out, st.aps[i].get(), i == n - 1 ? nullptr : st.xps[i + 1].get(),
-                                   st.ws.get(), st.ws.bytes(), s));
+                                   st.filters.get<char>() + i * fpair, st.ws.get(), st.ws.bytes(), s));
       cur = out;
     }
     if (st.index == stages() - 1)
@@ -493,11 +498,16 @@ void DecoupledTrainer::run_backward(Stage& st, const int32_t* labels, int nrows,
   if (st.tape_planes && st.fwd_rows == nrows) {
     auto* gp = st.g_p.get<uint16_t>();
     check(rp_op_split_planes(g, n, gp, gp + n, s));
+    // every block's input-gradient filters in one launch, from the current parameters
+    const int64_t fpair = rp_op_planes_filters_bytes(&geo_, 1);
+    check(rp_op_prep_planes_filters(&geo_, P + L.block0 + (int64_t)st.begin * L.block_stride, nb, 1,
+                                    st.filters.get(), s));
     for (int i = nb - 1; i >= 0; --i) {
       const int l = st.begin + i;
       const int64_t off = L.block0 + (int64_t)l * L.block_stride;
       check(rp_op_block_bwd_planes(&geo_, nrows, st.xps[i].get(), st.as[i].get(), st.aps[i].get(), P + off, g, gp,
-                                   st.dpre.get(), st.dpre_p.get(), G + off, st.ws.get(), st.ws.bytes(), s));
+                                   st.dpre.get(), st.dpre_p.get(), G + off, st.filters.get<char>() + i * fpair,
+                                   st.ws.get(), st.ws.bytes(), s));
     }
   } else
   for (int i = nb - 1; i >= 0; --i) {

@@ -381,6 +381,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_wait(&acc_empty[ab], aph ^ 1);
       tc_fence_after();
       if (a.trace && blockIdx.x < 2 && lane == 0 && u < 64) a.trace[(blockIdx.x * 64 + u) * 8 + 0] = globaltimer_ns();
+      const long long clk_u0 = a.trace ? clock64() : 0;
       const uint32_t d0 = tmem_base + (uint32_t)(ab * kS * 128);
       long long wait_h = 0, wait_w = 0;
       for (int c = 0; c < a.nchunks; ++c) {
@@ -495,6 +496,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         a.trace[(blockIdx.x * 64 + u) * 8 + 1] = globaltimer_ns();
         a.trace[(blockIdx.x * 64 + u) * 8 + 5] = (unsigned long long)wait_h;   // cycles waiting for the halo
         a.trace[(blockIdx.x * 64 + u) * 8 + 6] = (unsigned long long)wait_w;   // cycles waiting for weights
+        a.trace[(blockIdx.x * 64 + u) * 8 + 7] = (unsigned long long)(clock64() - clk_u0);   // SM cycles of the unit's issue
       }
       if (++ab == 2) ab = 0, aph ^= 1;
     }
@@ -707,14 +709,11 @@ __global__ void prep_weights_kernel(const float* __restrict__ w, int ci_src, int
 
 // X3BF16 weights: [cb][chunk][tap'][kg (2)][128 rows][8 bf16]: row r < 64 holds
 // W0 = bf16(w[co = 64 cb + r]), r >= 64 holds W1 = bf16(w - W0) for co = 64 cb + r - 64.
-__global__ void prep_weights_bf16x2_kernel(const float* __restrict__ w, int ci_src, int co_src, int flip,
-                                           __nv_bfloat16* __restrict__ out) {
+__device__ __forceinline__ __nv_bfloat16 prep_bf16x2_elem(const float* __restrict__ w, int ci_src, int co_src,
+                                                          int flip, int64_t idx) {
   const int Ci = flip ? co_src : ci_src;
-  const int Co = flip ? ci_src : co_src;
   const int64_t per_cb = 9LL * Ci * 128;
-  const int64_t total = per_cb * (Co / 64);
-  for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total;
-       idx += (int64_t)gridDim.x * blockDim.x) {
+  {
     const int cb = (int)(idx / per_cb);
     const int64_t li = idx - cb * per_cb;
     const int e = (int)(li & 7);
@@ -728,7 +727,35 @@ __global__ void prep_weights_bf16x2_kernel(const float* __restrict__ w, int ci_s
     const float v = !flip ? w[((int64_t)tap * ci_src + ci) * co_src + co]
                           : w[((int64_t)(8 - tap) * ci_src + co) * co_src + ci];
     const __nv_bfloat16 h = __float2bfloat16_rn(v);
-    out[idx] = r < 64 ? h : __float2bfloat16_rn(v - __bfloat162float(h));
+    return r < 64 ? h : __float2bfloat16_rn(v - __bfloat162float(h));
+  }
+}
+
+__global__ void prep_weights_bf16x2_kernel(const float* __restrict__ w, int ci_src, int co_src, int flip,
+                                           __nv_bfloat16* __restrict__ out) {
+  const int64_t total = 9LL * ci_src * co_src * 2;
+  for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total;
+       idx += (int64_t)gridDim.x * blockDim.x)
+    out[idx] = prep_bf16x2_elem(w, ci_src, co_src, flip, idx);
+}
+
+// Both filters of every block of a stage in one launch (plane path): filter j of block b
+// (parameters at pb + b * block_stride + off[j], HWIO ci_src[j] x co_src[j]) goes to
+// out + (2 b + j) * felems in the layout prep_weights_bf16x2_kernel writes.
+struct FilterPair {
+  int64_t off[2];
+  int ci_src[2], co_src[2];
+  int flip;
+};
+
+__global__ void prep_filters_planes_kernel(const float* __restrict__ pb, int64_t block_stride, int nblocks,
+                                           const FilterPair fp, int64_t felems, __nv_bfloat16* __restrict__ out) {
+  const int64_t total = (int64_t)nblocks * 2 * felems;
+  for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total;
+       idx += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t f = idx / felems;
+    const int b = (int)(f >> 1), j = (int)(f & 1);
+    out[idx] = prep_bf16x2_elem(pb + b * block_stride + fp.off[j], fp.ci_src[j], fp.co_src[j], fp.flip, idx - f * felems);
   }
 }
 
@@ -912,9 +939,24 @@ void conv3x3_tc_set_trace(unsigned long long* p) { g_trace = p; }
 
 int64_t conv3x3_tc_ws_bytes(const ConvShape& s) { return 9LL * s.ci * 2 * s.co * 4 + 256; }
 
+void prep_filters_planes(const float* pb, int64_t block_stride, int nblocks, const int64_t off[2],
+                         const int ci_src[2], const int co_src[2], bool dgrad, void* out, cudaStream_t st) {
+  if (nblocks <= 0) return;
+  FilterPair fp{};
+  for (int j = 0; j < 2; ++j) fp.off[j] = off[j], fp.ci_src[j] = ci_src[j], fp.co_src[j] = co_src[j];
+  fp.flip = dgrad ? 1 : 0;
+  const int64_t felems = 9LL * ci_src[0] * co_src[0] * 2;
+  if (9LL * ci_src[1] * co_src[1] * 2 != felems) fail(RP_ERR_INTERNAL, "prep_filters_planes: filter sizes differ");
+  const int64_t total = (int64_t)nblocks * 2 * felems;
+  const int grid = (int)std::min<int64_t>(ceil_div(total, 256), 16 * kNumSMs);
+  prep_filters_planes_kernel<<<grid, 256, 0, st>>>(pb, block_stride, nblocks, fp, felems,
+                                                   static_cast<__nv_bfloat16*>(out));
+  RP_LAUNCHED();
+}
+
 void conv3x3_fwd_tc(const ConvShape& s, const float* in, const float* w_hwio, bool dgrad_weights, const float* bias,
                     const float* aux, float h, int epi, float* out, int mode, void* ws, cudaStream_t st,
-                    void* out_planes, const void* in_planes) {
+                    void* out_planes, const void* in_planes, const void* wprep) {
   if (s.pixels() == 0) return;
   if (in_planes) mode = MODE_PLANES;
   const Plan p = plan_for(s, mode);
@@ -925,14 +967,19 @@ void conv3x3_fwd_tc(const ConvShape& s, const float* in, const float* w_hwio, bo
   const int co_src = dgrad_weights ? s.ci : s.co;
   const int64_t total = 9LL * s.ci * 2 * s.co;
   const int pgrid = (int)std::min<int64_t>(ceil_div(total, 256), 16 * kNumSMs);
-  if (mode == MODE_X3BF16 || mode == MODE_PLANES)
+  if (wprep && mode != MODE_PLANES) fail(RP_ERR_INTERNAL, "conv3x3_fwd_tc: prepared filters are plane-mode only");
+  if (wprep) {
+    // prepared by prep_filters_planes for the whole stage
+  } else if (mode == MODE_X3BF16 || mode == MODE_PLANES) {
     prep_weights_bf16x2_kernel<<<pgrid, 256, 0, st>>>(w_hwio, ci_src, co_src, dgrad_weights ? 1 : 0,
                                                       static_cast<__nv_bfloat16*>(ws));
-  else
+    RP_LAUNCHED();
+  } else {
     prep_weights_kernel<<<pgrid, 256, 0, st>>>(w_hwio, ci_src, co_src, dgrad_weights ? 1 : 0,
                                                static_cast<float*>(ws));
-  RP_LAUNCHED();
-  const float* wp = static_cast<const float*>(ws);
+    RP_LAUNCHED();
+  }
+  const float* wp = static_cast<const float*>(wprep ? wprep : ws);
   TcArgs a{};
   a.N = s.n;
   a.H = s.h;

@@ -61,7 +61,12 @@ int64_t conv3x3_tc_ws_bytes(const ConvShape& s);
 // 2-MMA plane mode (~2^-17 relative).
 void conv3x3_fwd_tc(const ConvShape& s, const float* in, const float* w_hwio, bool dgrad_weights, const float* bias,
                     const float* aux, float h, int epi, float* out, int mode, void* ws, cudaStream_t st,
-                    void* out_planes = nullptr, const void* in_planes = nullptr);
+                    void* out_planes = nullptr, const void* in_planes = nullptr, const void* wprep = nullptr);
+// The plane-mode A operands of both filters of nblocks blocks in one launch (filter j of block
+// b: HWIO at pb + b block_stride + off[j], ci_src[j] x co_src[j]; dgrad: flipped/transposed) into
+// out + (2 b + j) * 9 ci co * 2 bf16 -- the wprep argument of conv3x3_fwd_tc.
+void prep_filters_planes(const float* pb, int64_t block_stride, int nblocks, const int64_t off[2],
+                         const int ci_src[2], const int co_src[2], bool dgrad, void* out, cudaStream_t st);
 
 // tcgen05 bf16-operand conv, fp32 accumulate (conv_bf16.cu): Co % 128 == 0, Ci % 32 == 0.
 bool conv3x3_bf16_supported(const ConvShape& s);

@@ -71,9 +71,20 @@ def test_block_planes(n, hw, c, ch):
     xn_p = torch.empty(2 * ne, dtype=torch.int16, device=dev)
     x_p = torch.empty(2 * ne, dtype=torch.int16, device=dev)
     rp.check(lib().rp_op_split_planes(_p(tx), ne, _p(x_p), C.c_void_p(x_p.data_ptr() + 2 * ne), None))
+    # the block's filters prepared once (rp_op_prep_planes_filters) vs per conv (filters = NULL):
+    # bitwise the same
+    fbytes = lib().rp_op_planes_filters_bytes(C.byref(geo), 1)
+    ffwd = torch.empty(fbytes, dtype=torch.uint8, device=dev)
+    fbwd = torch.empty(fbytes, dtype=torch.uint8, device=dev)
+    rp.check(lib().rp_op_prep_planes_filters(C.byref(geo), pb, 1, 0, _p(ffwd), None))
+    rp.check(lib().rp_op_prep_planes_filters(C.byref(geo), pb, 1, 1, _p(fbwd), None))
     rp.check(lib().rp_op_block_fwd_planes(C.byref(geo), n, _p(tx), _p(x_p), pb, _p(a), _p(xn), _p(a_p), _p(xn_p),
-                                          _p(ws), wsb, None))
+                                          None, _p(ws), wsb, None))
+    xn_self = xn.clone()
+    rp.check(lib().rp_op_block_fwd_planes(C.byref(geo), n, _p(tx), _p(x_p), pb, _p(a), _p(xn), _p(a_p), _p(xn_p),
+                                          _p(ffwd), _p(ws), wsb, None))
     torch.cuda.synchronize()
+    assert torch.equal(xn, xn_self)
     a64, xn64 = a.cpu().numpy().astype(np.float64), xn.cpu().numpy().astype(np.float64)
     assert _rel(a64, a_ref.cpu().numpy().astype(np.float64)) < FWD_TOL
     assert _rel(xn64, xn_ref.cpu().numpy().astype(np.float64)) < FWD_TOL
@@ -91,7 +102,7 @@ def test_block_planes(n, hw, c, ch):
     gb = torch.zeros_like(tp)
     gbp = C.c_void_p(gb.data_ptr() + 4 * off)
     rp.check(lib().rp_op_block_bwd_planes(C.byref(geo), n, _p(x_p), _p(a), _p(a_p), pb, _p(g_io), _p(g_p), _p(dpre),
-                                          _p(dpre_p), gbp, _p(ws), wsb, None))
+                                          _p(dpre_p), gbp, _p(fbwd), _p(ws), wsb, None))
     g_ref = tup.clone().reshape(-1)
     gb_ref = torch.zeros_like(tp)
     rp.check(lib().rp_op_block_bwd(C.byref(geo), n, _p(tx), _p(a_ref), pb, _p(g_ref), _p(dpre),

@@ -20,7 +20,8 @@ g = rp.Geometry(cfg["cin"], cfg["h"], cfg["w"], cfg["c"], cfg["ch"], cfg["L"], b
 B, K = cfg["B"], cfg["K"]
 variants = [("paper", {}), ("kappa_lr=0", {"kappa_lr": 0.0}), ("lambda_lr=0", {"lambda_lr": 0.0}),
             ("lr=0", {"lr": 0.0}), ("penalty", {"mode": rp.PENALTY}), ("kappa_lr=6e-12", {"kappa_lr": 6e-12}),
-            ("kappa_lr=1e-10", {"kappa_lr": 1e-10})]
+            ("kappa_lr=1e-10", {"kappa_lr": 1e-10}), ("kappa_lr=1e-12", {"kappa_lr": 1e-12}),
+            ("kappa_lr=1e-13", {"kappa_lr": 1e-13}), ("kappa_lr=1e-14", {"kappa_lr": 1e-14})]
 if len(sys.argv) > 3:
     variants = [v for v in variants if v[0] in sys.argv[3].split(",")]
 for name, over in variants:

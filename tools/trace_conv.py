@@ -15,6 +15,7 @@ xp = torch.empty(2 * x.numel(), dtype=torch.bfloat16, device="cuda")
 op = torch.empty_like(xp)
 rp.check(lib().rp_op_split_planes(P(x.data_ptr()), x.numel(), P(xp.data_ptr()), P(xp.data_ptr() + 2 * x.numel()), None))
 for math in sys.argv[1:] or ("planes", "fp32"):
+    sys.stdout.flush()
     for it in range(3):
         if it == 2:
             L.rp_debug_set_trace(P(tr.data_ptr()))
@@ -37,5 +38,6 @@ for math in sys.argv[1:] or ("planes", "fp32"):
                 break
             print(f" cta{cta} u{u}: mma_start {(row[0]-t0)/1e3:7.2f} halo_c0 {(row[4]-t0)/1e3:7.2f}"
                   f" mma_end {(row[1]-t0)/1e3:7.2f} epi_start {(row[2]-t0)/1e3:7.2f} epi_end {(row[3]-t0)/1e3:7.2f}"
-                  f"  wait_halo {row[5]/1965:6.2f}us wait_w {row[6]/1965:6.2f}us")
+                  f"  wait_halo {row[5]/1965:6.2f}us wait_w {row[6]/1965:6.2f}us"
+                  f"  issue {row[7]:6d} cyc = {row[7] / max(1, row[1] - row[0]):5.3f} GHz")
     tr.zero_()
