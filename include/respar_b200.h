@@ -170,6 +170,7 @@ int64_t rp_op_conv3x3_wgrad_workspace_bytes(int32_t n, int32_t h, int32_t w, int
 
 /* bf16 plane pairs of an fp32 tensor: p0 = bf16(v), p1 = bf16(v - p0) (n % 4 == 0). */
 int rp_op_split_planes(const float* in, int64_t n, void* p0, void* p1, void* stream);
+/* (p1 may be NULL: p0 alone is the bf16 copy of in.) */
 /* Weight gradient from plane pairs (x = x0 + x1, gout = g0 + g1; bf16 NHWC planes), Ci and
  * Co multiples of 64: the fp32-accurate (~1e-5) tcgen05 wgrad fed by TMA alone. */
 int rp_op_conv3x3_wgrad_planes(int32_t n, int32_t h, int32_t w, int32_t ci, int32_t co, const void* x0, const void* x1,
@@ -209,6 +210,25 @@ int rp_op_block_bwd_planes(const rp_geometry* g, int32_t nrows, const void* x_pl
  * above skips their per-conv preparation (nullable: each conv then prepares its own).  The
  * pair reflects the parameters at preparation time. */
 int64_t rp_op_planes_filters_bytes(const rp_geometry* g, int32_t nblocks);
+/* The bf16 tape path (RP_MATH_BF16, C and hidden multiples of 128): every conv reads a bf16
+ * copy of its input by TMA (the values the fp32-input bf16 conv rounds to), and the tape is
+ * bf16 only.  Forward: x (fp32 residual stream) and x16 = bf16(x) in; a16 = bf16(a), d16 =
+ * bf16(1 - a^2) (tanh only; NULL for identity), x_next (fp32) and x_next16 (may be NULL: the
+ * stage's last block) out.  Backward: g_io (fp32, updated in place) and g16 = bf16(g_io) in,
+ * g16 rewritten with the new cotangent, dpre16 scratch, gb the block's gradients. */
+int32_t rp_op_block_bf16_tape_supported(const rp_geometry* g, int32_t nrows, int32_t math);
+int rp_op_block_fwd_bf16t(const rp_geometry* g, int32_t nrows, const float* x, const void* x16, const float* pb,
+                          void* a16, void* d16, float* x_next, void* x_next16, void* ws, int64_t ws_bytes,
+                          void* stream);
+int rp_op_block_bwd_bf16t(const rp_geometry* g, int32_t nrows, const void* x16, const void* a16, const void* d16,
+                          const float* pb, float* g_io, void* g16, void* dpre16, float* gb, void* ws,
+                          int64_t ws_bytes, void* stream);
+/* Weight gradient from single bf16 copies (bf16 x bf16 products, fp32 accumulate), Ci and Co
+ * multiples of 128. */
+int rp_op_conv3x3_wgrad_bf16p(int32_t n, int32_t h, int32_t w, int32_t ci, int32_t co, const void* x16,
+                              const void* g16, double scale, float* gw, float* gb, void* ws, int64_t ws_bytes,
+                              void* stream);
+int64_t rp_op_conv3x3_wgrad_bf16p_workspace_bytes(int32_t n, int32_t h, int32_t w, int32_t ci, int32_t co);
 int rp_op_prep_planes_filters(const rp_geometry* g, const float* pb, int32_t nblocks, int32_t dgrad, void* out,
                               void* stream);
 /* Device workspace the block/stem/head ops need for nrows samples (weight relayouts,

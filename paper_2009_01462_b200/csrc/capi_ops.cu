@@ -74,7 +74,7 @@ int64_t weight_ws_bytes(const rp_geometry& g) {
 int64_t wgrad_ws_bytes(const k::ConvShape& s) {
   return std::max({k::conv3x3_wgrad_ws_bytes(s), k::conv3x3_wgrad_tc_ws_bytes(s, true),
                    k::conv3x3_wgrad_tc_ws_bytes(s, false), k::conv3x3_wgrad_bf16_ws_bytes(s),
-                   k::conv3x3_wgrad_planes_ws_bytes(s)});
+                   k::conv3x3_wgrad_planes_ws_bytes(s), k::conv3x3_wgrad_bf16p_ws_bytes(s)});
 }
 
 // The plane-pair block path (fp32 math): every conv of the block on the tcgen05 kernel, whose
@@ -91,6 +91,22 @@ bool planes_path(const rp_geometry& g, int nrows, int math) {
   const k::ConvShape s2{nrows, g.height, g.width, g.hidden, g.channels};
   return k::conv3x3_tc_supported(s1) && k::conv3x3_tc_supported(s2) && k::conv3x3_wgrad_planes_supported(s1) &&
          k::conv3x3_wgrad_planes_supported(s2);
+}
+
+// The bf16 tape path (bf16 math): the bf16 conv epilogues also write a bf16 copy of their
+// output (the block inputs x, the activations a, dpre and the cotangent g), so both weight
+// gradients run on the TMA-fed single-plane wgrad (conv_wgrad_planes.cu, bf16p) instead of
+// staging fp32 operands through converter warps.  RP_BF16_TAPE=0 turns it off.
+bool bf16_tape_path(const rp_geometry& g, int nrows, int math) {
+  static const bool enabled = [] {
+    const char* e = std::getenv("RP_BF16_TAPE");
+    return !(e && std::string(e) == "0");
+  }();
+  if (!enabled || math != RP_MATH_BF16 || nrows <= 0) return false;
+  const k::ConvShape s1{nrows, g.height, g.width, g.channels, g.hidden};
+  const k::ConvShape s2{nrows, g.height, g.width, g.hidden, g.channels};
+  return k::conv3x3_bf16_supported(s1) && k::conv3x3_bf16_supported(s2) && k::conv3x3_wgrad_bf16p_supported(s1) &&
+         k::conv3x3_wgrad_bf16p_supported(s2);
 }
 
 // Weight gradient (+ bias sums): tcgen05 when the math mode and shape allow, SIMT otherwise.
@@ -249,6 +265,65 @@ void block_bwd_planes(const rp_geometry& g, int nrows, const void* x_p, const fl
   // g <- g + dpre * W1^T in place, and the planes of the new g   (network.cpp:104)
   conv(shape(g, nrows, Ch, C), dpre, pb + L.w1, true, nullptr, gio, 1.f, k::EPI_ADD, gio, RP_MATH_FP32, wws,
        RP_PROF_CONV_DGRAD, true, st, g_p, dpre_p, f ? f + fb : nullptr);
+}
+
+// bf16 tape variants.  Every conv reads its input as a bf16 tensor (TMA straight into the
+// MMA layout) -- the same values the fp32-input bf16 kernel's converters would produce (RNE)
+// -- and the tape holds bf16 only: x16 (block input), a16 (activation), d16 = bf16(1 - a^2)
+// (the tanh derivative), dpre16, g16.  The fp32 residual stream x (EPI_RESID's aux, the stage
+// output) and the fp32 cotangent g (EPI_ADD's aux) stay fp32.
+void block_fwd_bf16t(const rp_geometry& g, int nrows, const float* x, const void* x16, const float* pb, void* a16,
+                     void* d16, float* x_next, void* x_next16, void* ws, int64_t ws_bytes, cudaStream_t st) {
+  const ParamLayout L = ParamLayout::of(g);
+  const bool tanh_act = g.activation == RP_ACT_TANH;
+  if (ws_bytes < weight_ws_bytes(g)) fail(RP_ERR_RANGE, "block_fwd: workspace too small");
+  const k::ConvShape s1 = shape(g, nrows, g.channels, g.hidden), s2 = shape(g, nrows, g.hidden, g.channels);
+  {   // a = act(conv1(x) + b1): bf16 a and bf16 (1 - a^2)   (network.cpp:85-86)
+    prof::Scope ps(RP_PROF_CONV_FPROP, st, conv_flops(s1), 2.0 * s1.pixels() * (s1.ci + s1.co * (tanh_act ? 2 : 1)));
+    k::conv3x3_fwd_bf16_in16(s1, x16, pb + L.w1, false, pb + L.b1, nullptr, nullptr, 1.f,
+                             tanh_act ? k::EPI_BIAS_TANH : k::EPI_BIAS, nullptr, a16, tanh_act ? d16 : nullptr, ws,
+                             st);
+  }
+  {   // x' = x + h (conv2(a) + b2), fp32 and bf16                (network.cpp:87)
+    prof::Scope ps(RP_PROF_CONV_FPROP, st, conv_flops(s2),
+                   2.0 * s2.pixels() * s2.ci + 8.0 * s2.pixels() * s2.co + (x_next16 ? 2.0 * s2.pixels() * s2.co : 0.0));
+    k::conv3x3_fwd_bf16_in16(s2, a16, pb + L.w2, false, pb + L.b2, x, nullptr, (float)g.step_h, k::EPI_RESID, x_next,
+                             x_next16, nullptr, ws, st);
+  }
+}
+
+void wgrad_bf16p(const k::ConvShape& s, const void* x16, const void* g16, float scale, float* gw, float* gb, void* ws,
+                 cudaStream_t st) {
+  prof::Scope ps(RP_PROF_CONV_WGRAD, st, conv_flops(s), 2.0 * (double)s.pixels() * (s.ci + s.co));
+  k::conv3x3_wgrad_bf16p(s, x16, g16, scale, gw, gb, ws, st);
+}
+
+void block_bwd_bf16t(const rp_geometry& g, int nrows, const void* x16, const void* a16, const void* d16,
+                     const float* pb, float* gio, void* g16, void* dpre16, float* gb, void* ws, int64_t ws_bytes,
+                     cudaStream_t st) {
+  const ParamLayout L = ParamLayout::of(g);
+  const int C = g.channels, Ch = g.hidden;
+  const bool tanh_act = g.activation == RP_ACT_TANH;
+  const float h = (float)g.step_h;
+  Carve cv{static_cast<char*>(ws), ws_bytes};
+  void* wws = cv.take<char>(weight_ws_bytes(g));
+  const int64_t wg_bytes = std::max(wgrad_ws_bytes(shape(g, nrows, Ch, C)), wgrad_ws_bytes(shape(g, nrows, C, Ch)));
+  void* wgws = cv.take<char>(wg_bytes);
+  const k::ConvShape sd2 = shape(g, nrows, C, Ch), sd1 = shape(g, nrows, Ch, C);
+  {   // dpre = h (g * W2^T) (1 - a^2), bf16                      (network.cpp:100-101)
+    prof::Scope ps(RP_PROF_CONV_DGRAD, st, conv_flops(sd2), 2.0 * sd2.pixels() * (sd2.ci + sd2.co * (tanh_act ? 2 : 1)));
+    k::conv3x3_fwd_bf16_in16(sd2, g16, pb + L.w2, true, nullptr, nullptr, tanh_act ? d16 : nullptr, h,
+                             tanh_act ? k::EPI_DTANH16 : k::EPI_SCALE, nullptr, dpre16, nullptr, wws, st);
+  }
+  // gW2 = h a^T g, gb2 = h sum g                                    (network.cpp:98-99)
+  wgrad_bf16p(shape(g, nrows, Ch, C), a16, g16, h, gb + L.w2, gb + L.b2, wgws, st);
+  // gW1 = x^T dpre, gb1 = sum dpre                                  (network.cpp:102-103)
+  wgrad_bf16p(shape(g, nrows, C, Ch), x16, dpre16, 1.f, gb + L.w1, gb + L.b1, wgws, st);
+  {   // g <- g + dpre * W1^T in place, and its bf16 copy           (network.cpp:104)
+    prof::Scope ps(RP_PROF_CONV_DGRAD, st, conv_flops(sd1), 2.0 * sd1.pixels() * sd1.ci + 10.0 * sd1.pixels() * sd1.co);
+    k::conv3x3_fwd_bf16_in16(sd1, dpre16, pb + L.w1, true, nullptr, gio, nullptr, 1.f, k::EPI_ADD, gio, g16, nullptr,
+                             wws, st);
+  }
 }
 
 void stem_fwd(const rp_geometry& g, int nrows, const float* xr, const float* ps, float* x0, cudaStream_t st) {
@@ -551,12 +626,69 @@ int rp_op_block_bwd_planes(const rp_geometry* g, int32_t nrows, const void* x_pl
   });
 }
 
+int32_t rp_op_block_bf16_tape_supported(const rp_geometry* g, int32_t nrows, int32_t math) {
+  if (!g || nrows <= 0) return 0;
+  return bf16_tape_path(*g, nrows, math) ? 1 : 0;
+}
+
+int rp_op_block_fwd_bf16t(const rp_geometry* g, int32_t nrows, const float* x, const void* x16, const float* pb,
+                          void* a16, void* d16, float* x_next, void* x_next16, void* ws, int64_t ws_bytes,
+                          void* stream) {
+  return guard([&] {
+    need(g, "geometry");
+    if (!bf16_tape_path(*g, nrows, RP_MATH_BF16)) fail(RP_ERR_SHAPE, "block_fwd_bf16t: geometry not on the bf16 tape path");
+    need(x, "x");
+    need(x16, "x16");
+    need(pb, "pb");
+    need(a16, "a16");
+    if (g->activation == RP_ACT_TANH) need(d16, "d16");
+    need(x_next, "x_next");
+    block_fwd_bf16t(*g, nrows, x, x16, pb, a16, d16, x_next, x_next16, ws, ws_bytes, S(stream));
+  });
+}
+
+int rp_op_block_bwd_bf16t(const rp_geometry* g, int32_t nrows, const void* x16, const void* a16, const void* d16,
+                          const float* pb, float* g_io, void* g16, void* dpre16, float* gb, void* ws,
+                          int64_t ws_bytes, void* stream) {
+  return guard([&] {
+    need(g, "geometry");
+    if (!bf16_tape_path(*g, nrows, RP_MATH_BF16)) fail(RP_ERR_SHAPE, "block_bwd_bf16t: geometry not on the bf16 tape path");
+    if (ws_bytes < op_workspace_bytes(*g, nrows)) fail(RP_ERR_RANGE, "block_bwd_bf16t: workspace too small");
+    need(x16, "x16");
+    need(a16, "a16");
+    if (g->activation == RP_ACT_TANH) need(d16, "d16");
+    need(pb, "pb");
+    need(g_io, "g_io");
+    need(g16, "g16");
+    need(dpre16, "dpre16");
+    need(gb, "gb");
+    block_bwd_bf16t(*g, nrows, x16, a16, d16, pb, g_io, g16, dpre16, gb, ws, ws_bytes, S(stream));
+  });
+}
+
+int64_t rp_op_conv3x3_wgrad_bf16p_workspace_bytes(int32_t n, int32_t h, int32_t w, int32_t ci, int32_t co) {
+  return k::conv3x3_wgrad_bf16p_ws_bytes(k::ConvShape{n, h, w, ci, co});
+}
+
+int rp_op_conv3x3_wgrad_bf16p(int32_t n, int32_t h, int32_t w, int32_t ci, int32_t co, const void* x16,
+                              const void* g16, double scale, float* gw, float* gb, void* ws, int64_t ws_bytes,
+                              void* stream) {
+  return guard([&] {
+    const k::ConvShape s{n, h, w, ci, co};
+    if (!k::conv3x3_wgrad_bf16p_supported(s)) fail(RP_ERR_SHAPE, "conv3x3_wgrad_bf16p: unsupported shape");
+    if (ws_bytes < k::conv3x3_wgrad_bf16p_ws_bytes(s)) fail(RP_ERR_RANGE, "conv3x3_wgrad_bf16p: workspace too small");
+    need(x16, "x16");
+    need(g16, "g16");
+    need(gw, "gw");
+    wgrad_bf16p(s, x16, g16, (float)scale, gw, gb, ws, S(stream));
+  });
+}
+
 int rp_op_split_planes(const float* in, int64_t n, void* p0, void* p1, void* stream) {
   return guard([&] {
     if (n > 0) {
       need(in, "in");
       need(p0, "p0");
-      need(p1, "p1");
     }
     k::split_planes(in, n, p0, p1, S(stream));
   });

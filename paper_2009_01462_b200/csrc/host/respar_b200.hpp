@@ -231,6 +231,8 @@ class DecoupledTrainer {
     DeviceArray dpre_p, g_p;
     DeviceArray filters;  // plane path: the blocks' prepared filter pairs (forward, then reused for dgrad)
     bool tape_planes = false;
+    bool tape_bf16 = false;  // bf16 math: xps / aps / dpre_p / g_p hold single bf16 copies
+    std::vector<DeviceArray> dps;  // bf16 tape: bf16(1 - a^2) per block (as / dpre fp32 unused)
     DeviceArray x0, dpre, ws, red_ws, pooled, logits, loss;
     DeviceArray snap_lam, snap_kappa;
     int snap_rows = -1;

@@ -371,23 +371,33 @@ void DecoupledTrainer::ensure_capacity(int nrows) {
     Stage& st = stages_[k];
     if (st.cap_rows >= nrows) continue;
     const int n = st.end - st.begin;
+    const bool planes = rp_op_block_planes_supported(&geo_, nrows, math_) != 0;
+    const bool bf16t = rp_op_block_bf16_tape_supported(&geo_, nrows, math_) != 0;
+    // on the tape paths the backward reads the bf16 copies of the block inputs, so the fp32
+    // block inputs x_1.. only roll through two buffers (x_i feeds block i's forward alone)
+    const bool rolling = planes || bf16t;
     st.xs.resize(n);
     st.as.resize(n);
     for (int i = 0; i < n; ++i) {
-      if (i > 0) st.xs[i].allocate(st.device, (int64_t)nrows * feat() * 4);
-      st.as[i].allocate(st.device, (int64_t)nrows * hid() * 4);
+      if (i > 0 && (!rolling || i <= 2)) st.xs[i].allocate(st.device, (int64_t)nrows * feat() * 4);
+      if (!bf16t) st.as[i].allocate(st.device, (int64_t)nrows * hid() * 4);   // bf16 tape: a16 / d16 only
     }
     if (k == 0) st.x0.allocate(st.device, (int64_t)nrows * feat() * 4);
-    st.dpre.allocate(st.device, (int64_t)nrows * hid() * 4);
-    if (rp_op_block_planes_supported(&geo_, nrows, math_)) {
+    if (!bf16t) st.dpre.allocate(st.device, (int64_t)nrows * hid() * 4);
+    if (bf16t) {
+      st.dps.resize(n);
+      for (int i = 0; i < n; ++i) st.dps[i].allocate(st.device, (int64_t)nrows * hid() * 2);
+    }
+    if (rolling) {
+      const int64_t eb = planes ? 4 : 2;   // bytes per element: a bf16 plane pair, or one bf16 copy
       st.xps.resize(n);
       st.aps.resize(n);
       for (int i = 0; i < n; ++i) {
-        st.xps[i].allocate(st.device, (int64_t)nrows * feat() * 4);
-        st.aps[i].allocate(st.device, (int64_t)nrows * hid() * 4);
+        st.xps[i].allocate(st.device, (int64_t)nrows * feat() * eb);
+        st.aps[i].allocate(st.device, (int64_t)nrows * hid() * eb);
       }
-      st.dpre_p.allocate(st.device, (int64_t)nrows * hid() * 4);
-      st.g_p.allocate(st.device, (int64_t)nrows * feat() * 4);
+      st.dpre_p.allocate(st.device, (int64_t)nrows * hid() * eb);
+      st.g_p.allocate(st.device, (int64_t)nrows * feat() * eb);
       st.filters.allocate(st.device, std::max<int64_t>(256, rp_op_planes_filters_bytes(&geo_, n)));
     }
     st.ws.allocate(st.device, rp_op_workspace_bytes(&geo_, nrows, math_));
@@ -434,6 +444,22 @@ void DecoupledTrainer::run_forward(Stage& st, const float* input, int nrows, flo
   st.input0 = cur;
   const int n = st.end - st.begin;
   st.tape_planes = n > 0 && rp_op_block_planes_supported(&geo_, nrows, math_);
+  st.tape_bf16 = n > 0 && rp_op_block_bf16_tape_supported(&geo_, nrows, math_);
+  if (st.tape_bf16) {
+    // bf16 copies of every block input and activation for the TMA-fed bf16 wgrad
+    check(rp_op_split_planes(cur, (int64_t)nrows * feat(), st.xps[0].get(), nullptr, s));
+    for (int i = 0; i < n; ++i) {
+      const int l = st.begin + i;
+      float* out = i == n - 1 ? out_features : st.xs[1 + (i & 1)].get();
+      check(rp_op_block_fwd_bf16t(&geo_, nrows, cur, st.xps[i].get(), P + L.block0 + (int64_t)l * L.block_stride,
+                                  st.aps[i].get(), st.dps[i].get(), out,
+                                  i == n - 1 ? nullptr : st.xps[i + 1].get(), st.ws.get(), st.ws.bytes(), s));
+      cur = out;
+    }
+    if (st.index == stages() - 1)
+      check(rp_op_head_fwd(&geo_, nrows, out_features, P + L.t_w, st.pooled.get(), st.logits.get(), s));
+    return;
+  }
   if (st.tape_planes) {
     const int64_t e = (int64_t)nrows * feat();
     auto* p = st.xps[0].get<uint16_t>();
@@ -444,7 +470,7 @@ void DecoupledTrainer::run_forward(Stage& st, const float* input, int nrows, flo
                                     st.filters.get(), s));
     for (int i = 0; i < n; ++i) {
       const int l = st.begin + i;
-      float* out = i == n - 1 ? out_features : st.xs[i + 1].get();
+      float* out = i == n - 1 ? out_features : st.xs[1 + (i & 1)].get();
       check(rp_op_block_fwd_planes(&geo_, nrows, cur, st.xps[i].get(), P + L.block0 + (int64_t)l * L.block_stride,
                                    st.as[i].get(), out, st.aps[i].get(), i == n - 1 ? nullptr : st.xps[i + 1].get(),
                                    st.filters.get<char>() + i * fpair, st.ws.get(), st.ws.bytes(), s));
@@ -495,7 +521,16 @@ void DecoupledTrainer::run_backward(Stage& st, const int32_t* labels, int nrows,
     check(rp_op_synthetic_grad((int)kind_, lam_next, x_end, kap_next, n, w, g, st.red_ws.get(), s));
   }
   const int nb = st.end - st.begin;
-  if (st.tape_planes && st.fwd_rows == nrows) {
+  if (st.tape_bf16 && st.fwd_rows == nrows) {
+    auto* gp = st.g_p.get<uint16_t>();
+    check(rp_op_split_planes(g, n, gp, nullptr, s));
+    for (int i = nb - 1; i >= 0; --i) {
+      const int l = st.begin + i;
+      const int64_t off = L.block0 + (int64_t)l * L.block_stride;
+      check(rp_op_block_bwd_bf16t(&geo_, nrows, st.xps[i].get(), st.aps[i].get(), st.dps[i].get(), P + off, g, gp,
+                                  st.dpre_p.get(), G + off, st.ws.get(), st.ws.bytes(), s));
+    }
+  } else if (st.tape_planes && st.fwd_rows == nrows) {
     auto* gp = st.g_p.get<uint16_t>();
     check(rp_op_split_planes(g, n, gp, gp + n, s));
     // every block's input-gradient filters in one launch, from the current parameters
@@ -509,13 +544,16 @@ void DecoupledTrainer::run_backward(Stage& st, const int32_t* labels, int nrows,
                                    st.dpre.get(), st.dpre_p.get(), G + off, st.filters.get<char>() + i * fpair,
                                    st.ws.get(), st.ws.bytes(), s));
     }
-  } else
+  } else {
+    if ((st.tape_planes && nb > 1) || st.tape_bf16)   // the fp32 block inputs / activations were not kept
+      throw std::logic_error("stage_backward_update: rows differ from the stage's forward");
   for (int i = nb - 1; i >= 0; --i) {
     const int l = st.begin + i;
     const float* xin = i == 0 ? st.input0 : st.xs[i].get();
     const int64_t off = L.block0 + (int64_t)l * L.block_stride;
     check(rp_op_block_bwd(&geo_, nrows, xin, st.as[i].get(), P + off, g, st.dpre.get(), G + off, math_, st.ws.get(),
                           st.ws.bytes(), s));
+  }
   }
   if (k == 0) check(rp_op_stem_bwd(&geo_, nrows, st.raw, g, G, st.ws.get(), st.ws.bytes(), s));
   // apply_updates (network.cpp:174-191): the stage's parameter range is contiguous

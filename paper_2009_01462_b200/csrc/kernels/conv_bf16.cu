@@ -47,7 +47,10 @@ struct BfArgs {
   const __nv_bfloat16* w;   // prepped [cb][chunk][tap][kg][128 rows][8]
   const float* bias;
   const float* aux;
-  float* out;
+  const __nv_bfloat16* aux16;   // EPI_DTANH16: bf16(1 - a^2)
+  float* out;                   // may be null (bf16 tape outputs only)
+  __nv_bfloat16* out16;         // optional bf16 copy of out (the bf16 wgrad's operand)
+  __nv_bfloat16* out16d;        // optional bf16(1 - out^2)
 };
 
 // Work split as in conv_tc.cu: full kS-tile units round-robin from CTA 0, the per-image
@@ -90,7 +93,10 @@ __device__ __forceinline__ uint32_t pack_bf16(float a, float b) {
   return *reinterpret_cast<const uint32_t*>(&v);
 }
 
-template <int EPI>
+// BIN: the input is a bf16 tensor; TMA writes the halo chunk straight into the bf16 slot
+// (box 8 channels x positions x 4 channel groups = the [kg][pos][8] layout the MMA reads),
+// the converter warps idle and the MMA waits on the TMA barrier.
+template <int EPI, bool BIN>
 __global__ void __launch_bounds__(kThreads, 1)
     conv3x3_bf16_kernel(const __grid_constant__ CUtensorMap tmap, const BfArgs a) {
   extern __shared__ __align__(1024) uint8_t smem[];
@@ -156,10 +162,18 @@ __global__ void __launch_bounds__(kThreads, 1)
       const __nv_bfloat16* wcb = a.w + (int64_t)cb * a.nchunks * 9 * (a.w_tap / 2);
       const int y0 = (tile0 * 128) / Wp;
       for (int c = 0; c < a.nchunks; ++c) {
-        mbar_wait(&raw_empty[rs], rph ^ 1);
-        if (elect_one()) {
-          mbar_arrive_expect_tx(&raw_full[rs], a.raw_bytes);
-          tma_load_5d(&tmap, &raw_full[rs], raw_s(rs), 0, -1, y0 - 1, 8 * c, n);
+        if constexpr (BIN) {
+          mbar_wait(&bf_empty[rs], rph ^ 1);   // the MMA is done with this bf16 slot
+          if (elect_one()) {
+            mbar_arrive_expect_tx(&raw_full[rs], a.bf_bytes);
+            tma_load_5d(&tmap, &raw_full[rs], bf_s(rs), 0, -1, y0 - 1, 4 * c, n);
+          }
+        } else {
+          mbar_wait(&raw_empty[rs], rph ^ 1);
+          if (elect_one()) {
+            mbar_arrive_expect_tx(&raw_full[rs], a.raw_bytes);
+            tma_load_5d(&tmap, &raw_full[rs], raw_s(rs), 0, -1, y0 - 1, 8 * c, n);
+          }
         }
         __syncwarp();
         if (++rs == 2) rs = 0, rph ^= 1;
@@ -193,7 +207,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       tc_fence_after();
       const uint32_t d0 = tmem_base + (uint32_t)(ab * kS * 128);
       for (int c = 0; c < a.nchunks; ++c) {
-        mbar_wait(&bf_full[bs], bph);
+        mbar_wait(BIN ? &raw_full[bs] : &bf_full[bs], bph);
         tc_fence_after();
         const uint64_t dx0 = desc_kmajor_interleave(smem_u32(bf_s(bs)), kg_x, 128);
         for (int dy = 0; dy < 3; ++dy) {
@@ -228,6 +242,8 @@ __global__ void __launch_bounds__(kThreads, 1)
       if (++ab == 2) ab = 0, aph ^= 1;
     }
   } else if (warp < 6) {
+    if constexpr (BIN) {}   // nothing to convert
+    else {
     // ===================== converters: fp32 halo -> bf16 K-major interleave =====================
     // raw [g = 8 groups of 4 ch][pos][4 floats]  ->  bf16 [k = 4 groups of 8 ch][pos][8 bf16]
     const int tid = threadIdx.x - 64;
@@ -255,6 +271,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (++bs == 2) bs = 0, bph ^= 1;
       }
     }
+    }
   } else {
     // ===================== epilogue =====================
     // TMEM lane r = output channel cb*128 + r; a warp owns lanes 32q..32q+31 and walks
@@ -262,6 +279,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int q = warp & 3;
     constexpr bool kBias = EPI == EPI_BIAS || EPI == EPI_BIAS_TANH || EPI == EPI_RESID;
     constexpr bool kAux = EPI == EPI_RESID || EPI == EPI_TANH_BWD || EPI == EPI_ADD;
+    constexpr bool kAux16 = EPI == EPI_DTANH16;
     int ab = 0;
     uint32_t aph = 0;
     UnitIter it(a.Co / 128, a.N, a.T);
@@ -271,7 +289,10 @@ __global__ void __launch_bounds__(kThreads, 1)
       const int co = cb * 128 + q * 32 + lane;
       const float bias = kBias ? __ldg(a.bias + co) : 0.f;
       const float* auxb = kAux ? a.aux + img * a.Co + co : nullptr;
-      float* outb = a.out + img * a.Co + co;
+      float* outb = a.out ? a.out + img * a.Co + co : nullptr;
+      __nv_bfloat16* outb16 = a.out16 ? a.out16 + img * a.Co + co : nullptr;
+      __nv_bfloat16* outb16d = a.out16d ? a.out16d + img * a.Co + co : nullptr;
+      const __nv_bfloat16* auxb16 = kAux16 ? a.aux16 + img * a.Co + co : nullptr;
       mbar_wait(&acc_full[ab], aph);
       tc_fence_after();
       for (int s = 0; s < ntiles; ++s) {
@@ -292,6 +313,10 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
             for (int e = 0; e < 16; ++e) ax[e] = auxb[off[e]];
           }
+          if constexpr (kAux16) {
+#pragma unroll
+            for (int e = 0; e < 16; ++e) ax[e] = __bfloat162float(auxb16[off[e]]);
+          }
           uint32_t r[16];
           tmem_ld16(tcol + (uint32_t)p0, r);
           tmem_wait_ld();
@@ -305,8 +330,11 @@ __global__ void __launch_bounds__(kThreads, 1)
             else if constexpr (EPI == EPI_RESID) o = ax[e] + a.h * (v + bias);
             else if constexpr (EPI == EPI_TANH_BWD) o = (a.h * v) * (1.f - ax[e] * ax[e]);
             else if constexpr (EPI == EPI_ADD) o = ax[e] + v;
+            else if constexpr (EPI == EPI_DTANH16) o = (a.h * v) * ax[e];
             else o = a.h * v;
-            outb[off[e]] = o;
+            if (outb) outb[off[e]] = o;
+            if (outb16) outb16[off[e]] = __float2bfloat16_rn(o);
+            if (outb16d) outb16d[off[e]] = __float2bfloat16_rn(1.f - o * o);
           }
         }
       }
@@ -385,6 +413,22 @@ CUtensorMap make_halo_map(const float* in, const ConvShape& s, int Wp, int rows_
   return m;
 }
 
+// NHWC bf16 as 5-D (8 ch, W, H, C/8 groups, N); box (8, W+2 from x = -1, rows, 4 groups, 1):
+// the bf16 slot layout [kg][pos][8]
+CUtensorMap make_halo_map16(const void* in, const ConvShape& s, int Wp, int rows_h) {
+  CUtensorMap m;
+  const cuuint64_t dims[5] = {8, (cuuint64_t)s.w, (cuuint64_t)s.h, (cuuint64_t)(s.ci / 8), (cuuint64_t)s.n};
+  const cuuint64_t strides[4] = {(cuuint64_t)s.ci * 2, (cuuint64_t)s.w * s.ci * 2, 16,
+                                 (cuuint64_t)s.h * s.w * s.ci * 2};
+  const cuuint32_t box[5] = {8, (cuuint32_t)Wp, (cuuint32_t)rows_h, 4, 1};
+  const cuuint32_t estr[5] = {1, 1, 1, 1, 1};
+  CUresult r = encode_fn()(&m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 5, const_cast<void*>(in), dims, strides, box, estr,
+                           CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                           CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) fail(RP_ERR_CUDA, "cuTensorMapEncodeTiled (bf16 conv, bf16 in) failed (" + std::to_string((int)r) + ")");
+  return m;
+}
+
 struct Plan {
   bool ok = false;
   int Wp, rows_h, halo_pos, T;
@@ -392,7 +436,7 @@ struct Plan {
   size_t smem;
 };
 
-Plan plan_for(const ConvShape& s) {
+Plan plan_for(const ConvShape& s, bool bin = false) {
   Plan p;
   if (s.co % 128 != 0 || s.ci % kChunk != 0 || s.w + 2 > 256) return p;
   p.Wp = s.w + 2;
@@ -401,7 +445,7 @@ Plan plan_for(const ConvShape& s) {
   p.halo_pos = p.rows_h * p.Wp;
   p.T = (s.h * p.Wp + 127) / 128;
   p.raw_bytes = (uint32_t)p.halo_pos * kChunk * 4u;
-  p.raw_stride = (p.raw_bytes + 1023) / 1024 * 1024;
+  p.raw_stride = bin ? 0u : (p.raw_bytes + 1023) / 1024 * 1024;   // bf16 input: no fp32 staging
   p.bf_bytes = (uint32_t)p.halo_pos * kChunk * 2u;
   p.bf_stride = (128 + p.bf_bytes + 128 + 1023) / 1024 * 1024;
   p.w_tap = 4u * 128u * 16u;
@@ -411,27 +455,42 @@ Plan plan_for(const ConvShape& s) {
 }
 
 std::mutex g_map_mu;
-std::map<std::tuple<const void*, int, int, int, int, int>, CUtensorMap> g_maps;
+std::map<std::tuple<const void*, int, int, int, int, int, int>, CUtensorMap> g_maps;
 
-const CUtensorMap& cached_map(const float* in, const ConvShape& s, int Wp, int rows_h) {
+const CUtensorMap& cached_map(const void* in, const ConvShape& s, int Wp, int rows_h, bool bin = false) {
   std::lock_guard<std::mutex> lk(g_map_mu);
-  auto key = std::make_tuple((const void*)in, s.n, s.h, s.w, s.ci, rows_h);
+  auto key = std::make_tuple(in, s.n, s.h, s.w, s.ci, rows_h, bin ? 1 : 0);
   auto it = g_maps.find(key);
   if (it == g_maps.end()) {
     if (g_maps.size() > 4096) g_maps.clear();
-    it = g_maps.emplace(key, make_halo_map(in, s, Wp, rows_h)).first;
+    it = g_maps.emplace(key, bin ? make_halo_map16(in, s, Wp, rows_h)
+                                 : make_halo_map(static_cast<const float*>(in), s, Wp, rows_h)).first;
   }
   return it->second;
 }
 
-template <int EPI>
+template <int EPI, bool BIN>
 void launch(const CUtensorMap& m, const BfArgs& a, size_t smem, int grid, cudaStream_t st) {
   static bool configured = false;
   if (!configured) {
-    RP_CUDA(cudaFuncSetAttribute(conv3x3_bf16_kernel<EPI>, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxSmem));
+    RP_CUDA(cudaFuncSetAttribute(conv3x3_bf16_kernel<EPI, BIN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 kMaxSmem));
     configured = true;
   }
-  conv3x3_bf16_kernel<EPI><<<grid, kThreads, smem, st>>>(m, a);
+  conv3x3_bf16_kernel<EPI, BIN><<<grid, kThreads, smem, st>>>(m, a);
+}
+
+template <bool BIN>
+void launch_epi(int epi, const CUtensorMap& m, const BfArgs& a, size_t smem, int grid, cudaStream_t st) {
+  switch (epi) {
+    case EPI_BIAS: launch<EPI_BIAS, BIN>(m, a, smem, grid, st); break;
+    case EPI_BIAS_TANH: launch<EPI_BIAS_TANH, BIN>(m, a, smem, grid, st); break;
+    case EPI_RESID: launch<EPI_RESID, BIN>(m, a, smem, grid, st); break;
+    case EPI_TANH_BWD: launch<EPI_TANH_BWD, BIN>(m, a, smem, grid, st); break;
+    case EPI_ADD: launch<EPI_ADD, BIN>(m, a, smem, grid, st); break;
+    case EPI_DTANH16: launch<EPI_DTANH16, BIN>(m, a, smem, grid, st); break;
+    default: launch<EPI_SCALE, BIN>(m, a, smem, grid, st); break;
+  }
 }
 
 }  // namespace
@@ -440,11 +499,14 @@ bool conv3x3_bf16_supported(const ConvShape& s) { return plan_for(s).ok; }
 
 int64_t conv3x3_bf16_ws_bytes(const ConvShape& s) { return 9LL * s.ci * s.co * 2 + 256; }
 
-void conv3x3_fwd_bf16(const ConvShape& s, const float* in, const float* w_hwio, bool dgrad_weights, const float* bias,
-                      const float* aux, float h, int epi, float* out, void* ws, cudaStream_t st) {
+namespace {
+void conv_bf16_any(const ConvShape& s, const void* in, bool bin, const float* w_hwio, bool dgrad_weights,
+                   const float* bias, const float* aux, const void* aux16, float h, int epi, float* out, void* out16,
+                   void* out16d, void* ws, cudaStream_t st) {
   if (s.pixels() == 0) return;
-  const Plan p = plan_for(s);
+  const Plan p = plan_for(s, bin);
   if (!p.ok) fail(RP_ERR_INTERNAL, "conv3x3_fwd_bf16: unsupported shape");
+  if (epi == EPI_DTANH16 && !aux16) fail(RP_ERR_INTERNAL, "conv3x3_fwd_bf16: EPI_DTANH16 needs aux16");
   __nv_bfloat16* wp = static_cast<__nv_bfloat16*>(ws);
   const int ci_src = dgrad_weights ? s.co : s.ci;
   const int co_src = dgrad_weights ? s.ci : s.co;
@@ -472,19 +534,30 @@ void conv3x3_fwd_bf16(const ConvShape& s, const float* in, const float* w_hwio, 
   a.w = wp;
   a.bias = bias;
   a.aux = aux;
+  a.aux16 = static_cast<const __nv_bfloat16*>(aux16);
   a.out = out;
-  const CUtensorMap& m = cached_map(in, s, p.Wp, p.rows_h);
+  a.out16 = static_cast<__nv_bfloat16*>(out16);
+  a.out16d = static_cast<__nv_bfloat16*>(out16d);
+  const CUtensorMap& m = cached_map(in, s, p.Wp, p.rows_h, bin);
   const int units = (s.co / 128) * s.n * ((p.T + kS - 1) / kS);
   const int grid = std::min(units, kNumSMs);
-  switch (epi) {
-    case EPI_BIAS: launch<EPI_BIAS>(m, a, p.smem, grid, st); break;
-    case EPI_BIAS_TANH: launch<EPI_BIAS_TANH>(m, a, p.smem, grid, st); break;
-    case EPI_RESID: launch<EPI_RESID>(m, a, p.smem, grid, st); break;
-    case EPI_TANH_BWD: launch<EPI_TANH_BWD>(m, a, p.smem, grid, st); break;
-    case EPI_ADD: launch<EPI_ADD>(m, a, p.smem, grid, st); break;
-    default: launch<EPI_SCALE>(m, a, p.smem, grid, st); break;
-  }
+  if (bin)
+    launch_epi<true>(epi, m, a, p.smem, grid, st);
+  else
+    launch_epi<false>(epi, m, a, p.smem, grid, st);
   RP_LAUNCHED();
+}
+}  // namespace
+
+void conv3x3_fwd_bf16(const ConvShape& s, const float* in, const float* w_hwio, bool dgrad_weights, const float* bias,
+                      const float* aux, float h, int epi, float* out, void* ws, cudaStream_t st, void* out_bf16) {
+  conv_bf16_any(s, in, false, w_hwio, dgrad_weights, bias, aux, nullptr, h, epi, out, out_bf16, nullptr, ws, st);
+}
+
+void conv3x3_fwd_bf16_in16(const ConvShape& s, const void* in16, const float* w_hwio, bool dgrad_weights,
+                           const float* bias, const float* aux, const void* aux16, float h, int epi, float* out,
+                           void* out16, void* out16d, void* ws, cudaStream_t st) {
+  conv_bf16_any(s, in16, true, w_hwio, dgrad_weights, bias, aux, aux16, h, epi, out, out16, out16d, ws, st);
 }
 
 }  // namespace rp::k

@@ -14,6 +14,12 @@
 // 3 taps per tap group (TMEM 3 x 128 columns), (co block, ci block, tap group) work groups,
 // per-CTA partials and a fixed-order fp64 reduce, as in conv_wgrad_tc.cu.  The bias sums
 // g0 + g1 from the staged planes (bias warps, Kahan-compensated fp32).
+//
+// Single-plane mode (RP_MATH_BF16, config C5): x and g are one bf16 plane each (the bf16
+// conv epilogues write them); the two 64-channel atoms of A and B are then channels
+// [128 cob, +64) and [128 cob + 64, +64) of the same plane, so the identical MMA stream
+// yields a 128 co x 128 ci tile per tap, the epilogue stores all four quadrants and the
+// bias warps sum 128 channels.
 #include <cuda.h>
 #include <cuda_bf16.h>
 
@@ -40,14 +46,15 @@ constexpr int kTg = 3;              // taps per group
 
 struct PwArgs {
   int N, H, W, Ci, Co, Wp, rg, P, Pp, nstages;
-  int mo, mi;                    // 64-channel co / ci blocks
+  int mo, mi;                    // co / ci blocks (64 channels, single: 128)
+  int single;                    // 1: one bf16 plane per operand, 128-channel blocks
   int blocks_per_img, num_blocks;
   uint32_t g_slab;               // bytes per bf16 g plane slab (Pp rows x 128 B, 1 KB aligned)
   uint32_t x_slab;               // bytes per bf16 x plane slab (rg * Wp rows of one filter row, packed)
   uint32_t x_off;
   uint32_t stage;
-  float* part;                   // [grid][kTg * 64 (ci)][64 (co)]
-  double* part_bias;             // [grid][64]
+  float* part;                   // [grid][kTg * cblk (ci)][cblk (co)]
+  double* part_bias;             // [grid][cblk]
 };
 
 __device__ __forceinline__ int grp_start(int gid, int grid, const PwArgs& a) {
@@ -69,7 +76,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint64_t* bias_free = bars + 2 * kMaxStages;  // [S] bias warps -> TMA
   uint64_t* acc_full = bars + 3 * kMaxStages;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 3 * kMaxStages + 1);
-  double* bsum = reinterpret_cast<double*>(bars + 3 * kMaxStages + 2);   // [4 warps][64]
+  double* bsum = reinterpret_cast<double*>(bars + 3 * kMaxStages + 2);   // [4 warps][128]
 
   auto g_slab = [&](int s, int j) { return smem + s * a.stage + j * a.g_slab; };
   auto x_slab = [&](int s, int j) { return smem + s * a.stage + a.x_off + j * a.x_slab; };
@@ -124,10 +131,17 @@ __global__ void __launch_bounds__(kThreads, 1)
       if (do_bias) mbar_wait(&bias_free[s], ph ^ 1);
       if (elect_one()) {
         mbar_arrive_expect_tx(&full[s], bytes);
-        tma_load_4d(&tg0, &full[s], g_slab(s, 0), 64 * cob, -1, y0, n);
-        tma_load_4d(&tg1, &full[s], g_slab(s, 1), 64 * cob, -1, y0, n);
-        tma_load_4d(&tx0, &full[s], x_slab(s, 0), 64 * cib, -1, y0 - 1 + gi, n);
-        tma_load_4d(&tx1, &full[s], x_slab(s, 1), 64 * cib, -1, y0 - 1 + gi, n);
+        if (a.single) {   // the two 64-channel atoms of one plane
+          tma_load_4d(&tg0, &full[s], g_slab(s, 0), 128 * cob, -1, y0, n);
+          tma_load_4d(&tg0, &full[s], g_slab(s, 1), 128 * cob + 64, -1, y0, n);
+          tma_load_4d(&tx0, &full[s], x_slab(s, 0), 128 * cib, -1, y0 - 1 + gi, n);
+          tma_load_4d(&tx0, &full[s], x_slab(s, 1), 128 * cib + 64, -1, y0 - 1 + gi, n);
+        } else {
+          tma_load_4d(&tg0, &full[s], g_slab(s, 0), 64 * cob, -1, y0, n);
+          tma_load_4d(&tg1, &full[s], g_slab(s, 1), 64 * cob, -1, y0, n);
+          tma_load_4d(&tx0, &full[s], x_slab(s, 0), 64 * cib, -1, y0 - 1 + gi, n);
+          tma_load_4d(&tx1, &full[s], x_slab(s, 1), 64 * cib, -1, y0 - 1 + gi, n);
+        }
       }
       __syncwarp();
       if (++s == S) s = 0, ph ^= 1;
@@ -174,12 +188,15 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (do_bias) {
       const int tid = threadIdx.x - 64;
       const int cq = tid & 7, r0 = tid >> 3;
-      float bs[8] = {0, 0, 0, 0, 0, 0, 0, 0}, bk[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+      // pair mode: bs[0..7] = channels 8 cq + e of g0 + g1; single: bs[8 j + e] = channel
+      // 64 j + 8 cq + e (atom j)
+      float bs[16] = {}, bk[16] = {};
+      const bool single = a.single != 0;
       int s = 0;
       uint32_t ph = 0;
       for (int b = blk_beg; b < blk_end; ++b) {
         mbar_wait(&full[s], ph);
-        float bf[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+        float bf[16] = {};
         const uint8_t* p0 = g_slab(s, 0);
         const uint8_t* p1 = g_slab(s, 1);
         const uint32_t base0 = smem_u32(p0), base1 = smem_u32(p1);
@@ -189,14 +206,24 @@ __global__ void __launch_bounds__(kThreads, 1)
           const uint4 v = *reinterpret_cast<const uint4*>(p1 + (size_t)p * 128 + ((cq ^ ph1) << 4));
           const __nv_bfloat162* uh = reinterpret_cast<const __nv_bfloat162*>(&u);
           const __nv_bfloat162* vh = reinterpret_cast<const __nv_bfloat162*>(&v);
+          if (single) {
 #pragma unroll
-          for (int e = 0; e < 4; ++e) {
-            bf[2 * e] += __low2float(uh[e]) + __low2float(vh[e]);
-            bf[2 * e + 1] += __high2float(uh[e]) + __high2float(vh[e]);
+            for (int e = 0; e < 4; ++e) {
+              bf[2 * e] += __low2float(uh[e]);
+              bf[2 * e + 1] += __high2float(uh[e]);
+              bf[8 + 2 * e] += __low2float(vh[e]);
+              bf[8 + 2 * e + 1] += __high2float(vh[e]);
+            }
+          } else {
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+              bf[2 * e] += __low2float(uh[e]) + __low2float(vh[e]);
+              bf[2 * e + 1] += __high2float(uh[e]) + __high2float(vh[e]);
+            }
           }
         }
 #pragma unroll
-        for (int e = 0; e < 8; ++e) {
+        for (int e = 0; e < 16; ++e) {
           const float y = bf[e] - bk[e];
           const float t = bs[e] + y;
           bk[e] = (t - bs[e]) - y;
@@ -207,18 +234,20 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
       // threads t, t + 8, ... (same cq) combine in fixed order: lanes xor 8, 16, then warps
       const int cw = tid / 32;
+      const int nch = single ? 128 : 64;
 #pragma unroll
-      for (int e = 0; e < 8; ++e) {
+      for (int e = 0; e < 16; ++e) {
+        if (e >= 8 && !single) break;
         double d = (double)bs[e] - (double)bk[e];
         d += __shfl_xor_sync(0xffffffffu, d, 8);
         d += __shfl_xor_sync(0xffffffffu, d, 16);
-        if (lane < 8) bsum[cw * 64 + 8 * cq + e] = d;
+        if (lane < 8) bsum[cw * 128 + (e >> 3) * 64 + 8 * cq + (e & 7)] = d;
       }
       asm volatile("bar.sync 1, 128;" ::: "memory");
-      if (tid < 64) {
+      if (tid < nch) {
         double t = 0.0;
-        for (int w = 0; w < 4; ++w) t += bsum[w * 64 + tid];
-        a.part_bias[(size_t)blockIdx.x * 64 + tid] = t;
+        for (int w = 0; w < 4; ++w) t += bsum[w * 128 + tid];
+        a.part_bias[(size_t)blockIdx.x * nch + tid] = t;
       }
     }
   } else {
@@ -239,6 +268,21 @@ __global__ void __launch_bounds__(kThreads, 1)
     // stage memory is drained once the last MMAs completed and the bias warps let go
     if (do_bias) asm volatile("bar.sync 3, 256;" ::: "memory");
     const uint32_t trow = tmem_base + ((uint32_t)(q * 32) << 16);
+    if (a.single) {
+      // lane r = co r, column c = ci c of each tap: every quadrant is its own output
+      float* dst1 = a.part + (size_t)blockIdx.x * kTg * 128 * 128;
+      const int co1 = q * 32 + lane;
+      for (int ti = 0; ti < kTg; ++ti) {
+        for (int c = 0; c < 128; c += 16) {
+          uint32_t r[16];
+          tmem_ld16(trow + (uint32_t)(ti * 128 + c), r);
+          tmem_wait_ld();
+#pragma unroll
+          for (int e = 0; e < 16; ++e)
+            dst1[(size_t)(ti * 128 + c + e) * 128 + co1] = any ? __uint_as_float(r[e]) : 0.f;
+        }
+      }
+    } else
     for (int pass = 0; pass < 2; ++pass) {
       const bool mine = (pass == 0) == (q >= 2);
       if (mine) {
@@ -278,25 +322,26 @@ __global__ void wgrad_planes_reduce_kernel(const float* __restrict__ part, const
                                            float* __restrict__ gb) {
   const int Ci = a.Ci, Co = a.Co;
   const int total = 9 * Ci * Co;
-  const int64_t pstride = (int64_t)kTg * 64 * 64;
+  const int cbk = a.single ? 128 : 64;
+  const int64_t pstride = (int64_t)kTg * cbk * cbk;
   for (int idx = blockIdx.x * blockDim.x + threadIdx.x; idx < total + Co; idx += gridDim.x * blockDim.x) {
     if (idx < total) {
       const int co = idx % Co;
       const int ci = (idx / Co) % Ci;
       const int tap = idx / (Co * Ci);
-      const int gi = tap / kTg, cob = co / 64, cib = ci / 64;
+      const int gi = tap / kTg, cob = co / cbk, cib = ci / cbk;
       const int gid = (cob * a.mi + cib) * 3 + gi;
       const int c_lo = grp_start(gid, grid, a), c_hi = grp_start(gid + 1, grid, a);
-      const int64_t off = ((int64_t)(tap - gi * kTg) * 64 + (ci - cib * 64)) * 64 + (co - cob * 64);
+      const int64_t off = ((int64_t)(tap - gi * kTg) * cbk + (ci - cib * cbk)) * cbk + (co - cob * cbk);
       double s = 0.0;
       for (int b = c_lo; b < c_hi; ++b) s += (double)part[b * pstride + off];
       gw[idx] = (float)(scale * s);
     } else if (gb) {
-      const int co = idx - total, cob = co / 64;
+      const int co = idx - total, cob = co / cbk;
       const int gid = cob * a.mi * 3;
       const int c_lo = grp_start(gid, grid, a), c_hi = grp_start(gid + 1, grid, a);
       double s = 0.0;
-      for (int b = c_lo; b < c_hi; ++b) s += part_bias[(int64_t)b * 64 + (co - cob * 64)];
+      for (int b = c_lo; b < c_hi; ++b) s += part_bias[(int64_t)b * cbk + (co - cob * cbk)];
       gb[co] = (float)(scale * s);
     }
   }
@@ -311,7 +356,7 @@ __global__ void split_planes_kernel(const float4* __restrict__ in, int64_t n4, u
     const __nv_bfloat162 c = __floats2bfloat162_rn(v.x - __low2float(a), v.y - __high2float(a));
     const __nv_bfloat162 d = __floats2bfloat162_rn(v.z - __low2float(b), v.w - __high2float(b));
     p0[i] = make_uint2(*reinterpret_cast<const uint32_t*>(&a), *reinterpret_cast<const uint32_t*>(&b));
-    p1[i] = make_uint2(*reinterpret_cast<const uint32_t*>(&c), *reinterpret_cast<const uint32_t*>(&d));
+    if (p1) p1[i] = make_uint2(*reinterpret_cast<const uint32_t*>(&c), *reinterpret_cast<const uint32_t*>(&d));
   }
 }
 
@@ -371,10 +416,11 @@ struct PwPlan {
   size_t smem;
 };
 
-PwPlan plan(const ConvShape& s) {
+PwPlan plan(const ConvShape& s, bool single = false) {
   PwPlan p;
-  if (s.co % 64 != 0 || s.ci % 64 != 0 || s.w + 2 > 256) return p;
-  if (3 * (s.co / 64) * (s.ci / 64) > kNumSMs) return p;
+  const int cbk = single ? 128 : 64;
+  if (s.co % cbk != 0 || s.ci % cbk != 0 || s.w + 2 > 256) return p;
+  if (3 * (s.co / cbk) * (s.ci / cbk) > kNumSMs) return p;
   const int Wp = s.w + 2;
   // (rows per block, stages) in order of preference
   const int cand[][2] = {{4, 3}, {3, 3}, {2, 3}, {4, 2}, {2, 2}, {1, 2}};
@@ -389,9 +435,9 @@ PwPlan plan(const ConvShape& s) {
     q.x_slab = (uint32_t)rg * Wp * 128u;   // one filter row's x rows per tap group
     q.x_off = 2 * q.g_slab + kLead;
     q.stage = round1k((uint64_t)q.x_off + 2ull * q.x_slab + kTrail);
-    q.smem = st * (size_t)q.stage + (3 * kMaxStages + 2) * 8 + 4 * 64 * 8 + 256;
+    q.smem = st * (size_t)q.stage + (3 * kMaxStages + 2) * 8 + 4 * 128 * 8 + 256;
     if (q.smem > (size_t)kMaxSmem) continue;
-    if ((size_t)kTg * 64 * 64 * 4 > st * (size_t)q.stage) continue;
+    if ((size_t)kTg * 64 * 64 * 4 > st * (size_t)q.stage) continue;   // the pair epilogue's park buffer
     q.grid = kNumSMs;
     q.ok = true;
     return q;
@@ -399,7 +445,10 @@ PwPlan plan(const ConvShape& s) {
   return p;
 }
 
-int64_t part_bytes(const PwPlan& p) { return ((int64_t)p.grid * kTg * 64 * 64 * 4 + 255) / 256 * 256; }
+int64_t part_bytes(const PwPlan& p, bool single = false) {
+  const int64_t cbk = single ? 128 : 64;
+  return ((int64_t)p.grid * kTg * cbk * cbk * 4 + 255) / 256 * 256;
+}
 
 }  // namespace
 
@@ -421,11 +470,14 @@ void split_planes(const float* in, int64_t n, void* p0, void* p1, cudaStream_t s
   RP_LAUNCHED();
 }
 
-void conv3x3_wgrad_planes(const ConvShape& s, const void* x0, const void* x1, const void* g0, const void* g1,
-                          float scale, float* gw, float* gb, void* ws, cudaStream_t st) {
-  const PwPlan p = plan(s);
+namespace {
+void launch_wgrad_planes(const ConvShape& s, const void* x0, const void* x1, const void* g0, const void* g1,
+                         float scale, float* gw, float* gb, void* ws, cudaStream_t st, bool single) {
+  const PwPlan p = plan(s, single);
   if (!p.ok) fail(RP_ERR_INTERNAL, "conv3x3_wgrad_planes: unsupported shape");
+  const int cbk = single ? 128 : 64;
   PwArgs a{};
+  a.single = single ? 1 : 0;
   a.N = s.n;
   a.H = s.h;
   a.W = s.w;
@@ -436,8 +488,8 @@ void conv3x3_wgrad_planes(const ConvShape& s, const void* x0, const void* x1, co
   a.P = p.P;
   a.Pp = p.Pp;
   a.nstages = p.nstages;
-  a.mo = s.co / 64;
-  a.mi = s.ci / 64;
+  a.mo = s.co / cbk;
+  a.mi = s.ci / cbk;
   a.blocks_per_img = (s.h + p.rg - 1) / p.rg;
   a.num_blocks = s.n * a.blocks_per_img;
   a.g_slab = p.g_slab;
@@ -445,11 +497,11 @@ void conv3x3_wgrad_planes(const ConvShape& s, const void* x0, const void* x1, co
   a.x_off = p.x_off;
   a.stage = p.stage;
   a.part = static_cast<float*>(ws);
-  a.part_bias = reinterpret_cast<double*>(static_cast<char*>(ws) + part_bytes(p));
+  a.part_bias = reinterpret_cast<double*>(static_cast<char*>(ws) + part_bytes(p, single));
   const CUtensorMap& mg0 = cached(g0, s.n, s.h, s.w, s.co, p.rg);
-  const CUtensorMap& mg1 = cached(g1, s.n, s.h, s.w, s.co, p.rg);
+  const CUtensorMap& mg1 = cached(single ? g0 : g1, s.n, s.h, s.w, s.co, p.rg);
   const CUtensorMap& mx0 = cached(x0, s.n, s.h, s.w, s.ci, p.rg);
-  const CUtensorMap& mx1 = cached(x1, s.n, s.h, s.w, s.ci, p.rg);
+  const CUtensorMap& mx1 = cached(single ? x0 : x1, s.n, s.h, s.w, s.ci, p.rg);
   static bool configured = false;
   if (!configured) {
     RP_CUDA(cudaFuncSetAttribute(wgrad_planes_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxSmem));
@@ -461,6 +513,25 @@ void conv3x3_wgrad_planes(const ConvShape& s, const void* x0, const void* x1, co
   wgrad_planes_reduce_kernel<<<ceil_div(total, 256), 256, 0, st>>>(a.part, a.part_bias, a, p.grid, (double)scale,
                                                                    gw, gb);
   RP_LAUNCHED();
+}
+}  // namespace
+
+void conv3x3_wgrad_planes(const ConvShape& s, const void* x0, const void* x1, const void* g0, const void* g1,
+                          float scale, float* gw, float* gb, void* ws, cudaStream_t st) {
+  launch_wgrad_planes(s, x0, x1, g0, g1, scale, gw, gb, ws, st, false);
+}
+
+bool conv3x3_wgrad_bf16p_supported(const ConvShape& s) { return plan(s, true).ok; }
+
+int64_t conv3x3_wgrad_bf16p_ws_bytes(const ConvShape& s) {
+  const PwPlan p = plan(s, true);
+  if (!p.ok) return 0;
+  return part_bytes(p, true) + (int64_t)p.grid * 128 * 8 + 256;
+}
+
+void conv3x3_wgrad_bf16p(const ConvShape& s, const void* x, const void* g, float scale, float* gw, float* gb,
+                         void* ws, cudaStream_t st) {
+  launch_wgrad_planes(s, x, nullptr, g, nullptr, scale, gw, gb, ws, st, true);
 }
 
 }  // namespace rp::k

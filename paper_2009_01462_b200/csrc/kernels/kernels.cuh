@@ -30,7 +30,8 @@ enum Epilogue : int {
   EPI_RESID = 2,     // out = aux + h (acc + bias)                 (conv2: x' = x + h f)
   EPI_TANH_BWD = 3,  // out = h acc (1 - aux^2)                    (dgrad2 -> dpre, aux = a)
   EPI_ADD = 4,       // out = aux + acc   (in place allowed)       (dgrad1: g_prev = g + ...)
-  EPI_SCALE = 5      // out = h acc                                (identity dgrad2)
+  EPI_SCALE = 5,     // out = h acc                                (identity dgrad2)
+  EPI_DTANH16 = 6    // out = h acc aux16, aux16 = bf16(1 - a^2)   (bf16 tape dgrad2)
 };
 
 struct ConvShape {
@@ -71,8 +72,17 @@ void prep_filters_planes(const float* pb, int64_t block_stride, int nblocks, con
 // tcgen05 bf16-operand conv, fp32 accumulate (conv_bf16.cu): Co % 128 == 0, Ci % 32 == 0.
 bool conv3x3_bf16_supported(const ConvShape& s);
 int64_t conv3x3_bf16_ws_bytes(const ConvShape& s);
+// out_bf16 (optional): receives bf16(out) as well (the single-plane wgrad operand).
 void conv3x3_fwd_bf16(const ConvShape& s, const float* in, const float* w_hwio, bool dgrad_weights, const float* bias,
-                      const float* aux, float h, int epi, float* out, void* ws, cudaStream_t st);
+                      const float* aux, float h, int epi, float* out, void* ws, cudaStream_t st,
+                      void* out_bf16 = nullptr);
+// The bf16 tape form: the input is already bf16 (in16, loaded by TMA straight into the MMA
+// layout, no converter pass); out (fp32) may be null; out16 = bf16(out), out16d = bf16(1 -
+// out^2) (EPI_BIAS_TANH: the derivative the backward's EPI_DTANH16 reads as aux16), each
+// optional.
+void conv3x3_fwd_bf16_in16(const ConvShape& s, const void* in16, const float* w_hwio, bool dgrad_weights,
+                           const float* bias, const float* aux, const void* aux16, float h, int epi, float* out,
+                           void* out16, void* out16d, void* ws, cudaStream_t st);
 
 // tcgen05 weight gradient (conv_wgrad_tc.cu): gw[tap][ci][co], gb[co] (may be null),
 // scaled; deterministic (per-CTA partials + fixed-order fp64 reduce).
@@ -93,7 +103,13 @@ bool conv3x3_wgrad_planes_supported(const ConvShape& s);
 int64_t conv3x3_wgrad_planes_ws_bytes(const ConvShape& s);
 void conv3x3_wgrad_planes(const ConvShape& s, const void* x0, const void* x1, const void* g0, const void* g1,
                           float scale, float* gw, float* gb, void* ws, cudaStream_t st);
-// fp32 [n] -> bf16 planes p0 = bf16(v), p1 = bf16(v - p0)   (n % 4 == 0)
+// The same kernel on single bf16 planes (RP_MATH_BF16): x, g one bf16 NHWC tensor each,
+// 128-channel blocks (Ci, Co % 128 == 0); bf16 x bf16 products, fp32 accumulate.
+bool conv3x3_wgrad_bf16p_supported(const ConvShape& s);
+int64_t conv3x3_wgrad_bf16p_ws_bytes(const ConvShape& s);
+void conv3x3_wgrad_bf16p(const ConvShape& s, const void* x, const void* g, float scale, float* gw, float* gb,
+                         void* ws, cudaStream_t st);
+// fp32 [n] -> bf16 planes p0 = bf16(v), p1 = bf16(v - p0)   (n % 4 == 0; p1 may be null: bf16 copy)
 void split_planes(const float* in, int64_t n, void* p0, void* p1, cudaStream_t st);
 
 // ---- stem S (stem.cu): Cin <= 4 streaming kernels (SIMT conv path otherwise)

@@ -16,6 +16,7 @@ namespace rp::k {
 namespace {
 
 constexpr int kStemMaxCin = 4;
+constexpr int kStemTiles = 3;          // wgrad register tiles per thread ((9 Cin + 1) / 4 x C / 4 <= 768)
 constexpr int kStemGrid = 8 * kNumSMs;   // wgrad partials (8 CTAs / SM hide the gather latency)
 
 template <int Cin>
@@ -138,6 +139,8 @@ __global__ __launch_bounds__(256, 2) void stem_fwd4_kernel(const float* __restri
 // rows r = (tap, ci) plus a ones row (r = 9 Cin: the bias).  CTA b owns positions
 // [b P / G, (b+1) P / G), staged PC at a time into smem; thread (half h, row quad rb,
 // channel quad cb) accumulates a 4 x 4 register tile over the positions pp = h mod halves.
+// When the (row quad, channel quad) tiles outnumber the threads (C = 256: 7 x 64 = 448
+// tiles), every thread owns up to kStemTiles tiles (t, t + 256, ...) and halves = 1.
 template <int Cin>
 __global__ __launch_bounds__(256) void stem_wgrad_gemm_kernel(const float* __restrict__ x,
                                                               const float* __restrict__ g, int N, int H, int W,
@@ -150,11 +153,20 @@ __global__ __launch_bounds__(256) void stem_wgrad_gemm_kernel(const float* __res
   const int C4 = C / 4, nt = (RP / 4) * C4;
   const int halves = max(1, 256 / nt);
   const int t = threadIdx.x;
-  const int h = t / nt, rb = (t % nt) / C4, cb = t % C4;
+  const int h = nt >= 256 ? 0 : t / nt;
   const bool active = h < halves;
+  int rbs[kStemTiles], cbs[kStemTiles];
+  bool own[kStemTiles];
+#pragma unroll
+  for (int j = 0; j < kStemTiles; ++j) {
+    const int q = nt >= 256 ? t + 256 * j : (j == 0 ? t % nt : nt);
+    own[j] = active && q < nt;
+    rbs[j] = own[j] ? q / C4 : 0;
+    cbs[j] = own[j] ? q % C4 : 0;
+  }
   const int64_t P = (int64_t)N * H * W;
   const int64_t p0 = blockIdx.x * P / gridDim.x, p1 = (blockIdx.x + 1) * P / gridDim.x;
-  float acc[4][4] = {};
+  float acc[kStemTiles][4][4] = {};
   for (int64_t c0 = p0; c0 < p1; c0 += PC) {
     const int np = (int)(p1 - c0 < (int64_t)PC ? p1 - c0 : (int64_t)PC);
     __syncthreads();
@@ -185,25 +197,31 @@ __global__ __launch_bounds__(256) void stem_wgrad_gemm_kernel(const float* __res
     if (active) {
       const float4* X4 = reinterpret_cast<const float4*>(X);
       for (int pp = h; pp < np; pp += halves) {
-        const float4 xv = X4[pp * (RP / 4) + rb];
-        const float4 gv = G4[pp * C4 + cb];
-        const float xa[4] = {xv.x, xv.y, xv.z, xv.w};
-        const float ga[4] = {gv.x, gv.y, gv.z, gv.w};
 #pragma unroll
-        for (int i = 0; i < 4; ++i)
+        for (int q = 0; q < kStemTiles; ++q) {
+          if (!own[q]) continue;
+          const float4 xv = X4[pp * (RP / 4) + rbs[q]];
+          const float4 gv = G4[pp * C4 + cbs[q]];
+          const float xa[4] = {xv.x, xv.y, xv.z, xv.w};
+          const float ga[4] = {gv.x, gv.y, gv.z, gv.w};
 #pragma unroll
-          for (int j = 0; j < 4; ++j) acc[i][j] = fmaf(xa[i], ga[j], acc[i][j]);
+          for (int i = 0; i < 4; ++i)
+#pragma unroll
+            for (int j = 0; j < 4; ++j) acc[q][i][j] = fmaf(xa[i], ga[j], acc[q][i][j]);
+        }
       }
     }
   }
   // fixed-order combine of the halves, then the CTA partial [RP][C]
   __syncthreads();
   float* red = sm;                 // [halves][RP][C]
-  if (active)
 #pragma unroll
-    for (int i = 0; i < 4; ++i)
+  for (int q = 0; q < kStemTiles; ++q)
+    if (own[q])
 #pragma unroll
-      for (int j = 0; j < 4; ++j) red[((size_t)h * RP + rb * 4 + i) * C + cb * 4 + j] = acc[i][j];
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) red[((size_t)h * RP + rbs[q] * 4 + i) * C + cbs[q] * 4 + j] = acc[q][i][j];
   __syncthreads();
   for (int i = t; i < RP * C; i += blockDim.x) {
     float s = 0.f;

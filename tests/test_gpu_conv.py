@@ -231,3 +231,43 @@ def test_wgrad_deterministic():
     a = run_wgrad(2, 32, 32, 64, 64, "fp32", seed=5)
     b = run_wgrad(2, 32, 32, 64, 64, "fp32", seed=5)
     assert np.array_equal(a[0], b[0]) and np.array_equal(a[1], b[1])
+
+
+# The stem S (Cin -> C 3x3 conv, streaming kernels): forward and weight/bias gradients vs the
+# fp64 oracle.  C = 256 has more (row quad, channel quad) register tiles than the wgrad
+# kernel has threads (7 x 64 = 448 > 256): every tile must still be computed.
+@pytest.mark.parametrize("cin,c", [(1, 16), (3, 64), (3, 128), (3, 256), (4, 256), (2, 32)])
+def test_stem_fwd_and_wgrad(cin, c):
+    n, hh, ww = 3, 12, 10
+    rng = np.random.default_rng(17)
+    geo = rp.Geometry(cin, hh, ww, c, c, 1, 10).c()
+    npar = lib().rp_param_count(C.byref(geo))
+    params = rng.uniform(-0.3, 0.3, npar).astype(np.float32)
+    x = rng.uniform(-1, 1, (n, hh, ww, cin)).astype(np.float32)
+    g = rng.uniform(-1, 1, (n, hh, ww, c)).astype(np.float32)
+    sw = params[:9 * cin * c].reshape(3, 3, cin, c).astype(np.float64)
+    sb = params[9 * cin * c:9 * cin * c + c].astype(np.float64)
+    want_out = O.conv3x3(x.astype(np.float64), sw) + sb
+    want_gw = O.conv3x3_wgrad(x.astype(np.float64), g.astype(np.float64))
+    want_gb = g.astype(np.float64).reshape(-1, c).sum(axis=0)
+    dev = torch.device("cuda")
+    tp, tx, tg = (torch.from_numpy(v).to(dev) for v in (params, x, g))
+    out = torch.empty((n, hh, ww, c), device=dev)
+    grads = torch.full_like(tp, float("nan"))
+    wsb = lib().rp_op_workspace_bytes(C.byref(geo), n, rp.MATH["fp32"])
+    ws = torch.empty(wsb, dtype=torch.uint8, device=dev)
+    # stale, large values in the shared memory the wgrad kernel reuses must not leak in
+    junk = torch.full((1 << 22,), 1e6, device=dev)
+    junk.mul_(3.0)
+    rp.check(lib().rp_op_stem_fwd(C.byref(geo), n, C.c_void_p(tx.data_ptr()), C.c_void_p(tp.data_ptr()),
+                                  C.c_void_p(out.data_ptr()), rp.MATH["fp32"], C.c_void_p(ws.data_ptr()), wsb, None))
+    rp.check(lib().rp_op_stem_bwd(C.byref(geo), n, C.c_void_p(tx.data_ptr()), C.c_void_p(tg.data_ptr()),
+                                  C.c_void_p(grads.data_ptr()), C.c_void_p(ws.data_ptr()), wsb, None))
+    torch.cuda.synchronize()
+    o64 = out.cpu().numpy().astype(np.float64)
+    gr = grads.cpu().numpy().astype(np.float64)
+    ew = np.abs(gr[:9 * cin * c].reshape(3, 3, cin, c) - want_gw).max() / np.abs(want_gw).max()
+    eb = np.abs(gr[9 * cin * c:9 * cin * c + c] - want_gb).max() / np.abs(want_gb).max()
+    eo = np.abs(o64 - want_out).max() / np.abs(want_out).max()
+    print(f"stem cin={cin} c={c}: out {eo:.1e} gw {ew:.1e} gb {eb:.1e}")
+    assert eo <= 1e-5 and ew <= 1e-5 and eb <= 1e-5, (eo, ew, eb)

@@ -326,3 +326,28 @@ def test_cuda_graph_steps_equal_eager(mode):
     assert res[0][0] == res[1][0]
     for a, b in zip(res[0][1:], res[1][1:]):
         np.testing.assert_array_equal(a, b)
+
+
+# bf16 math (config C5's path: bf16 operands, fp32 accumulation) on geometries the bf16
+# kernels tile (C, hidden multiples of 128).  bf16 keeps 8 mantissa bits: the bar is 2e-2
+# max-norm relative per tensor against the fp64 oracle (BF16_TOL), loss 1e-3.
+BF16_TOL = 2e-2
+BF16_CASES = [
+    (O.Geometry(3, 8, 8, 128, 128, 4, 10), 2, O.ALM, O.SQUARED_L2, 4, 4, 2),
+    (O.Geometry(3, 10, 6, 128, 256, 3, 10, step_h=0.5), 3, O.PENALTY, O.SQUARED_L2, 3, 3, 1),
+    (O.Geometry(3, 8, 8, 128, 128, 2, 10, activation=O.IDENTITY), 1, O.PENALTY, O.SQUARED_L2, 2, 2, 2),
+]
+
+
+@pytest.mark.parametrize("case", range(len(BF16_CASES)))
+def test_bf16_trainer_vs_oracle(case):
+    og, K, mode, kind, N, batch, steps = BF16_CASES[case]
+    ot, o32, gt, lo, l32, lg = conv_case_run(og, K, mode, kind, N, batch, steps, "bf16")
+    assert rel_err(lg, lo) <= 1e-3, (lg, lo)
+    errs = param_rel_errs(og, gt.params().astype(np.float64), ot.net.flat())
+    worst = max(errs, key=errs.get)
+    print("bf16 trainer param errors:", {k: f"{v:.1e}" for k, v in errs.items()})
+    assert errs[worst] <= BF16_TOL, (worst, errs[worst])
+    for k in range(K):
+        got = gt.state(k, rp.BOUNDARY_OUT)
+        assert rel_err(got, ot.stage(k).boundary_out) <= BF16_TOL, (k, rel_err(got, ot.stage(k).boundary_out))

@@ -40,7 +40,7 @@ for src, (p0, p1) in ((x, planes[:2]), (g, planes[2:])):
     rp.check(lib().rp_op_split_planes(C.c_void_p(src.data_ptr()), src.numel(), C.c_void_p(p0.data_ptr()),
                                       C.c_void_p(p1.data_ptr()), None))
 ws_p = lib().rp_op_conv3x3_wgrad_planes_workspace_bytes(n, h, w, c, c)
-ws_b = max(ws_b, ws_p)
+ws_b = max(ws_b, ws_p, lib().rp_op_conv3x3_wgrad_bf16p_workspace_bytes(n, h, w, c, c))
 ws = torch.empty(ws_b, dtype=torch.uint8, device=dev)
 P = C.c_void_p
 m = rp.MATH[a.math]
@@ -63,6 +63,10 @@ for which in a.which.split(","):
                                                 P(b.data_ptr()), P(x.data_ptr()) if d else None, 1.0, 3 if d else 1,
                                                 P(out.data_ptr()), P(planes[2].data_ptr()), P(ws.data_ptr()), ws_b,
                                                 None))
+        elif which == "wgrad_bf16p":
+            rp.check(lib().rp_op_conv3x3_wgrad_bf16p(n, h, w, c, c, C.c_void_p(planes[0].data_ptr()),
+                                                     C.c_void_p(planes[2].data_ptr()), 1.0, P(gw.data_ptr()),
+                                                     P(gb.data_ptr()), P(ws.data_ptr()), ws_b, None))
         elif which == "wgrad_planes":
             rp.check(lib().rp_op_conv3x3_wgrad_planes(n, h, w, c, c, *[C.c_void_p(t.data_ptr()) for t in planes], 1.0,
                                                       P(gw.data_ptr()), P(gb.data_ptr()), P(ws.data_ptr()), ws_b,
