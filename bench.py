@@ -49,7 +49,7 @@ def flops_per_image(cfg):
 
 
 # effective multiplier step kappa_lr * # / (2 beta) of the bench's ALM runs (see step_params)
-KAPPA_STEP = 8e-7
+KAPPA_STEP = 1e-8
 
 
 def step_params(cfg):
@@ -209,7 +209,8 @@ def run_ours(args, cfg, rank, world):
     tr.use_cuda_graphs(False)                # per-kernel events need eager launches
     lib().rp_profile_enable(1)
     profile_classes()  # clear
-    for _ in range(args.steps):
+    prof_steps = min(args.steps, 5)
+    for _ in range(prof_steps):
         tr.step_device(x.data_ptr(), y.data_ptr(), B, 0, sp, read_loss=False)
     torch.cuda.synchronize()
     lib().rp_profile_enable(0)
@@ -235,7 +236,7 @@ def run_ours(args, cfg, rank, world):
         tr.step(xpn.reshape(B, -1), ypn, 0, sp)
     e2e_s = (time.perf_counter() - t0) / e2e_steps
     return dict(tr=tr, total_ms=total_ms, prof=prof, clocks=clk, launches=launches, loss=loss, e2e_s=e2e_s,
-                B=B, K=K, g=g)
+                B=B, K=K, g=g, prof_steps=prof_steps)
 
 
 def run_ours_distributed(args, cfg, rank, world):
@@ -287,7 +288,8 @@ def run_ours_distributed(args, cfg, rank, world):
     clk = clocks.stop()
     lib().rp_profile_enable(1)       # profiled pass for the roofline classes (untimed)
     profile_classes()
-    for _ in range(args.steps):
+    prof_steps = min(args.steps, 5)
+    for _ in range(prof_steps):
         tr.step(xp, yp, B, 0, sp)
     torch.cuda.synchronize()
     lib().rp_profile_enable(0)
@@ -314,7 +316,7 @@ def run_ours_distributed(args, cfg, rank, world):
     e2e_s = torch.tensor([(time.perf_counter() - t0) / e2e_steps], device="cuda")
     dist.all_reduce(e2e_s, op=dist.ReduceOp.MAX)
     return dict(tr=tr, total_ms=total_ms, prof=prof, clocks=clk, launches=launches, loss=loss,
-                e2e_s=float(e2e_s.item()), B=B, K=K, g=g, replicas=plc.replicas, plc=plc)
+                e2e_s=float(e2e_s.item()), B=B, K=K, g=g, replicas=plc.replicas, plc=plc, prof_steps=prof_steps)
 
 
 def _splitmix(seed):
@@ -435,29 +437,33 @@ def main():
     d = prof[dom]
     avg_ms = d["ms"] / d["launches"]
     achieved_tf = d["flops"] / d["launches"] / (avg_ms / 1e3) / 1e12
-    step_prof_ms = sum(v["ms"] for v in prof.values()) / args.steps
+    ps = r["prof_steps"]
+    step_prof_ms = sum(v["ms"] for v in prof.values()) / ps
     traffic = None
     tpath = os.path.join(ROOT, "profiles", "traffic.json")
     if os.path.isfile(tpath):
         with open(tpath) as f:
-            t = json.load(f).get(dom)
+            tj = json.load(f)
+            t = tj.get(f"{args.config}:{dom}") or tj.get(dom)
         traffic = t["bytes_per_launch"] if t else None
-    # the fp32-accurate kernels run every fp32 MAC as 3-4 reduced-precision tensor products
-    # (3xTF32 / 3xBF16 stacking): their own ceiling is a fraction of the bf16
-    # peak, reported beside the prescribed bf16-peak fraction
-    split = {"fp32": 8.0, "tf32": 2.0, "bf16": 1.0, "simt": None}.get(cfg["math"])
+    # the fp32-accurate kernels run every fp32 MAC as 4 bf16 tensor products (the plane path:
+    # [W0; W1] x {x0, x1} in fprop / dgrad, [g0; g1] x [x0 x1] in wgrad): their
+    # own ceiling is the bf16 peak / 4, reported beside the prescribed bf16-peak fraction
+    # together with the bf16 tensor work actually issued
+    split = {"fp32": 4.0, "tf32": 2.0, "bf16": 1.0, "simt": None}.get(cfg["math"])
     ceiling = peaks["bf16_tflops_sustained"] / split if split else None
     roof = {"bound": "tensor", "kernel": dom, "achieved": achieved_tf,
             "peak": peaks["bf16_tflops_sustained"], "unit": "TFLOP/s",
             "frac": achieved_tf / peaks["bf16_tflops_sustained"], "traffic": traffic,
             "traffic_unit": "bytes per launch (ncu --set full, profiles/traffic.json)",
             "math_ceiling": {"tflops": ceiling, "frac": achieved_tf / ceiling if ceiling else None,
-                             "note": "bf16 sustained peak / products per fp32-equivalent MAC "
-                                     "(fp32: 4 tf32 products at half the bf16 rate)"},
+                             "tensor_tflops_issued": achieved_tf * split if split else None,
+                             "note": "bf16 sustained peak / bf16 tensor products per fp32-equivalent MAC "
+                                     "(fp32 plane path: 4; bf16: 1)"},
             "peak_source": f"{peaks_kind} bf16 dense sustained (MEASURED_PEAKS.json)",
             "avg_launch_ms": avg_ms, "launches": d["launches"],
-            "share_of_step": d["ms"] / args.steps / step_prof_ms if step_prof_ms else None,
-            "kernel_classes": {k: {"launches": v["launches"], "ms_per_step": v["ms"] / args.steps,
+            "share_of_step": d["ms"] / ps / step_prof_ms if step_prof_ms else None,
+            "kernel_classes": {k: {"launches": v["launches"], "ms_per_step": v["ms"] / ps,
                                    "tflops": (v["flops"] / (v["ms"] / 1e3) / 1e12) if v["ms"] and v["flops"] else None,
                                    "gbs": (v["bytes"] / (v["ms"] / 1e3) / 1e9) if v["ms"] and v["bytes"] else None}
                                for k, v in prof.items()}}

@@ -137,6 +137,10 @@ int rp_op_psi_grad(int32_t kind, const float* lam, const float* x, int64_t n, do
  * w = beta/# (kappa_next may be NULL == zero). */
 int rp_op_synthetic_grad(int32_t kind, const float* lam_next, const float* x_end, const float* kappa_next,
                          int64_t n, double w, float* g, void* ws, void* stream);
+/* The same, also writing the bf16 plane pair of g (p0 = bf16(g), p1 = bf16(g - p0); p1 NULL:
+ * the bf16 copy alone) for the tape paths, in one pass over the data. */
+int rp_op_synthetic_grad_planes(int32_t kind, const float* lam_next, const float* x_end, const float* kappa_next,
+                                int64_t n, double w, float* g, void* p0, void* p1, void* ws, void* stream);
 /* One correct_aux pass and/or correct_multiplier (decoupled.cpp:135-170), fused:
  *   if update_lambda: lam -= eta_l * (w d_lambda psi(lam, x_prev) + p - kappa)
  *   if update_kappa:  kappa -= kappa_coef * (lam - x_prev)   (lam already updated)

@@ -66,6 +66,7 @@ SIGNATURES = {
     "rp_op_block_bwd_planes": (C.c_int, [_G, C.c_int32, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, C.c_int64, _P]),
     "rp_op_planes_filters_bytes": (C.c_int64, [_G, C.c_int32]),
     "rp_op_block_bf16_tape_supported": (C.c_int32, [_G, C.c_int32, C.c_int32]),
+    "rp_op_synthetic_grad_planes": (C.c_int, [C.c_int32, _P, _P, _P, C.c_int64, C.c_double, _P, _P, _P, _P, _P]),
     "rp_op_block_fwd_bf16t": (C.c_int, [_G, C.c_int32, _P, _P, _P, _P, _P, _P, _P, _P, C.c_int64, _P]),
     "rp_op_block_bwd_bf16t": (C.c_int, [_G, C.c_int32, _P, _P, _P, _P, _P, _P, _P, _P, _P, C.c_int64, _P]),
     "rp_op_conv3x3_wgrad_bf16p": (C.c_int, [C.c_int32] * 5 + [_P, _P, C.c_double, _P, _P, _P, C.c_int64, _P]),

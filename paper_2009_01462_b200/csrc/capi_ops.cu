@@ -141,7 +141,8 @@ int64_t op_workspace_bytes(const rp_geometry& g, int nrows) {
 void conv(const k::ConvShape& s, const float* in, const float* w, bool dgrad, const float* bias, const float* aux,
           float h, int epi, float* out, int math, void* wws, int prof_cls, bool aux_read, cudaStream_t st,
           void* out_planes = nullptr, const void* in_planes = nullptr, const void* wprep = nullptr) {
-  prof::Scope ps(prof_cls, st, conv_flops(s), conv_bytes(s, aux_read) + (out_planes ? 4.0 * s.pixels() * s.co : 0.0));
+  prof::Scope ps(prof_cls, st, conv_flops(s),
+                 conv_bytes(s, aux_read) + (out_planes ? 4.0 * s.pixels() * s.co : 0.0) - (out ? 0.0 : 4.0 * s.pixels() * s.co));
   if (out_planes || in_planes) {   // only the fp32 tcgen05 kernel reads / writes plane pairs (planes_path())
     if (math != RP_MATH_FP32 || !k::conv3x3_tc_supported(s)) fail(RP_ERR_INTERNAL, "conv: plane i/o needs fp32 tcgen05");
     k::conv3x3_fwd_tc(s, in, w, dgrad, bias, aux, h, epi, out, fp32_split(), wws, st, out_planes, in_planes,
@@ -253,10 +254,12 @@ void block_bwd_planes(const rp_geometry& g, int nrows, const void* x_p, const fl
   void* wws = cv.take<char>(weight_ws_bytes(g));
   const int64_t wg_bytes = std::max(wgrad_ws_bytes(shape(g, nrows, Ch, C)), wgrad_ws_bytes(shape(g, nrows, C, Ch)));
   void* wgws = cv.take<char>(wg_bytes);
-  // dpre = h (g * W2^T) (1 - a^2), and its planes                (network.cpp:100-101)
+  // dpre = h (g * W2^T) (1 - a^2) as planes only: its consumers (wgrad1, dgrad1) read the
+  // planes, so the fp32 dpre is not written                     (network.cpp:100-101)
   const char* f = static_cast<const char*>(filters);
   const int64_t fb = planes_filter_bytes(g);
-  conv(shape(g, nrows, C, Ch), gio, pb + L.w2, true, nullptr, a, h, tanh_act ? k::EPI_TANH_BWD : k::EPI_SCALE, dpre,
+  (void)dpre;
+  conv(shape(g, nrows, C, Ch), gio, pb + L.w2, true, nullptr, a, h, tanh_act ? k::EPI_TANH_BWD : k::EPI_SCALE, nullptr,
        RP_MATH_FP32, wws, RP_PROF_CONV_DGRAD, tanh_act, st, dpre_p, g_p, f);
   // gW2 = h a^T g, gb2 = h sum g                                  (network.cpp:98-99)
   wgrad_planes(shape(g, nrows, Ch, C), a_p, g_p, h, gb + L.w2, gb + L.b2, wgws, st);
@@ -466,6 +469,16 @@ int rp_op_synthetic_grad(int32_t kind, const float* lam_next, const float* x_end
     if (kind < 0 || kind > 2) fail(RP_ERR_RANGE, "unknown penalty kind");
     prof::Scope scope(RP_PROF_SYNTHETIC, S(stream), 0.0, (double)n * (kappa_next ? 16.0 : 12.0));
     k::synthetic_grad(kind, lam_next, x_end, kappa_next, n, w, g, ws, S(stream));
+  });
+}
+
+int rp_op_synthetic_grad_planes(int32_t kind, const float* lam_next, const float* x_end, const float* kappa_next,
+                                int64_t n, double w, float* g, void* p0, void* p1, void* ws, void* stream) {
+  return guard([&] {
+    if (kind < 0 || kind > 2) fail(RP_ERR_RANGE, "unknown penalty kind");
+    need(p0, "p0");
+    prof::Scope scope(RP_PROF_SYNTHETIC, S(stream), 0.0, (double)n * ((kappa_next ? 16.0 : 12.0) + (p1 ? 4.0 : 2.0)));
+    k::synthetic_grad(kind, lam_next, x_end, kappa_next, n, w, g, ws, S(stream), p0, p1);
   });
 }
 

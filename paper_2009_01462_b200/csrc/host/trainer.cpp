@@ -503,6 +503,11 @@ void DecoupledTrainer::run_backward(Stage& st, const int32_t* labels, int nrows,
   float* g = st.badj.get() + (int64_t)row0 * feat();
   const float* x_end = st.bout.get() + (int64_t)st.fwd_row0 * feat();
   const int64_t n = (int64_t)nrows * feat();
+  // the tape paths' first backward conv reads g as bf16 planes: the synthetic upstream writes
+  // them in the same pass (planes_done), the head's cotangent is split afterwards
+  const bool tape = (st.tape_bf16 || st.tape_planes) && st.fwd_rows == nrows;
+  uint16_t* gp16 = tape ? st.g_p.get<uint16_t>() : nullptr;
+  bool planes_done = false;
   if (k == stages() - 1) {
     check(rp_op_head_loss_bwd(&geo_, nrows, st.pooled.get(), st.logits.get(), P + L.t_w, labels, st.loss.get<double>(),
                               G + L.t_w, g, st.ws.get(), st.ws.bytes(), s));
@@ -518,12 +523,18 @@ void DecoupledTrainer::run_backward(Stage& st, const int32_t* labels, int nrows,
       kap_next = nx.kappa_zero ? nullptr : nx.kappa.get() + (int64_t)row0 * feat();
     }
     const double w = beta / static_cast<double>(normalizer(nrows, (int)feat()));
-    check(rp_op_synthetic_grad((int)kind_, lam_next, x_end, kap_next, n, w, g, st.red_ws.get(), s));
+    if (tape) {
+      check(rp_op_synthetic_grad_planes((int)kind_, lam_next, x_end, kap_next, n, w, g, gp16,
+                                        st.tape_bf16 ? nullptr : gp16 + n, st.red_ws.get(), s));
+      planes_done = true;
+    } else {
+      check(rp_op_synthetic_grad((int)kind_, lam_next, x_end, kap_next, n, w, g, st.red_ws.get(), s));
+    }
   }
   const int nb = st.end - st.begin;
   if (st.tape_bf16 && st.fwd_rows == nrows) {
     auto* gp = st.g_p.get<uint16_t>();
-    check(rp_op_split_planes(g, n, gp, nullptr, s));
+    if (!planes_done) check(rp_op_split_planes(g, n, gp, nullptr, s));
     for (int i = nb - 1; i >= 0; --i) {
       const int l = st.begin + i;
       const int64_t off = L.block0 + (int64_t)l * L.block_stride;
@@ -532,7 +543,7 @@ void DecoupledTrainer::run_backward(Stage& st, const int32_t* labels, int nrows,
     }
   } else if (st.tape_planes && st.fwd_rows == nrows) {
     auto* gp = st.g_p.get<uint16_t>();
-    check(rp_op_split_planes(g, n, gp, gp + n, s));
+    if (!planes_done) check(rp_op_split_planes(g, n, gp, gp + n, s));
     // every block's input-gradient filters in one launch, from the current parameters
     const int64_t fpair = rp_op_planes_filters_bytes(&geo_, 1);
     check(rp_op_prep_planes_filters(&geo_, P + L.block0 + (int64_t)st.begin * L.block_stride, nb, 1,

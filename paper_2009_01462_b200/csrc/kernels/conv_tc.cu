@@ -604,7 +604,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         const uint32_t tcol = tmem_base + ((uint32_t)(q * 32) << 16) + (uint32_t)((ab * kS + grp) * 128);
         const float* auxb = kAux ? a.aux + img * a.Co + co : nullptr;
-        float* outb = a.out + img * a.Co + co;
+        float* outb = a.out ? a.out + img * a.Co + co : nullptr;   // null: the planes alone
         const bool planes = a.p0 != nullptr;
         __nv_bfloat16* p0b = planes ? a.p0 + img * a.Co + co : nullptr;
         __nv_bfloat16* p1b = planes ? a.p1 + img * a.Co + co : nullptr;
@@ -645,7 +645,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                 else if constexpr (EPI == EPI_ADD) o[i] = xa[i] + v[i];
                 else o[i] = a.h * v[i];
               }
-              *reinterpret_cast<float4*>(outb + off) = make_float4(o[0], o[1], o[2], o[3]);
+              if (outb) *reinterpret_cast<float4*>(outb + off) = make_float4(o[0], o[1], o[2], o[3]);
               if (planes) {
                 uint32_t h[2], l[2];
 #pragma unroll

@@ -7,6 +7,8 @@
 // on stage placement or launch timing (runtime.hpp:28-32).
 #include <cmath>
 
+#include <cuda_bf16.h>
+
 #include "../common.cuh"
 #include "kernels.cuh"
 
@@ -135,8 +137,11 @@ __device__ __forceinline__ float dlam(int kind, float d, int64_t i, long long ar
 }
 
 // g = w * d_x + kappa,  d_x = -d_lambda   (decoupled.cpp:105-110)
+// p0 / p1 (optional): the bf16 plane pair of g (p0 = bf16(g), p1 = bf16(g - p0); p1 null: the
+// bf16 copy alone) for the tape paths' first backward conv, written in the same pass
 __global__ void synthetic_grad_vec4(int kind, const float4* __restrict__ lam, const float4* __restrict__ x,
-                                    const float4* __restrict__ kap, int64_t n4, float w, float4* __restrict__ g) {
+                                    const float4* __restrict__ kap, int64_t n4, float w, float4* __restrict__ g,
+                                    uint2* __restrict__ p0, uint2* __restrict__ p1) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n4; i += (int64_t)gridDim.x * blockDim.x) {
     const float4 l = lam[i], xe = x[i];
     float4 k4 = kap ? kap[i] : make_float4(0.f, 0.f, 0.f, 0.f);
@@ -146,6 +151,15 @@ __global__ void synthetic_grad_vec4(int kind, const float4* __restrict__ lam, co
     o.z = -dlam(kind, l.z - xe.z, 0, -1) * w + k4.z;
     o.w = -dlam(kind, l.w - xe.w, 0, -1) * w + k4.w;
     g[i] = o;
+    if (p0) {
+      const __nv_bfloat162 a = __floats2bfloat162_rn(o.x, o.y), b = __floats2bfloat162_rn(o.z, o.w);
+      p0[i] = make_uint2(*reinterpret_cast<const uint32_t*>(&a), *reinterpret_cast<const uint32_t*>(&b));
+      if (p1) {
+        const __nv_bfloat162 c = __floats2bfloat162_rn(o.x - __low2float(a), o.y - __high2float(a));
+        const __nv_bfloat162 d = __floats2bfloat162_rn(o.z - __low2float(b), o.w - __high2float(b));
+        p1[i] = make_uint2(*reinterpret_cast<const uint32_t*>(&c), *reinterpret_cast<const uint32_t*>(&d));
+      }
+    }
   }
 }
 
@@ -290,18 +304,21 @@ void psi_grad(int kind, const float* lam, const float* x, int64_t n, double scal
 }
 
 void synthetic_grad(int kind, const float* lam_next, const float* x_end, const float* kappa, int64_t n, double w,
-                    float* g, void* ws, cudaStream_t s) {
+                    float* g, void* ws, cudaStream_t s, void* p0, void* p1) {
   if (n <= 0) return;
   if (kind != RP_PSI_LINF && n % 4 == 0 && aligned16(lam_next) && aligned16(x_end) && aligned16(g) &&
-      (!kappa || aligned16(kappa))) {
+      (!kappa || aligned16(kappa)) && (!p0 || aligned16(p0)) && (!p1 || aligned16(p1))) {
     synthetic_grad_vec4<<<grid_for(n / 4), kThreads, 0, s>>>(
         kind, reinterpret_cast<const float4*>(lam_next), reinterpret_cast<const float4*>(x_end),
-        reinterpret_cast<const float4*>(kappa), n / 4, (float)w, reinterpret_cast<float4*>(g));
-  } else {
-    const ArgMax* am = kind == RP_PSI_LINF ? linf_argmax(lam_next, x_end, n, ws, s) : nullptr;
-    synthetic_grad_scalar<<<grid_for(n), kThreads, 0, s>>>(kind, lam_next, x_end, kappa, n, (float)w, am, g);
+        reinterpret_cast<const float4*>(kappa), n / 4, (float)w, reinterpret_cast<float4*>(g),
+        static_cast<uint2*>(p0), static_cast<uint2*>(p1));
+    RP_LAUNCHED();
+    return;
   }
+  const ArgMax* am = kind == RP_PSI_LINF ? linf_argmax(lam_next, x_end, n, ws, s) : nullptr;
+  synthetic_grad_scalar<<<grid_for(n), kThreads, 0, s>>>(kind, lam_next, x_end, kappa, n, (float)w, am, g);
   RP_LAUNCHED();
+  if (p0) split_planes(g, n, p0, p1, s);   // the planes in a second pass (LInf / unaligned)
 }
 
 void correct(int kind, float* lam, const float* x_prev, const float* p, float* kappa, int64_t n, double w,

@@ -16,8 +16,9 @@ void fill_normal(float* dst, int64_t n, uint64_t state, double mean, double sigm
 void psi_device(int kind, const float* a, const float* b, int64_t n, void* ws, double* out_dev, cudaStream_t s);
 void psi_grad(int kind, const float* lam, const float* x, int64_t n, double scale, float* out, void* ws,
               cudaStream_t s);
+// p0 / p1 (optional): also the bf16 plane pair of g (p1 null: the bf16 copy alone)
 void synthetic_grad(int kind, const float* lam_next, const float* x_end, const float* kappa, int64_t n, double w,
-                    float* g, void* ws, cudaStream_t s);
+                    float* g, void* ws, cudaStream_t s, void* p0 = nullptr, void* p1 = nullptr);
 void correct(int kind, float* lam, const float* x_prev, const float* p, float* kappa, int64_t n, double w,
              double eta, bool update_lambda, double kappa_coef, bool update_kappa, void* ws, cudaStream_t s);
 void sgd(float* w, const float* g, float* v, int64_t n, double lr, double momentum, cudaStream_t s);
