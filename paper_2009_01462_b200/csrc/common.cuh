@@ -4,6 +4,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <cstdlib>
 #include <stdexcept>
 #include <string>
 
@@ -69,6 +70,33 @@ struct ParamLayout {
     return p;
   }
 };
+
+// Launch with programmatic stream serialization (PDL): the kernel may start while the
+// previous kernel of the stream finishes; it must call pdl_wait() (umma.cuh) before touching
+// that kernel's outputs.  RP_PDL=0 launches plainly.
+inline bool pdl_enabled() {
+  static const bool on = [] {
+    const char* e = std::getenv("RP_PDL");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
+
+template <class Kernel, class... Args>
+inline void launch_pdl(Kernel k, int grid, int block, size_t smem, cudaStream_t st, Args... args) {
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(block);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = pdl_enabled() ? 1 : 0;
+  const cudaError_t e = cudaLaunchKernelEx(&cfg, k, args...);
+  if (e != cudaSuccess) fail(RP_ERR_CUDA, std::string("cudaLaunchKernelEx: ") + cudaGetErrorString(e));
+}
 
 inline void validate_geometry(const rp_geometry& g) {
   if (g.in_channels < 1 || g.height < 1 || g.width < 1 || g.channels < 1 || g.hidden < 1 ||

@@ -287,7 +287,11 @@ __global__ void __launch_bounds__(kThreads, 1)
   const uint32_t tmem_base = __shfl_sync(0xffffffffu, *tmem_slot, 0);
 
   const int Wp = a.Wp;
+  // PDL: the next conv / wgrad may now be scheduled; its prologue (barriers, TMEM, the resident
+  // filter load) then overlaps this grid's tail on the SMs it frees
+  pdl_launch_dependents();
 
+  if (warp != 14) pdl_wait();   // every role below reads or overwrites the previous grid's data
   if (warp == 0) {
     // ===================== halo TMA producer =====================
     // X3BF16: into the raw ring, released by the converters (runs up to raw_slots chunks
@@ -330,7 +334,10 @@ __global__ void __launch_bounds__(kThreads, 1)
     const uint32_t wbytes = 3 * a.w_tap;
     if (a.resident) {
       // the whole filter of the single co block, once per launch (stage c * 3 + dy = slot c * 3 + dy):
-      // the per-unit weight stream was ~16 B/clk/SM of L2 traffic on top of the halo and the epilogue
+      // the per-unit weight stream was ~16 B/clk/SM of L2 traffic on top of the halo and the epilogue.
+      // Issued before pdl_wait(): the prepared filter comes from a kernel that completed before
+      // the previous grid did (a plainly launched prep kernel, or one before a PDL chain member
+      // that itself waited).
       if (elect_one()) {
         mbar_arrive_expect_tx(&w_full[0], (uint32_t)wst * wbytes);
         for (int i = 0; i < wst; ++i)
@@ -338,6 +345,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
       __syncwarp();
     }
+    pdl_wait();
     UnitIter it(a.Co / 64, a.N, a.T);
     int cb, n, tile0, ntiles;
     while (!a.resident && it.next(cb, n, tile0, ntiles)) {
@@ -916,7 +924,7 @@ void launch_cfg(const CUtensorMap& m, const TcArgs& a, size_t smem, int grid, cu
                                  kMaxSmemRes));
     configured = true;
   }
-  conv3x3_tc_kernel<EPI, MODE><<<grid, kThreads, smem, st>>>(m, a);
+  launch_pdl(conv3x3_tc_kernel<EPI, MODE>, grid, kThreads, smem, st, m, a);
 }
 
 template <int EPI>

@@ -118,6 +118,10 @@ __global__ void __launch_bounds__(kThreads, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = __shfl_sync(0xffffffffu, *tmem_slot, 0);
+  // PDL: let the next grid's prologue overlap this grid's tail; the operands (and the partial
+  // buffer the previous reduce read) belong to the previous grids until pdl_wait()
+  pdl_launch_dependents();
+  pdl_wait();
 
   if (warp == 0) {
     // ===================== TMA producer: 4 plane loads per block =====================
@@ -507,7 +511,7 @@ void launch_wgrad_planes(const ConvShape& s, const void* x0, const void* x1, con
     RP_CUDA(cudaFuncSetAttribute(wgrad_planes_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxSmem));
     configured = true;
   }
-  wgrad_planes_kernel<<<p.grid, kThreads, p.smem, st>>>(mg0, mg1, mx0, mx1, a);
+  launch_pdl(wgrad_planes_kernel, p.grid, kThreads, p.smem, st, mg0, mg1, mx0, mx1, a);
   RP_LAUNCHED();
   const int total = 9 * s.ci * s.co + s.co;
   wgrad_planes_reduce_kernel<<<ceil_div(total, 256), 256, 0, st>>>(a.part, a.part_bias, a, p.grid, (double)scale,

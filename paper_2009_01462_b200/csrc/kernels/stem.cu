@@ -16,7 +16,7 @@ namespace rp::k {
 namespace {
 
 constexpr int kStemMaxCin = 4;
-constexpr int kStemTiles = 3;          // wgrad register tiles per thread ((9 Cin + 1) / 4 x C / 4 <= 768)
+constexpr int kStemTilesMax = 3;       // wgrad register tiles per thread ((9 Cin + 1) / 4 x C / 4 <= 768)
 constexpr int kStemGrid = 8 * kNumSMs;   // wgrad partials (8 CTAs / SM hide the gather latency)
 
 template <int Cin>
@@ -141,7 +141,7 @@ __global__ __launch_bounds__(256, 2) void stem_fwd4_kernel(const float* __restri
 // channel quad cb) accumulates a 4 x 4 register tile over the positions pp = h mod halves.
 // When the (row quad, channel quad) tiles outnumber the threads (C = 256: 7 x 64 = 448
 // tiles), every thread owns up to kStemTiles tiles (t, t + 256, ...) and halves = 1.
-template <int Cin>
+template <int Cin, int kStemTiles>
 __global__ __launch_bounds__(256) void stem_wgrad_gemm_kernel(const float* __restrict__ x,
                                                               const float* __restrict__ g, int N, int H, int W,
                                                               int C, int PC, float* __restrict__ part) {
@@ -170,23 +170,31 @@ __global__ __launch_bounds__(256) void stem_wgrad_gemm_kernel(const float* __res
   for (int64_t c0 = p0; c0 < p1; c0 += PC) {
     const int np = (int)(p1 - c0 < (int64_t)PC ? p1 - c0 : (int64_t)PC);
     __syncthreads();
-#pragma unroll 4
-    for (int i = t; i < PC * RP; i += blockDim.x) {
-      const int pp = i / RP, r = i % RP;
-      float v = 0.f;
+    // im2col rows of the chunk: one (position, tap) item per thread and step, the position's
+    // (n, y, x) from 32-bit divisions (P < 2^32, checked on the host), Cin contiguous loads
+    for (int i = t; i < PC * 9; i += blockDim.x) {
+      const int pp = i / 9, tap = i - pp * 9;
+      float v[Cin];
+#pragma unroll
+      for (int ci = 0; ci < Cin; ++ci) v[ci] = 0.f;
       if (pp < np) {
-        if (r < 9 * Cin) {
-          const int64_t p = c0 + pp;
-          const int xq = (int)(p % W), yq = (int)((p / W) % H);
-          const int64_t n = p / ((int64_t)W * H);
-          const int tap = r / Cin, ci = r % Cin;
-          const int yy = yq + tap / 3 - 1, xx = xq + tap % 3 - 1;
-          if (yy >= 0 && yy < H && xx >= 0 && xx < W) v = __ldg(x + ((n * H + yy) * W + xx) * Cin + ci);
-        } else if (r == 9 * Cin) {
-          v = 1.f;
+        const uint32_t p = (uint32_t)(c0 + pp);
+        const uint32_t r1 = p / (uint32_t)W, xq = p - r1 * (uint32_t)W;
+        const uint32_t n = r1 / (uint32_t)H, yq = r1 - n * (uint32_t)H;
+        const int yy = (int)yq + tap / 3 - 1, xx = (int)xq + tap % 3 - 1;
+        if (yy >= 0 && yy < H && xx >= 0 && xx < W) {
+          const float* src = x + (((int64_t)n * H + yy) * W + xx) * Cin;
+#pragma unroll
+          for (int ci = 0; ci < Cin; ++ci) v[ci] = __ldg(src + ci);
         }
       }
-      X[i] = v;
+#pragma unroll
+      for (int ci = 0; ci < Cin; ++ci) X[pp * RP + tap * Cin + ci] = v[ci];
+    }
+    // the ones row (bias) and the padding rows
+    for (int i = t; i < PC * (RP - 9 * Cin); i += blockDim.x) {
+      const int pp = i / (RP - 9 * Cin), j = i - pp * (RP - 9 * Cin);
+      X[pp * RP + 9 * Cin + j] = (j == 0 && pp < np) ? 1.f : 0.f;
     }
     const float4* g4 = reinterpret_cast<const float4*>(g + c0 * C);
     float4* G4 = reinterpret_cast<float4*>(G);
@@ -293,7 +301,13 @@ void launch_wgrad_gemm(const ConvShape& s, const float* x, const float* g, float
   const int PC = std::max(16, std::min(64, 24 * 1024 / ((RP + s.co) * 4)));
   const size_t smem = std::max<size_t>((size_t)PC * (RP + s.co) * 4,
                                        (size_t)std::max(1, 256 / ((RP / 4) * (s.co / 4))) * RP * s.co * 4);
-  stem_wgrad_gemm_kernel<Cin><<<kStemGrid, 256, smem, st>>>(x, g, s.n, s.h, s.w, s.co, PC, part);
+  if (s.pixels() >= (int64_t)1 << 32) fail(RP_ERR_SHAPE, "stem_wgrad: more than 2^32 positions");
+  // one register tile per thread while the tiles fit the 256 threads (registers -> occupancy)
+  const int nt = (RP / 4) * (s.co / 4);
+  if (nt <= 256)
+    stem_wgrad_gemm_kernel<Cin, 1><<<kStemGrid, 256, smem, st>>>(x, g, s.n, s.h, s.w, s.co, PC, part);
+  else
+    stem_wgrad_gemm_kernel<Cin, kStemTilesMax><<<kStemGrid, 256, smem, st>>>(x, g, s.n, s.h, s.w, s.co, PC, part);
 }
 
 void stem_wgrad(const ConvShape& s, const float* x, const float* g, float scale, float* gw, float* gb, void* ws,
