@@ -150,6 +150,10 @@ __global__ void __launch_bounds__(kThreads, 1)
   tc_fence_after();
   const uint32_t tmem_base = __shfl_sync(0xffffffffu, *tmem_slot, 0);
   const int Wp = a.Wp;
+  // PDL: the next grid's prologue may overlap this grid's tail; everything below reads or
+  // overwrites data of the previous grids
+  pdl_launch_dependents();
+  pdl_wait();
 
   if (warp == 0) {
     // ===================== TMA producer =====================
@@ -477,7 +481,7 @@ void launch(const CUtensorMap& m, const BfArgs& a, size_t smem, int grid, cudaSt
                                  kMaxSmem));
     configured = true;
   }
-  conv3x3_bf16_kernel<EPI, BIN><<<grid, kThreads, smem, st>>>(m, a);
+  launch_pdl(conv3x3_bf16_kernel<EPI, BIN>, grid, kThreads, smem, st, m, a);
 }
 
 template <bool BIN>

@@ -324,6 +324,8 @@ __global__ void __launch_bounds__(kThreads, 1)
 __global__ void wgrad_planes_reduce_kernel(const float* __restrict__ part, const double* __restrict__ part_bias,
                                            const PwArgs a, int grid, double scale, float* __restrict__ gw,
                                            float* __restrict__ gb) {
+  pdl_launch_dependents();   // the next grid's prologue may overlap; it waits before touching memory
+  pdl_wait();                // the partials of the weight-gradient grid
   const int Ci = a.Ci, Co = a.Co;
   const int total = 9 * Ci * Co;
   const int cbk = a.single ? 128 : 64;
@@ -514,8 +516,8 @@ void launch_wgrad_planes(const ConvShape& s, const void* x0, const void* x1, con
   launch_pdl(wgrad_planes_kernel, p.grid, kThreads, p.smem, st, mg0, mg1, mx0, mx1, a);
   RP_LAUNCHED();
   const int total = 9 * s.ci * s.co + s.co;
-  wgrad_planes_reduce_kernel<<<ceil_div(total, 256), 256, 0, st>>>(a.part, a.part_bias, a, p.grid, (double)scale,
-                                                                   gw, gb);
+  launch_pdl(wgrad_planes_reduce_kernel, ceil_div(total, 256), 256, 0, st, (const float*)a.part,
+             (const double*)a.part_bias, a, p.grid, (double)scale, gw, gb);
   RP_LAUNCHED();
 }
 }  // namespace
