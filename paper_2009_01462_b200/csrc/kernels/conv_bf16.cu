@@ -442,8 +442,8 @@ struct Plan {
 
 Plan plan_for(const ConvShape& s, bool bin = false) {
   Plan p;
-  if (s.co % 128 != 0 || s.ci % kChunk != 0 || s.w + 2 > 256) return p;
-  p.Wp = s.w + 2;
+  if (s.co % 128 != 0 || s.ci % kChunk != 0 || s.w + 1 > 256) return p;
+  p.Wp = s.w + 1;   // W + 1 frame columns: x = -1 of row y + 1 is x = W of row y (conv_tc.cu)
   p.rows_h = (3 * p.Wp + 128 * kS + p.Wp - 1) / p.Wp;
   if (p.rows_h > 256) return p;
   p.halo_pos = p.rows_h * p.Wp;

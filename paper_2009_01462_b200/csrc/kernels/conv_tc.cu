@@ -7,7 +7,8 @@
 //
 // Design:
 //  * Output positions live in the zero-padded "interior frame" of one image (H rows x
-//    (W+2) columns, flattened): tap (dy,dx) is then a constant shift of dy*(W+2)+dx
+//    (W+1) columns, flattened; the one zero column x = -1 of a row is also the previous
+//    row's x = W): tap (dy,dx) is then a constant shift of dy*(W+1)+dx
 //    positions, so one halo slab per 16-channel chunk, loaded once by TMA (out-of-bounds
 //    rows/columns zero-filled), serves all 9 taps as 9 shifted UMMA descriptors.  The 2
 //    padding columns per row are computed and discarded.
@@ -843,8 +844,10 @@ struct Plan {
 
 Plan plan_for(const ConvShape& s, int mode = MODE_X3TF32) {
   Plan p;
-  if (s.co % 64 != 0 || s.ci % kChunk != 0 || s.w + 2 > 256) return p;
-  p.Wp = s.w + 2;
+  if (s.co % 64 != 0 || s.ci % kChunk != 0 || s.w + 1 > 256) return p;
+  // W + 1 frame columns: one zero column (x = -1) per row also serves as the previous row's
+  // right pad (x = W), so 1/W of the MMA work is padding instead of 2/W
+  p.Wp = s.w + 1;
   p.rows_h = (3 * p.Wp + 128 * kS + p.Wp - 1) / p.Wp;
   if (p.rows_h > 256) return p;
   p.halo_pos = p.rows_h * p.Wp;
