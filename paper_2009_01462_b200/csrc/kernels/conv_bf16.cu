@@ -194,7 +194,6 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
   } else if (warp == 1) {
     // ===================== MMA issuer =====================
-    const uint32_t id = idesc(1, 128, 128);                 // bf16 x bf16 -> fp32, M 128, N 128
     const uint32_t kg_x = (uint32_t)a.halo_pos * 16u;     // bytes between 8-channel groups (halo)
     const uint32_t kg_w = 128u * 16u;                     // bytes between 8-channel groups (weights)
     const uint64_t xj = (uint64_t)((2 * kg_x) >> 4);      // one K = 16 step of B, 16-byte units
@@ -207,6 +206,11 @@ __global__ void __launch_bounds__(kThreads, 1)
     while (it.next(cb, n, tile0, ntiles)) {
       const int f0 = tile0 * 128;
       const int c0 = f0 - (f0 / Wp) * Wp;
+      // one MMA spans the unit's frame positions (N = 256 for two tiles, the image's last
+      // tile only as far as the frame goes): A is read once per (tap, k-step) instead of once
+      // per tile (an N = 128 MMA with a fresh A costs ~107 cycles against 64)
+      const int nvalid = min(ntiles * 128, a.H * Wp - f0);
+      const uint32_t id_unit = idesc(1, 128, (nvalid + 15) / 16 * 16);
       mbar_wait(&acc_empty[ab], aph ^ 1);
       tc_fence_after();
       const uint32_t d0 = tmem_base + (uint32_t)(ab * kS * 128);
@@ -227,9 +231,7 @@ __global__ void __launch_bounds__(kThreads, 1)
               for (int j = 0; j < 2; ++j) {
                 const uint64_t da = dw0 + dx * wtap + j * wj;
                 const uint32_t accum = (first && dx == 0 && j == 0) ? 0u : 1u;
-#pragma unroll
-                for (int s = 0; s < kS; ++s)
-                  if (s < ntiles) mma_f16(d0 + s * 128, da, bb + (uint64_t)(dx + 128 * s) + j * xj, id, accum);
+                mma_f16(d0, da, bb + (uint64_t)dx + j * xj, id_unit, accum);
               }
             }
             mma_commit(&w_empty[ws]);
