@@ -31,7 +31,9 @@ namespace {
 using namespace rp::umma;
 
 constexpr int kThreads = 320;
-constexpr int kWStages = 3;
+constexpr int kWStages = 3;          // weight ring depth, fp32-input mode
+constexpr int kBfMax = 4;            // bf16 halo slots, max (bf16-input mode)
+constexpr int kWMax = 6;             // weight ring depth, max
 constexpr int kChunk = 32;           // input channels per halo chunk
 constexpr int kS = 2;                // 128-position tiles per unit
 constexpr int kMaxSmem = 227 * 1024;
@@ -43,6 +45,7 @@ struct BfArgs {
   uint32_t bf_bytes;    // bf16 halo chunk: [4 kg][positions][8 ch]
   uint32_t bf_stride;   // bytes per bf16 slot (with zero pads before / after)
   uint32_t w_tap;       // bytes of one tap's A operand: 4 kg x 128 rows x 16 B
+  int nbf, nw;          // bf16 halo slots, weight ring depth
   float h;
   const __nv_bfloat16* w;   // prepped [cb][chunk][tap][kg][128 rows][8]
   const float* bias;
@@ -106,32 +109,35 @@ __global__ void __launch_bounds__(kThreads, 1)
   const uint32_t w_stage = 3 * a.w_tap;
   uint8_t* raw_base = smem;                                    // 2 fp32 slots
   uint8_t* bf_base = smem + 2 * a.raw_stride;                  // 2 bf16 slots
-  uint8_t* w_base = bf_base + 2 * a.bf_stride;                 // kWStages stages
-  uint64_t* bars = reinterpret_cast<uint64_t*>(w_base + kWStages * w_stage);
-  uint64_t* raw_full = bars;           // [2] TMA -> converters
-  uint64_t* raw_empty = bars + 2;      // [2] converters -> TMA
-  uint64_t* bf_full = bars + 4;        // [2] converters -> MMA
-  uint64_t* bf_empty = bars + 6;       // [2] MMA -> converters
-  uint64_t* w_full = bars + 8;         // [kWStages]
-  uint64_t* w_empty = bars + 8 + kWStages;
-  uint64_t* acc_full = bars + 8 + 2 * kWStages;    // [2]
-  uint64_t* acc_empty = bars + 10 + 2 * kWStages;  // [2]
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 12 + 2 * kWStages);
+  const int nbf = a.nbf, nw = a.nw;
+  uint8_t* w_base = bf_base + nbf * a.bf_stride;               // nw stages
+  uint64_t* bars = reinterpret_cast<uint64_t*>(w_base + nw * w_stage);
+  uint64_t* raw_full = bars;                    // [kBfMax] TMA -> converters (BIN: TMA -> MMA)
+  uint64_t* raw_empty = bars + kBfMax;          // [kBfMax] converters -> TMA
+  uint64_t* bf_full = bars + 2 * kBfMax;        // [kBfMax] converters -> MMA
+  uint64_t* bf_empty = bars + 3 * kBfMax;       // [kBfMax] MMA -> converters (BIN: MMA -> TMA)
+  uint64_t* w_full = bars + 4 * kBfMax;         // [kWMax]
+  uint64_t* w_empty = bars + 4 * kBfMax + kWMax;
+  uint64_t* acc_full = bars + 4 * kBfMax + 2 * kWMax;    // [2]
+  uint64_t* acc_empty = bars + 4 * kBfMax + 2 * kWMax + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 4 * kBfMax + 2 * kWMax + 4);
 
   auto raw_s = [&](int s) { return raw_base + s * a.raw_stride; };
   auto bf_s = [&](int s) { return bf_base + s * a.bf_stride + 128; };
   auto w_s = [&](int s) { return w_base + s * w_stage; };
 
   if (threadIdx.x == 0) {
-    for (int i = 0; i < 2; ++i) {
+    for (int i = 0; i < kBfMax; ++i) {
       mbar_init(&raw_full[i], 1);
       mbar_init(&raw_empty[i], 128);
       mbar_init(&bf_full[i], 128);
       mbar_init(&bf_empty[i], 1);
-      mbar_init(&acc_full[i], 1);
-      mbar_init(&acc_empty[i], 128);
     }
-    for (int i = 0; i < kWStages; ++i) {
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&acc_full[i], 1);
+      mbar_init(&acc_empty[i], BIN ? 256 : 128);   // every epilogue thread, once per unit
+    }
+    for (int i = 0; i < kWMax; ++i) {
       mbar_init(&w_full[i], 1);
       mbar_init(&w_empty[i], 1);
     }
@@ -140,7 +146,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   }
   if (warp == 1) tmem_alloc<512>(tmem_slot);
   // zero the 128-byte pads around the bf16 halo (read only for discarded positions)
-  for (int i = threadIdx.x; i < 2 * 2 * 32; i += blockDim.x) {
+  for (int i = threadIdx.x; i < nbf * 2 * 32; i += blockDim.x) {
     const int s = i / 64, part = (i / 32) & 1, w = i % 32;
     uint8_t* base = bf_base + s * a.bf_stride + (part == 0 ? 0 : 128 + a.bf_bytes);
     reinterpret_cast<uint32_t*>(base)[w] = 0u;
@@ -180,7 +186,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           }
         }
         __syncwarp();
-        if (++rs == 2) rs = 0, rph ^= 1;
+        if (++rs == (BIN ? nbf : 2)) rs = 0, rph ^= 1;
         for (int dy = 0; dy < 3; ++dy) {
           mbar_wait(&w_empty[ws], wph ^ 1);
           if (elect_one()) {
@@ -188,7 +194,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             bulk_load(w_s(ws), wcb + ((int64_t)c * 9 + 3 * dy) * (a.w_tap / 2), wbytes, &w_full[ws]);
           }
           __syncwarp();
-          if (++ws == kWStages) ws = 0, wph ^= 1;
+          if (++ws == nw) ws = 0, wph ^= 1;
         }
       }
     }
@@ -237,19 +243,18 @@ __global__ void __launch_bounds__(kThreads, 1)
             mma_commit(&w_empty[ws]);
           }
           __syncwarp();
-          if (++ws == kWStages) ws = 0, wph ^= 1;
+          if (++ws == nw) ws = 0, wph ^= 1;
         }
         if (elect_one()) mma_commit(&bf_empty[bs]);
         __syncwarp();
-        if (++bs == 2) bs = 0, bph ^= 1;
+        if (++bs == nbf) bs = 0, bph ^= 1;
       }
       if (elect_one()) mma_commit(&acc_full[ab]);
       __syncwarp();
       if (++ab == 2) ab = 0, aph ^= 1;
     }
-  } else if (warp < 6) {
-    if constexpr (BIN) {}   // nothing to convert
-    else {
+  } else if (!BIN && warp < 6) {
+    {
     // ===================== converters: fp32 halo -> bf16 K-major interleave =====================
     // raw [g = 8 groups of 4 ch][pos][4 floats]  ->  bf16 [k = 4 groups of 8 ch][pos][8 bf16]
     const int tid = threadIdx.x - 64;
@@ -274,15 +279,19 @@ __global__ void __launch_bounds__(kThreads, 1)
         mbar_arrive(&bf_full[bs]);
         mbar_arrive(&raw_empty[rs]);
         if (++rs == 2) rs = 0, rph ^= 1;
-        if (++bs == 2) bs = 0, bph ^= 1;
+        if (++bs == nbf) bs = 0, bph ^= 1;
       }
     }
     }
   } else {
     // ===================== epilogue =====================
-    // TMEM lane r = output channel cb*128 + r; a warp owns lanes 32q..32q+31 and walks
-    // the positions 16 columns at a time: one 128-byte store per position (NHWC).
+    // TMEM lane r = output channel cb*128 + r; a warp owns lanes 32q..32q+31 and walks the
+    // positions 16 columns at a time: one 128-byte store per position (NHWC).  bf16-input
+    // mode: the idle converter warps (2-5) form a second group, group g drains tile g of
+    // every unit; the aux operand of the next 16 positions is loaded before the current ones
+    // are finished, so the loads' latency overlaps the stores.
     const int q = warp & 3;
+    const int grp = BIN ? (warp >= 6 ? 0 : 1) : 0;
     constexpr bool kBias = EPI == EPI_BIAS || EPI == EPI_BIAS_TANH || EPI == EPI_RESID;
     constexpr bool kAux = EPI == EPI_RESID || EPI == EPI_TANH_BWD || EPI == EPI_ADD;
     constexpr bool kAux16 = EPI == EPI_DTANH16;
@@ -301,34 +310,39 @@ __global__ void __launch_bounds__(kThreads, 1)
       const __nv_bfloat16* auxb16 = kAux16 ? a.aux16 + img * a.Co + co : nullptr;
       mbar_wait(&acc_full[ab], aph);
       tc_fence_after();
-      for (int s = 0; s < ntiles; ++s) {
+      const int s_lo = BIN ? grp : 0, s_hi = BIN ? min(grp + 1, ntiles) : ntiles;
+      for (int s = s_lo; s < s_hi; ++s) {
         const uint32_t tcol = tmem_base + ((uint32_t)(q * 32) << 16) + (uint32_t)((ab * kS + s) * 128);
         const int fb = (tile0 + s) * 128;
-        int y = fb / Wp, X = fb - (fb / Wp) * Wp;
-        for (int p0 = 0; p0 < 128; p0 += 16) {
-          int off[16];
-          bool ok[16];
-          float ax[16];
+        const int nb = min(8, (a.H * Wp - fb + 15) / 16);   // 16-position batches with frame positions
+        int off[16];
+        float ax[16];
+        auto load = [&](int f0, int (&o)[16], float (&x)[16]) {
 #pragma unroll
           for (int e = 0; e < 16; ++e) {
-            ok[e] = y < a.H && X >= 1 && X <= a.W;
-            off[e] = ok[e] ? (y * a.W + (X - 1)) * a.Co : 0;
-            if (++X == Wp) X = 0, ++y;
+            const int f = f0 + e, y = f / Wp, X = f - y * Wp;
+            o[e] = (y < a.H && X >= 1 && X <= a.W) ? (y * a.W + (X - 1)) * a.Co : -1;
           }
           if constexpr (kAux) {
 #pragma unroll
-            for (int e = 0; e < 16; ++e) ax[e] = auxb[off[e]];
+            for (int e = 0; e < 16; ++e) x[e] = o[e] >= 0 ? auxb[o[e]] : 0.f;
           }
           if constexpr (kAux16) {
 #pragma unroll
-            for (int e = 0; e < 16; ++e) ax[e] = __bfloat162float(auxb16[off[e]]);
+            for (int e = 0; e < 16; ++e) x[e] = o[e] >= 0 ? __bfloat162float(auxb16[o[e]]) : 0.f;
           }
+        };
+        load(fb, off, ax);
+        for (int b = 0; b < nb; ++b) {
+          int offn[16];
+          float axn[16];
+          if (b + 1 < nb) load(fb + 16 * (b + 1), offn, axn);
           uint32_t r[16];
-          tmem_ld16(tcol + (uint32_t)p0, r);
+          tmem_ld16(tcol + (uint32_t)(16 * b), r);
           tmem_wait_ld();
 #pragma unroll
           for (int e = 0; e < 16; ++e) {
-            if (!ok[e]) continue;                               // warp-uniform
+            if (off[e] < 0) continue;                           // warp-uniform
             const float v = __uint_as_float(r[e]);
             float o;
             if constexpr (EPI == EPI_BIAS) o = v + bias;
@@ -342,6 +356,8 @@ __global__ void __launch_bounds__(kThreads, 1)
             if (outb16) outb16[off[e]] = __float2bfloat16_rn(o);
             if (outb16d) outb16d[off[e]] = __float2bfloat16_rn(1.f - o * o);
           }
+#pragma unroll
+          for (int e = 0; e < 16; ++e) off[e] = offn[e], ax[e] = axn[e];
         }
       }
       tc_fence_before();
@@ -439,6 +455,7 @@ struct Plan {
   bool ok = false;
   int Wp, rows_h, halo_pos, T;
   uint32_t raw_bytes, raw_stride, bf_bytes, bf_stride, w_tap;
+  int nbf = 2, nw = kWStages;
   size_t smem;
 };
 
@@ -455,7 +472,19 @@ Plan plan_for(const ConvShape& s, bool bin = false) {
   p.bf_bytes = (uint32_t)p.halo_pos * kChunk * 2u;
   p.bf_stride = (128 + p.bf_bytes + 128 + 1023) / 1024 * 1024;
   p.w_tap = 4u * 128u * 16u;
-  p.smem = 2 * (size_t)p.raw_stride + 2 * (size_t)p.bf_stride + kWStages * 3 * (size_t)p.w_tap + 512 + 1024;
+  const size_t fixed = 512 + 1024;
+  if (bin) {
+    // no fp32 staging: the freed space deepens the bf16 halo ring and the weight ring (the
+    // halo of a 32-channel chunk feeds 2304 MMA cycles; 2 slots left its TMA latency exposed)
+    p.ok = false;
+    for (int nb = kBfMax; nb >= 2 && !p.ok; --nb)
+      for (int w = kWMax; w >= kWStages && !p.ok; --w) {
+        const size_t need = nb * (size_t)p.bf_stride + w * 3 * (size_t)p.w_tap + fixed;
+        if (need <= (size_t)kMaxSmem) p.nbf = nb, p.nw = w, p.smem = need, p.ok = true;
+      }
+    return p;
+  }
+  p.smem = 2 * (size_t)p.raw_stride + 2 * (size_t)p.bf_stride + kWStages * 3 * (size_t)p.w_tap + fixed;
   p.ok = p.smem <= (size_t)kMaxSmem;
   return p;
 }
@@ -536,6 +565,8 @@ void conv_bf16_any(const ConvShape& s, const void* in, bool bin, const float* w_
   a.bf_bytes = p.bf_bytes;
   a.bf_stride = p.bf_stride;
   a.w_tap = p.w_tap;
+  a.nbf = p.nbf;
+  a.nw = p.nw;
   a.h = h;
   a.w = wp;
   a.bias = bias;
