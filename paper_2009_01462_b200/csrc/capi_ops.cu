@@ -261,10 +261,11 @@ void block_bwd_planes(const rp_geometry& g, int nrows, const void* x_p, const fl
   (void)dpre;
   conv(shape(g, nrows, C, Ch), gio, pb + L.w2, true, nullptr, a, h, tanh_act ? k::EPI_TANH_BWD : k::EPI_SCALE, nullptr,
        RP_MATH_FP32, wws, RP_PROF_CONV_DGRAD, tanh_act, st, dpre_p, g_p, f);
-  // gW2 = h a^T g, gb2 = h sum g                                  (network.cpp:98-99)
-  wgrad_planes(shape(g, nrows, Ch, C), a_p, g_p, h, gb + L.w2, gb + L.b2, wgws, st);
-  // gW1 = x^T dpre, gb1 = sum dpre                                (network.cpp:102-103)
+  // gW1 = x^T dpre, gb1 = sum dpre first, while dgrad2's dpre planes are still in L2
+  //                                                               (network.cpp:102-103)
   wgrad_planes(shape(g, nrows, C, Ch), x_p, dpre_p, 1.f, gb + L.w1, gb + L.b1, wgws, st);
+  // gW2 = h a^T g, gb2 = h sum g (before dgrad1 overwrites the g planes) (network.cpp:98-99)
+  wgrad_planes(shape(g, nrows, Ch, C), a_p, g_p, h, gb + L.w2, gb + L.b2, wgws, st);
   // g <- g + dpre * W1^T in place, and the planes of the new g   (network.cpp:104)
   conv(shape(g, nrows, Ch, C), dpre, pb + L.w1, true, nullptr, gio, 1.f, k::EPI_ADD, gio, RP_MATH_FP32, wws,
        RP_PROF_CONV_DGRAD, true, st, g_p, dpre_p, f ? f + fb : nullptr);
@@ -318,10 +319,10 @@ void block_bwd_bf16t(const rp_geometry& g, int nrows, const void* x16, const voi
     k::conv3x3_fwd_bf16_in16(sd2, g16, pb + L.w2, true, nullptr, nullptr, tanh_act ? d16 : nullptr, h,
                              tanh_act ? k::EPI_DTANH16 : k::EPI_SCALE, nullptr, dpre16, nullptr, wws, st);
   }
-  // gW2 = h a^T g, gb2 = h sum g                                    (network.cpp:98-99)
-  wgrad_bf16p(shape(g, nrows, Ch, C), a16, g16, h, gb + L.w2, gb + L.b2, wgws, st);
-  // gW1 = x^T dpre, gb1 = sum dpre                                  (network.cpp:102-103)
+  // gW1 = x^T dpre, gb1 = sum dpre first, while dpre16 is still in L2   (network.cpp:102-103)
   wgrad_bf16p(shape(g, nrows, C, Ch), x16, dpre16, 1.f, gb + L.w1, gb + L.b1, wgws, st);
+  // gW2 = h a^T g, gb2 = h sum g (before dgrad1 rewrites g16)             (network.cpp:98-99)
+  wgrad_bf16p(shape(g, nrows, Ch, C), a16, g16, h, gb + L.w2, gb + L.b2, wgws, st);
   {   // g <- g + dpre * W1^T in place, and its bf16 copy           (network.cpp:104)
     prof::Scope ps(RP_PROF_CONV_DGRAD, st, conv_flops(sd1), 2.0 * sd1.pixels() * sd1.ci + 10.0 * sd1.pixels() * sd1.co);
     k::conv3x3_fwd_bf16_in16(sd1, dpre16, pb + L.w1, true, nullptr, gio, nullptr, 1.f, k::EPI_ADD, gio, g16, nullptr,
