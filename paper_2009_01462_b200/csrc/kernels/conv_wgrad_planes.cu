@@ -23,6 +23,7 @@
 #include <cuda.h>
 #include <cuda_bf16.h>
 
+#include <cstdlib>
 #include <map>
 #include <mutex>
 #include <tuple>
@@ -48,6 +49,7 @@ struct PwArgs {
   int N, H, W, Ci, Co, Wp, rg, P, Pp, nstages;
   int mo, mi;                    // co / ci blocks (64 channels, single: 128)
   int single;                    // 1: one bf16 plane per operand, 128-channel blocks
+  int nobias;                    // diagnostics (RP_WGRAD_NOBIAS): skip the bias sums
   int blocks_per_img, num_blocks;
   uint32_t g_slab;               // bytes per bf16 g plane slab (Pp rows x 128 B, 1 KB aligned)
   uint32_t x_slab;               // bytes per bf16 x plane slab (rg * Wp rows of one filter row, packed)
@@ -92,7 +94,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int t0 = gi * kTg;
   const int Wp = a.Wp;
   const int xrows = a.rg * Wp;   // x rows of this tap group's filter row only (y0 - 1 + gi ..)
-  const bool do_bias = gi == 0 && cib == 0;
+  const bool do_bias = gi == 0 && cib == 0 && !a.nobias;
 
   if (threadIdx.x == 0) {
     for (int i = 0; i < S; ++i) {
@@ -430,7 +432,12 @@ PwPlan plan(const ConvShape& s, bool single = false) {
   const int Wp = s.w + 2;
   // (rows per block, stages) in order of preference
   const int cand[][2] = {{4, 3}, {3, 3}, {2, 3}, {4, 2}, {2, 2}, {1, 2}};
+  static const int forced = [] {   // diagnostics: RP_WGRAD_PCFG = rows * 10 + stages
+    const char* e = std::getenv("RP_WGRAD_PCFG");
+    return e ? std::atoi(e) : 0;
+  }();
   for (const auto& c : cand) {
+    if (forced && forced != c[0] * 10 + c[1]) continue;
     const int rg = std::min(c[0], s.h), st = c[1];
     PwPlan q;
     q.rg = rg;
@@ -484,6 +491,8 @@ void launch_wgrad_planes(const ConvShape& s, const void* x0, const void* x1, con
   const int cbk = single ? 128 : 64;
   PwArgs a{};
   a.single = single ? 1 : 0;
+  static const int nobias = std::getenv("RP_WGRAD_NOBIAS") ? 1 : 0;
+  a.nobias = nobias;
   a.N = s.n;
   a.H = s.h;
   a.W = s.w;
