@@ -351,3 +351,44 @@ def test_bf16_trainer_vs_oracle(case):
     for k in range(K):
         got = gt.state(k, rp.BOUNDARY_OUT)
         assert rel_err(got, ot.stage(k).boundary_out) <= BF16_TOL, (k, rel_err(got, ot.stage(k).boundary_out))
+
+
+_SWITCH_SCRIPT = r"""
+import hashlib, sys
+import numpy as np
+import torch
+sys.path.insert(0, sys.argv[1])
+import paper_2009_01462_b200 as rp
+from oracle import respar_oracle as O
+g = rp.Geometry(3, 16, 16, 64, 64, 4, 10)
+x, y = O.synthetic_batch(O.Geometry(3, 16, 16, 64, 64, 4, 10), 8, 3)
+xs = np.ascontiguousarray(x, np.float32)
+tr = rp.DecoupledTrainer(g, 2, rp.ALM, rp.SQUARED_L2, 8, seed_state=11)
+tr.reset_lambda_from_forward(xs)
+tr.use_cuda_graphs(True)
+xd = torch.from_numpy(xs).cuda()
+yd = torch.from_numpy(y.astype(np.int32)).cuda()
+sp = rp.StepParams(beta=0.1, lr=0.05, lambda_lr=0.05, kappa_lr=1e-6)
+for _ in range(3):
+    tr.step_device(xd.data_ptr(), yd.data_ptr(), 8, 0, sp)
+h = hashlib.sha256(tr.params().tobytes() + tr.state(1, rp.LAMBDA).tobytes() + tr.state(1, rp.KAPPA).tobytes())
+print(h.hexdigest())
+"""
+
+
+@pytest.mark.gpu
+def test_schedule_switches_are_bitwise_neutral():
+    """Programmatic dependent launch (RP_PDL) and the resident conv filter (RP_CONV_RESIDENT)
+    change when and from where kernels read, never what they compute: three graphed steps
+    give bitwise the same parameters and multipliers with either switched off."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    out = {}
+    for name, env in (("default", {}), ("no_pdl", {"RP_PDL": "0"}), ("streamed_filter", {"RP_CONV_RESIDENT": "0"})):
+        r = subprocess.run([sys.executable, "-c", _SWITCH_SCRIPT, root], env={**os.environ, **env},
+                           capture_output=True, text=True, timeout=300)
+        assert r.returncode == 0, r.stderr[-2000:]
+        out[name] = r.stdout.strip().splitlines()[-1]
+    assert out["default"] == out["no_pdl"] == out["streamed_filter"], out
