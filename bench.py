@@ -313,6 +313,7 @@ def run_ours_distributed(args, cfg, rank, world):
             y.copy_(y_host, non_blocking=True)
         torch.cuda.current_stream().synchronize()
         tr.step(xp, yp, B, 0, sp, read_loss=True)
+    torch.cuda.synchronize()   # every local stage's stream, not only the one the loss came from
     e2e_s = torch.tensor([(time.perf_counter() - t0) / e2e_steps], device="cuda")
     dist.all_reduce(e2e_s, op=dist.ReduceOp.MAX)
     return dict(tr=tr, total_ms=total_ms, prof=prof, clocks=clk, launches=launches, loss=loss,

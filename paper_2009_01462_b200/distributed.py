@@ -335,9 +335,14 @@ class DistributedDecoupledTrainer:
         import torch.distributed as dist
         p = self.plc
         last = p.rank_of_stage(p.stages - 1)
-        t = self.engine.loss_tensor().clone() if p.last else None
-        if p.group_size == 1:
-            return float(t.item())
+        t = None
+        if p.last:
+            # copy on the stream that wrote the loss (the last stage's), not torch's current
+            # stream, which does not wait for the engine's stage streams
+            with self.engine.stream(p.hi - 1):
+                t = self.engine.loss_tensor().clone()
+                if p.group_size == 1:
+                    return float(t.item())
         if t is None:
             t = self._zeros_like_loss()
         with self.engine.stream(p.hi - 1):
