@@ -378,17 +378,19 @@ print(h.hexdigest())
 
 @pytest.mark.gpu
 def test_schedule_switches_are_bitwise_neutral():
-    """Programmatic dependent launch (RP_PDL) and the resident conv filter (RP_CONV_RESIDENT)
-    change when and from where kernels read, never what they compute: three graphed steps
-    give bitwise the same parameters and multipliers with either switched off."""
+    """Programmatic dependent launch (RP_PDL), the resident conv filter (RP_CONV_RESIDENT) and
+    concurrent stage streams (RP_CONCURRENT_STAGES) change when and from where kernels read,
+    never what they compute: three graphed steps give bitwise the same parameters and
+    multipliers under each."""
     import os
     import subprocess
     import sys
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
     out = {}
-    for name, env in (("default", {}), ("no_pdl", {"RP_PDL": "0"}), ("streamed_filter", {"RP_CONV_RESIDENT": "0"})):
+    for name, env in (("default", {}), ("no_pdl", {"RP_PDL": "0"}), ("streamed_filter", {"RP_CONV_RESIDENT": "0"}),
+                      ("concurrent_stages", {"RP_CONCURRENT_STAGES": "1"})):
         r = subprocess.run([sys.executable, "-c", _SWITCH_SCRIPT, root], env={**os.environ, **env},
                            capture_output=True, text=True, timeout=300)
         assert r.returncode == 0, r.stderr[-2000:]
         out[name] = r.stdout.strip().splitlines()[-1]
-    assert out["default"] == out["no_pdl"] == out["streamed_filter"], out
+    assert out["default"] == out["no_pdl"] == out["streamed_filter"] == out["concurrent_stages"], out
