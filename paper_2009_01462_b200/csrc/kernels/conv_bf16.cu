@@ -16,6 +16,7 @@
 #include <cuda.h>
 #include <cuda_bf16.h>
 
+#include <cstdlib>
 #include <map>
 #include <mutex>
 #include <tuple>
@@ -54,6 +55,7 @@ struct BfArgs {
   float* out;                   // may be null (bf16 tape outputs only)
   __nv_bfloat16* out16;         // optional bf16 copy of out (the bf16 wgrad's operand)
   __nv_bfloat16* out16d;        // optional bf16(1 - out^2)
+  int dbg;                      // diagnostics (RP_BF16_DBG): 1 no aux loads, 2 no stores
 };
 
 // Work split as in conv_tc.cu: full kS-tile units round-robin from CTA 0, the per-image
@@ -308,6 +310,8 @@ __global__ void __launch_bounds__(kThreads, 1)
       __nv_bfloat16* outb16 = a.out16 ? a.out16 + img * a.Co + co : nullptr;
       __nv_bfloat16* outb16d = a.out16d ? a.out16d + img * a.Co + co : nullptr;
       const __nv_bfloat16* auxb16 = kAux16 ? a.aux16 + img * a.Co + co : nullptr;
+      const __nv_bfloat16* auxb16_pair = kAux16 ? a.aux16 + img * a.Co + (co & ~1) : nullptr;
+      const bool odd_ch = co & 1;
       mbar_wait(&acc_full[ab], aph);
       tc_fence_after();
       const int s_lo = BIN ? grp : 0, s_hi = BIN ? min(grp + 1, ntiles) : ntiles;
@@ -329,7 +333,14 @@ __global__ void __launch_bounds__(kThreads, 1)
           }
           if constexpr (kAux16) {
 #pragma unroll
-            for (int e = 0; e < 16; ++e) x[e] = o[e] >= 0 ? __bfloat162float(auxb16[o[e]]) : 0.f;
+            for (int e = 0; e < 16; ++e) {
+              // 32-bit read-only loads of the channel pair (lanes 2i, 2i+1 share the word), the
+              // lane's half selected: the 16-bit loads ran this epilogue at half speed
+              const uint32_t u = (o[e] >= 0 && !(a.dbg & 1))
+                                     ? __ldg(reinterpret_cast<const unsigned int*>(auxb16_pair + o[e]))
+                                     : 0x3f803f80u;
+              x[e] = __uint_as_float(odd_ch ? (u & 0xffff0000u) : (u << 16));
+            }
           }
         };
         load(fb, off, ax);
@@ -352,6 +363,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             else if constexpr (EPI == EPI_ADD) o = ax[e] + v;
             else if constexpr (EPI == EPI_DTANH16) o = (a.h * v) * ax[e];
             else o = a.h * v;
+            if (a.dbg & 2) continue;
             if (outb) outb[off[e]] = o;
             if (outb16) outb16[off[e]] = __float2bfloat16_rn(o);
             if (outb16d) outb16d[off[e]] = __float2bfloat16_rn(1.f - o * o);
@@ -575,6 +587,11 @@ void conv_bf16_any(const ConvShape& s, const void* in, bool bin, const float* w_
   a.out = out;
   a.out16 = static_cast<__nv_bfloat16*>(out16);
   a.out16d = static_cast<__nv_bfloat16*>(out16d);
+  static const int dbg = [] {
+    const char* e = std::getenv("RP_BF16_DBG");
+    return e ? std::atoi(e) : 0;
+  }();
+  a.dbg = dbg;
   const CUtensorMap& m = cached_map(in, s, p.Wp, p.rows_h, bin);
   const int units = (s.co / 128) * s.n * ((p.T + kS - 1) / kS);
   const int grid = std::min(units, kNumSMs);
