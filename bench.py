@@ -35,7 +35,9 @@ CONFIGS = {
     "C1": dict(cin=1, h=28, w=28, c=16, ch=16, L=8, K=2, B=128, mode="penalty", math="fp32"),
     "C2": dict(cin=3, h=32, w=32, c=64, ch=64, L=16, K=4, B=256, mode="alm", math="fp32", concurrent=True),
     "C3": dict(cin=3, h=32, w=32, c=64, ch=64, L=64, K=8, B=256, mode="alm", math="fp32", concurrent=True),
-    "C4": dict(cin=3, h=32, w=32, c=64, ch=64, L=64, K=1, B=256, mode="serial", math="fp32"),
+    # serial full backprop through 64 blocks diverges at lr 0.1 within ~15 steps (and at 0.03,
+    # tools/loss_steps.py); 0.005 keeps the timed steps on finite data
+    "C4": dict(cin=3, h=32, w=32, c=64, ch=64, L=64, K=1, B=256, mode="serial", math="fp32", lr=0.005),
     "C5": dict(cin=3, h=32, w=32, c=256, ch=256, L=64, K=8, B=1024, mode="alm", math="bf16"),
 }
 CLASSES = 10
@@ -66,7 +68,8 @@ def step_params(cfg):
     beta = 0.1 if cfg["mode"] == "alm" else 1.0
     n = cfg["B"] * cfg["h"] * cfg["w"] * cfg["c"]
     kappa_lr = KAPPA_STEP * 2.0 * beta / n
-    return rp.StepParams(beta=beta, tau=-1.0, lr=0.1, lambda_lr=0.1, kappa_lr=kappa_lr, max_corrections=1)
+    lr = cfg.get("lr", 0.1)
+    return rp.StepParams(beta=beta, tau=-1.0, lr=lr, lambda_lr=lr, kappa_lr=kappa_lr, max_corrections=1)
 
 
 class ClockSampler:
@@ -407,7 +410,7 @@ def run_reference(args, cfg, rank, world):
 def _cfg_json(cfg):
     return {"in": [cfg["cin"], cfg["h"], cfg["w"]], "global_batch": cfg["B"], "channels": cfg["c"],
             "hidden": cfg["ch"], "blocks": cfg["L"], "stages": cfg["K"], "mode": cfg["mode"],
-            "math": cfg["math"], "classes": CLASSES}
+            "math": cfg["math"], "classes": CLASSES, "lr": cfg.get("lr", 0.1)}
 
 
 def main():
