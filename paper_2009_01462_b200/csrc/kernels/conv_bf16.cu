@@ -123,6 +123,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint64_t* acc_full = bars + 4 * kBfMax + 2 * kWMax;    // [2]
   uint64_t* acc_empty = bars + 4 * kBfMax + 2 * kWMax + 2;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 4 * kBfMax + 2 * kWMax + 4);
+  float* xchg = reinterpret_cast<float*>(bars + 64);         // BIN epilogue: [2 groups][8 pos][128 co]
+  int* pos_tab = reinterpret_cast<int*>(xchg + 2 * 8 * 128); // BIN epilogue: [2 groups][128]
 
   auto raw_s = [&](int s) { return raw_base + s * a.raw_stride; };
   auto bf_s = [&](int s) { return bf_base + s * a.bf_stride + 128; };
@@ -287,6 +289,116 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
   } else {
     // ===================== epilogue =====================
+    if constexpr (BIN) {
+    // Two groups of 4 warps (the idle converter warps 2-5 and warps 6-9); group g drains tile g
+    // of every unit.  Batches of 8 positions: each warp moves its 32 rows (output channels) x 8
+    // columns to shared memory as [position][128 co]; the group reads it back transposed -- a
+    // thread owns 4 consecutive channels of a position (two items per batch) -- and finishes
+    // the fused epilogue with vector loads and stores: 16-byte fp32, 8-byte bf16 (the per-lane
+    // 2-byte bf16 accesses of a channel-per-lane epilogue ran at a fraction of the bandwidth).
+    // The next batch's aux operand is loaded before the current one is finished.
+    const int q = warp & 3;
+    const int grp = warp >= 6 ? 0 : 1;
+    const int gtid = (warp & 3) * 32 + lane;              // 0..127 within the group
+    constexpr bool kBias = EPI == EPI_BIAS || EPI == EPI_BIAS_TANH || EPI == EPI_RESID;
+    constexpr bool kAux = EPI == EPI_RESID || EPI == EPI_TANH_BWD || EPI == EPI_ADD;
+    constexpr bool kAux16 = EPI == EPI_DTANH16;
+    float* buf = xchg + grp * 8 * 128;
+    int* tab = pos_tab + grp * 128;
+    const uint32_t grp_bar = 6 + grp;
+    const int cg = gtid & 31;                             // channel group: channels 4 cg .. 4 cg + 3
+    const int pr0 = gtid >> 5;                            // items: positions pr0 and pr0 + 4 of a batch
+    int ab = 0;
+    uint32_t aph = 0;
+    UnitIter it(a.Co / 128, a.N, a.T);
+    int cb, n, tile0, ntiles;
+    while (it.next(cb, n, tile0, ntiles)) {
+      const int64_t img = (int64_t)n * a.H * a.W;
+      const int co4 = cb * 128 + 4 * cg;
+      float4 bias = make_float4(0.f, 0.f, 0.f, 0.f);
+      if (kBias) bias = *reinterpret_cast<const float4*>(a.bias + co4);
+      mbar_wait(&acc_full[ab], aph);
+      tc_fence_after();
+      if (grp < ntiles) {
+        const int fb = (tile0 + grp) * 128;
+        {
+          const int f = fb + gtid, y = f / Wp, X = f - y * Wp;
+          asm volatile("bar.sync %0, 128;" ::"r"(grp_bar) : "memory");   // previous tile's readers are done
+          tab[gtid] = (y < a.H && X >= 1 && X <= a.W) ? (y * a.W + (X - 1)) * a.Co : -1;
+          asm volatile("bar.sync %0, 128;" ::"r"(grp_bar) : "memory");
+        }
+        const uint32_t tcol = tmem_base + ((uint32_t)(q * 32) << 16) + (uint32_t)((ab * kS + grp) * 128);
+        const float* auxb = kAux ? a.aux + img * a.Co + co4 : nullptr;
+        const __nv_bfloat16* auxb16 = kAux16 ? a.aux16 + img * a.Co + co4 : nullptr;
+        float* outb = a.out ? a.out + img * a.Co + co4 : nullptr;
+        __nv_bfloat16* outb16 = a.out16 ? a.out16 + img * a.Co + co4 : nullptr;
+        __nv_bfloat16* outb16d = a.out16d ? a.out16d + img * a.Co + co4 : nullptr;
+        const int nb = min(16, (a.H * Wp - fb + 7) / 8);  // 8-position batches with frame positions
+        float4 ax[2];
+        auto load = [&](int b, float4 (&x)[2]) {
+#pragma unroll
+          for (int j = 0; j < 2; ++j) {
+            const int o = tab[8 * b + pr0 + 4 * j];
+            x[j] = make_float4(1.f, 1.f, 1.f, 1.f);
+            if constexpr (kAux) {
+              if (o >= 0) x[j] = __ldg(reinterpret_cast<const float4*>(auxb + o));
+            }
+            if constexpr (kAux16) {
+              if (o >= 0) {
+                const uint2 u = __ldg(reinterpret_cast<const uint2*>(auxb16 + o));
+                x[j] = make_float4(__uint_as_float(u.x << 16), __uint_as_float(u.x & 0xffff0000u),
+                                   __uint_as_float(u.y << 16), __uint_as_float(u.y & 0xffff0000u));
+              }
+            }
+          }
+        };
+        if (kAux || kAux16) load(0, ax);
+        for (int b = 0; b < nb; ++b) {
+          uint32_t r[8];
+          tmem_ld8(tcol + (uint32_t)(8 * b), r);
+          tmem_wait_ld();
+          asm volatile("bar.sync %0, 128;" ::"r"(grp_bar) : "memory");   // buf free
+#pragma unroll
+          for (int e = 0; e < 8; ++e) buf[e * 128 + q * 32 + lane] = __uint_as_float(r[e]);
+          asm volatile("bar.sync %0, 128;" ::"r"(grp_bar) : "memory");
+          float4 axn[2];
+          if ((kAux || kAux16) && b + 1 < nb) load(b + 1, axn);
+#pragma unroll
+          for (int j = 0; j < 2; ++j) {
+            const int pr = pr0 + 4 * j;
+            const int off = tab[8 * b + pr];
+            if (off < 0) continue;
+            const float4 v4 = *reinterpret_cast<const float4*>(buf + pr * 128 + 4 * cg);
+            const float v[4] = {v4.x, v4.y, v4.z, v4.w};
+            const float bb[4] = {bias.x, bias.y, bias.z, bias.w};
+            const float xa[4] = {ax[j].x, ax[j].y, ax[j].z, ax[j].w};
+            float o[4];
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+              if constexpr (EPI == EPI_BIAS) o[i] = v[i] + bb[i];
+              else if constexpr (EPI == EPI_BIAS_TANH) o[i] = tanhf(v[i] + bb[i]);
+              else if constexpr (EPI == EPI_RESID) o[i] = xa[i] + a.h * (v[i] + bb[i]);
+              else if constexpr (EPI == EPI_TANH_BWD) o[i] = (a.h * v[i]) * (1.f - xa[i] * xa[i]);
+              else if constexpr (EPI == EPI_ADD) o[i] = xa[i] + v[i];
+              else if constexpr (EPI == EPI_DTANH16) o[i] = (a.h * v[i]) * xa[i];
+              else o[i] = a.h * v[i];
+            }
+            if (a.dbg & 2) continue;
+            if (outb) *reinterpret_cast<float4*>(outb + off) = make_float4(o[0], o[1], o[2], o[3]);
+            if (outb16)
+              *reinterpret_cast<uint2*>(outb16 + off) = make_uint2(pack_bf16(o[0], o[1]), pack_bf16(o[2], o[3]));
+            if (outb16d)
+              *reinterpret_cast<uint2*>(outb16d + off) =
+                  make_uint2(pack_bf16(1.f - o[0] * o[0], 1.f - o[1] * o[1]), pack_bf16(1.f - o[2] * o[2], 1.f - o[3] * o[3]));
+          }
+          if (kAux || kAux16) ax[0] = axn[0], ax[1] = axn[1];
+        }
+      }
+      tc_fence_before();
+      mbar_arrive(&acc_empty[ab]);
+      if (++ab == 2) ab = 0, aph ^= 1;
+    }
+    } else {
     // TMEM lane r = output channel cb*128 + r; a warp owns lanes 32q..32q+31 and walks the
     // positions 16 columns at a time: one 128-byte store per position (NHWC).  bf16-input
     // mode: the idle converter warps (2-5) form a second group, group g drains tile g of
@@ -376,8 +488,8 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_arrive(&acc_empty[ab]);
       if (++ab == 2) ab = 0, aph ^= 1;
     }
+    }  // BIN / channel-per-lane epilogue
   }
-
   tc_fence_before();
   __syncthreads();
   if (warp == 1) {
@@ -486,12 +598,13 @@ Plan plan_for(const ConvShape& s, bool bin = false) {
   p.w_tap = 4u * 128u * 16u;
   const size_t fixed = 512 + 1024;
   if (bin) {
+    const size_t fixed_bin = 512 + 2 * 8 * 128 * 4 + 2 * 128 * 4 + 1024;   // + exchange and position tables
     // no fp32 staging: the freed space deepens the bf16 halo ring and the weight ring (the
     // halo of a 32-channel chunk feeds 2304 MMA cycles; 2 slots left its TMA latency exposed)
     p.ok = false;
     for (int nb = kBfMax; nb >= 2 && !p.ok; --nb)
       for (int w = kWMax; w >= kWStages && !p.ok; --w) {
-        const size_t need = nb * (size_t)p.bf_stride + w * 3 * (size_t)p.w_tap + fixed;
+        const size_t need = nb * (size_t)p.bf_stride + w * 3 * (size_t)p.w_tap + fixed_bin;
         if (need <= (size_t)kMaxSmem) p.nbf = nb, p.nw = w, p.smem = need, p.ok = true;
       }
     return p;
