@@ -50,6 +50,7 @@ struct PwArgs {
   int mo, mi;                    // co / ci blocks (64 channels, single: 128)
   int single;                    // 1: one bf16 plane per operand, 128-channel blocks
   int nobias;                    // diagnostics (RP_WGRAD_NOBIAS): skip the bias sums
+  int dbg;                       // diagnostics (RP_WGRAD_DBG): 1 no MMA, 2 no x loads, 4 no g loads
   int blocks_per_img, num_blocks;
   uint32_t g_slab;               // bytes per bf16 g plane slab (Pp rows x 128 B, 1 KB aligned)
   uint32_t x_slab;               // bytes per bf16 x plane slab (rg * Wp rows of one filter row, packed)
@@ -129,7 +130,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     // ===================== TMA producer: 4 plane loads per block =====================
     int s = 0;
     uint32_t ph = 0;
-    const uint32_t bytes = 2u * a.P * 128u + 2u * xrows * 128u;
+    const uint32_t bytes = ((a.dbg & 4) ? 0u : 2u * a.P * 128u) + ((a.dbg & 2) ? 0u : 2u * xrows * 128u);
     for (int b = blk_beg; b < blk_end; ++b) {
       const int n = b / a.blocks_per_img;
       const int y0 = (b - n * a.blocks_per_img) * a.rg;
@@ -137,7 +138,16 @@ __global__ void __launch_bounds__(kThreads, 1)
       if (do_bias) mbar_wait(&bias_free[s], ph ^ 1);
       if (elect_one()) {
         mbar_arrive_expect_tx(&full[s], bytes);
-        if (a.single) {   // the two 64-channel atoms of one plane
+        if (a.dbg & 6) {   // diagnostics: a subset of the loads
+          if (!(a.dbg & 4)) {
+            tma_load_4d(&tg0, &full[s], g_slab(s, 0), 64 * cob, -1, y0, n);
+            tma_load_4d(&tg1, &full[s], g_slab(s, 1), 64 * cob, -1, y0, n);
+          }
+          if (!(a.dbg & 2)) {
+            tma_load_4d(&tx0, &full[s], x_slab(s, 0), 64 * cib, -1, y0 - 1 + gi, n);
+            tma_load_4d(&tx1, &full[s], x_slab(s, 1), 64 * cib, -1, y0 - 1 + gi, n);
+          }
+        } else if (a.single) {   // the two 64-channel atoms of one plane
           tma_load_4d(&tg0, &full[s], g_slab(s, 0), 128 * cob, -1, y0, n);
           tma_load_4d(&tg0, &full[s], g_slab(s, 1), 128 * cob + 64, -1, y0, n);
           tma_load_4d(&tx0, &full[s], x_slab(s, 0), 128 * cib, -1, y0 - 1 + gi, n);
@@ -170,7 +180,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       uint64_t da = desc_general(smem_u32(g_slab(s, 0)), a.g_slab, 1024, 2, 0);
       uint64_t db = desc_general(smem_u32(x_slab(s, 0)), a.x_slab, 1024, 2, 0);
       if (elect_one()) {
-        for (int k = 0; k < ksteps; ++k) {
+        for (int k = 0; k < ksteps && !(a.dbg & 1); ++k) {
           const uint32_t accum = (b > blk_beg || k > 0) ? 1u : 0u;
           // the 3 taps share A (the g rows of these 16 positions): read it once through the
           // A collector instead of once per MMA (shared-memory operand bandwidth)
@@ -341,9 +351,18 @@ __global__ void wgrad_planes_reduce_kernel(const float* __restrict__ part, const
       const int gid = (cob * a.mi + cib) * 3 + gi;
       const int c_lo = grp_start(gid, grid, a), c_hi = grp_start(gid + 1, grid, a);
       const int64_t off = ((int64_t)(tap - gi * kTg) * cbk + (ci - cib * cbk)) * cbk + (co - cob * cbk);
-      double s = 0.0;
-      for (int b = c_lo; b < c_hi; ++b) s += (double)part[b * pstride + off];
-      gw[idx] = (float)(scale * s);
+      // 8 loads in flight, 4 accumulators combined in a fixed order (deterministic)
+      double s4[4] = {0.0, 0.0, 0.0, 0.0};
+      int b = c_lo;
+      for (; b + 8 <= c_hi; b += 8) {
+        float v[8];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) v[i] = __ldg(part + (int64_t)(b + i) * pstride + off);
+#pragma unroll
+        for (int i = 0; i < 8; ++i) s4[i & 3] += (double)v[i];
+      }
+      for (; b < c_hi; ++b) s4[0] += (double)__ldg(part + (int64_t)b * pstride + off);
+      gw[idx] = (float)(scale * ((s4[0] + s4[1]) + (s4[2] + s4[3])));
     } else if (gb) {
       const int co = idx - total, cob = co / cbk;
       const int gid = cob * a.mi * 3;
@@ -493,6 +512,11 @@ void launch_wgrad_planes(const ConvShape& s, const void* x0, const void* x1, con
   a.single = single ? 1 : 0;
   static const int nobias = std::getenv("RP_WGRAD_NOBIAS") ? 1 : 0;
   a.nobias = nobias;
+  static const int wdbg = [] {
+    const char* e = std::getenv("RP_WGRAD_DBG");
+    return e ? std::atoi(e) : 0;
+  }();
+  a.dbg = wdbg;
   a.N = s.n;
   a.H = s.h;
   a.W = s.w;
