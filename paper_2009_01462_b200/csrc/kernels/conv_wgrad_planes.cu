@@ -112,9 +112,25 @@ __global__ void __launch_bounds__(kThreads, 1)
   }
   if (warp == 1) tmem_alloc<512>(tmem_slot);
   {
-    uint4* z = reinterpret_cast<uint4*>(smem);
-    const int n16 = (int)((size_t)S * a.stage / 16);
-    for (int i = threadIdx.x; i < n16; i += blockDim.x) z[i] = make_uint4(0u, 0u, 0u, 0u);
+    // zero only what the MMAs read but TMA never writes: the g slabs' K-padding rows [P, Pp),
+    // the lead row before the x slabs (tap shift -1) and the trail after them
+    const int pad16 = (a.Pp - a.P) * 8;              // 16-byte words per g slab
+    const int lead16 = kLead / 16, trail16 = kTrail / 16;
+    const int per_stage = 2 * pad16 + lead16 + trail16;
+    for (int i = threadIdx.x; i < S * per_stage; i += blockDim.x) {
+      const int st = i / per_stage, r = i - st * per_stage;
+      uint8_t* base = smem + (size_t)st * a.stage;
+      uint8_t* dst;
+      if (r < 2 * pad16) {
+        const int j = r / pad16;
+        dst = base + (size_t)j * a.g_slab + (size_t)a.P * 128 + (size_t)(r - j * pad16) * 16;
+      } else if (r < 2 * pad16 + lead16) {
+        dst = base + a.x_off - kLead + (size_t)(r - 2 * pad16) * 16;
+      } else {
+        dst = base + a.x_off + 2 * (size_t)a.x_slab + (size_t)(r - 2 * pad16 - lead16) * 16;
+      }
+      *reinterpret_cast<uint4*>(dst) = make_uint4(0u, 0u, 0u, 0u);
+    }
   }
   fence_proxy_async_smem();
   tc_fence_before();
