@@ -261,11 +261,28 @@ void block_bwd_planes(const rp_geometry& g, int nrows, const void* x_p, const fl
   (void)dpre;
   conv(shape(g, nrows, C, Ch), gio, pb + L.w2, true, nullptr, a, h, tanh_act ? k::EPI_TANH_BWD : k::EPI_SCALE, nullptr,
        RP_MATH_FP32, wws, RP_PROF_CONV_DGRAD, tanh_act, st, dpre_p, g_p, f);
-  // gW1 = x^T dpre, gb1 = sum dpre first, while dgrad2's dpre planes are still in L2
-  //                                                               (network.cpp:102-103)
-  wgrad_planes(shape(g, nrows, C, Ch), x_p, dpre_p, 1.f, gb + L.w1, gb + L.b1, wgws, st);
-  // gW2 = h a^T g, gb2 = h sum g (before dgrad1 overwrites the g planes) (network.cpp:98-99)
-  wgrad_planes(shape(g, nrows, Ch, C), a_p, g_p, h, gb + L.w2, gb + L.b2, wgws, st);
+  if (C == Ch && !std::getenv("RP_WGRAD_UNPAIRED")) {
+    // gW1 = x^T dpre, gb1 = sum dpre and gW2 = h a^T g, gb2 = h sum g in ONE launch (same
+    // shape): half the launches' prologues, epilogues and reduces   (network.cpp:98-103)
+    const k::ConvShape sw = shape(g, nrows, C, Ch);
+    prof::Scope ps(RP_PROF_CONV_WGRAD, st, 2 * conv_flops(sw), 2 * 4.0 * (double)sw.pixels() * (sw.ci + sw.co));
+    const auto* x0 = static_cast<const uint16_t*>(x_p);
+    const auto* d0 = static_cast<const uint16_t*>(dpre_p);
+    const auto* a0 = static_cast<const uint16_t*>(a_p);
+    const auto* g0 = static_cast<const uint16_t*>(g_p);
+    const int64_t ne = sw.pixels() * C;
+    const void* xa[2] = {x0, x0 + ne};
+    const void* ga[2] = {d0, d0 + ne};
+    const void* xb[2] = {a0, a0 + ne};
+    const void* gb2[2] = {g0, g0 + ne};
+    k::conv3x3_wgrad_planes_pair(sw, xa, ga, 1.f, gb + L.w1, gb + L.b1, xb, gb2, h, gb + L.w2, gb + L.b2, wgws, st);
+  } else {
+    // gW1 = x^T dpre, gb1 = sum dpre first, while dgrad2's dpre planes are still in L2
+    //                                                               (network.cpp:102-103)
+    wgrad_planes(shape(g, nrows, C, Ch), x_p, dpre_p, 1.f, gb + L.w1, gb + L.b1, wgws, st);
+    // gW2 = h a^T g, gb2 = h sum g (before dgrad1 overwrites the g planes) (network.cpp:98-99)
+    wgrad_planes(shape(g, nrows, Ch, C), a_p, g_p, h, gb + L.w2, gb + L.b2, wgws, st);
+  }
   // g <- g + dpre * W1^T in place, and the planes of the new g   (network.cpp:104)
   conv(shape(g, nrows, Ch, C), dpre, pb + L.w1, true, nullptr, gio, 1.f, k::EPI_ADD, gio, RP_MATH_FP32, wws,
        RP_PROF_CONV_DGRAD, true, st, g_p, dpre_p, f ? f + fb : nullptr);

@@ -58,15 +58,21 @@ struct PwArgs {
   uint32_t stage;
   float* part;                   // [grid][kTg * cblk (ci)][cblk (co)]
   double* part_bias;             // [grid][cblk]
+  int njobs;                     // 1, or 2: two weight gradients of the same shape in one launch
+  float* gw[2];                  // reduce: per-job outputs and scales
+  float* gb[2];
+  double scale[2];
 };
 
 __device__ __forceinline__ int grp_start(int gid, int grid, const PwArgs& a) {
-  return (int)((int64_t)grid * gid / (3 * a.mo * a.mi));
+  return (int)((int64_t)grid * gid / (a.njobs * 3 * a.mo * a.mi));
 }
 
 __global__ void __launch_bounds__(kThreads, 1)
-    wgrad_planes_kernel(const __grid_constant__ CUtensorMap tg0, const __grid_constant__ CUtensorMap tg1,
-                        const __grid_constant__ CUtensorMap tx0, const __grid_constant__ CUtensorMap tx1,
+    wgrad_planes_kernel(const __grid_constant__ CUtensorMap tg0a, const __grid_constant__ CUtensorMap tg1a,
+                        const __grid_constant__ CUtensorMap tx0a, const __grid_constant__ CUtensorMap tx1a,
+                        const __grid_constant__ CUtensorMap tg0b, const __grid_constant__ CUtensorMap tg1b,
+                        const __grid_constant__ CUtensorMap tx0b, const __grid_constant__ CUtensorMap tx1b,
                         const PwArgs a) {
   extern __shared__ __align__(1024) uint8_t smem[];
   const int warp = __shfl_sync(0xffffffffu, (int)threadIdx.x / 32, 0);
@@ -84,11 +90,15 @@ __global__ void __launch_bounds__(kThreads, 1)
   auto g_slab = [&](int s, int j) { return smem + s * a.stage + j * a.g_slab; };
   auto x_slab = [&](int s, int j) { return smem + s * a.stage + a.x_off + j * a.x_slab; };
 
-  const int NG = 3 * a.mo * a.mi;
+  const int NG1 = 3 * a.mo * a.mi;                // work groups per job
+  const int NG = a.njobs * NG1;
   int gid = 0;
   while (gid + 1 < NG && grp_start(gid + 1, gridDim.x, a) <= (int)blockIdx.x) ++gid;
   const int c_lo = grp_start(gid, gridDim.x, a), c_hi = grp_start(gid + 1, gridDim.x, a);
-  const int gi = gid % 3, cib = (gid / 3) % a.mi, cob = gid / (3 * a.mi);
+  const int job = gid / NG1;
+  const int gj = gid - job * NG1;
+  const int gi = gj % 3, cib = (gj / 3) % a.mi, cob = gj / (3 * a.mi);
+
   const int jg = blockIdx.x - c_lo, ng = c_hi - c_lo;
   const int blk_beg = (int)((int64_t)jg * a.num_blocks / ng);
   const int blk_end = (int)((int64_t)(jg + 1) * a.num_blocks / ng);
@@ -105,10 +115,17 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     mbar_init(acc_full, 1);
     fence_barrier_init();
-    prefetch_tmap(&tg0);
-    prefetch_tmap(&tg1);
-    prefetch_tmap(&tx0);
-    prefetch_tmap(&tx1);
+    if (job == 0) {
+      prefetch_tmap(&tg0a);
+      prefetch_tmap(&tg1a);
+      prefetch_tmap(&tx0a);
+      prefetch_tmap(&tx1a);
+    } else {
+      prefetch_tmap(&tg0b);
+      prefetch_tmap(&tg1b);
+      prefetch_tmap(&tx0b);
+      prefetch_tmap(&tx1b);
+    }
   }
   if (warp == 1) tmem_alloc<512>(tmem_slot);
   {
@@ -147,6 +164,29 @@ __global__ void __launch_bounds__(kThreads, 1)
     int s = 0;
     uint32_t ph = 0;
     const uint32_t bytes = ((a.dbg & 4) ? 0u : 2u * a.P * 128u) + ((a.dbg & 2) ? 0u : 2u * xrows * 128u);
+    auto issue_loads = [&](const CUtensorMap* mg0, const CUtensorMap* mg1, const CUtensorMap* mx0,
+                           const CUtensorMap* mx1, int s, int y0, int n) {
+        if (a.dbg & 6) {   // diagnostics: a subset of the loads
+          if (!(a.dbg & 4)) {
+            tma_load_4d(mg0, &full[s], g_slab(s, 0), 64 * cob, -1, y0, n);
+            tma_load_4d(mg1, &full[s], g_slab(s, 1), 64 * cob, -1, y0, n);
+          }
+          if (!(a.dbg & 2)) {
+            tma_load_4d(mx0, &full[s], x_slab(s, 0), 64 * cib, -1, y0 - 1 + gi, n);
+            tma_load_4d(mx1, &full[s], x_slab(s, 1), 64 * cib, -1, y0 - 1 + gi, n);
+          }
+        } else if (a.single) {   // the two 64-channel atoms of one plane
+          tma_load_4d(mg0, &full[s], g_slab(s, 0), 128 * cob, -1, y0, n);
+          tma_load_4d(mg0, &full[s], g_slab(s, 1), 128 * cob + 64, -1, y0, n);
+          tma_load_4d(mx0, &full[s], x_slab(s, 0), 128 * cib, -1, y0 - 1 + gi, n);
+          tma_load_4d(mx0, &full[s], x_slab(s, 1), 128 * cib + 64, -1, y0 - 1 + gi, n);
+        } else {
+          tma_load_4d(mg0, &full[s], g_slab(s, 0), 64 * cob, -1, y0, n);
+          tma_load_4d(mg1, &full[s], g_slab(s, 1), 64 * cob, -1, y0, n);
+          tma_load_4d(mx0, &full[s], x_slab(s, 0), 64 * cib, -1, y0 - 1 + gi, n);
+          tma_load_4d(mx1, &full[s], x_slab(s, 1), 64 * cib, -1, y0 - 1 + gi, n);
+        }
+    };
     for (int b = blk_beg; b < blk_end; ++b) {
       const int n = b / a.blocks_per_img;
       const int y0 = (b - n * a.blocks_per_img) * a.rg;
@@ -154,26 +194,12 @@ __global__ void __launch_bounds__(kThreads, 1)
       if (do_bias) mbar_wait(&bias_free[s], ph ^ 1);
       if (elect_one()) {
         mbar_arrive_expect_tx(&full[s], bytes);
-        if (a.dbg & 6) {   // diagnostics: a subset of the loads
-          if (!(a.dbg & 4)) {
-            tma_load_4d(&tg0, &full[s], g_slab(s, 0), 64 * cob, -1, y0, n);
-            tma_load_4d(&tg1, &full[s], g_slab(s, 1), 64 * cob, -1, y0, n);
-          }
-          if (!(a.dbg & 2)) {
-            tma_load_4d(&tx0, &full[s], x_slab(s, 0), 64 * cib, -1, y0 - 1 + gi, n);
-            tma_load_4d(&tx1, &full[s], x_slab(s, 1), 64 * cib, -1, y0 - 1 + gi, n);
-          }
-        } else if (a.single) {   // the two 64-channel atoms of one plane
-          tma_load_4d(&tg0, &full[s], g_slab(s, 0), 128 * cob, -1, y0, n);
-          tma_load_4d(&tg0, &full[s], g_slab(s, 1), 128 * cob + 64, -1, y0, n);
-          tma_load_4d(&tx0, &full[s], x_slab(s, 0), 128 * cib, -1, y0 - 1 + gi, n);
-          tma_load_4d(&tx0, &full[s], x_slab(s, 1), 128 * cib + 64, -1, y0 - 1 + gi, n);
-        } else {
-          tma_load_4d(&tg0, &full[s], g_slab(s, 0), 64 * cob, -1, y0, n);
-          tma_load_4d(&tg1, &full[s], g_slab(s, 1), 64 * cob, -1, y0, n);
-          tma_load_4d(&tx0, &full[s], x_slab(s, 0), 64 * cib, -1, y0 - 1 + gi, n);
-          tma_load_4d(&tx1, &full[s], x_slab(s, 1), 64 * cib, -1, y0 - 1 + gi, n);
-        }
+        // the job's tensor maps are passed as direct grid-constant addresses in each branch
+        // (no select between the two sets)
+        if (job == 0)
+          issue_loads(&tg0a, &tg1a, &tx0a, &tx1a, s, y0, n);
+        else
+          issue_loads(&tg0b, &tg1b, &tx0b, &tx1b, s, y0, n);
       }
       __syncwarp();
       if (++s == S) s = 0, ph ^= 1;
@@ -350,21 +376,28 @@ __global__ void __launch_bounds__(kThreads, 1)
 }
 
 __global__ void wgrad_planes_reduce_kernel(const float* __restrict__ part, const double* __restrict__ part_bias,
-                                           const PwArgs a, int grid, double scale, float* __restrict__ gw,
-                                           float* __restrict__ gb) {
+                                           const PwArgs a, int grid) {
   pdl_launch_dependents();   // the next grid's prologue may overlap; it waits before touching memory
   pdl_wait();                // the partials of the weight-gradient grid
   const int Ci = a.Ci, Co = a.Co;
   const int total = 9 * Ci * Co;
   const int cbk = a.single ? 128 : 64;
   const int64_t pstride = (int64_t)kTg * cbk * cbk;
-  for (int idx = blockIdx.x * blockDim.x + threadIdx.x; idx < total + Co; idx += gridDim.x * blockDim.x) {
+  const int per_job = total + Co;
+  for (int gidx = blockIdx.x * blockDim.x + threadIdx.x; gidx < a.njobs * per_job;
+       gidx += gridDim.x * blockDim.x) {
+    const int job = gidx / per_job;
+    const int idx = gidx - job * per_job;
+    const int gbase = job * 3 * a.mo * a.mi;
+    float* gw = a.gw[job];
+    float* gb = a.gb[job];
+    const double scale = a.scale[job];
     if (idx < total) {
       const int co = idx % Co;
       const int ci = (idx / Co) % Ci;
       const int tap = idx / (Co * Ci);
       const int gi = tap / kTg, cob = co / cbk, cib = ci / cbk;
-      const int gid = (cob * a.mi + cib) * 3 + gi;
+      const int gid = gbase + (cob * a.mi + cib) * 3 + gi;
       const int c_lo = grp_start(gid, grid, a), c_hi = grp_start(gid + 1, grid, a);
       const int64_t off = ((int64_t)(tap - gi * kTg) * cbk + (ci - cib * cbk)) * cbk + (co - cob * cbk);
       // 8 loads in flight, 4 accumulators combined in a fixed order (deterministic)
@@ -381,7 +414,7 @@ __global__ void wgrad_planes_reduce_kernel(const float* __restrict__ part, const
       gw[idx] = (float)(scale * ((s4[0] + s4[1]) + (s4[2] + s4[3])));
     } else if (gb) {
       const int co = idx - total, cob = co / cbk;
-      const int gid = cob * a.mi * 3;
+      const int gid = gbase + cob * a.mi * 3;
       const int c_lo = grp_start(gid, grid, a), c_hi = grp_start(gid + 1, grid, a);
       double s = 0.0;
       for (int b = c_lo; b < c_hi; ++b) s += part_bias[(int64_t)b * cbk + (co - cob * cbk)];
@@ -519,8 +552,14 @@ void split_planes(const float* in, int64_t n, void* p0, void* p1, cudaStream_t s
 }
 
 namespace {
-void launch_wgrad_planes(const ConvShape& s, const void* x0, const void* x1, const void* g0, const void* g1,
-                         float scale, float* gw, float* gb, void* ws, cudaStream_t st, bool single) {
+struct WgJob {
+  const void *x0, *x1, *g0, *g1;
+  float scale;
+  float* gw;
+  float* gb;
+};
+
+void launch_wgrad_planes(const ConvShape& s, const WgJob* jobs, int njobs, void* ws, cudaStream_t st, bool single) {
   const PwPlan p = plan(s, single);
   if (!p.ok) fail(RP_ERR_INTERNAL, "conv3x3_wgrad_planes: unsupported shape");
   const int cbk = single ? 128 : 64;
@@ -553,27 +592,45 @@ void launch_wgrad_planes(const ConvShape& s, const void* x0, const void* x1, con
   a.stage = p.stage;
   a.part = static_cast<float*>(ws);
   a.part_bias = reinterpret_cast<double*>(static_cast<char*>(ws) + part_bytes(p, single));
-  const CUtensorMap& mg0 = cached(g0, s.n, s.h, s.w, s.co, p.rg);
-  const CUtensorMap& mg1 = cached(single ? g0 : g1, s.n, s.h, s.w, s.co, p.rg);
-  const CUtensorMap& mx0 = cached(x0, s.n, s.h, s.w, s.ci, p.rg);
-  const CUtensorMap& mx1 = cached(single ? x0 : x1, s.n, s.h, s.w, s.ci, p.rg);
+  a.njobs = njobs;
+  if (3 * njobs * a.mo * a.mi > p.grid) fail(RP_ERR_INTERNAL, "conv3x3_wgrad_planes: too many work groups");
+  const CUtensorMap* m[2][4];
+  for (int j = 0; j < njobs; ++j) {
+    const WgJob& jb = jobs[j];
+    m[j][0] = &cached(jb.g0, s.n, s.h, s.w, s.co, p.rg);
+    m[j][1] = &cached(single ? jb.g0 : jb.g1, s.n, s.h, s.w, s.co, p.rg);
+    m[j][2] = &cached(jb.x0, s.n, s.h, s.w, s.ci, p.rg);
+    m[j][3] = &cached(single ? jb.x0 : jb.x1, s.n, s.h, s.w, s.ci, p.rg);
+    a.gw[j] = jb.gw;
+    a.gb[j] = jb.gb;
+    a.scale[j] = (double)jb.scale;
+  }
+  if (njobs == 1)
+    for (int i = 0; i < 4; ++i) m[1][i] = m[0][i];
   static bool configured = false;
   if (!configured) {
     RP_CUDA(cudaFuncSetAttribute(wgrad_planes_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxSmem));
     configured = true;
   }
-  launch_pdl(wgrad_planes_kernel, p.grid, kThreads, p.smem, st, mg0, mg1, mx0, mx1, a);
-  RP_LAUNCHED();
-  const int total = 9 * s.ci * s.co + s.co;
+  launch_pdl(wgrad_planes_kernel, p.grid, kThreads, p.smem, st, *m[0][0], *m[0][1], *m[0][2], *m[0][3], *m[1][0],
+             *m[1][1], *m[1][2], *m[1][3], a);
+  const int total = njobs * (9 * s.ci * s.co + s.co);
   launch_pdl(wgrad_planes_reduce_kernel, ceil_div(total, 256), 256, 0, st, (const float*)a.part,
-             (const double*)a.part_bias, a, p.grid, (double)scale, gw, gb);
-  RP_LAUNCHED();
+             (const double*)a.part_bias, a, p.grid);
 }
 }  // namespace
 
 void conv3x3_wgrad_planes(const ConvShape& s, const void* x0, const void* x1, const void* g0, const void* g1,
                           float scale, float* gw, float* gb, void* ws, cudaStream_t st) {
-  launch_wgrad_planes(s, x0, x1, g0, g1, scale, gw, gb, ws, st, false);
+  const WgJob j{x0, x1, g0, g1, scale, gw, gb};
+  launch_wgrad_planes(s, &j, 1, ws, st, false);
+}
+
+void conv3x3_wgrad_planes_pair(const ConvShape& s, const void* const xa[2], const void* const ga[2], float scale_a,
+                               float* gwa, float* gba, const void* const xb[2], const void* const gb2[2],
+                               float scale_b, float* gwb, float* gbb, void* ws, cudaStream_t st) {
+  const WgJob j[2] = {{xa[0], xa[1], ga[0], ga[1], scale_a, gwa, gba}, {xb[0], xb[1], gb2[0], gb2[1], scale_b, gwb, gbb}};
+  launch_wgrad_planes(s, j, 2, ws, st, false);
 }
 
 bool conv3x3_wgrad_bf16p_supported(const ConvShape& s) { return plan(s, true).ok; }
@@ -586,7 +643,8 @@ int64_t conv3x3_wgrad_bf16p_ws_bytes(const ConvShape& s) {
 
 void conv3x3_wgrad_bf16p(const ConvShape& s, const void* x, const void* g, float scale, float* gw, float* gb,
                          void* ws, cudaStream_t st) {
-  launch_wgrad_planes(s, x, nullptr, g, nullptr, scale, gw, gb, ws, st, true);
+  const WgJob j{x, nullptr, g, nullptr, scale, gw, gb};
+  launch_wgrad_planes(s, &j, 1, ws, st, true);
 }
 
 }  // namespace rp::k

@@ -104,6 +104,11 @@ bool conv3x3_wgrad_planes_supported(const ConvShape& s);
 int64_t conv3x3_wgrad_planes_ws_bytes(const ConvShape& s);
 void conv3x3_wgrad_planes(const ConvShape& s, const void* x0, const void* x1, const void* g0, const void* g1,
                           float scale, float* gw, float* gb, void* ws, cudaStream_t st);
+// Two weight gradients of the same shape in one launch (the block's gW1 and gW2 when C ==
+// hidden): xa / ga = {plane 0, plane 1} of job a's operands, likewise job b.
+void conv3x3_wgrad_planes_pair(const ConvShape& s, const void* const xa[2], const void* const ga[2], float scale_a,
+                               float* gwa, float* gba, const void* const xb[2], const void* const gb2[2],
+                               float scale_b, float* gwb, float* gbb, void* ws, cudaStream_t st);
 // The same kernel on single bf16 planes (RP_MATH_BF16): x, g one bf16 NHWC tensor each,
 // 128-channel blocks (Ci, Co % 128 == 0); bf16 x bf16 products, fp32 accumulate.
 bool conv3x3_wgrad_bf16p_supported(const ConvShape& s);
