@@ -83,6 +83,7 @@ struct TcArgs {
   int raw_slots;        // X3BF16: depth of the raw ring (2 or 3); PLANES: halo slots (2..4)
   int wstages;          // depth of the weight ring (<= kWMax); resident: stages of the whole filter
   int resident;         // PLANES, Co = 64: the co block's whole prepped filter stays in shared memory
+  int tile;             // frame positions per tile (<= 128; PLANES: the image's frame split into equal units)
   float h;
   const float* w;       // prepped [chunk][tap][kg][128 rows][4]
   const float* bias;
@@ -304,7 +305,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     UnitIter it(a.Co / 64, a.N, a.T);
     int cb, n, tile0, ntiles;
     while (it.next(cb, n, tile0, ntiles)) {
-      const int f0 = tile0 * 128;
+      const int f0 = tile0 * a.tile;
       const int y0 = f0 / Wp;
       for (int c = 0; c < a.nchunks; ++c) {
         mbar_wait(BF ? &raw_empty[hs] : &halo_empty[hs], hph ^ 1);
@@ -383,9 +384,9 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     while (it.next(cb, n, tile0, ntiles)) {                   // warp-uniform
       const int u = ui++;
-      const int f0 = tile0 * 128;
+      const int f0 = tile0 * a.tile;
       const int c0 = f0 - (f0 / Wp) * Wp;
-      const int nvalid = min(ntiles * 128, a.H * Wp - f0);              // frame positions of the unit
+      const int nvalid = min(ntiles * a.tile, a.H * Wp - f0);           // frame positions of the unit
       const uint32_t id_unit = idesc(1, 128, (nvalid + 15) / 16 * 16);  // PLANES: N = 16 .. 256
       mbar_wait(&acc_empty[ab], aph ^ 1);
       tc_fence_after();
@@ -605,20 +606,20 @@ __global__ void __launch_bounds__(kThreads, 1)
       if (a.trace && blockIdx.x < 2 && threadIdx.x == 192) a.trace[(blockIdx.x * 64 + min(u, 63)) * 8 + 2] = globaltimer_ns();
       if (grp < ntiles && !(a.dbg & 1)) {
         {
-          const int f = (tile0 + grp) * 128 + gtid;
+          const int f = (tile0 + grp) * a.tile + gtid;
           const int y = f / Wp, X = f - y * Wp;
           asm volatile("bar.sync %0, 128;" ::"r"(grp_bar) : "memory");   // the last tile's readers are done
-          tab[gtid] = (y < a.H && X >= 1 && X <= a.W) ? (y * a.W + (X - 1)) * a.Co : -1;
+          tab[gtid] = (gtid < a.tile && y < a.H && X >= 1 && X <= a.W) ? (y * a.W + (X - 1)) * a.Co : -1;
           asm volatile("bar.sync %0, 128;" ::"r"(grp_bar) : "memory");   // table visible
         }
-        const uint32_t tcol = tmem_base + ((uint32_t)(q * 32) << 16) + (uint32_t)((ab * kS + grp) * 128);
+        const uint32_t tcol = tmem_base + ((uint32_t)(q * 32) << 16) + (uint32_t)(ab * kS * 128 + grp * a.tile);
         const float* auxb = kAux ? a.aux + img * a.Co + co : nullptr;
         float* outb = a.out ? a.out + img * a.Co + co : nullptr;   // null: the planes alone
         const bool planes = a.p0 != nullptr;
         __nv_bfloat16* p0b = planes ? a.p0 + img * a.Co + co : nullptr;
         __nv_bfloat16* p1b = planes ? a.p1 + img * a.Co + co : nullptr;
-        const int fvalid = a.H * Wp - (tile0 + grp) * 128;   // frame positions left in this tile
-        const int nb = min(128 / kEpiB, (fvalid + kEpiB - 1) / kEpiB);   // batches with frame positions
+        const int fvalid = min(a.tile, a.H * Wp - (tile0 + grp) * a.tile);   // frame positions of this tile
+        const int nb = (fvalid + kEpiB - 1) / kEpiB;                          // batches with frame positions
         float4 ax[128 / kEpiB];
         if constexpr (kAux) {
 #pragma unroll
@@ -839,6 +840,7 @@ struct Plan {
   uint32_t halo_bytes, w_tap, halo_stride, plane_bytes, raw_stride = 0;
   int raw_slots = 0, wstages = kWStages;
   bool resident = false;
+  int tile = 128;
   size_t smem;
 };
 
@@ -848,10 +850,22 @@ Plan plan_for(const ConvShape& s, int mode = MODE_X3TF32) {
   // W + 1 frame columns: one zero column (x = -1) per row also serves as the previous row's
   // right pad (x = W), so 1/W of the MMA work is padding instead of 2/W
   p.Wp = s.w + 1;
-  p.rows_h = (3 * p.Wp + 128 * kS + p.Wp - 1) / p.Wp;
+  static const bool equal_units = [] {
+    const char* e = std::getenv("RP_CONV_EQUAL_UNITS");
+    return !(e && e[0] == '0');
+  }();
+  if (mode == MODE_PLANES && equal_units) {
+    // equal units: the image's frame in ceil(frame / 256) units of two tiles, the tile rounded
+    // up to 16 positions (32x32: 1056 = 5 units of 224 positions instead of 4 x 256 + a 32-position
+    // tail unit that paid a whole unit's halo loads and MMA issue)
+    const int frame = s.h * p.Wp;
+    const int units = (frame + 2 * 128 - 1) / (2 * 128);
+    p.tile = std::min(128, ((frame + 2 * units - 1) / (2 * units) + 15) / 16 * 16);
+  }
+  p.rows_h = (3 * p.Wp + p.tile * kS + p.Wp - 1) / p.Wp;
   if (p.rows_h > 256) return p;
   p.halo_pos = p.rows_h * p.Wp;
-  p.T = (s.h * p.Wp + 127) / 128;
+  p.T = (s.h * p.Wp + p.tile - 1) / p.tile;
   p.units_per_img = (p.T + kS - 1) / kS;
   p.halo_bytes = (uint32_t)p.halo_pos * 64u;
   p.plane_bytes = (uint32_t)p.halo_pos * 32u;
@@ -1011,6 +1025,7 @@ void conv3x3_fwd_tc(const ConvShape& s, const float* in, const float* w_hwio, bo
   a.raw_slots = p.raw_slots;
   a.wstages = p.wstages;
   a.resident = p.resident ? 1 : 0;
+  a.tile = p.tile;
   a.h = h;
   a.w = wp;
   a.bias = bias;
