@@ -281,8 +281,15 @@ def run_ours_distributed(args, cfg, rank, world):
         raise SystemExit("bench: the serial config runs on one GPU (K = 1)")
     mode = {"alm": rp.ALM, "penalty": rp.PENALTY}[cfg["mode"]]
     plc = placement(K, world, rank)
-    eng = CudaStageEngine(g, K, mode, rp.SQUARED_L2, B, plc.lo, plc.hi, dev, seed_state=_splitmix(1),
-                          math=args.math or cfg["math"])
+    # several stages per rank (N < K): concurrent stage streams as at N = 1; the roofline pass
+    # then times overlapping kernels (noted in the line), one stage per rank is unaffected
+    concurrent = bool(cfg.get("concurrent")) and not args.serial_stages and plc.hi - plc.lo > 1
+    os.environ["RP_CONCURRENT_STAGES"] = "1" if concurrent else "0"
+    try:
+        eng = CudaStageEngine(g, K, mode, rp.SQUARED_L2, B, plc.lo, plc.hi, dev, seed_state=_splitmix(1),
+                              math=args.math or cfg["math"])
+    finally:
+        os.environ.pop("RP_CONCURRENT_STAGES", None)
     tr = DistributedDecoupledTrainer(eng, plc)
     x = torch.empty(B * g.raw_size, dtype=torch.float32, device="cuda")
     st = C.c_uint64(1000 + plc.replica)
@@ -341,7 +348,8 @@ def run_ours_distributed(args, cfg, rank, world):
     e2e_s = torch.tensor([(time.perf_counter() - t0) / e2e_steps], device="cuda")
     dist.all_reduce(e2e_s, op=dist.ReduceOp.MAX)
     return dict(tr=tr, total_ms=total_ms, prof=prof, clocks=clk, launches=launches, loss=loss,
-                e2e_s=float(e2e_s.item()), B=B, K=K, g=g, replicas=plc.replicas, plc=plc, prof_steps=prof_steps)
+                e2e_s=float(e2e_s.item()), B=B, K=K, g=g, replicas=plc.replicas, plc=plc, prof_steps=prof_steps,
+                concurrent=concurrent, prof_concurrent=concurrent)
 
 
 def _splitmix(seed):
@@ -488,6 +496,9 @@ def main():
                              "note": "bf16 sustained peak / bf16 tensor products per fp32-equivalent MAC "
                                      "(fp32 plane path: 4; bf16: 1)"},
             "peak_source": f"{peaks_kind} bf16 dense sustained (MEASURED_PEAKS.json)",
+            "kernel_timing": ("per-launch CUDA events with this rank's stages on concurrent streams (overlapping "
+                              "kernels: upper bounds)") if r.get("prof_concurrent") else
+                             "per-launch CUDA events, stages serialised (untimed pass)",
             "avg_launch_ms": avg_ms, "launches": d["launches"],
             "share_of_step": d["ms"] / ps / step_prof_ms if step_prof_ms else None,
             "kernel_classes": {k: {"launches": v["launches"], "ms_per_step": v["ms"] / ps,
