@@ -6,13 +6,17 @@
 // Same structure as conv_tc.cu (interior-frame halo, taps as shifted UMMA descriptors,
 // weights as the shared A operand, persistent warp-specialised CTAs), re-tiled for
 // kind::f16: M = 128 output channels per block (no hi / lo stacking), K = 16 channels
-// per MMA, 32-channel halo chunks.  Activations stay fp32 in HBM: TMA brings the fp32
-// halo, converter warps round it to bf16 (RNE) into the K-major interleaved layout the
-// MMA reads, the epilogue reads fp32 accumulators from TMEM and applies the same fused
-// bias / tanh / skip / (1 - a^2) / step-size as the fp32 kernel.
-//
-// Shared memory: 2 fp32 halo slots (TMA), 2 bf16 halo slots (MMA operand), 3 weight
-// stages (one filter row of one chunk).  TMEM: 2 units x 2 tiles x 128 columns.
+// per MMA, 32-channel halo chunks, one N <= 256 MMA per (unit, tap, k-step).
+//  * fp32-input mode: TMA brings the fp32 halo, converter warps round it to bf16 (RNE) into
+//    the K-major interleaved layout the MMA reads; 2 fp32 + 2 bf16 halo slots, 3 weight
+//    stages; one epilogue group, a channel per lane.
+//  * bf16-input (tape) mode, BIN: the input is a bf16 tensor loaded by TMA straight into the
+//    MMA layout (the values the converters would produce); 4 bf16 halo slots, 5 weight
+//    stages; the converter warps form a second epilogue group and the epilogue is transposed
+//    through shared memory (a thread owns 4 channels of a position: 16-byte fp32 / 8-byte
+//    bf16 accesses).  Optional bf16 outputs: out16 = bf16(out), out16d = bf16(1 - out^2).
+// The epilogue applies the fused bias / tanh / skip / (1 - a^2) / step size of the fp32
+// kernel on fp32 accumulators.  TMEM: 2 units x 2 tiles x 128 columns.
 #include <cuda.h>
 #include <cuda_bf16.h>
 

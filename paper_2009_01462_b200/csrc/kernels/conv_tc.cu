@@ -5,32 +5,33 @@
 // (block_forward's matmul(x, W1) / matmul(a, W2) and block_vjp's matmul(upstream,
 // W2^T) / matmul(dpre, W1^T), network.cpp:85-104, generalised to 3x3 taps.)
 //
-// Design (DESIGN.md §conv_tc):
+// Design (DESIGN.md §4.1):
 //  * Output positions live in the zero-padded "interior frame" of one image (H rows x
 //    (W+1) columns, flattened; the one zero column x = -1 of a row is also the previous
-//    row's x = W): tap (dy,dx) is then a constant shift of dy*(W+1)+dx
-//    positions, so one halo slab per 16-channel chunk, loaded once by TMA (out-of-bounds
-//    rows/columns zero-filled), serves all 9 taps as 9 shifted UMMA descriptors.  The 2
-//    padding columns per row are computed and discarded.
-//  * D^T = W^T x: the MMA's A operand is the (tiny) weight tile, M = 128 rows = the output
-//    channels stacked twice, [W_hi ; W_lo]; B is the shifted halo view, N = 128 positions.
-//    Consecutive MMAs share A (both operand splits of x, both tiles of a unit), which is
-//    what lets tcgen05 run at its full rate (tools/umma_bench.py: a new A every MMA
-//    costs ~40% through shared-memory operand bandwidth).
-//  * fp32 accuracy (RP_MATH_FP32, "3xTF32+"): v = hi + lo, hi = the tf32 truncation the
-//    tensor core applies to the raw fp32 halo, lo = v - hi (exact, written by converters).  MMA(A = [W_hi; W_lo], B = x_hi) and MMA(A, B = x_lo) accumulate all four
-//    products; the epilogue adds the hi-row and lo-row halves.  RP_MATH_TF32 drops the
-//    x_lo MMA (x enters truncated).
-//  * operands are K-major "interleaved" (no swizzle): for each group of 4 channels every
-//    position is 16 contiguous bytes, so a shift by one position is +16 B of descriptor
-//    start address.  The TMA box is (4 ch, W+2, rows, 4 kgroups, 1) over a 5-D view of
-//    NHWC whose 4th dim is the channel group (stride 16 B).
-//  * a unit = up to S = 2 consecutive 128-position tiles (accumulators 128 x 128 fp32 in
-//    TMEM, double-buffered across units); tiles past the image end are skipped.
-//  * warp roles (320 threads, persistent, 1 CTA/SM): w0 TMA producer, w1 MMA issuer
-//    (whole warp walks the loop so descriptors stay warp-uniform; one elected lane
-//    issues), w2-5 converters (halo lo part), w6-9 epilogue (TMEM -> registers ->
-//    hi+lo sum -> fused bias / tanh / skip / step-size -> coalesced NHWC stores).
+//    row's x = W): tap (dy,dx) is then a constant shift of dy*(W+1)+dx positions, so one
+//    halo slab per 16-channel chunk, loaded once by TMA (out-of-bounds rows/columns
+//    zero-filled), serves all 9 taps as 9 shifted UMMA descriptors.  The padding column is
+//    computed and discarded.
+//  * D^T = W^T x: the MMA's A operand is the (tiny) weight tile, M = 128 rows = the 64 output
+//    channels stacked twice ([W_hi; W_lo] / [W0; W1]); B is the shifted halo view, N = the
+//    unit's positions (<= 256).  Consecutive MMAs share A through the collector.
+//  * Operand modes.  PLANES (the fp32 default): the input arrives as a bf16 plane pair
+//    x = x0 + x1 written by the producing epilogue and loaded by TMA straight into the MMA
+//    layout; A = [W0; W1], two MMAs per 16 channels accumulate all four products; Co = 64
+//    keeps the whole prepared filter resident in shared memory.  X3TF32 / X3BF16 / TF32 read
+//    the fp32 halo and let converter warps (w2-5) write the low parts.
+//  * operands are K-major "interleaved" (no swizzle): every position is 16 contiguous bytes
+//    per 4 (tf32) or 8 (bf16) channels, so a shift by one position is +16 B of descriptor
+//    start address.
+//  * a unit = two consecutive tiles of <= 128 positions of one image (PLANES: the frame split
+//    into equal units), accumulators in TMEM double-buffered across units.
+//  * warp roles (480 threads, persistent, 1 CTA/SM): w0 halo TMA, w14 weight TMA, w1 MMA
+//    issuer (whole warp walks the loop so descriptors stay warp-uniform; one elected lane
+//    issues), w2-5 converters (fp32-operand modes), w6-13 two epilogue groups (one tile of
+//    each unit each: TMEM -> registers -> shared transpose -> hi + lo -> fused bias / tanh /
+//    skip / step size -> 16-byte NHWC stores of the output and its planes).
+//  * Programmatic dependent launch: the next grid's prologue and resident-filter load overlap
+//    this grid's tail (pdl_wait before touching the previous grid's data).
 #include <cuda.h>
 #include <cuda_bf16.h>
 

@@ -1,0 +1,14 @@
+"""bf16 MMA rate at M = 64 vs M = 128 (K-major interleave, A same, B rotating), 148 CTAs:
+whether an M = 64 MMA costs half an M = 128 one (same MAC rate) or the same time."""
+import ctypes as C, os, sys
+import torch
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+from paper_2009_01462_b200 import _lib
+L = C.CDLL(_lib.LIB_PATH)
+out = torch.zeros(148, device="cuda")
+for layout, M in ((0, 128), (4, 64)):
+    for N in (128, 256):
+        for nops, what in ((97, "A same, B rotating"), (1, "A re-read")):
+            rc = L.rp_debug_umma_bench(1, N, layout, 0, 0, 3600, 2, nops, 1, 148, C.c_void_p(out.data_ptr()))
+            cyc = float(out.mean())
+            print(f"bf16 M={M} N={N} {what:20s}: {cyc:6.1f} cyc/MMA -> {M * N * 16 / cyc:6.0f} MAC/clk/SM rc={rc}")
