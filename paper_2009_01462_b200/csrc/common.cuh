@@ -5,6 +5,9 @@
 
 #include <cstdint>
 #include <cstdlib>
+#include <mutex>
+#include <set>
+#include <utility>
 #include <stdexcept>
 #include <string>
 
@@ -96,6 +99,20 @@ inline void launch_pdl(Kernel k, int grid, int block, size_t smem, cudaStream_t 
   cfg.numAttrs = pdl_enabled() ? 1 : 0;
   const cudaError_t e = cudaLaunchKernelEx(&cfg, k, args...);
   if (e != cudaSuccess) fail(RP_ERR_CUDA, std::string("cudaLaunchKernelEx: ") + cudaGetErrorString(e));
+}
+
+// cudaFuncSetAttribute(MaxDynamicSharedMemorySize) once per (kernel, device): the attribute
+// belongs to the device's context, so a multi-device trainer needs it on every device.
+inline void ensure_max_dynamic_smem(const void* fn, int bytes) {
+  static std::mutex mu;
+  static std::set<std::pair<const void*, int>> done;
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) fail(RP_ERR_CUDA, "cudaGetDevice failed");
+  std::lock_guard<std::mutex> lk(mu);
+  if (done.count({fn, dev})) return;
+  const cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+  if (e != cudaSuccess) fail(RP_ERR_CUDA, std::string("cudaFuncSetAttribute: ") + cudaGetErrorString(e));
+  done.insert({fn, dev});
 }
 
 inline void validate_geometry(const rp_geometry& g) {

@@ -635,12 +635,7 @@ const CUtensorMap& cached_map(const void* in, const ConvShape& s, int Wp, int ro
 
 template <int EPI, bool BIN>
 void launch(const CUtensorMap& m, const BfArgs& a, size_t smem, int grid, cudaStream_t st) {
-  static bool configured = false;
-  if (!configured) {
-    RP_CUDA(cudaFuncSetAttribute(conv3x3_bf16_kernel<EPI, BIN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 kMaxSmem));
-    configured = true;
-  }
+  ensure_max_dynamic_smem(reinterpret_cast<const void*>(conv3x3_bf16_kernel<EPI, BIN>), kMaxSmem);
   launch_pdl(conv3x3_bf16_kernel<EPI, BIN>, grid, kThreads, smem, st, m, a);
 }
 

@@ -936,12 +936,7 @@ const CUtensorMap& cached_map(const void* in, const ConvShape& s, int Wp, int ro
 
 template <int EPI, int MODE>
 void launch_cfg(const CUtensorMap& m, const TcArgs& a, size_t smem, int grid, cudaStream_t st) {
-  static bool configured = false;
-  if (!configured) {
-    RP_CUDA(cudaFuncSetAttribute(conv3x3_tc_kernel<EPI, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 kMaxSmemRes));
-    configured = true;
-  }
+  ensure_max_dynamic_smem(reinterpret_cast<const void*>(conv3x3_tc_kernel<EPI, MODE>), kMaxSmemRes);
   launch_pdl(conv3x3_tc_kernel<EPI, MODE>, grid, kThreads, smem, st, m, a);
 }
 

@@ -486,11 +486,7 @@ void conv3x3_wgrad_bf16(const ConvShape& s, const float* in, const float* g, flo
   a.part_bias = reinterpret_cast<double*>(static_cast<char*>(ws) + part_bytes(p));
   const CUtensorMap& mg = cached(g, s.n, s.h, s.w, s.co, p.rg);
   const CUtensorMap& mx = cached(in, s.n, s.h, s.w, s.ci, p.rg + 2);
-  static bool configured = false;
-  if (!configured) {
-    RP_CUDA(cudaFuncSetAttribute(wgrad_bf16_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxSmem));
-    configured = true;
-  }
+  ensure_max_dynamic_smem(reinterpret_cast<const void*>(wgrad_bf16_kernel), kMaxSmem);
   wgrad_bf16_kernel<<<p.grid, kThreads, p.smem, st>>>(mg, mx, a);
   RP_LAUNCHED();
   const int total = 9 * s.ci * s.co + s.co;

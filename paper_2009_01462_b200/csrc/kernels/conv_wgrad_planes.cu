@@ -607,11 +607,7 @@ void launch_wgrad_planes(const ConvShape& s, const WgJob* jobs, int njobs, void*
   }
   if (njobs == 1)
     for (int i = 0; i < 4; ++i) m[1][i] = m[0][i];
-  static bool configured = false;
-  if (!configured) {
-    RP_CUDA(cudaFuncSetAttribute(wgrad_planes_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxSmem));
-    configured = true;
-  }
+  ensure_max_dynamic_smem(reinterpret_cast<const void*>(wgrad_planes_kernel), kMaxSmem);
   launch_pdl(wgrad_planes_kernel, p.grid, kThreads, p.smem, st, *m[0][0], *m[0][1], *m[0][2], *m[0][3], *m[1][0],
              *m[1][1], *m[1][2], *m[1][3], a);
   const int total = njobs * (9 * s.ci * s.co + s.co);

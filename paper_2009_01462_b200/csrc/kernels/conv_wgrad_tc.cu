@@ -554,11 +554,7 @@ void conv3x3_wgrad_tc(const ConvShape& s, const float* in, const float* g, float
   a.part_bias = reinterpret_cast<double*>(static_cast<char*>(ws) + part_bytes(p, s));
   const CUtensorMap& mg = cached(g, s.n, s.h, s.w, s.co, p.rg);
   const CUtensorMap& mx = cached(in, s.n, s.h, s.w, s.ci, p.rg + 2);
-  static bool configured = false;
-  if (!configured) {
-    RP_CUDA(cudaFuncSetAttribute(wgrad_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxSmem));
-    configured = true;
-  }
+  ensure_max_dynamic_smem(reinterpret_cast<const void*>(wgrad_tc_kernel), kMaxSmem);
   wgrad_tc_kernel<<<p.grid, kThreads, p.smem, st>>>(mg, mx, a);
   RP_LAUNCHED();
   const int total = 9 * s.ci * s.co + s.co;
