@@ -336,10 +336,19 @@ void block_bwd_bf16t(const rp_geometry& g, int nrows, const void* x16, const voi
     k::conv3x3_fwd_bf16_in16(sd2, g16, pb + L.w2, true, nullptr, nullptr, tanh_act ? d16 : nullptr, h,
                              tanh_act ? k::EPI_DTANH16 : k::EPI_SCALE, nullptr, dpre16, nullptr, wws, st);
   }
-  // gW1 = x^T dpre, gb1 = sum dpre first, while dpre16 is still in L2   (network.cpp:102-103)
-  wgrad_bf16p(shape(g, nrows, C, Ch), x16, dpre16, 1.f, gb + L.w1, gb + L.b1, wgws, st);
-  // gW2 = h a^T g, gb2 = h sum g (before dgrad1 rewrites g16)             (network.cpp:98-99)
-  wgrad_bf16p(shape(g, nrows, Ch, C), a16, g16, h, gb + L.w2, gb + L.b2, wgws, st);
+  const k::ConvShape sw = shape(g, nrows, C, Ch);
+  if (C == Ch && k::conv3x3_wgrad_bf16p_pair_supported(sw) && !std::getenv("RP_WGRAD_UNPAIRED")) {
+    // gW1 = x^T dpre, gb1 = sum dpre and gW2 = h a^T g, gb2 = h sum g in one launch
+    //                                                                (network.cpp:98-103)
+    prof::Scope ps(RP_PROF_CONV_WGRAD, st, 2 * conv_flops(sw), 2 * 2.0 * (double)sw.pixels() * (sw.ci + sw.co));
+    k::conv3x3_wgrad_bf16p_pair(sw, x16, dpre16, 1.f, gb + L.w1, gb + L.b1, a16, g16, h, gb + L.w2, gb + L.b2, wgws,
+                                st);
+  } else {
+    // gW1 = x^T dpre, gb1 = sum dpre first, while dpre16 is still in L2   (network.cpp:102-103)
+    wgrad_bf16p(shape(g, nrows, C, Ch), x16, dpre16, 1.f, gb + L.w1, gb + L.b1, wgws, st);
+    // gW2 = h a^T g, gb2 = h sum g (before dgrad1 rewrites g16)             (network.cpp:98-99)
+    wgrad_bf16p(shape(g, nrows, Ch, C), a16, g16, h, gb + L.w2, gb + L.b2, wgws, st);
+  }
   {   // g <- g + dpre * W1^T in place, and its bf16 copy           (network.cpp:104)
     prof::Scope ps(RP_PROF_CONV_DGRAD, st, conv_flops(sd1), 2.0 * sd1.pixels() * sd1.ci + 10.0 * sd1.pixels() * sd1.co);
     k::conv3x3_fwd_bf16_in16(sd1, dpre16, pb + L.w1, true, nullptr, gio, nullptr, 1.f, k::EPI_ADD, gio, g16, nullptr,

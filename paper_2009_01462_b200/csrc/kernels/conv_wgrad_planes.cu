@@ -643,4 +643,16 @@ void conv3x3_wgrad_bf16p(const ConvShape& s, const void* x, const void* g, float
   launch_wgrad_planes(s, &j, 1, ws, st, true);
 }
 
+bool conv3x3_wgrad_bf16p_pair_supported(const ConvShape& s) {
+  const PwPlan p = plan(s, true);
+  return p.ok && 2 * 3 * (s.co / 128) * (s.ci / 128) <= p.grid;
+}
+
+void conv3x3_wgrad_bf16p_pair(const ConvShape& s, const void* xa, const void* ga, float scale_a, float* gwa,
+                              float* gba, const void* xb, const void* gb2, float scale_b, float* gwb, float* gbb,
+                              void* ws, cudaStream_t st) {
+  const WgJob j[2] = {{xa, nullptr, ga, nullptr, scale_a, gwa, gba}, {xb, nullptr, gb2, nullptr, scale_b, gwb, gbb}};
+  launch_wgrad_planes(s, j, 2, ws, st, true);
+}
+
 }  // namespace rp::k

@@ -115,6 +115,11 @@ bool conv3x3_wgrad_bf16p_supported(const ConvShape& s);
 int64_t conv3x3_wgrad_bf16p_ws_bytes(const ConvShape& s);
 void conv3x3_wgrad_bf16p(const ConvShape& s, const void* x, const void* g, float scale, float* gw, float* gb,
                          void* ws, cudaStream_t st);
+// two of them (same shape) in one launch
+bool conv3x3_wgrad_bf16p_pair_supported(const ConvShape& s);
+void conv3x3_wgrad_bf16p_pair(const ConvShape& s, const void* xa, const void* ga, float scale_a, float* gwa,
+                              float* gba, const void* xb, const void* gb2, float scale_b, float* gwb, float* gbb,
+                              void* ws, cudaStream_t st);
 // fp32 [n] -> bf16 planes p0 = bf16(v), p1 = bf16(v - p0)   (n % 4 == 0; p1 may be null: bf16 copy)
 void split_planes(const float* in, int64_t n, void* p0, void* p1, cudaStream_t st);
 
