@@ -60,7 +60,8 @@ constexpr bool kUseCollector = false;  // A-operand collector reuse, tf32 modes 
 #endif
 constexpr bool kUseCollectorBF = RP_CONV_COLLECTOR_BF;   // X3BF16: A reuse across the 6 MMAs of a tap
 constexpr int kS = 2;                // 128-position tiles per unit
-constexpr int kEpiB = 8;             // epilogue batch (positions per TMEM load / exchange)
+constexpr int kEpiB = 16;            // epilogue batch (positions per TMEM load / exchange)
+constexpr int kEpiJ = kEpiB / 8;     // positions per thread and batch (128 threads x 4 channels)
 constexpr int kMaxSmem = 220 * 1024;      // streaming plans
 constexpr int kMaxSmemRes = 227 * 1024;   // resident-weight plan (the sm_100 per-CTA maximum)
 constexpr int kWResMax = 12;              // resident weight stages (Ci = 64: 4 chunks x 3 filter rows)
@@ -573,14 +574,14 @@ __global__ void __launch_bounds__(kThreads, 1)
     // ===================== epilogue =====================
     // Two groups of 4 warps; group g finishes tile s = g of every unit (both tiles of a unit
     // drain in parallel).  D row r: r < 64 -> W_hi (W0) products for co = r, r >= 64 ->
-    // W_lo (W1) products for co = r - 64.  Batches of 8 positions: every warp moves its 32
+    // W_lo (W1) products for co = r - 64.  Batches of 16 positions: every warp moves its 32
     // rows (TMEM lane quadrant) to shared memory as [hi|lo][position][64 ch]; the group then
-    // reads it back transposed -- thread t owns channels 4 (t & 15) .. +3 of position t >> 4
-    // -- and finishes hi + lo, the fused epilogue and the stores with 16-byte vectors
-    // (coalesced NHWC rows).  The small exchange buffer (8 KB for both groups) is what lets
-    // the resident-weight plan keep three halo slots; the tile's aux operand (16 float4 per
-    // thread) is loaded before the first batch, so a tile pays one memory latency.  Frame
-    // position -> NHWC offset comes from a per-tile table.
+    // reads it back transposed -- thread t owns channels 4 (t & 15) .. +3 of positions
+    // t >> 4 and (t >> 4) + 8 -- and finishes hi + lo, the fused epilogue and the stores with
+    // 16-byte vectors (coalesced NHWC rows).  The exchange buffer (16 KB for both groups) fits
+    // beside the resident filter and three halo slots because the slots are packed to 128 B;
+    // the tile's aux operand (16 float4 per thread) is loaded before the first batch, so a
+    // tile pays one memory latency.  Frame position -> NHWC offset comes from a per-tile table.
     const int q = warp & 3;                 // TMEM lane quadrant this warp may access
     const int grp = (warp - 6) >> 2;        // tile of the unit this warp drains
     const int gtid = (int)threadIdx.x - 192 - grp * 128;
@@ -621,31 +622,38 @@ __global__ void __launch_bounds__(kThreads, 1)
         __nv_bfloat16* p1b = planes ? a.p1 + img * a.Co + co : nullptr;
         const int fvalid = min(a.tile, a.H * Wp - (tile0 + grp) * a.tile);   // frame positions of this tile
         const int nb = (fvalid + kEpiB - 1) / kEpiB;                          // batches with frame positions
-        float4 ax[128 / kEpiB];
+        float4 ax[128 / 8];                                   // [batch][j]: one float4 per position owned
         if constexpr (kAux) {
 #pragma unroll
-          for (int b = 0; b < 128 / kEpiB; ++b) {
-            const int o = b < nb ? tab[b * kEpiB + prow] : -1;
-            ax[b] = o >= 0 ? __ldg(reinterpret_cast<const float4*>(auxb + o)) : make_float4(0.f, 0.f, 0.f, 0.f);
-          }
+          for (int b = 0; b < 128 / kEpiB; ++b)
+#pragma unroll
+            for (int j = 0; j < kEpiJ; ++j) {
+              const int o = b < nb ? tab[b * kEpiB + prow + 8 * j] : -1;
+              ax[b * kEpiJ + j] = o >= 0 ? __ldg(reinterpret_cast<const float4*>(auxb + o)) : make_float4(0.f, 0.f, 0.f, 0.f);
+            }
         }
 #pragma unroll
         for (int b = 0; b < 128 / kEpiB; ++b) {
           if (b < nb) {   // group-uniform
             uint32_t r[kEpiB];
-            tmem_ld8(tcol + (uint32_t)(b * kEpiB), r);
+            if constexpr (kEpiB == 16) tmem_ld16(tcol + (uint32_t)(b * kEpiB), r);
+            else tmem_ld8(tcol + (uint32_t)(b * kEpiB), *reinterpret_cast<uint32_t(*)[8]>(&r[0]));
             tmem_wait_ld();
             asm volatile("bar.sync %0, 128;" ::"r"(grp_bar) : "memory");   // buf free
 #pragma unroll
             for (int e = 0; e < kEpiB; ++e) wrow[e * 64] = __uint_as_float(r[e]);
             asm volatile("bar.sync %0, 128;" ::"r"(grp_bar) : "memory");
-            const int off = tab[b * kEpiB + prow];
-            if (off >= 0) {
-              const float4 hv = *reinterpret_cast<const float4*>(buf + prow * 64 + 4 * c4);
-              const float4 lv = *reinterpret_cast<const float4*>(buf + kEpiB * 64 + prow * 64 + 4 * c4);
+#pragma unroll
+            for (int j = 0; j < kEpiJ; ++j) {
+              const int pr = prow + 8 * j;
+              const int off = tab[b * kEpiB + pr];
+              if (off < 0) continue;
+              const float4 hv = *reinterpret_cast<const float4*>(buf + pr * 64 + 4 * c4);
+              const float4 lv = *reinterpret_cast<const float4*>(buf + kEpiB * 64 + pr * 64 + 4 * c4);
               const float v[4] = {hv.x + lv.x, hv.y + lv.y, hv.z + lv.z, hv.w + lv.w};
               const float bb[4] = {bias.x, bias.y, bias.z, bias.w};
-              const float xa[4] = {ax[b].x, ax[b].y, ax[b].z, ax[b].w};
+              const float4 axj = ax[b * kEpiJ + j];
+              const float xa[4] = {axj.x, axj.y, axj.z, axj.w};
               float o[4];
 #pragma unroll
               for (int i = 0; i < 4; ++i) {
@@ -873,7 +881,7 @@ Plan plan_for(const ConvShape& s, int mode = MODE_X3TF32) {
   const size_t fixed_bytes = 2 * 2 * kEpiB * 64 * 4 + 512 + 1024;   // xchg + barriers + table
   if (mode == MODE_PLANES) {
     p.w_tap = 128u * kChunk * 2u;
-    p.halo_stride = (128 + 2 * (p.plane_bytes + 255) + 1023) / 1024 * 1024;   // plane-pair slot (128 B pitch)
+    p.halo_stride = (128 + 2 * (p.plane_bytes + 255) + 127) / 128 * 128;   // plane-pair slot (128 B aligned TMA targets)
     // resident filter (one co block, every (chunk, filter row) stage) + 3 halo slots (2 if short)
     const int nst = 3 * (s.ci / kChunk);
     const int res_slots = nst * 3 * (size_t)p.w_tap + fixed_bytes + 3 * (size_t)p.halo_stride <= (size_t)kMaxSmemRes ? 3 : 2;
