@@ -356,7 +356,12 @@ __global__ void __launch_bounds__(kThreads, 1)
             }
           }
         };
-        if (kAux || kAux16) load(0, ax);
+        // aux loads run two batches ahead (a ring of three register pairs)
+        float4 ax1[2];
+        if (kAux || kAux16) {
+          load(0, ax);
+          if (nb > 1) load(1, ax1);
+        }
         for (int b = 0; b < nb; ++b) {
           uint32_t r[8];
           tmem_ld8(tcol + (uint32_t)(8 * b), r);
@@ -366,7 +371,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           for (int e = 0; e < 8; ++e) buf[e * 128 + q * 32 + lane] = __uint_as_float(r[e]);
           asm volatile("bar.sync %0, 128;" ::"r"(grp_bar) : "memory");
           float4 axn[2];
-          if ((kAux || kAux16) && b + 1 < nb) load(b + 1, axn);
+          if ((kAux || kAux16) && b + 2 < nb) load(b + 2, axn);
 #pragma unroll
           for (int j = 0; j < 2; ++j) {
             const int pr = pr0 + 4 * j;
@@ -395,7 +400,7 @@ __global__ void __launch_bounds__(kThreads, 1)
               *reinterpret_cast<uint2*>(outb16d + off) =
                   make_uint2(pack_bf16(1.f - o[0] * o[0], 1.f - o[1] * o[1]), pack_bf16(1.f - o[2] * o[2], 1.f - o[3] * o[3]));
           }
-          if (kAux || kAux16) ax[0] = axn[0], ax[1] = axn[1];
+          if (kAux || kAux16) ax[0] = ax1[0], ax[1] = ax1[1], ax1[0] = axn[0], ax1[1] = axn[1];
         }
       }
       tc_fence_before();
