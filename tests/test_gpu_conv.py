@@ -234,8 +234,8 @@ def test_wgrad_deterministic():
 
 
 # The stem S (Cin -> C 3x3 conv, streaming kernels): forward and weight/bias gradients vs the
-# fp64 oracle.  C = 256 has more (row quad, channel quad) register tiles than the wgrad
-# kernel has threads (7 x 64 = 448 > 256): every tile must still be computed.
+# fp64 oracle.  Cin = 4, C = 256 has more (row quad, channel octet) register tiles than the
+# wgrad kernel has threads (10 x 32 = 320 > 256): every tile must still be computed.
 @pytest.mark.parametrize("cin,c", [(1, 16), (3, 64), (3, 128), (3, 256), (4, 256), (2, 32)])
 def test_stem_fwd_and_wgrad(cin, c):
     n, hh, ww = 3, 12, 10
