@@ -241,6 +241,10 @@ int64_t rp_op_workspace_bytes(const rp_geometry* g, int32_t nrows, int32_t math)
 /* Stem S (affine_forward, network.cpp:108-110 as a 3x3 conv Cin->C). */
 int rp_op_stem_fwd(const rp_geometry* g, int32_t nrows, const float* x_raw, const float* ps, float* x0,
                    int32_t math, void* ws, int64_t ws_bytes, void* stream);
+/* The stem forward writing, in the same pass, the bf16 planes of x0 that rp_op_split_planes
+ * makes (p0 = bf16(x0), p1 = bf16(x0 - p0); p1 nullable): the first block's tape input. */
+int rp_op_stem_fwd_planes(const rp_geometry* g, int32_t nrows, const float* x_raw, const float* ps, float* x0,
+                          void* p0, void* p1, void* stream);
 int rp_op_stem_bwd(const rp_geometry* g, int32_t nrows, const float* x_raw, const float* g0, float* gs,
                    void* ws, int64_t ws_bytes, void* stream);
 /* Head T forward (affine_forward, network.cpp:108-110, as GAP + affine): pooled [nrows, C]

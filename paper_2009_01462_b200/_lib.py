@@ -79,6 +79,7 @@ SIGNATURES = {
     "rp_op_block_bwd": (C.c_int, [_G, C.c_int32, _P, _P, _P, _P, _P, _P, C.c_int32, _P, C.c_int64, _P]),
     "rp_op_workspace_bytes": (C.c_int64, [_G, C.c_int32, C.c_int32]),
     "rp_op_stem_fwd": (C.c_int, [_G, C.c_int32, _P, _P, _P, C.c_int32, _P, C.c_int64, _P]),
+    "rp_op_stem_fwd_planes": (C.c_int, [_G, C.c_int32, _P, _P, _P, _P, _P, _P]),
     "rp_op_stem_bwd": (C.c_int, [_G, C.c_int32, _P, _P, _P, _P, C.c_int64, _P]),
     "rp_op_head_fwd": (C.c_int, [_G, C.c_int32, _P, _P, _P, _P, _P]),
     "rp_op_head_loss_bwd": (C.c_int, [_G, C.c_int32, _P, _P, _P, _P, _P, _P, _P, _P, C.c_int64, _P]),

@@ -356,14 +356,17 @@ void block_bwd_bf16t(const rp_geometry& g, int nrows, const void* x16, const voi
   }
 }
 
-void stem_fwd(const rp_geometry& g, int nrows, const float* xr, const float* ps, float* x0, cudaStream_t st) {
+void stem_fwd(const rp_geometry& g, int nrows, const float* xr, const float* ps, float* x0, cudaStream_t st,
+              void* p0 = nullptr, void* p1 = nullptr) {
   const ParamLayout L = ParamLayout::of(g);
   const k::ConvShape sh = shape(g, nrows, g.in_channels, g.channels);
   prof::Scope scope(RP_PROF_STEM, st, conv_flops(sh), conv_bytes(sh, false));
-  if (k::stem_supported(sh))
-    k::stem_fwd(sh, xr, ps + L.s_w, ps + L.s_b, x0, st);
-  else
-    k::conv3x3_fwd_simt(sh, xr, ps + L.s_w, ps + L.s_b, nullptr, 1.f, k::EPI_BIAS, x0, st);
+  if (k::stem_supported(sh)) {
+    k::stem_fwd(sh, xr, ps + L.s_w, ps + L.s_b, x0, st, p0, p1);
+    return;
+  }
+  k::conv3x3_fwd_simt(sh, xr, ps + L.s_w, ps + L.s_b, nullptr, 1.f, k::EPI_BIAS, x0, st);
+  if (p0) k::split_planes(x0, sh.pixels() * sh.co, p0, p1, st);
 }
 
 void stem_bwd(const rp_geometry& g, int nrows, const float* xr, const float* g0, float* gs, void* ws,
@@ -763,6 +766,17 @@ int rp_op_stem_fwd(const rp_geometry* g, int32_t nrows, const float* x_raw, cons
     check_math(math);
     if (nrows <= 0) return;
     stem_fwd(*g, nrows, x_raw, ps, x0, S(stream));
+  });
+}
+
+int rp_op_stem_fwd_planes(const rp_geometry* g, int32_t nrows, const float* x_raw, const float* ps, float* x0, void* p0,
+                          void* p1, void* stream) {
+  return guard([&] {
+    need(g, "geometry");
+    validate_geometry(*g);
+    need(p0, "p0");
+    if (nrows <= 0) return;
+    stem_fwd(*g, nrows, x_raw, ps, x0, S(stream), p0, p1);
   });
 }
 

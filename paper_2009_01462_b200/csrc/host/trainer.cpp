@@ -436,18 +436,27 @@ void DecoupledTrainer::run_forward(Stage& st, const float* input, int nrows, flo
   const Layout L(geo_);
   const float* P = params_for(st.index);
   const float* cur = input;
+  const int n = st.end - st.begin;
+  st.tape_planes = n > 0 && rp_op_block_planes_supported(&geo_, nrows, math_);
+  st.tape_bf16 = n > 0 && rp_op_block_bf16_tape_supported(&geo_, nrows, math_);
+  // the first block's input planes: written by the stem in its pass, else split here
+  bool in_planes = false;
   if (st.index == 0) {
-    check(rp_op_stem_fwd(&geo_, nrows, input, P, st.x0.get(), math_, st.ws.get(), st.ws.bytes(), s));
+    if (st.tape_planes || st.tape_bf16) {
+      auto* p = st.xps[0].get<uint16_t>();
+      check(rp_op_stem_fwd_planes(&geo_, nrows, input, P, st.x0.get(), p,
+                                  st.tape_bf16 ? nullptr : p + (int64_t)nrows * feat(), s));
+      in_planes = true;
+    } else {
+      check(rp_op_stem_fwd(&geo_, nrows, input, P, st.x0.get(), math_, st.ws.get(), st.ws.bytes(), s));
+    }
     st.raw = input;
     cur = st.x0.get();
   }
   st.input0 = cur;
-  const int n = st.end - st.begin;
-  st.tape_planes = n > 0 && rp_op_block_planes_supported(&geo_, nrows, math_);
-  st.tape_bf16 = n > 0 && rp_op_block_bf16_tape_supported(&geo_, nrows, math_);
   if (st.tape_bf16) {
     // bf16 copies of every block input and activation for the TMA-fed bf16 wgrad
-    check(rp_op_split_planes(cur, (int64_t)nrows * feat(), st.xps[0].get(), nullptr, s));
+    if (!in_planes) check(rp_op_split_planes(cur, (int64_t)nrows * feat(), st.xps[0].get(), nullptr, s));
     for (int i = 0; i < n; ++i) {
       const int l = st.begin + i;
       float* out = i == n - 1 ? out_features : st.xs[1 + (i & 1)].get();
@@ -463,7 +472,7 @@ void DecoupledTrainer::run_forward(Stage& st, const float* input, int nrows, flo
   if (st.tape_planes) {
     const int64_t e = (int64_t)nrows * feat();
     auto* p = st.xps[0].get<uint16_t>();
-    check(rp_op_split_planes(cur, e, p, p + e, s));
+    if (!in_planes) check(rp_op_split_planes(cur, e, p, p + e, s));
     // every block's forward filters in one launch (not one per conv)
     const int64_t fpair = rp_op_planes_filters_bytes(&geo_, 1);
     check(rp_op_prep_planes_filters(&geo_, P + L.block0 + (int64_t)st.begin * L.block_stride, n, 0,

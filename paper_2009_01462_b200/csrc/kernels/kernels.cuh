@@ -126,7 +126,9 @@ void split_planes(const float* in, int64_t n, void* p0, void* p1, cudaStream_t s
 // ---- stem S (stem.cu): Cin <= 4 streaming kernels (SIMT conv path otherwise)
 bool stem_supported(const ConvShape& s);
 int64_t stem_wgrad_ws_bytes(const ConvShape& s);
-void stem_fwd(const ConvShape& s, const float* x, const float* w, const float* b, float* out, cudaStream_t st);
+// p0 (and p1, nullable): the output's bf16 planes as split_planes makes them, in the same pass
+void stem_fwd(const ConvShape& s, const float* x, const float* w, const float* b, float* out, cudaStream_t st,
+              void* p0 = nullptr, void* p1 = nullptr);
 void stem_wgrad(const ConvShape& s, const float* x, const float* g, float scale, float* gw, float* gb, void* ws,
                 cudaStream_t st);
 

@@ -8,6 +8,8 @@
 //   wgrad: gw[tap][ci][co] = scale * sum_p x[p + off(tap)][ci] * g[p][co],
 //          gb[co] = scale * sum_p g[p][co]   (deterministic: fixed position ranges per
 //          CTA, fixed-order lane / CTA reductions)
+#include <cuda_bf16.h>
+
 #include "../common.cuh"
 #include "kernels.cuh"
 
@@ -73,7 +75,8 @@ __global__ __launch_bounds__(256) void stem_fwd_kernel(const float* __restrict__
 template <int Cin, int CG>
 __global__ __launch_bounds__(256, CG == 8 ? 3 : 2) void stem_fwd4_kernel(const float* __restrict__ x, const float* __restrict__ w,
                                                         const float* __restrict__ b, int N, int H, int W, int C,
-                                                        float* __restrict__ out) {
+                                                        float* __restrict__ out, uint2* __restrict__ p0,
+                                                        uint2* __restrict__ p1) {
   extern __shared__ float ws[];
   const int nw = 9 * Cin * C;
   for (int i = threadIdx.x; i < nw + C; i += blockDim.x) ws[i] = i < nw ? w[i] : b[i - nw];
@@ -134,6 +137,19 @@ __global__ __launch_bounds__(256, CG == 8 ? 3 : 2) void stem_fwd4_kernel(const f
 #pragma unroll
       for (int qq = 0; qq < CG / 4; ++qq)
         o[qq] = make_float4(acc[i][4 * qq], acc[i][4 * qq + 1], acc[i][4 * qq + 2], acc[i][4 * qq + 3]);
+      if (p0) {   // the first block's input planes, as split_planes makes them
+        const int64_t e4 = (((n * H + yq) * (int64_t)W + x0 + i) * C + c0) / 4;
+#pragma unroll
+        for (int qq = 0; qq < CG / 4; ++qq) {
+          const float* v = &acc[i][4 * qq];
+          const __nv_bfloat162 hi0 = __floats2bfloat162_rn(v[0], v[1]), hi1 = __floats2bfloat162_rn(v[2], v[3]);
+          const __nv_bfloat162 lo0 = __floats2bfloat162_rn(v[0] - __low2float(hi0), v[1] - __high2float(hi0));
+          const __nv_bfloat162 lo1 = __floats2bfloat162_rn(v[2] - __low2float(hi1), v[3] - __high2float(hi1));
+          p0[e4 + qq] = make_uint2(*reinterpret_cast<const uint32_t*>(&hi0), *reinterpret_cast<const uint32_t*>(&hi1));
+          if (p1)
+            p1[e4 + qq] = make_uint2(*reinterpret_cast<const uint32_t*>(&lo0), *reinterpret_cast<const uint32_t*>(&lo1));
+        }
+      }
     }
   }
 }
@@ -311,20 +327,23 @@ int64_t stem_wgrad_ws_bytes(const ConvShape& s) {
   return (int64_t)kStemGrid * ((9 * s.ci + 1 + 3) / 4 * 4) * s.co * 4 + 256;
 }
 
-void stem_fwd(const ConvShape& s, const float* x, const float* w, const float* b, float* out, cudaStream_t st) {
+void stem_fwd(const ConvShape& s, const float* x, const float* w, const float* b, float* out, cudaStream_t st,
+              void* p0, void* p1) {
   const int64_t items = s.pixels() * (s.co / 16);
   const int grid = (int)std::min<int64_t>((items + 255) / 256, 32 * kNumSMs);
   const size_t smem = (size_t)(9 * s.ci * s.co + s.co) * 4;
   const dim3 gr(std::max(grid, 1));
   if (s.w % 4 == 0) {
     constexpr int CG = 8;
+    auto* u0 = static_cast<uint2*>(p0);
+    auto* u1 = static_cast<uint2*>(p1);
     const int64_t items4 = s.pixels() / 4 * (s.co / CG);
     const dim3 gr4((unsigned)std::max<int64_t>(1, std::min<int64_t>((items4 + 255) / 256, 32 * kNumSMs)));
     switch (s.ci) {
-      case 1: stem_fwd4_kernel<1, CG><<<gr4, 256, smem, st>>>(x, w, b, s.n, s.h, s.w, s.co, out); break;
-      case 2: stem_fwd4_kernel<2, CG><<<gr4, 256, smem, st>>>(x, w, b, s.n, s.h, s.w, s.co, out); break;
-      case 3: stem_fwd4_kernel<3, CG><<<gr4, 256, smem, st>>>(x, w, b, s.n, s.h, s.w, s.co, out); break;
-      default: stem_fwd4_kernel<4, CG><<<gr4, 256, smem, st>>>(x, w, b, s.n, s.h, s.w, s.co, out); break;
+      case 1: stem_fwd4_kernel<1, CG><<<gr4, 256, smem, st>>>(x, w, b, s.n, s.h, s.w, s.co, out, u0, u1); break;
+      case 2: stem_fwd4_kernel<2, CG><<<gr4, 256, smem, st>>>(x, w, b, s.n, s.h, s.w, s.co, out, u0, u1); break;
+      case 3: stem_fwd4_kernel<3, CG><<<gr4, 256, smem, st>>>(x, w, b, s.n, s.h, s.w, s.co, out, u0, u1); break;
+      default: stem_fwd4_kernel<4, CG><<<gr4, 256, smem, st>>>(x, w, b, s.n, s.h, s.w, s.co, out, u0, u1); break;
     }
     RP_LAUNCHED();
     return;
@@ -336,6 +355,7 @@ void stem_fwd(const ConvShape& s, const float* x, const float* w, const float* b
     default: stem_fwd_kernel<4><<<gr, 256, smem, st>>>(x, w, b, s.n, s.h, s.w, s.co, out); break;
   }
   RP_LAUNCHED();
+  if (p0) split_planes(out, s.pixels() * s.co, p0, p1, st);
 }
 
 // One wave: the grid is what fits the SMs at once (<= kStemGrid partials), so no CTA

@@ -271,3 +271,38 @@ def test_stem_fwd_and_wgrad(cin, c):
     eo = np.abs(o64 - want_out).max() / np.abs(want_out).max()
     print(f"stem cin={cin} c={c}: out {eo:.1e} gw {ew:.1e} gb {eb:.1e}")
     assert eo <= 1e-5 and ew <= 1e-5 and eb <= 1e-5, (eo, ew, eb)
+
+
+# rp_op_stem_fwd_planes: the stem output plus, in the same pass, the bf16 planes of it --
+# bitwise what rp_op_stem_fwd followed by rp_op_split_planes gives (W % 4 == 0: the fused
+# store; W = 10 / 6: the split after the streaming kernel).
+@pytest.mark.parametrize("cin,c,hh,ww,lo", [(3, 64, 8, 12, True), (3, 64, 8, 12, False), (1, 16, 7, 10, True),
+                                             (3, 256, 4, 8, False), (2, 32, 5, 6, True)])
+def test_stem_fwd_planes_matches_split(cin, c, hh, ww, lo):
+    n = 3
+    rng = np.random.default_rng(23)
+    geo = rp.Geometry(cin, hh, ww, c, c, 1, 10).c()
+    npar = lib().rp_param_count(C.byref(geo))
+    dev = torch.device("cuda")
+    tp = torch.from_numpy(rng.uniform(-0.3, 0.3, npar).astype(np.float32)).to(dev)
+    tx = torch.from_numpy(rng.uniform(-1, 1, (n, hh, ww, cin)).astype(np.float32)).to(dev)
+    e = n * hh * ww * c
+    wsb = lib().rp_op_workspace_bytes(C.byref(geo), n, rp.MATH["fp32"])
+    ws = torch.empty(wsb, dtype=torch.uint8, device=dev)
+    out_ref = torch.empty(e, device=dev)
+    rp.check(lib().rp_op_stem_fwd(C.byref(geo), n, C.c_void_p(tx.data_ptr()), C.c_void_p(tp.data_ptr()),
+                                  C.c_void_p(out_ref.data_ptr()), rp.MATH["fp32"], C.c_void_p(ws.data_ptr()), wsb,
+                                  None))
+    want = torch.full((2 * e,), 0x7FFF, dtype=torch.int16, device=dev)
+    rp.check(lib().rp_op_split_planes(C.c_void_p(out_ref.data_ptr()), e, C.c_void_p(want.data_ptr()),
+                                      C.c_void_p(want.data_ptr() + 2 * e) if lo else None, None))
+    out = torch.full((e,), float("nan"), device=dev)
+    got = torch.full((2 * e,), 0x7FFF, dtype=torch.int16, device=dev)
+    rp.check(lib().rp_op_stem_fwd_planes(C.byref(geo), n, C.c_void_p(tx.data_ptr()), C.c_void_p(tp.data_ptr()),
+                                         C.c_void_p(out.data_ptr()), C.c_void_p(got.data_ptr()),
+                                         C.c_void_p(got.data_ptr() + 2 * e) if lo else None, None))
+    torch.cuda.synchronize()
+    assert torch.equal(out, out_ref)
+    assert torch.equal(got, want)   # the lo plane untouched (sentinel) when p1 is NULL
+    if not lo:
+        assert bool((got[e:] == 0x7FFF).all())
