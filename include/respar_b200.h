@@ -257,6 +257,11 @@ int rp_op_head_fwd(const rp_geometry* g, int32_t nrows, const float* x_end, cons
 int rp_op_head_loss_bwd(const rp_geometry* g, int32_t nrows, const float* pooled, const float* logits,
                         const float* pt, const int32_t* labels, double* loss_dev, float* gt, float* g_out,
                         void* ws, int64_t ws_bytes, void* stream);
+/* rp_op_head_loss_bwd also writing the cotangent's bf16 planes (as rp_op_split_planes makes
+ * them; p1 nullable) in the broadcast pass: the last stage's first backward conv input. */
+int rp_op_head_loss_bwd_planes(const rp_geometry* g, int32_t nrows, const float* pooled, const float* logits,
+                               const float* pt, const int32_t* labels, double* loss_dev, float* gt, float* g_out,
+                               void* p0, void* p1, void* ws, int64_t ws_bytes, void* stream);
 /* Argmax hits (accuracy, network.cpp:223-234; ties -> lowest class); *hits host. */
 int rp_op_argmax_hits(const float* logits, const int32_t* labels, int32_t nrows, int32_t classes,
                       int64_t* hits, void* ws, void* stream);

@@ -83,6 +83,8 @@ SIGNATURES = {
     "rp_op_stem_bwd": (C.c_int, [_G, C.c_int32, _P, _P, _P, _P, C.c_int64, _P]),
     "rp_op_head_fwd": (C.c_int, [_G, C.c_int32, _P, _P, _P, _P, _P]),
     "rp_op_head_loss_bwd": (C.c_int, [_G, C.c_int32, _P, _P, _P, _P, _P, _P, _P, _P, C.c_int64, _P]),
+    "rp_op_head_loss_bwd_planes": (C.c_int, [_G, C.c_int32, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, C.c_int64,
+                                             _P]),
     "rp_op_argmax_hits": (C.c_int, [_P, _P, C.c_int32, C.c_int32, _I64P, _P, _P]),
     "rp_trainer_create": (C.c_int, [_G, C.c_int32, C.c_int32, C.c_int32, C.c_int32, _F, _U64P, C.c_int32,
                                     _I32, C.c_int32, C.POINTER(_P)]),

@@ -392,11 +392,11 @@ void head_fwd(const rp_geometry& g, int nrows, const float* x_end, const float* 
 
 void head_loss_bwd(const rp_geometry& g, int nrows, const float* pooled, const float* logits, const float* pt,
                    const int32_t* labels, double* loss_dev, float* gt, float* g_out, void* ws, int64_t ws_bytes,
-                   cudaStream_t st) {
+                   cudaStream_t st, void* p0 = nullptr, void* p1 = nullptr) {
   if (k::head_ws_bytes(nrows, g.channels, g.classes) > ws_bytes) fail(RP_ERR_RANGE, "head: workspace too small");
   prof::Scope scope(RP_PROF_HEAD, st, 0.0, 4.0 * nrows * g.height * g.width * g.channels);
   k::head_loss_backward(nrows, g.height * g.width, g.channels, g.classes, pooled, logits, pt, labels, loss_dev, gt,
-                        gt + (int64_t)g.channels * g.classes, g_out, ws, st);
+                        gt + (int64_t)g.channels * g.classes, g_out, ws, st, p0, p1);
 }
 
 void init_params(const rp_geometry& g, float* params, uint64_t* state, cudaStream_t st) {
@@ -806,6 +806,17 @@ int rp_op_head_loss_bwd(const rp_geometry* g, int32_t nrows, const float* pooled
     need(g, "geometry");
     validate_geometry(*g);
     head_loss_bwd(*g, nrows, pooled, logits, pt, labels, loss_dev, gt, g_out, ws, ws_bytes, S(stream));
+  });
+}
+
+int rp_op_head_loss_bwd_planes(const rp_geometry* g, int32_t nrows, const float* pooled, const float* logits,
+                               const float* pt, const int32_t* labels, double* loss_dev, float* gt, float* g_out,
+                               void* p0, void* p1, void* ws, int64_t ws_bytes, void* stream) {
+  return guard([&] {
+    need(g, "geometry");
+    validate_geometry(*g);
+    need(p0, "p0");
+    head_loss_bwd(*g, nrows, pooled, logits, pt, labels, loss_dev, gt, g_out, ws, ws_bytes, S(stream), p0, p1);
   });
 }
 

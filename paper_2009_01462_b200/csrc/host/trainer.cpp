@@ -518,8 +518,15 @@ void DecoupledTrainer::run_backward(Stage& st, const int32_t* labels, int nrows,
   uint16_t* gp16 = tape ? st.g_p.get<uint16_t>() : nullptr;
   bool planes_done = false;
   if (k == stages() - 1) {
-    check(rp_op_head_loss_bwd(&geo_, nrows, st.pooled.get(), st.logits.get(), P + L.t_w, labels, st.loss.get<double>(),
-                              G + L.t_w, g, st.ws.get(), st.ws.bytes(), s));
+    if (tape) {
+      check(rp_op_head_loss_bwd_planes(&geo_, nrows, st.pooled.get(), st.logits.get(), P + L.t_w, labels,
+                                       st.loss.get<double>(), G + L.t_w, g, gp16, st.tape_bf16 ? nullptr : gp16 + n,
+                                       st.ws.get(), st.ws.bytes(), s));
+      planes_done = true;
+    } else {
+      check(rp_op_head_loss_bwd(&geo_, nrows, st.pooled.get(), st.logits.get(), P + L.t_w, labels,
+                                st.loss.get<double>(), G + L.t_w, g, st.ws.get(), st.ws.bytes(), s));
+    }
   } else {
     const Stage& nx = stages_[k + 1];
     const float* lam_next;

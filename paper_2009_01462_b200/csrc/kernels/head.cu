@@ -1,6 +1,7 @@
 // Output map T and the task loss (network.cpp:108-110, 193-221), conv form:
 // global average pool -> affine C->classes -> mean softmax-CE, and its backward.
 // All reductions run in a fixed order (deterministic).
+#include <cuda_bf16.h>
 #include <cfloat>
 
 #include "../common.cuh"
@@ -159,15 +160,27 @@ __global__ void broadcast_kernel(const float* __restrict__ gpool, int64_t hw, in
   }
 }
 
+// p0 / p1 (nullable): the cotangent's bf16 planes as split_planes makes them, same pass
 __global__ void broadcast_kernel_vec4(const float* __restrict__ gpool, int64_t hw, int C, int64_t total4,
-                                      float inv_hw, float4* __restrict__ g) {
+                                      float inv_hw, float4* __restrict__ g, uint2* __restrict__ p0,
+                                      uint2* __restrict__ p1) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total4;
        i += (int64_t)gridDim.x * blockDim.x) {
     const int64_t e = i * 4;
     const int c = (int)(e % C);
     const int64_t b = e / ((int64_t)C * hw);
     const float* gp = gpool + b * C + c;
-    g[i] = make_float4(gp[0] * inv_hw, gp[1] * inv_hw, gp[2] * inv_hw, gp[3] * inv_hw);
+    const float4 v = make_float4(gp[0] * inv_hw, gp[1] * inv_hw, gp[2] * inv_hw, gp[3] * inv_hw);
+    g[i] = v;
+    if (p0) {
+      const __nv_bfloat162 a = __floats2bfloat162_rn(v.x, v.y), b2 = __floats2bfloat162_rn(v.z, v.w);
+      p0[i] = make_uint2(*reinterpret_cast<const uint32_t*>(&a), *reinterpret_cast<const uint32_t*>(&b2));
+      if (p1) {
+        const __nv_bfloat162 c = __floats2bfloat162_rn(v.x - __low2float(a), v.y - __high2float(a));
+        const __nv_bfloat162 d = __floats2bfloat162_rn(v.z - __low2float(b2), v.w - __high2float(b2));
+        p1[i] = make_uint2(*reinterpret_cast<const uint32_t*>(&c), *reinterpret_cast<const uint32_t*>(&d));
+      }
+    }
   }
 }
 
@@ -208,7 +221,7 @@ void head_forward(int nrows, int hw, int C, int classes, const float* x_end, con
 
 void head_loss_backward(int nrows, int hw, int C, int classes, const float* pooled, const float* logits,
                         const float* t_w, const int32_t* labels, double* loss_dev, float* gt_w, float* gt_b,
-                        float* g_out, void* ws, cudaStream_t st) {
+                        float* g_out, void* ws, cudaStream_t st, void* p0, void* p1) {
   if (nrows <= 0) return;
   char* w = static_cast<char*>(ws);
   float* glog = reinterpret_cast<float*>(w);
@@ -223,11 +236,15 @@ void head_loss_backward(int nrows, int hw, int C, int classes, const float* pool
   const int64_t n = (int64_t)nrows * hw * C;
   const float inv = 1.f / (float)hw;
   const int grid = (int)std::min<int64_t>((n / 4 + 255) / 256 + 1, 16 * kNumSMs);
-  if (C % 4 == 0 && (reinterpret_cast<uintptr_t>(g_out) & 15u) == 0)
-    broadcast_kernel_vec4<<<grid, 256, 0, st>>>(gpool, hw, C, n / 4, inv, reinterpret_cast<float4*>(g_out));
-  else
-    broadcast_kernel<<<grid, 256, 0, st>>>(gpool, hw, C, n, inv, g_out);
+  if (C % 4 == 0 && (reinterpret_cast<uintptr_t>(g_out) & 15u) == 0) {
+    broadcast_kernel_vec4<<<grid, 256, 0, st>>>(gpool, hw, C, n / 4, inv, reinterpret_cast<float4*>(g_out),
+                                                static_cast<uint2*>(p0), static_cast<uint2*>(p1));
+    RP_LAUNCHED();
+    return;
+  }
+  broadcast_kernel<<<grid, 256, 0, st>>>(gpool, hw, C, n, inv, g_out);
   RP_LAUNCHED();
+  if (p0) split_planes(g_out, n, p0, p1, st);
 }
 
 void argmax_hits(const float* logits, const int32_t* labels, int nrows, int classes, unsigned long long* hits_dev,

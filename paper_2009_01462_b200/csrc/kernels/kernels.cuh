@@ -138,7 +138,7 @@ void head_forward(int nrows, int hw, int channels, int classes, const float* x_e
                   const float* t_b, float* pooled, float* logits, cudaStream_t st);
 void head_loss_backward(int nrows, int hw, int channels, int classes, const float* pooled, const float* logits,
                         const float* t_w, const int32_t* labels, double* loss_dev, float* gt_w, float* gt_b,
-                        float* g_out, void* ws, cudaStream_t st);
+                        float* g_out, void* ws, cudaStream_t st, void* p0 = nullptr, void* p1 = nullptr);
 void argmax_hits(const float* logits, const int32_t* labels, int nrows, int classes, unsigned long long* hits_dev,
                  cudaStream_t st);
 

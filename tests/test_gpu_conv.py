@@ -306,3 +306,46 @@ def test_stem_fwd_planes_matches_split(cin, c, hh, ww, lo):
     assert torch.equal(got, want)   # the lo plane untouched (sentinel) when p1 is NULL
     if not lo:
         assert bool((got[e:] == 0x7FFF).all())
+
+
+# rp_op_head_loss_bwd_planes: the head backward plus the cotangent's bf16 planes in the
+# broadcast pass -- bitwise rp_op_head_loss_bwd followed by rp_op_split_planes.
+@pytest.mark.parametrize("c,lo", [(64, True), (128, False), (256, True)])
+def test_head_loss_bwd_planes_matches_split(c, lo):
+    n, hh, ww, classes = 5, 8, 8, 10
+    rng = np.random.default_rng(29)
+    geo = rp.Geometry(3, hh, ww, c, c, 1, classes).c()
+    npar = lib().rp_param_count(C.byref(geo))
+    dev = torch.device("cuda")
+    tp = torch.from_numpy(rng.uniform(-0.3, 0.3, npar).astype(np.float32)).to(dev)
+    pt = C.c_void_p(tp.data_ptr() + 4 * (npar - (c * classes + classes)))
+    e = n * hh * ww * c
+    x_end = torch.from_numpy(rng.uniform(-1, 1, e).astype(np.float32)).to(dev)
+    labels = torch.from_numpy(rng.integers(0, classes, n).astype(np.int32)).to(dev)
+    pooled = torch.empty(n * c, device=dev)
+    logits = torch.empty(n * classes, device=dev)
+    rp.check(lib().rp_op_head_fwd(C.byref(geo), n, C.c_void_p(x_end.data_ptr()), pt, C.c_void_p(pooled.data_ptr()),
+                                  C.c_void_p(logits.data_ptr()), None))
+    wsb = lib().rp_op_workspace_bytes(C.byref(geo), n, rp.MATH["fp32"])
+    ws = torch.empty(wsb, dtype=torch.uint8, device=dev)
+    outs = []
+    for fused in (False, True):
+        loss = torch.zeros(1, dtype=torch.float64, device=dev)
+        gt = torch.full((c * classes + classes,), float("nan"), device=dev)
+        g = torch.full((e,), float("nan"), device=dev)
+        planes = torch.full((2 * e,), 0x7FFF, dtype=torch.int16, device=dev)
+        p0 = C.c_void_p(planes.data_ptr())
+        p1 = C.c_void_p(planes.data_ptr() + 2 * e) if lo else None
+        args = (C.byref(geo), n, C.c_void_p(pooled.data_ptr()), C.c_void_p(logits.data_ptr()), pt,
+                C.c_void_p(labels.data_ptr()), C.c_void_p(loss.data_ptr()), C.c_void_p(gt.data_ptr()),
+                C.c_void_p(g.data_ptr()))
+        if fused:
+            rp.check(lib().rp_op_head_loss_bwd_planes(*args, p0, p1, C.c_void_p(ws.data_ptr()), wsb, None))
+        else:
+            rp.check(lib().rp_op_head_loss_bwd(*args, C.c_void_p(ws.data_ptr()), wsb, None))
+            rp.check(lib().rp_op_split_planes(C.c_void_p(g.data_ptr()), e, p0, p1, None))
+        torch.cuda.synchronize()
+        outs.append((loss, gt, g, planes))
+    for a, b in zip(*outs):
+        assert torch.equal(a, b)
+    assert bool(torch.isfinite(outs[1][2]).all())
