@@ -362,6 +362,20 @@ def net_vjp(net: ConvNet, tape: ForwardTape, upstream: np.ndarray):
     return cot, grads
 
 
+def grads_flat(g: Geometry, stage_grads, ranges) -> np.ndarray:
+    """Per-stage NetGrads (stage k owning blocks ranges[k]) as one vector in the flat
+    parameter layout (the device trainer's rp_trainer_get_grads)."""
+    net = zero_net(g)
+    for (b, _), gr in zip(ranges, stage_grads):
+        if gr.has_s:
+            net.s_w[...], net.s_b[...] = gr.s_w, gr.s_b
+        for i, (gw1, gb1, gw2, gb2) in enumerate(gr.blocks):
+            net.w1[b + i][...], net.b1[b + i][...], net.w2[b + i][...], net.b2[b + i][...] = gw1, gb1, gw2, gb2
+        if gr.has_t:
+            net.t_w[...], net.t_b[...] = gr.t_w, gr.t_b
+    return net.flat()
+
+
 def apply_updates(net: ConvNet, grads: NetGrads, from_block: int, lr: float) -> None:
     """apply_updates (network.cpp:174-191): W -= lr * g, S, blocks, T."""
     if grads.has_s:
@@ -634,9 +648,10 @@ class DecoupledTrainer:
         self.iteration += 1
         snaps = [self.take_snapshot(k, row0, nrows) if k + 1 < self.stages else None
                  for k in range(self.stages)]
+        self.last_grads = []              # per-stage NetGrads (the reference's step discards them)
         for k in range(self.stages):      # W=1 sequential reference order (runtime.cpp:44-46)
             self.stage_forward(k, batch_x, row0)
-            self.stage_backward_update(k, labels, snaps[k], p.beta, p.lr, row0)
+            self.last_grads.append(self.stage_backward_update(k, labels, snaps[k], p.beta, p.lr, row0))
         for k in range(1, self.stages):
             self.correct_aux(k, p, row0, nrows)
             if self.mode == ALM:

@@ -8,7 +8,9 @@ import ctypes as C
 import os
 
 _PKG = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_PKG, "librespar_b200.so")
+# RP_LIB_PATH: load another build of the same library (tools/mutation_check.sh points the
+# parity tests at a deliberately broken build to show that they fail)
+LIB_PATH = os.environ.get("RP_LIB_PATH") or os.path.join(_PKG, "librespar_b200.so")
 HEADER = os.path.join(os.path.dirname(_PKG), "include", "respar_b200.h")
 
 RP_OK, RP_ERR_SHAPE, RP_ERR_CONFIG, RP_ERR_STATE, RP_ERR_RANGE, RP_ERR_STAGE, RP_ERR_CUDA, RP_ERR_NCCL, \

@@ -57,7 +57,9 @@ class DeviceArray {
     swap(o);
     return *this;
   }
-  void allocate(int device, int64_t bytes);  // no-op when already at least that big
+  // no-op when already at least that big; returns true when it (re)allocated, which moves
+  // the buffer (a captured CUDA graph holding the old pointer must be re-captured)
+  bool allocate(int device, int64_t bytes);
   void zero(cudaStream_t s);
   template <class T = float>
   T* get() const {
@@ -284,8 +286,9 @@ class DecoupledTrainer {
     double beta = 0, tau = 0, lr = 0, lambda_lr = 0, kappa_lr = 0, momentum = 0;
     int max_corrections = 0;
     uint64_t kappa_zero_mask = 0;
+    uint64_t alloc_epoch = 0;   // buffer generation: any reallocation invalidates the graph
     bool operator==(const GraphKey& o) const {
-      return x == o.x && y == o.y && nrows == o.nrows && row0 == o.row0 && beta == o.beta && tau == o.tau &&
+      return alloc_epoch == o.alloc_epoch && x == o.x && y == o.y && nrows == o.nrows && row0 == o.row0 && beta == o.beta && tau == o.tau &&
              lr == o.lr && lambda_lr == o.lambda_lr && kappa_lr == o.kappa_lr && momentum == o.momentum &&
              max_corrections == o.max_corrections && kappa_zero_mask == o.kappa_zero_mask;
     }
@@ -297,6 +300,9 @@ class DecoupledTrainer {
   uint64_t graph_kernels_ = 0;   // kernel nodes of the captured iteration (launch accounting)
   void step_graphed(const float* batch_x, const int32_t* labels, int nrows, int row0, const StepParams& p);
   uint64_t kappa_zero_mask() const;
+  uint64_t alloc_epoch_ = 0;       // bumped whenever a buffer the step reads or writes moves
+  void ensure_momentum();          // velocity buffers, allocated and zeroed synchronously
+  void enable_peer_access();       // in-process multi-device: neighbouring stages read each other
 };
 
 }  // namespace respar::b200

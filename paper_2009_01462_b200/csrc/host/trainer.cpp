@@ -76,19 +76,20 @@ DeviceArray::~DeviceArray() {
   }
 }
 
-void DeviceArray::allocate(int device, int64_t bytes) {
-  if (ptr_ && bytes <= bytes_ && device == device_) return;
+bool DeviceArray::allocate(int device, int64_t bytes) {
+  if (ptr_ && bytes <= bytes_ && device == device_) return false;
   if (ptr_) {
     DeviceGuard g(device_);
     cudaFree(ptr_);
     ptr_ = nullptr;
     bytes_ = 0;
   }
-  if (bytes <= 0) return;
+  if (bytes <= 0) return true;
   DeviceGuard g(device);
   cu(cudaMalloc(&ptr_, static_cast<size_t>(bytes)), "cudaMalloc");
   bytes_ = bytes;
   device_ = device;
+  return true;
 }
 
 void DeviceArray::zero(cudaStream_t s) {
@@ -260,6 +261,7 @@ DecoupledTrainer::DecoupledTrainer(const rp_geometry& g, int stages, TrainMode m
     if (std::find(unique_devices_.begin(), unique_devices_.end(), devices_[k]) == unique_devices_.end())
       unique_devices_.push_back(devices_[k]);
   }
+  if (unique_devices_.size() > 1) enable_peer_access();
   params_.resize(unique_devices_.size());
   grads_.resize(unique_devices_.size());
   mom_.resize(unique_devices_.size());
@@ -406,17 +408,52 @@ void DecoupledTrainer::ensure_capacity(int nrows) {
       st.logits.allocate(st.device, (int64_t)nrows * geo_.classes * 4);
     }
     st.cap_rows = nrows;
+    ++alloc_epoch_;   // the tape / workspace pointers moved
   }
 }
 
 float* DecoupledTrainer::input_staging(int nrows) {
-  in_stage_.allocate(stages_[stage_lo_].device, std::max<int64_t>(1, (int64_t)nrows * raw_feat() * 4));
+  if (in_stage_.allocate(stages_[stage_lo_].device, std::max<int64_t>(1, (int64_t)nrows * raw_feat() * 4)))
+    ++alloc_epoch_;
   return in_stage_.get();
 }
 
 int32_t* DecoupledTrainer::label_staging(int nrows) {
-  lab_stage_.allocate(stages_[stage_hi_ - 1].device, std::max<int64_t>(4, (int64_t)nrows * 4));
+  if (lab_stage_.allocate(stages_[stage_hi_ - 1].device, std::max<int64_t>(4, (int64_t)nrows * 4))) ++alloc_epoch_;
   return lab_stage_.get<int32_t>();
+}
+
+void DecoupledTrainer::ensure_momentum() {
+  for (size_t i = 0; i < unique_devices_.size(); ++i) {
+    if (mom_[i].bytes() != 0) continue;
+    DeviceGuard g(unique_devices_[i]);
+    mom_[i].allocate(unique_devices_[i], param_total_ * 4);
+    cu(cudaMemset(mom_[i].get(), 0, (size_t)param_total_ * 4), "cudaMemset");
+    cu(cudaDeviceSynchronize(), "cudaDeviceSynchronize");
+    ++alloc_epoch_;
+  }
+}
+
+void DecoupledTrainer::enable_peer_access() {
+  // stage k's kernels read lambda / kappa of stage k+1 and the correction of boundary k
+  // reads X^{k-1}_end of stage k-1, so every pair of neighbouring devices needs peer access
+  for (size_t k = 1; k < devices_.size(); ++k) {
+    const int a = devices_[k - 1], b = devices_[k];
+    if (a == b) continue;
+    for (auto [from, to] : {std::pair<int, int>{a, b}, std::pair<int, int>{b, a}}) {
+      int ok = 0;
+      cu(cudaDeviceCanAccessPeer(&ok, from, to), "cudaDeviceCanAccessPeer");
+      if (!ok)
+        throw ConfigError("DecoupledTrainer: devices " + std::to_string(from) + " and " + std::to_string(to) +
+                          " have no peer access; run one process per GPU instead");
+      DeviceGuard g(from);
+      const cudaError_t e = cudaDeviceEnablePeerAccess(to, 0);
+      if (e == cudaErrorPeerAccessAlreadyEnabled)
+        cudaGetLastError();   // clear the non-sticky status
+      else
+        cu(e, "cudaDeviceEnablePeerAccess");
+    }
+  }
 }
 
 void DecoupledTrainer::need_local(int k, const char* where) const {
@@ -591,10 +628,7 @@ void DecoupledTrainer::run_backward(Stage& st, const int32_t* labels, int nrows,
   float* v = nullptr;
   if (momentum != 0.0) {
     const size_t di = dev_index(unique_devices_, st.device);
-    if (mom_[di].bytes() == 0) {
-      mom_[di].allocate(st.device, param_total_ * 4);
-      mom_[di].zero(s);
-    }
+    if (mom_[di].bytes() == 0) throw std::logic_error("stage_backward_update: momentum buffers not allocated");
     v = mom_[di].get() + beg;
   }
   check(rp_op_sgd(P + beg, G + beg, v, end - beg, lr, momentum, s));
@@ -705,6 +739,7 @@ void DecoupledTrainer::step_local(const float* batch_x, const int32_t* labels, i
   check_rows(row0, nrows, "step");
   if (nrows < 1) throw ShapeError("step: empty batch");
   ensure_capacity(nrows);
+  if (p.momentum != 0.0) ensure_momentum();
   ++iteration_;
   sched_->begin();
   // parallel phase: every stage's forward, synthetic/phi backward and update
@@ -764,6 +799,7 @@ void DecoupledTrainer::step_graphed(const float* batch_x, const int32_t* labels,
     return;
   }
   ensure_capacity(nrows);
+  if (p.momentum != 0.0) ensure_momentum();   // before the capture: no allocation inside it
   GraphKey key;
   key.x = batch_x;
   key.y = labels;
@@ -777,6 +813,7 @@ void DecoupledTrainer::step_graphed(const float* batch_x, const int32_t* labels,
   key.momentum = p.momentum;
   key.max_corrections = p.max_corrections;
   key.kappa_zero_mask = kappa_zero_mask();
+  key.alloc_epoch = alloc_epoch_;
   cudaStream_t ctl = sched_->control();
   DeviceGuard g(sched_->control_device());
   if (graph_valid_ && key == graph_key_) {
@@ -918,6 +955,7 @@ void DecoupledTrainer::stage_backward_update(int k, const int32_t* labels, doubl
                                   " needs the (lambda, kappa) snapshot of stage " + std::to_string(k + 1));
     if (st.snap_rows != nrows) throw ShapeError("stage_backward_update: snapshot rows do not match the batch");
   }
+  if (momentum != 0.0) ensure_momentum();
   DeviceGuard g(st.device);
   cudaStream_t s = sched_->stream(k);
   run_backward(st, labels, nrows, row0, beta, lr, momentum, true, s);

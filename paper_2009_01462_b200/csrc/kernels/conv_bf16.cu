@@ -626,12 +626,12 @@ Plan plan_for(const ConvShape& s, bool bin = false) {
 std::mutex g_map_mu;
 std::map<std::tuple<const void*, int, int, int, int, int, int>, CUtensorMap> g_maps;
 
-const CUtensorMap& cached_map(const void* in, const ConvShape& s, int Wp, int rows_h, bool bin = false) {
+CUtensorMap cached_map(const void* in, const ConvShape& s, int Wp, int rows_h, bool bin = false) {
   std::lock_guard<std::mutex> lk(g_map_mu);
   auto key = std::make_tuple(in, s.n, s.h, s.w, s.ci, rows_h, bin ? 1 : 0);
   auto it = g_maps.find(key);
   if (it == g_maps.end()) {
-    if (g_maps.size() > 4096) g_maps.clear();
+    if (g_maps.size() > 4096) g_maps.clear();   // callers hold copies, never references
     it = g_maps.emplace(key, bin ? make_halo_map16(in, s, Wp, rows_h)
                                  : make_halo_map(static_cast<const float*>(in), s, Wp, rows_h)).first;
   }
@@ -709,7 +709,7 @@ void conv_bf16_any(const ConvShape& s, const void* in, bool bin, const float* w_
     return e ? std::atoi(e) : 0;
   }();
   a.dbg = dbg;
-  const CUtensorMap& m = cached_map(in, s, p.Wp, p.rows_h, bin);
+  const CUtensorMap m = cached_map(in, s, p.Wp, p.rows_h, bin);
   const int units = (s.co / 128) * s.n * ((p.T + kS - 1) / kS);
   const int grid = std::min(units, kNumSMs);
   if (bin)

@@ -927,12 +927,12 @@ std::mutex g_map_mu;
 std::map<std::tuple<const void*, int, int, int, int, int, int>, CUtensorMap> g_maps;
 
 // kind: 0 interleaved fp32 halo, 1 raw fp32 [pos][16], 2 bf16 plane pair
-const CUtensorMap& cached_map(const void* in, const ConvShape& s, int Wp, int rows_h, int kind) {
+CUtensorMap cached_map(const void* in, const ConvShape& s, int Wp, int rows_h, int kind) {
   std::lock_guard<std::mutex> lk(g_map_mu);
   auto key = std::make_tuple(in, s.n, s.h, s.w, s.ci, rows_h, kind);
   auto it = g_maps.find(key);
   if (it == g_maps.end()) {
-    if (g_maps.size() > 4096) g_maps.clear();
+    if (g_maps.size() > 4096) g_maps.clear();   // callers hold copies, never references
     const float* f = static_cast<const float*>(in);
     it = g_maps.emplace(key, kind == 2   ? make_planes_map(in, s, Wp, rows_h)
                              : kind == 1 ? make_raw_map(f, s, Wp, rows_h)
@@ -1043,7 +1043,7 @@ void conv3x3_fwd_tc(const ConvShape& s, const float* in, const float* w_hwio, bo
     return e ? std::atoi(e) : 0;
   }();
   a.dbg = dbg;
-  const CUtensorMap& m = mode == MODE_PLANES ? cached_map(in_planes, s, p.Wp, p.rows_h, 2)
+  const CUtensorMap m = mode == MODE_PLANES ? cached_map(in_planes, s, p.Wp, p.rows_h, 2)
                                               : cached_map(in, s, p.Wp, p.rows_h, mode == MODE_X3BF16 ? 1 : 0);
   const int grid = std::min(a.num_tiles, kNumSMs);
   switch (epi) {

@@ -394,12 +394,12 @@ CUtensorMap make_map(const float* t, int n, int h, int w, int c, int rows) {
 std::mutex g_mu;
 std::map<std::tuple<const void*, int, int, int, int, int>, CUtensorMap> g_maps;
 
-const CUtensorMap& cached(const float* t, int n, int h, int w, int c, int rows) {
+CUtensorMap cached(const float* t, int n, int h, int w, int c, int rows) {
   std::lock_guard<std::mutex> lk(g_mu);
   auto key = std::make_tuple((const void*)t, n, h, w, c, rows);
   auto it = g_maps.find(key);
   if (it == g_maps.end()) {
-    if (g_maps.size() > 4096) g_maps.clear();
+    if (g_maps.size() > 4096) g_maps.clear();   // callers hold copies, never references
     it = g_maps.emplace(key, make_map(t, n, h, w, c, rows)).first;
   }
   return it->second;
@@ -484,8 +484,8 @@ void conv3x3_wgrad_bf16(const ConvShape& s, const float* in, const float* g, flo
   a.trace = g_bw_trace;
   a.part = static_cast<float*>(ws);
   a.part_bias = reinterpret_cast<double*>(static_cast<char*>(ws) + part_bytes(p));
-  const CUtensorMap& mg = cached(g, s.n, s.h, s.w, s.co, p.rg);
-  const CUtensorMap& mx = cached(in, s.n, s.h, s.w, s.ci, p.rg + 2);
+  const CUtensorMap mg = cached(g, s.n, s.h, s.w, s.co, p.rg);
+  const CUtensorMap mx = cached(in, s.n, s.h, s.w, s.ci, p.rg + 2);
   ensure_max_dynamic_smem(reinterpret_cast<const void*>(wgrad_bf16_kernel), kMaxSmem);
   wgrad_bf16_kernel<<<p.grid, kThreads, p.smem, st>>>(mg, mx, a);
   RP_LAUNCHED();

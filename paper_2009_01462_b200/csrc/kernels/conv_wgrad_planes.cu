@@ -472,12 +472,12 @@ CUtensorMap make_map(const void* t, int n, int h, int w, int c, int rows) {
 std::mutex g_mu;
 std::map<std::tuple<const void*, int, int, int, int, int>, CUtensorMap> g_maps;
 
-const CUtensorMap& cached(const void* t, int n, int h, int w, int c, int rows) {
+CUtensorMap cached(const void* t, int n, int h, int w, int c, int rows) {
   std::lock_guard<std::mutex> lk(g_mu);
   auto key = std::make_tuple(t, n, h, w, c, rows);
   auto it = g_maps.find(key);
   if (it == g_maps.end()) {
-    if (g_maps.size() > 4096) g_maps.clear();
+    if (g_maps.size() > 4096) g_maps.clear();   // callers hold copies, never references
     it = g_maps.emplace(key, make_map(t, n, h, w, c, rows)).first;
   }
   return it->second;
@@ -516,6 +516,10 @@ PwPlan plan(const ConvShape& s, bool single = false) {
     q.x_slab = (uint32_t)rg * Wp * 128u;   // one filter row's x rows per tap group
     q.x_off = 2 * q.g_slab + kLead;
     q.stage = round1k((uint64_t)q.x_off + 2ull * q.x_slab + kTrail);
+    // the pair epilogue parks kTg 64x64 fp32 partial sums in the drained stage memory: tiny
+    // images (H W <= 4: the dense H = W = 1 case) widen the stage stride to hold them
+    const uint64_t park = (uint64_t)kTg * 64 * 64 * 4;
+    if ((uint64_t)st * q.stage < park) q.stage = round1k((park + st - 1) / st);
     q.smem = st * (size_t)q.stage + (3 * kMaxStages + 2) * 8 + 4 * 128 * 8 + 256;
     if (q.smem > (size_t)kMaxSmem) continue;
     if ((size_t)kTg * 64 * 64 * 4 > st * (size_t)q.stage) continue;   // the pair epilogue's park buffer
@@ -594,13 +598,13 @@ void launch_wgrad_planes(const ConvShape& s, const WgJob* jobs, int njobs, void*
   a.part_bias = reinterpret_cast<double*>(static_cast<char*>(ws) + part_bytes(p, single));
   a.njobs = njobs;
   if (3 * njobs * a.mo * a.mi > p.grid) fail(RP_ERR_INTERNAL, "conv3x3_wgrad_planes: too many work groups");
-  const CUtensorMap* m[2][4];
+  CUtensorMap m[2][4];   // copies taken under the cache lock
   for (int j = 0; j < njobs; ++j) {
     const WgJob& jb = jobs[j];
-    m[j][0] = &cached(jb.g0, s.n, s.h, s.w, s.co, p.rg);
-    m[j][1] = &cached(single ? jb.g0 : jb.g1, s.n, s.h, s.w, s.co, p.rg);
-    m[j][2] = &cached(jb.x0, s.n, s.h, s.w, s.ci, p.rg);
-    m[j][3] = &cached(single ? jb.x0 : jb.x1, s.n, s.h, s.w, s.ci, p.rg);
+    m[j][0] = cached(jb.g0, s.n, s.h, s.w, s.co, p.rg);
+    m[j][1] = cached(single ? jb.g0 : jb.g1, s.n, s.h, s.w, s.co, p.rg);
+    m[j][2] = cached(jb.x0, s.n, s.h, s.w, s.ci, p.rg);
+    m[j][3] = cached(single ? jb.x0 : jb.x1, s.n, s.h, s.w, s.ci, p.rg);
     a.gw[j] = jb.gw;
     a.gb[j] = jb.gb;
     a.scale[j] = (double)jb.scale;
@@ -608,8 +612,8 @@ void launch_wgrad_planes(const ConvShape& s, const WgJob* jobs, int njobs, void*
   if (njobs == 1)
     for (int i = 0; i < 4; ++i) m[1][i] = m[0][i];
   ensure_max_dynamic_smem(reinterpret_cast<const void*>(wgrad_planes_kernel), kMaxSmem);
-  launch_pdl(wgrad_planes_kernel, p.grid, kThreads, p.smem, st, *m[0][0], *m[0][1], *m[0][2], *m[0][3], *m[1][0],
-             *m[1][1], *m[1][2], *m[1][3], a);
+  launch_pdl(wgrad_planes_kernel, p.grid, kThreads, p.smem, st, m[0][0], m[0][1], m[0][2], m[0][3], m[1][0],
+             m[1][1], m[1][2], m[1][3], a);
   const int total = njobs * (9 * s.ci * s.co + s.co);
   launch_pdl(wgrad_planes_reduce_kernel, ceil_div(total, 256), 256, 0, st, (const float*)a.part,
              (const double*)a.part_bias, a, p.grid);

@@ -26,7 +26,8 @@ def f32(a):
     return np.asarray(a, np.float32).astype(np.float64)
 
 
-def trainer_run(name, dims, K, mode, penalty, N, batch, epochs, sp, seed, kappa_init=None, noise=None):
+def trainer_run(name, dims, K, mode, penalty, N, batch, epochs, sp, seed, kappa_init=None, noise=None,
+                lam_perturb=None):
     in_dim, d, h, L, classes = dims
     rng = R.RefRng(seed)
     params = f32(R.make_net(rng, *dims))
@@ -38,7 +39,14 @@ def trainer_run(name, dims, K, mode, penalty, N, batch, epochs, sp, seed, kappa_
         krng = R.RefRng(kappa_init)
         for k in range(1, K):
             tr.set_state(k, 1, f32(krng.uniform(N, d, -0.05, 0.05)))
+    if lam_perturb is not None:
+        # lambda_k off the forward states: every stage's synthetic loss is non-stationary, so
+        # stage 0's gradients are non-zero from the first step
+        prng = R.RefRng(seed + 1000)
+        for k in range(1, K):
+            tr.set_state(k, 0, f32(tr.state(k, 0) + prng.uniform(N, d, -lam_perturb, lam_perturb)))
     kappa0 = [tr.state(k, 1) for k in range(1, K)]
+    lam0 = [tr.state(k, 0) for k in range(1, K)]
     losses = []
     for _ in range(epochs):
         for r0 in range(0, N, batch):
@@ -50,6 +58,8 @@ def trainer_run(name, dims, K, mode, penalty, N, batch, epochs, sp, seed, kappa_
                             sp["max_corrections"]]))
     for k in range(1, K):
         out[f"kappa0_{k}"] = kappa0[k - 1]
+        if lam_perturb is not None:
+            out[f"lam0_{k}"] = lam0[k - 1]
     for k in range(K):
         for w, nm in enumerate(("lam", "kappa", "bout", "badj")):
             v = tr.state(k, w)
@@ -61,12 +71,10 @@ def trainer_run(name, dims, K, mode, penalty, N, batch, epochs, sp, seed, kappa_
     print(name, "losses", out["losses"][:3], "...", "viol", mx)
 
 
-def pieces(name, seed=7):
+def pieces(name, seed=7, dims=(3, 6, 5, 6, 4), K=3, N=9):
     """stage_backward_update gradients for every stage under a frozen snapshot, the
     correction gradient, and one correct_aux / correct_multiplier (decoupled.cpp:65-170)."""
-    dims = (3, 6, 5, 6, 4)
     in_dim, d, h, L, classes = dims
-    K, N = 3, 9
     rng = R.RefRng(seed)
     params = f32(R.make_net(rng, *dims))
     x = f32(rng.uniform(N, in_dim, -1.0, 1.0))
@@ -156,5 +164,14 @@ if __name__ == "__main__":
     trainer_run("ref_k2_linf", (3, 5, 5, 4, 3), 2, 1, 2, 8, 8, 2,
                 dict(beta=2.0, tau=-1.0, lr=0.05, lambda_lr=0.02, kappa_lr=1e-9, max_corrections=1), seed=15)
     pieces("ref_pieces")
+    # d = h = 64: at H = W = 1 these hit the device's tcgen05 plane path (C = hidden = 64), so
+    # reference-held vectors pin the plane kernels, including stage 0 under a perturbed lambda
+    trainer_run("ref_k4_alm_d64", (3, 64, 64, 8, 10), 4, 2, 0, 32, 16, 2,
+                dict(beta=0.5, tau=-1.0, lr=0.05, lambda_lr=0.05, kappa_lr=1e-4, max_corrections=1), seed=21,
+                kappa_init=22, lam_perturb=0.1)
+    trainer_run("ref_k2_penalty_d64", (3, 64, 64, 4, 10), 2, 1, 0, 24, 24, 3,
+                dict(beta=1.0, tau=-1.0, lr=0.05, lambda_lr=0.05, kappa_lr=1e-9, max_corrections=1), seed=23,
+                lam_perturb=0.2)
+    pieces("ref_pieces_d64", seed=24, dims=(3, 64, 64, 6, 10), K=3, N=16)
     serial("ref_serial")
     psi_kats("ref_psi")

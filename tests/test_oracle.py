@@ -15,7 +15,8 @@ from tests.helpers import dense_geometry, load, rel_err
 
 TIGHT = 1e-12
 
-TRAINER_FIXTURES = ["ref_k2_penalty", "ref_k4_alm_minibatch", "ref_k1_alm", "ref_k3_l1_tau", "ref_k2_linf"]
+TRAINER_FIXTURES = ["ref_k2_penalty", "ref_k4_alm_minibatch", "ref_k1_alm", "ref_k3_l1_tau", "ref_k2_linf",
+                    "ref_k4_alm_d64", "ref_k2_penalty_d64"]
 
 
 def run_oracle_fixture(f):
@@ -28,6 +29,8 @@ def run_oracle_fixture(f):
     tr.reset_lambda_from_forward(x)
     for k in range(1, K):
         tr.stage(k).kappa[...] = f[f"kappa0_{k}"].reshape(N, 1, 1, g.channels)
+        if f"lam0_{k}" in f:
+            tr.stage(k).lam[...] = f[f"lam0_{k}"].reshape(N, 1, 1, g.channels)
     beta, tau, lr, llr, klr, mc = f["sp"]
     sp = O.StepParams(beta, tau, lr, llr, klr, int(mc))
     losses = []
@@ -56,8 +59,9 @@ def test_oracle_matches_reference_golden(name):
     assert rel_err(per, f["violation"]) <= 1e-10
 
 
-def test_oracle_pieces_golden():
-    f = load("ref_pieces")
+@pytest.mark.parametrize("name", ["ref_pieces", "ref_pieces_d64"])
+def test_oracle_pieces_golden(name):
+    f = load(name)
     g = dense_geometry(f["dims"])
     K, N = int(f["K"]), int(f["N"])
     net = O.zero_net(g)

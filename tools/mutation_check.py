@@ -1,0 +1,78 @@
+#!/usr/bin/env python
+"""Mutation check of the parity tests: build deliberately broken copies of the library and
+show that the GPU parity tests FAIL against them (a test suite that still passes on a
+broken kernel proves nothing).
+
+    python tools/mutation_check.py build              # here (nvcc cross-compiles), -> tools/_mut/<name>/
+    python tools/mutation_check.py run [tests...]     # on the GPU box: every mutant must fail
+
+Each mutant is one textual change in a copy of paper_2009_01462_b200/csrc; the copy is built
+with the package's own build.py into tools/_mut/<name>/librespar_b200.so (git-ignored, but it
+travels to the GPU box with the snapshot) and the tests load it through RP_LIB_PATH.
+"""
+from __future__ import annotations
+
+import os
+import shutil
+import subprocess
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+OUT = os.path.join(ROOT, "tools", "_mut")
+PKG = "paper_2009_01462_b200"
+
+MUTANTS = {
+    # the low plane of the synthetic upstream (the bf16 pair the first backward conv reads)
+    "p1_plane_zero": ("csrc/kernels/elementwise.cu",
+                      "p1[i] = make_uint2(*reinterpret_cast<const uint32_t*>(&c), *reinterpret_cast<const uint32_t*>(&d));",
+                      "p1[i] = make_uint2(0u, 0u);"),
+    # the multiplier term of the synthetic upstream, one lane of four
+    "kappa_term_sign": ("csrc/kernels/elementwise.cu",
+                        "o.x = -dlam(kind, l.x - xe.x, 0, -1) * w + k4.x;",
+                        "o.x = -dlam(kind, l.x - xe.x, 0, -1) * w - k4.x;"),
+}
+
+DEFAULT_TESTS = ["tests/test_gpu_plane_parity.py"]
+
+
+def build():
+    for name, (rel, old, new) in MUTANTS.items():
+        d = os.path.join(OUT, name)
+        shutil.rmtree(d, ignore_errors=True)
+        shutil.copytree(os.path.join(ROOT, PKG), os.path.join(d, PKG),
+                        ignore=shutil.ignore_patterns("_build", "*.so", "__pycache__"))
+        shutil.copytree(os.path.join(ROOT, "include"), os.path.join(d, "include"))
+        src = os.path.join(d, PKG, rel)
+        text = open(src).read()
+        if text.count(old) != 1:
+            raise SystemExit(f"{name}: pattern not found exactly once in {rel}")
+        open(src, "w").write(text.replace(old, new))
+        r = subprocess.run([sys.executable, os.path.join(d, PKG, "build.py")], capture_output=True, text=True)
+        if r.returncode != 0:
+            raise SystemExit(f"{name}: build failed\n{r.stderr[-3000:]}")
+        lib = os.path.join(d, PKG, "librespar_b200.so")
+        shutil.move(lib, os.path.join(d, "librespar_b200.so"))
+        shutil.rmtree(os.path.join(d, PKG))
+        shutil.rmtree(os.path.join(d, "include"))
+        print(f"built {name}")
+
+
+def run(tests):
+    ok = True
+    for name in MUTANTS:
+        lib = os.path.join(OUT, name, "librespar_b200.so")
+        env = {**os.environ, "RP_LIB_PATH": lib}
+        r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-m", "gpu", "-p", "no:cacheprovider", *tests],
+                           env=env, capture_output=True, text=True, cwd=ROOT)
+        tail = [ln for ln in r.stdout.splitlines() if "passed" in ln or "failed" in ln][-1:]
+        caught = r.returncode != 0
+        ok &= caught
+        print(f"{name}: {'CAUGHT' if caught else 'NOT CAUGHT'} ({tail[0] if tail else r.stdout[-300:]})")
+    return ok
+
+
+if __name__ == "__main__":
+    if len(sys.argv) > 1 and sys.argv[1] == "build":
+        build()
+    else:
+        sys.exit(0 if run(sys.argv[2:] or DEFAULT_TESTS) else 1)

@@ -8,7 +8,7 @@ import ctypes as C, os, sys
 import torch
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 from paper_2009_01462_b200 import _lib
-L = C.CDLL(_lib.LIB_PATH)
+L = C.CDLL(os.path.join(os.path.dirname(os.path.abspath(__file__)), "umma_probe", "librp_probe.so"))  # tools/umma_probe/build.sh
 out = torch.zeros(148, device="cuda")
 for layout in (0, 2):
     for N in (64, 128, 256):

@@ -3,7 +3,7 @@ import ctypes as C, os, sys
 import torch
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 from paper_2009_01462_b200 import _lib
-L = C.CDLL(_lib.LIB_PATH)
+L = C.CDLL(os.path.join(os.path.dirname(os.path.abspath(__file__)), "umma_probe", "librp_probe.so"))  # tools/umma_probe/build.sh
 out = torch.zeros(148, device="cuda")
 for layout, M in ((0, 128), (4, 64)):
     for N in (128, 256):

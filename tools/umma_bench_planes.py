@@ -7,7 +7,7 @@ import ctypes as C, os, sys
 import torch
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 from paper_2009_01462_b200 import _lib
-L = C.CDLL(_lib.LIB_PATH)
+L = C.CDLL(os.path.join(os.path.dirname(os.path.abspath(__file__)), "umma_probe", "librp_probe.so"))  # tools/umma_probe/build.sh
 out = torch.zeros(148, device="cuda")
 for nops, what in ((80, "shifted B, collector"), (81, "aligned B, collector"), (82, "shifted B, no collector")):
     for bmn, data in ((0, "const"), (2, "random")):

@@ -2,7 +2,7 @@ import ctypes as C, os, sys
 import torch
 sys.path.insert(0, "/root/repo")
 from paper_2009_01462_b200 import _lib
-L = C.CDLL(_lib.LIB_PATH)
+L = C.CDLL(os.path.join(os.path.dirname(os.path.abspath(__file__)), "umma_probe", "librp_probe.so"))  # tools/umma_probe/build.sh
 out = torch.zeros(148, device="cuda")
 for chain in (1, 2, 4, 8, 256):
     for bmn in (0, 2):

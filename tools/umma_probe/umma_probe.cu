@@ -1,8 +1,15 @@
-// Diagnostic: one tcgen05.mma (M=128, N=16, K=8, tf32) on known operands in a chosen
+// Diagnostic tool, NOT part of the product library (built separately by
+// tools/umma_probe/build.sh into tools/umma_probe/librp_probe.so).
+// One tcgen05.mma (M=128, N=16, K=8, tf32) on known operands in a chosen
 // shared-memory layout, to pin down UMMA descriptor semantics on the device.  Exposed
 // as rp_debug_umma_probe (tests only; never on the training path).
-#include "../common.cuh"
-#include "umma.cuh"
+#include "common.cuh"
+#include "kernels/umma.cuh"
+
+// standalone: the product library's launch counter is not linked in
+namespace rp {
+__attribute__((weak)) void note_launch() {}
+}
 
 namespace rp::k {
 
@@ -469,14 +476,3 @@ extern "C" int rp_debug_umma_bench(int fmt, int N, int layout, int a_mn, int b_m
   }
 }
 
-namespace rp::k {
-void conv3x3_tc_set_trace(unsigned long long* p);
-void conv3x3_wgrad_tc_set_trace(unsigned long long* p);
-void conv3x3_wgrad_bf16_set_trace(unsigned long long* p);
-}
-extern "C" int rp_debug_set_trace(unsigned long long* p) {
-  rp::k::conv3x3_tc_set_trace(p);
-  rp::k::conv3x3_wgrad_tc_set_trace(p);
-  rp::k::conv3x3_wgrad_bf16_set_trace(p);
-  return 0;
-}
