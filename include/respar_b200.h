@@ -137,10 +137,20 @@ int rp_op_psi_grad(int32_t kind, const float* lam, const float* x, int64_t n, do
  * w = beta/# (kappa_next may be NULL == zero). */
 int rp_op_synthetic_grad(int32_t kind, const float* lam_next, const float* x_end, const float* kappa_next,
                          int64_t n, double w, float* g, void* ws, void* stream);
-/* The same, also writing the bf16 plane pair of g (p0 = bf16(g), p1 = bf16(g - p0); p1 NULL:
- * the bf16 copy alone) for the tape paths, in one pass over the data. */
+/* Plane encodings (the tensor-core operands of the fp32 and bf16 paths):
+ *   plane PAIR  (fp32 math): two fp16 [elements] buffers p0, p1 with v s = p0 + p1,
+ *                p0 = fp16(v s), p1 = fp16(v s - p0) -- 22 significant bits (|v s - p0 - p1|
+ *                <= 2^-24 |v s|) -- and a power-of-two scale s: 2^7 for forward activations
+ *                (the meaning of every NULL scale argument; |v| < 2^8), the cotangent side a
+ *                device scale (a buffer of rp_op_plane_scale_bytes(), the scale at float [0])
+ *                set so max |g s| is in [2^7, 2^8).
+ *   SINGLE plane (bf16 math): p0 = bf16(v). */
+int64_t rp_op_plane_scale_bytes(void);
+/* The same, also writing the planes of g for the tape paths: p1 non-NULL: the fp16 pair of
+ * g s with s computed from max |g| and stored in *scale; p1 NULL: the bf16 single plane. */
 int rp_op_synthetic_grad_planes(int32_t kind, const float* lam_next, const float* x_end, const float* kappa_next,
-                                int64_t n, double w, float* g, void* p0, void* p1, void* ws, void* stream);
+                                int64_t n, double w, float* g, void* p0, void* p1, float* scale, void* ws,
+                                void* stream);
 /* One correct_aux pass and/or correct_multiplier (decoupled.cpp:135-170), fused:
  *   if update_lambda: lam -= eta_l * (w d_lambda psi(lam, x_prev) + p - kappa)
  *   if update_kappa:  kappa -= kappa_coef * (lam - x_prev)   (lam already updated)
@@ -160,26 +170,30 @@ int rp_op_conv3x3(int32_t n, int32_t h, int32_t w, int32_t ci, int32_t co, const
                   int32_t dgrad, const float* bias, const float* aux, double hstep, int32_t epi, float* out,
                   int32_t math, void* ws, int64_t ws_bytes, void* stream);
 int64_t rp_op_conv3x3_workspace_bytes(int32_t ci, int32_t co);
-/* The same conv reading its input as a bf16 plane pair (in_planes = [2][n h w ci]: x = p0 + p1)
- * on the tcgen05 plane mode (Co % 64 == 0, Ci % 16 == 0; ~2^-17 relative); out_planes
- * (optional, [2][n h w co] bf16) receives the plane pair of out. */
+/* The same conv reading its input as an fp16 plane pair (in_planes = [2][n h w ci]:
+ * x in_s = p0 + p1) on the tcgen05 plane mode (Co % 64 == 0, Ci % 16 == 0; fp32-class
+ * accuracy); out_planes (optional, [2][n h w co] fp16) receives the plane pair of out out_s.
+ * in_scale / out_scale: device scalars (NULL = the activation scale 2^7). */
 int rp_op_conv3x3_planes(int32_t n, int32_t h, int32_t w, int32_t ci, int32_t co, const void* in_planes,
                          const float* w_hwio, int32_t dgrad, const float* bias, const float* aux, double hstep,
-                         int32_t epi, float* out, void* out_planes, void* ws, int64_t ws_bytes, void* stream);
+                         int32_t epi, float* out, void* out_planes, const float* in_scale, const float* out_scale,
+                         void* ws, int64_t ws_bytes, void* stream);
 /* Weight gradient of that conv: gw[3][3][ci][co] = scale sum_p in[p+tap][ci] gout[p][co],
  * gb[co] = scale sum_p gout[p][co] (gb may be NULL).  Deterministic. */
 int rp_op_conv3x3_wgrad(int32_t n, int32_t h, int32_t w, int32_t ci, int32_t co, const float* in, const float* gout,
                         double scale, float* gw, float* gb, int32_t math, void* ws, int64_t ws_bytes, void* stream);
 int64_t rp_op_conv3x3_wgrad_workspace_bytes(int32_t n, int32_t h, int32_t w, int32_t ci, int32_t co);
 
-/* bf16 plane pairs of an fp32 tensor: p0 = bf16(v), p1 = bf16(v - p0) (n % 4 == 0). */
-int rp_op_split_planes(const float* in, int64_t n, void* p0, void* p1, void* stream);
-/* (p1 may be NULL: p0 alone is the bf16 copy of in.) */
-/* Weight gradient from plane pairs (x = x0 + x1, gout = g0 + g1; bf16 NHWC planes), Ci and
- * Co multiples of 64: the fp32-accurate (~1e-5) tcgen05 wgrad fed by TMA alone. */
+/* Planes of an fp32 tensor (n % 4 == 0): p1 non-NULL: the fp16 pair of v 2^7 (scale_out NULL) or of
+ * v s with s computed from max |v| and stored in *scale_out (a rp_op_plane_scale_bytes()
+ * buffer); p1 NULL: p0 alone is the bf16 single plane. */
+int rp_op_split_planes(const float* in, int64_t n, void* p0, void* p1, float* scale_out, void* stream);
+/* Weight gradient from fp16 plane pairs (x 2^7 = x0 + x1, gout g_s = g0 + g1 with g_scale the
+ * device scale, NULL = 2^7), Ci and Co multiples of 64: the fp32-accurate tcgen05 wgrad fed by
+ * TMA alone. */
 int rp_op_conv3x3_wgrad_planes(int32_t n, int32_t h, int32_t w, int32_t ci, int32_t co, const void* x0, const void* x1,
-                               const void* g0, const void* g1, double scale, float* gw, float* gb, void* ws,
-                               int64_t ws_bytes, void* stream);
+                               const void* g0, const void* g1, double scale, const float* g_scale, float* gw,
+                               float* gb, void* ws, int64_t ws_bytes, void* stream);
 int64_t rp_op_conv3x3_wgrad_planes_workspace_bytes(int32_t n, int32_t h, int32_t w, int32_t ci, int32_t co);
 
 /* Residual block on nrows samples (network.cpp:82-106), block params at `pb` in the
@@ -192,21 +206,22 @@ int rp_op_block_fwd(const rp_geometry* g, int32_t nrows, const float* x, const f
 int rp_op_block_bwd(const rp_geometry* g, int32_t nrows, const float* x, const float* a, const float* pb,
                     float* g_io, float* dpre, float* gb, int32_t math, void* ws, int64_t ws_bytes,
                     void* stream);
-/* Plane-pair block path (RP_MATH_FP32 only): every conv reads its input as a bf16 plane
- * pair (v = p0 + p1, each a [2][elements] bf16 buffer: p0 then p1) and writes the plane
- * pair of its output (a, x_next, dpre, the updated cotangent) next to the fp32 tensor; both
- * weight gradients run on rp_op_conv3x3_wgrad_planes.  ~1e-5 relative (2^-17 operand
- * splits) where rp_op_block_fwd / _bwd are ~4e-6.
- * x_next_planes may be NULL (a stage's last block).  Backward reads g_planes as the planes
- * of g_io on entry and leaves the planes of the new g_io there. */
+/* Plane-pair block path (RP_MATH_FP32 only): every conv reads its input as an fp16 plane
+ * pair (each a [2][elements] fp16 buffer: p0 then p1) and writes the plane pair of its
+ * output (a, x_next, dpre, the updated cotangent) next to the fp32 tensor; both weight
+ * gradients run on rp_op_conv3x3_wgrad_planes.  fp32-class accuracy (22-bit operands,
+ * fp32 accumulation).  x_next_planes may be NULL (a stage's last block).  Backward reads
+ * g_planes as the planes of g_io g_scale on entry (g_scale: the device scale written by
+ * rp_op_synthetic_grad_planes / rp_op_head_loss_bwd_planes / rp_op_split_planes) and
+ * leaves the planes of the new g_io (same scale) there. */
 int32_t rp_op_block_planes_supported(const rp_geometry* g, int32_t nrows, int32_t math);
 int rp_op_block_fwd_planes(const rp_geometry* g, int32_t nrows, const float* x, const void* x_planes,
                            const float* pb, float* a, float* x_next, void* a_planes, void* x_next_planes,
                            const void* filters, void* ws, int64_t ws_bytes, void* stream);
 int rp_op_block_bwd_planes(const rp_geometry* g, int32_t nrows, const void* x_planes, const float* a,
-                           const void* a_planes, const float* pb, float* g_io, void* g_planes, float* dpre,
-                           void* dpre_planes, float* gb, const void* filters, void* ws, int64_t ws_bytes,
-                           void* stream);
+                           const void* a_planes, const float* pb, float* g_io, void* g_planes, const float* g_scale,
+                           float* dpre, void* dpre_planes, float* gb, const void* filters, void* ws,
+                           int64_t ws_bytes, void* stream);
 /* The plane path's tcgen05 filter operands for nblocks consecutive blocks (pb = the first
  * block's parameters) in one launch: dgrad = 0 the forward filters (W1, W2), 1 the
  * input-gradient filters (W2, W1 flipped and transposed), one pair per block, each pair
@@ -241,8 +256,9 @@ int64_t rp_op_workspace_bytes(const rp_geometry* g, int32_t nrows, int32_t math)
 /* Stem S (affine_forward, network.cpp:108-110 as a 3x3 conv Cin->C). */
 int rp_op_stem_fwd(const rp_geometry* g, int32_t nrows, const float* x_raw, const float* ps, float* x0,
                    int32_t math, void* ws, int64_t ws_bytes, void* stream);
-/* The stem forward writing, in the same pass, the bf16 planes of x0 that rp_op_split_planes
- * makes (p0 = bf16(x0), p1 = bf16(x0 - p0); p1 nullable): the first block's tape input. */
+/* The stem forward writing, in the same pass, the planes of x0 that rp_op_split_planes makes
+ * without a scale argument (p1 non-NULL: the fp16 pair of x0 2^7; NULL: the bf16 single
+ * plane): the first block's tape input. */
 int rp_op_stem_fwd_planes(const rp_geometry* g, int32_t nrows, const float* x_raw, const float* ps, float* x0,
                           void* p0, void* p1, void* stream);
 int rp_op_stem_bwd(const rp_geometry* g, int32_t nrows, const float* x_raw, const float* g0, float* gs,
@@ -257,11 +273,12 @@ int rp_op_head_fwd(const rp_geometry* g, int32_t nrows, const float* x_end, cons
 int rp_op_head_loss_bwd(const rp_geometry* g, int32_t nrows, const float* pooled, const float* logits,
                         const float* pt, const int32_t* labels, double* loss_dev, float* gt, float* g_out,
                         void* ws, int64_t ws_bytes, void* stream);
-/* rp_op_head_loss_bwd also writing the cotangent's bf16 planes (as rp_op_split_planes makes
- * them; p1 nullable) in the broadcast pass: the last stage's first backward conv input. */
+/* rp_op_head_loss_bwd also writing the cotangent's planes (as rp_op_split_planes makes them:
+ * p1 non-NULL the scaled fp16 pair with its scale in *scale, NULL the bf16 single plane): the
+ * last stage's first backward conv input. */
 int rp_op_head_loss_bwd_planes(const rp_geometry* g, int32_t nrows, const float* pooled, const float* logits,
                                const float* pt, const int32_t* labels, double* loss_dev, float* gt, float* g_out,
-                               void* p0, void* p1, void* ws, int64_t ws_bytes, void* stream);
+                               void* p0, void* p1, float* scale, void* ws, int64_t ws_bytes, void* stream);
 /* Argmax hits (accuracy, network.cpp:223-234; ties -> lowest class); *hits host. */
 int rp_op_argmax_hits(const float* logits, const int32_t* labels, int32_t nrows, int32_t classes,
                       int64_t* hits, void* ws, void* stream);

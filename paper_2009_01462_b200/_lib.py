@@ -60,22 +60,25 @@ SIGNATURES = {
     "rp_op_conv3x3_workspace_bytes": (C.c_int64, [C.c_int32, C.c_int32]),
     "rp_op_conv3x3_wgrad": (C.c_int, [C.c_int32] * 5 + [_P, _P, C.c_double, _P, _P, C.c_int32, _P, C.c_int64, _P]),
     "rp_op_conv3x3_wgrad_workspace_bytes": (C.c_int64, [C.c_int32] * 5),
-    "rp_op_split_planes": (C.c_int, [_P, C.c_int64, _P, _P, _P]),
+    "rp_op_split_planes": (C.c_int, [_P, C.c_int64, _P, _P, _P, _P]),
     "rp_op_conv3x3_planes": (C.c_int, [C.c_int32] * 5 + [_P, _P, C.c_int32, _P, _P, C.c_double, C.c_int32, _P, _P,
-                                                         _P, C.c_int64, _P]),
+                                                         _P, _P, _P, C.c_int64, _P]),
     "rp_op_block_planes_supported": (C.c_int32, [_G, C.c_int32, C.c_int32]),
     "rp_op_block_fwd_planes": (C.c_int, [_G, C.c_int32, _P, _P, _P, _P, _P, _P, _P, _P, _P, C.c_int64, _P]),
-    "rp_op_block_bwd_planes": (C.c_int, [_G, C.c_int32, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, C.c_int64, _P]),
+    "rp_op_block_bwd_planes": (C.c_int, [_G, C.c_int32, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, C.c_int64,
+                                         _P]),
     "rp_op_planes_filters_bytes": (C.c_int64, [_G, C.c_int32]),
     "rp_op_block_bf16_tape_supported": (C.c_int32, [_G, C.c_int32, C.c_int32]),
-    "rp_op_synthetic_grad_planes": (C.c_int, [C.c_int32, _P, _P, _P, C.c_int64, C.c_double, _P, _P, _P, _P, _P]),
+    "rp_op_synthetic_grad_planes": (C.c_int, [C.c_int32, _P, _P, _P, C.c_int64, C.c_double, _P, _P, _P, _P, _P,
+                                               _P]),
+    "rp_op_plane_scale_bytes": (C.c_int64, []),
     "rp_op_block_fwd_bf16t": (C.c_int, [_G, C.c_int32, _P, _P, _P, _P, _P, _P, _P, _P, C.c_int64, _P]),
     "rp_op_block_bwd_bf16t": (C.c_int, [_G, C.c_int32, _P, _P, _P, _P, _P, _P, _P, _P, _P, C.c_int64, _P]),
     "rp_op_conv3x3_wgrad_bf16p": (C.c_int, [C.c_int32] * 5 + [_P, _P, C.c_double, _P, _P, _P, C.c_int64, _P]),
     "rp_op_conv3x3_wgrad_bf16p_workspace_bytes": (C.c_int64, [C.c_int32] * 5),
     "rp_op_prep_planes_filters": (C.c_int, [_G, _P, C.c_int32, C.c_int32, _P, _P]),
-    "rp_op_conv3x3_wgrad_planes": (C.c_int, [C.c_int32] * 5 + [_P, _P, _P, _P, C.c_double, _P, _P, _P, C.c_int64,
-                                                                _P]),
+    "rp_op_conv3x3_wgrad_planes": (C.c_int, [C.c_int32] * 5 + [_P, _P, _P, _P, C.c_double, _P, _P, _P, _P,
+                                                                C.c_int64, _P]),
     "rp_op_conv3x3_wgrad_planes_workspace_bytes": (C.c_int64, [C.c_int32] * 5),
     "rp_op_block_fwd": (C.c_int, [_G, C.c_int32, _P, _P, _P, _P, C.c_int32, _P, C.c_int64, _P]),
     "rp_op_block_bwd": (C.c_int, [_G, C.c_int32, _P, _P, _P, _P, _P, _P, C.c_int32, _P, C.c_int64, _P]),
@@ -85,8 +88,8 @@ SIGNATURES = {
     "rp_op_stem_bwd": (C.c_int, [_G, C.c_int32, _P, _P, _P, _P, C.c_int64, _P]),
     "rp_op_head_fwd": (C.c_int, [_G, C.c_int32, _P, _P, _P, _P, _P]),
     "rp_op_head_loss_bwd": (C.c_int, [_G, C.c_int32, _P, _P, _P, _P, _P, _P, _P, _P, C.c_int64, _P]),
-    "rp_op_head_loss_bwd_planes": (C.c_int, [_G, C.c_int32, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, C.c_int64,
-                                             _P]),
+    "rp_op_head_loss_bwd_planes": (C.c_int, [_G, C.c_int32, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P,
+                                             C.c_int64, _P]),
     "rp_op_argmax_hits": (C.c_int, [_P, _P, C.c_int32, C.c_int32, _I64P, _P, _P]),
     "rp_trainer_create": (C.c_int, [_G, C.c_int32, C.c_int32, C.c_int32, C.c_int32, _F, _U64P, C.c_int32,
                                     _I32, C.c_int32, C.POINTER(_P)]),

@@ -78,7 +78,7 @@ int64_t wgrad_ws_bytes(const k::ConvShape& s) {
 }
 
 // The plane-pair block path (fp32 math): every conv of the block on the tcgen05 kernel, whose
-// epilogue also writes the bf16 plane pair (v = p0 + p1) of its output, so both weight
+// epilogue also writes the fp16 plane pair (v s = p0 + p1, planes.cuh) of its output, so both weight
 // gradients run on the TMA-fed plane wgrad (conv_wgrad_planes.cu). RP_WGRAD_PLANES=0 turns
 // it off (the fp32-operand 3xTF32 wgrad then runs).
 bool planes_path(const rp_geometry& g, int nrows, int math) {
@@ -140,13 +140,14 @@ int64_t op_workspace_bytes(const rp_geometry& g, int nrows) {
 // dgrad: `w` is the forward conv's HWIO weight; the conv runs on the cotangent.
 void conv(const k::ConvShape& s, const float* in, const float* w, bool dgrad, const float* bias, const float* aux,
           float h, int epi, float* out, int math, void* wws, int prof_cls, bool aux_read, cudaStream_t st,
-          void* out_planes = nullptr, const void* in_planes = nullptr, const void* wprep = nullptr) {
+          void* out_planes = nullptr, const void* in_planes = nullptr, const void* wprep = nullptr,
+          const float* in_scale = nullptr, const float* out_scale = nullptr) {
   prof::Scope ps(prof_cls, st, conv_flops(s),
                  conv_bytes(s, aux_read) + (out_planes ? 4.0 * s.pixels() * s.co : 0.0) - (out ? 0.0 : 4.0 * s.pixels() * s.co));
   if (out_planes || in_planes) {   // only the fp32 tcgen05 kernel reads / writes plane pairs (planes_path())
     if (math != RP_MATH_FP32 || !k::conv3x3_tc_supported(s)) fail(RP_ERR_INTERNAL, "conv: plane i/o needs fp32 tcgen05");
     k::conv3x3_fwd_tc(s, in, w, dgrad, bias, aux, h, epi, out, fp32_split(), wws, st, out_planes, in_planes,
-                      in_planes ? wprep : nullptr);
+                      in_planes ? wprep : nullptr, in_scale, out_scale);
     return;
   }
   // RP_MATH_BF16: bf16 operands where the bf16 kernel tiles the shape (Co % 128, Ci % 32),
@@ -204,7 +205,8 @@ void block_bwd(const rp_geometry& g, int nrows, const float* x, const float* a, 
        RP_PROF_CONV_DGRAD, true, st);
 }
 
-// Plane-pair variants: a_p / x_next_p / x_p / g_p / dpre_p are bf16 [2][elements] pairs.
+// Plane-pair variants: a_p / x_next_p / x_p / g_p / dpre_p are fp16 [2][elements] pairs
+// (planes.cuh); the cotangent-side pairs g_p / dpre_p carry the stage's scale *gscale.
 // filters (nullable): the block's two prepared plane-mode filters (prep_planes_filters), else
 // each conv prepares its own.
 int64_t planes_filter_bytes(const rp_geometry& g) { return 9LL * g.channels * g.hidden * 2 * 2; }
@@ -236,16 +238,16 @@ void block_fwd_planes(const rp_geometry& g, int nrows, const float* x, const voi
 }
 
 void wgrad_planes(const k::ConvShape& s, const void* xp, const void* gp, float scale, float* gw, float* gb, void* ws,
-                  cudaStream_t st) {
+                  cudaStream_t st, const float* gscale) {
   prof::Scope ps(RP_PROF_CONV_WGRAD, st, conv_flops(s), 4.0 * (double)s.pixels() * (s.ci + s.co));
-  const auto* x0 = static_cast<const uint16_t*>(xp);   // bf16 bits
+  const auto* x0 = static_cast<const uint16_t*>(xp);   // fp16 bits
   const auto* g0 = static_cast<const uint16_t*>(gp);
-  k::conv3x3_wgrad_planes(s, x0, x0 + s.pixels() * s.ci, g0, g0 + s.pixels() * s.co, scale, gw, gb, ws, st);
+  k::conv3x3_wgrad_planes(s, x0, x0 + s.pixels() * s.ci, g0, g0 + s.pixels() * s.co, scale, gw, gb, ws, st, gscale);
 }
 
 void block_bwd_planes(const rp_geometry& g, int nrows, const void* x_p, const float* a, const void* a_p,
-                      const float* pb, float* gio, void* g_p, float* dpre, void* dpre_p, float* gb,
-                      const void* filters, void* ws, int64_t ws_bytes, cudaStream_t st) {
+                      const float* pb, float* gio, void* g_p, const float* gscale, float* dpre, void* dpre_p,
+                      float* gb, const void* filters, void* ws, int64_t ws_bytes, cudaStream_t st) {
   const ParamLayout L = ParamLayout::of(g);
   const int C = g.channels, Ch = g.hidden;
   const bool tanh_act = g.activation == RP_ACT_TANH;
@@ -259,8 +261,9 @@ void block_bwd_planes(const rp_geometry& g, int nrows, const void* x_p, const fl
   const char* f = static_cast<const char*>(filters);
   const int64_t fb = planes_filter_bytes(g);
   (void)dpre;
+  // (the dpre planes keep the cotangent scale: in and out scale are both *gscale)
   conv(shape(g, nrows, C, Ch), gio, pb + L.w2, true, nullptr, a, h, tanh_act ? k::EPI_TANH_BWD : k::EPI_SCALE, nullptr,
-       RP_MATH_FP32, wws, RP_PROF_CONV_DGRAD, tanh_act, st, dpre_p, g_p, f);
+       RP_MATH_FP32, wws, RP_PROF_CONV_DGRAD, tanh_act, st, dpre_p, g_p, f, gscale, gscale);
   if (C == Ch && !std::getenv("RP_WGRAD_UNPAIRED")) {
     // gW1 = x^T dpre, gb1 = sum dpre and gW2 = h a^T g, gb2 = h sum g in ONE launch (same
     // shape): half the launches' prologues, epilogues and reduces   (network.cpp:98-103)
@@ -275,17 +278,18 @@ void block_bwd_planes(const rp_geometry& g, int nrows, const void* x_p, const fl
     const void* ga[2] = {d0, d0 + ne};
     const void* xb[2] = {a0, a0 + ne};
     const void* gb2[2] = {g0, g0 + ne};
-    k::conv3x3_wgrad_planes_pair(sw, xa, ga, 1.f, gb + L.w1, gb + L.b1, xb, gb2, h, gb + L.w2, gb + L.b2, wgws, st);
+    k::conv3x3_wgrad_planes_pair(sw, xa, ga, 1.f, gb + L.w1, gb + L.b1, xb, gb2, h, gb + L.w2, gb + L.b2, wgws, st,
+                                 gscale, gscale);
   } else {
     // gW1 = x^T dpre, gb1 = sum dpre first, while dgrad2's dpre planes are still in L2
     //                                                               (network.cpp:102-103)
-    wgrad_planes(shape(g, nrows, C, Ch), x_p, dpre_p, 1.f, gb + L.w1, gb + L.b1, wgws, st);
+    wgrad_planes(shape(g, nrows, C, Ch), x_p, dpre_p, 1.f, gb + L.w1, gb + L.b1, wgws, st, gscale);
     // gW2 = h a^T g, gb2 = h sum g (before dgrad1 overwrites the g planes) (network.cpp:98-99)
-    wgrad_planes(shape(g, nrows, Ch, C), a_p, g_p, h, gb + L.w2, gb + L.b2, wgws, st);
+    wgrad_planes(shape(g, nrows, Ch, C), a_p, g_p, h, gb + L.w2, gb + L.b2, wgws, st, gscale);
   }
   // g <- g + dpre * W1^T in place, and the planes of the new g   (network.cpp:104)
   conv(shape(g, nrows, Ch, C), dpre, pb + L.w1, true, nullptr, gio, 1.f, k::EPI_ADD, gio, RP_MATH_FP32, wws,
-       RP_PROF_CONV_DGRAD, true, st, g_p, dpre_p, f ? f + fb : nullptr);
+       RP_PROF_CONV_DGRAD, true, st, g_p, dpre_p, f ? f + fb : nullptr, gscale, gscale);
 }
 
 // bf16 tape variants.  Every conv reads its input as a bf16 tensor (TMA straight into the
@@ -392,11 +396,11 @@ void head_fwd(const rp_geometry& g, int nrows, const float* x_end, const float* 
 
 void head_loss_bwd(const rp_geometry& g, int nrows, const float* pooled, const float* logits, const float* pt,
                    const int32_t* labels, double* loss_dev, float* gt, float* g_out, void* ws, int64_t ws_bytes,
-                   cudaStream_t st, void* p0 = nullptr, void* p1 = nullptr) {
+                   cudaStream_t st, void* p0 = nullptr, void* p1 = nullptr, float* scale = nullptr) {
   if (k::head_ws_bytes(nrows, g.channels, g.classes) > ws_bytes) fail(RP_ERR_RANGE, "head: workspace too small");
   prof::Scope scope(RP_PROF_HEAD, st, 0.0, 4.0 * nrows * g.height * g.width * g.channels);
   k::head_loss_backward(nrows, g.height * g.width, g.channels, g.classes, pooled, logits, pt, labels, loss_dev, gt,
-                        gt + (int64_t)g.channels * g.classes, g_out, ws, st, p0, p1);
+                        gt + (int64_t)g.channels * g.classes, g_out, ws, st, p0, p1, scale);
 }
 
 void init_params(const rp_geometry& g, float* params, uint64_t* state, cudaStream_t st) {
@@ -503,14 +507,19 @@ int rp_op_synthetic_grad(int32_t kind, const float* lam_next, const float* x_end
 }
 
 int rp_op_synthetic_grad_planes(int32_t kind, const float* lam_next, const float* x_end, const float* kappa_next,
-                                int64_t n, double w, float* g, void* p0, void* p1, void* ws, void* stream) {
+                                int64_t n, double w, float* g, void* p0, void* p1, float* scale, void* ws,
+                                void* stream) {
   return guard([&] {
     if (kind < 0 || kind > 2) fail(RP_ERR_RANGE, "unknown penalty kind");
     need(p0, "p0");
-    prof::Scope scope(RP_PROF_SYNTHETIC, S(stream), 0.0, (double)n * ((kappa_next ? 16.0 : 12.0) + (p1 ? 4.0 : 2.0)));
-    k::synthetic_grad(kind, lam_next, x_end, kappa_next, n, w, g, ws, S(stream), p0, p1);
+    if (p1) need(scale, "scale");
+    // the pair: + a second read of g for the scaled split
+    prof::Scope scope(RP_PROF_SYNTHETIC, S(stream), 0.0, (double)n * ((kappa_next ? 16.0 : 12.0) + (p1 ? 8.0 : 2.0)));
+    k::synthetic_grad(kind, lam_next, x_end, kappa_next, n, w, g, ws, S(stream), p0, p1, scale);
   });
 }
+
+int64_t rp_op_plane_scale_bytes(void) { return k::plane_scale_bytes(); }
 
 int rp_op_correct(int32_t kind, float* lam, const float* x_prev, const float* p, float* kappa, int64_t n, double w,
                   double eta_l, int32_t update_lambda, double kappa_coef, int32_t update_kappa, void* ws,
@@ -561,7 +570,8 @@ int rp_op_conv3x3_wgrad(int32_t n, int32_t h, int32_t w, int32_t ci, int32_t co,
 
 int rp_op_conv3x3_planes(int32_t n, int32_t h, int32_t w, int32_t ci, int32_t co, const void* in_planes,
                          const float* w_hwio, int32_t dgrad, const float* bias, const float* aux, double hstep,
-                         int32_t epi, float* out, void* out_planes, void* ws, int64_t ws_bytes, void* stream) {
+                         int32_t epi, float* out, void* out_planes, const float* in_scale, const float* out_scale,
+                         void* ws, int64_t ws_bytes, void* stream) {
   return guard([&] {
     if (epi < 0 || epi > 5) fail(RP_ERR_RANGE, "conv3x3_planes: unknown epilogue");
     if (n < 0 || h < 1 || w < 1 || ci < 1 || co < 1) fail(RP_ERR_SHAPE, "conv3x3_planes: bad shape");
@@ -571,7 +581,7 @@ int rp_op_conv3x3_planes(int32_t n, int32_t h, int32_t w, int32_t ci, int32_t co
       fail(RP_ERR_RANGE, "conv3x3_planes: workspace too small");
     if (n > 0) need(in_planes, "in_planes");
     conv(s, nullptr, w_hwio, dgrad != 0, bias, aux, (float)hstep, epi, out, RP_MATH_FP32, ws, RP_PROF_OTHER,
-         aux != nullptr, S(stream), out_planes, in_planes);
+         aux != nullptr, S(stream), out_planes, in_planes, nullptr, in_scale, out_scale);
   });
 }
 
@@ -648,9 +658,9 @@ int rp_op_prep_planes_filters(const rp_geometry* g, const float* pb, int32_t nbl
 }
 
 int rp_op_block_bwd_planes(const rp_geometry* g, int32_t nrows, const void* x_planes, const float* a,
-                           const void* a_planes, const float* pb, float* g_io, void* g_planes, float* dpre,
-                           void* dpre_planes, float* gb, const void* filters, void* ws, int64_t ws_bytes,
-                           void* stream) {
+                           const void* a_planes, const float* pb, float* g_io, void* g_planes, const float* g_scale,
+                           float* dpre, void* dpre_planes, float* gb, const void* filters, void* ws,
+                           int64_t ws_bytes, void* stream) {
   return guard([&] {
     need(g, "geometry");
     if (!planes_path(*g, nrows, RP_MATH_FP32)) fail(RP_ERR_SHAPE, "block_bwd_planes: geometry not on the plane path");
@@ -664,8 +674,8 @@ int rp_op_block_bwd_planes(const rp_geometry* g, int32_t nrows, const void* x_pl
     need(dpre, "dpre");
     need(dpre_planes, "dpre_planes");
     need(gb, "gb");
-    block_bwd_planes(*g, nrows, x_planes, a, a_planes, pb, g_io, g_planes, dpre, dpre_planes, gb, filters, ws,
-                     ws_bytes, S(stream));
+    block_bwd_planes(*g, nrows, x_planes, a, a_planes, pb, g_io, g_planes, g_scale, dpre, dpre_planes, gb, filters,
+                     ws, ws_bytes, S(stream));
   });
 }
 
@@ -727,13 +737,14 @@ int rp_op_conv3x3_wgrad_bf16p(int32_t n, int32_t h, int32_t w, int32_t ci, int32
   });
 }
 
-int rp_op_split_planes(const float* in, int64_t n, void* p0, void* p1, void* stream) {
+int rp_op_split_planes(const float* in, int64_t n, void* p0, void* p1, float* scale_out, void* stream) {
   return guard([&] {
     if (n > 0) {
       need(in, "in");
       need(p0, "p0");
     }
-    k::split_planes(in, n, p0, p1, S(stream));
+    if (scale_out && !p1) fail(RP_ERR_RANGE, "split_planes: a scale needs the plane pair (p1)");
+    k::split_planes(in, n, p0, p1, S(stream), scale_out);
   });
 }
 
@@ -742,8 +753,8 @@ int64_t rp_op_conv3x3_wgrad_planes_workspace_bytes(int32_t n, int32_t h, int32_t
 }
 
 int rp_op_conv3x3_wgrad_planes(int32_t n, int32_t h, int32_t w, int32_t ci, int32_t co, const void* x0, const void* x1,
-                               const void* g0, const void* g1, double scale, float* gw, float* gb, void* ws,
-                               int64_t ws_bytes, void* stream) {
+                               const void* g0, const void* g1, double scale, const float* g_scale, float* gw,
+                               float* gb, void* ws, int64_t ws_bytes, void* stream) {
   return guard([&] {
     const k::ConvShape s{n, h, w, ci, co};
     if (!k::conv3x3_wgrad_planes_supported(s)) fail(RP_ERR_SHAPE, "conv3x3_wgrad_planes: unsupported shape");
@@ -754,7 +765,7 @@ int rp_op_conv3x3_wgrad_planes(int32_t n, int32_t h, int32_t w, int32_t ci, int3
     need(g1, "g1");
     need(gw, "gw");
     prof::Scope ps(RP_PROF_CONV_WGRAD, S(stream), conv_flops(s), 2.0 * (double)s.pixels() * (s.ci + s.co));
-    k::conv3x3_wgrad_planes(s, x0, x1, g0, g1, (float)scale, gw, gb, ws, S(stream));
+    k::conv3x3_wgrad_planes(s, x0, x1, g0, g1, (float)scale, gw, gb, ws, S(stream), g_scale);
   });
 }
 
@@ -811,12 +822,13 @@ int rp_op_head_loss_bwd(const rp_geometry* g, int32_t nrows, const float* pooled
 
 int rp_op_head_loss_bwd_planes(const rp_geometry* g, int32_t nrows, const float* pooled, const float* logits,
                                const float* pt, const int32_t* labels, double* loss_dev, float* gt, float* g_out,
-                               void* p0, void* p1, void* ws, int64_t ws_bytes, void* stream) {
+                               void* p0, void* p1, float* scale, void* ws, int64_t ws_bytes, void* stream) {
   return guard([&] {
     need(g, "geometry");
     validate_geometry(*g);
     need(p0, "p0");
-    head_loss_bwd(*g, nrows, pooled, logits, pt, labels, loss_dev, gt, g_out, ws, ws_bytes, S(stream), p0, p1);
+    if (p1) need(scale, "scale");
+    head_loss_bwd(*g, nrows, pooled, logits, pt, labels, loss_dev, gt, g_out, ws, ws_bytes, S(stream), p0, p1, scale);
   });
 }
 

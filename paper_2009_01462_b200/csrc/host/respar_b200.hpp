@@ -231,6 +231,7 @@ class DecoupledTrainer {
     // inputs x_0..x_{n-1} and of a_0..a_{n-1}; dpre_p / g_p are backward scratch
     std::vector<DeviceArray> xps, aps;
     DeviceArray dpre_p, g_p;
+    DeviceArray gscale;   // plane path: the cotangent planes' power-of-two scale (+ max partials)
     DeviceArray filters;  // plane path: the blocks' prepared filter pairs (forward, then reused for dgrad)
     bool tape_planes = false;
     bool tape_bf16 = false;  // bf16 math: xps / aps / dpre_p / g_p hold single bf16 copies

@@ -401,6 +401,7 @@ void DecoupledTrainer::ensure_capacity(int nrows) {
       st.dpre_p.allocate(st.device, (int64_t)nrows * hid() * eb);
       st.g_p.allocate(st.device, (int64_t)nrows * feat() * eb);
       st.filters.allocate(st.device, std::max<int64_t>(256, rp_op_planes_filters_bytes(&geo_, n)));
+      st.gscale.allocate(st.device, rp_op_plane_scale_bytes());   // the cotangent planes' scale
     }
     st.ws.allocate(st.device, rp_op_workspace_bytes(&geo_, nrows, math_));
     if (k == stages() - 1) {
@@ -493,7 +494,7 @@ void DecoupledTrainer::run_forward(Stage& st, const float* input, int nrows, flo
   st.input0 = cur;
   if (st.tape_bf16) {
     // bf16 copies of every block input and activation for the TMA-fed bf16 wgrad
-    if (!in_planes) check(rp_op_split_planes(cur, (int64_t)nrows * feat(), st.xps[0].get(), nullptr, s));
+    if (!in_planes) check(rp_op_split_planes(cur, (int64_t)nrows * feat(), st.xps[0].get(), nullptr, nullptr, s));
     for (int i = 0; i < n; ++i) {
       const int l = st.begin + i;
       float* out = i == n - 1 ? out_features : st.xs[1 + (i & 1)].get();
@@ -509,7 +510,7 @@ void DecoupledTrainer::run_forward(Stage& st, const float* input, int nrows, flo
   if (st.tape_planes) {
     const int64_t e = (int64_t)nrows * feat();
     auto* p = st.xps[0].get<uint16_t>();
-    if (!in_planes) check(rp_op_split_planes(cur, e, p, p + e, s));
+    if (!in_planes) check(rp_op_split_planes(cur, e, p, p + e, nullptr, s));
     // every block's forward filters in one launch (not one per conv)
     const int64_t fpair = rp_op_planes_filters_bytes(&geo_, 1);
     check(rp_op_prep_planes_filters(&geo_, P + L.block0 + (int64_t)st.begin * L.block_stride, n, 0,
@@ -558,7 +559,7 @@ void DecoupledTrainer::run_backward(Stage& st, const int32_t* labels, int nrows,
     if (tape) {
       check(rp_op_head_loss_bwd_planes(&geo_, nrows, st.pooled.get(), st.logits.get(), P + L.t_w, labels,
                                        st.loss.get<double>(), G + L.t_w, g, gp16, st.tape_bf16 ? nullptr : gp16 + n,
-                                       st.ws.get(), st.ws.bytes(), s));
+                                       st.tape_bf16 ? nullptr : st.gscale.get(), st.ws.get(), st.ws.bytes(), s));
       planes_done = true;
     } else {
       check(rp_op_head_loss_bwd(&geo_, nrows, st.pooled.get(), st.logits.get(), P + L.t_w, labels,
@@ -578,7 +579,8 @@ void DecoupledTrainer::run_backward(Stage& st, const int32_t* labels, int nrows,
     const double w = beta / static_cast<double>(normalizer(nrows, (int)feat()));
     if (tape) {
       check(rp_op_synthetic_grad_planes((int)kind_, lam_next, x_end, kap_next, n, w, g, gp16,
-                                        st.tape_bf16 ? nullptr : gp16 + n, st.red_ws.get(), s));
+                                        st.tape_bf16 ? nullptr : gp16 + n, st.tape_bf16 ? nullptr : st.gscale.get(),
+                                        st.red_ws.get(), s));
       planes_done = true;
     } else {
       check(rp_op_synthetic_grad((int)kind_, lam_next, x_end, kap_next, n, w, g, st.red_ws.get(), s));
@@ -587,7 +589,7 @@ void DecoupledTrainer::run_backward(Stage& st, const int32_t* labels, int nrows,
   const int nb = st.end - st.begin;
   if (st.tape_bf16 && st.fwd_rows == nrows) {
     auto* gp = st.g_p.get<uint16_t>();
-    if (!planes_done) check(rp_op_split_planes(g, n, gp, nullptr, s));
+    if (!planes_done) check(rp_op_split_planes(g, n, gp, nullptr, nullptr, s));
     for (int i = nb - 1; i >= 0; --i) {
       const int l = st.begin + i;
       const int64_t off = L.block0 + (int64_t)l * L.block_stride;
@@ -596,7 +598,7 @@ void DecoupledTrainer::run_backward(Stage& st, const int32_t* labels, int nrows,
     }
   } else if (st.tape_planes && st.fwd_rows == nrows) {
     auto* gp = st.g_p.get<uint16_t>();
-    if (!planes_done) check(rp_op_split_planes(g, n, gp, gp + n, s));
+    if (!planes_done) check(rp_op_split_planes(g, n, gp, gp + n, st.gscale.get(), s));
     // every block's input-gradient filters in one launch, from the current parameters
     const int64_t fpair = rp_op_planes_filters_bytes(&geo_, 1);
     check(rp_op_prep_planes_filters(&geo_, P + L.block0 + (int64_t)st.begin * L.block_stride, nb, 1,
@@ -605,6 +607,7 @@ void DecoupledTrainer::run_backward(Stage& st, const int32_t* labels, int nrows,
       const int l = st.begin + i;
       const int64_t off = L.block0 + (int64_t)l * L.block_stride;
       check(rp_op_block_bwd_planes(&geo_, nrows, st.xps[i].get(), st.as[i].get(), st.aps[i].get(), P + off, g, gp,
+                                   st.gscale.get(),
                                    st.dpre.get(), st.dpre_p.get(), G + off, st.filters.get<char>() + i * fpair,
                                    st.ws.get(), st.ws.bytes(), s));
     }

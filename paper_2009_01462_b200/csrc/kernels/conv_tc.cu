@@ -15,10 +15,12 @@
 //  * D^T = W^T x: the MMA's A operand is the (tiny) weight tile, M = 128 rows = the 64 output
 //    channels stacked twice ([W_hi; W_lo] / [W0; W1]); B is the shifted halo view, N = the
 //    unit's positions (<= 256).  Consecutive MMAs share A through the collector.
-//  * Operand modes.  PLANES (the fp32 default): the input arrives as a bf16 plane pair
-//    x = x0 + x1 written by the producing epilogue and loaded by TMA straight into the MMA
-//    layout; A = [W0; W1], two MMAs per 16 channels accumulate all four products; Co = 64
-//    keeps the whole prepared filter resident in shared memory.  X3TF32 / X3BF16 / TF32 read
+//  * Operand modes.  PLANES (the fp32 default): the input arrives as an fp16 plane pair
+//    x s = x0 + x1 (planes.cuh: 22 significant bits, power-of-two scale s) written by the
+//    producing epilogue and loaded by TMA straight into the MMA layout; A = [W0; W1] (fp16
+//    pair of W 2^8), two kind::f16 MMAs per 16 channels accumulate all four products, the
+//    epilogue divides the scales out; Co = 64 keeps the whole prepared filter resident in
+//    shared memory.  X3TF32 / X3BF16 / TF32 read
 //    the fp32 halo and let converter warps (w2-5) write the low parts.
 //  * operands are K-major "interleaved" (no swizzle): every position is 16 contiguous bytes
 //    per 4 (tf32) or 8 (bf16) channels, so a shift by one position is +16 B of descriptor
@@ -42,6 +44,7 @@
 
 #include "../common.cuh"
 #include "kernels.cuh"
+#include "planes.cuh"
 #include "umma.cuh"
 
 namespace rp::k {
@@ -70,9 +73,9 @@ constexpr int kWResMax = 12;              // resident weight stages (Ci = 64: 4 
 // X3BF16 (the default fp32-accurate path, capi_ops.cu fp32_split) ([W0; W1] x {x0, x1, x2} with bf16 splits: W to
 // 16 significant bits, x to 24; products W0x0 .. W1x2 cover everything above 2^-18 of |W x|,
 // in 3 MMAs of K = 16 per 16 channels instead of 4 of K = 8).
-// MODE_PLANES: the input arrives as a bf16 plane pair (x = x0 + x1, written by the
+// MODE_PLANES: the input arrives as an fp16 plane pair (x s = x0 + x1, written by the
 // producing conv's epilogue): TMA loads both planes straight into the MMA layout (no
-// converters) and [W0; W1] x {x0, x1} is 2 MMAs per 16 channels (~2^-17 relative).
+// converters) and [W0; W1] x {x0, x1} is 2 MMAs per 16 channels (~2^-23 relative).
 enum { MODE_TF32 = 0, MODE_X3TF32 = 1, MODE_X3BF16 = 2, MODE_PLANES = 3 };
 
 struct TcArgs {
@@ -91,8 +94,11 @@ struct TcArgs {
   const float* bias;
   const float* aux;
   float* out;
-  __nv_bfloat16* p0;           // optional bf16 plane pair of out: p0 = bf16(o), p1 = bf16(o - p0)
-  __nv_bfloat16* p1;
+  uint16_t* p0;                // optional fp16 plane pair of out * (*out_scale) (planes.cuh)
+  uint16_t* p1;
+  const float* in_scale;       // PLANES: the input planes' scale (device scalar; null = kActPlaneScale)
+  const float* out_scale;      // the output planes' scale (device scalar; null = kActPlaneScale)
+  float wscale_inv;            // 1 / the prepared filter's scale (PLANES: 2^-8)
   unsigned long long* trace;   // diagnostics (tools/trace_conv.py): per-unit timestamps, null = off
   int dbg;                     // diagnostics (RP_CONV_DBG): 1 no epilogue, 2 no halo TMA, 4 no weight TMA, 8 no MMA
 };
@@ -389,7 +395,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       const int f0 = tile0 * a.tile;
       const int c0 = f0 - (f0 / Wp) * Wp;
       const int nvalid = min(ntiles * a.tile, a.H * Wp - f0);           // frame positions of the unit
-      const uint32_t id_unit = idesc(1, 128, (nvalid + 15) / 16 * 16);  // PLANES: N = 16 .. 256
+      const uint32_t id_unit = idesc(0, 128, (nvalid + 15) / 16 * 16);  // PLANES (fp16 pairs): N = 16 .. 256
       mbar_wait(&acc_empty[ab], aph ^ 1);
       tc_fence_after();
       if (a.trace && blockIdx.x < 2 && lane == 0 && u < 64) a.trace[(blockIdx.x * 64 + u) * 8 + 0] = globaltimer_ns();
@@ -417,7 +423,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           const uint64_t bq = dxq0 + (uint64_t)row;
           const bool first = (c == 0 && dy == 0);
           if (PL) {
-            // 16 channels = one K = 16 step; A = [W0; W1] (bf16), B = planes x0, x1.  One MMA
+            // 16 channels = one K = 16 step; A = [W0; W1] (fp16), B = planes x0, x1.  One MMA
             // spans the unit's frame positions (N = 256 for two tiles; the image's last tile
             // only as far as the frame goes, e.g. 64 of 128 positions at 32x32)
             if (elect_one()) {
@@ -593,6 +599,10 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int prow = gtid >> 4;                           // position prow of each batch
     int* tab = pos_tab + grp * 128;
     const uint32_t grp_bar = 6 + grp;                     // the group (128 threads)
+    // operand scales (planes.cuh): the accumulator carries wscale x in_scale, the output planes
+    // out_scale (device scalars written by earlier kernels: read after pdl_wait)
+    const float acc_mul = a.wscale_inv / (a.in_scale ? *a.in_scale : (MODE == MODE_PLANES ? kActPlaneScale : 1.f));
+    const float out_mul = a.out_scale ? *a.out_scale : kActPlaneScale;
     int ab = 0;
     uint32_t aph = 0;
     UnitIter it(a.Co / 64, a.N, a.T);
@@ -618,8 +628,8 @@ __global__ void __launch_bounds__(kThreads, 1)
         const float* auxb = kAux ? a.aux + img * a.Co + co : nullptr;
         float* outb = a.out ? a.out + img * a.Co + co : nullptr;   // null: the planes alone
         const bool planes = a.p0 != nullptr;
-        __nv_bfloat16* p0b = planes ? a.p0 + img * a.Co + co : nullptr;
-        __nv_bfloat16* p1b = planes ? a.p1 + img * a.Co + co : nullptr;
+        uint16_t* p0b = planes ? a.p0 + img * a.Co + co : nullptr;
+        uint16_t* p1b = planes ? a.p1 + img * a.Co + co : nullptr;
         const int fvalid = min(a.tile, a.H * Wp - (tile0 + grp) * a.tile);   // frame positions of this tile
         const int nb = (fvalid + kEpiB - 1) / kEpiB;                          // batches with frame positions
         float4 ax[128 / 8];                                   // [batch][j]: one float4 per position owned
@@ -650,7 +660,8 @@ __global__ void __launch_bounds__(kThreads, 1)
               if (off < 0) continue;
               const float4 hv = *reinterpret_cast<const float4*>(buf + pr * 64 + 4 * c4);
               const float4 lv = *reinterpret_cast<const float4*>(buf + kEpiB * 64 + pr * 64 + 4 * c4);
-              const float v[4] = {hv.x + lv.x, hv.y + lv.y, hv.z + lv.z, hv.w + lv.w};
+              const float v[4] = {(hv.x + lv.x) * acc_mul, (hv.y + lv.y) * acc_mul, (hv.z + lv.z) * acc_mul,
+                                  (hv.w + lv.w) * acc_mul};
               const float bb[4] = {bias.x, bias.y, bias.z, bias.w};
               const float4 axj = ax[b * kEpiJ + j];
               const float xa[4] = {axj.x, axj.y, axj.z, axj.w};
@@ -665,17 +676,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                 else o[i] = a.h * v[i];
               }
               if (outb) *reinterpret_cast<float4*>(outb + off) = make_float4(o[0], o[1], o[2], o[3]);
-              if (planes) {
-                uint32_t h[2], l[2];
-#pragma unroll
-                for (int i = 0; i < 2; ++i) {
-                  const __nv_bfloat162 hh = __floats2bfloat162_rn(o[2 * i], o[2 * i + 1]);
-                  h[i] = *reinterpret_cast<const uint32_t*>(&hh);
-                  l[i] = pack_bf16x2(o[2 * i] - __low2float(hh), o[2 * i + 1] - __high2float(hh));
-                }
-                *reinterpret_cast<uint2*>(p0b + off) = make_uint2(h[0], h[1]);
-                *reinterpret_cast<uint2*>(p1b + off) = make_uint2(l[0], l[1]);
-              }
+              if (planes) pack_pair4(o, out_mul, *reinterpret_cast<uint2*>(p0b + off), *reinterpret_cast<uint2*>(p1b + off));
             }
           }
         }
@@ -767,14 +768,44 @@ struct FilterPair {
   int flip;
 };
 
+// PLANES filters: the same layout, rows r < 64 W0 = fp16(W 2^8), r >= 64 W1 = fp16(W 2^8 - W0)
+// (planes.cuh: |W| < 2^7)
+__device__ __forceinline__ __half prep_f16x2_elem(const float* __restrict__ w, int ci_src, int co_src, int flip,
+                                                  int64_t idx) {
+  const int Ci = flip ? co_src : ci_src;
+  const int64_t per_cb = 9LL * Ci * 128;
+  const int cb = (int)(idx / per_cb);
+  const int64_t li = idx - cb * per_cb;
+  const int e = (int)(li & 7);
+  const int r = (int)((li >> 3) & 127);
+  const int64_t rest = li >> 10;              // (chunk, tap, kg)
+  const int kg = (int)(rest % 2);
+  const int tap = (int)((rest / 2) % 9);
+  const int chunk = (int)(rest / 18);
+  const int ci = chunk * kChunk + kg * 8 + e;
+  const int co = cb * 64 + (r < 64 ? r : r - 64);
+  const float v = (!flip ? w[((int64_t)tap * ci_src + ci) * co_src + co]
+                         : w[((int64_t)(8 - tap) * ci_src + co) * co_src + ci]) * kWeightPlaneScale;
+  const __half h = __float2half_rn(v);
+  return r < 64 ? h : __float2half_rn(v - __half2float(h));
+}
+
+__global__ void prep_weights_f16x2_kernel(const float* __restrict__ w, int ci_src, int co_src, int flip,
+                                          __half* __restrict__ out) {
+  const int64_t total = 9LL * ci_src * co_src * 2;
+  for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total;
+       idx += (int64_t)gridDim.x * blockDim.x)
+    out[idx] = prep_f16x2_elem(w, ci_src, co_src, flip, idx);
+}
+
 __global__ void prep_filters_planes_kernel(const float* __restrict__ pb, int64_t block_stride, int nblocks,
-                                           const FilterPair fp, int64_t felems, __nv_bfloat16* __restrict__ out) {
+                                           const FilterPair fp, int64_t felems, __half* __restrict__ out) {
   const int64_t total = (int64_t)nblocks * 2 * felems;
   for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total;
        idx += (int64_t)gridDim.x * blockDim.x) {
     const int64_t f = idx / felems;
     const int b = (int)(f >> 1), j = (int)(f & 1);
-    out[idx] = prep_bf16x2_elem(pb + b * block_stride + fp.off[j], fp.ci_src[j], fp.co_src[j], fp.flip, idx - f * felems);
+    out[idx] = prep_f16x2_elem(pb + b * block_stride + fp.off[j], fp.ci_src[j], fp.co_src[j], fp.flip, idx - f * felems);
   }
 }
 
@@ -822,7 +853,7 @@ CUtensorMap make_planes_map(const void* planes, const ConvShape& s, int Wp, int 
                                  (cuuint64_t)s.h * s.w * s.ci * 2};
   const cuuint32_t box[5] = {8, (cuuint32_t)Wp, (cuuint32_t)rows_h, 2, 1};
   const cuuint32_t estr[5] = {1, 1, 1, 1, 1};
-  CUresult r = encode_fn()(&m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 5, const_cast<void*>(planes), dims, strides, box,
+  CUresult r = encode_fn()(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 5, const_cast<void*>(planes), dims, strides, box,
                            estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
                            CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) fail(RP_ERR_CUDA, "cuTensorMapEncodeTiled failed (" + std::to_string((int)r) + ")");
@@ -978,14 +1009,14 @@ void prep_filters_planes(const float* pb, int64_t block_stride, int nblocks, con
   if (9LL * ci_src[1] * co_src[1] * 2 != felems) fail(RP_ERR_INTERNAL, "prep_filters_planes: filter sizes differ");
   const int64_t total = (int64_t)nblocks * 2 * felems;
   const int grid = (int)std::min<int64_t>(ceil_div(total, 256), 16 * kNumSMs);
-  prep_filters_planes_kernel<<<grid, 256, 0, st>>>(pb, block_stride, nblocks, fp, felems,
-                                                   static_cast<__nv_bfloat16*>(out));
+  prep_filters_planes_kernel<<<grid, 256, 0, st>>>(pb, block_stride, nblocks, fp, felems, static_cast<__half*>(out));
   RP_LAUNCHED();
 }
 
 void conv3x3_fwd_tc(const ConvShape& s, const float* in, const float* w_hwio, bool dgrad_weights, const float* bias,
                     const float* aux, float h, int epi, float* out, int mode, void* ws, cudaStream_t st,
-                    void* out_planes, const void* in_planes, const void* wprep) {
+                    void* out_planes, const void* in_planes, const void* wprep, const float* in_scale,
+                    const float* out_scale) {
   if (s.pixels() == 0) return;
   if (in_planes) mode = MODE_PLANES;
   const Plan p = plan_for(s, mode);
@@ -999,7 +1030,11 @@ void conv3x3_fwd_tc(const ConvShape& s, const float* in, const float* w_hwio, bo
   if (wprep && mode != MODE_PLANES) fail(RP_ERR_INTERNAL, "conv3x3_fwd_tc: prepared filters are plane-mode only");
   if (wprep) {
     // prepared by prep_filters_planes for the whole stage
-  } else if (mode == MODE_X3BF16 || mode == MODE_PLANES) {
+  } else if (mode == MODE_PLANES) {
+    prep_weights_f16x2_kernel<<<pgrid, 256, 0, st>>>(w_hwio, ci_src, co_src, dgrad_weights ? 1 : 0,
+                                                     static_cast<__half*>(ws));
+    RP_LAUNCHED();
+  } else if (mode == MODE_X3BF16) {
     prep_weights_bf16x2_kernel<<<pgrid, 256, 0, st>>>(w_hwio, ci_src, co_src, dgrad_weights ? 1 : 0,
                                                       static_cast<__nv_bfloat16*>(ws));
     RP_LAUNCHED();
@@ -1035,8 +1070,12 @@ void conv3x3_fwd_tc(const ConvShape& s, const float* in, const float* w_hwio, bo
   a.bias = bias;
   a.aux = aux;
   a.out = out;
-  a.p0 = static_cast<__nv_bfloat16*>(out_planes);
+  a.p0 = static_cast<uint16_t*>(out_planes);
   a.p1 = out_planes ? a.p0 + s.pixels() * s.co : nullptr;
+  if (in_scale && mode != MODE_PLANES) fail(RP_ERR_INTERNAL, "conv3x3_fwd_tc: an input scale needs plane input");
+  a.in_scale = in_scale;
+  a.out_scale = out_scale;
+  a.wscale_inv = mode == MODE_PLANES ? kWeightPlaneScaleInv : 1.f;
   a.trace = g_trace;
   static const int dbg = [] {
     const char* e = std::getenv("RP_CONV_DBG");

@@ -1,12 +1,13 @@
-// tcgen05 weight gradient from bf16 *plane pairs* (fp32-accurate path, RP_MATH_FP32):
+// tcgen05 weight gradient from fp16 *plane pairs* (fp32-accurate path, RP_MATH_FP32):
 //
 //   gW[tap][ci][co] = scale * sum_p x[p + off(tap)][ci] * g[p][co],  gb[co] = scale * sum_p g[p][co]
 //
-// with x = x0 + x1 and g = g0 + g1, x0 = bf16(x), x1 = bf16(x - x0) (16 significant bits; the
-// producing epilogues write the planes next to the fp32 tensor).  Operands go from HBM to the
+// with x = x0 + x1 and g s = g0 + g1, x0 = fp16(x), x1 = fp16(x - x0) (22 significant bits,
+// planes.cuh; the producing epilogues write the planes next to the fp32 tensor, the cotangent
+// side with its power-of-two scale s, divided out in the reduce).  Operands go from HBM to the
 // MMA by TMA alone -- no fp32 staging, no converter pass -- which is what bounded the fp32
 // wgrad kernels (conv_wgrad_tc.cu, conv_wgrad_bf16.cu: three shared-memory passes per block):
-//   A = [g0 ; g1]  (M = 128 for a 64-channel co block, MN-major bf16, 128B swizzle)
+//   A = [g0 ; g1]  (M = 128 for a 64-channel co block, MN-major fp16, 128B swizzle)
 //   B = [x0 ; x1]  (N = 128 for a 64-channel ci block)
 // one M128 x N128 x K16 MMA per (16 positions, tap) yields g0x0 + g1x0 + g0x1 + g1x1 in the
 // four quadrants of D (everything above 2^-17 |g x|); the epilogue adds the quadrants.
@@ -30,6 +31,7 @@
 
 #include "../common.cuh"
 #include "kernels.cuh"
+#include "planes.cuh"
 #include "umma.cuh"
 
 namespace rp::k {
@@ -62,6 +64,7 @@ struct PwArgs {
   float* gw[2];                  // reduce: per-job outputs and scales
   float* gb[2];
   double scale[2];
+  const float* gsc[2];           // the A (g-side) planes' power-of-two scale (device; null: kActPlaneScale)
 };
 
 __device__ __forceinline__ int grp_start(int gid, int grid, const PwArgs& a) {
@@ -206,7 +209,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
   } else if (warp == 1) {
     // ===================== MMA issuer =====================
-    const uint32_t id = idesc(1, 128, 128, 1, 1);
+    const uint32_t id = idesc(a.single ? 1 : 0, 128, 128, 1, 1);   // single: bf16; pair: fp16
     const int ksteps = a.Pp / 16;
     uint64_t boff[kTg];
 #pragma unroll
@@ -262,9 +265,9 @@ __global__ void __launch_bounds__(kThreads, 1)
           const int ph0 = (int)(((base0 >> 7) + p) & 7), ph1 = (int)(((base1 >> 7) + p) & 7);
           const uint4 u = *reinterpret_cast<const uint4*>(p0 + (size_t)p * 128 + ((cq ^ ph0) << 4));
           const uint4 v = *reinterpret_cast<const uint4*>(p1 + (size_t)p * 128 + ((cq ^ ph1) << 4));
-          const __nv_bfloat162* uh = reinterpret_cast<const __nv_bfloat162*>(&u);
-          const __nv_bfloat162* vh = reinterpret_cast<const __nv_bfloat162*>(&v);
           if (single) {
+            const __nv_bfloat162* uh = reinterpret_cast<const __nv_bfloat162*>(&u);
+            const __nv_bfloat162* vh = reinterpret_cast<const __nv_bfloat162*>(&v);
 #pragma unroll
             for (int e = 0; e < 4; ++e) {
               bf[2 * e] += __low2float(uh[e]);
@@ -273,6 +276,8 @@ __global__ void __launch_bounds__(kThreads, 1)
               bf[8 + 2 * e + 1] += __high2float(vh[e]);
             }
           } else {
+            const __half2* uh = reinterpret_cast<const __half2*>(&u);
+            const __half2* vh = reinterpret_cast<const __half2*>(&v);
 #pragma unroll
             for (int e = 0; e < 4; ++e) {
               bf[2 * e] += __low2float(uh[e]) + __low2float(vh[e]);
@@ -391,7 +396,11 @@ __global__ void wgrad_planes_reduce_kernel(const float* __restrict__ part, const
     const int gbase = job * 3 * a.mo * a.mi;
     float* gw = a.gw[job];
     float* gb = a.gb[job];
-    const double scale = a.scale[job];
+    // pairs: the g side carries *gsc (null: the activation scale), the x side the activation
+    // scale; the bias sums are of the g side alone
+    const double gs = a.single ? 1.0 : (a.gsc[job] ? (double)*a.gsc[job] : (double)kActPlaneScale);
+    const double scale = a.scale[job] / (a.single ? 1.0 : gs * (double)kActPlaneScale);
+    const double bscale = a.scale[job] / gs;
     if (idx < total) {
       const int co = idx % Co;
       const int ci = (idx / Co) % Ci;
@@ -418,21 +427,63 @@ __global__ void wgrad_planes_reduce_kernel(const float* __restrict__ part, const
       const int c_lo = grp_start(gid, grid, a), c_hi = grp_start(gid + 1, grid, a);
       double s = 0.0;
       for (int b = c_lo; b < c_hi; ++b) s += part_bias[(int64_t)b * cbk + (co - cob * cbk)];
-      gb[co] = (float)(scale * s);
+      gb[co] = (float)(bscale * s);
     }
   }
 }
 
-// fp32 -> (bf16(v), bf16(v - bf16(v))) planes, for tensors not written by a conv epilogue
+// fp32 -> planes (planes.cuh) for tensors not written by a conv epilogue: p1 non-null: the
+// fp16 pair of v s (s = *scale, or the activation scale); p1 null: the bf16 single plane
 __global__ void split_planes_kernel(const float4* __restrict__ in, int64_t n4, uint2* __restrict__ p0,
-                                    uint2* __restrict__ p1) {
+                                    uint2* __restrict__ p1, const float* __restrict__ scale) {
+  const float sc = scale ? *scale : kActPlaneScale;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n4; i += (int64_t)gridDim.x * blockDim.x) {
     const float4 v = in[i];
-    const __nv_bfloat162 a = __floats2bfloat162_rn(v.x, v.y), b = __floats2bfloat162_rn(v.z, v.w);
-    const __nv_bfloat162 c = __floats2bfloat162_rn(v.x - __low2float(a), v.y - __high2float(a));
-    const __nv_bfloat162 d = __floats2bfloat162_rn(v.z - __low2float(b), v.w - __high2float(b));
-    p0[i] = make_uint2(*reinterpret_cast<const uint32_t*>(&a), *reinterpret_cast<const uint32_t*>(&b));
-    if (p1) p1[i] = make_uint2(*reinterpret_cast<const uint32_t*>(&c), *reinterpret_cast<const uint32_t*>(&d));
+    const float vv[4] = {v.x, v.y, v.z, v.w};
+    if (p1)
+      pack_pair4(vv, sc, p0[i], p1[i]);
+    else
+      p0[i] = pack_single4(vv);
+  }
+}
+
+// per-CTA max |v| (exact, order-independent: deterministic)
+__global__ void absmax_partial_kernel(const float4* __restrict__ in, int64_t n4, float* __restrict__ part) {
+  __shared__ float sh[8];
+  float m = 0.f;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n4; i += (int64_t)gridDim.x * blockDim.x) {
+    const float4 v = in[i];
+    m = fmaxf(m, fmaxf(fmaxf(fabsf(v.x), fabsf(v.y)), fmaxf(fabsf(v.z), fabsf(v.w))));
+  }
+  for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+  if ((threadIdx.x & 31) == 0) sh[threadIdx.x >> 5] = m;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int w = 1; w < (int)(blockDim.x >> 5); ++w) m = fmaxf(m, sh[w]);
+    part[blockIdx.x] = fmaxf(m, sh[0]);
+  }
+}
+
+// the scale of a cotangent plane pair from the max partials, computed by every CTA (CTA 0 stores it)
+__global__ void split_planes_scaled_kernel(const float4* __restrict__ in, int64_t n4, uint2* __restrict__ p0,
+                                           uint2* __restrict__ p1, const float* __restrict__ part, int nparts,
+                                           float* __restrict__ scale_out) {
+  __shared__ float sh_s;
+  if (threadIdx.x < 32) {
+    float m = 0.f;
+    for (int i = threadIdx.x; i < nparts; i += 32) m = fmaxf(m, part[i]);
+    for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+    if (threadIdx.x == 0) {
+      sh_s = cotangent_plane_scale(m);
+      if (blockIdx.x == 0) *scale_out = sh_s;
+    }
+  }
+  __syncthreads();
+  const float sc = sh_s;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n4; i += (int64_t)gridDim.x * blockDim.x) {
+    const float4 v = in[i];
+    const float vv[4] = {v.x, v.y, v.z, v.w};
+    pack_pair4(vv, sc, p0[i], p1[i]);
   }
 }
 
@@ -545,13 +596,37 @@ int64_t conv3x3_wgrad_planes_ws_bytes(const ConvShape& s) {
   return part_bytes(p) + (int64_t)p.grid * 64 * 8 + 256;
 }
 
-void split_planes(const float* in, int64_t n, void* p0, void* p1, cudaStream_t st) {
+void split_planes(const float* in, int64_t n, void* p0, void* p1, cudaStream_t st, float* scale_out) {
   if (n <= 0) return;
   if (n % 4) fail(RP_ERR_SHAPE, "split_planes: element count must be a multiple of 4");
   const int64_t n4 = n / 4;
   const int grid = (int)std::min<int64_t>((n4 + 255) / 256, 16 * kNumSMs);
+  if (scale_out) {
+    if (!p1) fail(RP_ERR_INTERNAL, "split_planes: a scale needs the fp16 pair");
+    // [0]: the scale, [kPlaneScalePartOffset ..]: per-CTA max |v|
+    float* part = scale_out + kPlaneScalePartOffset;
+    const int pgrid = (int)std::min<int64_t>((n4 + 255) / 256, kPlaneScaleMaxParts);
+    absmax_partial_kernel<<<pgrid, 256, 0, st>>>(reinterpret_cast<const float4*>(in), n4, part);
+    RP_LAUNCHED();
+    split_planes_scaled_kernel<<<grid, 256, 0, st>>>(reinterpret_cast<const float4*>(in), n4, static_cast<uint2*>(p0),
+                                                     static_cast<uint2*>(p1), part, pgrid, scale_out);
+    RP_LAUNCHED();
+    return;
+  }
   split_planes_kernel<<<grid, 256, 0, st>>>(reinterpret_cast<const float4*>(in), n4, static_cast<uint2*>(p0),
-                                           static_cast<uint2*>(p1));
+                                           static_cast<uint2*>(p1), nullptr);
+  RP_LAUNCHED();
+}
+
+void split_planes_from_parts(const float* in, int64_t n, void* p0, void* p1, const float* part, int nparts,
+                             float* scale_out, cudaStream_t st) {
+  if (n <= 0) return;
+  if (n % 4) fail(RP_ERR_SHAPE, "split_planes: element count must be a multiple of 4");
+  if (nparts > 2 * kPlaneScaleMaxParts) fail(RP_ERR_INTERNAL, "split_planes: too many max partials");
+  const int64_t n4 = n / 4;
+  const int grid = (int)std::min<int64_t>((n4 + 255) / 256, 16 * kNumSMs);
+  split_planes_scaled_kernel<<<grid, 256, 0, st>>>(reinterpret_cast<const float4*>(in), n4, static_cast<uint2*>(p0),
+                                                   static_cast<uint2*>(p1), part, nparts, scale_out);
   RP_LAUNCHED();
 }
 
@@ -561,6 +636,7 @@ struct WgJob {
   float scale;
   float* gw;
   float* gb;
+  const float* gsc;   // the g planes' scale (device; null: 1)
 };
 
 void launch_wgrad_planes(const ConvShape& s, const WgJob* jobs, int njobs, void* ws, cudaStream_t st, bool single) {
@@ -608,6 +684,7 @@ void launch_wgrad_planes(const ConvShape& s, const WgJob* jobs, int njobs, void*
     a.gw[j] = jb.gw;
     a.gb[j] = jb.gb;
     a.scale[j] = (double)jb.scale;
+    a.gsc[j] = jb.gsc;
   }
   if (njobs == 1)
     for (int i = 0; i < 4; ++i) m[1][i] = m[0][i];
@@ -621,15 +698,17 @@ void launch_wgrad_planes(const ConvShape& s, const WgJob* jobs, int njobs, void*
 }  // namespace
 
 void conv3x3_wgrad_planes(const ConvShape& s, const void* x0, const void* x1, const void* g0, const void* g1,
-                          float scale, float* gw, float* gb, void* ws, cudaStream_t st) {
-  const WgJob j{x0, x1, g0, g1, scale, gw, gb};
+                          float scale, float* gw, float* gb, void* ws, cudaStream_t st, const float* gscale) {
+  const WgJob j{x0, x1, g0, g1, scale, gw, gb, gscale};
   launch_wgrad_planes(s, &j, 1, ws, st, false);
 }
 
 void conv3x3_wgrad_planes_pair(const ConvShape& s, const void* const xa[2], const void* const ga[2], float scale_a,
                                float* gwa, float* gba, const void* const xb[2], const void* const gb2[2],
-                               float scale_b, float* gwb, float* gbb, void* ws, cudaStream_t st) {
-  const WgJob j[2] = {{xa[0], xa[1], ga[0], ga[1], scale_a, gwa, gba}, {xb[0], xb[1], gb2[0], gb2[1], scale_b, gwb, gbb}};
+                               float scale_b, float* gwb, float* gbb, void* ws, cudaStream_t st, const float* gsc_a,
+                               const float* gsc_b) {
+  const WgJob j[2] = {{xa[0], xa[1], ga[0], ga[1], scale_a, gwa, gba, gsc_a},
+                      {xb[0], xb[1], gb2[0], gb2[1], scale_b, gwb, gbb, gsc_b}};
   launch_wgrad_planes(s, j, 2, ws, st, false);
 }
 
@@ -643,7 +722,7 @@ int64_t conv3x3_wgrad_bf16p_ws_bytes(const ConvShape& s) {
 
 void conv3x3_wgrad_bf16p(const ConvShape& s, const void* x, const void* g, float scale, float* gw, float* gb,
                          void* ws, cudaStream_t st) {
-  const WgJob j{x, nullptr, g, nullptr, scale, gw, gb};
+  const WgJob j{x, nullptr, g, nullptr, scale, gw, gb, nullptr};
   launch_wgrad_planes(s, &j, 1, ws, st, true);
 }
 
@@ -655,7 +734,8 @@ bool conv3x3_wgrad_bf16p_pair_supported(const ConvShape& s) {
 void conv3x3_wgrad_bf16p_pair(const ConvShape& s, const void* xa, const void* ga, float scale_a, float* gwa,
                               float* gba, const void* xb, const void* gb2, float scale_b, float* gwb, float* gbb,
                               void* ws, cudaStream_t st) {
-  const WgJob j[2] = {{xa, nullptr, ga, nullptr, scale_a, gwa, gba}, {xb, nullptr, gb2, nullptr, scale_b, gwb, gbb}};
+  const WgJob j[2] = {{xa, nullptr, ga, nullptr, scale_a, gwa, gba, nullptr},
+                      {xb, nullptr, gb2, nullptr, scale_b, gwb, gbb, nullptr}};
   launch_wgrad_planes(s, j, 2, ws, st, true);
 }
 

@@ -11,6 +11,7 @@
 
 #include "../common.cuh"
 #include "kernels.cuh"
+#include "planes.cuh"
 
 namespace rp::k {
 
@@ -137,11 +138,12 @@ __device__ __forceinline__ float dlam(int kind, float d, int64_t i, long long ar
 }
 
 // g = w * d_x + kappa,  d_x = -d_lambda   (decoupled.cpp:105-110)
-// p0 / p1 (optional): the bf16 plane pair of g (p0 = bf16(g), p1 = bf16(g - p0); p1 null: the
-// bf16 copy alone) for the tape paths' first backward conv, written in the same pass
+// p0 (p1 null, optional): the bf16 single plane of g for the bf16 tape path, same pass.
+// bmax (optional): per-CTA max |g| (the plane-pair scale is formed from these afterwards).
 __global__ void synthetic_grad_vec4(int kind, const float4* __restrict__ lam, const float4* __restrict__ x,
                                     const float4* __restrict__ kap, int64_t n4, float w, float4* __restrict__ g,
-                                    uint2* __restrict__ p0, uint2* __restrict__ p1) {
+                                    uint2* __restrict__ p0, float* __restrict__ bmax) {
+  float m = 0.f;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n4; i += (int64_t)gridDim.x * blockDim.x) {
     const float4 l = lam[i], xe = x[i];
     float4 k4 = kap ? kap[i] : make_float4(0.f, 0.f, 0.f, 0.f);
@@ -151,14 +153,20 @@ __global__ void synthetic_grad_vec4(int kind, const float4* __restrict__ lam, co
     o.z = -dlam(kind, l.z - xe.z, 0, -1) * w + k4.z;
     o.w = -dlam(kind, l.w - xe.w, 0, -1) * w + k4.w;
     g[i] = o;
+    m = fmaxf(m, fmaxf(fmaxf(fabsf(o.x), fabsf(o.y)), fmaxf(fabsf(o.z), fabsf(o.w))));
     if (p0) {
-      const __nv_bfloat162 a = __floats2bfloat162_rn(o.x, o.y), b = __floats2bfloat162_rn(o.z, o.w);
-      p0[i] = make_uint2(*reinterpret_cast<const uint32_t*>(&a), *reinterpret_cast<const uint32_t*>(&b));
-      if (p1) {
-        const __nv_bfloat162 c = __floats2bfloat162_rn(o.x - __low2float(a), o.y - __high2float(a));
-        const __nv_bfloat162 d = __floats2bfloat162_rn(o.z - __low2float(b), o.w - __high2float(b));
-        p1[i] = make_uint2(*reinterpret_cast<const uint32_t*>(&c), *reinterpret_cast<const uint32_t*>(&d));
-      }
+      const float v[4] = {o.x, o.y, o.z, o.w};
+      p0[i] = pack_single4(v);
+    }
+  }
+  if (bmax) {
+    __shared__ float sh[kThreads / 32];
+    for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+    if ((threadIdx.x & 31) == 0) sh[threadIdx.x >> 5] = m;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      for (int wi = 1; wi < kThreads / 32; ++wi) m = fmaxf(m, sh[wi]);
+      bmax[blockIdx.x] = fmaxf(m, sh[0]);
     }
   }
 }
@@ -304,21 +312,25 @@ void psi_grad(int kind, const float* lam, const float* x, int64_t n, double scal
 }
 
 void synthetic_grad(int kind, const float* lam_next, const float* x_end, const float* kappa, int64_t n, double w,
-                    float* g, void* ws, cudaStream_t s, void* p0, void* p1) {
+                    float* g, void* ws, cudaStream_t s, void* p0, void* p1, float* scale) {
   if (n <= 0) return;
+  if (p1 && !scale) fail(RP_ERR_INTERNAL, "synthetic_grad: the cotangent plane pair needs a scale buffer");
   if (kind != RP_PSI_LINF && n % 4 == 0 && aligned16(lam_next) && aligned16(x_end) && aligned16(g) &&
       (!kappa || aligned16(kappa)) && (!p0 || aligned16(p0)) && (!p1 || aligned16(p1))) {
-    synthetic_grad_vec4<<<grid_for(n / 4), kThreads, 0, s>>>(
+    const int grid = grid_for(n / 4);
+    float* part = p1 ? scale + kPlaneScalePartOffset : nullptr;   // grid <= 8 x 148 partials
+    synthetic_grad_vec4<<<grid, kThreads, 0, s>>>(
         kind, reinterpret_cast<const float4*>(lam_next), reinterpret_cast<const float4*>(x_end),
         reinterpret_cast<const float4*>(kappa), n / 4, (float)w, reinterpret_cast<float4*>(g),
-        static_cast<uint2*>(p0), static_cast<uint2*>(p1));
+        p1 ? nullptr : static_cast<uint2*>(p0), part);
     RP_LAUNCHED();
+    if (p1) split_planes_from_parts(g, n, p0, p1, part, grid, scale, s);
     return;
   }
   const ArgMax* am = kind == RP_PSI_LINF ? linf_argmax(lam_next, x_end, n, ws, s) : nullptr;
   synthetic_grad_scalar<<<grid_for(n), kThreads, 0, s>>>(kind, lam_next, x_end, kappa, n, (float)w, am, g);
   RP_LAUNCHED();
-  if (p0) split_planes(g, n, p0, p1, s);   // the planes in a second pass (LInf / unaligned)
+  if (p0) split_planes(g, n, p0, p1, s, p1 ? scale : nullptr);   // the planes in a second pass (LInf / unaligned)
 }
 
 void correct(int kind, float* lam, const float* x_prev, const float* p, float* kappa, int64_t n, double w,

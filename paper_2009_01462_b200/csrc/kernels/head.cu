@@ -6,6 +6,7 @@
 
 #include "../common.cuh"
 #include "kernels.cuh"
+#include "planes.cuh"
 
 namespace rp::k {
 
@@ -160,10 +161,12 @@ __global__ void broadcast_kernel(const float* __restrict__ gpool, int64_t hw, in
   }
 }
 
-// p0 / p1 (nullable): the cotangent's bf16 planes as split_planes makes them, same pass
+// p0 (nullable): the cotangent's bf16 single plane (bf16 tape path), same pass; bmax (nullable):
+// per-CTA max |g| for the fp16 pair's scale (planes.cuh), split afterwards
 __global__ void broadcast_kernel_vec4(const float* __restrict__ gpool, int64_t hw, int C, int64_t total4,
                                       float inv_hw, float4* __restrict__ g, uint2* __restrict__ p0,
-                                      uint2* __restrict__ p1) {
+                                      float* __restrict__ bmax) {
+  float m = 0.f;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total4;
        i += (int64_t)gridDim.x * blockDim.x) {
     const int64_t e = i * 4;
@@ -172,14 +175,20 @@ __global__ void broadcast_kernel_vec4(const float* __restrict__ gpool, int64_t h
     const float* gp = gpool + b * C + c;
     const float4 v = make_float4(gp[0] * inv_hw, gp[1] * inv_hw, gp[2] * inv_hw, gp[3] * inv_hw);
     g[i] = v;
+    m = fmaxf(m, fmaxf(fmaxf(fabsf(v.x), fabsf(v.y)), fmaxf(fabsf(v.z), fabsf(v.w))));
     if (p0) {
-      const __nv_bfloat162 a = __floats2bfloat162_rn(v.x, v.y), b2 = __floats2bfloat162_rn(v.z, v.w);
-      p0[i] = make_uint2(*reinterpret_cast<const uint32_t*>(&a), *reinterpret_cast<const uint32_t*>(&b2));
-      if (p1) {
-        const __nv_bfloat162 c = __floats2bfloat162_rn(v.x - __low2float(a), v.y - __high2float(a));
-        const __nv_bfloat162 d = __floats2bfloat162_rn(v.z - __low2float(b2), v.w - __high2float(b2));
-        p1[i] = make_uint2(*reinterpret_cast<const uint32_t*>(&c), *reinterpret_cast<const uint32_t*>(&d));
-      }
+      const float vv[4] = {v.x, v.y, v.z, v.w};
+      p0[i] = pack_single4(vv);
+    }
+  }
+  if (bmax) {
+    __shared__ float sh[8];
+    for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+    if ((threadIdx.x & 31) == 0) sh[threadIdx.x >> 5] = m;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      for (int w = 1; w < (int)(blockDim.x >> 5); ++w) m = fmaxf(m, sh[w]);
+      bmax[blockIdx.x] = fmaxf(m, sh[0]);
     }
   }
 }
@@ -221,8 +230,9 @@ void head_forward(int nrows, int hw, int C, int classes, const float* x_end, con
 
 void head_loss_backward(int nrows, int hw, int C, int classes, const float* pooled, const float* logits,
                         const float* t_w, const int32_t* labels, double* loss_dev, float* gt_w, float* gt_b,
-                        float* g_out, void* ws, cudaStream_t st, void* p0, void* p1) {
+                        float* g_out, void* ws, cudaStream_t st, void* p0, void* p1, float* scale) {
   if (nrows <= 0) return;
+  if (p1 && !scale) fail(RP_ERR_INTERNAL, "head_loss_backward: the cotangent plane pair needs a scale buffer");
   char* w = static_cast<char*>(ws);
   float* glog = reinterpret_cast<float*>(w);
   double* loss_b = reinterpret_cast<double*>(w + align256((int64_t)nrows * classes * 4));
@@ -235,16 +245,18 @@ void head_loss_backward(int nrows, int hw, int C, int classes, const float* pool
   RP_LAUNCHED();
   const int64_t n = (int64_t)nrows * hw * C;
   const float inv = 1.f / (float)hw;
-  const int grid = (int)std::min<int64_t>((n / 4 + 255) / 256 + 1, 16 * kNumSMs);
+  const int grid = (int)std::min<int64_t>((n / 4 + 255) / 256 + 1, 2 * kPlaneScaleMaxParts);
   if (C % 4 == 0 && (reinterpret_cast<uintptr_t>(g_out) & 15u) == 0) {
+    float* part = p1 ? scale + kPlaneScalePartOffset : nullptr;
     broadcast_kernel_vec4<<<grid, 256, 0, st>>>(gpool, hw, C, n / 4, inv, reinterpret_cast<float4*>(g_out),
-                                                static_cast<uint2*>(p0), static_cast<uint2*>(p1));
+                                                p1 ? nullptr : static_cast<uint2*>(p0), part);
     RP_LAUNCHED();
+    if (p1) split_planes_from_parts(g_out, n, p0, p1, part, grid, scale, st);
     return;
   }
   broadcast_kernel<<<grid, 256, 0, st>>>(gpool, hw, C, n, inv, g_out);
   RP_LAUNCHED();
-  if (p0) split_planes(g_out, n, p0, p1, st);
+  if (p0) split_planes(g_out, n, p0, p1, st, p1 ? scale : nullptr);
 }
 
 void argmax_hits(const float* logits, const int32_t* labels, int nrows, int classes, unsigned long long* hits_dev,

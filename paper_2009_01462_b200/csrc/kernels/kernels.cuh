@@ -16,9 +16,12 @@ void fill_normal(float* dst, int64_t n, uint64_t state, double mean, double sigm
 void psi_device(int kind, const float* a, const float* b, int64_t n, void* ws, double* out_dev, cudaStream_t s);
 void psi_grad(int kind, const float* lam, const float* x, int64_t n, double scale, float* out, void* ws,
               cudaStream_t s);
-// p0 / p1 (optional): also the bf16 plane pair of g (p1 null: the bf16 copy alone)
+// p0 / p1 (optional): also the planes of g (planes.cuh): p1 non-null: the fp16 pair of g s with
+// the cotangent scale s written to *scale (a buffer of plane_scale_bytes()); p1 null: the bf16
+// single plane
 void synthetic_grad(int kind, const float* lam_next, const float* x_end, const float* kappa, int64_t n, double w,
-                    float* g, void* ws, cudaStream_t s, void* p0 = nullptr, void* p1 = nullptr);
+                    float* g, void* ws, cudaStream_t s, void* p0 = nullptr, void* p1 = nullptr,
+                    float* scale = nullptr);
 void correct(int kind, float* lam, const float* x_prev, const float* p, float* kappa, int64_t n, double w,
              double eta, bool update_lambda, double kappa_coef, bool update_kappa, void* ws, cudaStream_t s);
 void sgd(float* w, const float* g, float* v, int64_t n, double lr, double momentum, cudaStream_t s);
@@ -58,15 +61,17 @@ void conv3x3_wgrad_simt(const ConvShape& s, const float* in, const float* g, flo
 enum { TC_MODE_TF32 = 0, TC_MODE_X3TF32 = 1, TC_MODE_X3BF16 = 2 };
 bool conv3x3_tc_supported(const ConvShape& s);
 int64_t conv3x3_tc_ws_bytes(const ConvShape& s);
-// out_planes (optional): bf16 [2][pixels * co] receives the plane pair of out.
-// in_planes (optional): bf16 [2][pixels * ci], the input as a plane pair (in unused): the
-// 2-MMA plane mode (~2^-17 relative).
+// out_planes (optional): fp16 [2][pixels * co] receives the plane pair of out * (*out_scale).
+// in_planes (optional): fp16 [2][pixels * ci], the input times (*in_scale) as a plane pair
+// (in unused): the 2-MMA plane mode (planes.cuh, ~2^-23 relative).  Scales: device scalars,
+// null = 1.
 void conv3x3_fwd_tc(const ConvShape& s, const float* in, const float* w_hwio, bool dgrad_weights, const float* bias,
                     const float* aux, float h, int epi, float* out, int mode, void* ws, cudaStream_t st,
-                    void* out_planes = nullptr, const void* in_planes = nullptr, const void* wprep = nullptr);
+                    void* out_planes = nullptr, const void* in_planes = nullptr, const void* wprep = nullptr,
+                    const float* in_scale = nullptr, const float* out_scale = nullptr);
 // The plane-mode A operands of both filters of nblocks blocks in one launch (filter j of block
 // b: HWIO at pb + b block_stride + off[j], ci_src[j] x co_src[j]; dgrad: flipped/transposed) into
-// out + (2 b + j) * 9 ci co * 2 bf16 -- the wprep argument of conv3x3_fwd_tc.
+// out + (2 b + j) * 9 ci co * 2 fp16 (W * kWeightPlaneScale) -- the wprep argument of conv3x3_fwd_tc.
 void prep_filters_planes(const float* pb, int64_t block_stride, int nblocks, const int64_t off[2],
                          const int ci_src[2], const int co_src[2], bool dgrad, void* out, cudaStream_t st);
 
@@ -98,17 +103,19 @@ int64_t conv3x3_wgrad_bf16_ws_bytes(const ConvShape& s);
 void conv3x3_wgrad_bf16(const ConvShape& s, const float* in, const float* g, float scale, float* gw, float* gb,
                         void* ws, cudaStream_t st);
 
-// tcgen05 weight gradient from bf16 plane pairs x = x0 + x1, g = g0 + g1 (conv_wgrad_planes.cu):
-// the fp32-accurate wgrad when the producers wrote the planes; Ci, Co % 64 == 0.
+// tcgen05 weight gradient from fp16 plane pairs x = x0 + x1, g s = g0 + g1 (conv_wgrad_planes.cu):
+// the fp32-accurate wgrad when the producers wrote the planes; Ci, Co % 64 == 0.  gscale: the
+// g planes' scale s (device scalar, null = 1), divided out.
 bool conv3x3_wgrad_planes_supported(const ConvShape& s);
 int64_t conv3x3_wgrad_planes_ws_bytes(const ConvShape& s);
 void conv3x3_wgrad_planes(const ConvShape& s, const void* x0, const void* x1, const void* g0, const void* g1,
-                          float scale, float* gw, float* gb, void* ws, cudaStream_t st);
+                          float scale, float* gw, float* gb, void* ws, cudaStream_t st, const float* gscale);
 // Two weight gradients of the same shape in one launch (the block's gW1 and gW2 when C ==
 // hidden): xa / ga = {plane 0, plane 1} of job a's operands, likewise job b.
 void conv3x3_wgrad_planes_pair(const ConvShape& s, const void* const xa[2], const void* const ga[2], float scale_a,
                                float* gwa, float* gba, const void* const xb[2], const void* const gb2[2],
-                               float scale_b, float* gwb, float* gbb, void* ws, cudaStream_t st);
+                               float scale_b, float* gwb, float* gbb, void* ws, cudaStream_t st, const float* gsc_a,
+                               const float* gsc_b);
 // The same kernel on single bf16 planes (RP_MATH_BF16): x, g one bf16 NHWC tensor each,
 // 128-channel blocks (Ci, Co % 128 == 0); bf16 x bf16 products, fp32 accumulate.
 bool conv3x3_wgrad_bf16p_supported(const ConvShape& s);
@@ -120,13 +127,21 @@ bool conv3x3_wgrad_bf16p_pair_supported(const ConvShape& s);
 void conv3x3_wgrad_bf16p_pair(const ConvShape& s, const void* xa, const void* ga, float scale_a, float* gwa,
                               float* gba, const void* xb, const void* gb2, float scale_b, float* gwb, float* gbb,
                               void* ws, cudaStream_t st);
-// fp32 [n] -> bf16 planes p0 = bf16(v), p1 = bf16(v - p0)   (n % 4 == 0; p1 may be null: bf16 copy)
-void split_planes(const float* in, int64_t n, void* p0, void* p1, cudaStream_t st);
+// fp32 [n] -> planes (planes.cuh; n % 4 == 0): p1 non-null: the fp16 pair, of v * s when
+// scale_out is given (s from max |v| on device, stored at scale_out[0]; the buffer must hold
+// plane_scale_bytes()), else of v; p1 null: the bf16 single plane.
+constexpr int kPlaneScalePartOffset = 16;     // floats: [0] the scale, [16, 16 + parts) max partials
+constexpr int kPlaneScaleMaxParts = 1024;
+inline int64_t plane_scale_bytes() { return 4LL * (kPlaneScalePartOffset + 2 * kPlaneScaleMaxParts); }   // 8.2 KB
+void split_planes(const float* in, int64_t n, void* p0, void* p1, cudaStream_t st, float* scale_out = nullptr);
+// the scaled pair from per-CTA max |v| partials already computed by the producer (part[0, nparts))
+void split_planes_from_parts(const float* in, int64_t n, void* p0, void* p1, const float* part, int nparts,
+                             float* scale_out, cudaStream_t st);
 
 // ---- stem S (stem.cu): Cin <= 4 streaming kernels (SIMT conv path otherwise)
 bool stem_supported(const ConvShape& s);
 int64_t stem_wgrad_ws_bytes(const ConvShape& s);
-// p0 (and p1, nullable): the output's bf16 planes as split_planes makes them, in the same pass
+// p0 (and p1, nullable): the output's planes as split_planes makes them (unscaled), in the same pass
 void stem_fwd(const ConvShape& s, const float* x, const float* w, const float* b, float* out, cudaStream_t st,
               void* p0 = nullptr, void* p1 = nullptr);
 void stem_wgrad(const ConvShape& s, const float* x, const float* g, float scale, float* gw, float* gb, void* ws,
@@ -138,7 +153,8 @@ void head_forward(int nrows, int hw, int channels, int classes, const float* x_e
                   const float* t_b, float* pooled, float* logits, cudaStream_t st);
 void head_loss_backward(int nrows, int hw, int channels, int classes, const float* pooled, const float* logits,
                         const float* t_w, const int32_t* labels, double* loss_dev, float* gt_w, float* gt_b,
-                        float* g_out, void* ws, cudaStream_t st, void* p0 = nullptr, void* p1 = nullptr);
+                        float* g_out, void* ws, cudaStream_t st, void* p0 = nullptr, void* p1 = nullptr,
+                        float* scale = nullptr);
 void argmax_hits(const float* logits, const int32_t* labels, int nrows, int classes, unsigned long long* hits_dev,
                  cudaStream_t st);
 

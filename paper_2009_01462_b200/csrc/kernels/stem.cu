@@ -12,6 +12,7 @@
 
 #include "../common.cuh"
 #include "kernels.cuh"
+#include "planes.cuh"
 
 namespace rp::k {
 
@@ -137,17 +138,15 @@ __global__ __launch_bounds__(256, CG == 8 ? 3 : 2) void stem_fwd4_kernel(const f
 #pragma unroll
       for (int qq = 0; qq < CG / 4; ++qq)
         o[qq] = make_float4(acc[i][4 * qq], acc[i][4 * qq + 1], acc[i][4 * qq + 2], acc[i][4 * qq + 3]);
-      if (p0) {   // the first block's input planes, as split_planes makes them
+      if (p0) {   // the first block's input planes (planes.cuh), as split_planes makes them
         const int64_t e4 = (((n * H + yq) * (int64_t)W + x0 + i) * C + c0) / 4;
 #pragma unroll
         for (int qq = 0; qq < CG / 4; ++qq) {
-          const float* v = &acc[i][4 * qq];
-          const __nv_bfloat162 hi0 = __floats2bfloat162_rn(v[0], v[1]), hi1 = __floats2bfloat162_rn(v[2], v[3]);
-          const __nv_bfloat162 lo0 = __floats2bfloat162_rn(v[0] - __low2float(hi0), v[1] - __high2float(hi0));
-          const __nv_bfloat162 lo1 = __floats2bfloat162_rn(v[2] - __low2float(hi1), v[3] - __high2float(hi1));
-          p0[e4 + qq] = make_uint2(*reinterpret_cast<const uint32_t*>(&hi0), *reinterpret_cast<const uint32_t*>(&hi1));
+          const float v[4] = {acc[i][4 * qq], acc[i][4 * qq + 1], acc[i][4 * qq + 2], acc[i][4 * qq + 3]};
           if (p1)
-            p1[e4 + qq] = make_uint2(*reinterpret_cast<const uint32_t*>(&lo0), *reinterpret_cast<const uint32_t*>(&lo1));
+            pack_pair4(v, kActPlaneScale, p0[e4 + qq], p1[e4 + qq]);   // fp32 path: the fp16 pair
+          else
+            p0[e4 + qq] = pack_single4(v);                  // bf16 tape path: the bf16 copy
         }
       }
     }

@@ -2,10 +2,13 @@
 the fp32 trainer runs on tcgen05 shapes, against the fp64 oracle block (block_forward /
 block_vjp, network.cpp:82-106) and against the fp32-operand block path.
 
-Every conv of the plane path reads its input as a bf16 plane pair (2^-17 relative split) and
-writes the plane pair of its output, which must reconstruct the fp32 output to bf16-pair
-precision (|v - p0 - p1| <= 2^-16 |v|).  Tolerances: 2e-5 of the tensor's max |value| against
-the fp64 oracle for activations / cotangents, 5e-5 for the weight gradients."""
+Every conv of the plane path reads its input as an fp16 plane pair (v s = p0 + p1: 22
+significant bits, planes.cuh) and writes the plane pair of its output, which must reconstruct
+the fp32 output to fp16-pair precision (|v s - p0 - p1| <= 2^-22 |v s| + 2^-25, the second term
+for subnormal low planes).  The cotangent enters at 1e-5 scale (the size of a synthetic-loss
+upstream), so its pair carries a device scale.  Tolerances: 1e-5 of the tensor's max |value|
+against the fp64 oracle for activations / cotangents, 2e-5 for the weight gradients (the
+operands are fp32-class; tcgen05's fp32 accumulation costs ~2e-6 per 576-term conv)."""
 import ctypes as C
 
 import numpy as np
@@ -18,17 +21,24 @@ from oracle import respar_oracle as O
 pytestmark = pytest.mark.gpu
 torch = pytest.importorskip("torch")
 
-GW_TOL = 5e-5    # weight / bias gradients, relative to the tensor's max |value|
-FWD_TOL = 2e-5   # a, x_next, input cotangent
+GW_TOL = 2e-5    # weight / bias gradients, relative to the tensor's max |value|
+FWD_TOL = 1e-5   # a, x_next, input cotangent (tcgen05 fp32 accumulation: ~2e-6 per conv)
 
 
 def _p(t):
     return C.c_void_p(t.data_ptr())
 
 
-def _planes_to_f64(t, n):
-    b = t.view(torch.bfloat16).float().cpu().numpy().astype(np.float64)
-    return b[:n] + b[n:2 * n]
+ACT = 128.0   # the forward activations' plane scale (planes.cuh kActPlaneScale)
+
+
+def _planes_to_f64(t, n, scale=ACT):
+    b = t.view(torch.float16).float().cpu().numpy().astype(np.float64)
+    return (b[:n] + b[n:2 * n]) / scale
+
+
+def _pair_ok(t, n, v, scale=ACT):
+    return np.all(np.abs(_planes_to_f64(t, n, scale) - v) <= (2.0 ** -22 * np.abs(v) + 2.0 ** -25 / scale))
 
 
 def _rel(got, want):
@@ -50,7 +60,7 @@ def test_block_planes(n, hw, c, ch):
 
     rng = np.random.default_rng(5)
     x = rng.uniform(-1, 1, (n, hw, hw, c)).astype(np.float32)
-    up = rng.uniform(-1, 1, (n, hw, hw, c)).astype(np.float32)
+    up = (rng.uniform(-1, 1, (n, hw, hw, c)) * 1e-5).astype(np.float32)
     dev = torch.device("cuda")
     tx, tup, tp = (torch.from_numpy(v).to(dev) for v in (x, up, flat))
     off = lib().rp_param_offset_block(C.byref(geo), 0)
@@ -70,7 +80,7 @@ def test_block_planes(n, hw, c, ch):
     a_p = torch.empty(2 * nh, dtype=torch.int16, device=dev)
     xn_p = torch.empty(2 * ne, dtype=torch.int16, device=dev)
     x_p = torch.empty(2 * ne, dtype=torch.int16, device=dev)
-    rp.check(lib().rp_op_split_planes(_p(tx), ne, _p(x_p), C.c_void_p(x_p.data_ptr() + 2 * ne), None))
+    rp.check(lib().rp_op_split_planes(_p(tx), ne, _p(x_p), C.c_void_p(x_p.data_ptr() + 2 * ne), None, None))
     # the block's filters prepared once (rp_op_prep_planes_filters) vs per conv (filters = NULL):
     # bitwise the same
     fbytes = lib().rp_op_planes_filters_bytes(C.byref(geo), 1)
@@ -88,20 +98,22 @@ def test_block_planes(n, hw, c, ch):
     a64, xn64 = a.cpu().numpy().astype(np.float64), xn.cpu().numpy().astype(np.float64)
     assert _rel(a64, a_ref.cpu().numpy().astype(np.float64)) < FWD_TOL
     assert _rel(xn64, xn_ref.cpu().numpy().astype(np.float64)) < FWD_TOL
-    assert np.all(np.abs(_planes_to_f64(a_p, nh) - a64) <= 2.0 ** -16 * np.abs(a64))
-    assert np.all(np.abs(_planes_to_f64(xn_p, ne) - xn64) <= 2.0 ** -16 * np.abs(xn64))
+    assert _pair_ok(a_p, nh, a64)
+    assert _pair_ok(xn_p, ne, xn64)
     want_xn, cache = O.block_forward(net32, 0, x.astype(np.float64))
     assert _rel(xn64.reshape(want_xn.shape), want_xn) < FWD_TOL
 
     # backward: plane path vs oracle and vs fp32-operand path
     g_io = tup.clone().reshape(-1)
     g_p = torch.empty(2 * ne, dtype=torch.int16, device=dev)
-    rp.check(lib().rp_op_split_planes(_p(g_io), ne, _p(g_p), C.c_void_p(g_p.data_ptr() + 2 * ne), None))
+    gscale = torch.zeros(lib().rp_op_plane_scale_bytes() // 4, device=dev)
+    rp.check(lib().rp_op_split_planes(_p(g_io), ne, _p(g_p), C.c_void_p(g_p.data_ptr() + 2 * ne), _p(gscale), None))
     dpre = torch.empty(nh, device=dev)
     dpre_p = torch.empty(2 * nh, dtype=torch.int16, device=dev)
     gb = torch.zeros_like(tp)
     gbp = C.c_void_p(gb.data_ptr() + 4 * off)
-    rp.check(lib().rp_op_block_bwd_planes(C.byref(geo), n, _p(x_p), _p(a), _p(a_p), pb, _p(g_io), _p(g_p), _p(dpre),
+    rp.check(lib().rp_op_block_bwd_planes(C.byref(geo), n, _p(x_p), _p(a), _p(a_p), pb, _p(g_io), _p(g_p), _p(gscale),
+                                          _p(dpre),
                                           _p(dpre_p), gbp, _p(fbwd), _p(ws), wsb, None))
     g_ref = tup.clone().reshape(-1)
     gb_ref = torch.zeros_like(tp)
@@ -110,7 +122,9 @@ def test_block_planes(n, hw, c, ch):
     torch.cuda.synchronize()
     g64 = g_io.cpu().numpy().astype(np.float64)
     assert _rel(g64, g_ref.cpu().numpy().astype(np.float64)) < FWD_TOL
-    assert np.all(np.abs(_planes_to_f64(g_p, ne) - g64) <= 2.0 ** -16 * np.abs(g64))
+    s = float(gscale[0].item())
+    assert s == 2.0 ** (8 - np.frexp(np.abs(up).max())[1])     # max |g s| in [2^7, 2^8)
+    assert _pair_ok(g_p, ne, g64, s)
 
     p_prev, (gw1, gb1, gw2, gb2) = O.block_vjp(net32, 0, O.BlockCache(x.astype(np.float64), a64.reshape(
         n, hw, hw, ch)), up.astype(np.float64))

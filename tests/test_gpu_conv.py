@@ -81,7 +81,8 @@ PLANE_SHAPES = [(2, 32, 32, 64, 64), (1, 32, 32, 64, 128), (2, 32, 32, 128, 64),
                 (1, 12, 10, 16, 64), (2, 16, 16, 128, 128), (1, 16, 16, 256, 256), (1, 9, 11, 256, 64)]
 
 
-# plane mode: the input enters as a bf16 pair (2^-17 relative), W as [W0; W1] (2^-17)
+# plane mode: the input enters as an fp16 pair (22 bits, planes.cuh), W as [W0; W1] (W 2^8, 22 bits);
+# dgrad runs on a cotangent-sized input (1e-5) whose pair carries a device scale (in and out)
 @pytest.mark.parametrize("shape", PLANE_SHAPES)
 @pytest.mark.parametrize("dgrad", [False, True])
 def test_conv_planes(shape, dgrad):
@@ -92,34 +93,43 @@ def test_conv_planes(shape, dgrad):
     for epi in range(6):
         rng = np.random.default_rng(epi)
         cin, cout = (co, ci) if dgrad else (ci, co)
-        x = rng.uniform(-1, 1, (n, hh, ww, cin)).astype(np.float32)
+        x = (rng.uniform(-1, 1, (n, hh, ww, cin)) * (1e-5 if dgrad else 1.0)).astype(np.float32)
         w = (rng.uniform(-1, 1, (3, 3, ci, co)) / np.sqrt(9 * ci)).astype(np.float32)
-        bias = rng.uniform(-0.2, 0.2, cout).astype(np.float32)
+        bias = (rng.uniform(-0.2, 0.2, cout) * (1e-5 if dgrad else 1.0)).astype(np.float32)
         aux = rng.uniform(-0.9, 0.9, (n, hh, ww, cout)).astype(np.float32)
+        if dgrad and epi in (2, 4):
+            aux *= 1e-5   # the residual adds a cotangent of the same size
         acc = O.conv3x3_dgrad(x.astype(np.float64), w.astype(np.float64)) if dgrad else \
             O.conv3x3(x.astype(np.float64), w.astype(np.float64))
         want = want_epi(epi, acc, bias.astype(np.float64), aux.astype(np.float64), np.float32(0.7))
         tx, tw, tb, taux = (torch.from_numpy(v).to(dev) for v in (x, w, bias, aux))
-        xp = torch.empty(2 * tx.numel(), dtype=torch.bfloat16, device=dev)
+        xp = torch.empty(2 * tx.numel(), dtype=torch.float16, device=dev)
+        sc = torch.zeros(lib().rp_op_plane_scale_bytes() // 4, device=dev) if dgrad else None
         rp.check(lib().rp_op_split_planes(C.c_void_p(tx.data_ptr()), tx.numel(), C.c_void_p(xp.data_ptr()),
-                                          C.c_void_p(xp.data_ptr() + 2 * tx.numel()), None))
+                                          C.c_void_p(xp.data_ptr() + 2 * tx.numel()),
+                                          C.c_void_p(sc.data_ptr()) if dgrad else None, None))
         out = taux.clone() if epi == 4 else torch.empty((n, hh, ww, cout), device=dev)
-        op = torch.empty(2 * out.numel(), dtype=torch.bfloat16, device=dev)
+        op = torch.empty(2 * out.numel(), dtype=torch.float16, device=dev)
         wsb = lib().rp_op_conv3x3_workspace_bytes(ci, co)
         ws = torch.empty(wsb, dtype=torch.uint8, device=dev)
         use_aux = epi in (2, 3, 4)
         rp.check(lib().rp_op_conv3x3_planes(
             n, hh, ww, cin, cout, C.c_void_p(xp.data_ptr()), C.c_void_p(tw.data_ptr()), 1 if dgrad else 0,
             C.c_void_p(tb.data_ptr()), C.c_void_p(out.data_ptr() if epi == 4 else taux.data_ptr()) if use_aux else None,
-            0.7, epi, C.c_void_p(out.data_ptr()), C.c_void_p(op.data_ptr()), C.c_void_p(ws.data_ptr()), wsb, None))
+            0.7, epi, C.c_void_p(out.data_ptr()), C.c_void_p(op.data_ptr()),
+            C.c_void_p(sc.data_ptr()) if dgrad else None, C.c_void_p(sc.data_ptr()) if dgrad else None,
+            C.c_void_p(ws.data_ptr()), wsb, None))
         torch.cuda.synchronize()
         got = out.cpu().numpy().astype(np.float64)
         err = np.abs(got - want).max() / max(np.abs(want).max(), 1e-30)
         print(f"planes {shape} dgrad={dgrad} {EPIS[epi]}: {err:.2e}")
-        assert err <= 2e-5, (EPIS[epi], err)
+        # tcgen05's fp32 accumulation loses ~2^-24 relative per MMA step: the error grows with
+        # the reduction length 9 Ci (measured 2e-6 at Ci = 64, 6e-6 at 256; tools/acc_probe.py)
+        assert err <= 3e-6 * max(1.0, cin / 64), (EPIS[epi], err)
+        s_out = float(sc[0].item()) if dgrad else 128.0   # dgrad: the cotangent's scale; fprop: 2^7
         pl = op.float().cpu().numpy().astype(np.float64)
-        rec = (pl[:out.numel()] + pl[out.numel():]).reshape(got.shape)
-        assert np.all(np.abs(rec - got) <= 2.0 ** -16 * np.abs(got)), EPIS[epi]
+        rec = (pl[:out.numel()] + pl[out.numel():]).reshape(got.shape) / s_out
+        assert np.all(np.abs(rec - got) <= 2.0 ** -22 * np.abs(got) + 2.0 ** -25 / s_out), EPIS[epi]
 
 
 BF16_SHAPES = [(2, 16, 16, 128, 128), (1, 16, 16, 256, 256), (2, 9, 11, 64, 128), (1, 32, 32, 128, 256),
@@ -195,28 +205,30 @@ def test_wgrad_bf16(shape):
 def run_wgrad_planes(n, hh, ww, ci, co, seed=0, scale=0.37):
     rng = np.random.default_rng(seed)
     x = rng.uniform(-1, 1, (n, hh, ww, ci)).astype(np.float32)
-    g = rng.uniform(-1, 1, (n, hh, ww, co)).astype(np.float32)
+    g = (rng.uniform(-1, 1, (n, hh, ww, co)) * 3e-6).astype(np.float32)   # cotangent-sized: a scaled pair
     want_w = scale * O.conv3x3_wgrad(x.astype(np.float64), g.astype(np.float64))
     want_b = scale * g.astype(np.float64).reshape(-1, co).sum(axis=0)
     dev = torch.device("cuda")
     tx, tg = torch.from_numpy(x).to(dev), torch.from_numpy(g).to(dev)
-    planes = [torch.empty(t.numel(), dtype=torch.bfloat16, device=dev) for t in (tx, tx, tg, tg)]
+    planes = [torch.empty(t.numel(), dtype=torch.float16, device=dev) for t in (tx, tx, tg, tg)]
+    sc = torch.zeros(lib().rp_op_plane_scale_bytes() // 4, device=dev)
     rp.check(lib().rp_op_split_planes(C.c_void_p(tx.data_ptr()), tx.numel(), C.c_void_p(planes[0].data_ptr()),
-                                      C.c_void_p(planes[1].data_ptr()), None))
+                                      C.c_void_p(planes[1].data_ptr()), None, None))
     rp.check(lib().rp_op_split_planes(C.c_void_p(tg.data_ptr()), tg.numel(), C.c_void_p(planes[2].data_ptr()),
-                                      C.c_void_p(planes[3].data_ptr()), None))
+                                      C.c_void_p(planes[3].data_ptr()), C.c_void_p(sc.data_ptr()), None))
     gw = torch.full((3, 3, ci, co), float("nan"), device=dev)
     gb = torch.full((co,), float("nan"), device=dev)
     wsb = lib().rp_op_conv3x3_wgrad_planes_workspace_bytes(n, hh, ww, ci, co)
     ws = torch.empty(wsb, dtype=torch.uint8, device=dev)
     rp.check(lib().rp_op_conv3x3_wgrad_planes(n, hh, ww, ci, co, *[C.c_void_p(t.data_ptr()) for t in planes], scale,
-                                              C.c_void_p(gw.data_ptr()), C.c_void_p(gb.data_ptr()),
+                                              C.c_void_p(sc.data_ptr()), C.c_void_p(gw.data_ptr()),
+                                              C.c_void_p(gb.data_ptr()),
                                               C.c_void_p(ws.data_ptr()), wsb, None))
     torch.cuda.synchronize()
     return gw.cpu().numpy().astype(np.float64), gb.cpu().numpy().astype(np.float64), want_w, want_b
 
 
-# x, g as 16-bit-mantissa plane pairs: ~2^-17 relative per product
+# x, g as fp16 plane pairs (22 bits; g with its device scale): fp32-class products
 @pytest.mark.parametrize("shape", [(2, 32, 32, 64, 64), (3, 8, 8, 64, 64), (1, 12, 10, 64, 64), (2, 16, 16, 128, 64),
                                    (2, 8, 8, 64, 128), (1, 16, 16, 256, 256), (2, 7, 9, 64, 64)])
 def test_wgrad_planes(shape):
@@ -224,7 +236,7 @@ def test_wgrad_planes(shape):
     ew = np.abs(gw - ww_).max() / np.abs(ww_).max()
     eb = np.abs(gb - wb).max() / np.abs(wb).max()
     print(f"wgrad planes {shape}: w {ew:.2e} b {eb:.2e}")
-    assert ew <= 3e-5 and eb <= 3e-5, (ew, eb)
+    assert ew <= 1e-6 and eb <= 1e-6, (ew, eb)
 
 
 def test_wgrad_deterministic():
@@ -273,7 +285,7 @@ def test_stem_fwd_and_wgrad(cin, c):
     assert eo <= 1e-5 and ew <= 1e-5 and eb <= 1e-5, (eo, ew, eb)
 
 
-# rp_op_stem_fwd_planes: the stem output plus, in the same pass, the bf16 planes of it --
+# rp_op_stem_fwd_planes: the stem output plus, in the same pass, the planes of it --
 # bitwise what rp_op_stem_fwd followed by rp_op_split_planes gives (W % 4 == 0: the fused
 # store; W = 10 / 6: the split after the streaming kernel).
 @pytest.mark.parametrize("cin,c,hh,ww,lo", [(3, 64, 8, 12, True), (3, 64, 8, 12, False), (1, 16, 7, 10, True),
@@ -295,7 +307,7 @@ def test_stem_fwd_planes_matches_split(cin, c, hh, ww, lo):
                                   None))
     want = torch.full((2 * e,), 0x7FFF, dtype=torch.int16, device=dev)
     rp.check(lib().rp_op_split_planes(C.c_void_p(out_ref.data_ptr()), e, C.c_void_p(want.data_ptr()),
-                                      C.c_void_p(want.data_ptr() + 2 * e) if lo else None, None))
+                                      C.c_void_p(want.data_ptr() + 2 * e) if lo else None, None, None))
     out = torch.full((e,), float("nan"), device=dev)
     got = torch.full((2 * e,), 0x7FFF, dtype=torch.int16, device=dev)
     rp.check(lib().rp_op_stem_fwd_planes(C.byref(geo), n, C.c_void_p(tx.data_ptr()), C.c_void_p(tp.data_ptr()),
@@ -308,8 +320,8 @@ def test_stem_fwd_planes_matches_split(cin, c, hh, ww, lo):
         assert bool((got[e:] == 0x7FFF).all())
 
 
-# rp_op_head_loss_bwd_planes: the head backward plus the cotangent's bf16 planes in the
-# broadcast pass -- bitwise rp_op_head_loss_bwd followed by rp_op_split_planes.
+# rp_op_head_loss_bwd_planes: the head backward plus the cotangent's planes (the scaled fp16
+# pair, or the bf16 single plane) -- bitwise rp_op_head_loss_bwd followed by rp_op_split_planes.
 @pytest.mark.parametrize("c,lo", [(64, True), (128, False), (256, True)])
 def test_head_loss_bwd_planes_matches_split(c, lo):
     n, hh, ww, classes = 5, 8, 8, 10
@@ -336,16 +348,18 @@ def test_head_loss_bwd_planes_matches_split(c, lo):
         planes = torch.full((2 * e,), 0x7FFF, dtype=torch.int16, device=dev)
         p0 = C.c_void_p(planes.data_ptr())
         p1 = C.c_void_p(planes.data_ptr() + 2 * e) if lo else None
+        sc = torch.zeros(lib().rp_op_plane_scale_bytes() // 4, device=dev)
+        scp = C.c_void_p(sc.data_ptr()) if lo else None
         args = (C.byref(geo), n, C.c_void_p(pooled.data_ptr()), C.c_void_p(logits.data_ptr()), pt,
                 C.c_void_p(labels.data_ptr()), C.c_void_p(loss.data_ptr()), C.c_void_p(gt.data_ptr()),
                 C.c_void_p(g.data_ptr()))
         if fused:
-            rp.check(lib().rp_op_head_loss_bwd_planes(*args, p0, p1, C.c_void_p(ws.data_ptr()), wsb, None))
+            rp.check(lib().rp_op_head_loss_bwd_planes(*args, p0, p1, scp, C.c_void_p(ws.data_ptr()), wsb, None))
         else:
             rp.check(lib().rp_op_head_loss_bwd(*args, C.c_void_p(ws.data_ptr()), wsb, None))
-            rp.check(lib().rp_op_split_planes(C.c_void_p(g.data_ptr()), e, p0, p1, None))
+            rp.check(lib().rp_op_split_planes(C.c_void_p(g.data_ptr()), e, p0, p1, scp, None))
         torch.cuda.synchronize()
-        outs.append((loss, gt, g, planes))
+        outs.append((loss, gt, g, planes, sc[:1]))
     for a, b in zip(*outs):
         assert torch.equal(a, b)
     assert bool(torch.isfinite(outs[1][2]).all())

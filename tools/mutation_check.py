@@ -22,14 +22,19 @@ OUT = os.path.join(ROOT, "tools", "_mut")
 PKG = "paper_2009_01462_b200"
 
 MUTANTS = {
-    # the low plane of the synthetic upstream (the bf16 pair the first backward conv reads)
-    "p1_plane_zero": ("csrc/kernels/elementwise.cu",
-                      "p1[i] = make_uint2(*reinterpret_cast<const uint32_t*>(&c), *reinterpret_cast<const uint32_t*>(&d));",
-                      "p1[i] = make_uint2(0u, 0u);"),
+    # the low plane of the scaled cotangent pair (the synthetic / loss upstream the first
+    # backward conv and the weight gradients read)
+    "cotangent_p1_zero": ("csrc/kernels/conv_wgrad_planes.cu",
+                          "    pack_pair4(vv, sc, p0[i], p1[i]);\n  }\n}\n\ntypedef",
+                          "    pack_pair4(vv, sc, p0[i], p1[i]);\n    p1[i] = make_uint2(0u, 0u);\n  }\n}\n\ntypedef"),
     # the multiplier term of the synthetic upstream, one lane of four
     "kappa_term_sign": ("csrc/kernels/elementwise.cu",
                         "o.x = -dlam(kind, l.x - xe.x, 0, -1) * w + k4.x;",
                         "o.x = -dlam(kind, l.x - xe.x, 0, -1) * w - k4.x;"),
+    # the weight scale divided out of one conv epilogue off by 2^-16 (a 1.5e-5 relative bias)
+    "epilogue_scale_bias": ("csrc/kernels/conv_tc.cu",
+                            "const float acc_mul = a.wscale_inv / ",
+                            "const float acc_mul = (a.wscale_inv * (1.f + 0x1p-16f)) / "),
 }
 
 DEFAULT_TESTS = ["tests/test_gpu_plane_parity.py"]

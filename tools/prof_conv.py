@@ -33,12 +33,12 @@ ws = torch.empty(ws_b, dtype=torch.uint8, device=dev)
 gw = torch.empty(3, 3, c, c, device=dev)
 gb = torch.empty(c, device=dev)
 ne = n * h * w * c
-xp = torch.empty(2 * ne, dtype=torch.bfloat16, device=dev)   # plane pairs: p1 = p0 + ne
-gp = torch.empty(2 * ne, dtype=torch.bfloat16, device=dev)
+xp = torch.empty(2 * ne, dtype=torch.float16, device=dev)   # plane pairs: p1 = p0 + ne
+gp = torch.empty(2 * ne, dtype=torch.float16, device=dev)
 planes = [xp[:ne], xp[ne:], gp[:ne], gp[ne:]]
 for src, (p0, p1) in ((x, planes[:2]), (g, planes[2:])):
     rp.check(lib().rp_op_split_planes(C.c_void_p(src.data_ptr()), src.numel(), C.c_void_p(p0.data_ptr()),
-                                      C.c_void_p(p1.data_ptr()), None))
+                                      C.c_void_p(p1.data_ptr()), None, None))
 ws_p = lib().rp_op_conv3x3_wgrad_planes_workspace_bytes(n, h, w, c, c)
 ws_b = max(ws_b, ws_p, lib().rp_op_conv3x3_wgrad_bf16p_workspace_bytes(n, h, w, c, c))
 ws = torch.empty(ws_b, dtype=torch.uint8, device=dev)
@@ -61,15 +61,15 @@ for which in a.which.split(","):
             d = which == "dgrad_planes"
             rp.check(lib().rp_op_conv3x3_planes(n, h, w, c, c, P(planes[0].data_ptr()), P(wt.data_ptr()), int(d),
                                                 P(b.data_ptr()), P(x.data_ptr()) if d else None, 1.0, 3 if d else 1,
-                                                P(out.data_ptr()), P(planes[2].data_ptr()), P(ws.data_ptr()), ws_b,
-                                                None))
+                                                P(out.data_ptr()), P(planes[2].data_ptr()), None, None,
+                                                P(ws.data_ptr()), ws_b, None))
         elif which == "wgrad_bf16p":
             rp.check(lib().rp_op_conv3x3_wgrad_bf16p(n, h, w, c, c, C.c_void_p(planes[0].data_ptr()),
                                                      C.c_void_p(planes[2].data_ptr()), 1.0, P(gw.data_ptr()),
                                                      P(gb.data_ptr()), P(ws.data_ptr()), ws_b, None))
         elif which == "wgrad_planes":
             rp.check(lib().rp_op_conv3x3_wgrad_planes(n, h, w, c, c, *[C.c_void_p(t.data_ptr()) for t in planes], 1.0,
-                                                      P(gw.data_ptr()), P(gb.data_ptr()), P(ws.data_ptr()), ws_b,
+                                                      None, P(gw.data_ptr()), P(gb.data_ptr()), P(ws.data_ptr()), ws_b,
                                                       None))
         else:
             rp.check(lib().rp_op_conv3x3_wgrad(n, h, w, c, c, P(x.data_ptr()), P(g.data_ptr()), 1.0,
