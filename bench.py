@@ -2,13 +2,19 @@
 """Benchmark: train images/sec of one layer-parallel training iteration
 (DecoupledTrainer::step, reference decoupled.cpp:172-194) on B200.
 
-Default (N=1): BASELINE.json configs[1] == SURVEY §8 C2: ODE-ResNet 3x32x32, batch 256,
-C=64, L=16, K=4 stages, augmented Lagrangian (kappa updates), fp32, full batch
-(N_train = B).  Inputs are synthetic and device-resident for `value`; `e2e` times the
-same step through the public C ABI with pinned host buffers (H2D of x and labels,
-D2H of the loss inside the timed region).
+Default: BASELINE.json configs[2] == SURVEY §8 C3, the metric's own network: ODE-ResNet
+3x32x32, batch 256, C = 64, L = 64 residual blocks, K = 8 stages, augmented Lagrangian
+(kappa updates), fp32 math, full batch (N_train = B).  At N = 1 the 8 stages share the GPU
+(concurrent streams); at N = 2/4/8 stage k runs on GPU floor(k N / 8) with the neighbour
+exchange over NCCL (N = 8: one stage per B200).  Inputs are synthetic (the reference's
+splitmix64 stream: pixels U[-1,1), then labels next_u64() % 10) and device-resident for
+`value`; `e2e` times the same step through the public C ABI with pinned host buffers (H2D of
+x and labels, D2H of the loss inside the timed region).
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--config C2]
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--config C3]
+
+--gpus N without a torchrun environment re-launches itself under torch.distributed.run
+with N ranks (one per GPU); under torchrun, WORLD_SIZE must equal N.
 
 `--impl reference` times the reference's own CPU trainer (oracle/_ref, compiled from
 the reference sources) on the same config's dense 1x1-conv analogue, a bounded sample

@@ -375,6 +375,35 @@ int rp_trainer_region(rp_trainer* t, int32_t which, float* ms);
 int rp_serial_train_step(rp_trainer* t, const float* x_host, const int32_t* labels_host, int32_t nrows,
                          double lr, double* loss_out);
 
+/* ---- stage pipeline over NCCL (StagePool replacement across processes, runtime.hpp:33-67) --
+ * One process per B200: each holds the stage-sharded trainers (rp_trainer_create_local) of
+ * its stages and a pipeline that runs DecoupledTrainer::step (decoupled.cpp:172-194) with the
+ * neighbour exchange -- p_k upstream, the corrected lambda_k downstream -- as NCCL point-to-point
+ * transfers on dedicated streams, in `chunks` row chunks, overlapped with the corrections
+ * (host/pipeline.hpp).  Two communicators over the same ranks (one per direction); peers are
+ * ranks in them (-1: none).  NCCL is opened at run time (dlopen; RP_NCCL_LIBRARY overrides).
+ * A rank may list several consecutive trainers (the single-process loopback: peers = own rank). */
+typedef struct rp_comm rp_comm;
+typedef struct rp_pipeline rp_pipeline;
+int rp_comm_unique_id(uint8_t* id128);
+int rp_comm_create(const uint8_t* id128, int32_t nranks, int32_t rank, int32_t device, rp_comm** out);
+int rp_comm_destroy(rp_comm* c);
+int rp_pipeline_create(rp_comm* comm_a, rp_comm* comm_b, rp_trainer* const* trainers, const int32_t* prev_peer,
+                       const int32_t* next_peer, int32_t ntrainers, int32_t chunks, rp_pipeline** out);
+/* reset_lambda_from_forward (decoupled.cpp:44-63) as a chained forward; x_full: device raw
+ * inputs of all num_samples rows (read on the rank holding stage 0). */
+int rp_pipeline_reset_lambda_from_forward(rp_pipeline* p, const float* x_full_dev);
+/* One iteration on device buffers; loss_out (nullable) only on the rank holding stage K-1. */
+int rp_pipeline_step(rp_pipeline* p, const float* x_dev, const int32_t* labels_dev, int32_t nrows, int32_t row0,
+                     const rp_step_params* sp, double* loss_out);
+int rp_pipeline_loss(rp_pipeline* p, double* loss_out);
+/* Capture the step (kernels, events, NCCL calls) in a CUDA graph and replay it. */
+int rp_pipeline_set_graphs(rp_pipeline* p, int32_t on);
+/* which 0: start a device-timed region; 1: end it, *ms = elapsed (every stream joined). */
+int rp_pipeline_region(rp_pipeline* p, int32_t which, float* ms);
+int rp_pipeline_sync(rp_pipeline* p);
+int rp_pipeline_destroy(rp_pipeline* p);
+
 #ifdef __cplusplus
 }
 #endif

@@ -129,6 +129,17 @@ SIGNATURES = {
     "rp_trainer_last_step_ms": (C.c_int, [_P, C.POINTER(C.c_float)]),
     "rp_serial_train_step": (C.c_int, [_P, _F, _I32, C.c_int32, C.c_double, _D]),
     "rp_trainer_region": (C.c_int, [_P, C.c_int32, C.POINTER(C.c_float)]),
+    "rp_comm_unique_id": (C.c_int, [_P]),
+    "rp_comm_create": (C.c_int, [_P, C.c_int32, C.c_int32, C.c_int32, C.POINTER(_P)]),
+    "rp_comm_destroy": (C.c_int, [_P]),
+    "rp_pipeline_create": (C.c_int, [_P, _P, C.POINTER(_P), _I32, _I32, C.c_int32, C.c_int32, C.POINTER(_P)]),
+    "rp_pipeline_reset_lambda_from_forward": (C.c_int, [_P, _P]),
+    "rp_pipeline_step": (C.c_int, [_P, _P, _P, C.c_int32, C.c_int32, _SP, _D]),
+    "rp_pipeline_loss": (C.c_int, [_P, _D]),
+    "rp_pipeline_set_graphs": (C.c_int, [_P, C.c_int32]),
+    "rp_pipeline_region": (C.c_int, [_P, C.c_int32, C.POINTER(C.c_float)]),
+    "rp_pipeline_sync": (C.c_int, [_P]),
+    "rp_pipeline_destroy": (C.c_int, [_P]),
     "rp_profile_enable": (C.c_int, [C.c_int32]),
     "rp_profile_collect": (C.c_int, [_I64P, _D, _D, _D]),
     "rp_profile_class_name": (C.c_char_p, [C.c_int32]),

@@ -10,6 +10,8 @@
 #include <vector>
 
 #include "common.cuh"
+#include "host/comm.hpp"
+#include "host/pipeline.hpp"
 #include "host/respar_b200.hpp"
 
 namespace rp {
@@ -31,6 +33,14 @@ using respar::b200::StepParams;
 struct rp_trainer {
   std::unique_ptr<DecoupledTrainer> tr;
   bool serial = false;
+};
+
+struct rp_comm {
+  std::unique_ptr<respar::b200::NcclComm> c;
+};
+
+struct rp_pipeline {
+  std::unique_ptr<respar::b200::StagePipeline> p;
 };
 
 namespace {
@@ -517,6 +527,105 @@ int rp_serial_train_step(rp_trainer* t, const float* x_host, const int32_t* labe
     const double loss = tr.step(x, y, nrows, 0, to_params(&p), true);
     if (loss_out) *loss_out = loss;
   });
+}
+
+// ---- stage pipeline over NCCL (host/pipeline.hpp) ------------------------------------
+int rp_comm_unique_id(uint8_t* id) {
+  return tguard([&] {
+    need(id, "id");
+    respar::b200::NcclComm::unique_id(id);
+  });
+}
+
+int rp_comm_create(const uint8_t* id, int32_t nranks, int32_t rank, int32_t device, rp_comm** out) {
+  return tguard([&] {
+    need(id, "id");
+    need(out, "out");
+    *out = nullptr;
+    auto h = std::make_unique<rp_comm>();
+    h->c = std::make_unique<respar::b200::NcclComm>(id, nranks, rank, device);
+    *out = h.release();
+  });
+}
+
+int rp_comm_destroy(rp_comm* c) {
+  return tguard([&] { delete c; });
+}
+
+int rp_pipeline_create(rp_comm* comm_a, rp_comm* comm_b, rp_trainer* const* trainers, const int32_t* prev_peer,
+                       const int32_t* next_peer, int32_t n, int32_t chunks, rp_pipeline** out) {
+  return tguard([&] {
+    need(comm_a, "comm_a");
+    need(comm_b, "comm_b");
+    need(trainers, "trainers");
+    need(prev_peer, "prev_peer");
+    need(next_peer, "next_peer");
+    need(out, "out");
+    *out = nullptr;
+    if (n < 1) throw std::invalid_argument("pipeline: no trainers");
+    std::vector<respar::b200::StagePipeline::Member> m;
+    for (int i = 0; i < n; ++i) {
+      need(trainers[i], "trainer");
+      m.push_back({trainers[i]->tr.get(), prev_peer[i], next_peer[i]});
+    }
+    auto h = std::make_unique<rp_pipeline>();
+    h->p = std::make_unique<respar::b200::StagePipeline>(comm_a->c.get(), comm_b->c.get(), std::move(m), chunks);
+    *out = h.release();
+  });
+}
+
+int rp_pipeline_reset_lambda_from_forward(rp_pipeline* p, const float* x_full_dev) {
+  return tguard([&] {
+    need(p, "pipeline");
+    p->p->reset_lambda_from_forward(x_full_dev);
+  });
+}
+
+int rp_pipeline_step(rp_pipeline* p, const float* x_dev, const int32_t* labels_dev, int32_t nrows, int32_t row0,
+                     const rp_step_params* sp, double* loss_out) {
+  return tguard([&] {
+    need(p, "pipeline");
+    p->p->step(x_dev, labels_dev, nrows, row0, to_params(sp));
+    if (loss_out) *loss_out = p->p->loss();
+  });
+}
+
+int rp_pipeline_loss(rp_pipeline* p, double* loss_out) {
+  return tguard([&] {
+    need(p, "pipeline");
+    need(loss_out, "loss_out");
+    *loss_out = p->p->loss();
+  });
+}
+
+int rp_pipeline_set_graphs(rp_pipeline* p, int32_t on) {
+  return tguard([&] {
+    need(p, "pipeline");
+    p->p->set_graphs(on != 0);
+  });
+}
+
+int rp_pipeline_region(rp_pipeline* p, int32_t which, float* ms) {
+  return tguard([&] {
+    need(p, "pipeline");
+    if (which == 0) {
+      p->p->region_begin();
+    } else {
+      const float v = p->p->region_end();
+      if (ms) *ms = v;
+    }
+  });
+}
+
+int rp_pipeline_sync(rp_pipeline* p) {
+  return tguard([&] {
+    need(p, "pipeline");
+    p->p->sync();
+  });
+}
+
+int rp_pipeline_destroy(rp_pipeline* p) {
+  return tguard([&] { delete p; });
 }
 
 }  // extern "C"

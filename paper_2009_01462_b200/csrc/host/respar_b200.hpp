@@ -121,6 +121,7 @@ class StageScheduler {
   enum Mark { kBackwardDone = 0, kCorrectionDone = 1, kStageDone = 2, kNumMarks = 3 };
   void record(int j, Mark what);
   void wait(int k, int j, Mark what);
+  cudaEvent_t mark_event(int j, Mark what) const { return marks_.at((size_t)j * kNumMarks + what); }
   float last_ms() const;  // device time between begin() and end() (control stream)
   // device-timed region over many iterations on the control stream
   void region_begin();
@@ -183,6 +184,16 @@ class DecoupledTrainer {
   void set_graphs(bool on);
   bool graphs() const { return graphs_; }
   void correct_ghost(const StepParams& p, int row0, int nrows);
+  // the ghost boundary's correction on rows [row0 + sub0, row0 + sub0 + subn) of the batch
+  // [row0, row0 + nrows) (normaliser of the whole batch): the chunked exchange of the stage
+  // pipeline corrects each chunk as its adjoint rows arrive.  Elementwise kinds, one pass.
+  void correct_ghost_rows(const StepParams& p, int row0, int nrows, int sub0, int subn);
+  // ---- for the stage pipeline (pipeline.hpp), which drives step_local / correct_ghost_rows
+  // and may capture them into its own CUDA graph
+  void prepare(int nrows, const StepParams& p);          // buffers the step will use (no capture)
+  void note_replayed_step(int nrows, int row0);          // host bookkeeping of a replayed step
+  uint64_t kappa_zero_mask() const;
+  uint64_t alloc_epoch() const { return alloc_epoch_; }
   int stage_lo() const { return stage_lo_; }
   int stage_hi() const { return stage_hi_; }
   bool is_local(int k) const { return k >= stage_lo_ && k < stage_hi_; }
@@ -254,7 +265,8 @@ class DecoupledTrainer {
   void run_forward(Stage& st, const float* input, int nrows, float* out_features, cudaStream_t s);
   void run_backward(Stage& st, const int32_t* labels, int nrows, int row0, double beta, double lr, double momentum,
                     bool use_snapshot, cudaStream_t s);
-  void run_correction(int k, const StepParams& p, int row0, int nrows, bool fuse_kappa, cudaStream_t s);
+  void run_correction(int k, const StepParams& p, int row0, int nrows, bool fuse_kappa, cudaStream_t s,
+                      int sub0 = 0, int subn = -1);
   void check_rows(int row0, int nrows, const char* where) const;
   void need_local(int k, const char* where) const;
   bool owns_state(int k) const { return is_local(k) || k == stage_hi_; }
@@ -300,7 +312,6 @@ class DecoupledTrainer {
   cudaGraphExec_t graph_exec_ = nullptr;
   uint64_t graph_kernels_ = 0;   // kernel nodes of the captured iteration (launch accounting)
   void step_graphed(const float* batch_x, const int32_t* labels, int nrows, int row0, const StepParams& p);
-  uint64_t kappa_zero_mask() const;
   uint64_t alloc_epoch_ = 0;       // bumped whenever a buffer the step reads or writes moves
   void ensure_momentum();          // velocity buffers, allocated and zeroed synchronously
   void enable_peer_access();       // in-process multi-device: neighbouring stages read each other

@@ -639,12 +639,16 @@ void DecoupledTrainer::run_backward(Stage& st, const int32_t* labels, int nrows,
 
 // correct_aux + correct_multiplier (decoupled.cpp:135-170) for boundary k.
 void DecoupledTrainer::run_correction(int k, const StepParams& p, int row0, int nrows, bool fuse_kappa,
-                                      cudaStream_t s) {
+                                      cudaStream_t s, int sub0, int subn) {
   Stage& st = stages_[k];
   const Stage& prev = stages_[k - 1];
-  const int64_t off = (int64_t)row0 * feat();
-  const int64_t n = (int64_t)nrows * feat();
-  const long norm = normalizer(nrows, (int)feat());
+  if (subn < 0) subn = nrows - sub0;
+  const bool part = sub0 != 0 || subn != nrows;
+  if (part && (kind_ == PenaltyKind::LInf || (p.max_corrections > 1 && p.tau >= 0.0)))
+    throw std::logic_error("correction: a row sub-range needs an elementwise penalty and a single pass");
+  const int64_t off = (int64_t)(row0 + sub0) * feat();
+  const int64_t n = (int64_t)subn * feat();
+  const long norm = normalizer(nrows, (int)feat());   // # of the whole mini-batch slice
   const double w = p.beta / static_cast<double>(norm);
   float* lam = st.lam.get() + off;
   const float* xp = prev.bout.get() + off;
@@ -668,7 +672,7 @@ void DecoupledTrainer::run_correction(int k, const StepParams& p, int row0, int 
     }
     if (alm) check(rp_op_correct((int)kind_, lam, xp, pk, kap, n, w, 0.0, 0, coef, 1, st.red_ws.get(), s));
   }
-  if (alm) st.kappa_zero = false;
+  if (alm && !part) st.kappa_zero = false;
 }
 
 void DecoupledTrainer::reset_lambda_from_forward(const float* full_x) {
@@ -868,6 +872,33 @@ void DecoupledTrainer::step_graphed(const float* batch_x, const int32_t* labels,
   graph_key_.kappa_zero_mask = kappa_zero_mask();
   graph_valid_ = graph_key_.kappa_zero_mask == key.kappa_zero_mask;   // replayable as is
   cu(cudaGraphLaunch(graph_exec_, ctl), "cudaGraphLaunch");
+}
+
+void DecoupledTrainer::correct_ghost_rows(const StepParams& p, int row0, int nrows, int sub0, int subn) {
+  if (!has_ghost()) throw std::logic_error("correct_ghost: this trainer owns the last stage");
+  check_rows(row0, nrows, "correct_ghost");
+  if (sub0 < 0 || subn < 0 || sub0 + subn > nrows) throw std::invalid_argument("correct_ghost: bad row sub-range");
+  DeviceGuard g(stages_[stage_hi_ - 1].device);
+  run_correction(stage_hi_, p, row0, nrows, true, sched_->stream(stage_hi_ - 1), sub0, subn);
+  // the multiplier state is non-zero once the last chunk of an ALM correction ran
+  if (mode_ == TrainMode::Alm && sub0 + subn == nrows) stages_[stage_hi_].kappa_zero = false;
+}
+
+void DecoupledTrainer::prepare(int nrows, const StepParams& p) {
+  check_rows(0, nrows, "prepare");
+  ensure_capacity(nrows);
+  if (p.momentum != 0.0) ensure_momentum();
+}
+
+void DecoupledTrainer::note_replayed_step(int nrows, int row0) {
+  ++iteration_;
+  for (int k = stage_lo_; k < stage_hi_; ++k) {
+    Stage& st = stages_[k];
+    st.version = iteration_;
+    st.fwd_rows = nrows;
+    st.fwd_row0 = row0;
+  }
+  has_forward_ = true;
 }
 
 void DecoupledTrainer::correct_ghost(const StepParams& p, int row0, int nrows) {

@@ -27,8 +27,14 @@ One iteration on every rank, with one pair of point-to-point exchanges per bound
 Every correction of the reference's serial sweep (decoupled.cpp:189-192) reads only its
 own boundary's state, so running them on different ranks reproduces the reference's
 result bit for bit (tests/test_distributed.py checks this against the single-process
-trainer).  The engine is the CUDA trainer (``CudaStageEngine``) on B200; the transport
-ops run on the owning stage's CUDA stream, so NCCL overlaps nothing it must not.
+trainer).  The engine is the CUDA trainer (``CudaStageEngine``) on B200 or the oracle in
+the CPU tests; each transfer is posted on a stage stream after every local stage stream has
+been joined into it (``CudaStageEngine.join``), so nothing is sent before it is written.
+
+This torch.distributed form is the protocol's reference implementation (gloo-testable on
+CPU).  The B200 multi-GPU path is ``NcclStagePipeline`` below: the same protocol driven from
+the C++ host over NCCL (csrc/host/pipeline.hpp) with chunked, overlapped transfers on
+dedicated streams and CUDA-graph replay.
 
 When R > K the job runs R / K independent replicas of the K-stage pipeline ("replicas
 only": the reference has no data-parallel gradient exchange, so none is invented).
@@ -45,7 +51,7 @@ from ._lib import lib
 from .trainer import (BOUNDARY_ADJOINT, LAMBDA, MATH, ConfigError, Geometry, StepParams, _kind, _mode, check,
                       param_count)
 
-__all__ = ["StagePlacement", "placement", "CudaStageEngine", "DistributedDecoupledTrainer"]
+__all__ = ["StagePlacement", "placement", "CudaStageEngine", "DistributedDecoupledTrainer", "NcclStagePipeline"]
 
 
 @dataclass(frozen=True)
@@ -160,6 +166,21 @@ class CudaStageEngine:
         ext = self.torch.cuda.ExternalStream(s.value, device=f"cuda:{self.device}")
         return self.torch.cuda.stream(ext)
 
+    def join(self, k: int) -> None:
+        """Make stage k's stream wait for the work already queued on every local stage stream
+        (a transfer posted on stream k then sees data any local stage wrote)."""
+        ks = C.c_void_p()
+        check(lib().rp_trainer_stage_stream(self._h, k, C.byref(ks)))
+        target = self.torch.cuda.ExternalStream(ks.value, device=f"cuda:{self.device}")
+        for j in range(self.lo, min(self.hi + 1, self.stages)):
+            if j == k:
+                continue
+            s = C.c_void_p()
+            check(lib().rp_trainer_stage_stream(self._h, j, C.byref(s)))
+            ev = self.torch.cuda.Event()
+            ev.record(self.torch.cuda.ExternalStream(s.value, device=f"cuda:{self.device}"))
+            target.wait_event(ev)
+
     # -- algorithm --
     def reset(self, x_ptr: Optional[int]) -> None:
         check(lib().rp_trainer_reset_local(self._h, C.c_void_p(x_ptr) if x_ptr else None))
@@ -251,6 +272,9 @@ class DistributedDecoupledTrainer:
               [dist.P2POp(dist.irecv, t, peer, self.group) for t, peer in recvs]
         if not ops:
             return
+        join = getattr(self.engine, "join", None)
+        if join is not None:
+            join(k_stream)   # the sent rows may come from another local stage's stream
         with self.engine.stream(k_stream):
             for req in dist.batch_isend_irecv(ops):
                 req.wait()
@@ -362,3 +386,146 @@ class DistributedDecoupledTrainer:
         import torch
         return torch.zeros(1, dtype=torch.float64, device=f"cuda:{self.engine.device}")
 
+
+
+class NcclStagePipeline:
+    """``DecoupledTrainer::step`` across processes with the neighbour exchange driven from the
+    C++ host over NCCL (``rp_pipeline_*``, csrc/host/pipeline.hpp): p_k upstream and the
+    corrected lambda_k downstream in ``chunks`` row chunks on dedicated streams, overlapped with
+    the corrections, optionally captured in one CUDA graph per step.
+
+    ``members``: this process's stage ranges ``[(lo, hi, prev_peer, next_peer)]`` in stage order
+    (one per rank in a multi-process job -- ``for_rank``; several with peers == 0 in the
+    single-process loopback -- ``loopback``)."""
+
+    def __init__(self, geometry: Geometry, stages: int, mode, penalty, num_samples: int, device: int, members,
+                 nranks: int, rank: int, ids, chunks: int = 4, math: str = "fp32", seed_state: int = 0,
+                 params: Optional[np.ndarray] = None):
+        import torch   # loads the process's libnccl (torch's), which rp_comm_create then binds
+        self.torch = torch
+        self.geometry, self.stages, self.num_samples, self.device = geometry, stages, num_samples, device
+        self.members = [tuple(int(v) for v in m) for m in members]
+        self._g = geometry.c()
+        self._comms = []
+        self._trainers = []
+        self._h = C.c_void_p()
+        torch.cuda.set_device(device)
+        for idb in ids:
+            buf = (C.c_uint8 * 128).from_buffer_copy(idb)
+            h = C.c_void_p()
+            check(lib().rp_comm_create(buf, nranks, rank, device, C.byref(h)))
+            self._comms.append(h)
+        p = None if params is None else np.ascontiguousarray(params, dtype=np.float32)
+        for lo, hi, _, _ in self.members:
+            st = C.c_uint64(seed_state)
+            h = C.c_void_p()
+            check(lib().rp_trainer_create_local(C.byref(self._g), stages, _mode(mode), _kind(penalty), num_samples,
+                                                p.ctypes.data_as(C.POINTER(C.c_float)) if p is not None else None,
+                                                C.byref(st), MATH[math], device, lo, hi, C.byref(h)))
+            self._trainers.append(h)
+        n = len(self.members)
+        arr = (C.c_void_p * n)(*[t.value for t in self._trainers])
+        prev = (C.c_int32 * n)(*[m[2] for m in self.members])
+        nxt = (C.c_int32 * n)(*[m[3] for m in self.members])
+        check(lib().rp_pipeline_create(self._comms[0], self._comms[1], arr, prev, nxt, n, chunks, C.byref(self._h)))
+        self.first = self.members[0][0] == 0
+        self.last = self.members[-1][1] == stages
+        self.nparams = param_count(geometry)
+
+    @staticmethod
+    def unique_ids(count: int = 2):
+        out = []
+        for _ in range(count):
+            buf = (C.c_uint8 * 128)()
+            check(lib().rp_comm_unique_id(buf))
+            out.append(bytes(buf))
+        return out
+
+    @classmethod
+    def for_rank(cls, geometry: Geometry, stages: int, mode, penalty, num_samples: int, plc: StagePlacement,
+                 device: int, group=None, **kw):
+        """One process per GPU: this rank's stages [plc.lo, plc.hi); the two communicators span
+        every rank of the job (the ids travel from rank 0 over torch.distributed)."""
+        import torch.distributed as dist
+        ids = [cls.unique_ids(2) if plc.rank == 0 else None]
+        dist.broadcast_object_list(ids, src=0, group=group)
+        m = [(plc.lo, plc.hi, -1 if plc.prev_rank is None else plc.prev_rank,
+              -1 if plc.next_rank is None else plc.next_rank)]
+        return cls(geometry, stages, mode, penalty, num_samples, device, m, plc.world, plc.rank, ids[0], **kw)
+
+    @classmethod
+    def loopback(cls, geometry: Geometry, stages: int, mode, penalty, num_samples: int, splits, device: int = 0,
+                 **kw):
+        """One process, one rank: the stages split into consecutive members at ``splits``
+        (e.g. [2] for K = 4: [0, 2) and [2, 4)), exchanging with themselves over NCCL."""
+        bounds = [0] + list(splits) + [stages]
+        m = [(bounds[i], bounds[i + 1], -1 if i == 0 else 0, -1 if i == len(bounds) - 2 else 0)
+             for i in range(len(bounds) - 1)]
+        return cls(geometry, stages, mode, penalty, num_samples, device, m, 1, 0, cls.unique_ids(2), **kw)
+
+    def close(self):
+        if getattr(self, "_h", None) is not None and self._h.value:
+            lib().rp_pipeline_destroy(self._h)
+            self._h = C.c_void_p()
+        for t in getattr(self, "_trainers", []):
+            lib().rp_trainer_destroy(t)
+        self._trainers = []
+        for c in getattr(self, "_comms", []):
+            lib().rp_comm_destroy(c)
+        self._comms = []
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    # -- algorithm --
+    def reset_lambda_from_forward(self, x_ptr: Optional[int]) -> None:
+        check(lib().rp_pipeline_reset_lambda_from_forward(self._h, C.c_void_p(x_ptr) if x_ptr else None))
+
+    def step(self, x_ptr: Optional[int], labels_ptr: Optional[int], nrows: int, row0: int, sp: StepParams,
+             read_loss: bool = False) -> Optional[float]:
+        loss = C.c_double()
+        check(lib().rp_pipeline_step(self._h, C.c_void_p(x_ptr) if x_ptr else None,
+                                     C.c_void_p(labels_ptr) if labels_ptr else None, nrows, row0,
+                                     C.byref(sp.c()), C.byref(loss) if (read_loss and self.last) else None))
+        return loss.value if (read_loss and self.last) else None
+
+    def loss(self) -> float:
+        v = C.c_double()
+        check(lib().rp_pipeline_loss(self._h, C.byref(v)))
+        return v.value
+
+    def set_graphs(self, on: bool) -> None:
+        check(lib().rp_pipeline_set_graphs(self._h, 1 if on else 0))
+
+    def region(self, which: int) -> float:
+        ms = C.c_float()
+        check(lib().rp_pipeline_region(self._h, which, C.byref(ms)))
+        return ms.value
+
+    def sync(self) -> None:
+        check(lib().rp_pipeline_sync(self._h))
+
+    # -- state (the members' stages; params: the local stages' slices, other entries 0) --
+    def params(self) -> np.ndarray:
+        out = np.zeros(self.nparams, np.float32)
+        tmp = np.zeros(self.nparams, np.float32)
+        for t in self._trainers:
+            tmp[:] = 0
+            check(lib().rp_trainer_get_params(t, tmp.ctypes.data_as(C.POINTER(C.c_float))))
+            out += tmp
+        return out
+
+    def state(self, k: int, which: int) -> np.ndarray:
+        """lambda / kappa of boundary k come from the member that corrects it (the one holding
+        stage k-1, as a ghost when k is another member's first stage)."""
+        g = self.geometry
+        out = np.empty((self.num_samples, g.height, g.width, g.channels), np.float32)
+        for (lo, hi, _, _), t in zip(self.members, self._trainers):
+            owner = (lo < k <= hi) if which in (0, 1) else (lo <= k < hi)
+            if owner:
+                check(lib().rp_trainer_get_state(t, k, which, out.ctypes.data_as(C.POINTER(C.c_float))))
+                return out
+        raise ConfigError(f"state: boundary {k} is not held by this process")
