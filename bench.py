@@ -189,15 +189,8 @@ def run_ours(args, cfg, rank, world):
             os.environ.pop("RP_CONCURRENT_STAGES", None)
 
     tr = make_trainer(concurrent)
-    # synthetic data, device-resident: pixels U[-1,1) from the splitmix64 stream (seed 1 + rank),
-    # labels uniform over the classes
-    x = torch.empty(B * g.raw_size, dtype=torch.float32, device="cuda")
-    st = C.c_uint64(1000 + rank)
-    rp.check(lib().rp_op_fill_uniform(C.c_void_p(x.data_ptr()), x.numel(), C.byref(st), -1.0, 1.0, 1.0, None))
-    gen = torch.Generator(device="cuda")
-    gen.manual_seed(7 + rank)
-    y = torch.randint(0, CLASSES, (B,), dtype=torch.int32, device="cuda", generator=gen)
-    torch.cuda.synchronize()
+    # synthetic data, device-resident, from the reference's RNG stream (seed 1000 + replica)
+    x, y = synthetic_data(cfg, B, 1000 + rank, torch, rp, lib)
     x_host = x.cpu().numpy().reshape(B, cfg['h'], cfg['w'], cfg['cin'])
     tr.reset_lambda_from_forward(x_host)
     sp = step_params(cfg)
@@ -206,6 +199,8 @@ def run_ours(args, cfg, rank, world):
     for _ in range(args.warmup):
         tr.step_device(x.data_ptr(), y.data_ptr(), B, 0, sp, read_loss=False)
     torch.cuda.synchronize()
+    settle_steps, settle_s = settle(lambda: tr.step_device(x.data_ptr(), y.data_ptr(), B, 0, sp, read_loss=False),
+                                    args.settle_s, torch.cuda.synchronize)
     if world > 1:
         import torch.distributed as dist
         dist.barrier()
@@ -266,18 +261,20 @@ def run_ours(args, cfg, rank, world):
     lib().rp_profile_enable(0)
     prof = profile_classes()
     return dict(tr=tr, total_ms=total_ms, prof=prof, clocks=clk, launches=launches, loss=loss, e2e_s=e2e_s,
-                B=B, K=K, g=g, prof_steps=prof_steps, concurrent=concurrent)
+                B=B, K=K, g=g, prof_steps=prof_steps, concurrent=concurrent, settle=(settle_steps, settle_s))
 
 
 def run_ours_distributed(args, cfg, rank, world):
     """N > 1: one process per GPU, stage k of the K-stage pipeline on rank floor(k G / K)
-    (paper_2009_01462_b200/distributed.py); N > K runs N / K pipeline replicas, each on
-    its own synthetic batch.  Neighbour exchange over NCCL point-to-point."""
+    (paper_2009_01462_b200/distributed.py: placement); N > K runs N / K pipeline replicas, each
+    on its own synthetic batch.  The step runs on the C++-host NCCL pipeline
+    (NcclStagePipeline, csrc/host/pipeline.hpp): chunked p / lambda transfers on dedicated
+    streams overlapped with the corrections, the whole step replayed from one CUDA graph."""
     import torch
     import torch.distributed as dist
     import paper_2009_01462_b200 as rp
     from paper_2009_01462_b200._lib import lib
-    from paper_2009_01462_b200.distributed import CudaStageEngine, DistributedDecoupledTrainer, placement
+    from paper_2009_01462_b200.distributed import NcclStagePipeline, placement
 
     dev = int(os.environ.get("LOCAL_RANK", "0"))
     torch.cuda.set_device(dev)
@@ -287,57 +284,45 @@ def run_ours_distributed(args, cfg, rank, world):
         raise SystemExit("bench: the serial config runs on one GPU (K = 1)")
     mode = {"alm": rp.ALM, "penalty": rp.PENALTY}[cfg["mode"]]
     plc = placement(K, world, rank)
-    # several stages per rank (N < K): concurrent stage streams as at N = 1; the roofline pass
-    # then times overlapping kernels (noted in the line), one stage per rank is unaffected
+    # several stages per rank (N < K): concurrent stage streams as at N = 1
     concurrent = bool(cfg.get("concurrent")) and not args.serial_stages and plc.hi - plc.lo > 1
     os.environ["RP_CONCURRENT_STAGES"] = "1" if concurrent else "0"
     try:
-        eng = CudaStageEngine(g, K, mode, rp.SQUARED_L2, B, plc.lo, plc.hi, dev, seed_state=_splitmix(1),
-                              math=args.math or cfg["math"])
+        tr = NcclStagePipeline.for_rank(g, K, mode, rp.SQUARED_L2, B, plc, dev, seed_state=_splitmix(1),
+                                        math=args.math or cfg["math"], chunks=args.chunks)
     finally:
         os.environ.pop("RP_CONCURRENT_STAGES", None)
-    tr = DistributedDecoupledTrainer(eng, plc)
-    x = torch.empty(B * g.raw_size, dtype=torch.float32, device="cuda")
-    st = C.c_uint64(1000 + plc.replica)
-    rp.check(lib().rp_op_fill_uniform(C.c_void_p(x.data_ptr()), x.numel(), C.byref(st), -1.0, 1.0, 1.0, None))
-    gen = torch.Generator(device="cuda")
-    gen.manual_seed(7 + plc.replica)
-    y = torch.randint(0, CLASSES, (B,), dtype=torch.int32, device="cuda", generator=gen)
-    torch.cuda.synchronize()
-    tr.reset_lambda_from_forward(x.data_ptr(), B)
+    x, y = synthetic_data(cfg, B, 1000 + plc.replica, torch, rp, lib)
+    tr.reset_lambda_from_forward(x.data_ptr() if plc.first else None)
     sp = step_params(cfg)
+    tr.set_graphs(not args.no_graphs)
     xp = x.data_ptr() if plc.first else None
     yp = y.data_ptr() if plc.last else None
     for _ in range(args.warmup):
         tr.step(xp, yp, B, 0, sp)
-    torch.cuda.synchronize()
+    tr.sync()
+    settle_steps, settle_s = settle(lambda: tr.step(xp, yp, B, 0, sp), args.settle_s, tr.sync)
     dist.barrier()
     torch.cuda.synchronize()
     clocks = ClockSampler(dev)
     clocks.start()
     n0 = rp.launch_count()
-    eng.region(0)
+    tr.region(0)
     for _ in range(args.steps):
         tr.step(xp, yp, B, 0, sp)
-    total_ms = eng.region(1)
-    torch.cuda.synchronize()
+    total_ms = tr.region(1)
     launches = rp.launch_count() - n0
     clk = clocks.stop()
-    lib().rp_profile_enable(1)       # profiled pass for the roofline classes (untimed)
-    profile_classes()
-    prof_steps = min(args.steps, 5)
-    for _ in range(prof_steps):
-        tr.step(xp, yp, B, 0, sp)
-    torch.cuda.synchronize()
-    lib().rp_profile_enable(0)
-    prof = profile_classes()
     t = torch.tensor([total_ms], device="cuda")
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     total_ms = float(t.item())
-    loss = tr.loss()
+    # the last stage's loss, to every rank (a scalar, off the data path)
+    lt = torch.tensor([tr.loss() if plc.last else 0.0], dtype=torch.float64, device="cuda")
+    dist.all_reduce(lt, op=dist.ReduceOp.SUM)
+    loss = float(lt.item()) / max(1, plc.replicas)
 
-    # e2e: pinned host batch -> device (stage 0 rank: pixels, last-stage rank: labels), the
-    # step, the loss read back on every rank; wall clock, max over ranks
+    # e2e: pinned host batch -> device (stage-0 rank: pixels, last-stage rank: labels), the
+    # step, the loss read back on the last-stage rank; wall clock, max over ranks
     x_host = x.cpu().pin_memory()
     y_host = y.cpu().pin_memory()
     e2e_steps = max(1, min(args.steps, 10))
@@ -350,12 +335,63 @@ def run_ours_distributed(args, cfg, rank, world):
             y.copy_(y_host, non_blocking=True)
         torch.cuda.current_stream().synchronize()
         tr.step(xp, yp, B, 0, sp, read_loss=True)
-    torch.cuda.synchronize()   # every local stage's stream, not only the one the loss came from
+    tr.sync()
     e2e_s = torch.tensor([(time.perf_counter() - t0) / e2e_steps], device="cuda")
     dist.all_reduce(e2e_s, op=dist.ReduceOp.MAX)
+
+    # profiled pass for the roofline classes (untimed, eager launches)
+    tr.set_graphs(False)
+    lib().rp_profile_enable(1)
+    profile_classes()
+    prof_steps = min(args.steps, 5)
+    for _ in range(prof_steps):
+        tr.step(xp, yp, B, 0, sp)
+    tr.sync()
+    lib().rp_profile_enable(0)
+    prof = profile_classes()
     return dict(tr=tr, total_ms=total_ms, prof=prof, clocks=clk, launches=launches, loss=loss,
                 e2e_s=float(e2e_s.item()), B=B, K=K, g=g, replicas=plc.replicas, plc=plc, prof_steps=prof_steps,
-                concurrent=concurrent, prof_concurrent=concurrent)
+                concurrent=concurrent, prof_concurrent=concurrent, settle=(settle_steps, settle_s))
+
+
+def reference_labels(seed, n_before, count):
+    """next_u64() % 10 for draws n_before .. n_before + count - 1 of Rng(seed)
+    (tensor.cpp:163-169: draw i = mix(seed + (i + 1) gamma))."""
+    M = (1 << 64) - 1
+    out = []
+    for j in range(count):
+        z = (seed + (n_before + j + 1) * 0x9E3779B97F4A7C15) & M
+        z = ((z ^ (z >> 30)) * 0xBF58476D1CE4E5B9) & M
+        z = ((z ^ (z >> 27)) * 0x94D049BB133111EB) & M
+        out.append((z ^ (z >> 31)) % CLASSES)
+    return out
+
+
+def synthetic_data(cfg, B, seed, torch, rp, lib):
+    """The reference's synthetic batch (acceptance.cpp:69-73 pattern): pixels
+    rng_uniform(B H W Cin, -1, 1) from Rng(seed) (tensor.cpp:177-185; filled on device by the
+    same splitmix64 stream), then labels next_u64() % 10 from the draws that follow."""
+    n = B * cfg["h"] * cfg["w"] * cfg["cin"]
+    x = torch.empty(n, dtype=torch.float32, device="cuda")
+    st = C.c_uint64(seed)
+    rp.check(lib().rp_op_fill_uniform(C.c_void_p(x.data_ptr()), n, C.byref(st), -1.0, 1.0, 1.0, None))
+    y = torch.tensor(reference_labels(seed, n, B), dtype=torch.int32, device="cuda")
+    torch.cuda.synchronize()
+    return x, y
+
+
+def settle(step_fn, seconds, sync):
+    """Untimed steps beyond the warm-up until the part has run the step for `seconds` (its
+    clocks reach the power-capped steady state the timed steps then measure)."""
+    n = 0
+    t0 = time.perf_counter()
+    while seconds > 0 and time.perf_counter() - t0 < seconds:
+        step_fn()
+        n += 1
+        if n % 8 == 0:
+            sync()
+    sync()
+    return n, time.perf_counter() - t0
 
 
 def _splitmix(seed):
@@ -390,6 +426,25 @@ def cpu_reference_sample(cfg, images, workers):
     return time.perf_counter() - t0
 
 
+def cpu_port_sample(cfg, images):
+    """The CPU restatement of the same 3x3-conv step (oracle/respar_oracle.py, numpy fp64, the
+    checker the parity tests use) on a sample of `images`: seconds per step.  Secondary CPU
+    baseline: the reference itself has no convolution."""
+    import numpy as np
+    from oracle import respar_oracle as O
+    og = O.Geometry(cfg["cin"], cfg["h"], cfg["w"], cfg["c"], cfg["ch"], cfg["L"], CLASSES)
+    net = O.make_net(og, O.Rng(1))
+    x, y = O.synthetic_batch(og, images, seed=1000)
+    mode = {"alm": O.ALM, "penalty": O.PENALTY, "serial": O.PENALTY}[cfg["mode"]]
+    tr = O.DecoupledTrainer(net, cfg["K"], mode, O.SQUARED_L2, images)
+    tr.reset_lambda_from_forward(x)
+    beta = 0.1 if cfg["mode"] == "alm" else 1.0
+    t0 = time.perf_counter()
+    tr.step(x, y, 0, O.StepParams(beta=beta, tau=-1.0, lr=cfg.get("lr", 0.1), lambda_lr=cfg.get("lr", 0.1),
+                                  kappa_lr=KAPPA_STEP * 2.0 * beta / (images * og.feature_size)))
+    return time.perf_counter() - t0
+
+
 def run_reference(args, cfg, rank, world):
     if rank != 0:
         return
@@ -408,11 +463,13 @@ def run_reference(args, cfg, rank, world):
     v = images / per_step
     line = {
         "metric": METRIC, "value": v, "unit": "images/s", "impl": "reference", "n_gpus": args.gpus,
-        "steps": args.steps, "warmup": args.warmup, "ms_per_step": per_step * 1e3 * cfg["B"] / images,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": per_step * 1e3,
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic",
         "config": {"workload": f"{args.config}: reference DecoupledTrainer::step (fp64 CPU) on the dense 1x1-conv "
-                               f"analogue rows=images*H*W", **_cfg_json(cfg)},
+                               f"analogue rows=images*H*W", **_cfg_json(cfg),
+                   "sample_images_per_step": images,
+                   "ms_per_step_is": f"the measured time of one step on the {images}-image sample"},
         "cpu_baseline": {"value": v, "unit": "images/s", "cores": workers, "kind": "reference",
                          "sample": f"{images} image(s) x {cfg['h']}x{cfg['w']} rows per step, one "
                                    f"DecoupledTrainer::step, StagePool with {workers} workers"},
@@ -422,18 +479,52 @@ def run_reference(args, cfg, rank, world):
 
 
 def _cfg_json(cfg):
+    beta = 0.1 if cfg["mode"] == "alm" else 1.0
+    n = cfg["B"] * cfg["h"] * cfg["w"] * cfg["c"]
+    operands = {"fp32": "fp16x2 plane pairs (22-bit significands, power-of-two scales), fp32 accumulate",
+                "bf16": "bf16 operands, fp32 accumulate", "tf32": "tf32 operands, fp32 accumulate",
+                "simt": "fp32 CUDA cores"}[cfg["math"]]
     return {"in": [cfg["cin"], cfg["h"], cfg["w"]], "global_batch": cfg["B"], "channels": cfg["c"],
             "hidden": cfg["ch"], "blocks": cfg["L"], "stages": cfg["K"], "mode": cfg["mode"],
-            "math": cfg["math"], "classes": CLASSES, "lr": cfg.get("lr", 0.1)}
+            "math": cfg["math"], "conv_operands": operands, "classes": CLASSES, "lr": cfg.get("lr", 0.1),
+            "beta": beta, "lambda_lr": cfg.get("lr", 0.1),
+            "kappa_lr": KAPPA_STEP * 2.0 * beta / n if cfg["mode"] == "alm" else None,
+            "kappa_step": KAPPA_STEP if cfg["mode"] == "alm" else None, "penalty": "squared_l2",
+            "data_rng": "reference splitmix64 (seed 1000 + replica): pixels U[-1,1), then labels next_u64() % 10"}
+
+
+def spawn_ranks(n, check_devices=True):
+    """--gpus N outside torchrun: re-launch this command under torch.distributed.run with N
+    ranks (one per GPU, rendezvous on 127.0.0.1); the ranks' output is this process's."""
+    import socket
+    try:
+        import torch
+        avail = torch.cuda.device_count()
+    except Exception:
+        avail = 0
+    if check_devices and avail < n:
+        raise SystemExit(f"bench: --gpus {n} but only {avail} CUDA device(s) are visible")
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr=127.0.0.1", f"--master-port={port}", os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.run(cmd).returncode
 
 
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=10)
-    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--steps", type=int, default=100)
+    ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--config", default="C2", choices=sorted(CONFIGS))
+    ap.add_argument("--config", default="C3", choices=sorted(CONFIGS))
+    ap.add_argument("--settle-s", type=float, default=1.5,
+                    help="untimed steps after the warm-up for this many seconds (clocks at their sustained, "
+                         "power-capped level before the timed steps); 0 disables")
+    ap.add_argument("--chunks", type=int, default=4, help="N > 1: row chunks of the p / lambda exchange")
+    ap.add_argument("--cpu-port-images", type=int, default=1,
+                    help="images of the 3x3 CPU restatement sample (secondary CPU baseline; 0 disables)")
     ap.add_argument("--math", default=None, choices=[None, "fp32", "tf32", "bf16", "simt"])
     ap.add_argument("--ref-images", type=int, default=2)
     ap.add_argument("--cpu-images", type=int, default=4)
@@ -441,6 +532,9 @@ def main():
     ap.add_argument("--no-graphs", action="store_true", help="launch every kernel eagerly (no CUDA graph replay)")
     ap.add_argument("--serial-stages", action="store_true",
                     help="stages sharing the GPU on one stream also in the timed run (default: concurrent for C2/C3)")
+    ap.add_argument("--plan", action="store_true",
+                    help="print each rank's stages and neighbours (one JSON line per rank) and exit: the launcher "
+                         "and placement without a GPU")
     ap.add_argument("--dist-path", action="store_true",
                     help="run the one-process-per-GPU stage-sharded path even at N=1 (smoke of the N>1 code)")
     args = ap.parse_args()
@@ -451,7 +545,21 @@ def main():
     world = int(os.environ.get("WORLD_SIZE", "1"))
 
     if args.impl == "reference":
+        # the reference arm is a CPU run: rank 0 alone (the other ranks of a torchrun exit 0)
         run_reference(args, cfg, rank, world)
+        return
+
+    if "WORLD_SIZE" not in os.environ and args.gpus > 1:
+        sys.exit(spawn_ranks(args.gpus, check_devices=not args.plan))
+    if world != args.gpus:
+        raise SystemExit(f"bench: --gpus {args.gpus} but WORLD_SIZE={world}: launch one rank per GPU "
+                         f"(torchrun --nproc-per-node {args.gpus}) or drop the torchrun environment")
+    if args.plan:
+        from paper_2009_01462_b200.distributed import placement
+        plc = placement(cfg["K"], world, rank)
+        print(json.dumps({"rank": rank, "world": world, "local_rank": int(os.environ.get("LOCAL_RANK", "0")),
+                          "stages": [plc.lo, plc.hi], "prev_rank": plc.prev_rank, "next_rank": plc.next_rank,
+                          "replica": plc.replica, "replicas": plc.replicas}), flush=True)
         return
 
     distributed = world > 1 or args.dist_path
@@ -487,10 +595,10 @@ def main():
             tj = json.load(f)
             t = tj.get(f"{args.config}:{dom}") or tj.get(dom)
         traffic = t["bytes_per_launch"] if t else None
-    # the fp32-accurate kernels run every fp32 MAC as 4 bf16 tensor products (the plane path:
-    # [W0; W1] x {x0, x1} in fprop / dgrad, [g0; g1] x [x0 x1] in wgrad): their
-    # own ceiling is the bf16 peak / 4, reported beside the prescribed bf16-peak fraction
-    # together with the bf16 tensor work actually issued
+    # the fp32-accurate kernels run every fp32 MAC as 4 fp16 tensor products (the plane path:
+    # [W0; W1] x {x0, x1} in fprop / dgrad, [g0; g1] x [x0 x1] in wgrad; fp16
+    # and bf16 MMAs run at the same rate): their own ceiling is the 16-bit peak / 4, reported
+    # beside the prescribed bf16-peak fraction together with the tensor work actually issued
     split = {"fp32": 4.0, "tf32": 2.0, "bf16": 1.0, "simt": None}.get(cfg["math"])
     ceiling = peaks["bf16_tflops_sustained"] / split if split else None
     roof = {"bound": "tensor", "kernel": dom, "achieved": achieved_tf,
@@ -499,8 +607,8 @@ def main():
             "traffic_unit": "bytes per launch (ncu --set full, profiles/traffic.json)",
             "math_ceiling": {"tflops": ceiling, "frac": achieved_tf / ceiling if ceiling else None,
                              "tensor_tflops_issued": achieved_tf * split if split else None,
-                             "note": "bf16 sustained peak / bf16 tensor products per fp32-equivalent MAC "
-                                     "(fp32 plane path: 4; bf16: 1)"},
+                             "note": "bf16 sustained peak / 16-bit tensor products per fp32-equivalent MAC "
+                                     "(fp32 plane path: 4 fp16 products; bf16: 1)"},
             "peak_source": f"{peaks_kind} bf16 dense sustained (MEASURED_PEAKS.json)",
             "kernel_timing": ("per-launch CUDA events with this rank's stages on concurrent streams (overlapping "
                               "kernels: upper bounds)") if r.get("prof_concurrent") else
@@ -521,9 +629,10 @@ def main():
         "config": {"workload": f"{args.config}: ODE-ResNet {cfg['cin']}x{cfg['h']}x{cfg['w']}, batch {B}, "
                                f"C={cfg['c']}, L={cfg['L']}, K={K} stages, {cfg['mode']}, math {cfg['math']}",
                    **_cfg_json(cfg),
-                   "parallelism": f"{K} stages on {min(world, K)} GPU(s) (stage k on rank floor(k G / K), NCCL "
-                                  f"point-to-point neighbour exchange)" + (f" x {replicas} replicas" if replicas > 1
-                                                                           else "")
+                   "parallelism": f"{K} stages on {min(world, K)} GPU(s) (stage k on rank floor(k G / K); N > 1: "
+                                  f"C++-host NCCL point-to-point exchange of p / lambda in {args.chunks} chunks on "
+                                  f"dedicated streams, CUDA-graph replay)" + (f" x {replicas} replicas" if replicas > 1
+                                                                             else "")
                                   + ("; stages sharing a GPU on concurrent streams" if r.get("concurrent") else ""),
                    "l2": "inputs larger than L2 (per-iteration working set > 2 GB)",
                    "model_flops_per_iter": flops_iter,
@@ -537,8 +646,19 @@ def main():
         "roofline": roof,
         "e2e": {"value": replicas * B / r["e2e_s"], "unit": "images/s",
                 "h2d_bytes_per_step": replicas * (B * r["g"].raw_size * 4 + B * 4),
-                "d2h_bytes_per_step": 8 * world},
+                "d2h_bytes_per_step": 8 * replicas},
     }
+    line["config"]["settle"] = {"untimed_steps": r["settle"][0], "seconds": round(r["settle"][1], 3),
+                                "note": "after the W warm-up steps, before the K timed steps"}
+    if not args.no_cpu_baseline and args.cpu_port_images > 0:
+        try:
+            t = cpu_port_sample(cfg, args.cpu_port_images)
+            line["cpu_baseline_3x3"] = {"value": args.cpu_port_images / t, "unit": "images/s", "cores": os.cpu_count(),
+                                        "kind": "port",
+                                        "sample": f"{args.cpu_port_images} image(s) of the 3x3-conv network, one step "
+                                                  f"of oracle/respar_oracle.py (numpy fp64, BLAS threads)"}
+        except Exception as e:  # reported, never fatal
+            line["cpu_baseline_3x3"] = {"value": None, "unit": "images/s", "sample": f"failed: {e}"}
     if not args.no_cpu_baseline:
         try:
             workers = min(K, os.cpu_count() or 1)

@@ -642,13 +642,24 @@ __global__ void __launch_bounds__(kThreads, 1)
               ax[b * kEpiJ + j] = o >= 0 ? __ldg(reinterpret_cast<const float4*>(auxb + o)) : make_float4(0.f, 0.f, 0.f, 0.f);
             }
         }
+        // batch b's accumulators are loaded while batch b - 1 is finished (double-buffered
+        // registers: the TMEM load latency is off the critical path)
+        uint32_t rn[kEpiB];
+        if (nb > 0) {
+          if constexpr (kEpiB == 16) tmem_ld16(tcol, rn);
+          else tmem_ld8(tcol, *reinterpret_cast<uint32_t(*)[8]>(&rn[0]));
+        }
 #pragma unroll
         for (int b = 0; b < 128 / kEpiB; ++b) {
           if (b < nb) {   // group-uniform
             uint32_t r[kEpiB];
-            if constexpr (kEpiB == 16) tmem_ld16(tcol + (uint32_t)(b * kEpiB), r);
-            else tmem_ld8(tcol + (uint32_t)(b * kEpiB), *reinterpret_cast<uint32_t(*)[8]>(&r[0]));
             tmem_wait_ld();
+#pragma unroll
+            for (int e = 0; e < kEpiB; ++e) r[e] = rn[e];
+            if (b + 1 < nb) {
+              if constexpr (kEpiB == 16) tmem_ld16(tcol + (uint32_t)((b + 1) * kEpiB), rn);
+              else tmem_ld8(tcol + (uint32_t)((b + 1) * kEpiB), *reinterpret_cast<uint32_t(*)[8]>(&rn[0]));
+            }
             asm volatile("bar.sync %0, 128;" ::"r"(grp_bar) : "memory");   // buf free
 #pragma unroll
             for (int e = 0; e < kEpiB; ++e) wrow[e * 64] = __uint_as_float(r[e]);
