@@ -226,3 +226,40 @@ def test_oracle_vs_live_reference(K, mode, kind):
             b = tr.step(xo[r0:r0 + 5], y[r0:r0 + 5], r0, sp)
             assert abs(a - b) <= 1e-12 * max(1.0, abs(a))
     assert rel_err(O.extract_dense_params(g, net.flat()), ref.params()) <= TIGHT
+
+
+def test_torch64_oracle_matches_numpy_oracle():
+    """oracle/respar_torch64.py (the BASELINE-size checker of tests/test_gpu_configs.py) is the
+    numpy oracle restated over torch fp64: equal to it at 1e-12 over 3 ALM steps with lambda
+    perturbed and kappa non-zero, for the step's loss, parameters, lambda, kappa, X_end and p."""
+    import torch
+    from oracle import respar_torch64 as T
+    og = O.Geometry(3, 6, 5, 8, 8, 4, 10, step_h=0.7)
+    net = O.make_net(og, O.Rng(3))
+    x, y = O.synthetic_batch(og, 6, seed=4)
+    K = 2
+    on = O.DecoupledTrainer(net.copy(), K, O.ALM, O.SQUARED_L2, 6)
+    tn = T.DecoupledTrainer(T.Net(og, net.flat(), "cpu"), K, T.ALM, T.SQUARED_L2, 6)
+    on.reset_lambda_from_forward(x)
+    tn.reset_lambda_from_forward(torch.from_numpy(x))
+    rng = O.Rng(9)
+    lam = on.stage(1).lam + O.rng_uniform(rng, on.stage(1).lam.size, -0.1, 0.1).reshape(on.stage(1).lam.shape)
+    kap = O.rng_uniform(rng, lam.size, -1e-3, 1e-3).reshape(lam.shape)
+    on.stage(1).lam[...] = lam
+    on.stage(1).kappa[...] = kap
+    tn.lam[1][...] = torch.from_numpy(lam)
+    tn.kappa[1][...] = torch.from_numpy(kap)
+    sp = O.StepParams(beta=0.5, lr=0.05, lambda_lr=0.05, kappa_lr=1e-3)
+    yt = torch.from_numpy(y.astype(np.int64))
+    for r0, nr in ((0, 6), (0, 3), (3, 3)):
+        a = on.step(x[r0:r0 + nr], y[r0:r0 + nr], r0, sp)
+        b = tn.step(torch.from_numpy(x[r0:r0 + nr]), yt[r0:r0 + nr], r0, sp)
+        assert abs(a - b) <= 1e-12 * abs(a)
+    assert rel_err(tn.net.flat(), on.net.flat()) <= 1e-12
+    for k in range(K):
+        assert rel_err(tn.bout[k].numpy(), on.stage(k).boundary_out) <= 1e-12
+        assert rel_err(tn.badj[k].numpy(), on.stage(k).boundary_adjoint) <= 1e-11
+    assert rel_err(tn.lam[1].numpy(), on.stage(1).lam) <= 1e-12
+    assert rel_err(tn.kappa[1].numpy(), on.stage(1).kappa) <= 1e-11
+    ranges = O.partition(og.blocks, K)
+    assert rel_err(T.grads_flat(og, tn.last_grads, ranges), O.grads_flat(og, on.last_grads, ranges)) <= 1e-11
