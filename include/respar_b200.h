@@ -280,6 +280,12 @@ int rp_op_head_loss_bwd_planes(const rp_geometry* g, int32_t nrows, const float*
                                const float* pt, const int32_t* labels, double* loss_dev, float* gt, float* g_out,
                                void* p0, void* p1, float* scale, void* ws, int64_t ws_bytes, void* stream);
 /* Argmax hits (accuracy, network.cpp:223-234; ties -> lowest class); *hits host. */
+/* loss_phi's value and accuracy of device logits [nrows, classes] (network.cpp:193-234), both
+ * reduced on device in a fixed order: *loss (host) = mean softmax-CE (fp64), *hits (host) =
+ * argmax hits (ties to the lowest class); pred (device, nullable) = per-row argmax. */
+int64_t rp_op_eval_workspace_bytes(int32_t nrows);
+int rp_op_eval_loss_accuracy(const float* logits, const int32_t* labels, int32_t nrows, int32_t classes,
+                             double* loss, int64_t* hits, int32_t* pred, void* ws, int64_t ws_bytes, void* stream);
 int rp_op_argmax_hits(const float* logits, const int32_t* labels, int32_t nrows, int32_t classes,
                       int64_t* hits, void* ws, void* stream);
 
@@ -363,6 +369,11 @@ int rp_trainer_get_state(rp_trainer* t, int32_t k, int32_t which, float* host);
 int rp_trainer_set_state(rp_trainer* t, int32_t k, int32_t which, const float* host);
 /* Full serial forward (eval, decoupled.cpp:332-347): logits host [n, classes]. */
 int rp_trainer_forward(rp_trainer* t, const float* x_host, int32_t nrows, float* logits_host);
+/* Evaluation on device (decoupled.cpp:332-347: the full serial forward, then loss_phi and
+ * accuracy, network.cpp:193-234): *loss = mean softmax-CE, *accuracy = argmax hits / nrows
+ * (ties to the lowest class).  Labels are validated (std::invalid_argument). */
+int rp_trainer_evaluate(rp_trainer* t, const float* x_host, const int32_t* labels_host, int32_t nrows,
+                        double* loss, double* accuracy);
 int64_t rp_trainer_iteration(rp_trainer* t);
 int32_t rp_trainer_stages(rp_trainer* t);
 /* Device-side timing of the last step: max over stage streams (ms). */

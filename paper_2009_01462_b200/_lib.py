@@ -129,6 +129,9 @@ SIGNATURES = {
     "rp_trainer_last_step_ms": (C.c_int, [_P, C.POINTER(C.c_float)]),
     "rp_serial_train_step": (C.c_int, [_P, _F, _I32, C.c_int32, C.c_double, _D]),
     "rp_trainer_region": (C.c_int, [_P, C.c_int32, C.POINTER(C.c_float)]),
+    "rp_op_eval_workspace_bytes": (C.c_int64, [C.c_int32]),
+    "rp_op_eval_loss_accuracy": (C.c_int, [_P, _P, C.c_int32, C.c_int32, _D, _I64P, _P, _P, C.c_int64, _P]),
+    "rp_trainer_evaluate": (C.c_int, [_P, _F, _I32, C.c_int32, _D, _D]),
     "rp_comm_unique_id": (C.c_int, [_P]),
     "rp_comm_create": (C.c_int, [_P, C.c_int32, C.c_int32, C.c_int32, C.POINTER(_P)]),
     "rp_comm_destroy": (C.c_int, [_P]),

@@ -846,4 +846,27 @@ int rp_op_argmax_hits(const float* logits, const int32_t* labels, int32_t nrows,
   });
 }
 
+int64_t rp_op_eval_workspace_bytes(int32_t nrows) { return k::eval_ws_bytes(std::max(0, nrows)) + 16; }
+
+int rp_op_eval_loss_accuracy(const float* logits, const int32_t* labels, int32_t nrows, int32_t classes,
+                             double* loss_out, int64_t* hits_out, int32_t* pred, void* ws, int64_t ws_bytes,
+                             void* stream) {
+  return guard([&] {
+    if (nrows < 0 || classes < 2 || classes > 1024) fail(RP_ERR_SHAPE, "eval: bad shape");
+    need(ws, "ws");
+    if (ws_bytes < rp_op_eval_workspace_bytes(nrows)) fail(RP_ERR_RANGE, "eval: workspace too small");
+    if (nrows > 0) {
+      need(logits, "logits");
+      need(labels, "labels");
+    }
+    double* out2 = static_cast<double*>(ws);
+    k::eval_loss_hits(logits, labels, nrows, classes, out2, pred, static_cast<char*>(ws) + 16, S(stream));
+    double h[2] = {0.0, 0.0};
+    RP_CUDA(cudaMemcpyAsync(h, out2, sizeof(h), cudaMemcpyDeviceToHost, S(stream)));
+    RP_CUDA(cudaStreamSynchronize(S(stream)));
+    if (loss_out) *loss_out = h[0];
+    if (hits_out) *hits_out = (int64_t)h[1];
+  });
+}
+
 }  // extern "C"

@@ -33,6 +33,7 @@ using respar::b200::StepParams;
 struct rp_trainer {
   std::unique_ptr<DecoupledTrainer> tr;
   bool serial = false;
+  respar::b200::DeviceArray eval_logits, eval_ws;   // rp_trainer_evaluate scratch
 };
 
 struct rp_comm {
@@ -486,6 +487,37 @@ int rp_trainer_forward(rp_trainer* t, const float* x_host, int32_t nrows, float*
       throw;
     }
     cudaFree(dev);
+  });
+}
+
+int rp_trainer_evaluate(rp_trainer* t, const float* x_host, const int32_t* labels_host, int32_t nrows,
+                        double* loss_out, double* accuracy_out) {
+  return tguard([&] {
+    need(t, "trainer");
+    DecoupledTrainer& tr = *t->tr;
+    if (nrows < 0) throw respar::b200::ShapeError("evaluate: negative row count");
+    if (nrows == 0) {   // accuracy of nothing (network.cpp:226)
+      if (loss_out) *loss_out = 0.0;
+      if (accuracy_out) *accuracy_out = 0.0;
+      return;
+    }
+    need(x_host, "x");
+    need(labels_host, "labels");
+    check_labels(labels_host, nrows, tr.geometry().classes);
+    const float* x = stage_input(tr, x_host, nrows);
+    const int32_t* y = stage_labels(tr, labels_host, nrows);
+    const int dev = tr.scheduler().device_of(0);
+    t->eval_logits.allocate(dev, std::max<int64_t>(4, (int64_t)nrows * tr.geometry().classes * 4));
+    const int64_t wsb = rp_op_eval_workspace_bytes(nrows);
+    t->eval_ws.allocate(dev, wsb);
+    tr.forward(x, nrows, t->eval_logits.get());   // the full serial forward (synchronous)
+    double loss = 0.0;
+    int64_t hits = 0;
+    const int rc = rp_op_eval_loss_accuracy(t->eval_logits.get(), y, nrows, tr.geometry().classes, &loss, &hits,
+                                            nullptr, t->eval_ws.get(), wsb, nullptr);
+    if (rc != RP_OK) respar::b200::throw_status(rc, rp_last_error());
+    if (loss_out) *loss_out = loss;
+    if (accuracy_out) *accuracy_out = (double)hits / (double)nrows;
   });
 }
 

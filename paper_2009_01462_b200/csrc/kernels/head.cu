@@ -2,6 +2,7 @@
 // global average pool -> affine C->classes -> mean softmax-CE, and its backward.
 // All reductions run in a fixed order (deterministic).
 #include <cuda_bf16.h>
+#include <algorithm>
 #include <cfloat>
 
 #include "../common.cuh"
@@ -206,7 +207,88 @@ __global__ void argmax_hits_kernel(const float* __restrict__ logits, const int32
 
 int64_t align256(int64_t v) { return (v + 255) / 256 * 256; }
 
+// Evaluation (network.cpp:193-234): per row the softmax-CE term lse - logit[y] (fp64, max-shifted,
+// as loss_grad_kernel) and the argmax (strict '>': ties to the lowest class), one warp per row;
+// per-CTA fp64 partial sums of the loss terms and hit counts in fixed order.
+constexpr int kEvalRows = 8;   // rows (warps) per CTA
+__global__ void eval_rows_kernel(const float* __restrict__ logits, const int32_t* __restrict__ labels, int nrows,
+                                 int classes, double* __restrict__ part_loss, unsigned long long* __restrict__ part_hits,
+                                 int32_t* __restrict__ pred) {
+  __shared__ double sl[kEvalRows];
+  __shared__ unsigned long long sh[kEvalRows];
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int b = blockIdx.x * kEvalRows + w;
+  double term = 0.0;
+  unsigned long long hit = 0;
+  if (b < nrows) {
+    const float* l = logits + (int64_t)b * classes;
+    // argmax, lowest index on ties: per-lane best, then a fixed-order butterfly on (value, index)
+    float bv = -INFINITY;
+    int bi = classes;
+    double m = -INFINITY;
+    for (int c = lane; c < classes; c += 32) {
+      const float v = l[c];
+      if (v > bv) bv = v, bi = c;
+      m = fmax(m, (double)v);
+    }
+    for (int o = 16; o > 0; o >>= 1) {
+      const float ov = __shfl_xor_sync(0xffffffffu, bv, o);
+      const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+      if (ov > bv || (ov == bv && oi < bi)) bv = ov, bi = oi;
+      m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
+    }
+    double z = 0.0;
+    for (int c = lane; c < classes; c += 32) z += exp((double)l[c] - m);
+    for (int o = 16; o > 0; o >>= 1) z += __shfl_xor_sync(0xffffffffu, z, o);
+    const int y = labels[b];
+    term = (y >= 0 && y < classes) ? m + log(z) - (double)l[y] : __longlong_as_double(0x7ff8000000000000LL);
+    hit = bi == y ? 1ull : 0ull;
+    if (pred && lane == 0) pred[b] = bi;
+  }
+  if (lane == 0) {
+    sl[w] = term;
+    sh[w] = hit;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double s = 0.0;
+    unsigned long long h = 0;
+    for (int i = 0; i < kEvalRows; ++i) s += sl[i], h += sh[i];
+    part_loss[blockIdx.x] = s;
+    part_hits[blockIdx.x] = h;
+  }
+}
+
+__global__ void eval_final_kernel(const double* __restrict__ part_loss, const unsigned long long* __restrict__ part_hits,
+                                  int nparts, int nrows, double* __restrict__ out) {
+  if (threadIdx.x == 0) {
+    double s = 0.0;
+    unsigned long long h = 0;
+    for (int i = 0; i < nparts; ++i) s += part_loss[i], h += part_hits[i];
+    out[0] = nrows ? s / (double)nrows : 0.0;
+    out[1] = (double)h;
+  }
+}
+
 }  // namespace
+
+int64_t eval_ws_bytes(int nrows) {
+  const int64_t parts = (nrows + kEvalRows - 1) / kEvalRows;
+  return align256(parts * 8) * 2 + 256;
+}
+
+void eval_loss_hits(const float* logits, const int32_t* labels, int nrows, int classes, double* out2, int32_t* pred,
+                    void* ws, cudaStream_t st) {
+  const int parts = std::max(1, (nrows + kEvalRows - 1) / kEvalRows);
+  double* pl = static_cast<double*>(ws);
+  auto* ph = reinterpret_cast<unsigned long long*>(static_cast<char*>(ws) + align256((int64_t)parts * 8));
+  if (nrows > 0) {
+    eval_rows_kernel<<<parts, 32 * kEvalRows, 0, st>>>(logits, labels, nrows, classes, pl, ph, pred);
+    RP_LAUNCHED();
+  }
+  eval_final_kernel<<<1, 32, 0, st>>>(pl, ph, nrows > 0 ? parts : 0, nrows, out2);
+  RP_LAUNCHED();
+}
 
 int64_t head_ws_bytes(int nrows, int channels, int classes) {
   return align256((int64_t)nrows * classes * 4) + align256((int64_t)nrows * 8) + align256((int64_t)nrows * channels * 4);

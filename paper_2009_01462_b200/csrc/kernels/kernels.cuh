@@ -157,5 +157,10 @@ void head_loss_backward(int nrows, int hw, int channels, int classes, const floa
                         float* scale = nullptr);
 void argmax_hits(const float* logits, const int32_t* labels, int nrows, int classes, unsigned long long* hits_dev,
                  cudaStream_t st);
+// evaluation (network.cpp:193-234): out2[0] = mean softmax-CE, out2[1] = argmax hits (ties to the
+// lowest class), both deterministic; pred (nullable) = per-row argmax.  ws >= eval_ws_bytes(nrows).
+int64_t eval_ws_bytes(int nrows);
+void eval_loss_hits(const float* logits, const int32_t* labels, int nrows, int classes, double* out2, int32_t* pred,
+                    void* ws, cudaStream_t st);
 
 }  // namespace rp::k

@@ -201,6 +201,24 @@ class CudaStageEngine:
     def buffer(self, numel: int):
         return self.torch.empty(numel, dtype=self.torch.float32, device=f"cuda:{self.device}")
 
+    def loss_accuracy(self, logits, labels, nrows: int):
+        """loss_phi and accuracy of device logits on device (rp_op_eval_loss_accuracy)."""
+        if nrows == 0:
+            return 0.0, 0.0
+        y = np.ascontiguousarray(labels, dtype=np.int32).reshape(-1)
+        if y.size != nrows or np.any(y < 0) or np.any(y >= self.geometry.classes):
+            raise ConfigError("evaluate: labels must be nrows values in [0, classes)")
+        yd = self.torch.from_numpy(y).to(f"cuda:{self.device}")
+        wsb = lib().rp_op_eval_workspace_bytes(nrows)
+        ws = self.torch.empty(wsb, dtype=self.torch.uint8, device=f"cuda:{self.device}")
+        loss, hits = C.c_double(), C.c_int64()
+        s = C.c_void_p()
+        check(lib().rp_trainer_stage_stream(self._h, self.hi - 1, C.byref(s)))
+        check(lib().rp_op_eval_loss_accuracy(C.c_void_p(logits.data_ptr()), C.c_void_p(yd.data_ptr()), nrows,
+                                             self.geometry.classes, C.byref(loss), C.byref(hits), None,
+                                             C.c_void_p(ws.data_ptr()), wsb, s))
+        return loss.value, hits.value / nrows
+
     def input_tensor(self, x_ptr: int, nrows: int):
         g = self.geometry
         return self.torch.as_tensor(_DeviceArray(x_ptr, (nrows * g.height * g.width * g.in_channels,), "<f4"),
@@ -325,12 +343,7 @@ class DistributedDecoupledTrainer:
             self._exchange([(out, p.next_rank)], [], p.hi - 1)
         res = self._zeros_like_loss().new_zeros(2)
         if p.last:
-            logits = out.detach().to("cpu").double().numpy().reshape(nrows, e.geometry.classes)
-            y = np.asarray(labels).reshape(-1)
-            m = logits.max(axis=1, keepdims=True)
-            lse = m[:, 0] + np.log(np.exp(logits - m).sum(axis=1))
-            loss = float((lse - logits[np.arange(nrows), y]).mean()) if nrows else 0.0
-            acc = float((np.argmax(logits, axis=1) == y).mean()) if nrows else 0.0
+            loss, acc = e.loss_accuracy(out, labels, nrows)   # on the engine (device for CUDA)
             res[0], res[1] = loss, acc
         if self._replica_group is not None:
             import torch.distributed as dist

@@ -365,16 +365,6 @@ class TrainResult:
     params: Optional[np.ndarray] = None
 
 
-def _loss_and_accuracy(logits: np.ndarray, labels: np.ndarray):
-    """loss_phi value (network.cpp:193-221) and accuracy (network.cpp:223-234)."""
-    z = logits.astype(np.float64)
-    m = z.max(axis=1, keepdims=True)
-    lse = m[:, 0] + np.log(np.exp(z - m).sum(axis=1))
-    loss = float((lse - z[np.arange(z.shape[0]), labels]).mean()) if z.shape[0] else 0.0
-    acc = float((np.argmax(z, axis=1) == labels).mean()) if z.shape[0] else 0.0
-    return loss, acc
-
-
 def train(cfg: TrainConfig, train_set: Dataset, test_set: Dataset) -> TrainResult:
     """train (decoupled.cpp:268-351) on the B200 trainer."""
     cfg.validate()
@@ -427,11 +417,11 @@ def train(cfg: TrainConfig, train_set: Dataset, test_set: Dataset) -> TrainResul
         wall = time.perf_counter() - t0
         res.timings.append(EpochTiming(epoch, wall))
         # evaluation through a full serial forward pass; excluded from timings
-        train_loss, _ = _loss_and_accuracy(tr.forward(train_set.points), train_set.labels)
+        train_loss, _ = tr.evaluate(train_set.points, train_set.labels)   # on device
         if not math.isfinite(train_loss):
             raise DivergedError(f"training diverged: non-finite loss at epoch {epoch} (mode {cfg.mode}, "
                                 f"K={cfg.stages})")
-        _, test_acc = _loss_and_accuracy(tr.forward(test_set.points), test_set.labels)
+        _, test_acc = tr.evaluate(test_set.points, test_set.labels)
         row = MetricsRow(epoch=epoch, train_loss=train_loss, test_accuracy=test_acc, lr=sp.lr,
                          epoch_seconds=wall if cfg.emit_timing else 0.0)
         if cfg.mode != "serial":

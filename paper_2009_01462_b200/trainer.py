@@ -323,12 +323,21 @@ class DecoupledTrainer:
         check(lib().rp_trainer_forward(self._h, _fp(x), x.shape[0], _fp(out)))
         return out
 
+    def evaluate(self, x, labels):
+        """(loss_phi, accuracy) of the current net on (x, labels), computed on device
+        (decoupled.cpp:332-347, network.cpp:193-234): the full serial forward, mean softmax-CE,
+        argmax hits with ties to the lowest class."""
+        x = self._x(x)
+        y = np.ascontiguousarray(labels, dtype=np.int32)
+        if y.size != x.shape[0]:
+            raise ShapeError(f"loss_phi: {y.size} labels for {x.shape[0]} samples")
+        loss, acc = C.c_double(), C.c_double()
+        check(lib().rp_trainer_evaluate(self._h, _fp(x), _ip(y), x.shape[0], C.byref(loss), C.byref(acc)))
+        return loss.value, acc.value
+
     def accuracy(self, x, labels) -> float:
-        """accuracy (network.cpp:223-234): argmax with ties to the lowest class."""
-        logits = self.forward(x)
-        if logits.shape[0] == 0:
-            return 0.0
-        return float((np.argmax(logits, axis=1) == np.asarray(labels)).mean())
+        """accuracy (network.cpp:223-234): argmax with ties to the lowest class (on device)."""
+        return self.evaluate(x, labels)[1]
 
 
 class SerialTrainer(DecoupledTrainer):

@@ -116,6 +116,15 @@ class OracleStageEngine:
     def loss_tensor(self):
         return torch.tensor([self.tr.last_stage_loss], dtype=torch.float64)
 
+    def loss_accuracy(self, logits, labels, nrows):
+        """The test engine's evaluation: the oracle's loss_phi / accuracy (network.cpp:193-234)."""
+        if nrows == 0:
+            return 0.0, 0.0
+        z = logits.detach().double().numpy().reshape(nrows, -1)
+        y = np.asarray(labels).reshape(-1)
+        loss, _ = O.loss_phi(z, y)
+        return loss, float((O.argmax_lowest(z) == y).mean())
+
     def loss_like(self):
         return torch.zeros(1, dtype=torch.float64)
 

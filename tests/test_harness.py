@@ -84,6 +84,7 @@ def _oracle_train(cfg, train_set, test_set):
                    blocks=cfg.num_blocks, classes=cfg.classes)
     root = O.Rng(cfg.seed)
     net_rng = root.split()
+    noise_rng = root.split()                                      # decoupled.cpp:274-276
     mode = {"serial": O.SERIAL, "penalty": O.PENALTY, "alm": O.ALM}[cfg.mode]
     init = {"multilevel": O.MULTILEVEL, "warmstart": O.WARMSTART, "random": O.RANDOM}[cfg.init]
     x = train_set.points.astype(np.float64)
@@ -99,6 +100,9 @@ def _oracle_train(cfg, train_set, test_set):
                           lambda_lr=lr * s.lambda_lr_scale, kappa_lr=s.kappa_lr,
                           max_corrections=s.correction_max_iters)
         tr.step(x, train_set.labels, 0, sp)
+        if s.noise_sigma_last > 0.0 and cfg.stages >= 2:   # decoupled.cpp:315-321: lambda_{K-1} += N(0, s^2)
+            lam = tr.stage(cfg.stages - 1).lam
+            lam += O.rng_normal(noise_rng, lam.size, 0.0, s.noise_sigma_last).reshape(lam.shape)
         lt = O.net_forward(tr.net, x, 0, g.blocks).logits
         loss = O.loss_phi(lt, train_set.labels)[0]
         acc = O.accuracy(tr.net, test_set.points.astype(np.float64), test_set.labels)
@@ -121,6 +125,68 @@ def test_device_train_matches_oracle_loop(mode, init):
         assert abs(row.train_loss - loss) <= 1e-4 * abs(loss)
         assert abs(row.test_accuracy - acc) <= 1.0 / 30 + 1e-12      # at most one tie-break flip
         assert abs(row.max_violation - viol) <= 1e-3 * max(abs(viol), 1e-12) + 1e-10
+
+
+@pytest.mark.gpu
+def test_device_train_with_noise_matches_oracle_loop():
+    """Noise injection into lambda_{K-1} (decoupled.cpp:315-321): the device draws the
+    reference's Box-Muller stream (tensor.cpp:187-197) from the second root split, so the
+    trajectory tracks the oracle's with the same noise."""
+    cfg = Hn.default_config("penalty")
+    cfg.num_blocks, cfg.feature_dim, cfg.hidden_dim = 4, 8, 8
+    cfg.epochs, cfg.coarse_epochs = 3, 2
+    cfg.train_points, cfg.test_points, cfg.seed = 40, 30, 5
+    cfg.schedules.noise_sigma_last = 0.05
+    train_set, test_set = Hn.gen_circles(40, 5), Hn.gen_circles(30, 6)
+    res = Hn.train(cfg, train_set, test_set)
+    want = _oracle_train(cfg, train_set, test_set)
+    quiet = Hn.default_config("penalty")
+    for a in ("num_blocks", "feature_dim", "hidden_dim", "epochs", "coarse_epochs", "train_points", "test_points",
+              "seed"):
+        setattr(quiet, a, getattr(cfg, a))
+    no_noise = Hn.train(quiet, train_set, test_set)
+    for row, (loss, acc, viol) in zip(res.metrics, want):
+        assert abs(row.train_loss - loss) <= 1e-4 * abs(loss)
+        assert abs(row.max_violation - viol) <= 1e-3 * max(abs(viol), 1e-12) + 1e-10
+    # and the noise is really there: the violation differs from the noiseless run
+    assert res.metrics[-1].max_violation != no_noise.metrics[-1].max_violation
+
+
+@pytest.mark.gpu
+def test_fill_normal_is_the_reference_box_muller_stream():
+    """rp_op_fill_normal == rng_normal (tensor.cpp:187-197) draw for draw (fp64 math on both
+    sides, rounded to fp32), and the state advances by 2 n draws."""
+    import ctypes as C
+    import torch
+    from paper_2009_01462_b200._lib import lib
+    n = 100003
+    rng = O.Rng(77)
+    rng.split()
+    nrng = rng.split()
+    state = nrng.state
+    want = O.rng_normal(nrng, n, 0.25, 0.05).astype(np.float32)
+    out = torch.zeros(n, device="cuda")
+    st = C.c_uint64(state)
+    rp = pytest.importorskip("paper_2009_01462_b200")
+    rp.check(lib().rp_op_fill_normal(C.c_void_p(out.data_ptr()), n, C.byref(st), 0.25, 0.05, 0, None))
+    got = out.cpu().numpy()
+    ulp = np.spacing(np.abs(want))
+    assert np.all(np.abs(got - want) <= ulp)             # libm vs CUDA fp64 log / cos: at most 1 fp32 ulp
+    assert np.mean(got == want) > 0.999
+    assert st.value == nrng.state                        # 2 draws per sample consumed
+    # accumulate mode adds onto the buffer (lambda += noise)
+    base = torch.full((n,), 1.5, device="cuda")
+    st2 = C.c_uint64(state)
+    rp.check(lib().rp_op_fill_normal(C.c_void_p(base.data_ptr()), n, C.byref(st2), 0.25, 0.05, 1, None))
+    acc = base.cpu().numpy()
+    want_acc = (1.5 + O.rng_normal(_restate(state), n, 0.25, 0.05)).astype(np.float32)
+    assert np.all(np.abs(acc - want_acc) <= np.spacing(np.abs(want_acc)))
+
+
+def _restate(state):
+    r = O.Rng(0)
+    r.state = np.uint64(state)
+    return r
 
 
 @pytest.mark.gpu
