@@ -101,6 +101,28 @@ inline void launch_pdl(Kernel k, int grid, int block, size_t smem, cudaStream_t 
   if (e != cudaSuccess) fail(RP_ERR_CUDA, std::string("cudaLaunchKernelEx: ") + cudaGetErrorString(e));
 }
 
+// The same with a 1-D thread-block cluster of `cluster` CTAs (grid % cluster == 0).
+template <class Kernel, class... Args>
+inline void launch_pdl_cluster(Kernel k, int grid, int block, size_t smem, cudaStream_t st, int cluster,
+                               Args... args) {
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(block);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[2];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = cluster;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[1].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = pdl_enabled() ? 2 : 1;
+  const cudaError_t e = cudaLaunchKernelEx(&cfg, k, args...);
+  if (e != cudaSuccess) fail(RP_ERR_CUDA, std::string("cudaLaunchKernelEx (cluster): ") + cudaGetErrorString(e));
+}
+
 // cudaFuncSetAttribute(MaxDynamicSharedMemorySize) once per (kernel, device): the attribute
 // belongs to the device's context, so a multi-device trainer needs it on every device.
 inline void ensure_max_dynamic_smem(const void* fn, int bytes) {

@@ -24,6 +24,7 @@
 #include <cuda.h>
 #include <cuda_bf16.h>
 
+#include <cstdio>
 #include <cstdlib>
 #include <map>
 #include <mutex>
@@ -65,12 +66,28 @@ struct PwArgs {
   float* gb[2];
   double scale[2];
   const float* gsc[2];           // the A (g-side) planes' power-of-two scale (device; null: kActPlaneScale)
+  int mc;                        // 1: clusters of 3 CTAs (the tap groups of one work group) share the
+                                 //    operand loads by TMA multicast (wgrad_planes_kernel<true>)
 };
 
 __device__ __forceinline__ int grp_start(int gid, int grid, const PwArgs& a) {
   return (int)((int64_t)grid * gid / (a.njobs * 3 * a.mo * a.mi));
 }
 
+// clustered form: work group w (job, co block, ci block) owns clusters [cgrp_start(w), cgrp_start(w + 1))
+// of the ncl = grid / 3 clusters; CTA 3 cl + r of a cluster is tap group r
+__host__ __device__ __forceinline__ int cgrp_start(int w, int ncl, const PwArgs& a) {
+  return (int)((int64_t)ncl * w / (a.njobs * a.mo * a.mi));
+}
+
+// MC (clustered multicast): the three tap groups of a work group run as one
+// cluster on the same blocks.  The g planes are identical for them and their x rows overlap
+// (filter rows dy = 0..2 shift them by one row), so per stage rank 0 loads the g0 slab, rank 1
+// the g1 slab and rank 2 both x slabs over the union of the three groups' rows (rg + 2), each
+// multicast into all three CTAs: every operand byte leaves L2 once per cluster instead of once
+// per tap group.  A stage is free once all three CTAs' MMAs (multicast commits) and rank 0's
+// bias warps (remote arrives) are done with it.
+template <bool MC>
 __global__ void __launch_bounds__(kThreads, 1)
     wgrad_planes_kernel(const __grid_constant__ CUtensorMap tg0a, const __grid_constant__ CUtensorMap tg1a,
                         const __grid_constant__ CUtensorMap tx0a, const __grid_constant__ CUtensorMap tx1a,
@@ -93,27 +110,49 @@ __global__ void __launch_bounds__(kThreads, 1)
   auto g_slab = [&](int s, int j) { return smem + s * a.stage + j * a.g_slab; };
   auto x_slab = [&](int s, int j) { return smem + s * a.stage + a.x_off + j * a.x_slab; };
 
-  const int NG1 = 3 * a.mo * a.mi;                // work groups per job
-  const int NG = a.njobs * NG1;
-  int gid = 0;
-  while (gid + 1 < NG && grp_start(gid + 1, gridDim.x, a) <= (int)blockIdx.x) ++gid;
-  const int c_lo = grp_start(gid, gridDim.x, a), c_hi = grp_start(gid + 1, gridDim.x, a);
-  const int job = gid / NG1;
-  const int gj = gid - job * NG1;
-  const int gi = gj % 3, cib = (gj / 3) % a.mi, cob = gj / (3 * a.mi);
-
-  const int jg = blockIdx.x - c_lo, ng = c_hi - c_lo;
+  int job, gi, cib, cob, jg, ng;
+  if constexpr (MC) {
+    const int NW = a.njobs * a.mo * a.mi;
+    const int ncl = gridDim.x / 3, cl = blockIdx.x / 3;
+    int w = 0;
+    while (w + 1 < NW && cgrp_start(w + 1, ncl, a) <= cl) ++w;
+    const int c_lo = cgrp_start(w, ncl, a), c_hi = cgrp_start(w + 1, ncl, a);
+    job = w / (a.mo * a.mi);
+    const int gj = w - job * a.mo * a.mi;
+    cib = gj % a.mi;
+    cob = gj / a.mi;
+    gi = (int)cluster_ctarank();
+    jg = cl - c_lo;
+    ng = c_hi - c_lo;
+  } else {
+    const int NG1 = 3 * a.mo * a.mi;                // work groups per job
+    const int NG = a.njobs * NG1;
+    int gid = 0;
+    while (gid + 1 < NG && grp_start(gid + 1, gridDim.x, a) <= (int)blockIdx.x) ++gid;
+    const int c_lo = grp_start(gid, gridDim.x, a), c_hi = grp_start(gid + 1, gridDim.x, a);
+    job = gid / NG1;
+    const int gj = gid - job * NG1;
+    gi = gj % 3;
+    cib = (gj / 3) % a.mi;
+    cob = gj / (3 * a.mi);
+    jg = blockIdx.x - c_lo;
+    ng = c_hi - c_lo;
+  }
   const int blk_beg = (int)((int64_t)jg * a.num_blocks / ng);
   const int blk_end = (int)((int64_t)(jg + 1) * a.num_blocks / ng);
   const int t0 = gi * kTg;
   const int Wp = a.Wp;
   const int xrows = a.rg * Wp;   // x rows of this tap group's filter row only (y0 - 1 + gi ..)
-  const bool do_bias = gi == 0 && cib == 0 && !a.nobias;
+  const bool cl_bias = cib == 0 && !a.nobias;      // this work group sums the bias
+  // unclustered: tap group 0 sums it; clustered: the three CTAs hold the same g slab and each sums
+  // a third of its rows (a slot is gated by every CTA's bias warps, so they share the work)
+  const bool do_bias = (MC || gi == 0) && cl_bias;
+  const int bias_p0 = MC ? gi * a.P / 3 : 0, bias_p1 = MC ? (gi + 1) * a.P / 3 : a.P;
 
   if (threadIdx.x == 0) {
     for (int i = 0; i < S; ++i) {
       mbar_init(&full[i], 1);
-      mbar_init(&empty[i], 1);
+      mbar_init(&empty[i], MC ? 3 + (cl_bias ? 3 : 0) : 1);
       mbar_init(&bias_free[i], 128);
     }
     mbar_init(acc_full, 1);
@@ -154,7 +193,10 @@ __global__ void __launch_bounds__(kThreads, 1)
   }
   fence_proxy_async_smem();
   tc_fence_before();
-  __syncthreads();
+  if constexpr (MC)
+    cluster_sync();   // every CTA's barriers exist before any peer multicasts into its shared memory
+  else
+    __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = __shfl_sync(0xffffffffu, *tmem_slot, 0);
   // PDL: let the next grid's prologue overlap this grid's tail; the operands (and the partial
@@ -190,6 +232,34 @@ __global__ void __launch_bounds__(kThreads, 1)
           tma_load_4d(mx1, &full[s], x_slab(s, 1), 64 * cib, -1, y0 - 1 + gi, n);
         }
     };
+    if constexpr (MC) {
+      // my share of every stage, multicast to the cluster (rank 0: g atom 0, 1: g atom 1, 2: x)
+      const uint32_t bytes_mc = 2u * a.P * 128u + 2u * (uint32_t)(a.rg + 2) * Wp * 128u;
+      const CUtensorMap* mg0 = job == 0 ? &tg0a : &tg0b;
+      const CUtensorMap* mg1 = job == 0 ? (a.single ? &tg0a : &tg1a) : (a.single ? &tg0b : &tg1b);
+      const CUtensorMap* mx0 = job == 0 ? &tx0a : &tx0b;
+      const CUtensorMap* mx1 = job == 0 ? (a.single ? &tx0a : &tx1a) : (a.single ? &tx0b : &tx1b);
+      const int cg0 = a.single ? 128 * cob : 64 * cob, cg1 = a.single ? 128 * cob + 64 : 64 * cob;
+      const int cx0 = a.single ? 128 * cib : 64 * cib, cx1 = a.single ? 128 * cib + 64 : 64 * cib;
+      for (int b = blk_beg; b < blk_end; ++b) {
+        const int n = b / a.blocks_per_img;
+        const int y0 = (b - n * a.blocks_per_img) * a.rg;
+        mbar_wait(&empty[s], ph ^ 1);   // every CTA (and rank 0's bias warps) released the slot
+        if (elect_one()) {
+          mbar_arrive_expect_tx(&full[s], bytes_mc);
+          if (gi == 0) {
+            tma_load_4d_mc(mg0, &full[s], g_slab(s, 0), cg0, -1, y0, n, 0x7);
+          } else if (gi == 1) {
+            tma_load_4d_mc(mg1, &full[s], g_slab(s, 1), cg1, -1, y0, n, 0x7);
+          } else {
+            tma_load_4d_mc(mx0, &full[s], x_slab(s, 0), cx0, -1, y0 - 1, n, 0x7);
+            tma_load_4d_mc(mx1, &full[s], x_slab(s, 1), cx1, -1, y0 - 1, n, 0x7);
+          }
+        }
+        __syncwarp();
+        if (++s == S) s = 0, ph ^= 1;
+      }
+    } else
     for (int b = blk_beg; b < blk_end; ++b) {
       const int n = b / a.blocks_per_img;
       const int y0 = (b - n * a.blocks_per_img) * a.rg;
@@ -223,7 +293,8 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_wait(&full[s], ph);
       tc_fence_after();
       uint64_t da = desc_general(smem_u32(g_slab(s, 0)), a.g_slab, 1024, 2, 0);
-      uint64_t db = desc_general(smem_u32(x_slab(s, 0)), a.x_slab, 1024, 2, 0);
+      // MC: this tap group's filter row dy = gi starts gi rows into the union slab
+      uint64_t db = desc_general(smem_u32(x_slab(s, 0)) + (MC ? (uint32_t)(gi * Wp * 128) : 0u), a.x_slab, 1024, 2, 0);
       if (elect_one()) {
         for (int k = 0; k < ksteps && !(a.dbg & 1); ++k) {
           const uint32_t accum = (b > blk_beg || k > 0) ? 1u : 0u;
@@ -235,7 +306,10 @@ __global__ void __launch_bounds__(kThreads, 1)
           da += 128;   // 16 positions = 16 rows x 128 B, in 16-byte units
           db += 128;
         }
-        mma_commit(&empty[s]);
+        if constexpr (MC)
+          mma_commit_mc(&empty[s], 0x7);   // the slot is free in every CTA once all three are done
+        else
+          mma_commit(&empty[s]);
       }
       __syncwarp();
       if (++s == S) s = 0, ph ^= 1;
@@ -261,7 +335,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         const uint8_t* p0 = g_slab(s, 0);
         const uint8_t* p1 = g_slab(s, 1);
         const uint32_t base0 = smem_u32(p0), base1 = smem_u32(p1);
-        for (int p = r0; p < a.P; p += 16) {
+        for (int p = bias_p0 + r0; p < bias_p1; p += 16) {
           const int ph0 = (int)(((base0 >> 7) + p) & 7), ph1 = (int)(((base1 >> 7) + p) & 7);
           const uint4 u = *reinterpret_cast<const uint4*>(p0 + (size_t)p * 128 + ((cq ^ ph0) << 4));
           const uint4 v = *reinterpret_cast<const uint4*>(p1 + (size_t)p * 128 + ((cq ^ ph1) << 4));
@@ -292,7 +366,14 @@ __global__ void __launch_bounds__(kThreads, 1)
           bk[e] = (t - bs[e]) - y;
           bs[e] = t;
         }
-        mbar_arrive(&bias_free[s]);
+        if constexpr (MC) {
+          // each CTA's bias warps release the slot in all three CTAs (they all write into this one)
+          asm volatile("bar.sync 1, 128;" ::: "memory");
+          if (tid == 0)
+            for (uint32_t r = 0; r < 3; ++r) mbar_arrive_cluster(&empty[s], r);
+        } else {
+          mbar_arrive(&bias_free[s]);
+        }
         if (++s == S) s = 0, ph ^= 1;
       }
       // threads t, t + 8, ... (same cq) combine in fixed order: lanes xor 8, 16, then warps
@@ -373,7 +454,10 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (do_bias && warp >= 2 && warp < 6) asm volatile("bar.sync 3, 256;" ::: "memory");
 
   tc_fence_before();
-  __syncthreads();
+  if constexpr (MC)
+    cluster_sync();   // no peer arrives on (or multicasts into) this CTA's shared memory after it exits
+  else
+    __syncthreads();
   if (warp == 1) {
     tc_fence_after();
     tmem_dealloc<512>(tmem_base);
@@ -406,27 +490,44 @@ __global__ void wgrad_planes_reduce_kernel(const float* __restrict__ part, const
       const int ci = (idx / Co) % Ci;
       const int tap = idx / (Co * Ci);
       const int gi = tap / kTg, cob = co / cbk, cib = ci / cbk;
-      const int gid = gbase + (cob * a.mi + cib) * 3 + gi;
-      const int c_lo = grp_start(gid, grid, a), c_hi = grp_start(gid + 1, grid, a);
+      // the CTAs of this (job, co block, ci block, tap group): first + stride * [0, count)
+      int first, stride, count;
+      if (a.mc) {
+        const int w = job * a.mo * a.mi + cob * a.mi + cib, ncl = grid / 3;
+        const int c_lo = cgrp_start(w, ncl, a), c_hi = cgrp_start(w + 1, ncl, a);
+        first = 3 * c_lo + gi, stride = 3, count = c_hi - c_lo;
+      } else {
+        const int gid = gbase + (cob * a.mi + cib) * 3 + gi;
+        const int c_lo = grp_start(gid, grid, a), c_hi = grp_start(gid + 1, grid, a);
+        first = c_lo, stride = 1, count = c_hi - c_lo;
+      }
       const int64_t off = ((int64_t)(tap - gi * kTg) * cbk + (ci - cib * cbk)) * cbk + (co - cob * cbk);
       // 8 loads in flight, 4 accumulators combined in a fixed order (deterministic)
       double s4[4] = {0.0, 0.0, 0.0, 0.0};
-      int b = c_lo;
-      for (; b + 8 <= c_hi; b += 8) {
+      int i0 = 0;
+      for (; i0 + 8 <= count; i0 += 8) {
         float v[8];
 #pragma unroll
-        for (int i = 0; i < 8; ++i) v[i] = __ldg(part + (int64_t)(b + i) * pstride + off);
+        for (int i = 0; i < 8; ++i) v[i] = __ldg(part + (int64_t)(first + (i0 + i) * stride) * pstride + off);
 #pragma unroll
         for (int i = 0; i < 8; ++i) s4[i & 3] += (double)v[i];
       }
-      for (; b < c_hi; ++b) s4[0] += (double)__ldg(part + (int64_t)b * pstride + off);
+      for (; i0 < count; ++i0) s4[0] += (double)__ldg(part + (int64_t)(first + i0 * stride) * pstride + off);
       gw[idx] = (float)(scale * ((s4[0] + s4[1]) + (s4[2] + s4[3])));
     } else if (gb) {
       const int co = idx - total, cob = co / cbk;
-      const int gid = gbase + cob * a.mi * 3;
-      const int c_lo = grp_start(gid, grid, a), c_hi = grp_start(gid + 1, grid, a);
+      int first, stride, count;   // the ci-block-0 CTAs of this co block that sum the bias
+      if (a.mc) {   // all three CTAs of each cluster (a third of the rows each), in CTA order
+        const int w = job * a.mo * a.mi + cob * a.mi, ncl = grid / 3;
+        const int c_lo = cgrp_start(w, ncl, a), c_hi = cgrp_start(w + 1, ncl, a);
+        first = 3 * c_lo, stride = 1, count = 3 * (c_hi - c_lo);
+      } else {
+        const int gid = gbase + cob * a.mi * 3;
+        const int c_lo = grp_start(gid, grid, a), c_hi = grp_start(gid + 1, grid, a);
+        first = c_lo, stride = 1, count = c_hi - c_lo;
+      }
       double s = 0.0;
-      for (int b = c_lo; b < c_hi; ++b) s += part_bias[(int64_t)b * cbk + (co - cob * cbk)];
+      for (int i = 0; i < count; ++i) s += part_bias[(int64_t)(first + i * stride) * cbk + (co - cob * cbk)];
       gb[co] = (float)(bscale * s);
     }
   }
@@ -543,7 +644,9 @@ struct PwPlan {
   size_t smem;
 };
 
-PwPlan plan(const ConvShape& s, bool single = false) {
+// mc: the clustered multicast kernel (x slabs over the union of the three tap groups' rows,
+// grid a multiple of 3)
+PwPlan plan(const ConvShape& s, bool single = false, bool mc = false) {
   PwPlan p;
   const int cbk = single ? 128 : 64;
   if (s.co % cbk != 0 || s.ci % cbk != 0 || s.w + 2 > 256) return p;
@@ -564,7 +667,7 @@ PwPlan plan(const ConvShape& s, bool single = false) {
     q.P = rg * Wp;
     q.Pp = (q.P + 15) / 16 * 16;
     q.g_slab = round1k((uint64_t)q.Pp * 128);
-    q.x_slab = (uint32_t)rg * Wp * 128u;   // one filter row's x rows per tap group
+    q.x_slab = (uint32_t)(mc ? rg + 2 : rg) * Wp * 128u;   // one filter row's x rows per tap group (mc: all three)
     q.x_off = 2 * q.g_slab + kLead;
     q.stage = round1k((uint64_t)q.x_off + 2ull * q.x_slab + kTrail);
     // the pair epilogue parks kTg 64x64 fp32 partial sums in the drained stage memory: tiny
@@ -574,7 +677,7 @@ PwPlan plan(const ConvShape& s, bool single = false) {
     q.smem = st * (size_t)q.stage + (3 * kMaxStages + 2) * 8 + 4 * 128 * 8 + 256;
     if (q.smem > (size_t)kMaxSmem) continue;
     if ((size_t)kTg * 64 * 64 * 4 > st * (size_t)q.stage) continue;   // the pair epilogue's park buffer
-    q.grid = kNumSMs;
+    q.grid = mc ? 3 * (kNumSMs / 3) : kNumSMs;
     q.ok = true;
     return q;
   }
@@ -640,8 +743,60 @@ struct WgJob {
 };
 
 void launch_wgrad_planes(const ConvShape& s, const WgJob* jobs, int njobs, void* ws, cudaStream_t st, bool single) {
-  const PwPlan p = plan(s, single);
+  PwPlan p = plan(s, single);
   if (!p.ok) fail(RP_ERR_INTERNAL, "conv3x3_wgrad_planes: unsupported shape");
+  // RP_WGRAD_MC=1: the clustered multicast kernel.  Measured (C2/C3 shape, one launch): DRAM reads
+  // 1.00x algorithmic (135 MB; unclustered 1.36x) and half the L2 traffic, but 1.9x the time --
+  // the three CTAs advance in lockstep and every stage's release waits on all of them and on the
+  // bias warps, a round trip the 3-stage ring does not cover.  Off by default.
+  static const bool mc_on = [] {
+    const char* e = std::getenv("RP_WGRAD_MC");
+    return e && e[0] == '1';
+  }();
+  static const int wdbg0 = [] {
+    const char* e = std::getenv("RP_WGRAD_DBG");
+    return e ? std::atoi(e) : 0;
+  }();
+  bool mc = false;
+  {
+    const int cbk0 = single ? 128 : 64;
+    PwPlan q = plan(s, single, true);
+    if (mc_on && !wdbg0 && q.ok) {
+      // one wave of clusters: as many 3-CTA clusters as the GPCs hold at once (not every GPC's SM
+      // count is a multiple of 3)
+      ensure_max_dynamic_smem(reinterpret_cast<const void*>(wgrad_planes_kernel<true>), kMaxSmem);
+      static int max_clusters = -1;
+      static size_t max_clusters_smem = 0;
+      if (max_clusters < 0 || max_clusters_smem != q.smem) {
+        cudaLaunchConfig_t cfg{};
+        cfg.gridDim = dim3(q.grid);
+        cfg.blockDim = dim3(kThreads);
+        cfg.dynamicSmemBytes = q.smem;
+        cudaLaunchAttribute attr[1];
+        attr[0].id = cudaLaunchAttributeClusterDimension;
+        attr[0].val.clusterDim.x = 3;
+        attr[0].val.clusterDim.y = 1;
+        attr[0].val.clusterDim.z = 1;
+        cfg.attrs = attr;
+        cfg.numAttrs = 1;
+        int n = 0;
+        if (cudaOccupancyMaxActiveClusters(&n, wgrad_planes_kernel<true>, &cfg) != cudaSuccess) {
+          cudaGetLastError();
+          n = 0;
+        }
+        max_clusters = n;
+        max_clusters_smem = q.smem;
+      }
+      q.grid = 3 * std::min(max_clusters, kNumSMs / 3);
+      if (std::getenv("RP_WGRAD_VERBOSE"))
+        fprintf(stderr, "wgrad_planes mc: max active clusters %d, grid %d, rg %d, stages %d, smem %zu\n", max_clusters,
+                q.grid, q.rg, q.nstages, q.smem);
+      if (q.grid > 0 && njobs * (s.co / cbk0) * (s.ci / cbk0) <= q.grid / 3) {
+        p = q;
+        mc = true;
+      }
+    }
+  }
   const int cbk = single ? 128 : 64;
   PwArgs a{};
   a.single = single ? 1 : 0;
@@ -674,13 +829,15 @@ void launch_wgrad_planes(const ConvShape& s, const WgJob* jobs, int njobs, void*
   a.part_bias = reinterpret_cast<double*>(static_cast<char*>(ws) + part_bytes(p, single));
   a.njobs = njobs;
   if (3 * njobs * a.mo * a.mi > p.grid) fail(RP_ERR_INTERNAL, "conv3x3_wgrad_planes: too many work groups");
+  a.mc = mc ? 1 : 0;
+  const int xrows = mc ? p.rg + 2 : p.rg;
   CUtensorMap m[2][4];   // copies taken under the cache lock
   for (int j = 0; j < njobs; ++j) {
     const WgJob& jb = jobs[j];
     m[j][0] = cached(jb.g0, s.n, s.h, s.w, s.co, p.rg);
     m[j][1] = cached(single ? jb.g0 : jb.g1, s.n, s.h, s.w, s.co, p.rg);
-    m[j][2] = cached(jb.x0, s.n, s.h, s.w, s.ci, p.rg);
-    m[j][3] = cached(single ? jb.x0 : jb.x1, s.n, s.h, s.w, s.ci, p.rg);
+    m[j][2] = cached(jb.x0, s.n, s.h, s.w, s.ci, xrows);
+    m[j][3] = cached(single ? jb.x0 : jb.x1, s.n, s.h, s.w, s.ci, xrows);
     a.gw[j] = jb.gw;
     a.gb[j] = jb.gb;
     a.scale[j] = (double)jb.scale;
@@ -688,9 +845,15 @@ void launch_wgrad_planes(const ConvShape& s, const WgJob* jobs, int njobs, void*
   }
   if (njobs == 1)
     for (int i = 0; i < 4; ++i) m[1][i] = m[0][i];
-  ensure_max_dynamic_smem(reinterpret_cast<const void*>(wgrad_planes_kernel), kMaxSmem);
-  launch_pdl(wgrad_planes_kernel, p.grid, kThreads, p.smem, st, m[0][0], m[0][1], m[0][2], m[0][3], m[1][0],
-             m[1][1], m[1][2], m[1][3], a);
+  if (mc) {
+    ensure_max_dynamic_smem(reinterpret_cast<const void*>(wgrad_planes_kernel<true>), kMaxSmem);
+    launch_pdl_cluster(wgrad_planes_kernel<true>, p.grid, kThreads, p.smem, st, 3, m[0][0], m[0][1], m[0][2],
+                       m[0][3], m[1][0], m[1][1], m[1][2], m[1][3], a);
+  } else {
+    ensure_max_dynamic_smem(reinterpret_cast<const void*>(wgrad_planes_kernel<false>), kMaxSmem);
+    launch_pdl(wgrad_planes_kernel<false>, p.grid, kThreads, p.smem, st, m[0][0], m[0][1], m[0][2], m[0][3],
+               m[1][0], m[1][1], m[1][2], m[1][3], a);
+  }
   const int total = njobs * (9 * s.ci * s.co + s.co);
   launch_pdl(wgrad_planes_reduce_kernel, ceil_div(total, 256), 256, 0, st, (const float*)a.part,
              (const double*)a.part_bias, a, p.grid);

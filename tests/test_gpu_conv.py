@@ -363,3 +363,29 @@ def test_head_loss_bwd_planes_matches_split(c, lo):
     for a, b in zip(*outs):
         assert torch.equal(a, b)
     assert bool(torch.isfinite(outs[1][2]).all())
+
+
+_MC_SCRIPT = r"""
+import sys
+sys.path.insert(0, sys.argv[1])
+import numpy as np
+from tests.test_gpu_conv import run_wgrad_planes
+for shape in ((2, 32, 32, 64, 64), (1, 12, 10, 64, 64), (1, 16, 16, 256, 256)):
+    gw, gb, ww_, wb = run_wgrad_planes(*shape)
+    ew = np.abs(gw - ww_).max() / np.abs(ww_).max()
+    eb = np.abs(gb - wb).max() / np.abs(wb).max()
+    assert ew <= 1e-6 and eb <= 1e-6, (shape, ew, eb)
+print("ok")
+"""
+
+
+def test_wgrad_planes_clustered_multicast():
+    """RP_WGRAD_MC=1: the 3-CTA cluster form of the plane wgrad (TMA multicast of the shared g / x
+    rows, distributed bias sums) against the fp64 oracle at the same bar as the default kernel."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    r = subprocess.run([sys.executable, "-c", _MC_SCRIPT, root], env={**os.environ, "RP_WGRAD_MC": "1"},
+                       capture_output=True, text=True, timeout=300, cwd=root)
+    assert r.returncode == 0 and r.stdout.strip().endswith("ok"), r.stderr[-2000:]
