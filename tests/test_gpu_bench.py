@@ -28,4 +28,4 @@ def test_bench_default_line():
         assert k in roof, k
     assert 0 < roof["frac"] < 1 and roof["achieved"] > 0
     assert d["e2e"]["h2d_bytes_per_step"] > 0 and d["e2e"]["d2h_bytes_per_step"] > 0
-    assert d["config"]["workload"].startswith("C2")
+    assert d["config"]["workload"].startswith("C3")   # the metric's 64-block, 8-stage network
