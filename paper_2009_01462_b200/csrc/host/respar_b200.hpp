@@ -90,6 +90,13 @@ struct StepParams {
   double momentum = 0.0;
 };
 
+// NetGrads (network.hpp:81-87) of one stage: its contiguous slice [begin, begin + size) of the
+// flat parameter layout (S when k = 0, the stage's blocks, T when k = K-1), copied to the host.
+struct NetGrads {
+  int64_t begin = 0;
+  std::vector<float> values;
+};
+
 struct ViolationReport {
   std::vector<double> per_stage;
   double max_violation = 0.0;
@@ -169,7 +176,10 @@ class DecoupledTrainer {
               bool read_loss = true);
   void take_snapshot(int k, int row0, int nrows);
   void stage_forward(int k, const float* batch_x, int nrows, int row0);
-  void stage_backward_update(int k, const int32_t* labels, double beta, double lr, int row0, double momentum = 0.0);
+  // returns the stage's gradients, as the reference does (decoupled.hpp:78-79)
+  NetGrads stage_backward_update(int k, const int32_t* labels, double beta, double lr, int row0,
+                                 double momentum = 0.0);
+  NetGrads stage_grads(int k) const;   // the last backward's gradients of stage k
   void correct_aux(int k, const StepParams& p, int row0, int nrows);
   void correct_multiplier(int k, double beta, double kappa_lr, int row0, int nrows);
   void correction_gradient(int k, double beta, int row0, int nrows, float* out) const;

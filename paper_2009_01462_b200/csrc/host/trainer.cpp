@@ -973,8 +973,27 @@ void DecoupledTrainer::stage_forward(int k, const float* batch_x, int nrows, int
   cu(cudaStreamSynchronize(s), "cudaStreamSynchronize");
 }
 
-void DecoupledTrainer::stage_backward_update(int k, const int32_t* labels, double beta, double lr, int row0,
-                                             double momentum) {
+NetGrads DecoupledTrainer::stage_grads(int k) const {
+  if (k < 0 || k >= stages()) throw std::out_of_range("stage_grads: bad stage index");
+  need_local(k, "stage_grads");
+  sched_->sync();
+  const Layout L(geo_);
+  const Stage& st = stages_[k];
+  int64_t beg = L.block0 + (int64_t)st.begin * L.block_stride;
+  int64_t end = L.block0 + (int64_t)st.end * L.block_stride;
+  if (k == 0) beg = 0;
+  if (k == stages() - 1) end = L.total;
+  NetGrads g;
+  g.begin = beg;
+  g.values.resize((size_t)(end - beg));
+  DeviceGuard dg(st.device);
+  const float* src = grads_[dev_index(unique_devices_, st.device)].get();
+  cu(cudaMemcpy(g.values.data(), src + beg, (size_t)(end - beg) * 4, cudaMemcpyDeviceToHost), "cudaMemcpy D2H");
+  return g;
+}
+
+NetGrads DecoupledTrainer::stage_backward_update(int k, const int32_t* labels, double beta, double lr, int row0,
+                                                 double momentum) {
   if (k < 0 || k >= stages()) throw std::out_of_range("stage_backward_update: bad stage index");
   need_local(k, "stage_backward_update");
   Stage& st = stages_[k];
@@ -990,10 +1009,13 @@ void DecoupledTrainer::stage_backward_update(int k, const int32_t* labels, doubl
     if (st.snap_rows != nrows) throw ShapeError("stage_backward_update: snapshot rows do not match the batch");
   }
   if (momentum != 0.0) ensure_momentum();
-  DeviceGuard g(st.device);
-  cudaStream_t s = sched_->stream(k);
-  run_backward(st, labels, nrows, row0, beta, lr, momentum, true, s);
-  cu(cudaStreamSynchronize(s), "cudaStreamSynchronize");
+  {
+    DeviceGuard g(st.device);
+    cudaStream_t s = sched_->stream(k);
+    run_backward(st, labels, nrows, row0, beta, lr, momentum, true, s);
+    cu(cudaStreamSynchronize(s), "cudaStreamSynchronize");
+  }
+  return stage_grads(k);
 }
 
 void DecoupledTrainer::correct_aux(int k, const StepParams& p, int row0, int nrows) {
