@@ -5,6 +5,7 @@
 // as rp_debug_umma_probe (tests only; never on the training path).
 #include "common.cuh"
 #include "kernels/umma.cuh"
+#include <cuda_fp16.h>
 
 // standalone: the product library's launch counter is not linked in
 namespace rp {
@@ -476,3 +477,82 @@ extern "C" int rp_debug_umma_bench(int fmt, int N, int layout, int a_mn, int b_m
   }
 }
 
+
+// Where does row i of an M = 64 kind::f16 MMA's D land in TMEM?  A[i][k] = (k == 0) ? i + 1 : 0
+// (64 x 16 fp16, K-major interleave), B[n][k] = (k == 0) ? 1 : 0 (16 x 16): D[i][n] = i + 1.
+// Writes TMEM lanes 0..127, columns 0..15 to out[lane * 16 + col] (untouched lanes: -1).
+namespace rp::k {
+__global__ void umma_m64_layout_kernel(float* out) {
+  __shared__ __align__(1024) uint16_t sa[64 * 16];
+  __shared__ __align__(1024) uint16_t sb[16 * 16];
+  __shared__ uint64_t bar;
+  __shared__ uint32_t slot;
+  const int tid = threadIdx.x;
+  // K-major interleave: core matrix = 8 rows x 8 halves (16 B); lbo = distance between the two
+  // K-halves (k 0-7, 8-15), sbo = distance between 8-row groups
+  for (int i = tid; i < 64 * 16; i += blockDim.x) {
+    const int m = i / 16, k = i % 16;
+    const int idx = (k / 8) * (64 * 8) + (m / 8) * 64 + (m % 8) * 8 + (k % 8);
+    sa[idx] = k == 0 ? __half_as_ushort(__float2half((float)(m + 1))) : 0;
+  }
+  for (int i = tid; i < 16 * 16; i += blockDim.x) {
+    const int n = i / 16, k = i % 16;
+    const int idx = (k / 8) * (16 * 8) + (n / 8) * 64 + (n % 8) * 8 + (k % 8);
+    sb[idx] = k == 0 ? __half_as_ushort(__float2half(1.f)) : 0;
+  }
+  if (tid == 0) {
+    umma::mbar_init(&bar, 1);
+    umma::fence_barrier_init();
+  }
+  if (tid < 32) umma::tmem_alloc<32>(&slot);
+  umma::fence_proxy_async_smem();
+  umma::tc_fence_before();
+  __syncthreads();
+  umma::tc_fence_after();
+  const uint32_t tmem = slot;
+  // pre-fill TMEM with -1 so untouched lanes show
+  {
+    const int w = tid / 32;
+    uint32_t v[16];
+    for (int j = 0; j < 16; ++j) v[j] = __float_as_uint(-1.f);
+    asm volatile("tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};"
+                 ::"r"(tmem + ((uint32_t)(w * 32) << 16)), "r"(v[0]), "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]),
+                 "r"(v[5]), "r"(v[6]), "r"(v[7]), "r"(v[8]), "r"(v[9]), "r"(v[10]), "r"(v[11]), "r"(v[12]),
+                 "r"(v[13]), "r"(v[14]), "r"(v[15]));
+    asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+  }
+  umma::tc_fence_before();
+  __syncthreads();
+  umma::tc_fence_after();
+  if (tid < 32) {
+    const uint64_t da = umma::desc_general(umma::smem_u32(sa), 64 * 8 * 2, 64 * 2, 0, 0);
+    const uint64_t db = umma::desc_general(umma::smem_u32(sb), 16 * 8 * 2, 64 * 2, 0, 0);
+    if (umma::elect_one()) {
+      umma::mma_f16(tmem, da, db, umma::idesc(0, 64, 16), 0u);
+      umma::mma_commit(&bar);
+    }
+    __syncwarp();
+  }
+  umma::mbar_wait(&bar, 0);
+  umma::tc_fence_after();
+  const int w = tid / 32;
+  uint32_t r[16];
+  umma::tmem_ld16(tmem + ((uint32_t)(w * 32) << 16), r);
+  umma::tmem_wait_ld();
+  for (int j = 0; j < 16; ++j) out[(w * 32 + (tid % 32)) * 16 + j] = __uint_as_float(r[j]);
+  umma::tc_fence_before();
+  __syncthreads();
+  if (tid < 32) umma::tmem_dealloc<32>(tmem);
+}
+}  // namespace rp::k
+
+extern "C" int rp_debug_umma_m64_layout(float* out) {
+  try {
+    rp::k::umma_m64_layout_kernel<<<1, 128>>>(out);
+    RP_LAUNCHED();
+    RP_CUDA(cudaDeviceSynchronize());
+    return 0;
+  } catch (const rp::Error& e) {
+    return e.code;
+  }
+}
