@@ -171,13 +171,19 @@ int rp_op_conv3x3(int32_t n, int32_t h, int32_t w, int32_t ci, int32_t co, const
                   int32_t math, void* ws, int64_t ws_bytes, void* stream);
 int64_t rp_op_conv3x3_workspace_bytes(int32_t ci, int32_t co);
 /* The same conv reading its input as an fp16 plane pair (in_planes = [2][n h w ci]:
- * x in_s = p0 + p1) on the tcgen05 plane mode (Co % 64 == 0, Ci % 16 == 0; fp32-class
- * accuracy); out_planes (optional, [2][n h w co] fp16) receives the plane pair of out out_s.
- * in_scale / out_scale: device scalars (NULL = the activation scale 2^7). */
+ * x in_s = p0 + p1) on a tcgen05 plane kernel (Co in {16, 32} or Co % 64 == 0, Ci % 16 == 0;
+ * fp32-class accuracy); out_planes (optional, [2][n h w co] fp16) receives the plane pair of
+ * out out_s.  in_scale / out_scale: device scalars (NULL = the activation scale 2^7). */
 int rp_op_conv3x3_planes(int32_t n, int32_t h, int32_t w, int32_t ci, int32_t co, const void* in_planes,
                          const float* w_hwio, int32_t dgrad, const float* bias, const float* aux, double hstep,
                          int32_t epi, float* out, void* out_planes, const float* in_scale, const float* out_scale,
                          void* ws, int64_t ws_bytes, void* stream);
+/* Which plane kernel the plane convs use: 1 positions-as-M (conv_pm.cu: Co <= 64, 3 tensor
+ * products per MAC), 0 channels-as-M (conv_tc.cu: Co % 64 == 0, 4 products), -1 the default
+ * (process-wide; the env var RP_CONV_PM sets the initial value).  A shape only one kernel takes
+ * always runs on it.  rp_op_plane_conv_kernel reports the choice for a shape (1, 0; -1 none). */
+int rp_op_set_plane_conv_kernel(int32_t which);
+int32_t rp_op_plane_conv_kernel(int32_t n, int32_t h, int32_t w, int32_t ci, int32_t co);
 /* Weight gradient of that conv: gw[3][3][ci][co] = scale sum_p in[p+tap][ci] gout[p][co],
  * gb[co] = scale sum_p gout[p][co] (gb may be NULL).  Deterministic. */
 int rp_op_conv3x3_wgrad(int32_t n, int32_t h, int32_t w, int32_t ci, int32_t co, const float* in, const float* gout,
@@ -189,8 +195,8 @@ int64_t rp_op_conv3x3_wgrad_workspace_bytes(int32_t n, int32_t h, int32_t w, int
  * buffer); p1 NULL: p0 alone is the bf16 single plane. */
 int rp_op_split_planes(const float* in, int64_t n, void* p0, void* p1, float* scale_out, void* stream);
 /* Weight gradient from fp16 plane pairs (x 2^7 = x0 + x1, gout g_s = g0 + g1 with g_scale the
- * device scale, NULL = 2^7), Ci and Co multiples of 64: the fp32-accurate tcgen05 wgrad fed by
- * TMA alone. */
+ * device scale, NULL = 2^7), Ci and Co multiples of 64, or Ci 16 and Co in {16, 32}: the
+ * fp32-accurate tcgen05 wgrad fed by TMA alone. */
 int rp_op_conv3x3_wgrad_planes(int32_t n, int32_t h, int32_t w, int32_t ci, int32_t co, const void* x0, const void* x1,
                                const void* g0, const void* g1, double scale, const float* g_scale, float* gw,
                                float* gb, void* ws, int64_t ws_bytes, void* stream);

@@ -4,6 +4,7 @@
 #include <cstdlib>
 #include <string>
 #include <algorithm>
+#include <atomic>
 #include <cstring>
 #include <string>
 
@@ -11,6 +12,10 @@
 #include "common.cuh"
 #include "kernels/kernels.cuh"
 #include "profile.hpp"
+
+#ifndef RP_CONV_PM_DEFAULT
+#define RP_CONV_PM_DEFAULT 0   // Co = 64: conv_tc.cu unless RP_CONV_PM=1
+#endif
 
 namespace rp {
 
@@ -74,13 +79,36 @@ int64_t weight_ws_bytes(const rp_geometry& g) {
 int64_t wgrad_ws_bytes(const k::ConvShape& s) {
   return std::max({k::conv3x3_wgrad_ws_bytes(s), k::conv3x3_wgrad_tc_ws_bytes(s, true),
                    k::conv3x3_wgrad_tc_ws_bytes(s, false), k::conv3x3_wgrad_bf16_ws_bytes(s),
-                   k::conv3x3_wgrad_planes_ws_bytes(s), k::conv3x3_wgrad_bf16p_ws_bytes(s)});
+                   k::conv3x3_wgrad_planes_ws_bytes(s), k::conv3x3_wgrad_bf16p_ws_bytes(s),
+                   k::conv3x3_wgrad_small_ws_bytes(s)});
 }
 
 // The plane-pair block path (fp32 math): every conv of the block on the tcgen05 kernel, whose
 // epilogue also writes the fp16 plane pair (v s = p0 + p1, planes.cuh) of its output, so both weight
 // gradients run on the TMA-fed plane wgrad (conv_wgrad_planes.cu). RP_WGRAD_PLANES=0 turns
 // it off (the fp32-operand 3xTF32 wgrad then runs).
+// Plane-input convs: the positions-as-M kernel (conv_pm.cu, 3 products per MAC) or conv_tc.cu's
+// channels-as-M kernel (4 products; Co % 64 == 0).  g_plane_conv: -1 auto (conv_pm where it is
+// the only kernel or RP_CONV_PM_DEFAULT), 0 conv_tc where supported, 1 conv_pm where supported;
+// initialised from RP_CONV_PM, set by rp_op_set_plane_conv_kernel.
+std::atomic<int> g_plane_conv{[] {
+  const char* e = std::getenv("RP_CONV_PM");
+  return e ? (std::atoi(e) != 0 ? 1 : 0) : -1;
+}()};
+
+bool plane_conv_pm(const k::ConvShape& s) {
+  if (!k::conv3x3_pm_supported(s)) return false;
+  if (!k::conv3x3_tc_supported(s)) return true;
+  const int f = g_plane_conv.load(std::memory_order_relaxed);
+  return f >= 0 ? f != 0 : RP_CONV_PM_DEFAULT != 0;
+}
+
+bool plane_wgrad_supported(const k::ConvShape& s) {
+  return k::conv3x3_wgrad_planes_supported(s) || k::conv3x3_wgrad_small_supported(s);
+}
+
+bool plane_conv_supported(const k::ConvShape& s) { return k::conv3x3_pm_supported(s) || k::conv3x3_tc_supported(s); }
+
 bool planes_path(const rp_geometry& g, int nrows, int math) {
   static const bool enabled = [] {
     const char* e = std::getenv("RP_WGRAD_PLANES");
@@ -89,8 +117,8 @@ bool planes_path(const rp_geometry& g, int nrows, int math) {
   if (!enabled || math != RP_MATH_FP32 || nrows <= 0) return false;
   const k::ConvShape s1{nrows, g.height, g.width, g.channels, g.hidden};
   const k::ConvShape s2{nrows, g.height, g.width, g.hidden, g.channels};
-  return k::conv3x3_tc_supported(s1) && k::conv3x3_tc_supported(s2) && k::conv3x3_wgrad_planes_supported(s1) &&
-         k::conv3x3_wgrad_planes_supported(s2);
+  return plane_conv_supported(s1) && plane_conv_supported(s2) && plane_wgrad_supported(s1) &&
+         plane_wgrad_supported(s2);
 }
 
 // The bf16 tape path (bf16 math): the bf16 conv epilogues also write a bf16 copy of their
@@ -144,8 +172,14 @@ void conv(const k::ConvShape& s, const float* in, const float* w, bool dgrad, co
           const float* in_scale = nullptr, const float* out_scale = nullptr) {
   prof::Scope ps(prof_cls, st, conv_flops(s),
                  conv_bytes(s, aux_read) + (out_planes ? 4.0 * s.pixels() * s.co : 0.0) - (out ? 0.0 : 4.0 * s.pixels() * s.co));
-  if (out_planes || in_planes) {   // only the fp32 tcgen05 kernel reads / writes plane pairs (planes_path())
-    if (math != RP_MATH_FP32 || !k::conv3x3_tc_supported(s)) fail(RP_ERR_INTERNAL, "conv: plane i/o needs fp32 tcgen05");
+  if (out_planes || in_planes) {   // only the fp32 tcgen05 kernels read / write plane pairs (planes_path())
+    if (math != RP_MATH_FP32) fail(RP_ERR_INTERNAL, "conv: plane i/o needs fp32 math");
+    if (in_planes && plane_conv_pm(s)) {
+      k::conv3x3_fwd_pm(s, w, dgrad, bias, aux, h, epi, out, wws, st, out_planes, in_planes, wprep, in_scale,
+                        out_scale);
+      return;
+    }
+    if (!k::conv3x3_tc_supported(s)) fail(RP_ERR_INTERNAL, "conv: plane i/o needs fp32 tcgen05");
     k::conv3x3_fwd_tc(s, in, w, dgrad, bias, aux, h, epi, out, fp32_split(), wws, st, out_planes, in_planes,
                       in_planes ? wprep : nullptr, in_scale, out_scale);
     return;
@@ -242,6 +276,10 @@ void wgrad_planes(const k::ConvShape& s, const void* xp, const void* gp, float s
   prof::Scope ps(RP_PROF_CONV_WGRAD, st, conv_flops(s), 4.0 * (double)s.pixels() * (s.ci + s.co));
   const auto* x0 = static_cast<const uint16_t*>(xp);   // fp16 bits
   const auto* g0 = static_cast<const uint16_t*>(gp);
+  if (!k::conv3x3_wgrad_planes_supported(s)) {   // the 16-channel form (plane_wgrad_supported)
+    k::conv3x3_wgrad_small(s, x0, x0 + s.pixels() * s.ci, g0, g0 + s.pixels() * s.co, scale, gw, gb, ws, st, gscale);
+    return;
+  }
   k::conv3x3_wgrad_planes(s, x0, x0 + s.pixels() * s.ci, g0, g0 + s.pixels() * s.co, scale, gw, gb, ws, st, gscale);
 }
 
@@ -264,7 +302,7 @@ void block_bwd_planes(const rp_geometry& g, int nrows, const void* x_p, const fl
   // (the dpre planes keep the cotangent scale: in and out scale are both *gscale)
   conv(shape(g, nrows, C, Ch), gio, pb + L.w2, true, nullptr, a, h, tanh_act ? k::EPI_TANH_BWD : k::EPI_SCALE, nullptr,
        RP_MATH_FP32, wws, RP_PROF_CONV_DGRAD, tanh_act, st, dpre_p, g_p, f, gscale, gscale);
-  if (C == Ch && !std::getenv("RP_WGRAD_UNPAIRED")) {
+  if (C == Ch && k::conv3x3_wgrad_planes_supported(shape(g, nrows, C, Ch)) && !std::getenv("RP_WGRAD_UNPAIRED")) {
     // gW1 = x^T dpre, gb1 = sum dpre and gW2 = h a^T g, gb2 = h sum g in ONE launch (same
     // shape): half the launches' prologues, epilogues and reduces   (network.cpp:98-103)
     const k::ConvShape sw = shape(g, nrows, C, Ch);
@@ -568,6 +606,18 @@ int rp_op_conv3x3_wgrad(int32_t n, int32_t h, int32_t w, int32_t ci, int32_t co,
   });
 }
 
+int rp_op_set_plane_conv_kernel(int32_t which) {
+  return guard([&] {
+    if (which < -1 || which > 1) fail(RP_ERR_RANGE, "set_plane_conv_kernel: which must be -1, 0 or 1");
+    g_plane_conv.store(which);
+  });
+}
+
+int32_t rp_op_plane_conv_kernel(int32_t n, int32_t h, int32_t w, int32_t ci, int32_t co) {
+  const k::ConvShape s{n, h, w, ci, co};
+  return plane_conv_pm(s) ? 1 : (k::conv3x3_tc_supported(s) ? 0 : -1);
+}
+
 int rp_op_conv3x3_planes(int32_t n, int32_t h, int32_t w, int32_t ci, int32_t co, const void* in_planes,
                          const float* w_hwio, int32_t dgrad, const float* bias, const float* aux, double hstep,
                          int32_t epi, float* out, void* out_planes, const float* in_scale, const float* out_scale,
@@ -576,7 +626,7 @@ int rp_op_conv3x3_planes(int32_t n, int32_t h, int32_t w, int32_t ci, int32_t co
     if (epi < 0 || epi > 5) fail(RP_ERR_RANGE, "conv3x3_planes: unknown epilogue");
     if (n < 0 || h < 1 || w < 1 || ci < 1 || co < 1) fail(RP_ERR_SHAPE, "conv3x3_planes: bad shape");
     const k::ConvShape s{n, h, w, ci, co};
-    if (!k::conv3x3_tc_supported(s)) fail(RP_ERR_SHAPE, "conv3x3_planes: unsupported shape (Co % 64, Ci % 16)");
+    if (!plane_conv_supported(s)) fail(RP_ERR_SHAPE, "conv3x3_planes: unsupported shape (Co % 64 or Co in {16, 32}, Ci % 16)");
     if (ws_bytes < rp_op_conv3x3_workspace_bytes(std::min(ci, co), std::max(ci, co)))
       fail(RP_ERR_RANGE, "conv3x3_planes: workspace too small");
     if (n > 0) need(in_planes, "in_planes");
@@ -749,7 +799,8 @@ int rp_op_split_planes(const float* in, int64_t n, void* p0, void* p1, float* sc
 }
 
 int64_t rp_op_conv3x3_wgrad_planes_workspace_bytes(int32_t n, int32_t h, int32_t w, int32_t ci, int32_t co) {
-  return k::conv3x3_wgrad_planes_ws_bytes(k::ConvShape{n, h, w, ci, co});
+  const k::ConvShape s{n, h, w, ci, co};
+  return std::max(k::conv3x3_wgrad_planes_ws_bytes(s), k::conv3x3_wgrad_small_ws_bytes(s));
 }
 
 int rp_op_conv3x3_wgrad_planes(int32_t n, int32_t h, int32_t w, int32_t ci, int32_t co, const void* x0, const void* x1,
@@ -757,15 +808,21 @@ int rp_op_conv3x3_wgrad_planes(int32_t n, int32_t h, int32_t w, int32_t ci, int3
                                float* gb, void* ws, int64_t ws_bytes, void* stream) {
   return guard([&] {
     const k::ConvShape s{n, h, w, ci, co};
-    if (!k::conv3x3_wgrad_planes_supported(s)) fail(RP_ERR_SHAPE, "conv3x3_wgrad_planes: unsupported shape");
-    if (ws_bytes < k::conv3x3_wgrad_planes_ws_bytes(s)) fail(RP_ERR_RANGE, "conv3x3_wgrad_planes: workspace too small");
+    const bool small = !k::conv3x3_wgrad_planes_supported(s) && k::conv3x3_wgrad_small_supported(s);
+    if (!small && !k::conv3x3_wgrad_planes_supported(s))
+      fail(RP_ERR_SHAPE, "conv3x3_wgrad_planes: unsupported shape (Ci, Co % 64 == 0, or Ci 16 and Co in {16, 32})");
+    if (ws_bytes < (small ? k::conv3x3_wgrad_small_ws_bytes(s) : k::conv3x3_wgrad_planes_ws_bytes(s)))
+      fail(RP_ERR_RANGE, "conv3x3_wgrad_planes: workspace too small");
     need(x0, "x0");
     need(x1, "x1");
     need(g0, "g0");
     need(g1, "g1");
     need(gw, "gw");
     prof::Scope ps(RP_PROF_CONV_WGRAD, S(stream), conv_flops(s), 2.0 * (double)s.pixels() * (s.ci + s.co));
-    k::conv3x3_wgrad_planes(s, x0, x1, g0, g1, (float)scale, gw, gb, ws, S(stream), g_scale);
+    if (small)
+      k::conv3x3_wgrad_small(s, x0, x1, g0, g1, (float)scale, gw, gb, ws, S(stream), g_scale);
+    else
+      k::conv3x3_wgrad_planes(s, x0, x1, g0, g1, (float)scale, gw, gb, ws, S(stream), g_scale);
   });
 }
 

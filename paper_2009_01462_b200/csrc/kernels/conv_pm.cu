@@ -1,0 +1,515 @@
+// tcgen05 3x3 convolution on fp16 plane pairs with the output POSITIONS as the MMA's M
+// (fp32-accurate path, RP_MATH_FP32):
+//
+//   out[p][co] = epi( sum_{tap, ci} x[p + off(tap)][ci] * w[tap][ci][co] )
+//
+// (block_forward's matmul(x, W1) / matmul(a, W2) and block_vjp's matmul(upstream, W2^T) /
+// matmul(dpre, W1^T), network.cpp:85-104, generalised to 3x3 taps.)
+//
+// conv_tc.cu puts the output channels on M ([W0; W1] stacked, M = 128 for 64 channels), so the
+// x1 plane pays for a W1 x1 product nobody needs: 4 tensor products per fp32 MAC.  Here
+//   A = the shifted x-plane halo view, M = 128 frame positions (K-major interleave, the same
+//       TMA-loaded slab conv_tc's B reads: a shift by one position is +16 B of start address),
+//   B = the filter, N = 2 Co rows [W0; W1] for the x0 plane, N = Co rows (W0) for the x1 plane:
+// x0 W0 + x0 W1 + x1 W0 is 3 products per MAC (the dropped |W1 x1| <= 2^-24 |W x|, fp32's own
+// rounding).  Measured MMA time per tap and 256 positions (tools/umma_bench_pm.py, Co = 64):
+// 224.7 cycles against conv_tc's 256.4.  D's row = position, so the epilogue needs no transpose:
+// a thread owns one position, adds the W0 and W1 columns, and stores that position's channels.
+//
+//  * frame, units, halo: as conv_tc.cu (H rows x (W + 1) columns per image; units of two
+//    128-position tiles, a shorter tail unit per image; one halo slab per 16-channel chunk
+//    serves all 9 taps); the whole prepared filter stays resident in shared memory (Co <= 64).
+//  * warp roles (384 threads, persistent, 1 CTA/SM): w0 halo TMA, w1 MMA issuer, w2 filter
+//    load, w4-11 two epilogue groups (one tile of each unit each: TMEM -> registers -> W0 + W1,
+//    fused bias / tanh / skip / step size -> NHWC stores of the output and its planes).
+//  * Co in {16, 32, 64}: config C1's 16-channel network runs on the tensor cores too.
+#include <cuda.h>
+
+#include <algorithm>
+#include <cstdlib>
+#include <map>
+#include <mutex>
+#include <tuple>
+
+#include "../common.cuh"
+#include "kernels.cuh"
+#include "planes.cuh"
+#include "umma.cuh"
+
+namespace rp::k {
+
+namespace {
+
+using namespace rp::umma;
+
+constexpr int kThreads = 384;
+constexpr int kTile = 128;          // positions per tile (the MMA's M)
+constexpr int kS = 2;               // tiles per unit
+constexpr int kChunk = 16;          // input channels per halo chunk (one K = 16 step)
+constexpr int kMaxSlots = 8;
+constexpr int kMaxSmem = 227 * 1024;
+constexpr int kPieceBytes = 32 * 1024;   // filter load: bulk copies of <= 32 KB
+constexpr int kXchgBytes = 4096;         // per epilogue warp: 32 positions x 32 channels fp32
+
+struct PmArgs {
+  int N, H, W, Ci, Co, Wp, rows_h, T, nchunks, slots;
+  int halo_pos;            // positions per halo plane (rows_h x Wp)
+  uint32_t plane_bytes;    // one fp16 plane of a chunk's halo: [2 kg][halo_pos][8]
+  uint32_t halo_stride;    // bytes per halo slot (pads + two planes)
+  uint32_t w_bytes;        // the whole prepared filter
+  float h;
+  const uint16_t* w;       // prepared filter [chunk][tap][kg 2][2 Co rows][8] fp16 (W * 2^8 pair)
+  const float* bias;
+  const float* aux;
+  float* out;              // null: the planes alone
+  uint16_t* p0;            // optional fp16 plane pair of out * (*out_scale)
+  uint16_t* p1;
+  const float* in_scale;   // the input planes' scale (device scalar; null = kActPlaneScale)
+  const float* out_scale;  // the output planes' scale (device scalar; null = kActPlaneScale)
+  int dbg;                 // diagnostics (RP_CONV_DBG): 1 no epilogue, 2 no halo TMA, 8 no MMA
+};
+
+// Work split: units of kS tiles of one image; T = ceil(frame / 128) tiles per image leaves a
+// tail unit when kS does not divide T.  Full units round-robin from CTA 0 up, tail units from
+// CTA G - 1 down (every CTA ends within one tile of the mean).
+struct Units {
+  int f, tl, nf, ntail, fu, T, G;
+  __device__ Units(int N, int T_) : T(T_) {
+    G = gridDim.x;
+    fu = T / kS;
+    nf = N * fu;
+    ntail = (T % kS) ? N : 0;
+    f = blockIdx.x;
+    tl = G - 1 - (int)blockIdx.x;
+  }
+  __device__ bool next(int& n, int& tile0, int& ntiles) {
+    if (f < nf) {
+      n = f / fu;
+      tile0 = (f - n * fu) * kS;
+      ntiles = kS;
+      f += G;
+      return true;
+    }
+    if (tl < ntail) {
+      n = tl;
+      tile0 = fu * kS;
+      ntiles = T - tile0;
+      tl += G;
+      return true;
+    }
+    return false;
+  }
+};
+
+__device__ __forceinline__ uint4 cat2(uint2 a, uint2 b) { return make_uint4(a.x, a.y, b.x, b.y); }
+
+template <int EPI, int CO>
+__global__ void __launch_bounds__(kThreads, 1)
+    conv3x3_pm_kernel(const __grid_constant__ CUtensorMap tmap, const PmArgs a) {
+  extern __shared__ __align__(1024) uint8_t smem[];
+  constexpr int kCols = 2 * CO;                                        // accumulator columns per tile
+  constexpr int kTmemCols = 2 * kS * kCols < 32 ? 32 : 2 * kS * kCols;  // double-buffered units
+  const int warp = __shfl_sync(0xffffffffu, (int)threadIdx.x / 32, 0);
+  const int lane = threadIdx.x & 31;
+
+  // ---- shared memory: [slots halo slots][filter][barriers]
+  const uint32_t plane_pitch = ((a.plane_bytes + 127u) & ~127u) + 128u;
+  auto plane = [&](int s, int p) { return smem + s * a.halo_stride + 128 + p * plane_pitch; };
+  uint8_t* wres = smem + a.slots * a.halo_stride;
+  uint8_t* xchg = wres + a.w_bytes;                                    // [8 epilogue warps][kXchgBytes]
+  uint64_t* bars = reinterpret_cast<uint64_t*>(xchg + 8 * kXchgBytes);
+  uint64_t* halo_full = bars;                    // [kMaxSlots]
+  uint64_t* halo_empty = bars + kMaxSlots;       // [kMaxSlots]
+  uint64_t* w_full = bars + 2 * kMaxSlots;       // [1]
+  uint64_t* acc_full = bars + 2 * kMaxSlots + 1; // [2]
+  uint64_t* acc_empty = bars + 2 * kMaxSlots + 3;  // [2]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * kMaxSlots + 5);
+
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < kMaxSlots; ++i) {
+      mbar_init(&halo_full[i], 1);
+      mbar_init(&halo_empty[i], 1);
+    }
+    mbar_init(w_full, 1);
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&acc_full[i], 1);
+      mbar_init(&acc_empty[i], 256);
+    }
+    fence_barrier_init();
+    prefetch_tmap(&tmap);
+  }
+  if (warp == 1) tmem_alloc<kTmemCols>(tmem_slot);
+  // zero the 128-byte pads in front of / behind the planes (read only for discarded positions)
+  for (int i = threadIdx.x; i < a.slots * 3 * 32; i += blockDim.x) {
+    const int s = i / 96, part = (i / 32) % 3, w = i % 32;
+    uint8_t* base = part == 0 ? smem + s * a.halo_stride : plane(s, part - 1) + a.plane_bytes;
+    reinterpret_cast<uint32_t*>(base)[w] = 0u;
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = __shfl_sync(0xffffffffu, *tmem_slot, 0);
+  const int Wp = a.Wp;
+  pdl_launch_dependents();
+
+  if (warp == 2) {
+    // ===================== resident filter =====================
+    // issued before pdl_wait(): the prepared filter comes from a kernel that completed before
+    // the previous grid did (conv_tc.cu, same argument)
+    if (elect_one()) {
+      mbar_arrive_expect_tx(w_full, a.w_bytes);
+      for (uint32_t o = 0; o < a.w_bytes; o += kPieceBytes)
+        bulk_load(wres + o, reinterpret_cast<const uint8_t*>(a.w) + o, min((uint32_t)kPieceBytes, a.w_bytes - o),
+                  w_full);
+    }
+    __syncwarp();
+  } else if (warp == 0) {
+    // ===================== halo TMA producer =====================
+    pdl_wait();
+    int hs = 0;
+    uint32_t hph = 0;
+    Units it(a.N, a.T);
+    int n, tile0, ntiles;
+    while (it.next(n, tile0, ntiles)) {
+      const int y0 = tile0 * kTile / Wp;
+      for (int c = 0; c < a.nchunks; ++c) {
+        mbar_wait(&halo_empty[hs], hph ^ 1);
+        if (elect_one()) {
+          if (a.dbg & 2) {
+            mbar_arrive(&halo_full[hs]);
+          } else {
+            // both planes of the chunk: images [0, N) are plane 0, [N, 2N) plane 1
+            mbar_arrive_expect_tx(&halo_full[hs], 2 * a.plane_bytes);
+            tma_load_5d(&tmap, &halo_full[hs], plane(hs, 0), 0, -1, y0 - 1, 2 * c, n);
+            tma_load_5d(&tmap, &halo_full[hs], plane(hs, 1), 0, -1, y0 - 1, 2 * c, n + a.N);
+          }
+        }
+        __syncwarp();
+        if (++hs == a.slots) hs = 0, hph ^= 1;
+      }
+    }
+  } else if (warp == 1) {
+    // ===================== MMA issuer =====================
+    const uint32_t id_x0 = idesc(0, 128, kCols);      // x0 x [W0; W1]
+    const uint32_t id_x1 = idesc(0, 128, CO);         // x1 x W0
+    const uint32_t lbo_x = (uint32_t)a.halo_pos * 16u;
+    const uint32_t lbo_w = (uint32_t)kCols * 16u;
+    const uint32_t w_tap = (uint32_t)kCols * 32u;     // bytes of one (chunk, tap) filter slice
+    int hs = 0, ab = 0;
+    uint32_t hph = 0, aph = 0;
+    mbar_wait(w_full, 0);   // unconditionally: no CTA may exit with the filter load in flight
+    tc_fence_after();
+    Units it(a.N, a.T);
+    int n, tile0, ntiles;
+    while (it.next(n, tile0, ntiles)) {
+      const int f0 = tile0 * kTile;
+      const int c0 = f0 - (f0 / Wp) * Wp;
+      mbar_wait(&acc_empty[ab], aph ^ 1);
+      tc_fence_after();
+      const uint32_t d0 = tmem_base + (uint32_t)(ab * kS * kCols);
+      for (int c = 0; c < a.nchunks; ++c) {
+        mbar_wait(&halo_full[hs], hph);
+        tc_fence_after();
+        const uint64_t ax0 = desc_kmajor_interleave(smem_u32(plane(hs, 0)), lbo_x, 128);
+        const uint64_t ax1 = desc_kmajor_interleave(smem_u32(plane(hs, 1)), lbo_x, 128);
+        if (elect_one() && !(a.dbg & 8)) {
+          for (int dy = 0; dy < 3; ++dy) {
+#pragma unroll
+            for (int dx = 0; dx < 3; ++dx) {
+              const uint64_t db =
+                  desc_kmajor_interleave(smem_u32(wres + (uint32_t)(c * 9 + 3 * dy + dx) * w_tap), lbo_w, 128);
+              const int64_t row = c0 + dy * Wp + dx - 1;    // halo position of the tile's first row, >= -1
+              const uint32_t accum = (c == 0 && dy == 0 && dx == 0) ? 0u : 1u;
+#pragma unroll
+              for (int s = 0; s < kS; ++s) {
+                if (s < ntiles) {
+                  const uint64_t ao = (uint64_t)(row + s * kTile);   // 16-byte units: one position = 1
+                  mma_f16(d0 + s * kCols, ax0 + ao, db, id_x0, accum);
+                  mma_f16(d0 + s * kCols, ax1 + ao, db, id_x1, 1u);
+                }
+              }
+            }
+          }
+        }
+        __syncwarp();
+        if (elect_one()) mma_commit(&halo_empty[hs]);
+        __syncwarp();
+        if (++hs == a.slots) hs = 0, hph ^= 1;
+      }
+      if (elect_one()) mma_commit(&acc_full[ab]);
+      __syncwarp();
+      if (++ab == 2) ab = 0, aph ^= 1;
+    }
+  } else if (warp >= 4) {
+    // ===================== epilogue =====================
+    // group g (warps 4 + 4g .. 7 + 4g) drains tile g of every unit; warp w reads TMEM lane
+    // quadrant w % 4: thread = position q * 32 + lane of the tile, columns [0, Co) = W0
+    // products, [Co, 2 Co) = W1 products of the same output channels.
+    pdl_wait();
+    const int q = warp & 3;
+    const int grp = (warp - 4) >> 2;
+    const int pt = q * 32 + lane;
+    constexpr bool kBias = EPI == EPI_BIAS || EPI == EPI_BIAS_TANH || EPI == EPI_RESID;
+    constexpr bool kAux = EPI == EPI_RESID || EPI == EPI_TANH_BWD || EPI == EPI_ADD;
+    const float acc_mul = kWeightPlaneScaleInv / (a.in_scale ? *a.in_scale : kActPlaneScale);
+    const float out_mul = a.out_scale ? *a.out_scale : kActPlaneScale;
+    const bool planes = a.p0 != nullptr;
+    constexpr int kCh = CO < 32 ? CO : 32;      // channels per exchange pass
+    constexpr int kNJ = kCh / 4;                // 16-byte pieces per position and pass
+    float4* xrow = reinterpret_cast<float4*>(xchg + (warp - 4) * kXchgBytes);
+    int ab = 0;
+    uint32_t aph = 0;
+    Units it(a.N, a.T);
+    int n, tile0, ntiles;
+    while (it.next(n, tile0, ntiles)) {
+      const int f = (tile0 + grp) * kTile + pt;
+      const int y = f / Wp, X = f - y * Wp;
+      const bool valid = grp < ntiles && y < a.H && X >= 1;
+      const int64_t off = valid ? (((int64_t)n * a.H + y) * a.W + (X - 1)) * CO : 0;
+      // the tile's aux operand first: its latency overlaps the wait for the accumulator
+      float4 ax[kAux ? CO / 4 : 1];
+      if constexpr (kAux) {
+#pragma unroll
+        for (int i = 0; i < CO / 4; ++i)
+          ax[i] = valid ? __ldg(reinterpret_cast<const float4*>(a.aux + off) + i) : make_float4(0.f, 0.f, 0.f, 0.f);
+      }
+      mbar_wait(&acc_full[ab], aph);
+      tc_fence_after();
+      if (grp < ntiles && !(a.dbg & 1)) {
+        const uint32_t tcol = tmem_base + ((uint32_t)(q * 32) << 16) + (uint32_t)(ab * kS * kCols + grp * kCols);
+#pragma unroll
+        for (int hf = 0; hf < CO / kCh; ++hf) {
+          // this position's kCh channels [hf kCh, +kCh): W0 + W1 columns, scales, epilogue
+          float o[kCh];
+#pragma unroll
+          for (int cc = 0; cc < kCh / 16; ++cc) {
+            uint32_t hi[16], lo[16];
+            tmem_ld16(tcol + hf * kCh + cc * 16, hi);
+            tmem_ld16(tcol + CO + hf * kCh + cc * 16, lo);
+            tmem_wait_ld();
+#pragma unroll
+            for (int i = 0; i < 16; ++i) {
+              const float v = (__uint_as_float(hi[i]) + __uint_as_float(lo[i])) * acc_mul;
+              const int co = hf * kCh + cc * 16 + i;
+              const float xa = kAux ? reinterpret_cast<const float*>(&ax[0])[co] : 0.f;
+              float r;
+              if constexpr (EPI == EPI_BIAS) r = v + __ldg(a.bias + co);
+              else if constexpr (EPI == EPI_BIAS_TANH) r = tanhf(v + __ldg(a.bias + co));
+              else if constexpr (EPI == EPI_RESID) r = xa + a.h * (v + __ldg(a.bias + co));
+              else if constexpr (EPI == EPI_TANH_BWD) r = (a.h * v) * (1.f - xa * xa);
+              else if constexpr (EPI == EPI_ADD) r = xa + v;
+              else r = a.h * v;
+              o[cc * 16 + i] = r;
+            }
+          }
+          // stores through the warp's exchange rows (thread = position -> kNJ 16-byte pieces of
+          // consecutive positions per instruction: 32 / kNJ positions x kCh * 4 bytes contiguous);
+          // 16-byte slots XOR-swizzled by position (conflict-free both ways)
+          if (a.out) {
+#pragma unroll
+            for (int j = 0; j < kNJ; ++j)
+              xrow[lane * kNJ + (j ^ (lane & (kNJ - 1)))] =
+                  make_float4(o[4 * j], o[4 * j + 1], o[4 * j + 2], o[4 * j + 3]);
+            __syncwarp();
+#pragma unroll
+            for (int k = 0; k < kNJ; ++k) {
+              const int src = k * (32 / kNJ) + lane / kNJ, j = lane % kNJ;
+              const float4 v = xrow[src * kNJ + (j ^ (src & (kNJ - 1)))];
+              const int64_t so = __shfl_sync(0xffffffffu, off, src);
+              if (__shfl_sync(0xffffffffu, (int)valid, src))
+                *reinterpret_cast<float4*>(a.out + so + hf * kCh + 4 * j) = v;
+            }
+            __syncwarp();
+          }
+          if (planes) {
+            // [p0 | p1] of the kCh channels: kNJ / 2 16-byte pieces each
+#pragma unroll
+            for (int j = 0; j < kNJ / 2; ++j) {
+              uint2 h0a, h1a, h0b, h1b;
+              const float va[4] = {o[8 * j], o[8 * j + 1], o[8 * j + 2], o[8 * j + 3]};
+              const float vb[4] = {o[8 * j + 4], o[8 * j + 5], o[8 * j + 6], o[8 * j + 7]};
+              pack_pair4(va, out_mul, h0a, h1a);
+              pack_pair4(vb, out_mul, h0b, h1b);
+              const uint4 u0 = cat2(h0a, h0b), u1 = cat2(h1a, h1b);
+              xrow[lane * kNJ + (j ^ (lane & (kNJ - 1)))] = *reinterpret_cast<const float4*>(&u0);
+              xrow[lane * kNJ + ((j + kNJ / 2) ^ (lane & (kNJ - 1)))] = *reinterpret_cast<const float4*>(&u1);
+            }
+            __syncwarp();
+#pragma unroll
+            for (int k = 0; k < kNJ; ++k) {
+              const int src = k * (32 / kNJ) + lane / kNJ, j = lane % kNJ;
+              const float4 v = xrow[src * kNJ + (j ^ (src & (kNJ - 1)))];
+              const int64_t so = __shfl_sync(0xffffffffu, off, src);
+              uint16_t* dst = j < kNJ / 2 ? a.p0 + so + hf * kCh + 8 * j : a.p1 + so + hf * kCh + 8 * (j - kNJ / 2);
+              if (__shfl_sync(0xffffffffu, (int)valid, src)) *reinterpret_cast<float4*>(dst) = v;
+            }
+            __syncwarp();
+          }
+        }
+      }
+      tc_fence_before();
+      mbar_arrive(&acc_empty[ab]);
+      if (++ab == 2) ab = 0, aph ^= 1;
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_dealloc<kTmemCols>(tmem_base);
+  }
+}
+
+// ---------------------------------------------------------------- host side
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                  const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+EncodeTiledFn encode_fn() {
+  static EncodeTiledFn fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<EncodeTiledFn>(p);
+  });
+  if (!fn) fail(RP_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
+  return fn;
+}
+
+// fp16 planes [2][N][H][W][Ci] viewed as 2N images of 8-channel groups; box {8 ch, W + 1
+// columns from x = -1, rows_h rows from y0 - 1, 2 groups, 1 image} = the slot layout
+// [2 kg][positions][8], out-of-bounds rows / columns zero-filled
+CUtensorMap make_map(const void* planes, const ConvShape& s, int Wp, int rows_h) {
+  CUtensorMap m;
+  const cuuint64_t dims[5] = {8, (cuuint64_t)s.w, (cuuint64_t)s.h, (cuuint64_t)(s.ci / 8), (cuuint64_t)(2 * s.n)};
+  const cuuint64_t strides[4] = {(cuuint64_t)s.ci * 2, (cuuint64_t)s.w * s.ci * 2, 16,
+                                 (cuuint64_t)s.h * s.w * s.ci * 2};
+  const cuuint32_t box[5] = {8, (cuuint32_t)Wp, (cuuint32_t)rows_h, 2, 1};
+  const cuuint32_t estr[5] = {1, 1, 1, 1, 1};
+  CUresult r = encode_fn()(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 5, const_cast<void*>(planes), dims, strides, box, estr,
+                           CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                           CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) fail(RP_ERR_CUDA, "cuTensorMapEncodeTiled failed (" + std::to_string((int)r) + ")");
+  return m;
+}
+
+std::mutex g_map_mu;
+std::map<std::tuple<const void*, int, int, int, int, int>, CUtensorMap> g_maps;
+
+CUtensorMap cached_map(const void* in, const ConvShape& s, int Wp, int rows_h) {
+  std::lock_guard<std::mutex> lk(g_map_mu);
+  auto key = std::make_tuple(in, s.n, s.h, s.w, s.ci, rows_h);
+  auto it = g_maps.find(key);
+  if (it == g_maps.end()) {
+    if (g_maps.size() > 4096) g_maps.clear();   // callers hold copies, never references
+    it = g_maps.emplace(key, make_map(in, s, Wp, rows_h)).first;
+  }
+  return it->second;
+}
+
+struct Plan {
+  bool ok = false;
+  int Wp, rows_h, halo_pos, T, slots;
+  uint32_t plane_bytes, halo_stride, w_bytes;
+  size_t smem;
+};
+
+Plan plan_for(const ConvShape& s) {
+  Plan p;
+  if (!(s.co == 16 || s.co == 32 || s.co == 64) || s.ci % kChunk != 0 || s.ci <= 0 || s.w + 1 > 256) return p;
+  p.Wp = s.w + 1;
+  // a tile's A view reaches rows [c0 - 1, c0 + 2 Wp + 1 + 255] of the halo (c0 < Wp)
+  p.rows_h = (3 * p.Wp + kS * kTile + p.Wp - 1) / p.Wp;
+  if (p.rows_h > 256) return p;
+  p.halo_pos = p.rows_h * p.Wp;
+  p.T = (s.h * p.Wp + kTile - 1) / kTile;
+  p.plane_bytes = (uint32_t)p.halo_pos * 32u;
+  const uint32_t pitch = ((p.plane_bytes + 127u) & ~127u) + 128u;
+  p.halo_stride = 128u + 2u * pitch;
+  p.w_bytes = (uint32_t)(s.ci / kChunk) * 9u * (uint32_t)(2 * s.co) * 32u;
+  const size_t fixed = 8 * kXchgBytes + 1024;   // epilogue exchange, barriers, TMEM slot
+  for (int sl = kMaxSlots; sl >= 2 && !p.ok; --sl) {
+    const size_t need = (size_t)sl * p.halo_stride + p.w_bytes + fixed;
+    if (need <= (size_t)kMaxSmem) p.slots = sl, p.smem = need, p.ok = true;
+  }
+  return p;
+}
+
+template <int EPI, int CO>
+void launch_co(const CUtensorMap& m, const PmArgs& a, size_t smem, int grid, cudaStream_t st) {
+  ensure_max_dynamic_smem(reinterpret_cast<const void*>(conv3x3_pm_kernel<EPI, CO>), kMaxSmem);
+  launch_pdl(conv3x3_pm_kernel<EPI, CO>, grid, kThreads, smem, st, m, a);
+}
+
+template <int EPI>
+void launch_epi(const CUtensorMap& m, const PmArgs& a, size_t smem, int grid, cudaStream_t st) {
+  if (a.Co == 64)
+    launch_co<EPI, 64>(m, a, smem, grid, st);
+  else if (a.Co == 32)
+    launch_co<EPI, 32>(m, a, smem, grid, st);
+  else
+    launch_co<EPI, 16>(m, a, smem, grid, st);
+}
+
+}  // namespace
+
+bool conv3x3_pm_supported(const ConvShape& s) { return plan_for(s).ok; }
+
+void conv3x3_fwd_pm(const ConvShape& s, const float* w_hwio, bool dgrad_weights, const float* bias, const float* aux,
+                    float h, int epi, float* out, void* ws, cudaStream_t st, void* out_planes, const void* in_planes,
+                    const void* wprep, const float* in_scale, const float* out_scale) {
+  if (s.pixels() == 0) return;
+  const Plan p = plan_for(s);
+  if (!p.ok) fail(RP_ERR_INTERNAL, "conv3x3_fwd_pm: unsupported shape");
+  if (!in_planes) fail(RP_ERR_INTERNAL, "conv3x3_fwd_pm: needs plane input");
+  if (!wprep) {   // the filter of this conv alone (a stage prepares all of its filters at once)
+    prep_filter_planes(w_hwio, dgrad_weights ? s.co : s.ci, dgrad_weights ? s.ci : s.co, dgrad_weights, ws, st);
+    wprep = ws;
+  }
+  PmArgs a{};
+  a.N = s.n;
+  a.H = s.h;
+  a.W = s.w;
+  a.Ci = s.ci;
+  a.Co = s.co;
+  a.Wp = p.Wp;
+  a.rows_h = p.rows_h;
+  a.T = p.T;
+  a.nchunks = s.ci / kChunk;
+  a.slots = p.slots;
+  a.halo_pos = p.halo_pos;
+  a.plane_bytes = p.plane_bytes;
+  a.halo_stride = p.halo_stride;
+  a.w_bytes = p.w_bytes;
+  a.h = h;
+  a.w = static_cast<const uint16_t*>(wprep);
+  a.bias = bias;
+  a.aux = aux;
+  a.out = out;
+  a.p0 = static_cast<uint16_t*>(out_planes);
+  a.p1 = out_planes ? a.p0 + s.pixels() * s.co : nullptr;
+  a.in_scale = in_scale;
+  a.out_scale = out_scale;
+  static const int dbg = [] {
+    const char* e = std::getenv("RP_CONV_DBG");
+    return e ? std::atoi(e) : 0;
+  }();
+  a.dbg = dbg;
+  const CUtensorMap m = cached_map(in_planes, s, p.Wp, p.rows_h);
+  const int units = s.n * ((p.T + kS - 1) / kS);
+  const int grid = std::min(units, kNumSMs);
+  switch (epi) {
+    case EPI_BIAS: launch_epi<EPI_BIAS>(m, a, p.smem, grid, st); break;
+    case EPI_BIAS_TANH: launch_epi<EPI_BIAS_TANH>(m, a, p.smem, grid, st); break;
+    case EPI_RESID: launch_epi<EPI_RESID>(m, a, p.smem, grid, st); break;
+    case EPI_TANH_BWD: launch_epi<EPI_TANH_BWD>(m, a, p.smem, grid, st); break;
+    case EPI_ADD: launch_epi<EPI_ADD>(m, a, p.smem, grid, st); break;
+    default: launch_epi<EPI_SCALE>(m, a, p.smem, grid, st); break;
+  }
+  RP_LAUNCHED();
+}
+
+}  // namespace rp::k

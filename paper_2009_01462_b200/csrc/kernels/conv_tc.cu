@@ -780,25 +780,29 @@ struct FilterPair {
 };
 
 // PLANES filters: the same layout, rows r < 64 W0 = fp16(W 2^8), r >= 64 W1 = fp16(W 2^8 - W0)
-// (planes.cuh: |W| < 2^7)
+// (planes.cuh: |W| < 2^7).  Co < 64 (conv_pm.cu only): R = 2 Co rows per (chunk, tap, kg), r < Co
+// W0, r >= Co W1 -- for Co = 64 the same bytes, so both kernels read one prepared filter.
 __device__ __forceinline__ __half prep_f16x2_elem(const float* __restrict__ w, int ci_src, int co_src, int flip,
                                                   int64_t idx) {
   const int Ci = flip ? co_src : ci_src;
-  const int64_t per_cb = 9LL * Ci * 128;
+  const int Co = flip ? ci_src : co_src;
+  const int R = Co < 64 ? 2 * Co : 128;       // rows per (chunk, tap, kg) and output-channel block
+  const int half = R / 2;
+  const int64_t per_cb = 9LL * Ci * R;
   const int cb = (int)(idx / per_cb);
   const int64_t li = idx - cb * per_cb;
   const int e = (int)(li & 7);
-  const int r = (int)((li >> 3) & 127);
-  const int64_t rest = li >> 10;              // (chunk, tap, kg)
+  const int r = (int)((li >> 3) % R);
+  const int64_t rest = (li >> 3) / R;         // (chunk, tap, kg)
   const int kg = (int)(rest % 2);
   const int tap = (int)((rest / 2) % 9);
   const int chunk = (int)(rest / 18);
   const int ci = chunk * kChunk + kg * 8 + e;
-  const int co = cb * 64 + (r < 64 ? r : r - 64);
+  const int co = cb * half + (r < half ? r : r - half);
   const float v = (!flip ? w[((int64_t)tap * ci_src + ci) * co_src + co]
                          : w[((int64_t)(8 - tap) * ci_src + co) * co_src + ci]) * kWeightPlaneScale;
   const __half h = __float2half_rn(v);
-  return r < 64 ? h : __float2half_rn(v - __half2float(h));
+  return r < half ? h : __float2half_rn(v - __half2float(h));
 }
 
 __global__ void prep_weights_f16x2_kernel(const float* __restrict__ w, int ci_src, int co_src, int flip,
@@ -1021,6 +1025,13 @@ void prep_filters_planes(const float* pb, int64_t block_stride, int nblocks, con
   const int64_t total = (int64_t)nblocks * 2 * felems;
   const int grid = (int)std::min<int64_t>(ceil_div(total, 256), 16 * kNumSMs);
   prep_filters_planes_kernel<<<grid, 256, 0, st>>>(pb, block_stride, nblocks, fp, felems, static_cast<__half*>(out));
+  RP_LAUNCHED();
+}
+
+void prep_filter_planes(const float* w_hwio, int ci_src, int co_src, bool dgrad, void* out, cudaStream_t st) {
+  const int64_t total = 9LL * ci_src * co_src * 2;
+  const int grid = (int)std::min<int64_t>(ceil_div(total, 256), 16 * kNumSMs);
+  prep_weights_f16x2_kernel<<<grid, 256, 0, st>>>(w_hwio, ci_src, co_src, dgrad ? 1 : 0, static_cast<__half*>(out));
   RP_LAUNCHED();
 }
 

@@ -75,6 +75,15 @@ void conv3x3_fwd_tc(const ConvShape& s, const float* in, const float* w_hwio, bo
 void prep_filters_planes(const float* pb, int64_t block_stride, int nblocks, const int64_t off[2],
                          const int ci_src[2], const int co_src[2], bool dgrad, void* out, cudaStream_t st);
 
+// One conv's plane-mode filter (the layout prep_filters_planes writes), 9 ci co * 2 fp16.
+void prep_filter_planes(const float* w_hwio, int ci_src, int co_src, bool dgrad, void* out, cudaStream_t st);
+// The positions-as-M plane conv (conv_pm.cu): fp16 plane-pair input only, Co in {16, 32, 64},
+// Ci % 16 == 0; 3 tensor products per MAC.  Arguments as conv3x3_fwd_tc's plane mode.
+bool conv3x3_pm_supported(const ConvShape& s);
+void conv3x3_fwd_pm(const ConvShape& s, const float* w_hwio, bool dgrad_weights, const float* bias, const float* aux,
+                    float h, int epi, float* out, void* ws, cudaStream_t st, void* out_planes, const void* in_planes,
+                    const void* wprep, const float* in_scale, const float* out_scale);
+
 // tcgen05 bf16-operand conv, fp32 accumulate (conv_bf16.cu): Co % 128 == 0, Ci % 32 == 0.
 bool conv3x3_bf16_supported(const ConvShape& s);
 int64_t conv3x3_bf16_ws_bytes(const ConvShape& s);
@@ -116,6 +125,12 @@ void conv3x3_wgrad_planes_pair(const ConvShape& s, const void* const xa[2], cons
                                float* gwa, float* gba, const void* const xb[2], const void* const gb2[2],
                                float scale_b, float* gwb, float* gbb, void* ws, cudaStream_t st, const float* gsc_a,
                                const float* gsc_b);
+// The 16-channel form (conv_wgrad_small.cu, config C1): Ci == 16, Co in {16, 32}; arguments as
+// conv3x3_wgrad_planes.
+bool conv3x3_wgrad_small_supported(const ConvShape& s);
+int64_t conv3x3_wgrad_small_ws_bytes(const ConvShape& s);
+void conv3x3_wgrad_small(const ConvShape& s, const void* x0, const void* x1, const void* g0, const void* g1,
+                         float scale, float* gw, float* gb, void* ws, cudaStream_t st, const float* gscale);
 // The same kernel on single bf16 planes (RP_MATH_BF16): x, g one bf16 NHWC tensor each,
 // 128-channel blocks (Ci, Co % 128 == 0); bf16 x bf16 products, fp32 accumulate.
 bool conv3x3_wgrad_bf16p_supported(const ConvShape& s);

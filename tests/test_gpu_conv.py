@@ -78,17 +78,29 @@ def test_conv_all_epilogues(shape, math, tol, dgrad):
 
 
 PLANE_SHAPES = [(2, 32, 32, 64, 64), (1, 32, 32, 64, 128), (2, 32, 32, 128, 64), (5, 7, 7, 48, 64),
-                (1, 12, 10, 16, 64), (2, 16, 16, 128, 128), (1, 16, 16, 256, 256), (1, 9, 11, 256, 64)]
+                (1, 12, 10, 16, 64), (2, 16, 16, 128, 128), (1, 16, 16, 256, 256), (1, 9, 11, 256, 64),
+                # the positions-as-M kernel's own shapes (Co in {16, 32}; config C1 is 16 x 28 x 28)
+                (3, 28, 28, 16, 16), (2, 9, 13, 32, 16), (1, 6, 7, 16, 32), (2, 17, 5, 32, 32), (1, 1, 1, 16, 16)]
+
+
+@pytest.fixture(params=["pm", "tc"])
+def plane_kernel(request):
+    """run the plane convs on conv_pm.cu (positions as M) or conv_tc.cu (channels as M)"""
+    lib().rp_op_set_plane_conv_kernel(1 if request.param == "pm" else 0)
+    yield request.param
+    lib().rp_op_set_plane_conv_kernel(-1)
 
 
 # plane mode: the input enters as an fp16 pair (22 bits, planes.cuh), W as [W0; W1] (W 2^8, 22 bits);
 # dgrad runs on a cotangent-sized input (1e-5) whose pair carries a device scale (in and out)
 @pytest.mark.parametrize("shape", PLANE_SHAPES)
 @pytest.mark.parametrize("dgrad", [False, True])
-def test_conv_planes(shape, dgrad):
+def test_conv_planes(shape, dgrad, plane_kernel):
     n, hh, ww, ci, co = shape
-    if dgrad and ci % 64:
-        pytest.skip("dgrad output channels (the forward ci) must be a multiple of 64")
+    cin, cout = (co, ci) if dgrad else (ci, co)
+    which = lib().rp_op_plane_conv_kernel(n, hh, ww, cin, cout)
+    if which < 0 or which != (1 if plane_kernel == "pm" else 0):
+        pytest.skip(f"{plane_kernel} does not take Ci {cin} -> Co {cout}")
     dev = torch.device("cuda")
     for epi in range(6):
         rng = np.random.default_rng(epi)
@@ -230,7 +242,10 @@ def run_wgrad_planes(n, hh, ww, ci, co, seed=0, scale=0.37):
 
 # x, g as fp16 plane pairs (22 bits; g with its device scale): fp32-class products
 @pytest.mark.parametrize("shape", [(2, 32, 32, 64, 64), (3, 8, 8, 64, 64), (1, 12, 10, 64, 64), (2, 16, 16, 128, 64),
-                                   (2, 8, 8, 64, 128), (1, 16, 16, 256, 256), (2, 7, 9, 64, 64)])
+                                   (2, 8, 8, 64, 128), (1, 16, 16, 256, 256), (2, 7, 9, 64, 64),
+                                   # the 16-channel kernel (conv_wgrad_small.cu; config C1 = 128 x 28 x 28 x 16)
+                                   (128, 28, 28, 16, 16), (3, 7, 9, 16, 16), (2, 5, 6, 16, 32), (1, 1, 1, 16, 16),
+                                   (4, 28, 28, 16, 32), (2, 33, 17, 16, 16)])
 def test_wgrad_planes(shape):
     gw, gb, ww_, wb = run_wgrad_planes(*shape)
     ew = np.abs(gw - ww_).max() / np.abs(ww_).max()
@@ -242,6 +257,9 @@ def test_wgrad_planes(shape):
 def test_wgrad_deterministic():
     a = run_wgrad(2, 32, 32, 64, 64, "fp32", seed=5)
     b = run_wgrad(2, 32, 32, 64, 64, "fp32", seed=5)
+    assert np.array_equal(a[0], b[0]) and np.array_equal(a[1], b[1])
+    a = run_wgrad_planes(16, 28, 28, 16, 16, seed=5)
+    b = run_wgrad_planes(16, 28, 28, 16, 16, seed=5)
     assert np.array_equal(a[0], b[0]) and np.array_equal(a[1], b[1])
 
 

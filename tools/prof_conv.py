@@ -20,7 +20,9 @@ ap.add_argument("--c", type=int, default=64)
 ap.add_argument("--iters", type=int, default=5)
 ap.add_argument("--math", default="fp32")
 ap.add_argument("--which", default="fprop,dgrad,wgrad")
+ap.add_argument("--kernel", type=int, default=-1, help="plane convs: 1 conv_pm, 0 conv_tc, -1 default")
 a = ap.parse_args()
+lib().rp_op_set_plane_conv_kernel(a.kernel)
 n, h, w, c = a.n, a.hw, a.hw, a.c
 dev = torch.device("cuda")
 x = torch.randn(n, h, w, c, device=dev)

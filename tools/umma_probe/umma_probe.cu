@@ -329,6 +329,64 @@ __global__ void __launch_bounds__(128, 1) umma_bench_kernel(int fmt, int N, int 
         __syncwarp();
         if (++dy == 3) dy = 0;
       }
+    } else if (nops == 70 || nops == 71 || nops == 72) {
+      // positions-as-M plane conv pattern (conv_pm): A = the shifted x-plane halo (M = 128
+      // positions, K-major interleave, LBO = chain * 16), B = the filter [kg 2][2 Co rows][8]
+      // (LBO = 2 Co x 16 B); per tap and 128-position tile: x0 x [W0; W1] (N = 2 Co) and x1 x W0
+      // (N = Co).  N = the 2 Co of the call; 71: both with N = 2 Co (4 products); 72: x0 only.
+      const uint32_t w0 = umma::smem_u32(sm), xh = umma::smem_u32(sm + 64 * 1024), xl = umma::smem_u32(sm + 96 * 1024);
+      const uint32_t kgx = (uint32_t)chain * 16u;
+      const uint64_t dw = umma::desc_kmajor_interleave(w0, (uint32_t)N * 16u, 128);
+      const uint64_t ah = umma::desc_kmajor_interleave(xh, kgx, 128);
+      const uint64_t al = umma::desc_kmajor_interleave(xl, kgx, 128);
+      const uint32_t id_full = umma::idesc(0, 128, N);
+      const uint32_t id_half = umma::idesc(0, 128, nops == 71 ? N : N / 2);
+      const uint64_t wtap = (uint64_t)(N * 32 / 16);   // one tap's filter (2 kg x N rows x 16 B) in 16 B units
+      int dy = 0;
+      const int per = nops == 72 ? 6 : 12;
+      for (int r = 0; r < reps; r += per) {
+        const uint64_t row = (uint64_t)(dy * 34 + 1);
+        if (umma::elect_one()) {
+#pragma unroll
+          for (int dx = 0; dx < 3; ++dx) {
+            const uint64_t db = dw + dx * wtap;
+#pragma unroll
+            for (int t = 0; t < 2; ++t) {
+              const uint64_t a0 = row + dx + (uint64_t)(t * 128);
+              umma::mma_f16(tm + (uint32_t)(t * 256), ah + a0, db, id_full, 1u);
+              if (nops != 72) umma::mma_f16(tm + (uint32_t)(t * 256), al + a0, db, id_half, 1u);
+            }
+          }
+        }
+        __syncwarp();
+        if (++dy == 3) dy = 0;
+      }
+    } else if (nops >= 60 && nops <= 64) {
+      // wgrad_small pattern (conv_wgrad_small.cu): positions are K; A = g groups, B = x groups,
+      // both MN-major no-swizzle ([group][position][8], group stride S = chain * 16 B, LBO = 128 B
+      // between 8-position core matrices); per K-step (16 positions) 9 taps with B shifted by
+      // dy * 34 + dx - 1 positions, each into its own TMEM column block of N.
+      // 60: M = 64 (layout 4) / 128 (else); 61: all taps into one column block; 62: K-major
+      // descriptors instead (same bytes, wrong math; rate only); 63: tap shifts 0
+      const uint32_t S = (uint32_t)chain * 16u;
+      const uint32_t ga = umma::smem_u32(sm), gx = umma::smem_u32(sm + 64 * 1024);
+      const bool mn = nops != 62;
+      const uint64_t dA = mn ? umma::desc_kmajor_interleave(ga, 128, S) : umma::desc_kmajor_interleave(ga, S, 128);
+      const uint64_t dB = mn ? umma::desc_kmajor_interleave(gx, 128, S) : umma::desc_kmajor_interleave(gx, S, 128);
+      const uint32_t idm = umma::idesc(0, layout == 4 ? 64 : 128, N, mn ? 1 : 0, mn ? 1 : 0);
+      int k = 0;
+      for (int r = 0; r < reps; r += 9) {
+        if (umma::elect_one()) {
+#pragma unroll
+          for (int tap = 0; tap < 9; ++tap) {
+            const int sh = nops == 63 ? 0 : (tap / 3) * 34 + (tap % 3) - 1 + 1;
+            umma::mma_f16(tm + (uint32_t)((nops == 61 ? 0 : tap) * N), dA + (uint64_t)(16 * k),
+                          dB + (uint64_t)(sh + 16 * k), idm, 1u);
+          }
+        }
+        __syncwarp();
+        if (++k == 8) k = 0;
+      }
     } else if (nops == 93) {
       // 94 without the k-step advance (B offsets fixed per tap)
       for (int r = 0; r < reps; r += nacc) {
