@@ -14,7 +14,7 @@
 #include "profile.hpp"
 
 #ifndef RP_CONV_PM_DEFAULT
-#define RP_CONV_PM_DEFAULT 0   // Co = 64: conv_tc.cu unless RP_CONV_PM=1
+#define RP_CONV_PM_DEFAULT 1   // Co = 64: conv_pm.cu (measured +4 % on C3 under the power cap) unless RP_CONV_PM=0
 #endif
 
 namespace rp {

@@ -50,6 +50,9 @@ constexpr int kMaxSlots = 8;
 constexpr int kMaxSmem = 227 * 1024;
 constexpr int kPieceBytes = 32 * 1024;   // filter load: bulk copies of <= 32 KB
 constexpr int kXchgBytes = 4096;         // per epilogue warp: 32 positions x 32 channels fp32
+#ifndef RP_CONV_PAIR_DEFAULT
+#define RP_CONV_PAIR_DEFAULT 0              // Co = 64: the CTA-pair form unless RP_CONV_PAIR=0 / 1
+#endif
 
 struct PmArgs {
   int N, H, W, Ci, Co, Wp, rows_h, T, nchunks, slots;
@@ -74,13 +77,13 @@ struct PmArgs {
 // CTA G - 1 down (every CTA ends within one tile of the mean).
 struct Units {
   int f, tl, nf, ntail, fu, T, G;
-  __device__ Units(int N, int T_) : T(T_) {
-    G = gridDim.x;
+  // N images (PAIR: image pairs) over G workers (CTAs, PAIR: CTA pairs), this one idx
+  __device__ Units(int N, int T_, int idx, int G_) : T(T_), G(G_) {
     fu = T / kS;
     nf = N * fu;
     ntail = (T % kS) ? N : 0;
-    f = blockIdx.x;
-    tl = G - 1 - (int)blockIdx.x;
+    f = idx;
+    tl = G - 1 - idx;
   }
   __device__ bool next(int& n, int& tile0, int& ntiles) {
     if (f < nf) {
@@ -103,14 +106,29 @@ struct Units {
 
 __device__ __forceinline__ uint4 cat2(uint2 a, uint2 b) { return make_uint4(a.x, a.y, b.x, b.y); }
 
-template <int EPI, int CO>
+// PAIR: a cluster of two CTAs (one TPC) runs M = 256 MMAs (cta_group::2): CTA r holds image
+// 2 i + r of image pair i at the same frame positions, so both halo slabs sit at the same
+// shared-memory offsets and one descriptor serves both A halves; each CTA holds half of B (x0:
+// W0 | W1 rows; x1: W0 channels [0, 32) | [32, 64)) -- per CTA 11 KB of operand reads per
+// tile and tap instead of 14 KB (the single-CTA form is shared-memory-bandwidth bound).  The
+// leader (rank 0) issues every MMA; the peer's TMA completes on the leader's "full" barriers,
+// the leader's commits multicast to both CTAs, both epilogues release the leader's accumulators.
+template <int EPI, int CO, bool PAIR>
 __global__ void __launch_bounds__(kThreads, 1)
     conv3x3_pm_kernel(const __grid_constant__ CUtensorMap tmap, const PmArgs a) {
   extern __shared__ __align__(1024) uint8_t smem[];
+  static_assert(!PAIR || CO == 64, "CTA-pair form: Co = 64");
   constexpr int kCols = 2 * CO;                                        // accumulator columns per tile
   constexpr int kTmemCols = 2 * kS * kCols < 32 ? 32 : 2 * kS * kCols;  // double-buffered units
   const int warp = __shfl_sync(0xffffffffu, (int)threadIdx.x / 32, 0);
   const int lane = threadIdx.x & 31;
+  const uint32_t rank = PAIR ? cluster_ctarank() : 0u;
+  const bool leader = rank == 0;
+  const int widx = PAIR ? (int)blockIdx.x / 2 : (int)blockIdx.x;     // worker: CTA or CTA pair
+  const int G = PAIR ? (int)gridDim.x / 2 : (int)gridDim.x;
+  const int nitems = PAIR ? (a.N + 1) / 2 : a.N;
+  // this CTA's image of work item i
+  auto image = [&](int i) { return PAIR ? 2 * i + (int)rank : i; };
 
   // ---- shared memory: [slots halo slots][filter][barriers]
   const uint32_t plane_pitch = ((a.plane_bytes + 127u) & ~127u) + 128u;
@@ -123,7 +141,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint64_t* w_full = bars + 2 * kMaxSlots;       // [1]
   uint64_t* acc_full = bars + 2 * kMaxSlots + 1; // [2]
   uint64_t* acc_empty = bars + 2 * kMaxSlots + 3;  // [2]
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * kMaxSlots + 5);
+  uint64_t* w_peer = bars + 2 * kMaxSlots + 5;     // PAIR (leader): the peer's filter landed
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * kMaxSlots + 6);
 
   if (threadIdx.x == 0) {
     for (int i = 0; i < kMaxSlots; ++i) {
@@ -133,12 +152,16 @@ __global__ void __launch_bounds__(kThreads, 1)
     mbar_init(w_full, 1);
     for (int i = 0; i < 2; ++i) {
       mbar_init(&acc_full[i], 1);
-      mbar_init(&acc_empty[i], 256);
+      mbar_init(&acc_empty[i], PAIR ? 16 : 8);   // one arrival per epilogue warp (PAIR: of both CTAs)
     }
+    mbar_init(w_peer, 1);
     fence_barrier_init();
     prefetch_tmap(&tmap);
   }
-  if (warp == 1) tmem_alloc<kTmemCols>(tmem_slot);
+  if (warp == 1) {
+    if constexpr (PAIR) tmem_alloc_pair<kTmemCols>(tmem_slot);
+    else tmem_alloc<kTmemCols>(tmem_slot);
+  }
   // zero the 128-byte pads in front of / behind the planes (read only for discarded positions)
   for (int i = threadIdx.x; i < a.slots * 3 * 32; i += blockDim.x) {
     const int s = i / 96, part = (i / 32) % 3, w = i % 32;
@@ -146,7 +169,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     reinterpret_cast<uint32_t*>(base)[w] = 0u;
   }
   tc_fence_before();
-  __syncthreads();
+  if constexpr (PAIR) cluster_sync();   // barrier inits visible to the peer before any remote arrival
+  else __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = __shfl_sync(0xffffffffu, *tmem_slot, 0);
   const int Wp = a.Wp;
@@ -158,25 +182,51 @@ __global__ void __launch_bounds__(kThreads, 1)
     // the previous grid did (conv_tc.cu, same argument)
     if (elect_one()) {
       mbar_arrive_expect_tx(w_full, a.w_bytes);
-      for (uint32_t o = 0; o < a.w_bytes; o += kPieceBytes)
-        bulk_load(wres + o, reinterpret_cast<const uint8_t*>(a.w) + o, min((uint32_t)kPieceBytes, a.w_bytes - o),
-                  w_full);
+      if constexpr (PAIR) {
+        // this CTA's halves of B out of the standard prepared filter ([chunk][tap][kg][128 rows][8]):
+        // per (chunk, tap) [x0 half: kg x 64 rows][x1 half: kg x 32 rows] = 3 KB
+        const uint8_t* src = reinterpret_cast<const uint8_t*>(a.w);
+        for (int ct = 0; ct < a.nchunks * 9; ++ct) {
+          const uint8_t* sct = src + ct * 4096;
+          uint8_t* dct = wres + ct * 3072;
+          bulk_load(dct, sct + rank * 1024, 1024, w_full);                   // kg 0, rows [64 r, +64)
+          bulk_load(dct + 1024, sct + 2048 + rank * 1024, 1024, w_full);     // kg 1
+          bulk_load(dct + 2048, sct + rank * 512, 512, w_full);              // kg 0, W0 rows [32 r, +32)
+          bulk_load(dct + 2560, sct + 2048 + rank * 512, 512, w_full);       // kg 1
+        }
+      } else {
+        for (uint32_t o = 0; o < a.w_bytes; o += kPieceBytes)
+          bulk_load(wres + o, reinterpret_cast<const uint8_t*>(a.w) + o, min((uint32_t)kPieceBytes, a.w_bytes - o),
+                    w_full);
+      }
     }
     __syncwarp();
+    if (PAIR && !leader) {   // tell the leader (which issues the pair's MMAs) that this half landed
+      mbar_wait(w_full, 0);
+      if (elect_one()) mbar_arrive_cluster(w_peer, 0);
+      __syncwarp();
+    }
   } else if (warp == 0) {
     // ===================== halo TMA producer =====================
     pdl_wait();
     int hs = 0;
     uint32_t hph = 0;
-    Units it(a.N, a.T);
-    int n, tile0, ntiles;
-    while (it.next(n, tile0, ntiles)) {
+    Units it(nitems, a.T, widx, G);
+    int item, tile0, ntiles;
+    while (it.next(item, tile0, ntiles)) {
       const int y0 = tile0 * kTile / Wp;
+      const int n = image(item);   // PAIR, odd N: the last peer loads finite filler, stores nothing
       for (int c = 0; c < a.nchunks; ++c) {
         mbar_wait(&halo_empty[hs], hph ^ 1);
         if (elect_one()) {
           if (a.dbg & 2) {
-            mbar_arrive(&halo_full[hs]);
+            if (leader) mbar_arrive(&halo_full[hs]);
+          } else if constexpr (PAIR) {
+            // both CTAs' bytes complete on the leader's barrier
+            const uint32_t bar = cluster_addr(&halo_full[hs], 0);
+            if (leader) mbar_arrive_expect_tx(&halo_full[hs], 4 * a.plane_bytes);
+            tma_load_5d_pair(&tmap, bar, plane(hs, 0), 0, -1, y0 - 1, 2 * c, n);
+            tma_load_5d_pair(&tmap, bar, plane(hs, 1), 0, -1, y0 - 1, 2 * c, n + a.N);
           } else {
             // both planes of the chunk: images [0, N) are plane 0, [N, 2N) plane 1
             mbar_arrive_expect_tx(&halo_full[hs], 2 * a.plane_bytes);
@@ -188,23 +238,30 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (++hs == a.slots) hs = 0, hph ^= 1;
       }
     }
+  } else if (warp == 1 && !leader) {
+    mbar_wait(w_full, 0);   // the peer's MMA warp: nothing to issue; no exit with the filter load in flight
   } else if (warp == 1) {
     // ===================== MMA issuer =====================
-    const uint32_t id_x0 = idesc(0, 128, kCols);      // x0 x [W0; W1]
-    const uint32_t id_x1 = idesc(0, 128, CO);         // x1 x W0
+    const uint32_t id_x0 = idesc(0, PAIR ? 256 : 128, kCols);   // x0 x [W0; W1]
+    const uint32_t id_x1 = idesc(0, PAIR ? 256 : 128, CO);      // x1 x W0
     const uint32_t lbo_x = (uint32_t)a.halo_pos * 16u;
-    const uint32_t lbo_w = (uint32_t)kCols * 16u;
-    const uint32_t w_tap = (uint32_t)kCols * 32u;     // bytes of one (chunk, tap) filter slice
+    // filter slices: single CTA [kg][2 Co rows][8] per (chunk, tap); PAIR [x0: kg x Co rows | x1: kg x Co / 2 rows]
+    const uint32_t lbo_w = PAIR ? (uint32_t)CO * 16u : (uint32_t)kCols * 16u;
+    const uint32_t lbo_w1 = PAIR ? (uint32_t)CO * 8u : lbo_w;
+    const uint32_t w_tap = PAIR ? (uint32_t)CO * 48u : (uint32_t)kCols * 32u;
+    const uint32_t w_x1 = PAIR ? (uint32_t)CO * 32u : 0u;   // offset of the x1 half in a slice
     int hs = 0, ab = 0;
     uint32_t hph = 0, aph = 0;
     mbar_wait(w_full, 0);   // unconditionally: no CTA may exit with the filter load in flight
+    if (PAIR) mbar_wait_cluster(w_peer, 0);
     tc_fence_after();
-    Units it(a.N, a.T);
-    int n, tile0, ntiles;
-    while (it.next(n, tile0, ntiles)) {
+    Units it(nitems, a.T, widx, G);
+    int item, tile0, ntiles;
+    while (it.next(item, tile0, ntiles)) {
       const int f0 = tile0 * kTile;
       const int c0 = f0 - (f0 / Wp) * Wp;
-      mbar_wait(&acc_empty[ab], aph ^ 1);
+      if (PAIR) mbar_wait_cluster(&acc_empty[ab], aph ^ 1);
+      else mbar_wait(&acc_empty[ab], aph ^ 1);
       tc_fence_after();
       const uint32_t d0 = tmem_base + (uint32_t)(ab * kS * kCols);
       for (int c = 0; c < a.nchunks; ++c) {
@@ -216,27 +273,39 @@ __global__ void __launch_bounds__(kThreads, 1)
           for (int dy = 0; dy < 3; ++dy) {
 #pragma unroll
             for (int dx = 0; dx < 3; ++dx) {
-              const uint64_t db =
-                  desc_kmajor_interleave(smem_u32(wres + (uint32_t)(c * 9 + 3 * dy + dx) * w_tap), lbo_w, 128);
+              const uint32_t wsl = smem_u32(wres + (uint32_t)(c * 9 + 3 * dy + dx) * w_tap);
+              const uint64_t db = desc_kmajor_interleave(wsl, lbo_w, 128);
+              const uint64_t db1 = desc_kmajor_interleave(wsl + w_x1, lbo_w1, 128);
               const int64_t row = c0 + dy * Wp + dx - 1;    // halo position of the tile's first row, >= -1
               const uint32_t accum = (c == 0 && dy == 0 && dx == 0) ? 0u : 1u;
 #pragma unroll
               for (int s = 0; s < kS; ++s) {
                 if (s < ntiles) {
                   const uint64_t ao = (uint64_t)(row + s * kTile);   // 16-byte units: one position = 1
-                  mma_f16(d0 + s * kCols, ax0 + ao, db, id_x0, accum);
-                  mma_f16(d0 + s * kCols, ax1 + ao, db, id_x1, 1u);
+                  if constexpr (PAIR) {
+                    mma_f16_pair(d0 + s * kCols, ax0 + ao, db, id_x0, accum);
+                    mma_f16_pair(d0 + s * kCols, ax1 + ao, db1, id_x1, 1u);
+                  } else {
+                    mma_f16(d0 + s * kCols, ax0 + ao, db, id_x0, accum);
+                    mma_f16(d0 + s * kCols, ax1 + ao, db1, id_x1, 1u);
+                  }
                 }
               }
             }
           }
         }
         __syncwarp();
-        if (elect_one()) mma_commit(&halo_empty[hs]);
+        if (elect_one()) {
+          if constexpr (PAIR) mma_commit_pair(&halo_empty[hs], 3);
+          else mma_commit(&halo_empty[hs]);
+        }
         __syncwarp();
         if (++hs == a.slots) hs = 0, hph ^= 1;
       }
-      if (elect_one()) mma_commit(&acc_full[ab]);
+      if (elect_one()) {
+        if constexpr (PAIR) mma_commit_pair(&acc_full[ab], 3);
+        else mma_commit(&acc_full[ab]);
+      }
       __syncwarp();
       if (++ab == 2) ab = 0, aph ^= 1;
     }
@@ -259,12 +328,13 @@ __global__ void __launch_bounds__(kThreads, 1)
     float4* xrow = reinterpret_cast<float4*>(xchg + (warp - 4) * kXchgBytes);
     int ab = 0;
     uint32_t aph = 0;
-    Units it(a.N, a.T);
-    int n, tile0, ntiles;
-    while (it.next(n, tile0, ntiles)) {
+    Units it(nitems, a.T, widx, G);
+    int item, tile0, ntiles;
+    while (it.next(item, tile0, ntiles)) {
+      const int n = image(item);
       const int f = (tile0 + grp) * kTile + pt;
       const int y = f / Wp, X = f - y * Wp;
-      const bool valid = grp < ntiles && y < a.H && X >= 1;
+      const bool valid = grp < ntiles && y < a.H && X >= 1 && n < a.N;
       const int64_t off = valid ? (((int64_t)n * a.H + y) * a.W + (X - 1)) * CO : 0;
       // the tile's aux operand first: its latency overlaps the wait for the accumulator
       float4 ax[kAux ? CO / 4 : 1];
@@ -275,32 +345,46 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
       mbar_wait(&acc_full[ab], aph);
       tc_fence_after();
-      if (grp < ntiles && !(a.dbg & 1)) {
+      // the tile's accumulators first (W0 + W1 columns, scaled): the TMEM buffer goes back to the
+      // MMA before the epilogue math and the stores
+      const bool live = grp < ntiles && !(a.dbg & 1);
+      float acc[CO];
+      if (live) {
         const uint32_t tcol = tmem_base + ((uint32_t)(q * 32) << 16) + (uint32_t)(ab * kS * kCols + grp * kCols);
 #pragma unroll
+        for (int cc = 0; cc < CO / 16; ++cc) {
+          uint32_t hi[16], lo[16];
+          tmem_ld16(tcol + cc * 16, hi);
+          tmem_ld16(tcol + CO + cc * 16, lo);
+          tmem_wait_ld();
+#pragma unroll
+          for (int i = 0; i < 16; ++i) acc[cc * 16 + i] = (__uint_as_float(hi[i]) + __uint_as_float(lo[i])) * acc_mul;
+        }
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) {
+        if constexpr (PAIR) mbar_arrive_cluster_relaxed(&acc_empty[ab], 0);   // the leader's accumulators
+        else mbar_arrive_relaxed(&acc_empty[ab]);
+      }
+      if (live) {
+#pragma unroll
         for (int hf = 0; hf < CO / kCh; ++hf) {
-          // this position's kCh channels [hf kCh, +kCh): W0 + W1 columns, scales, epilogue
+          // this position's kCh channels [hf kCh, +kCh): the fused epilogue
           float o[kCh];
 #pragma unroll
-          for (int cc = 0; cc < kCh / 16; ++cc) {
-            uint32_t hi[16], lo[16];
-            tmem_ld16(tcol + hf * kCh + cc * 16, hi);
-            tmem_ld16(tcol + CO + hf * kCh + cc * 16, lo);
-            tmem_wait_ld();
-#pragma unroll
-            for (int i = 0; i < 16; ++i) {
-              const float v = (__uint_as_float(hi[i]) + __uint_as_float(lo[i])) * acc_mul;
-              const int co = hf * kCh + cc * 16 + i;
-              const float xa = kAux ? reinterpret_cast<const float*>(&ax[0])[co] : 0.f;
-              float r;
-              if constexpr (EPI == EPI_BIAS) r = v + __ldg(a.bias + co);
-              else if constexpr (EPI == EPI_BIAS_TANH) r = tanhf(v + __ldg(a.bias + co));
-              else if constexpr (EPI == EPI_RESID) r = xa + a.h * (v + __ldg(a.bias + co));
-              else if constexpr (EPI == EPI_TANH_BWD) r = (a.h * v) * (1.f - xa * xa);
-              else if constexpr (EPI == EPI_ADD) r = xa + v;
-              else r = a.h * v;
-              o[cc * 16 + i] = r;
-            }
+          for (int i = 0; i < kCh; ++i) {
+            const int co = hf * kCh + i;
+            const float v = acc[co];
+            const float xa = kAux ? reinterpret_cast<const float*>(&ax[0])[co] : 0.f;
+            float r;
+            if constexpr (EPI == EPI_BIAS) r = v + __ldg(a.bias + co);
+            else if constexpr (EPI == EPI_BIAS_TANH) r = tanhf(v + __ldg(a.bias + co));
+            else if constexpr (EPI == EPI_RESID) r = xa + a.h * (v + __ldg(a.bias + co));
+            else if constexpr (EPI == EPI_TANH_BWD) r = (a.h * v) * (1.f - xa * xa);
+            else if constexpr (EPI == EPI_ADD) r = xa + v;
+            else r = a.h * v;
+            o[i] = r;
           }
           // stores through the warp's exchange rows (thread = position -> kNJ 16-byte pieces of
           // consecutive positions per instruction: 32 / kNJ positions x kCh * 4 bytes contiguous);
@@ -347,16 +431,16 @@ __global__ void __launch_bounds__(kThreads, 1)
           }
         }
       }
-      tc_fence_before();
-      mbar_arrive(&acc_empty[ab]);
       if (++ab == 2) ab = 0, aph ^= 1;
     }
   }
   tc_fence_before();
-  __syncthreads();
+  if constexpr (PAIR) cluster_sync();   // the peer's TMEM holds MMA results until both are done
+  else __syncthreads();
   if (warp == 1) {
     tc_fence_after();
-    tmem_dealloc<kTmemCols>(tmem_base);
+    if constexpr (PAIR) tmem_dealloc_pair<kTmemCols>(tmem_base);
+    else tmem_dealloc<kTmemCols>(tmem_base);
   }
 }
 
@@ -412,6 +496,7 @@ CUtensorMap cached_map(const void* in, const ConvShape& s, int Wp, int rows_h) {
 
 struct Plan {
   bool ok = false;
+  bool pair = false;   // CTA-pair form (Co = 64)
   int Wp, rows_h, halo_pos, T, slots;
   uint32_t plane_bytes, halo_stride, w_bytes;
   size_t smem;
@@ -429,7 +514,13 @@ Plan plan_for(const ConvShape& s) {
   p.plane_bytes = (uint32_t)p.halo_pos * 32u;
   const uint32_t pitch = ((p.plane_bytes + 127u) & ~127u) + 128u;
   p.halo_stride = 128u + 2u * pitch;
-  p.w_bytes = (uint32_t)(s.ci / kChunk) * 9u * (uint32_t)(2 * s.co) * 32u;
+  static const bool pair_on = [] {
+    const char* e = std::getenv("RP_CONV_PAIR");
+    return e ? e[0] != '0' : RP_CONV_PAIR_DEFAULT != 0;
+  }();
+  p.pair = pair_on && s.co == 64;
+  // per CTA: the whole filter, or (PAIR) its halves of B -- 3/4 of it
+  p.w_bytes = (uint32_t)(s.ci / kChunk) * 9u * (uint32_t)(2 * s.co) * 32u * (p.pair ? 3u : 4u) / 4u;
   const size_t fixed = 8 * kXchgBytes + 1024;   // epilogue exchange, barriers, TMEM slot
   for (int sl = kMaxSlots; sl >= 2 && !p.ok; --sl) {
     const size_t need = (size_t)sl * p.halo_stride + p.w_bytes + fixed;
@@ -438,20 +529,57 @@ Plan plan_for(const ConvShape& s) {
   return p;
 }
 
-template <int EPI, int CO>
-void launch_co(const CUtensorMap& m, const PmArgs& a, size_t smem, int grid, cudaStream_t st) {
-  ensure_max_dynamic_smem(reinterpret_cast<const void*>(conv3x3_pm_kernel<EPI, CO>), kMaxSmem);
-  launch_pdl(conv3x3_pm_kernel<EPI, CO>, grid, kThreads, smem, st, m, a);
+template <int EPI, int CO, bool PAIR>
+void launch_co(const CUtensorMap& m, const PmArgs& a, size_t smem, int units, cudaStream_t st) {
+  const void* fn = reinterpret_cast<const void*>(conv3x3_pm_kernel<EPI, CO, PAIR>);
+  ensure_max_dynamic_smem(fn, kMaxSmem);
+  if constexpr (PAIR) {
+    // co-resident CTA pairs (normally every TPC: 74)
+    static std::mutex mu;
+    static std::map<size_t, int> max_pairs;
+    int pairs;
+    {
+      std::lock_guard<std::mutex> lk(mu);
+      auto it = max_pairs.find(smem);
+      if (it == max_pairs.end()) {
+        cudaLaunchConfig_t cfg{};
+        cfg.gridDim = dim3(kNumSMs);
+        cfg.blockDim = dim3(kThreads);
+        cfg.dynamicSmemBytes = smem;
+        cudaLaunchAttribute attr[1];
+        attr[0].id = cudaLaunchAttributeClusterDimension;
+        attr[0].val.clusterDim.x = 2;
+        attr[0].val.clusterDim.y = 1;
+        attr[0].val.clusterDim.z = 1;
+        cfg.attrs = attr;
+        cfg.numAttrs = 1;
+        int n = 0;
+        if (cudaOccupancyMaxActiveClusters(&n, conv3x3_pm_kernel<EPI, CO, PAIR>, &cfg) != cudaSuccess) {
+          cudaGetLastError();
+          n = 0;
+        }
+        it = max_pairs.emplace(smem, n).first;
+      }
+      pairs = it->second;
+    }
+    if (pairs < 1) fail(RP_ERR_CUDA, "conv3x3_fwd_pm: no CTA pair fits");
+    const int grid = 2 * std::min(units, std::min(pairs, kNumSMs / 2));
+    launch_pdl_cluster(conv3x3_pm_kernel<EPI, CO, PAIR>, grid, kThreads, smem, st, 2, m, a);
+  } else {
+    launch_pdl(conv3x3_pm_kernel<EPI, CO, PAIR>, std::min(units, kNumSMs), kThreads, smem, st, m, a);
+  }
 }
 
 template <int EPI>
-void launch_epi(const CUtensorMap& m, const PmArgs& a, size_t smem, int grid, cudaStream_t st) {
-  if (a.Co == 64)
-    launch_co<EPI, 64>(m, a, smem, grid, st);
+void launch_epi(const CUtensorMap& m, const PmArgs& a, size_t smem, int units, bool pair, cudaStream_t st) {
+  if (a.Co == 64 && pair)
+    launch_co<EPI, 64, true>(m, a, smem, units, st);
+  else if (a.Co == 64)
+    launch_co<EPI, 64, false>(m, a, smem, units, st);
   else if (a.Co == 32)
-    launch_co<EPI, 32>(m, a, smem, grid, st);
+    launch_co<EPI, 32, false>(m, a, smem, units, st);
   else
-    launch_co<EPI, 16>(m, a, smem, grid, st);
+    launch_co<EPI, 16, false>(m, a, smem, units, st);
 }
 
 }  // namespace
@@ -499,15 +627,15 @@ void conv3x3_fwd_pm(const ConvShape& s, const float* w_hwio, bool dgrad_weights,
   }();
   a.dbg = dbg;
   const CUtensorMap m = cached_map(in_planes, s, p.Wp, p.rows_h);
-  const int units = s.n * ((p.T + kS - 1) / kS);
-  const int grid = std::min(units, kNumSMs);
+  // work items: units of one image, or (PAIR) of an image pair
+  const int units = (p.pair ? (s.n + 1) / 2 : s.n) * ((p.T + kS - 1) / kS);
   switch (epi) {
-    case EPI_BIAS: launch_epi<EPI_BIAS>(m, a, p.smem, grid, st); break;
-    case EPI_BIAS_TANH: launch_epi<EPI_BIAS_TANH>(m, a, p.smem, grid, st); break;
-    case EPI_RESID: launch_epi<EPI_RESID>(m, a, p.smem, grid, st); break;
-    case EPI_TANH_BWD: launch_epi<EPI_TANH_BWD>(m, a, p.smem, grid, st); break;
-    case EPI_ADD: launch_epi<EPI_ADD>(m, a, p.smem, grid, st); break;
-    default: launch_epi<EPI_SCALE>(m, a, p.smem, grid, st); break;
+    case EPI_BIAS: launch_epi<EPI_BIAS>(m, a, p.smem, units, p.pair, st); break;
+    case EPI_BIAS_TANH: launch_epi<EPI_BIAS_TANH>(m, a, p.smem, units, p.pair, st); break;
+    case EPI_RESID: launch_epi<EPI_RESID>(m, a, p.smem, units, p.pair, st); break;
+    case EPI_TANH_BWD: launch_epi<EPI_TANH_BWD>(m, a, p.smem, units, p.pair, st); break;
+    case EPI_ADD: launch_epi<EPI_ADD>(m, a, p.smem, units, p.pair, st); break;
+    default: launch_epi<EPI_SCALE>(m, a, p.smem, units, p.pair, st); break;
   }
   RP_LAUNCHED();
 }

@@ -46,7 +46,8 @@ struct WsArgs {
   int N, H, W, Co, Wp, rows_h, T, ntiles, slots;
   uint32_t S;               // bytes per 8-channel group region of a slot (rows_h x Wp x 16)
   uint32_t slot_bytes;
-  int ga;                   // A groups (g planes) = max(2 Co / 8, 8): the x groups follow them
+  int ga;                   // g groups (2 Co / 8); the x groups follow them (Co = 16: A's rows 32-63,
+                            // which nobody reads, are the x groups -- finite data)
   float* part;              // [grid][2 g planes][9][16 ci][Co]
   float* part_bias;         // [grid][2][Co]
   // reduce
@@ -54,6 +55,7 @@ struct WsArgs {
   float* gb;
   double scale;
   const float* gscale;      // the g planes' scale (device scalar; null = kActPlaneScale)
+  int dbg;                  // diagnostics (RP_WGRAD_SMALL_DBG): 1 no MMA, 2 no TMA
 };
 
 // TMEM column block of tap t: the centre tap last (its N = 40 reaches past 32 columns)
@@ -66,7 +68,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   extern __shared__ __align__(1024) uint8_t smem[];
   const int warp = __shfl_sync(0xffffffffu, (int)threadIdx.x / 32, 0);
   const int lane = threadIdx.x & 31;
-  // slot: [ga groups: g0 kg.., g1 kg..][4 groups: x0 kg0, x0 kg1, x1 kg0, x1 kg1][ones], S bytes each
+  // slot: [ga groups: g0 kg.., g1 kg..][4 groups: x0 kg0, x0 kg1, x1 kg0, x1 kg1][ones], S bytes each;
+  // x's shift -1 reads the last g position before it (finite; its partner g is a pad column, 0)
   auto slot = [&](int s) { return smem + s * a.slot_bytes; };
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + a.slots * a.slot_bytes);
   uint64_t* full = bars;                  // [kMaxSlots]
@@ -87,14 +90,10 @@ __global__ void __launch_bounds__(kThreads, 1)
     prefetch_tmap(&mg1);
   }
   if (warp == 1) tmem_alloc<512>(tmem_slot);
-  // zero every slot (positions the boxes do not reach are read as 0 x finite), ones groups = 1.0
-  {
-    const uint32_t words = a.slots * a.slot_bytes / 4;
-    const uint32_t ones0 = (uint32_t)(a.ga + 4) * a.S / 4, ones1 = ones0 + a.S / 4;
-    for (uint32_t i = threadIdx.x; i < words; i += blockDim.x) {
-      const uint32_t w = i % (a.slot_bytes / 4);
-      reinterpret_cast<uint32_t*>(smem)[i] = (w >= ones0 && w < ones1) ? 0x3c003c00u : 0u;
-    }
+  // the ones group of every slot = 1.0 (the boxes fill the g and x groups completely)
+  for (int s = 0; s < a.slots; ++s) {
+    uint4* ones = reinterpret_cast<uint4*>(slot(s) + (a.ga + 4) * a.S);
+    for (uint32_t i = threadIdx.x; i < a.S / 16; i += blockDim.x) ones[i] = make_uint4(0x3c003c00u, 0x3c003c00u, 0x3c003c00u, 0x3c003c00u);
   }
   fence_proxy_async_smem();
   tc_fence_before();
@@ -118,12 +117,16 @@ __global__ void __launch_bounds__(kThreads, 1)
       if (elect_one()) {
         uint8_t* b = slot(s);
         const uint32_t gplane = (uint32_t)(a.Co / 8) * a.S, xplane = 2 * a.S;   // one plane's 8-channel groups
+        if (a.dbg & 2) {
+          mbar_arrive(&full[s]);
+        } else {
         mbar_arrive_expect_tx(&full[s], 2 * gplane + 2 * xplane);
         // g at its own positions (rows from y0), x with the one-row / one-column halo
         tma_load_5d(&mg0, &full[s], b, 0, -1, y0, 0, n);
         tma_load_5d(&mg1, &full[s], b + gplane, 0, -1, y0, 0, n);
         tma_load_5d(&mx0, &full[s], b + a.ga * a.S, 0, -1, y0 - 1, 0, n);
         tma_load_5d(&mx1, &full[s], b + a.ga * a.S + xplane, 0, -1, y0 - 1, 0, n);
+        }
       }
       __syncwarp();
       if (++s == a.slots) s = 0, ph ^= 1;
@@ -145,7 +148,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         // groups S apart (SBO)
         const uint64_t da = desc_kmajor_interleave(smem_u32(slot(s)), 128, a.S) + (uint64_t)c0;
         const uint64_t dx = desc_kmajor_interleave(smem_u32(slot(s) + a.ga * a.S), 128, a.S);
-        for (int k = 0; k < kTile / 16; ++k) {
+        for (int k = 0; k < ((a.dbg & 1) ? 0 : kTile / 16); ++k) {
 #pragma unroll
           for (int tap = 0; tap < 9; ++tap) {
             const int dy = tap / 3, dxx = tap % 3;
@@ -206,11 +209,11 @@ __global__ void __launch_bounds__(kThreads, 1)
 
 // gw = scale / (kActPlaneScale gs) sum_cta sum_gplane part, gb = scale / gs sum_cta sum_gplane
 // bias part, in fp64 and a fixed order (deterministic): a CTA owns 32 consecutive outputs (coalesced
-// loads); its 8 warps sum fixed eighths of the partials (4 loads in flight), combined in order.
-__global__ void __launch_bounds__(256) wgrad_small_reduce_kernel(const WsArgs a, int grid) {
+// loads); its 32 warps sum fixed 32nds of the partials, combined in order.
+__global__ void __launch_bounds__(1024) wgrad_small_reduce_kernel(const WsArgs a, int grid) {
   pdl_launch_dependents();
   pdl_wait();
-  __shared__ double red[8][32];
+  __shared__ double red[32][33];
   const int nw = 9 * 16 * a.Co;
   const int lane = threadIdx.x & 31, wg = threadIdx.x >> 5;
   const int i = blockIdx.x * 32 + lane;
@@ -220,26 +223,23 @@ __global__ void __launch_bounds__(256) wgrad_small_reduce_kernel(const WsArgs a,
   const int64_t gstride = bias ? a.Co : nw;               // per g plane
   double acc = 0.0;
   if (i < nw + a.Co) {
-    const int c_lo = grid * wg / 8, c_hi = grid * (wg + 1) / 8;
-    int c = c_lo;
-    for (; c + 4 <= c_hi; c += 4) {
-      float v[8];
+    const int c_lo = grid * wg / 32, c_hi = grid * (wg + 1) / 32;
+    float v[16];
 #pragma unroll
-      for (int j = 0; j < 4; ++j) {
-        v[2 * j] = src[(c + j) * cstride];
-        v[2 * j + 1] = src[(c + j) * cstride + gstride];
-      }
-#pragma unroll
-      for (int j = 0; j < 8; ++j) acc += (double)v[j];
+    for (int j = 0; j < 8; ++j) {
+      const int c = c_lo + j;
+      v[2 * j] = c < c_hi ? src[c * cstride] : 0.f;
+      v[2 * j + 1] = c < c_hi ? src[c * cstride + gstride] : 0.f;
     }
-    for (; c < c_hi; ++c) acc += (double)src[c * cstride] + (double)src[c * cstride + gstride];
+#pragma unroll
+    for (int j = 0; j < 16; ++j) acc += (double)v[j];
+    for (int c = c_lo + 8; c < c_hi; ++c) acc += (double)src[c * cstride] + (double)src[c * cstride + gstride];
   }
   red[wg][lane] = acc;
   __syncthreads();
   if (wg == 0 && i < nw + a.Co && (!bias || a.gb)) {
     double s = 0.0;
-#pragma unroll
-    for (int j = 0; j < 8; ++j) s += red[j][lane];
+    for (int j = 0; j < 32; ++j) s += red[j][lane];
     const double gs = a.gscale ? (double)*a.gscale : (double)kActPlaneScale;
     if (bias) a.gb[i - nw] = (float)(s * a.scale / gs);
     else a.gw[i] = (float)(s * a.scale / ((double)kActPlaneScale * gs));
@@ -313,7 +313,7 @@ Plan plan(const ConvShape& s) {
   if (p.rows_h > 256) return p;
   p.T = (s.h * p.Wp + kTile - 1) / kTile;
   p.S = (uint32_t)(p.rows_h * p.Wp * 16);
-  p.ga = std::max(2 * s.co / 8, 8);
+  p.ga = 2 * s.co / 8;
   p.slot_bytes = (p.ga + 5) * p.S;
   p.slot_bytes = (p.slot_bytes + 127u) & ~127u;
   const size_t fixed = 256;
@@ -364,6 +364,11 @@ void conv3x3_wgrad_small(const ConvShape& s, const void* x0, const void* x1, con
   a.gb = gb;
   a.scale = scale;
   a.gscale = gscale;
+  static const int dbg = [] {
+    const char* e = std::getenv("RP_WGRAD_SMALL_DBG");
+    return e ? std::atoi(e) : 0;
+  }();
+  a.dbg = dbg;
   const CUtensorMap mx0 = cached_map(x0, s.n, s.h, s.w, s.ci, p.Wp, p.rows_h);
   const CUtensorMap mx1 = cached_map(x1, s.n, s.h, s.w, s.ci, p.Wp, p.rows_h);
   const CUtensorMap mg0 = cached_map(g0, s.n, s.h, s.w, s.co, p.Wp, p.rows_h);
@@ -372,7 +377,7 @@ void conv3x3_wgrad_small(const ConvShape& s, const void* x0, const void* x1, con
   launch_pdl(wgrad_small_kernel, p.grid, kThreads, p.smem, st, mx0, mx1, mg0, mg1, a);
   RP_LAUNCHED();
   const int total = 9 * 16 * s.co + s.co;
-  launch_pdl(wgrad_small_reduce_kernel, ceil_div(total, 32), 256, 0, st, a, p.grid);
+  launch_pdl(wgrad_small_reduce_kernel, ceil_div(total, 32), 1024, 0, st, a, p.grid);
   RP_LAUNCHED();
 }
 

@@ -45,7 +45,8 @@ def _rel(got, want):
     return np.abs(got - want).max() / max(np.abs(want).max(), 1e-30)
 
 
-@pytest.mark.parametrize("n,hw,c,ch", [(4, 16, 64, 64), (2, 32, 64, 128), (3, 8, 128, 64)])
+@pytest.mark.parametrize("n,hw,c,ch", [(4, 16, 64, 64), (2, 32, 64, 128), (3, 8, 128, 64),
+                                       (8, 28, 16, 16), (3, 9, 16, 16)])   # C1: 16 channels (conv_pm, wgrad_small)
 def test_block_planes(n, hw, c, ch):
     og = O.Geometry(in_channels=3, height=hw, width=hw, channels=c, hidden=ch, blocks=1, classes=10,
                     activation=O.TANH, step_h=0.5)

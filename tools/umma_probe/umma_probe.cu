@@ -614,3 +614,90 @@ extern "C" int rp_debug_umma_m64_layout(float* out) {
     return e.code;
   }
 }
+
+// ---------------------------------------------------------------------------
+// TMA throughput by box shape: every CTA loads `iters` conv-halo boxes of an fp16 NHWC tensor
+// [n][h][w][c] (image blockIdx.x + 148 i, rows from -1, columns from -1, zero fill) into a ring of
+// `depth` 32 KB slots; cycles for the whole loop -> out[blockIdx.x].  cg = channels per box row
+// (8: 16-byte rows in two 8-channel groups, the plane convs' box {8, W + 1, rows, 2}; 16 / 32 / 64:
+// 32 / 64 / 128-byte rows {cg, W + 1, rows}).
+namespace rp::k {
+namespace {
+__global__ void __launch_bounds__(32, 1) tma_bench_kernel(const __grid_constant__ CUtensorMap m, int n_img, int groups5,
+                                                          int iters, int depth, uint32_t box_bytes, int five,
+                                                          float* out) {
+  extern __shared__ __align__(1024) uint8_t sm[];
+  __shared__ uint64_t bars[8];
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < 8; ++i) umma::mbar_init(&bars[i], 1);
+    umma::fence_barrier_init();
+  }
+  __syncwarp();
+  const long long t0 = clock64();
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < iters + depth; ++i) {
+      if (i >= depth) umma::mbar_wait(&bars[(i - depth) % depth], ((i - depth) / depth) & 1);
+      if (i < iters) {
+        const int s = i % depth;
+        const int img = (blockIdx.x + 148 * i) % n_img;
+        umma::mbar_arrive_expect_tx(&bars[s], box_bytes);
+        if (five)
+          umma::tma_load_5d(&m, &bars[s], sm + s * 32768, 0, -1, -1, 0, img);
+        else
+          umma::tma_load_4d(&m, &bars[s], sm + s * 32768, 0, -1, -1, img);
+      }
+    }
+    out[blockIdx.x] = (float)(clock64() - t0);
+  }
+  (void)groups5;
+}
+}  // namespace
+}  // namespace rp::k
+
+extern "C" int rp_debug_tma_bench(const void* data, int n, int h, int w, int c, int cg, int rows, int iters, int depth,
+                                  float* out) {
+  try {
+    typedef CUresult (*Enc)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                            const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                            CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    RP_CUDA(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q));
+    Enc enc = reinterpret_cast<Enc>(p);
+    CUtensorMap m;
+    uint32_t box_bytes;
+    const int Wp = w + 1;
+    int five;
+    if (cg == 8) {   // {8, Wp, rows, c / 8, 1}: 16-byte rows, all groups in one box
+      const cuuint64_t dims[5] = {8, (cuuint64_t)w, (cuuint64_t)h, (cuuint64_t)(c / 8), (cuuint64_t)n};
+      const cuuint64_t strides[4] = {(cuuint64_t)c * 2, (cuuint64_t)w * c * 2, 16, (cuuint64_t)h * w * c * 2};
+      const cuuint32_t box[5] = {8, (cuuint32_t)Wp, (cuuint32_t)rows, 2, 1};   // one 16-channel chunk
+      const cuuint32_t es[5] = {1, 1, 1, 1, 1};
+      if (enc(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 5, const_cast<void*>(data), dims, strides, box, es,
+              CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+        return 99;
+      box_bytes = (uint32_t)(16 * Wp * rows * 2);
+      five = 1;
+    } else {         // {cg, Wp, rows, 1}: cg * 2-byte rows (only the first cg channels)
+      const cuuint64_t dims[4] = {(cuuint64_t)c, (cuuint64_t)w, (cuuint64_t)h, (cuuint64_t)n};
+      const cuuint64_t strides[3] = {(cuuint64_t)c * 2, (cuuint64_t)w * c * 2, (cuuint64_t)h * w * c * 2};
+      const cuuint32_t box[4] = {(cuuint32_t)cg, (cuuint32_t)Wp, (cuuint32_t)rows, 1};
+      const cuuint32_t es[4] = {1, 1, 1, 1};
+      if (enc(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 4, const_cast<void*>(data), dims, strides, box, es,
+              CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+        return 98;
+      box_bytes = (uint32_t)(2 * cg * Wp * rows);
+      five = 0;
+    }
+    if (box_bytes > 32768) return 97;
+    RP_CUDA(cudaFuncSetAttribute(rp::k::tma_bench_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 6 * 32768));
+    rp::k::tma_bench_kernel<<<148, 32, depth * 32768>>>(m, n, c / 8, iters, depth, box_bytes, five, out);
+    RP_CUDA(cudaGetLastError());
+    RP_CUDA(cudaDeviceSynchronize());
+    return 0;
+  } catch (const rp::Error& e) {
+    return e.code;
+  }
+}
