@@ -69,6 +69,7 @@ struct PmArgs {
   uint16_t* p1;
   const float* in_scale;   // the input planes' scale (device scalar; null = kActPlaneScale)
   const float* out_scale;  // the output planes' scale (device scalar; null = kActPlaneScale)
+  int sw32;                // halo slab: 32-byte swizzled position rows (1) or the [kg][pos][8] interleave (0)
   int dbg;                 // diagnostics (RP_CONV_DBG): 1 no epilogue, 2 no halo TMA, 8 no MMA
 };
 
@@ -131,8 +132,10 @@ __global__ void __launch_bounds__(kThreads, 1)
   auto image = [&](int i) { return PAIR ? 2 * i + (int)rank : i; };
 
   // ---- shared memory: [slots halo slots][filter][barriers]
-  const uint32_t plane_pitch = ((a.plane_bytes + 127u) & ~127u) + 128u;
-  auto plane = [&](int s, int p) { return smem + s * a.halo_stride + 128 + p * plane_pitch; };
+  // slot: [pad][plane 0][pad][plane 1][pad]; SW32: 256-byte aligned planes (the swizzle atom)
+  const uint32_t al = a.sw32 ? 256u : 128u;
+  const uint32_t plane_pitch = ((a.plane_bytes + al - 1) & ~(al - 1)) + al;
+  auto plane = [&](int s, int p) { return smem + s * a.halo_stride + al + p * plane_pitch; };
   uint8_t* wres = smem + a.slots * a.halo_stride;
   uint8_t* xchg = wres + a.w_bytes;                                    // [8 epilogue warps][kXchgBytes]
   uint64_t* bars = reinterpret_cast<uint64_t*>(xchg + 8 * kXchgBytes);
@@ -165,7 +168,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   // zero the 128-byte pads in front of / behind the planes (read only for discarded positions)
   for (int i = threadIdx.x; i < a.slots * 3 * 32; i += blockDim.x) {
     const int s = i / 96, part = (i / 32) % 3, w = i % 32;
-    uint8_t* base = part == 0 ? smem + s * a.halo_stride : plane(s, part - 1) + a.plane_bytes;
+    uint8_t* base = part == 0 ? plane(s, 0) - 128 : plane(s, part - 1) + a.plane_bytes;
     reinterpret_cast<uint32_t*>(base)[w] = 0u;
   }
   tc_fence_before();
@@ -225,13 +228,23 @@ __global__ void __launch_bounds__(kThreads, 1)
             // both CTAs' bytes complete on the leader's barrier
             const uint32_t bar = cluster_addr(&halo_full[hs], 0);
             if (leader) mbar_arrive_expect_tx(&halo_full[hs], 4 * a.plane_bytes);
-            tma_load_5d_pair(&tmap, bar, plane(hs, 0), 0, -1, y0 - 1, 2 * c, n);
-            tma_load_5d_pair(&tmap, bar, plane(hs, 1), 0, -1, y0 - 1, 2 * c, n + a.N);
+            if (a.sw32) {
+              tma_load_4d_pair(&tmap, bar, plane(hs, 0), kChunk * c, -1, y0 - 1, n);
+              tma_load_4d_pair(&tmap, bar, plane(hs, 1), kChunk * c, -1, y0 - 1, n + a.N);
+            } else {
+              tma_load_5d_pair(&tmap, bar, plane(hs, 0), 0, -1, y0 - 1, 2 * c, n);
+              tma_load_5d_pair(&tmap, bar, plane(hs, 1), 0, -1, y0 - 1, 2 * c, n + a.N);
+            }
           } else {
             // both planes of the chunk: images [0, N) are plane 0, [N, 2N) plane 1
             mbar_arrive_expect_tx(&halo_full[hs], 2 * a.plane_bytes);
-            tma_load_5d(&tmap, &halo_full[hs], plane(hs, 0), 0, -1, y0 - 1, 2 * c, n);
-            tma_load_5d(&tmap, &halo_full[hs], plane(hs, 1), 0, -1, y0 - 1, 2 * c, n + a.N);
+            if (a.sw32) {   // 32-byte box rows (16 channels), 32B-swizzled: half the TMA row count
+              tma_load_4d(&tmap, &halo_full[hs], plane(hs, 0), kChunk * c, -1, y0 - 1, n);
+              tma_load_4d(&tmap, &halo_full[hs], plane(hs, 1), kChunk * c, -1, y0 - 1, n + a.N);
+            } else {
+              tma_load_5d(&tmap, &halo_full[hs], plane(hs, 0), 0, -1, y0 - 1, 2 * c, n);
+              tma_load_5d(&tmap, &halo_full[hs], plane(hs, 1), 0, -1, y0 - 1, 2 * c, n + a.N);
+            }
           }
         }
         __syncwarp();
@@ -267,8 +280,14 @@ __global__ void __launch_bounds__(kThreads, 1)
       for (int c = 0; c < a.nchunks; ++c) {
         mbar_wait(&halo_full[hs], hph);
         tc_fence_after();
-        const uint64_t ax0 = desc_kmajor_interleave(smem_u32(plane(hs, 0)), lbo_x, 128);
-        const uint64_t ax1 = desc_kmajor_interleave(smem_u32(plane(hs, 1)), lbo_x, 128);
+        // K-major A: interleave ([kg][pos][8], one position = 16 B) or SW32 ([pos][16] in 32-byte
+        // swizzled rows, 8-row atoms 256 B apart; one position = 32 B): the start shifts by whole rows
+        // (the swizzle follows the absolute address bits, as the TMA wrote it)
+        const uint64_t ax0 = a.sw32 ? desc_general(smem_u32(plane(hs, 0)), 16, 256, 6, 0)
+                                    : desc_kmajor_interleave(smem_u32(plane(hs, 0)), lbo_x, 128);
+        const uint64_t ax1 = a.sw32 ? desc_general(smem_u32(plane(hs, 1)), 16, 256, 6, 0)
+                                    : desc_kmajor_interleave(smem_u32(plane(hs, 1)), lbo_x, 128);
+        const int pstep = a.sw32 ? 2 : 1;   // 16-byte units per position
         if (elect_one() && !(a.dbg & 8)) {
           for (int dy = 0; dy < 3; ++dy) {
 #pragma unroll
@@ -281,7 +300,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
               for (int s = 0; s < kS; ++s) {
                 if (s < ntiles) {
-                  const uint64_t ao = (uint64_t)(row + s * kTile);   // 16-byte units: one position = 1
+                  const uint64_t ao = (uint64_t)((row + s * kTile) * pstep);   // 16-byte units
                   if constexpr (PAIR) {
                     mma_f16_pair(d0 + s * kCols, ax0 + ao, db, id_x0, accum);
                     mma_f16_pair(d0 + s * kCols, ax1 + ao, db1, id_x1, 1u);
@@ -466,36 +485,49 @@ EncodeTiledFn encode_fn() {
 // fp16 planes [2][N][H][W][Ci] viewed as 2N images of 8-channel groups; box {8 ch, W + 1
 // columns from x = -1, rows_h rows from y0 - 1, 2 groups, 1 image} = the slot layout
 // [2 kg][positions][8], out-of-bounds rows / columns zero-filled
-CUtensorMap make_map(const void* planes, const ConvShape& s, int Wp, int rows_h) {
+CUtensorMap make_map(const void* planes, const ConvShape& s, int Wp, int rows_h, bool sw32) {
   CUtensorMap m;
-  const cuuint64_t dims[5] = {8, (cuuint64_t)s.w, (cuuint64_t)s.h, (cuuint64_t)(s.ci / 8), (cuuint64_t)(2 * s.n)};
-  const cuuint64_t strides[4] = {(cuuint64_t)s.ci * 2, (cuuint64_t)s.w * s.ci * 2, 16,
-                                 (cuuint64_t)s.h * s.w * s.ci * 2};
-  const cuuint32_t box[5] = {8, (cuuint32_t)Wp, (cuuint32_t)rows_h, 2, 1};
-  const cuuint32_t estr[5] = {1, 1, 1, 1, 1};
-  CUresult r = encode_fn()(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 5, const_cast<void*>(planes), dims, strides, box, estr,
-                           CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
-                           CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  CUresult r;
+  if (sw32) {
+    // [2N][H][W][Ci] fp16, box {16 ch, W + 1 columns from x = -1, rows_h rows, 1 image}, 32B swizzle
+    const cuuint64_t dims[4] = {(cuuint64_t)s.ci, (cuuint64_t)s.w, (cuuint64_t)s.h, (cuuint64_t)(2 * s.n)};
+    const cuuint64_t strides[3] = {(cuuint64_t)s.ci * 2, (cuuint64_t)s.w * s.ci * 2, (cuuint64_t)s.h * s.w * s.ci * 2};
+    const cuuint32_t box[4] = {16, (cuuint32_t)Wp, (cuuint32_t)rows_h, 1};
+    const cuuint32_t estr[4] = {1, 1, 1, 1};
+    r = encode_fn()(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 4, const_cast<void*>(planes), dims, strides, box, estr,
+                    CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_32B, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+                    CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  } else {
+    const cuuint64_t dims[5] = {8, (cuuint64_t)s.w, (cuuint64_t)s.h, (cuuint64_t)(s.ci / 8), (cuuint64_t)(2 * s.n)};
+    const cuuint64_t strides[4] = {(cuuint64_t)s.ci * 2, (cuuint64_t)s.w * s.ci * 2, 16,
+                                   (cuuint64_t)s.h * s.w * s.ci * 2};
+    const cuuint32_t box[5] = {8, (cuuint32_t)Wp, (cuuint32_t)rows_h, 2, 1};
+    const cuuint32_t estr[5] = {1, 1, 1, 1, 1};
+    r = encode_fn()(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 5, const_cast<void*>(planes), dims, strides, box, estr,
+                    CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+                    CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  }
   if (r != CUDA_SUCCESS) fail(RP_ERR_CUDA, "cuTensorMapEncodeTiled failed (" + std::to_string((int)r) + ")");
   return m;
 }
 
 std::mutex g_map_mu;
-std::map<std::tuple<const void*, int, int, int, int, int>, CUtensorMap> g_maps;
+std::map<std::tuple<const void*, int, int, int, int, int, bool>, CUtensorMap> g_maps;
 
-CUtensorMap cached_map(const void* in, const ConvShape& s, int Wp, int rows_h) {
+CUtensorMap cached_map(const void* in, const ConvShape& s, int Wp, int rows_h, bool sw32) {
   std::lock_guard<std::mutex> lk(g_map_mu);
-  auto key = std::make_tuple(in, s.n, s.h, s.w, s.ci, rows_h);
+  auto key = std::make_tuple(in, s.n, s.h, s.w, s.ci, rows_h, sw32);
   auto it = g_maps.find(key);
   if (it == g_maps.end()) {
     if (g_maps.size() > 4096) g_maps.clear();   // callers hold copies, never references
-    it = g_maps.emplace(key, make_map(in, s, Wp, rows_h)).first;
+    it = g_maps.emplace(key, make_map(in, s, Wp, rows_h, sw32)).first;
   }
   return it->second;
 }
 
 struct Plan {
   bool ok = false;
+  bool sw32 = true;    // halo slab in 32-byte swizzled rows (RP_CONV_HALO_SW=0: the 16-byte interleave)
   bool pair = false;   // CTA-pair form (Co = 64)
   int Wp, rows_h, halo_pos, T, slots;
   uint32_t plane_bytes, halo_stride, w_bytes;
@@ -512,8 +544,14 @@ Plan plan_for(const ConvShape& s) {
   p.halo_pos = p.rows_h * p.Wp;
   p.T = (s.h * p.Wp + kTile - 1) / kTile;
   p.plane_bytes = (uint32_t)p.halo_pos * 32u;
-  const uint32_t pitch = ((p.plane_bytes + 127u) & ~127u) + 128u;
-  p.halo_stride = 128u + 2u * pitch;
+  static const bool sw_on = [] {
+    const char* e = std::getenv("RP_CONV_HALO_SW");
+    return !(e && e[0] == '0');
+  }();
+  p.sw32 = sw_on;
+  const uint32_t al = p.sw32 ? 256u : 128u;
+  const uint32_t pitch = ((p.plane_bytes + al - 1) & ~(al - 1)) + al;
+  p.halo_stride = al + 2u * pitch;
   static const bool pair_on = [] {
     const char* e = std::getenv("RP_CONV_PAIR");
     return e ? e[0] != '0' : RP_CONV_PAIR_DEFAULT != 0;
@@ -626,7 +664,8 @@ void conv3x3_fwd_pm(const ConvShape& s, const float* w_hwio, bool dgrad_weights,
     return e ? std::atoi(e) : 0;
   }();
   a.dbg = dbg;
-  const CUtensorMap m = cached_map(in_planes, s, p.Wp, p.rows_h);
+  a.sw32 = p.sw32 ? 1 : 0;
+  const CUtensorMap m = cached_map(in_planes, s, p.Wp, p.rows_h, p.sw32);
   // work items: units of one image, or (PAIR) of an image pair
   const int units = (p.pair ? (s.n + 1) / 2 : s.n) * ((p.T + kS - 1) / kS);
   switch (epi) {
