@@ -481,7 +481,9 @@ def run_reference(args, cfg, rank, world):
 def _cfg_json(cfg):
     beta = 0.1 if cfg["mode"] == "alm" else 1.0
     n = cfg["B"] * cfg["h"] * cfg["w"] * cfg["c"]
-    operands = {"fp32": "fp16x2 plane pairs (22-bit significands, power-of-two scales), fp32 accumulate",
+    operands = {"fp32": "fp16x2 plane pairs (22-bit significands, power-of-two scales), fp32 accumulate; "
+                        "fprop / dgrad 3 tensor products per MAC (positions-as-M conv_pm.cu, C <= 64; "
+                        "x0 W0 + x0 W1 + x1 W0), wgrad 4 ([g0; g1] x [x0 x1])",
                 "bf16": "bf16 operands, fp32 accumulate", "tf32": "tf32 operands, fp32 accumulate",
                 "simt": "fp32 CUDA cores"}[cfg["math"]]
     return {"in": [cfg["cin"], cfg["h"], cfg["w"]], "global_batch": cfg["B"], "channels": cfg["c"],
@@ -491,6 +493,14 @@ def _cfg_json(cfg):
             "kappa_lr": KAPPA_STEP * 2.0 * beta / n if cfg["mode"] == "alm" else None,
             "kappa_step": KAPPA_STEP if cfg["mode"] == "alm" else None, "penalty": "squared_l2",
             "data_rng": "reference splitmix64 (seed 1000 + replica): pixels U[-1,1), then labels next_u64() % 10"}
+
+
+def plane_conv_products(cfg):
+    """Tensor products per fp32 MAC of the config's plane convs: 3 on conv_pm.cu, 4 on conv_tc.cu."""
+    from paper_2009_01462_b200._lib import lib
+    kinds = {lib().rp_op_plane_conv_kernel(cfg["B"], cfg["h"], cfg["w"], ci, co)
+             for ci, co in ((cfg["c"], cfg["ch"]), (cfg["ch"], cfg["c"]))}
+    return 3 if kinds == {1} else 4
 
 
 def spawn_ranks(n, check_devices=True):
@@ -600,6 +610,8 @@ def main():
     # and bf16 MMAs run at the same rate): their own ceiling is the 16-bit peak / 4, reported
     # beside the prescribed bf16-peak fraction together with the tensor work actually issued
     split = {"fp32": 4.0, "tf32": 2.0, "bf16": 1.0, "simt": None}.get(cfg["math"])
+    if cfg["math"] == "fp32" and dom != "conv_wgrad" and plane_conv_products(cfg) == 3:
+        split = 3.0   # the positions-as-M plane conv drops the W1 x1 product
     ceiling = peaks["bf16_tflops_sustained"] / split if split else None
     roof = {"bound": "tensor", "kernel": dom, "achieved": achieved_tf,
             "peak": peaks["bf16_tflops_sustained"], "unit": "TFLOP/s",
@@ -607,8 +619,9 @@ def main():
             "traffic_unit": "bytes per launch (ncu --set full, profiles/traffic.json)",
             "math_ceiling": {"tflops": ceiling, "frac": achieved_tf / ceiling if ceiling else None,
                              "tensor_tflops_issued": achieved_tf * split if split else None,
+                             "products_per_mac": split,
                              "note": "bf16 sustained peak / 16-bit tensor products per fp32-equivalent MAC "
-                                     "(fp32 plane path: 4 fp16 products; bf16: 1)"},
+                                     "(fp32 plane path: fprop / dgrad 3 (conv_pm) or 4 (conv_tc), wgrad 4; bf16: 1)"},
             "peak_source": f"{peaks_kind} bf16 dense sustained (MEASURED_PEAKS.json)",
             "kernel_timing": ("per-launch CUDA events with this rank's stages on concurrent streams (overlapping "
                               "kernels: upper bounds)") if r.get("prof_concurrent") else
