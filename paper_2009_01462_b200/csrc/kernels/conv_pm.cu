@@ -51,7 +51,7 @@ constexpr int kMaxSmem = 227 * 1024;
 constexpr int kPieceBytes = 32 * 1024;   // filter load: bulk copies of <= 32 KB
 constexpr int kXchgBytes = 4096;         // per epilogue warp: 32 positions x 32 channels fp32
 #ifndef RP_CONV_PAIR_DEFAULT
-#define RP_CONV_PAIR_DEFAULT 0              // Co = 64: the CTA-pair form unless RP_CONV_PAIR=0 / 1
+#define RP_CONV_PAIR_DEFAULT 1              // Co = 64: CTA pairs (measured +1.6 % on C3 over single CTAs) unless RP_CONV_PAIR=0
 #endif
 
 struct PmArgs {
@@ -355,53 +355,78 @@ __global__ void __launch_bounds__(kThreads, 1)
       const int y = f / Wp, X = f - y * Wp;
       const bool valid = grp < ntiles && y < a.H && X >= 1 && n < a.N;
       const int64_t off = valid ? (((int64_t)n * a.H + y) * a.W + (X - 1)) * CO : 0;
-      // the tile's aux operand first: its latency overlaps the wait for the accumulator
-      float4 ax[kAux ? CO / 4 : 1];
+      // the tile's aux operand first, coalesced (instruction k: kPW consecutive positions of the
+      // warp as whole contiguous rows, 16-byte piece lane % kPR), its latency overlapping the
+      // wait for the accumulator; each pass moves its pieces to thread = position through the
+      // warp's exchange rows
+      constexpr int kPR = CO / 4;       // 16-byte pieces per position row
+      constexpr int kPW = 32 / kPR;     // positions per load instruction
+      float4 ax[kAux ? kPR : 1];
       if constexpr (kAux) {
 #pragma unroll
-        for (int i = 0; i < CO / 4; ++i)
-          ax[i] = valid ? __ldg(reinterpret_cast<const float4*>(a.aux + off) + i) : make_float4(0.f, 0.f, 0.f, 0.f);
+        for (int k = 0; k < kPR; ++k) {
+          const int src = k * kPW + lane / kPR, j = lane % kPR;
+          const int64_t so = __shfl_sync(0xffffffffu, off, src);
+          const bool sv = __shfl_sync(0xffffffffu, (int)valid, src) != 0;
+          ax[k] = sv ? __ldg(reinterpret_cast<const float4*>(a.aux + so) + j) : make_float4(0.f, 0.f, 0.f, 0.f);
+        }
       }
       mbar_wait(&acc_full[ab], aph);
       tc_fence_after();
-      // the tile's accumulators first (W0 + W1 columns, scaled): the TMEM buffer goes back to the
-      // MMA before the epilogue math and the stores
       const bool live = grp < ntiles && !(a.dbg & 1);
-      float acc[CO];
-      if (live) {
-        const uint32_t tcol = tmem_base + ((uint32_t)(q * 32) << 16) + (uint32_t)(ab * kS * kCols + grp * kCols);
+      const uint32_t tcol = tmem_base + ((uint32_t)(q * 32) << 16) + (uint32_t)(ab * kS * kCols + grp * kCols);
 #pragma unroll
-        for (int cc = 0; cc < CO / 16; ++cc) {
-          uint32_t hi[16], lo[16];
-          tmem_ld16(tcol + cc * 16, hi);
-          tmem_ld16(tcol + CO + cc * 16, lo);
-          tmem_wait_ld();
+      for (int hf = 0; hf < CO / kCh; ++hf) {
+        // this position's kCh channels [hf kCh, +kCh): W0 + W1 columns, scaled
+        float o[kCh];
+        if (live) {
 #pragma unroll
-          for (int i = 0; i < 16; ++i) acc[cc * 16 + i] = (__uint_as_float(hi[i]) + __uint_as_float(lo[i])) * acc_mul;
+          for (int cc = 0; cc < kCh / 16; ++cc) {
+            uint32_t hi[16], lo[16];
+            tmem_ld16(tcol + hf * kCh + cc * 16, hi);
+            tmem_ld16(tcol + CO + hf * kCh + cc * 16, lo);
+            tmem_wait_ld();
+#pragma unroll
+            for (int i = 0; i < 16; ++i)
+              o[cc * 16 + i] = (__uint_as_float(hi[i]) + __uint_as_float(lo[i])) * acc_mul;
+          }
         }
-      }
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) {
-        if constexpr (PAIR) mbar_arrive_cluster_relaxed(&acc_empty[ab], 0);   // the leader's accumulators
-        else mbar_arrive_relaxed(&acc_empty[ab]);
-      }
-      if (live) {
+        if (hf == CO / kCh - 1) {   // every accumulator is in registers: the buffer goes back to the MMA
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) {
+            if constexpr (PAIR) mbar_arrive_cluster_relaxed(&acc_empty[ab], 0);   // the leader's accumulators
+            else mbar_arrive_relaxed(&acc_empty[ab]);
+          }
+        }
+        if (!live) continue;
+        float4 xa[kAux ? kNJ : 1];
+        if constexpr (kAux) {
 #pragma unroll
-        for (int hf = 0; hf < CO / kCh; ++hf) {
-          // this position's kCh channels [hf kCh, +kCh): the fused epilogue
-          float o[kCh];
+          for (int k = 0; k < kPR; ++k) {
+            const int j = lane % kPR;
+            if (j / kNJ == hf) {
+              const int src = k * kPW + lane / kPR, jj = j - hf * kNJ;
+              xrow[src * kNJ + (jj ^ (src & (kNJ - 1)))] = ax[k];
+            }
+          }
+          __syncwarp();
+#pragma unroll
+          for (int j = 0; j < kNJ; ++j) xa[j] = xrow[lane * kNJ + (j ^ (lane & (kNJ - 1)))];
+          __syncwarp();
+        }
+        {
 #pragma unroll
           for (int i = 0; i < kCh; ++i) {
             const int co = hf * kCh + i;
-            const float v = acc[co];
-            const float xa = kAux ? reinterpret_cast<const float*>(&ax[0])[co] : 0.f;
+            const float v = o[i];
+            const float xa_i = kAux ? reinterpret_cast<const float*>(&xa[0])[i] : 0.f;
             float r;
             if constexpr (EPI == EPI_BIAS) r = v + __ldg(a.bias + co);
             else if constexpr (EPI == EPI_BIAS_TANH) r = tanhf(v + __ldg(a.bias + co));
-            else if constexpr (EPI == EPI_RESID) r = xa + a.h * (v + __ldg(a.bias + co));
-            else if constexpr (EPI == EPI_TANH_BWD) r = (a.h * v) * (1.f - xa * xa);
-            else if constexpr (EPI == EPI_ADD) r = xa + v;
+            else if constexpr (EPI == EPI_RESID) r = xa_i + a.h * (v + __ldg(a.bias + co));
+            else if constexpr (EPI == EPI_TANH_BWD) r = (a.h * v) * (1.f - xa_i * xa_i);
+            else if constexpr (EPI == EPI_ADD) r = xa_i + v;
             else r = a.h * v;
             o[i] = r;
           }

@@ -1,6 +1,7 @@
 #!/bin/bash
-# C3 bench with the plane convs on conv_tc (default), conv_pm, conv_pm CTA pairs; interleaved twice
+# C3 bench with the plane convs on conv_tc / conv_pm (/ CTA pairs), interleaved twice on one box
 mkdir -p gpurun_out
+rm -f gpurun_out/pmb_*.json
 for rep in 1 2; do
   for cfg in "0 0" "1 0" "1 1"; do
     set -- $cfg
