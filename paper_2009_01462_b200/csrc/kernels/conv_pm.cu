@@ -70,7 +70,8 @@ struct PmArgs {
   const float* in_scale;   // the input planes' scale (device scalar; null = kActPlaneScale)
   const float* out_scale;  // the output planes' scale (device scalar; null = kActPlaneScale)
   int sw32;                // halo slab: 32-byte swizzled position rows (1) or the [kg][pos][8] interleave (0)
-  int dbg;                 // diagnostics (RP_CONV_DBG): 1 no epilogue, 2 no halo TMA, 8 no MMA
+  int dbg;                 // diagnostics (RP_CONV_DBG): 1 no epilogue, 2 no halo TMA, 8 no MMA, 16 no fp32
+                           // output stores, 32 no plane stores
 };
 
 // Work split: units of kS tiles of one image; T = ceil(frame / 128) tiles per image leaves a
@@ -345,6 +346,13 @@ __global__ void __launch_bounds__(kThreads, 1)
     constexpr int kCh = CO < 32 ? CO : 32;      // channels per exchange pass
     constexpr int kNJ = kCh / 4;                // 16-byte pieces per position and pass
     float4* xrow = reinterpret_cast<float4*>(xchg + (warp - 4) * kXchgBytes);
+    // the bias in shared memory: a warp-uniform LDS.128 per 4 channels instead of an LDG per
+    // channel and position
+    float* sbias = reinterpret_cast<float*>(bars + 2 * kMaxSlots + 8);
+    if constexpr (kBias) {
+      if (threadIdx.x - 128 < (unsigned)CO) sbias[threadIdx.x - 128] = a.bias[threadIdx.x - 128];
+      asm volatile("bar.sync 1, 256;" ::: "memory");   // the 8 epilogue warps
+    }
     int ab = 0;
     uint32_t aph = 0;
     Units it(nitems, a.T, widx, G);
@@ -401,6 +409,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         if (!live) continue;
         float4 xa[kAux ? kNJ : 1];
+        float bq[4] = {0.f, 0.f, 0.f, 0.f};
         if constexpr (kAux) {
 #pragma unroll
           for (int k = 0; k < kPR; ++k) {
@@ -418,13 +427,20 @@ __global__ void __launch_bounds__(kThreads, 1)
         {
 #pragma unroll
           for (int i = 0; i < kCh; ++i) {
-            const int co = hf * kCh + i;
             const float v = o[i];
             const float xa_i = kAux ? reinterpret_cast<const float*>(&xa[0])[i] : 0.f;
+            float bco = 0.f;
+            if constexpr (kBias) {
+              if ((i & 3) == 0) {
+                const float4 b4 = reinterpret_cast<const float4*>(sbias)[(hf * kCh + i) / 4];
+                bq[0] = b4.x, bq[1] = b4.y, bq[2] = b4.z, bq[3] = b4.w;
+              }
+              bco = bq[i & 3];
+            }
             float r;
-            if constexpr (EPI == EPI_BIAS) r = v + __ldg(a.bias + co);
-            else if constexpr (EPI == EPI_BIAS_TANH) r = tanhf(v + __ldg(a.bias + co));
-            else if constexpr (EPI == EPI_RESID) r = xa_i + a.h * (v + __ldg(a.bias + co));
+            if constexpr (EPI == EPI_BIAS) r = v + bco;
+            else if constexpr (EPI == EPI_BIAS_TANH) r = tanhf(v + bco);
+            else if constexpr (EPI == EPI_RESID) r = xa_i + a.h * (v + bco);
             else if constexpr (EPI == EPI_TANH_BWD) r = (a.h * v) * (1.f - xa_i * xa_i);
             else if constexpr (EPI == EPI_ADD) r = xa_i + v;
             else r = a.h * v;
@@ -433,7 +449,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           // stores through the warp's exchange rows (thread = position -> kNJ 16-byte pieces of
           // consecutive positions per instruction: 32 / kNJ positions x kCh * 4 bytes contiguous);
           // 16-byte slots XOR-swizzled by position (conflict-free both ways)
-          if (a.out) {
+          if (a.out && !(a.dbg & 16)) {
 #pragma unroll
             for (int j = 0; j < kNJ; ++j)
               xrow[lane * kNJ + (j ^ (lane & (kNJ - 1)))] =
@@ -449,7 +465,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             }
             __syncwarp();
           }
-          if (planes) {
+          if (planes && !(a.dbg & 32)) {
             // [p0 | p1] of the kCh channels: kNJ / 2 16-byte pieces each
 #pragma unroll
             for (int j = 0; j < kNJ / 2; ++j) {

@@ -1,5 +1,5 @@
 #!/bin/bash
-# halo loads vs the rest: RP_CONV_DBG=2 (no halo TMA) for conv_pm and conv_tc at N = 1024
-for k in 1 0; do for d in 0 2 3; do
-  echo "kernel $k dbg $d"; RP_CONV_DBG=$d timeout 120 python tools/prof_conv.py --n 1024 --iters 10 --which fprop_planes,dgrad_planes --kernel $k
-done; done > gpurun_out/pm_epi2.txt 2>&1
+# conv_pm (CTA pairs, N = 1024) with parts of the epilogue's stores off: RP_CONV_DBG 16 no fp32 output, 32 no planes
+for d in 0 16 32 48; do
+  echo "dbg $d"; RP_CONV_DBG=$d timeout 120 python tools/prof_conv.py --n 1024 --iters 10 --which fprop_planes,dgrad_planes --kernel 1
+done > gpurun_out/pm_epi4.txt 2>&1
