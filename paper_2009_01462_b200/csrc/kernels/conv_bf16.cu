@@ -59,6 +59,7 @@ struct BfArgs {
   float* out;                   // may be null (bf16 tape outputs only)
   __nv_bfloat16* out16;         // optional bf16 copy of out (the bf16 wgrad's operand)
   __nv_bfloat16* out16d;        // optional bf16(1 - out^2)
+  int sw64;                     // BIN: the halo slab in 64-byte 64B-swizzled rows ([pos][32 ch]), else [kg][pos][8]
   int dbg;                      // diagnostics (RP_BF16_DBG): 1 no aux loads, 2 no stores
 };
 
@@ -131,7 +132,9 @@ __global__ void __launch_bounds__(kThreads, 1)
   int* pos_tab = reinterpret_cast<int*>(xchg + 2 * 8 * 128); // BIN epilogue: [2 groups][128]
 
   auto raw_s = [&](int s) { return raw_base + s * a.raw_stride; };
-  auto bf_s = [&](int s) { return bf_base + s * a.bf_stride + 128; };
+  // BIN + SW64: 512-byte aligned slabs (the swizzle atom); the front pad holds the shift -1 row
+  const bool sw = BIN && a.sw64;
+  auto bf_s = [&](int s) { return bf_base + s * a.bf_stride + (sw ? 512 : 128); };
   auto w_s = [&](int s) { return w_base + s * w_stage; };
 
   if (threadIdx.x == 0) {
@@ -156,7 +159,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   // zero the 128-byte pads around the bf16 halo (read only for discarded positions)
   for (int i = threadIdx.x; i < nbf * 2 * 32; i += blockDim.x) {
     const int s = i / 64, part = (i / 32) & 1, w = i % 32;
-    uint8_t* base = bf_base + s * a.bf_stride + (part == 0 ? 0 : 128 + a.bf_bytes);
+    uint8_t* base = part == 0 ? bf_s(s) - 128 : bf_s(s) + a.bf_bytes;
     reinterpret_cast<uint32_t*>(base)[w] = 0u;
   }
   tc_fence_before();
@@ -184,7 +187,10 @@ __global__ void __launch_bounds__(kThreads, 1)
           mbar_wait(&bf_empty[rs], rph ^ 1);   // the MMA is done with this bf16 slot
           if (elect_one()) {
             mbar_arrive_expect_tx(&raw_full[rs], a.bf_bytes);
-            tma_load_5d(&tmap, &raw_full[rs], bf_s(rs), 0, -1, y0 - 1, 4 * c, n);
+            if (sw)   // 64-byte box rows (32 channels): a quarter of the 16-byte rows' TMA row count
+              tma_load_4d(&tmap, &raw_full[rs], bf_s(rs), kChunk * c, -1, y0 - 1, n);
+            else
+              tma_load_5d(&tmap, &raw_full[rs], bf_s(rs), 0, -1, y0 - 1, 4 * c, n);
           }
         } else {
           mbar_wait(&raw_empty[rs], rph ^ 1);
@@ -231,12 +237,17 @@ __global__ void __launch_bounds__(kThreads, 1)
       for (int c = 0; c < a.nchunks; ++c) {
         mbar_wait(BIN ? &raw_full[bs] : &bf_full[bs], bph);
         tc_fence_after();
-        const uint64_t dx0 = desc_kmajor_interleave(smem_u32(bf_s(bs)), kg_x, 128);
+        // B: interleave ([kg][pos][8]: a position = 16 B, a K step = 2 kg) or SW64 ([pos][32] in
+        // 64-byte rows, 8-row atoms 512 B apart: a position = 64 B, a K step = 32 B into the row)
+        const uint64_t dx0 = sw ? desc_general(smem_u32(bf_s(bs)), 16, 512, 4, 0)
+                                : desc_kmajor_interleave(smem_u32(bf_s(bs)), kg_x, 128);
+        const int64_t pstep = sw ? 4 : 1;
+        const uint64_t xjs = sw ? 2 : xj;
         for (int dy = 0; dy < 3; ++dy) {
           mbar_wait(&w_full[ws], wph);
           tc_fence_after();
           const uint64_t dw0 = desc_kmajor_interleave(smem_u32(w_s(ws)), kg_w, 128);
-          const uint64_t bb = dx0 + (uint64_t)(int64_t)(c0 + dy * Wp - 1);   // one position = 16 B
+          const uint64_t bb = dx0 + (uint64_t)((int64_t)(c0 + dy * Wp - 1) * pstep);
           const bool first = (c == 0 && dy == 0);
           if (elect_one()) {
 #pragma unroll
@@ -245,7 +256,7 @@ __global__ void __launch_bounds__(kThreads, 1)
               for (int j = 0; j < 2; ++j) {
                 const uint64_t da = dw0 + dx * wtap + j * wj;
                 const uint32_t accum = (first && dx == 0 && j == 0) ? 0u : 1u;
-                mma_f16(d0, da, bb + (uint64_t)dx + j * xj, id_unit, accum);
+                mma_f16(d0, da, bb + (uint64_t)(dx * pstep) + j * xjs, id_unit, accum);
               }
             }
             mma_commit(&w_empty[ws]);
@@ -584,6 +595,14 @@ CUtensorMap make_halo_map16(const void* in, const ConvShape& s, int Wp, int rows
   return m;
 }
 
+bool halo_sw64() {
+  static const bool on = [] {
+    const char* e = std::getenv("RP_BF16_HALO_SW");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
+
 struct Plan {
   bool ok = false;
   int Wp, rows_h, halo_pos, T;
@@ -603,7 +622,7 @@ Plan plan_for(const ConvShape& s, bool bin = false) {
   p.raw_bytes = (uint32_t)p.halo_pos * kChunk * 4u;
   p.raw_stride = bin ? 0u : (p.raw_bytes + 1023) / 1024 * 1024;   // bf16 input: no fp32 staging
   p.bf_bytes = (uint32_t)p.halo_pos * kChunk * 2u;
-  p.bf_stride = (128 + p.bf_bytes + 128 + 1023) / 1024 * 1024;
+  p.bf_stride = ((bin && halo_sw64() ? 512 : 128) + p.bf_bytes + 128 + 1023) / 1024 * 1024;
   p.w_tap = 4u * 128u * 16u;
   const size_t fixed = 512 + 1024;
   if (bin) {
@@ -623,17 +642,34 @@ Plan plan_for(const ConvShape& s, bool bin = false) {
   return p;
 }
 
+// NHWC bf16 as 4-D (C, W, H, N); box (32 ch, W+2 from x = -1, rows, 1), 64B swizzle: the SW64
+// slab [pos][32 ch]
+CUtensorMap make_halo_map16_sw(const void* in, const ConvShape& s, int Wp, int rows_h) {
+  CUtensorMap m;
+  const cuuint64_t dims[4] = {(cuuint64_t)s.ci, (cuuint64_t)s.w, (cuuint64_t)s.h, (cuuint64_t)s.n};
+  const cuuint64_t strides[3] = {(cuuint64_t)s.ci * 2, (cuuint64_t)s.w * s.ci * 2, (cuuint64_t)s.h * s.w * s.ci * 2};
+  const cuuint32_t box[4] = {(cuuint32_t)kChunk, (cuuint32_t)Wp, (cuuint32_t)rows_h, 1};
+  const cuuint32_t estr[4] = {1, 1, 1, 1};
+  CUresult r = encode_fn()(&m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<void*>(in), dims, strides, box, estr,
+                           CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B,
+                           CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) fail(RP_ERR_CUDA, "cuTensorMapEncodeTiled (bf16 conv, SW64) failed (" + std::to_string((int)r) + ")");
+  return m;
+}
+
 std::mutex g_map_mu;
 std::map<std::tuple<const void*, int, int, int, int, int, int>, CUtensorMap> g_maps;
 
 CUtensorMap cached_map(const void* in, const ConvShape& s, int Wp, int rows_h, bool bin = false) {
   std::lock_guard<std::mutex> lk(g_map_mu);
-  auto key = std::make_tuple(in, s.n, s.h, s.w, s.ci, rows_h, bin ? 1 : 0);
+  const int kind = bin ? (halo_sw64() ? 2 : 1) : 0;
+  auto key = std::make_tuple(in, s.n, s.h, s.w, s.ci, rows_h, kind);
   auto it = g_maps.find(key);
   if (it == g_maps.end()) {
     if (g_maps.size() > 4096) g_maps.clear();   // callers hold copies, never references
-    it = g_maps.emplace(key, bin ? make_halo_map16(in, s, Wp, rows_h)
-                                 : make_halo_map(static_cast<const float*>(in), s, Wp, rows_h)).first;
+    it = g_maps.emplace(key, kind == 2   ? make_halo_map16_sw(in, s, Wp, rows_h)
+                             : kind == 1 ? make_halo_map16(in, s, Wp, rows_h)
+                                         : make_halo_map(static_cast<const float*>(in), s, Wp, rows_h)).first;
   }
   return it->second;
 }
@@ -693,6 +729,7 @@ void conv_bf16_any(const ConvShape& s, const void* in, bool bin, const float* w_
   a.raw_stride = p.raw_stride;
   a.bf_bytes = p.bf_bytes;
   a.bf_stride = p.bf_stride;
+  a.sw64 = halo_sw64() ? 1 : 0;
   a.w_tap = p.w_tap;
   a.nbf = p.nbf;
   a.nw = p.nw;
