@@ -127,3 +127,17 @@ def test_block_bf16_tape_matches_staged_bf16_block():
     eb = np.abs(blk[b_idx] - ref[b_idx]).max() / np.abs(ref[b_idx]).max()
     print(f"bf16 tape block: dpre {e_dpre:.2e} g {e_g:.2e} gW {ew:.2e} gb {eb:.2e}")
     assert e_dpre <= 1e-2 and e_g <= 1e-2 and ew <= 1e-2 and eb <= 1e-2, (e_dpre, e_g, ew, eb)
+
+
+def test_bf16_tape_halo_interleave_fallback():
+    """RP_BF16_HALO_SW=0: the bf16 tape conv with its halo in 16-byte interleaved rows instead of
+    64-byte swizzled ones passes the same block test."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-x", "-m", "gpu", "-p", "no:cacheprovider",
+                        "tests/test_gpu_bf16_tape.py::test_block_bf16_tape_matches_staged_bf16_block"],
+                       env={**os.environ, "RP_BF16_HALO_SW": "0"}, capture_output=True, text=True, timeout=600,
+                       cwd=root)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]

@@ -409,16 +409,18 @@ def test_wgrad_planes_clustered_multicast():
     assert r.returncode == 0 and r.stdout.strip().endswith("ok"), r.stderr[-2000:]
 
 
-@pytest.mark.parametrize("pair", ["0", "1"])
-def test_conv_planes_cta_pair_and_single(pair):
-    """RP_CONV_PAIR=1 / 0: conv_pm.cu's CTA-pair form (M = 256 MMAs across a cluster of two CTAs,
-    each holding half of the filter; the Co = 64 default) and its single-CTA form through the
-    plane-conv parity test and a block's forward and backward, at the same bars."""
+@pytest.mark.parametrize("env", [{"RP_CONV_PAIR": "0"}, {"RP_CONV_PAIR": "1"},
+                                 {"RP_CONV_PAIR": "0", "RP_CONV_HALO_SW": "0"}], ids=["single", "pair", "halo16"])
+def test_conv_planes_cta_pair_and_single(env):
+    """conv_pm.cu's forms: CTA pairs (M = 256 MMAs across a cluster of two CTAs, each holding half
+    of the filter; the Co = 64 default), single CTAs, and the halo in 16-byte interleaved rows
+    instead of 32-byte swizzled ones, through the plane-conv parity test and a block's forward and
+    backward, at the same bars."""
     import os
     import subprocess
     import sys
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
     r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-x", "-m", "gpu", "-p", "no:cacheprovider",
                         "tests/test_gpu_conv.py::test_conv_planes", "tests/test_gpu_block_planes.py", "-k", "pm or block"],
-                       env={**os.environ, "RP_CONV_PAIR": pair}, capture_output=True, text=True, timeout=600, cwd=root)
+                       env={**os.environ, **env}, capture_output=True, text=True, timeout=600, cwd=root)
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]
