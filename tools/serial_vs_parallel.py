@@ -19,9 +19,12 @@ ap.add_argument("--steps", type=int, default=60)
 ap.add_argument("--ks", default="1,2,4,8")
 ap.add_argument("--mode", default="alm")
 ap.add_argument("--both", action="store_true", help="K > 1 also with the stages serialised on one stream")
+ap.add_argument("--batch", type=int, default=None, help="override C3's B (per-launch fixed-cost study)")
 a = ap.parse_args()
 cfg = dict(bench.CONFIGS["C3"])
 cfg["lr"] = a.lr
+if a.batch:
+    cfg["B"] = a.batch
 B = cfg["B"]
 g = rp.Geometry(3, 32, 32, 64, 64, 64, 10)
 x, y = bench.synthetic_data(cfg, B, 1000, torch, rp, lib)
@@ -64,7 +67,7 @@ for K in [int(k) for k in a.ks.split(",")]:
         torch.cuda.synchronize()
         lib().rp_profile_enable(0)
         prof = bench.profile_classes()
-        row = {"K": K, "concurrent": conc, "img_s": B * a.steps / (ms.value / 1e3), "ms_step": ms.value / a.steps,
+        row = {"K": K, "B": B, "concurrent": conc, "img_s": B * a.steps / (ms.value / 1e3), "ms_step": ms.value / a.steps,
                "loss": loss, "lr": a.lr, "sm_mhz": clk["sm_mhz"], "clock_reasons": clk["reasons"],
                "classes_ms": {k: round(v["ms"] / 3, 3) for k, v in prof.items()},
                "conv_tflops": {k: round(v["flops"] / (v["ms"] / 1e3) / 1e12, 1) for k, v in prof.items()
