@@ -5,7 +5,8 @@ compiled reference): the bench's own networks, batch, stages, mode and step para
 
 * C2 at full size (B 256, 3x32x32, C 64, L 16, K 4, ALM): one iteration compared quantity by
   quantity, and the loss curve of 20 iterations tracking the oracle's;
-* C3 (L 64, K 8) at B 32; C4 (serial, the same 64-block network) at B 16;
+* C3 (L 64, K 8) at B 32, and its loss curve over 10 iterations at B 16; C4 (serial, the same
+  64-block network) at B 16;
 * C1 (1x28x28, C 16: the SIMT conv path) at full size;
 * C5 (C 256, bf16 operands with fp32 accumulation) at full width, B 4.
 
@@ -154,6 +155,26 @@ def test_config_three_iterations(name, B):
                                        split_params(og, want_g32)):
         ok, e = _close_derived(a, b, c)
         assert ok, (name, "grad", nm, e)
+
+
+def test_c3_ten_step_loss_curve():
+    """C3's 64-block, 8-stage network (conv_pm CTA pairs on every fprop / dgrad, the paired plane
+    wgrad) at B 16: the loss curve of 10 iterations tracks the fp64 oracle's at FP32_TOL, and
+    the parameters after them too."""
+    cfg, og, p32, x32, y, sp, osp, g = _setup("C3", B=16)
+    K, B = cfg["K"], cfg["B"]
+    gt = rp.DecoupledTrainer(g, K, rp.ALM, rp.SQUARED_L2, B, params=p32)
+    gt.reset_lambda_from_forward(x32)
+    ot, xt = _oracle(og, p32, x32, cfg, K)
+    yt = torch.from_numpy(y.astype(np.int64)).cuda()
+    lg, lo = [], []
+    for _ in range(10):
+        lg.append(gt.step(x32, y, 0, sp))
+        lo.append(ot.step(xt, yt, 0, osp))
+    errs = [abs(a - b) / abs(b) for a, b in zip(lg, lo)]
+    print("C3 loss curve (gpu, oracle, rel):", [(round(a, 6), round(b, 6), f"{e:.1e}") for a, b, e in zip(lg, lo, errs)])
+    assert max(errs) <= FP32_TOL, max(errs)
+    assert rel_err(gt.params(), ot.net.flat()) <= FP32_TOL
 
 
 def test_c4_serial_64_blocks():
