@@ -575,7 +575,7 @@ struct Plan {
   size_t smem;
 };
 
-Plan plan_for(const ConvShape& s) {
+Plan plan_for(const ConvShape& s, bool allow_pair = true) {
   Plan p;
   if (!(s.co == 16 || s.co == 32 || s.co == 64) || s.ci % kChunk != 0 || s.ci <= 0 || s.w + 1 > 256) return p;
   p.Wp = s.w + 1;
@@ -597,7 +597,7 @@ Plan plan_for(const ConvShape& s) {
     const char* e = std::getenv("RP_CONV_PAIR");
     return e ? e[0] != '0' : RP_CONV_PAIR_DEFAULT != 0;
   }();
-  p.pair = pair_on && s.co == 64;
+  p.pair = allow_pair && pair_on && s.co == 64;
   // per CTA: the whole filter, or (PAIR) its halves of B -- 3/4 of it
   p.w_bytes = (uint32_t)(s.ci / kChunk) * 9u * (uint32_t)(2 * s.co) * 32u * (p.pair ? 3u : 4u) / 4u;
   const size_t fixed = 8 * kXchgBytes + 1024;   // epilogue exchange, barriers, TMEM slot
@@ -608,40 +608,54 @@ Plan plan_for(const ConvShape& s) {
   return p;
 }
 
+// co-resident CTA pairs of the pair kernel at this shared-memory size (normally every TPC: 74;
+// 0 where clusters of two do not fit -- the launch then falls back to single CTAs)
+template <int EPI>
+int max_pairs(size_t smem) {
+  static std::mutex mu;
+  static std::map<size_t, int> cache;
+  std::lock_guard<std::mutex> lk(mu);
+  auto it = cache.find(smem);
+  if (it == cache.end()) {
+    ensure_max_dynamic_smem(reinterpret_cast<const void*>(conv3x3_pm_kernel<EPI, 64, true>), kMaxSmem);
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(kNumSMs);
+    cfg.blockDim = dim3(kThreads);
+    cfg.dynamicSmemBytes = smem;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = 2;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    int n = 0;
+    if (cudaOccupancyMaxActiveClusters(&n, conv3x3_pm_kernel<EPI, 64, true>, &cfg) != cudaSuccess) {
+      cudaGetLastError();
+      n = 0;
+    }
+    it = cache.emplace(smem, n).first;
+  }
+  return it->second;
+}
+
+int max_pairs_epi(int epi, size_t smem) {
+  switch (epi) {
+    case EPI_BIAS: return max_pairs<EPI_BIAS>(smem);
+    case EPI_BIAS_TANH: return max_pairs<EPI_BIAS_TANH>(smem);
+    case EPI_RESID: return max_pairs<EPI_RESID>(smem);
+    case EPI_TANH_BWD: return max_pairs<EPI_TANH_BWD>(smem);
+    case EPI_ADD: return max_pairs<EPI_ADD>(smem);
+    default: return max_pairs<EPI_SCALE>(smem);
+  }
+}
+
 template <int EPI, int CO, bool PAIR>
 void launch_co(const CUtensorMap& m, const PmArgs& a, size_t smem, int units, cudaStream_t st) {
-  const void* fn = reinterpret_cast<const void*>(conv3x3_pm_kernel<EPI, CO, PAIR>);
-  ensure_max_dynamic_smem(fn, kMaxSmem);
+  ensure_max_dynamic_smem(reinterpret_cast<const void*>(conv3x3_pm_kernel<EPI, CO, PAIR>), kMaxSmem);
   if constexpr (PAIR) {
-    // co-resident CTA pairs (normally every TPC: 74)
-    static std::mutex mu;
-    static std::map<size_t, int> max_pairs;
-    int pairs;
-    {
-      std::lock_guard<std::mutex> lk(mu);
-      auto it = max_pairs.find(smem);
-      if (it == max_pairs.end()) {
-        cudaLaunchConfig_t cfg{};
-        cfg.gridDim = dim3(kNumSMs);
-        cfg.blockDim = dim3(kThreads);
-        cfg.dynamicSmemBytes = smem;
-        cudaLaunchAttribute attr[1];
-        attr[0].id = cudaLaunchAttributeClusterDimension;
-        attr[0].val.clusterDim.x = 2;
-        attr[0].val.clusterDim.y = 1;
-        attr[0].val.clusterDim.z = 1;
-        cfg.attrs = attr;
-        cfg.numAttrs = 1;
-        int n = 0;
-        if (cudaOccupancyMaxActiveClusters(&n, conv3x3_pm_kernel<EPI, CO, PAIR>, &cfg) != cudaSuccess) {
-          cudaGetLastError();
-          n = 0;
-        }
-        it = max_pairs.emplace(smem, n).first;
-      }
-      pairs = it->second;
-    }
-    if (pairs < 1) fail(RP_ERR_CUDA, "conv3x3_fwd_pm: no CTA pair fits");
+    const int pairs = max_pairs<EPI>(smem);
+    if (pairs < 1) fail(RP_ERR_INTERNAL, "conv3x3_fwd_pm: no CTA pair fits");
     const int grid = 2 * std::min(units, std::min(pairs, kNumSMs / 2));
     launch_pdl_cluster(conv3x3_pm_kernel<EPI, CO, PAIR>, grid, kThreads, smem, st, 2, m, a);
   } else {
@@ -669,8 +683,9 @@ void conv3x3_fwd_pm(const ConvShape& s, const float* w_hwio, bool dgrad_weights,
                     float h, int epi, float* out, void* ws, cudaStream_t st, void* out_planes, const void* in_planes,
                     const void* wprep, const float* in_scale, const float* out_scale) {
   if (s.pixels() == 0) return;
-  const Plan p = plan_for(s);
+  Plan p = plan_for(s);
   if (!p.ok) fail(RP_ERR_INTERNAL, "conv3x3_fwd_pm: unsupported shape");
+  if (p.pair && max_pairs_epi(epi, p.smem) < 1) p = plan_for(s, false);   // no co-resident pairs: single CTAs
   if (!in_planes) fail(RP_ERR_INTERNAL, "conv3x3_fwd_pm: needs plane input");
   if (!wprep) {   // the filter of this conv alone (a stage prepares all of its filters at once)
     prep_filter_planes(w_hwio, dgrad_weights ? s.co : s.ci, dgrad_weights ? s.ci : s.co, dgrad_weights, ws, st);
