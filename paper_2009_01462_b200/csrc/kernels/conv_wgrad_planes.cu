@@ -28,6 +28,7 @@
 #include <cstdlib>
 #include <map>
 #include <mutex>
+#include <string>
 #include <tuple>
 
 #include "../common.cuh"
@@ -67,7 +68,8 @@ struct PwArgs {
   double scale[2];
   const float* gsc[2];           // the A (g-side) planes' power-of-two scale (device; null: kActPlaneScale)
   int mc;                        // 1: clusters of 3 CTAs (the tap groups of one work group) share the
-                                 //    operand loads by TMA multicast (wgrad_planes_kernel<true>)
+                                 //    operand loads by TMA multicast (wgrad_planes_kernel<true>);
+                                 // 2: the same CTA-triple mapping without clusters (each loads its own)
 };
 
 __device__ __forceinline__ int grp_start(int gid, int grid, const PwArgs& a) {
@@ -122,6 +124,21 @@ __global__ void __launch_bounds__(kThreads, 1)
     cib = gj % a.mi;
     cob = gj / a.mi;
     gi = (int)cluster_ctarank();
+    jg = cl - c_lo;
+    ng = c_hi - c_lo;
+  } else if (a.mc == 2) {
+    // triples: CTA 3 t + r is tap group r of triple t's position range (the MC mapping without
+    // clusters): the three CTAs reading the same g and x rows are adjacent in launch order
+    const int NW = a.njobs * a.mo * a.mi;
+    const int ncl = gridDim.x / 3, cl = blockIdx.x / 3;
+    int w = 0;
+    while (w + 1 < NW && cgrp_start(w + 1, ncl, a) <= cl) ++w;
+    const int c_lo = cgrp_start(w, ncl, a), c_hi = cgrp_start(w + 1, ncl, a);
+    job = w / (a.mo * a.mi);
+    const int gj = w - job * a.mo * a.mi;
+    cib = gj % a.mi;
+    cob = gj / a.mi;
+    gi = (int)(blockIdx.x % 3);
     jg = cl - c_lo;
     ng = c_hi - c_lo;
   } else {
@@ -492,7 +509,7 @@ __global__ void wgrad_planes_reduce_kernel(const float* __restrict__ part, const
       const int gi = tap / kTg, cob = co / cbk, cib = ci / cbk;
       // the CTAs of this (job, co block, ci block, tap group): first + stride * [0, count)
       int first, stride, count;
-      if (a.mc) {
+      if (a.mc) {   // clusters or triples: CTA 3 t + gi
         const int w = job * a.mo * a.mi + cob * a.mi + cib, ncl = grid / 3;
         const int c_lo = cgrp_start(w, ncl, a), c_hi = cgrp_start(w + 1, ncl, a);
         first = 3 * c_lo + gi, stride = 3, count = c_hi - c_lo;
@@ -517,10 +534,14 @@ __global__ void wgrad_planes_reduce_kernel(const float* __restrict__ part, const
     } else if (gb) {
       const int co = idx - total, cob = co / cbk;
       int first, stride, count;   // the ci-block-0 CTAs of this co block that sum the bias
-      if (a.mc) {   // all three CTAs of each cluster (a third of the rows each), in CTA order
+      if (a.mc == 1) {   // all three CTAs of each cluster (a third of the rows each), in CTA order
         const int w = job * a.mo * a.mi + cob * a.mi, ncl = grid / 3;
         const int c_lo = cgrp_start(w, ncl, a), c_hi = cgrp_start(w + 1, ncl, a);
         first = 3 * c_lo, stride = 1, count = 3 * (c_hi - c_lo);
+      } else if (a.mc == 2) {   // triples: tap group 0 of each triple sums its rows
+        const int w = job * a.mo * a.mi + cob * a.mi, ncl = grid / 3;
+        const int c_lo = cgrp_start(w, ncl, a), c_hi = cgrp_start(w + 1, ncl, a);
+        first = 3 * c_lo, stride = 3, count = c_hi - c_lo;
       } else {
         const int gid = gbase + cob * a.mi * 3;
         const int c_lo = grp_start(gid, grid, a), c_hi = grp_start(gid + 1, grid, a);
@@ -829,7 +850,15 @@ void launch_wgrad_planes(const ConvShape& s, const WgJob* jobs, int njobs, void*
   a.part_bias = reinterpret_cast<double*>(static_cast<char*>(ws) + part_bytes(p, single));
   a.njobs = njobs;
   if (3 * njobs * a.mo * a.mi > p.grid) fail(RP_ERR_INTERNAL, "conv3x3_wgrad_planes: too many work groups");
+  static const bool triples = [] {
+    const char* e = std::getenv("RP_WGRAD_MAP");
+    return e && std::string(e) == "triples";
+  }();
   a.mc = mc ? 1 : 0;
+  if (!mc && triples && njobs * a.mo * a.mi <= kNumSMs / 3) {
+    a.mc = 2;
+    p.grid = 3 * (kNumSMs / 3);
+  }
   const int xrows = mc ? p.rg + 2 : p.rg;
   CUtensorMap m[2][4];   // copies taken under the cache lock
   for (int j = 0; j < njobs; ++j) {

@@ -397,6 +397,18 @@ print("ok")
 """
 
 
+def test_wgrad_planes_cta_triples():
+    """RP_WGRAD_MAP=triples: the plane wgrad with CTA 3 t + r as tap group r of triple t's
+    position range (no clusters) against the fp64 oracle at the default kernel's bar."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    r = subprocess.run([sys.executable, "-c", _MC_SCRIPT, root], env={**os.environ, "RP_WGRAD_MAP": "triples"},
+                       capture_output=True, text=True, timeout=300, cwd=root)
+    assert r.returncode == 0 and r.stdout.strip().endswith("ok"), r.stderr[-2000:]
+
+
 def test_wgrad_planes_clustered_multicast():
     """RP_WGRAD_MC=1: the 3-CTA cluster form of the plane wgrad (TMA multicast of the shared g / x
     rows, distributed bias sums) against the fp64 oracle at the same bar as the default kernel."""
