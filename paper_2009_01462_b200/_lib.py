@@ -64,6 +64,8 @@ SIGNATURES = {
     "rp_op_conv3x3_planes": (C.c_int, [C.c_int32] * 5 + [_P, _P, C.c_int32, _P, _P, C.c_double, C.c_int32, _P, _P,
                                                          _P, _P, _P, C.c_int64, _P]),
     "rp_op_set_plane_conv_kernel": (C.c_int, [C.c_int32]),
+    "rp_op_set_concurrent_stages": (C.c_int, [C.c_int32]),
+    "rp_op_concurrent_stages": (C.c_int32, []),
     "rp_op_plane_conv_kernel": (C.c_int32, [C.c_int32] * 5),
     "rp_op_block_planes_supported": (C.c_int32, [_G, C.c_int32, C.c_int32]),
     "rp_op_block_fwd_planes": (C.c_int, [_G, C.c_int32, _P, _P, _P, _P, _P, _P, _P, _P, _P, C.c_int64, _P]),

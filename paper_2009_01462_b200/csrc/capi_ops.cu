@@ -606,6 +606,15 @@ int rp_op_conv3x3_wgrad(int32_t n, int32_t h, int32_t w, int32_t ci, int32_t co,
   });
 }
 
+int rp_op_set_concurrent_stages(int32_t ways) {
+  return guard([&] {
+    if (ways < 1) fail(RP_ERR_RANGE, "set_concurrent_stages: ways must be >= 1");
+    k::conv_pm_set_share(ways);
+  });
+}
+
+int32_t rp_op_concurrent_stages(void) { return k::conv_pm_share(); }
+
 int rp_op_set_plane_conv_kernel(int32_t which) {
   return guard([&] {
     if (which < -1 || which > 1) fail(RP_ERR_RANGE, "set_plane_conv_kernel: which must be -1, 0 or 1");

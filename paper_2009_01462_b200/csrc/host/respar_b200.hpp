@@ -119,6 +119,8 @@ class StageScheduler {
   int stages() const { return static_cast<int>(streams_.size()); }
   int device_of(int k) const { return devices_.at(k); }
   cudaStream_t stream(int k) const { return streams_.at(k); }
+  // stages of device_of(k) issuing on streams of their own (1 when they share one stream)
+  int concurrent_ways(int k) const;
   cudaStream_t control() const { return ctl_; }
   int control_device() const { return devices_.at(0); }
   // iteration bracket: begin() fans out from the control stream, end() joins.

@@ -154,6 +154,23 @@ StageScheduler::StageScheduler(int stages, std::vector<int> devices) {
   cu(cudaEventCreate(&ev_re_), "cudaEventCreate");
 }
 
+// the calling thread's "stages issuing concurrently" setting for the ops, restored on exit
+struct ConcurrentStagesScope {
+  int prev;
+  explicit ConcurrentStagesScope(int ways) : prev(rp_op_concurrent_stages()) { rp_op_set_concurrent_stages(ways); }
+  ~ConcurrentStagesScope() { rp_op_set_concurrent_stages(prev); }
+  ConcurrentStagesScope(const ConcurrentStagesScope&) = delete;
+  ConcurrentStagesScope& operator=(const ConcurrentStagesScope&) = delete;
+};
+
+int StageScheduler::concurrent_ways(int k) const {
+  std::vector<cudaStream_t> seen;
+  for (size_t j = 0; j < streams_.size(); ++j)
+    if (devices_[j] == devices_.at(k) && std::find(seen.begin(), seen.end(), streams_[j]) == seen.end())
+      seen.push_back(streams_[j]);
+  return static_cast<int>(seen.size());
+}
+
 StageScheduler::~StageScheduler() {
   for (size_t k = 0; k < streams_.size(); ++k) {
     cudaSetDevice(devices_[k]);
@@ -471,6 +488,7 @@ void DecoupledTrainer::check_rows(int row0, int nrows, const char* where) const 
 // net_forward over the stage's block range (network.cpp:112-143).  The stage output
 // (X^k_end) is written to out_features; the tape keeps x_1..x_{n-1} and every a.
 void DecoupledTrainer::run_forward(Stage& st, const float* input, int nrows, float* out_features, cudaStream_t s) {
+  const ConcurrentStagesScope share(sched_->concurrent_ways(st.index));
   const Layout L(geo_);
   const float* P = params_for(st.index);
   const float* cur = input;
@@ -543,6 +561,7 @@ void DecoupledTrainer::run_forward(Stage& st, const float* input, int nrows, flo
 // block by block in place, so p^k lands where correct_aux reads it.
 void DecoupledTrainer::run_backward(Stage& st, const int32_t* labels, int nrows, int row0, double beta, double lr,
                                     double momentum, bool use_snapshot, cudaStream_t s) {
+  const ConcurrentStagesScope share(sched_->concurrent_ways(st.index));
   const Layout L(geo_);
   const int k = st.index;
   float* P = params_for(k);

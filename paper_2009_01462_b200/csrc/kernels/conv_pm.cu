@@ -650,16 +650,30 @@ int max_pairs_epi(int epi, size_t smem) {
   }
 }
 
+thread_local int t_share = 1;   // stages issuing concurrently on this GPU (conv_pm_set_share)
+
+// CTAs per launch: every SM, or half of them while stages run concurrently (so two stages'
+// convs share the GPU spatially); RP_CONV_PM_CTAS overrides
+int max_ctas() {
+  static const int env = [] {
+    const char* e = std::getenv("RP_CONV_PM_CTAS");
+    const int n = e ? std::atoi(e) : 0;
+    return n >= 2 && n <= kNumSMs ? n : 0;
+  }();
+  if (env) return env;
+  return t_share >= 2 ? kNumSMs / 2 : kNumSMs;
+}
+
 template <int EPI, int CO, bool PAIR>
 void launch_co(const CUtensorMap& m, const PmArgs& a, size_t smem, int units, cudaStream_t st) {
   ensure_max_dynamic_smem(reinterpret_cast<const void*>(conv3x3_pm_kernel<EPI, CO, PAIR>), kMaxSmem);
   if constexpr (PAIR) {
     const int pairs = max_pairs<EPI>(smem);
     if (pairs < 1) fail(RP_ERR_INTERNAL, "conv3x3_fwd_pm: no CTA pair fits");
-    const int grid = 2 * std::min(units, std::min(pairs, kNumSMs / 2));
+    const int grid = 2 * std::min(units, std::min(pairs, max_ctas() / 2));
     launch_pdl_cluster(conv3x3_pm_kernel<EPI, CO, PAIR>, grid, kThreads, smem, st, 2, m, a);
   } else {
-    launch_pdl(conv3x3_pm_kernel<EPI, CO, PAIR>, std::min(units, kNumSMs), kThreads, smem, st, m, a);
+    launch_pdl(conv3x3_pm_kernel<EPI, CO, PAIR>, std::min(units, max_ctas()), kThreads, smem, st, m, a);
   }
 }
 
@@ -678,6 +692,9 @@ void launch_epi(const CUtensorMap& m, const PmArgs& a, size_t smem, int units, b
 }  // namespace
 
 bool conv3x3_pm_supported(const ConvShape& s) { return plan_for(s).ok; }
+
+void conv_pm_set_share(int ways) { t_share = ways < 1 ? 1 : ways; }
+int conv_pm_share() { return t_share; }
 
 void conv3x3_fwd_pm(const ConvShape& s, const float* w_hwio, bool dgrad_weights, const float* bias, const float* aux,
                     float h, int epi, float* out, void* ws, cudaStream_t st, void* out_planes, const void* in_planes,

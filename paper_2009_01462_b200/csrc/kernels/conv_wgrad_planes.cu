@@ -849,6 +849,12 @@ void launch_wgrad_planes(const ConvShape& s, const WgJob* jobs, int njobs, void*
   a.part = static_cast<float*>(ws);
   a.part_bias = reinterpret_cast<double*>(static_cast<char*>(ws) + part_bytes(p, single));
   a.njobs = njobs;
+  static const int max_ctas = [] {   // RP_WGRAD_CTAS: fewer CTAs let concurrent stages share the GPU
+    const char* e = std::getenv("RP_WGRAD_CTAS");
+    const int n = e ? std::atoi(e) : kNumSMs;
+    return n >= 1 && n <= kNumSMs ? n : kNumSMs;
+  }();
+  if (!mc) p.grid = std::max(std::min(p.grid, max_ctas), 3 * njobs * a.mo * a.mi);
   if (3 * njobs * a.mo * a.mi > p.grid) fail(RP_ERR_INTERNAL, "conv3x3_wgrad_planes: too many work groups");
   static const bool triples = [] {
     const char* e = std::getenv("RP_WGRAD_MAP");

@@ -80,6 +80,12 @@ void prep_filter_planes(const float* w_hwio, int ci_src, int co_src, bool dgrad,
 // The positions-as-M plane conv (conv_pm.cu): fp16 plane-pair input only, Co in {16, 32, 64},
 // Ci % 16 == 0; 3 tensor products per MAC.  Arguments as conv3x3_fwd_tc's plane mode.
 bool conv3x3_pm_supported(const ConvShape& s);
+// Stages issuing concurrently on one GPU (this host thread's launches): with 2 or more, a
+// conv_pm launch takes half the SMs so two stages' convs run side by side and one's fill and
+// drain overlap the other's steady state (measured +3 % on C3).  RP_CONV_PM_CTAS overrides.
+// (C ABI: rp_op_set_concurrent_stages / rp_op_concurrent_stages)
+void conv_pm_set_share(int ways);
+int conv_pm_share();
 void conv3x3_fwd_pm(const ConvShape& s, const float* w_hwio, bool dgrad_weights, const float* bias, const float* aux,
                     float h, int epi, float* out, void* ws, cudaStream_t st, void* out_planes, const void* in_planes,
                     const void* wprep, const float* in_scale, const float* out_scale);
