@@ -31,10 +31,15 @@ MUTANTS = {
     "kappa_term_sign": ("csrc/kernels/elementwise.cu",
                         "o.x = -dlam(kind, l.x - xe.x, 0, -1) * w + k4.x;",
                         "o.x = -dlam(kind, l.x - xe.x, 0, -1) * w - k4.x;"),
-    # the weight scale divided out of one conv epilogue off by 2^-16 (a 1.5e-5 relative bias)
-    "epilogue_scale_bias": ("csrc/kernels/conv_tc.cu",
-                            "const float acc_mul = a.wscale_inv / ",
-                            "const float acc_mul = (a.wscale_inv * (1.f + 0x1p-16f)) / "),
+    # the weight scale divided out of the plane conv epilogue off by 2^-16 (a 1.5e-5 relative bias)
+    "epilogue_scale_bias": ("csrc/kernels/conv_pm.cu",
+                            "const float acc_mul = kWeightPlaneScaleInv / ",
+                            "const float acc_mul = (kWeightPlaneScaleInv * (1.f + 0x1p-16f)) / "),
+    # CTA pairs: the peer holds W0 channels [0, 32) instead of [32, 64) for the x1 product (an
+    # error at the 2^-11 relative level of the low plane, in half the output channels)
+    "pair_x1_half": ("csrc/kernels/conv_pm.cu",
+                     "bulk_load(dct + 2048, sct + rank * 512, 512, w_full);",
+                     "bulk_load(dct + 2048, sct, 512, w_full);"),
 }
 
 DEFAULT_TESTS = ["tests/test_gpu_plane_parity.py"]
@@ -70,7 +75,8 @@ def run(tests):
         r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-m", "gpu", "-p", "no:cacheprovider", *tests],
                            env=env, capture_output=True, text=True, cwd=ROOT)
         tail = [ln for ln in r.stdout.splitlines() if "passed" in ln or "failed" in ln][-1:]
-        caught = r.returncode != 0
+        # caught = the tests ran and failed (not an import or collection error)
+        caught = r.returncode == 1 and bool(tail) and "failed" in tail[0]
         ok &= caught
         print(f"{name}: {'CAUGHT' if caught else 'NOT CAUGHT'} ({tail[0] if tail else r.stdout[-300:]})")
     return ok
