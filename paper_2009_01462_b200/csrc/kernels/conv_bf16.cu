@@ -373,10 +373,16 @@ __global__ void __launch_bounds__(kThreads, 1)
           load(0, ax);
           if (nb > 1) load(1, ax1);
         }
+        // batch b + 1's accumulators are loaded while batch b is finished (double-buffered
+        // registers: the TMEM load latency leaves the critical path)
+        uint32_t rn[8];
+        if (nb > 0) tmem_ld8(tcol, rn);
         for (int b = 0; b < nb; ++b) {
           uint32_t r[8];
-          tmem_ld8(tcol + (uint32_t)(8 * b), r);
           tmem_wait_ld();
+#pragma unroll
+          for (int e = 0; e < 8; ++e) r[e] = rn[e];
+          if (b + 1 < nb) tmem_ld8(tcol + (uint32_t)(8 * (b + 1)), rn);
           asm volatile("bar.sync %0, 128;" ::"r"(grp_bar) : "memory");   // buf free
 #pragma unroll
           for (int e = 0; e < 8; ++e) buf[e * 128 + q * 32 + lane] = __uint_as_float(r[e]);
