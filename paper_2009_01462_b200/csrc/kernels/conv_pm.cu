@@ -8,8 +8,9 @@
 //
 // conv_tc.cu puts the output channels on M ([W0; W1] stacked, M = 128 for 64 channels), so the
 // x1 plane pays for a W1 x1 product nobody needs: 4 tensor products per fp32 MAC.  Here
-//   A = the shifted x-plane halo view, M = 128 frame positions (K-major interleave, the same
-//       TMA-loaded slab conv_tc's B reads: a shift by one position is +16 B of start address),
+//   A = the shifted x-plane halo view, M = 128 frame positions (K-major: [pos][16 ch] in 32-byte
+//       rows with the 32B swizzle, one TMA box per plane; a shift by one position is +32 B of
+//       start address -- or the [kg][pos][8] interleave conv_tc's B reads, RP_CONV_HALO_SW=0),
 //   B = the filter, N = 2 Co rows [W0; W1] for the x0 plane, N = Co rows (W0) for the x1 plane:
 // x0 W0 + x0 W1 + x1 W0 is 3 products per MAC (the dropped |W1 x1| <= 2^-24 |W x|, fp32's own
 // rounding).  Measured MMA time per tap and 256 positions (tools/umma_bench_pm.py, Co = 64):
@@ -21,7 +22,10 @@
 //    serves all 9 taps); the whole prepared filter stays resident in shared memory (Co <= 64).
 //  * warp roles (384 threads, persistent, 1 CTA/SM): w0 halo TMA, w1 MMA issuer, w2 filter
 //    load, w4-11 two epilogue groups (one tile of each unit each: TMEM -> registers -> W0 + W1,
-//    fused bias / tanh / skip / step size -> NHWC stores of the output and its planes).
+//    fused bias / tanh / skip / step size -> NHWC stores of the output and its planes through a
+//    per-warp swizzled exchange row; the aux operand comes in the same way).
+//  * CTA pairs (Co = 64 default, see the kernel) and half-GPU grids while several stages run
+//    concurrently (conv_pm_set_share) -- DESIGN.md §4.1a.
 //  * Co in {16, 32, 64}: config C1's 16-channel network runs on the tensor cores too.
 #include <cuda.h>
 
@@ -57,7 +61,7 @@ constexpr int kXchgBytes = 4096;         // per epilogue warp: 32 positions x 32
 struct PmArgs {
   int N, H, W, Ci, Co, Wp, rows_h, T, nchunks, slots;
   int halo_pos;            // positions per halo plane (rows_h x Wp)
-  uint32_t plane_bytes;    // one fp16 plane of a chunk's halo: [2 kg][halo_pos][8]
+  uint32_t plane_bytes;    // one fp16 plane of a chunk's halo: halo_pos x 32 B ([pos][16] or [2 kg][pos][8])
   uint32_t halo_stride;    // bytes per halo slot (pads + two planes)
   uint32_t w_bytes;        // the whole prepared filter
   float h;
