@@ -232,7 +232,7 @@ def run_ours(args, cfg, rank, world):
     yp = y.cpu().pin_memory()
     xpn = xp.numpy()
     ypn = yp.numpy()
-    e2e_steps = max(1, min(args.steps, 10))
+    e2e_steps = max(1, args.steps)   # as many steps as the timed region: both sustained
     tr.step(xpn.reshape(B, -1), ypn, 0, sp)  # warm the staging buffers
     torch.cuda.synchronize()
     t0 = time.perf_counter()
@@ -325,7 +325,7 @@ def run_ours_distributed(args, cfg, rank, world):
     # step, the loss read back on the last-stage rank; wall clock, max over ranks
     x_host = x.cpu().pin_memory()
     y_host = y.cpu().pin_memory()
-    e2e_steps = max(1, min(args.steps, 10))
+    e2e_steps = max(1, args.steps)   # as many steps as the timed region: both sustained
     dist.barrier()
     t0 = time.perf_counter()
     for _ in range(e2e_steps):
@@ -659,7 +659,9 @@ def main():
         "roofline": roof,
         "e2e": {"value": replicas * B / r["e2e_s"], "unit": "images/s",
                 "h2d_bytes_per_step": replicas * (B * r["g"].raw_size * 4 + B * 4),
-                "d2h_bytes_per_step": 8 * replicas},
+                "d2h_bytes_per_step": 8 * replicas, "steps": args.steps,
+                "timing": "wall clock around the steps, each step: H2D of pixels and labels from pinned "
+                          "host memory, the step, D2H of the loss (synchronising)"},
     }
     line["config"]["settle"] = {"untimed_steps": r["settle"][0], "seconds": round(r["settle"][1], 3),
                                 "note": "after the W warm-up steps, before the K timed steps"}
