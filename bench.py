@@ -199,8 +199,9 @@ def run_ours(args, cfg, rank, world):
     for _ in range(args.warmup):
         tr.step_device(x.data_ptr(), y.data_ptr(), B, 0, sp, read_loss=False)
     torch.cuda.synchronize()
-    settle_steps, settle_s = settle(lambda: tr.step_device(x.data_ptr(), y.data_ptr(), B, 0, sp, read_loss=False),
-                                    args.settle_s, torch.cuda.synchronize)
+    settle_steps, settle_s, settle_mhz = settle(
+        lambda: tr.step_device(x.data_ptr(), y.data_ptr(), B, 0, sp, read_loss=False), args.settle_s,
+        torch.cuda.synchronize, dev)
     if world > 1:
         import torch.distributed as dist
         dist.barrier()
@@ -261,7 +262,7 @@ def run_ours(args, cfg, rank, world):
     lib().rp_profile_enable(0)
     prof = profile_classes()
     return dict(tr=tr, total_ms=total_ms, prof=prof, clocks=clk, launches=launches, loss=loss, e2e_s=e2e_s,
-                B=B, K=K, g=g, prof_steps=prof_steps, concurrent=concurrent, settle=(settle_steps, settle_s))
+                B=B, K=K, g=g, prof_steps=prof_steps, concurrent=concurrent, settle=(settle_steps, settle_s, settle_mhz))
 
 
 def run_ours_distributed(args, cfg, rank, world):
@@ -301,7 +302,7 @@ def run_ours_distributed(args, cfg, rank, world):
     for _ in range(args.warmup):
         tr.step(xp, yp, B, 0, sp)
     tr.sync()
-    settle_steps, settle_s = settle(lambda: tr.step(xp, yp, B, 0, sp), args.settle_s, tr.sync)
+    settle_steps, settle_s, settle_mhz = settle(lambda: tr.step(xp, yp, B, 0, sp), args.settle_s, tr.sync, dev)
     dist.barrier()
     torch.cuda.synchronize()
     clocks = ClockSampler(dev)
@@ -351,7 +352,7 @@ def run_ours_distributed(args, cfg, rank, world):
     prof = profile_classes()
     return dict(tr=tr, total_ms=total_ms, prof=prof, clocks=clk, launches=launches, loss=loss,
                 e2e_s=float(e2e_s.item()), B=B, K=K, g=g, replicas=plc.replicas, plc=plc, prof_steps=prof_steps,
-                concurrent=concurrent, prof_concurrent=concurrent, settle=(settle_steps, settle_s))
+                concurrent=concurrent, prof_concurrent=concurrent, settle=(settle_steps, settle_s, settle_mhz))
 
 
 def reference_labels(seed, n_before, count):
@@ -380,18 +381,43 @@ def synthetic_data(cfg, B, seed, torch, rp, lib):
     return x, y
 
 
-def settle(step_fn, seconds, sync):
-    """Untimed steps beyond the warm-up until the part has run the step for `seconds` (its
-    clocks reach the power-capped steady state the timed steps then measure)."""
+def settle(step_fn, seconds, sync, gpu=0, max_seconds=20.0):
+    """Untimed steps beyond the warm-up until the SM clock has settled: at least `seconds`, then
+    until three consecutive ~0.5 s windows agree on the median SM clock within 1.5 % (nvidia-smi,
+    100 ms samples), at most `max_seconds`.  Measured on B200s under the 1 kW cap: the first
+    ~4 s of a conv-heavy step run at ~1.5 GHz, after which the part holds 1.965 GHz at the same
+    power (tools/clock_timeline.py) -- a timed region inside that transient understates the
+    sustained rate.  Returns (steps, seconds, [window medians])."""
+    sampler = ClockSampler(gpu)
+    sampler.start()
     n = 0
     t0 = time.perf_counter()
-    while seconds > 0 and time.perf_counter() - t0 < seconds:
-        step_fn()
-        n += 1
-        if n % 8 == 0:
-            sync()
-    sync()
-    return n, time.perf_counter() - t0
+    meds = []
+    while True:
+        w0 = time.perf_counter()
+        mark = len(sampler.lines)
+        while time.perf_counter() - w0 < 0.5:
+            step_fn()
+            n += 1
+            if n % 4 == 0:
+                sync()
+        sync()
+        el = time.perf_counter() - t0
+        win = [ln for ln in sampler.lines[mark:]]
+        clk = []
+        for ln in win:
+            try:
+                clk.append(float(ln.split(",")[0]))
+            except (ValueError, IndexError):
+                pass
+        if clk:
+            meds.append(sorted(clk)[len(clk) // 2])
+        if seconds <= 0 or el >= max_seconds or (el >= seconds and sampler.proc is None):
+            break
+        if el >= seconds and len(meds) >= 3 and max(meds[-3:]) - min(meds[-3:]) <= 0.015 * max(meds[-3:]):
+            break
+    sampler.stop()
+    return n, time.perf_counter() - t0, meds
 
 
 def _splitmix(seed):
@@ -529,9 +555,9 @@ def main():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="C3", choices=sorted(CONFIGS))
-    ap.add_argument("--settle-s", type=float, default=1.5,
-                    help="untimed steps after the warm-up for this many seconds (clocks at their sustained, "
-                         "power-capped level before the timed steps); 0 disables")
+    ap.add_argument("--settle-s", type=float, default=6.0,
+                    help="untimed steps after the warm-up for at least this many seconds, then until the SM clock "
+                         "is steady (the power-capped part's first ~4 s run a lower clock); 0 disables")
     ap.add_argument("--chunks", type=int, default=4, help="N > 1: row chunks of the p / lambda exchange")
     ap.add_argument("--cpu-port-images", type=int, default=1,
                     help="images of the 3x3 CPU restatement sample (secondary CPU baseline; 0 disables)")
@@ -664,7 +690,11 @@ def main():
                           "host memory, the step, D2H of the loss (synchronising)"},
     }
     line["config"]["settle"] = {"untimed_steps": r["settle"][0], "seconds": round(r["settle"][1], 3),
-                                "note": "after the W warm-up steps, before the K timed steps"}
+                                "sm_mhz_windows": r["settle"][2][-12:],
+                                "note": "after the W warm-up steps, before the K timed steps: at least --settle-s, "
+                                        "then until three ~0.5 s windows agree on the median SM clock within 1.5 % "
+                                        "(the first seconds under the power cap run a lower clock at the same power; "
+                                        "tools/clock_timeline.py)"}
     if not args.no_cpu_baseline and args.cpu_port_images > 0:
         try:
             t = cpu_port_sample(cfg, args.cpu_port_images)
