@@ -39,11 +39,16 @@ sys.path.insert(0, ROOT)
 CONFIGS = {
     # id: (Cin, H, W, C, Ch, L, K, B, mode, math, classes)
     "C1": dict(cin=1, h=28, w=28, c=16, ch=16, L=8, K=2, B=128, mode="penalty", math="fp32"),
-    "C2": dict(cin=3, h=32, w=32, c=64, ch=64, L=16, K=4, B=256, mode="alm", math="fp32", concurrent=True),
-    "C3": dict(cin=3, h=32, w=32, c=64, ch=64, L=64, K=8, B=256, mode="alm", math="fp32", concurrent=True),
-    # serial full backprop through 64 blocks diverges at lr 0.1 within ~15 steps (and at 0.03,
-    # tools/loss_steps.py); 0.005 keeps the timed steps on finite data
-    "C4": dict(cin=3, h=32, w=32, c=64, ch=64, L=64, K=1, B=256, mode="serial", math="fp32", lr=0.005),
+    # lr 0.1 fits C2's repeated batch through loss spikes (0.002 .. 7 at the end of a run, by step
+    # count); 0.01 keeps it smooth
+    "C2": dict(cin=3, h=32, w=32, c=64, ch=64, L=16, K=4, B=256, mode="alm", math="fp32", concurrent=True, lr=0.01),
+    # the 64-block network on one repeated synthetic batch: at lr 0.1 the layer-parallel step
+    # diverges after ~170 steps (C3) and serial backprop within ~15 (C4); at 0.005 the serial one
+    # after ~500.  lr 0.002 keeps both finite for > 1,000 steps (tools/clock_timeline.py, loss per
+    # window) -- a benchmark on non-finite data is void: the tensor pipe draws less power on NaN
+    # and the capped clock jumps from ~1.5 to ~1.9 GHz (profiles/r02_clock_timeline.txt)
+    "C3": dict(cin=3, h=32, w=32, c=64, ch=64, L=64, K=8, B=256, mode="alm", math="fp32", concurrent=True, lr=0.002),
+    "C4": dict(cin=3, h=32, w=32, c=64, ch=64, L=64, K=1, B=256, mode="serial", math="fp32", lr=0.002),
     "C5": dict(cin=3, h=32, w=32, c=256, ch=256, L=64, K=8, B=1024, mode="alm", math="bf16"),
 }
 CLASSES = 10
@@ -237,10 +242,12 @@ def run_ours(args, cfg, rank, world):
     tr.step(xpn.reshape(B, -1), ypn, 0, sp)  # warm the staging buffers
     torch.cuda.synchronize()
     t0 = time.perf_counter()
+    loss_e2e = float("nan")
     for _ in range(e2e_steps):
-        tr.step(xpn.reshape(B, -1), ypn, 0, sp)
+        loss_e2e = tr.step(xpn.reshape(B, -1), ypn, 0, sp)
     torch.cuda.synchronize()
     e2e_s = (time.perf_counter() - t0) / e2e_steps
+    loss = loss if math.isfinite(loss_e2e) else loss_e2e   # a non-finite e2e loss voids the line too
 
     # a second, profiled pass of the same step: per-kernel-class CUDA-event times for the
     # roofline (event records on the launching streams; not part of the timed value), on a
@@ -384,10 +391,7 @@ def synthetic_data(cfg, B, seed, torch, rp, lib):
 def settle(step_fn, seconds, sync, gpu=0, max_seconds=20.0):
     """Untimed steps beyond the warm-up until the SM clock has settled: at least `seconds`, then
     until three consecutive ~0.5 s windows agree on the median SM clock within 1.5 % (nvidia-smi,
-    100 ms samples), at most `max_seconds`.  Measured on B200s under the 1 kW cap: the first
-    ~4 s of a conv-heavy step run at ~1.5 GHz, after which the part holds 1.965 GHz at the same
-    power (tools/clock_timeline.py) -- a timed region inside that transient understates the
-    sustained rate.  Returns (steps, seconds, [window medians])."""
+    100 ms samples), at most `max_seconds`.  Returns (steps, seconds, [window medians])."""
     sampler = ClockSampler(gpu)
     sampler.start()
     n = 0
@@ -555,9 +559,9 @@ def main():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="C3", choices=sorted(CONFIGS))
-    ap.add_argument("--settle-s", type=float, default=6.0,
+    ap.add_argument("--settle-s", type=float, default=1.5,
                     help="untimed steps after the warm-up for at least this many seconds, then until the SM clock "
-                         "is steady (the power-capped part's first ~4 s run a lower clock); 0 disables")
+                         "is steady; 0 disables")
     ap.add_argument("--chunks", type=int, default=4, help="N > 1: row chunks of the p / lambda exchange")
     ap.add_argument("--cpu-port-images", type=int, default=1,
                     help="images of the 3x3 CPU restatement sample (secondary CPU baseline; 0 disables)")
@@ -680,6 +684,8 @@ def main():
         # batch after ~10 iterations - the reference itself does the same (tools/ref_loss_curve.py);
         # a non-finite value is reported as null so the line stays valid JSON
         "loss": r["loss"] if math.isfinite(r["loss"]) else None,
+        # the timed and e2e steps must run on finite data (a diverged step draws different power)
+        "diverged": not math.isfinite(r["loss"]),
         "clocks": r["clocks"],
         "gpu_launches": r["launches"],
         "roofline": roof,
@@ -692,9 +698,7 @@ def main():
     line["config"]["settle"] = {"untimed_steps": r["settle"][0], "seconds": round(r["settle"][1], 3),
                                 "sm_mhz_windows": r["settle"][2][-12:],
                                 "note": "after the W warm-up steps, before the K timed steps: at least --settle-s, "
-                                        "then until three ~0.5 s windows agree on the median SM clock within 1.5 % "
-                                        "(the first seconds under the power cap run a lower clock at the same power; "
-                                        "tools/clock_timeline.py)"}
+                                        "then until three ~0.5 s windows agree on the median SM clock within 1.5 %"}
     if not args.no_cpu_baseline and args.cpu_port_images > 0:
         try:
             t = cpu_port_sample(cfg, args.cpu_port_images)
@@ -716,6 +720,9 @@ def main():
         except Exception as e:  # reported, never fatal
             line["cpu_baseline"] = {"value": None, "unit": "images/s", "cores": 0, "kind": "reference",
                                     "sample": f"failed: {e}"}
+    if line.get("diverged"):
+        print("bench: the loss went non-finite during the timed / e2e steps -- the line is void (lower the "
+              "config's lr)", file=sys.stderr)
     print(json.dumps(line))
 
 

@@ -22,7 +22,7 @@ def test_bench_default_line():
     for k in ("metric", "value", "unit", "n_gpus", "steps", "warmup", "ms_per_step", "higher_is_better", "scaling",
               "vs_baseline", "dtype", "data", "config", "clocks", "gpu_launches", "roofline", "e2e", "loss"):
         assert k in d, k
-    assert d["value"] > 0 and d["gpu_launches"] > 0 and d["loss"] is not None
+    assert d["value"] > 0 and d["gpu_launches"] > 0 and d["loss"] is not None and not d["diverged"]
     roof = d["roofline"]
     for k in ("bound", "achieved", "peak", "unit", "frac", "traffic"):
         assert k in roof, k

@@ -397,14 +397,15 @@ print("ok")
 """
 
 
-def test_wgrad_planes_cta_triples():
-    """RP_WGRAD_MAP=triples: the plane wgrad with CTA 3 t + r as tap group r of triple t's
-    position range (no clusters) against the fp64 oracle at the default kernel's bar."""
+def test_wgrad_planes_contiguous_ranges():
+    """RP_WGRAD_MAP=contiguous: the plane wgrad with contiguous CTA ranges per tap group (the
+    default is CTA triples: CTA 3 t + r is tap group r of triple t's position range) against the
+    fp64 oracle at the default kernel's bar."""
     import os
     import subprocess
     import sys
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-    r = subprocess.run([sys.executable, "-c", _MC_SCRIPT, root], env={**os.environ, "RP_WGRAD_MAP": "triples"},
+    r = subprocess.run([sys.executable, "-c", _MC_SCRIPT, root], env={**os.environ, "RP_WGRAD_MAP": "contiguous"},
                        capture_output=True, text=True, timeout=300, cwd=root)
     assert r.returncode == 0 and r.stdout.strip().endswith("ok"), r.stderr[-2000:]
 

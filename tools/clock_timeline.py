@@ -10,8 +10,11 @@ from paper_2009_01462_b200._lib import lib
 ap = argparse.ArgumentParser()
 ap.add_argument("--seconds", type=float, default=60.0)
 ap.add_argument("--config", default="C3")
+ap.add_argument("--lr", type=float, default=None, help="override the config's lr")
 a = ap.parse_args()
 cfg = dict(bench.CONFIGS[a.config])
+if a.lr is not None:
+    cfg["lr"] = a.lr
 B, K = cfg["B"], cfg["K"]
 g = rp.Geometry(cfg["cin"], cfg["h"], cfg["w"], cfg["c"], cfg["ch"], cfg["L"], 10)
 os.environ["RP_CONCURRENT_STAGES"] = "1"
@@ -46,7 +49,8 @@ while time.time() - t_start < a.seconds:
     pw = sorted(float(l.split(",")[2]) for l in win if len(l.split(",")) >= 7) or [0.0]
     tmp = [l.split(",")[3].strip() for l in win if len(l.split(",")) >= 7]
     cap = sum(1 for l in win if len(l.split(",")) >= 7 and "Active" in l.split(",")[4])
-    print(f"t={t0 - t_start:5.1f}s {B * n / (t1 - t0):8.0f} img/s  sm {sm[len(sm) // 2]:.0f} MHz  "
+    loss = tr.last_loss()
+    print(f"t={t0 - t_start:5.1f}s loss {loss:.4g} {B * n / (t1 - t0):8.0f} img/s  sm {sm[len(sm) // 2]:.0f} MHz  "
           f"power {pw[len(pw) // 2]:.0f} W  temp {tmp[-1] if tmp else '?'} C  power-cap samples {cap}/{len(win)}",
           flush=True)
 proc.terminate()

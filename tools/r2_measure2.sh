@@ -6,7 +6,7 @@ python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/r2f/smoke.log 2>
 python bench.py > gpurun_out/r2f/bench_c3.json 2> gpurun_out/r2f/bench_c3.err; echo "c3 rc=$?"
 python bench.py --config C2 --steps 300 > gpurun_out/r2f/bench_c2.json 2> gpurun_out/r2f/bench_c2.err; echo "c2 rc=$?"
 python bench.py --config C4 --steps 60 > gpurun_out/r2f/bench_c4.json 2> gpurun_out/r2f/bench_c4.err; echo "c4 rc=$?"
-python bench.py --config C5 --steps 8 --warmup 3 --settle-s 2 > gpurun_out/r2f/bench_c5.json 2> gpurun_out/r2f/bench_c5.err; echo "c5 rc=$?"
+python bench.py --config C5 --steps 8 --warmup 3 > gpurun_out/r2f/bench_c5.json 2> gpurun_out/r2f/bench_c5.err; echo "c5 rc=$?"
 python bench.py --config C1 --steps 1000 > gpurun_out/r2f/bench_c1.json 2> gpurun_out/r2f/bench_c1.err; echo "c1 rc=$?"
 python bench.py --impl reference --steps 5 --warmup 1 > gpurun_out/r2f/bench_ref.json 2>&1; echo "ref rc=$?"
 B="python bench.py --steps 2 --warmup 1 --settle-s 0 --no-cpu-baseline"

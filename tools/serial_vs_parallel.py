@@ -14,7 +14,7 @@ from paper_2009_01462_b200._lib import lib
 from paper_2009_01462_b200.trainer import SerialTrainer
 
 ap = argparse.ArgumentParser()
-ap.add_argument("--lr", type=float, default=0.005)
+ap.add_argument("--lr", type=float, default=0.002)
 ap.add_argument("--steps", type=int, default=60)
 ap.add_argument("--ks", default="1,2,4,8")
 ap.add_argument("--mode", default="alm")
