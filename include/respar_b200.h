@@ -183,10 +183,10 @@ int rp_op_conv3x3_planes(int32_t n, int32_t h, int32_t w, int32_t ci, int32_t co
  * (process-wide; the env var RP_CONV_PM sets the initial value).  A shape only one kernel takes
  * always runs on it.  rp_op_plane_conv_kernel reports the choice for a shape (1, 0; -1 none). */
 int rp_op_set_plane_conv_kernel(int32_t which);
-/* Stages issuing kernels concurrently on the calling thread's GPU (default 1).  With 2 or more,
- * each positions-as-M plane conv takes half the SMs, so two stages' convs run side by side and
- * one's fill and drain overlap the other's steady state.  The trainer sets it around a stage's
- * launches (thread-local; RP_CONV_PM_CTAS overrides the grid). */
+/* Stages issuing kernels concurrently on the calling thread's GPU (default 1).  With n >= 2,
+ * each positions-as-M plane conv takes 1 / max(2, n / 2) of the SMs, so several stages' convs
+ * run side by side and one's fill and drain overlap the others' steady state.  The trainer sets
+ * it around a stage's launches (thread-local; RP_CONV_PM_CTAS overrides the grid). */
 int rp_op_set_concurrent_stages(int32_t ways);
 int32_t rp_op_concurrent_stages(void);
 int32_t rp_op_plane_conv_kernel(int32_t n, int32_t h, int32_t w, int32_t ci, int32_t co);
