@@ -849,11 +849,14 @@ void launch_wgrad_planes(const ConvShape& s, const WgJob* jobs, int njobs, void*
   a.part = static_cast<float*>(ws);
   a.part_bias = reinterpret_cast<double*>(static_cast<char*>(ws) + part_bytes(p, single));
   a.njobs = njobs;
-  static const int max_ctas = [] {   // RP_WGRAD_CTAS: fewer CTAs let concurrent stages share the GPU
+  // CTAs: every SM, or SMs / (n / 4) while n >= 8 stages run concurrently (conv_pm_share; measured
+  // on finite data: C3's 8 stages +1.1 % at half, C2's 4 -1.0 %); RP_WGRAD_CTAS overrides
+  static const int env_ctas = [] {
     const char* e = std::getenv("RP_WGRAD_CTAS");
-    const int n = e ? std::atoi(e) : kNumSMs;
-    return n >= 1 && n <= kNumSMs ? n : kNumSMs;
+    const int n = e ? std::atoi(e) : 0;
+    return n >= 1 && n <= kNumSMs ? n : 0;
   }();
+  const int max_ctas = env_ctas ? env_ctas : kNumSMs / std::max(1, conv_pm_share() / 4);
   if (!mc) p.grid = std::max(std::min(p.grid, max_ctas), 3 * njobs * a.mo * a.mi);
   if (3 * njobs * a.mo * a.mi > p.grid) fail(RP_ERR_INTERNAL, "conv3x3_wgrad_planes: too many work groups");
   // CTA triples by default (DRAM reads 1.00x algorithmic, C3 +2.7 %); RP_WGRAD_MAP=contiguous
@@ -865,7 +868,7 @@ void launch_wgrad_planes(const ConvShape& s, const WgJob* jobs, int njobs, void*
   a.mc = mc ? 1 : 0;
   if (!mc && triples && njobs * a.mo * a.mi <= kNumSMs / 3) {
     a.mc = 2;
-    p.grid = 3 * (kNumSMs / 3);
+    p.grid = 3 * std::max(njobs * a.mo * a.mi, std::min(kNumSMs, max_ctas) / 3);
   }
   const int xrows = mc ? p.rg + 2 : p.rg;
   CUtensorMap m[2][4];   // copies taken under the cache lock
