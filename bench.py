@@ -181,7 +181,7 @@ def run_ours(args, cfg, rank, world):
     # (cfg "concurrent": the small C = 64 convs leave SMs idle in every kernel's tail, which a
     # neighbouring stage's kernels fill); the roofline pass below uses a serialised trainer so
     # every kernel's event-timed duration is its own.
-    concurrent = bool(cfg.get("concurrent")) and not args.serial_stages
+    concurrent = (bool(cfg.get("concurrent")) or args.concurrent_stages) and not args.serial_stages
 
     def make_trainer(conc):
         os.environ["RP_CONCURRENT_STAGES"] = "1" if conc else "0"
@@ -293,7 +293,8 @@ def run_ours_distributed(args, cfg, rank, world):
     mode = {"alm": rp.ALM, "penalty": rp.PENALTY}[cfg["mode"]]
     plc = placement(K, world, rank)
     # several stages per rank (N < K): concurrent stage streams as at N = 1
-    concurrent = bool(cfg.get("concurrent")) and not args.serial_stages and plc.hi - plc.lo > 1
+    concurrent = ((bool(cfg.get("concurrent")) or args.concurrent_stages) and not args.serial_stages
+                  and plc.hi - plc.lo > 1)
     os.environ["RP_CONCURRENT_STAGES"] = "1" if concurrent else "0"
     try:
         tr = NcclStagePipeline.for_rank(g, K, mode, rp.SQUARED_L2, B, plc, dev, seed_state=_splitmix(1),
@@ -570,6 +571,8 @@ def main():
     ap.add_argument("--cpu-images", type=int, default=4)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-graphs", action="store_true", help="launch every kernel eagerly (no CUDA graph replay)")
+    ap.add_argument("--concurrent-stages", action="store_true",
+                    help="stages sharing a GPU on streams of their own even where the config does not")
     ap.add_argument("--serial-stages", action="store_true",
                     help="stages sharing the GPU on one stream also in the timed run (default: concurrent for C2/C3)")
     ap.add_argument("--plan", action="store_true",
