@@ -600,9 +600,12 @@ def main():
     if args.plan:
         from paper_2009_01462_b200.distributed import placement
         plc = placement(cfg["K"], world, rank)
-        print(json.dumps({"rank": rank, "world": world, "local_rank": int(os.environ.get("LOCAL_RANK", "0")),
-                          "stages": [plc.lo, plc.hi], "prev_rank": plc.prev_rank, "next_rank": plc.next_rank,
-                          "replica": plc.replica, "replicas": plc.replicas}), flush=True)
+        # one write per line: the ranks share the parent's stdout (print writes text and newline apart)
+        sys.stdout.write(json.dumps({"rank": rank, "world": world, "local_rank": int(os.environ.get("LOCAL_RANK", "0")),
+                                     "stages": [plc.lo, plc.hi], "prev_rank": plc.prev_rank,
+                                     "next_rank": plc.next_rank, "replica": plc.replica,
+                                     "replicas": plc.replicas}) + "\n")
+        sys.stdout.flush()
         return
 
     distributed = world > 1 or args.dist_path
