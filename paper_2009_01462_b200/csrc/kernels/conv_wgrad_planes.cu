@@ -849,14 +849,14 @@ void launch_wgrad_planes(const ConvShape& s, const WgJob* jobs, int njobs, void*
   a.part = static_cast<float*>(ws);
   a.part_bias = reinterpret_cast<double*>(static_cast<char*>(ws) + part_bytes(p, single));
   a.njobs = njobs;
-  // CTAs: every SM, or SMs / (n / 4) while n >= 8 stages run concurrently (conv_pm_share; measured
-  // on finite data: C3's 8 stages +1.1 % at half, C2's 4 -1.0 %); RP_WGRAD_CTAS overrides
-  static const int env_ctas = [] {
+  // CTAs: every SM (RP_WGRAD_CTAS overrides).  Not shared out among concurrent stages like the
+  // convs: the per-CTA partials -- and so the last bits of the gradient -- depend on the grid, and
+  // results must not depend on how stages are scheduled (a half grid measured +1.1 % on C3)
+  static const int max_ctas = [] {
     const char* e = std::getenv("RP_WGRAD_CTAS");
     const int n = e ? std::atoi(e) : 0;
-    return n >= 1 && n <= kNumSMs ? n : 0;
+    return n >= 1 && n <= kNumSMs ? n : kNumSMs;
   }();
-  const int max_ctas = env_ctas ? env_ctas : kNumSMs / std::max(1, conv_pm_share() / 4);
   if (!mc) p.grid = std::max(std::min(p.grid, max_ctas), 3 * njobs * a.mo * a.mi);
   if (3 * njobs * a.mo * a.mi > p.grid) fail(RP_ERR_INTERNAL, "conv3x3_wgrad_planes: too many work groups");
   // CTA triples by default (DRAM reads 1.00x algorithmic, C3 +2.7 %); RP_WGRAD_MAP=contiguous

@@ -360,10 +360,11 @@ import torch
 sys.path.insert(0, sys.argv[1])
 import paper_2009_01462_b200 as rp
 from oracle import respar_oracle as O
-g = rp.Geometry(3, 16, 16, 64, 64, 4, 10)
-x, y = O.synthetic_batch(O.Geometry(3, 16, 16, 64, 64, 4, 10), 8, 3)
+L, K = int(sys.argv[2]), int(sys.argv[3])
+g = rp.Geometry(3, 16, 16, 64, 64, L, 10)
+x, y = O.synthetic_batch(O.Geometry(3, 16, 16, 64, 64, L, 10), 8, 3)
 xs = np.ascontiguousarray(x, np.float32)
-tr = rp.DecoupledTrainer(g, 2, rp.ALM, rp.SQUARED_L2, 8, seed_state=11)
+tr = rp.DecoupledTrainer(g, K, rp.ALM, rp.SQUARED_L2, 8, seed_state=11)
 tr.reset_lambda_from_forward(xs)
 tr.use_cuda_graphs(True)
 xd = torch.from_numpy(xs).cuda()
@@ -377,11 +378,12 @@ print(h.hexdigest())
 
 
 @pytest.mark.gpu
-def test_schedule_switches_are_bitwise_neutral():
+@pytest.mark.parametrize("blocks,stages", [(4, 2), (8, 8)])
+def test_schedule_switches_are_bitwise_neutral(blocks, stages):
     """Programmatic dependent launch (RP_PDL), the resident conv filter (RP_CONV_RESIDENT) and
-    concurrent stage streams (RP_CONCURRENT_STAGES) change when and from where kernels read,
-    never what they compute: three graphed steps give bitwise the same parameters and
-    multipliers under each."""
+    concurrent stage streams (RP_CONCURRENT_STAGES; with 8 stages the convs then also take a
+    quarter of the SMs each) change when and from where kernels read, never what they compute:
+    three graphed steps give bitwise the same parameters and multipliers under each."""
     import os
     import subprocess
     import sys
@@ -389,7 +391,7 @@ def test_schedule_switches_are_bitwise_neutral():
     out = {}
     for name, env in (("default", {}), ("no_pdl", {"RP_PDL": "0"}), ("streamed_filter", {"RP_CONV_RESIDENT": "0"}),
                       ("concurrent_stages", {"RP_CONCURRENT_STAGES": "1"})):
-        r = subprocess.run([sys.executable, "-c", _SWITCH_SCRIPT, root], env={**os.environ, **env},
+        r = subprocess.run([sys.executable, "-c", _SWITCH_SCRIPT, root, str(blocks), str(stages)], env={**os.environ, **env},
                            capture_output=True, text=True, timeout=300)
         assert r.returncode == 0, r.stderr[-2000:]
         out[name] = r.stdout.strip().splitlines()[-1]
