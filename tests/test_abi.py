@@ -92,3 +92,38 @@ def test_no_cpu_fallback():
     g = rp.Geometry(3, 8, 8, 16, 16, 4, 10)
     with pytest.raises(rp.DeviceError):
         rp.DecoupledTrainer(g, 2, rp.ALM, rp.SQUARED_L2, 4, seed_state=1)
+
+
+def test_plane_conv_kernel_choice_and_share_switches():
+    """Host-only plan logic: which plane conv takes a shape (1 positions-as-M, 0 channels-as-M,
+    -1 none), the process-wide override, and the thread-local concurrent-stage setting."""
+    L = _lib.lib()
+    assert L.rp_op_plane_conv_kernel(256, 32, 32, 64, 64) == 1      # C = 64: conv_pm by default
+    assert L.rp_op_plane_conv_kernel(128, 28, 28, 16, 16) == 1      # C1's 16 channels: conv_pm only
+    assert L.rp_op_plane_conv_kernel(4, 16, 16, 64, 128) == 0       # Co 128: conv_tc only
+    assert L.rp_op_plane_conv_kernel(4, 16, 16, 24, 24) == -1       # Ci % 16 != 0: neither
+    try:
+        assert L.rp_op_set_plane_conv_kernel(0) == 0
+        assert L.rp_op_plane_conv_kernel(256, 32, 32, 64, 64) == 0  # forced conv_tc where both apply
+        assert L.rp_op_plane_conv_kernel(128, 28, 28, 16, 16) == 1  # a shape only conv_pm takes stays
+    finally:
+        L.rp_op_set_plane_conv_kernel(-1)
+    assert L.rp_op_set_plane_conv_kernel(2) != 0                    # range-checked
+    assert L.rp_op_concurrent_stages() == 1
+    try:
+        assert L.rp_op_set_concurrent_stages(8) == 0 and L.rp_op_concurrent_stages() == 8
+    finally:
+        L.rp_op_set_concurrent_stages(1)
+    assert L.rp_op_set_concurrent_stages(0) != 0
+
+
+def test_plane_path_coverage():
+    """The fp32 plane path (tensor cores end to end) takes C = hidden = 64 and C1's 16 channels;
+    32 channels stay on the fp32-operand kernels (no 32-channel weight gradient on planes)."""
+    L = _lib.lib()
+    fp32 = rp.MATH["fp32"]
+    for c, h, w, n, want in ((64, 32, 32, 256, 1), (16, 28, 28, 128, 1), (32, 16, 16, 8, 0), (128, 16, 16, 4, 1)):
+        geo = _lib.rp_geometry(3, h, w, c, c, 4, 10, 0, 0.5)
+        assert L.rp_op_block_planes_supported(C.byref(geo), n, fp32) == want, c
+    geo = _lib.rp_geometry(3, 32, 32, 64, 64, 4, 10, 0, 0.5)
+    assert L.rp_op_block_planes_supported(C.byref(geo), 8, rp.MATH["bf16"]) == 0
