@@ -40,9 +40,18 @@ MUTANTS = {
     "pair_x1_half": ("csrc/kernels/conv_pm.cu",
                      "bulk_load(dct + 2048, sct + rank * 512, 512, w_full);",
                      "bulk_load(dct + 2048, sct, 512, w_full);"),
+    # the weight-gradient reduce sums the wrong CTAs' partials under the CTA-triple mapping
+    "triples_reduce_stride": ("csrc/kernels/conv_wgrad_planes.cu",
+                              "first = 3 * c_lo + gi, stride = 3, count = c_hi - c_lo;",
+                              "first = 3 * c_lo + gi, stride = 1, count = c_hi - c_lo;"),
+    # the 16-channel weight gradient accumulates its first K-step onto stale TMEM
+    "wsmall_stale_accumulator": ("csrc/kernels/conv_wgrad_small.cu",
+                                 "tap == kBiasTap ? id_b : id, (first && k == 0) ? 0u : 1u);",
+                                 "tap == kBiasTap ? id_b : id, 1u);"),
 }
 
-DEFAULT_TESTS = ["tests/test_gpu_plane_parity.py"]
+DEFAULT_TESTS = ["tests/test_gpu_plane_parity.py", "tests/test_gpu_block_planes.py",
+                 "tests/test_gpu_configs.py::test_config_three_iterations"]
 
 
 def build():
