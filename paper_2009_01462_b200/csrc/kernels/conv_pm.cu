@@ -23,7 +23,8 @@
 //  * warp roles (384 threads, persistent, 1 CTA/SM): w0 halo TMA, w1 MMA issuer, w2 filter
 //    load, w4-11 two epilogue groups (one tile of each unit each: TMEM -> registers -> W0 + W1,
 //    fused bias / tanh / skip / step size -> NHWC stores of the output and its planes through a
-//    per-warp swizzled exchange row; the aux operand comes in the same way).
+//    per-warp swizzled exchange row; the aux operand comes in the same way -- or, Co < 64, as
+//    32-byte sector loads / stores of the thread's own position, no exchange).
 //  * CTA pairs (Co = 64 default, see the kernel) and half-GPU grids while several stages run
 //    concurrently (conv_pm_set_share) -- DESIGN.md §4.1a.
 //  * Co in {16, 32, 64}: config C1's 16-channel network runs on the tensor cores too.
@@ -74,6 +75,8 @@ struct PmArgs {
   const float* in_scale;   // the input planes' scale (device scalar; null = kActPlaneScale)
   const float* out_scale;  // the output planes' scale (device scalar; null = kActPlaneScale)
   int sw32;                // halo slab: 32-byte swizzled position rows (1) or the [kg][pos][8] interleave (0)
+  int direct;              // epilogue: per-thread 32-byte global loads / stores of the thread's own
+                           // position (1) or coalesced through the exchange rows (0)
   int dbg;                 // diagnostics (RP_CONV_DBG): 1 no epilogue, 2 no halo TMA, 8 no MMA, 16 no fp32
                            // output stores, 32 no plane stores
 };
@@ -111,6 +114,18 @@ struct Units {
 };
 
 __device__ __forceinline__ uint4 cat2(uint2 a, uint2 b) { return make_uint4(a.x, a.y, b.x, b.y); }
+
+// 32-byte (one sector) global accesses: a thread moves whole sectors of its own position's row
+__device__ __forceinline__ void ldg256(const float* p, float4& a, float4& b) {
+  asm volatile("ld.global.nc.v8.f32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+               : "=f"(a.x), "=f"(a.y), "=f"(a.z), "=f"(a.w), "=f"(b.x), "=f"(b.y), "=f"(b.z), "=f"(b.w)
+               : "l"(p));
+}
+__device__ __forceinline__ void stg256(void* p, uint4 a, uint4 b) {
+  asm volatile("st.global.v8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"l"(p), "r"(a.x), "r"(a.y), "r"(a.z),
+               "r"(a.w), "r"(b.x), "r"(b.y), "r"(b.z), "r"(b.w)
+               : "memory");
+}
 
 // PAIR: a cluster of two CTAs (one TPC) runs M = 256 MMAs (cta_group::2): CTA r holds image
 // 2 i + r of image pair i at the same frame positions, so both halo slabs sit at the same
@@ -375,6 +390,13 @@ __global__ void __launch_bounds__(kThreads, 1)
       constexpr int kPW = 32 / kPR;     // positions per load instruction
       float4 ax[kAux ? kPR : 1];
       if constexpr (kAux) {
+        if (a.direct) {
+#pragma unroll
+          for (int k = 0; k < kPR; k += 2) {
+            if (valid) ldg256(a.aux + off + 4 * k, ax[k], ax[k + 1]);
+            else ax[k] = ax[k + 1] = make_float4(0.f, 0.f, 0.f, 0.f);
+          }
+        } else
 #pragma unroll
         for (int k = 0; k < kPR; ++k) {
           const int src = k * kPW + lane / kPR, j = lane % kPR;
@@ -415,6 +437,10 @@ __global__ void __launch_bounds__(kThreads, 1)
         float4 xa[kAux ? kNJ : 1];
         float bq[4] = {0.f, 0.f, 0.f, 0.f};
         if constexpr (kAux) {
+          if (a.direct) {
+#pragma unroll
+            for (int j = 0; j < kNJ; ++j) xa[j] = ax[hf * kNJ + j];
+          } else {
 #pragma unroll
           for (int k = 0; k < kPR; ++k) {
             const int j = lane % kPR;
@@ -427,6 +453,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
           for (int j = 0; j < kNJ; ++j) xa[j] = xrow[lane * kNJ + (j ^ (lane & (kNJ - 1)))];
           __syncwarp();
+          }
         }
         {
 #pragma unroll
@@ -453,6 +480,32 @@ __global__ void __launch_bounds__(kThreads, 1)
           // stores through the warp's exchange rows (thread = position -> kNJ 16-byte pieces of
           // consecutive positions per instruction: 32 / kNJ positions x kCh * 4 bytes contiguous);
           // 16-byte slots XOR-swizzled by position (conflict-free both ways)
+          if (a.direct) {
+            if (valid && a.out && !(a.dbg & 16)) {
+#pragma unroll
+              for (int j = 0; j < kCh / 8; ++j)
+                stg256(a.out + off + hf * kCh + 8 * j,
+                       make_uint4(__float_as_uint(o[8 * j]), __float_as_uint(o[8 * j + 1]),
+                                  __float_as_uint(o[8 * j + 2]), __float_as_uint(o[8 * j + 3])),
+                       make_uint4(__float_as_uint(o[8 * j + 4]), __float_as_uint(o[8 * j + 5]),
+                                  __float_as_uint(o[8 * j + 6]), __float_as_uint(o[8 * j + 7])));
+            }
+            if (valid && planes && !(a.dbg & 32)) {
+#pragma unroll
+              for (int j = 0; j < kCh / 16; ++j) {
+                uint2 h0[4], h1[4];
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                  const float v4[4] = {o[16 * j + 4 * u], o[16 * j + 4 * u + 1], o[16 * j + 4 * u + 2],
+                                       o[16 * j + 4 * u + 3]};
+                  pack_pair4(v4, out_mul, h0[u], h1[u]);
+                }
+                stg256(a.p0 + off + hf * kCh + 16 * j, cat2(h0[0], h0[1]), cat2(h0[2], h0[3]));
+                stg256(a.p1 + off + hf * kCh + 16 * j, cat2(h1[0], h1[1]), cat2(h1[2], h1[3]));
+              }
+            }
+            continue;
+          }
           if (a.out && !(a.dbg & 16)) {
 #pragma unroll
             for (int j = 0; j < kNJ; ++j)
@@ -743,6 +796,14 @@ void conv3x3_fwd_pm(const ConvShape& s, const float* w_hwio, bool dgrad_weights,
     return e ? std::atoi(e) : 0;
   }();
   a.dbg = dbg;
+  // epilogue global accesses: per-thread sectors for Co < 64 (C1: +6 %), the exchange rows for Co =
+  // 64 (per-thread sectors measured 1-1.5 % slower on C2 / C3 steps; profiles/r02_pm_direct.txt);
+  // RP_CONV_PM_DIRECT=0/1 forces either
+  static const int direct_env = [] {
+    const char* e = std::getenv("RP_CONV_PM_DIRECT");
+    return e ? (e[0] != '0' ? 1 : 0) : -1;
+  }();
+  a.direct = direct_env >= 0 ? direct_env : (s.co < 64 ? 1 : 0);
   a.sw32 = p.sw32 ? 1 : 0;
   const CUtensorMap m = cached_map(in_planes, s, p.Wp, p.rows_h, p.sw32);
   // work items: units of one image, or (PAIR) of an image pair
