@@ -23,8 +23,9 @@
 //  * warp roles (384 threads, persistent, 1 CTA/SM): w0 halo TMA, w1 MMA issuer, w2 filter
 //    load, w4-11 two epilogue groups (one tile of each unit each: TMEM -> registers -> W0 + W1,
 //    fused bias / tanh / skip / step size -> NHWC stores of the output and its planes through a
-//    per-warp swizzled exchange row; the aux operand comes in the same way -- or, Co < 64, as
-//    32-byte sector loads / stores of the thread's own position, no exchange).
+//    per-warp swizzled exchange row; the aux operand comes in the same way -- or as 32-byte
+//    sector loads / stores of the thread's own position, no exchange: all of them for Co < 64,
+//    the plane stores for Co = 64).
 //  * CTA pairs (Co = 64 default, see the kernel) and half-GPU grids while several stages run
 //    concurrently (conv_pm_set_share) -- DESIGN.md §4.1a.
 //  * Co in {16, 32, 64}: config C1's 16-channel network runs on the tensor cores too.
@@ -75,8 +76,9 @@ struct PmArgs {
   const float* in_scale;   // the input planes' scale (device scalar; null = kActPlaneScale)
   const float* out_scale;  // the output planes' scale (device scalar; null = kActPlaneScale)
   int sw32;                // halo slab: 32-byte swizzled position rows (1) or the [kg][pos][8] interleave (0)
-  int direct;              // epilogue: per-thread 32-byte global loads / stores of the thread's own
-                           // position (1) or coalesced through the exchange rows (0)
+  int direct;              // epilogue: per-thread 32-byte global accesses of the thread's own position
+                           // instead of coalesced ones through the exchange rows, bit mask: 1 aux
+                           // loads, 2 fp32 output stores, 4 plane stores
   int dbg;                 // diagnostics (RP_CONV_DBG): 1 no epilogue, 2 no halo TMA, 8 no MMA, 16 no fp32
                            // output stores, 32 no plane stores
 };
@@ -390,7 +392,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       constexpr int kPW = 32 / kPR;     // positions per load instruction
       float4 ax[kAux ? kPR : 1];
       if constexpr (kAux) {
-        if (a.direct) {
+        if (a.direct & 1) {
 #pragma unroll
           for (int k = 0; k < kPR; k += 2) {
             if (valid) ldg256(a.aux + off + 4 * k, ax[k], ax[k + 1]);
@@ -437,7 +439,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         float4 xa[kAux ? kNJ : 1];
         float bq[4] = {0.f, 0.f, 0.f, 0.f};
         if constexpr (kAux) {
-          if (a.direct) {
+          if (a.direct & 1) {
 #pragma unroll
             for (int j = 0; j < kNJ; ++j) xa[j] = ax[hf * kNJ + j];
           } else {
@@ -480,7 +482,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           // stores through the warp's exchange rows (thread = position -> kNJ 16-byte pieces of
           // consecutive positions per instruction: 32 / kNJ positions x kCh * 4 bytes contiguous);
           // 16-byte slots XOR-swizzled by position (conflict-free both ways)
-          if (a.direct) {
+          if (a.direct & 2) {
             if (valid && a.out && !(a.dbg & 16)) {
 #pragma unroll
               for (int j = 0; j < kCh / 8; ++j)
@@ -490,23 +492,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                        make_uint4(__float_as_uint(o[8 * j + 4]), __float_as_uint(o[8 * j + 5]),
                                   __float_as_uint(o[8 * j + 6]), __float_as_uint(o[8 * j + 7])));
             }
-            if (valid && planes && !(a.dbg & 32)) {
-#pragma unroll
-              for (int j = 0; j < kCh / 16; ++j) {
-                uint2 h0[4], h1[4];
-#pragma unroll
-                for (int u = 0; u < 4; ++u) {
-                  const float v4[4] = {o[16 * j + 4 * u], o[16 * j + 4 * u + 1], o[16 * j + 4 * u + 2],
-                                       o[16 * j + 4 * u + 3]};
-                  pack_pair4(v4, out_mul, h0[u], h1[u]);
-                }
-                stg256(a.p0 + off + hf * kCh + 16 * j, cat2(h0[0], h0[1]), cat2(h0[2], h0[3]));
-                stg256(a.p1 + off + hf * kCh + 16 * j, cat2(h1[0], h1[1]), cat2(h1[2], h1[3]));
-              }
-            }
-            continue;
-          }
-          if (a.out && !(a.dbg & 16)) {
+          } else if (a.out && !(a.dbg & 16)) {
 #pragma unroll
             for (int j = 0; j < kNJ; ++j)
               xrow[lane * kNJ + (j ^ (lane & (kNJ - 1)))] =
@@ -522,7 +508,22 @@ __global__ void __launch_bounds__(kThreads, 1)
             }
             __syncwarp();
           }
-          if (planes && !(a.dbg & 32)) {
+          if (a.direct & 4) {
+            if (valid && planes && !(a.dbg & 32)) {
+#pragma unroll
+              for (int j = 0; j < kCh / 16; ++j) {
+                uint2 h0[4], h1[4];
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                  const float v4[4] = {o[16 * j + 4 * u], o[16 * j + 4 * u + 1], o[16 * j + 4 * u + 2],
+                                       o[16 * j + 4 * u + 3]};
+                  pack_pair4(v4, out_mul, h0[u], h1[u]);
+                }
+                stg256(a.p0 + off + hf * kCh + 16 * j, cat2(h0[0], h0[1]), cat2(h0[2], h0[3]));
+                stg256(a.p1 + off + hf * kCh + 16 * j, cat2(h1[0], h1[1]), cat2(h1[2], h1[3]));
+              }
+            }
+          } else if (planes && !(a.dbg & 32)) {
             // [p0 | p1] of the kCh channels: kNJ / 2 16-byte pieces each
 #pragma unroll
             for (int j = 0; j < kNJ / 2; ++j) {
@@ -796,14 +797,14 @@ void conv3x3_fwd_pm(const ConvShape& s, const float* w_hwio, bool dgrad_weights,
     return e ? std::atoi(e) : 0;
   }();
   a.dbg = dbg;
-  // epilogue global accesses: per-thread sectors for Co < 64 (C1: +6 %), the exchange rows for Co =
-  // 64 (per-thread sectors measured 1-1.5 % slower on C2 / C3 steps; profiles/r02_pm_direct.txt);
-  // RP_CONV_PM_DIRECT=0/1 forces either
+  // epilogue global accesses: per-thread sectors for Co < 64 (C1: +6 %); for Co = 64 the plane
+  // stores alone (C2 / C3 +0.8-1 %; all three per thread: -1-1.5 %; profiles/r02_pm_direct.txt);
+  // RP_CONV_PM_DIRECT=<mask 0..7> forces a choice (1 aux loads, 2 fp32 stores, 4 plane stores)
   static const int direct_env = [] {
     const char* e = std::getenv("RP_CONV_PM_DIRECT");
-    return e ? (e[0] != '0' ? 1 : 0) : -1;
+    return e ? (std::atoi(e) & 7) : -1;
   }();
-  a.direct = direct_env >= 0 ? direct_env : (s.co < 64 ? 1 : 0);
+  a.direct = direct_env >= 0 ? direct_env : (s.co < 64 ? 7 : 4);
   a.sw32 = p.sw32 ? 1 : 0;
   const CUtensorMap m = cached_map(in_planes, s, p.Wp, p.rows_h, p.sw32);
   // work items: units of one image, or (PAIR) of an image pair

@@ -424,13 +424,13 @@ def test_wgrad_planes_clustered_multicast():
 
 @pytest.mark.parametrize("env", [{"RP_CONV_PAIR": "0"}, {"RP_CONV_PAIR": "1"},
                                  {"RP_CONV_PAIR": "0", "RP_CONV_HALO_SW": "0"},
-                                 {"RP_CONV_PM_DIRECT": "1"}, {"RP_CONV_PM_DIRECT": "0"}],
+                                 {"RP_CONV_PM_DIRECT": "7"}, {"RP_CONV_PM_DIRECT": "0"}],
                          ids=["single", "pair", "halo16", "direct", "exchange"])
 def test_conv_planes_cta_pair_and_single(env):
     """conv_pm.cu's forms: CTA pairs (M = 256 MMAs across a cluster of two CTAs, each holding half
     of the filter; the Co = 64 default), single CTAs, the halo in 16-byte interleaved rows instead
-    of 32-byte swizzled ones, and the epilogue's global accesses as per-thread sectors (the Co < 64
-    default) or through the exchange rows (the Co = 64 default), for every Co, through the
+    of 32-byte swizzled ones, and the epilogue's global accesses all as per-thread sectors (the Co < 64
+    default) or all through the exchange rows (the Co = 64 default mixes them), for every Co, through the
     plane-conv parity test and a block's forward and backward, at the same bars."""
     import os
     import subprocess
