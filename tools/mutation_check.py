@@ -48,6 +48,11 @@ MUTANTS = {
     "wsmall_stale_accumulator": ("csrc/kernels/conv_wgrad_small.cu",
                                  "tap == kBiasTap ? id_b : id, (first && k == 0) ? 0u : 1u);",
                                  "tap == kBiasTap ? id_b : id, 1u);"),
+    # the per-thread plane stores (the Co = 64 default) swap the two 16-byte halves of every
+    # 32-byte low-plane sector (channels 8 apart trade their low planes)
+    "direct_plane_halves": ("csrc/kernels/conv_pm.cu",
+                            "stg256(a.p1 + off + hf * kCh + 16 * j, cat2(h1[0], h1[1]), cat2(h1[2], h1[3]));",
+                            "stg256(a.p1 + off + hf * kCh + 16 * j, cat2(h1[2], h1[3]), cat2(h1[0], h1[1]));"),
 }
 
 DEFAULT_TESTS = ["tests/test_gpu_plane_parity.py", "tests/test_gpu_block_planes.py",
