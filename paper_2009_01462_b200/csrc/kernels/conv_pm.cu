@@ -479,9 +479,10 @@ __global__ void __launch_bounds__(kThreads, 1)
             else r = a.h * v;
             o[i] = r;
           }
-          // stores through the warp's exchange rows (thread = position -> kNJ 16-byte pieces of
-          // consecutive positions per instruction: 32 / kNJ positions x kCh * 4 bytes contiguous);
-          // 16-byte slots XOR-swizzled by position (conflict-free both ways)
+          // stores: per thread (its position's kCh channels as 32-byte sectors), or through the
+          // warp's exchange rows (thread = position -> kNJ 16-byte pieces of consecutive positions
+          // per instruction: 32 / kNJ positions x kCh * 4 bytes contiguous; 16-byte slots
+          // XOR-swizzled by position, conflict-free both ways)
           if (a.direct & 2) {
             if (valid && a.out && !(a.dbg & 16)) {
 #pragma unroll
