@@ -806,6 +806,11 @@ void conv3x3_fwd_pm(const ConvShape& s, const float* w_hwio, bool dgrad_weights,
     return e ? (std::atoi(e) & 7) : -1;
   }();
   a.direct = direct_env >= 0 ? direct_env : (s.co < 64 ? 7 : 4);
+  // 32-byte accesses need 32-byte aligned rows (C-ABI callers may pass any 16-byte aligned view)
+  auto a32 = [](const void* q) { return (reinterpret_cast<uintptr_t>(q) & 31u) == 0; };
+  if (!a32(aux)) a.direct &= ~1;
+  if (!a32(out)) a.direct &= ~2;
+  if (!a32(a.p0) || !a32(a.p1)) a.direct &= ~4;
   a.sw32 = p.sw32 ? 1 : 0;
   const CUtensorMap m = cached_map(in_planes, s, p.Wp, p.rows_h, p.sw32);
   // work items: units of one image, or (PAIR) of an image pair

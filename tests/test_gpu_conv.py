@@ -144,6 +144,47 @@ def test_conv_planes(shape, dgrad, plane_kernel):
         assert np.all(np.abs(rec - got) <= 2.0 ** -22 * np.abs(got) + 2.0 ** -25 / s_out), EPIS[epi]
 
 
+@pytest.mark.parametrize("shape", [(2, 9, 11, 16, 16), (2, 8, 8, 64, 64)], ids=["co16", "co64"])
+def test_conv_planes_16byte_views(shape):
+    """conv_pm's epilogue moves whole 32-byte sectors per thread where it can (every access at
+    Co < 64, the plane stores at Co = 64); C-ABI callers may pass views that are only 16-byte
+    aligned, which must take the exchange-row path for that operand and give the same bits."""
+    n, hh, ww, ci, co = shape
+    if lib().rp_op_plane_conv_kernel(n, hh, ww, ci, co) != 1:
+        pytest.skip("conv_pm does not take this shape")
+    dev = torch.device("cuda")
+    rng = np.random.default_rng(7)
+    x = rng.uniform(-1, 1, (n, hh, ww, ci)).astype(np.float32)
+    w = (rng.uniform(-1, 1, (3, 3, ci, co)) / np.sqrt(9 * ci)).astype(np.float32)
+    bias = rng.uniform(-0.2, 0.2, co).astype(np.float32)
+    aux = rng.uniform(-0.9, 0.9, (n, hh, ww, co)).astype(np.float32)
+    tx, tw, tb = (torch.from_numpy(v).to(dev) for v in (x, w, bias))
+    xp = torch.empty(2 * tx.numel(), dtype=torch.float16, device=dev)
+    rp.check(lib().rp_op_split_planes(C.c_void_p(tx.data_ptr()), tx.numel(), C.c_void_p(xp.data_ptr()),
+                                      C.c_void_p(xp.data_ptr() + 2 * tx.numel()), None, None))
+    ne = n * hh * ww * co
+    wsb = lib().rp_op_conv3x3_workspace_bytes(ci, co)
+    ws = torch.empty(wsb, dtype=torch.uint8, device=dev)
+    res = {}
+    for shift in (0, 1):   # 0: 32-byte aligned buffers; 1: every output / aux view 16 bytes off
+        taux = torch.empty(ne + 4, device=dev)[4 * shift:4 * shift + ne]
+        taux.copy_(torch.from_numpy(aux.ravel()).to(dev))
+        out = torch.empty(ne + 4, device=dev)[4 * shift:4 * shift + ne]
+        op = torch.empty(2 * ne + 8, dtype=torch.float16, device=dev)[8 * shift:8 * shift + 2 * ne]
+        assert (out.data_ptr() % 32 == 16) == bool(shift) and (op.data_ptr() % 32 == 16) == bool(shift)
+        rp.check(lib().rp_op_conv3x3_planes(
+            n, hh, ww, ci, co, C.c_void_p(xp.data_ptr()), C.c_void_p(tw.data_ptr()), 0, C.c_void_p(tb.data_ptr()),
+            C.c_void_p(taux.data_ptr()), 0.7, 2, C.c_void_p(out.data_ptr()), C.c_void_p(op.data_ptr()), None, None,
+            C.c_void_p(ws.data_ptr()), wsb, None))
+        torch.cuda.synchronize()
+        res[shift] = (out.cpu().numpy().copy(), op.cpu().numpy().copy())
+    assert np.array_equal(res[0][0], res[1][0]) and np.array_equal(res[0][1], res[1][1])
+    acc = O.conv3x3(x.astype(np.float64), w.astype(np.float64))
+    want = want_epi(2, acc, bias.astype(np.float64), aux.astype(np.float64), np.float32(0.7))
+    got = res[1][0].reshape(want.shape).astype(np.float64)
+    assert np.abs(got - want).max() / np.abs(want).max() <= 3e-6
+
+
 BF16_SHAPES = [(2, 16, 16, 128, 128), (1, 16, 16, 256, 256), (2, 9, 11, 64, 128), (1, 32, 32, 128, 256),
                (2, 8, 8, 64, 64)]   # the last falls back to 3xTF32 (Co % 128 != 0)
 
